@@ -1,0 +1,648 @@
+// The C ABI (include/twg.h): object lifetimes, host<->device staging, error
+// mapping. Every compute call is a device kernel; there is no CPU path.
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "primitives.cuh"
+#include "rng.cuh"
+#include "walk.cuh"
+#include "window.cuh"
+
+using namespace twg;
+
+struct twg_ctx {
+  Ctx c;
+};
+struct twg_store {
+  Store* s;
+};
+struct twg_window {
+  Window* w;
+  twg_ctx* ctx;
+};
+struct twg_walkset {
+  WalkSetDev* w;
+};
+
+namespace {
+
+thread_local std::string g_error;
+
+// CounterRng state for a seed (rng.hpp:25)
+inline u64 mix64_host(u64 seed) { return mix64(seed ^ 0x6a09e667f3bcc909ULL); }
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return TWG_OK;
+  } catch (const Error& e) {
+    g_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    g_error = e.what();
+    return TWG_ENOMEM;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return TWG_ECUDA;
+  }
+}
+
+void require(bool ok, const char* what) {
+  if (!ok) fail(TWG_EINVAL, what);
+}
+
+BuildOpts to_opts(const twg_build_opts* o) {
+  BuildOpts b;
+  if (o) {
+    b.weights = o->weights != 0;
+    b.adjacency = o->adjacency != 0;
+  }
+  return b;
+}
+
+template <class T>
+void h2d(Ctx& c, DevBuf<T>& d, const T* h, u64 n) {
+  d.alloc(n ? n : 1, c.stream);
+  if (n) TWG_CUDA(cudaMemcpyAsync(d.p, h, n * sizeof(T), cudaMemcpyHostToDevice, c.stream));
+}
+
+template <class T>
+void d2h(Ctx& c, T* h, const T* d, u64 n) {
+  if (n) TWG_CUDA(cudaMemcpyAsync(h, d, n * sizeof(T), cudaMemcpyDeviceToHost, c.stream));
+}
+
+void sync(Ctx& c) { TWG_CUDA(cudaStreamSynchronize(c.stream)); }
+
+__global__ void k_split_aos(const twg_edge* e, u64 n, i64* s, i64* d, i64* t) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const twg_edge x = e[i];
+    s[i] = x.src;
+    d[i] = x.dst;
+    t[i] = x.t;
+  }
+}
+
+struct SoA {
+  DevBuf<i64> s, d, t;
+};
+
+void upload_edges(Ctx& c, const twg_edge* edges, u64 n, SoA& out) {
+  DevBuf<twg_edge> raw;
+  h2d(c, raw, edges, n);
+  out.s.alloc(n ? n : 1, c.stream);
+  out.d.alloc(n ? n : 1, c.stream);
+  out.t.alloc(n ? n : 1, c.stream);
+  if (n) {
+    k_split_aos<<<grid_for(n, 256, c.sm_count * 16), 256, 0, c.stream>>>(raw.p, n, out.s.p, out.d.p, out.t.p);
+    TWG_LAUNCHED(c);
+  }
+}
+
+// ---- synthetic stream (C5 law; draws as synthetic.cpp:17-20, :92-96)
+__host__ __device__ inline void stream_edge(u64 nodes, u64 i, u64 key, i64* s, i64* d, i64* t) {
+  auto mix = [](u64 x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+  };
+  auto bits = [&](u64 walk, u64 hop, u64 ord) { return mix(mix(mix(key ^ walk) ^ hop) ^ ord); };
+  const double u = static_cast<double>(bits(2, i, 1) >> 11) * 0x1.0p-53;
+#ifdef __CUDA_ARCH__
+  i64 dv = static_cast<i64>(__dmul_rn(__dmul_rn(__dmul_rn(static_cast<double>(nodes), u), u), u));
+#else
+  i64 dv = static_cast<i64>(static_cast<double>(nodes) * u * u * u);
+#endif
+  if (dv > static_cast<i64>(nodes) - 1) dv = static_cast<i64>(nodes) - 1;
+  *s = static_cast<i64>(bits(1, i, 0) % nodes);
+  *d = dv;
+  *t = static_cast<i64>(i / 4);
+}
+
+__global__ void k_synth_stream(u64 nodes, u64 first, u64 count, u64 key, i64* s, i64* d, i64* t) {
+  for (u64 k = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; k < count;
+       k += static_cast<u64>(gridDim.x) * blockDim.x)
+    stream_edge(nodes, first + k, key, s + k, d + k, t + k);
+}
+
+// make_uniform_graph (synthetic.cpp:24-36)
+__global__ void k_synth_uniform(u64 nodes, u64 count, i64 t_max, u64 key, i64* s, i64* d, i64* t) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    auto mix = [](u64 x) {
+      x += 0x9e3779b97f4a7c15ULL;
+      x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+      x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+      return x ^ (x >> 31);
+    };
+    auto bits = [&](u64 walk, u64 hop, u64 ord) { return mix(mix(mix(key ^ walk) ^ hop) ^ ord); };
+    s[i] = static_cast<i64>(bits(1, i, 0) % nodes);
+    d[i] = static_cast<i64>(bits(2, i, 0) % nodes);
+    t[i] = static_cast<i64>(bits(3, i, 0) % (static_cast<u64>(t_max) + 1));
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int twg_abi_version(void) { return TWG_ABI_VERSION; }
+const char* twg_last_error(void) { return g_error.c_str(); }
+
+int twg_ctx_create(int device, twg_ctx** out) {
+  return guarded([&] {
+    auto* h = new twg_ctx;
+    Ctx& c = h->c;
+    try {
+      c.device = device;
+      TWG_CUDA(cudaSetDevice(device));
+      TWG_CUDA(cudaDeviceGetAttribute(&c.sm_count, cudaDevAttrMultiProcessorCount, device));
+      TWG_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+      TWG_CUDA(cudaDeviceGetDefaultMemPool(&c.pool, device));
+      u64 threshold = ~0ull;
+      TWG_CUDA(cudaMemPoolSetAttribute(c.pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+      // glibc tables: same libm as the reference
+      std::vector<double> e(kExpTableSize), x(701);
+      for (int k = 0; k < kExpTableSize; ++k) e[k] = std::exp(static_cast<double>(-k));
+      for (int n = 0; n <= 700; ++n) x[n] = std::expm1(static_cast<double>(n));
+      TWG_CUDA(cudaMalloc(&c.d_exp_neg, e.size() * sizeof(double)));
+      TWG_CUDA(cudaMalloc(&c.d_expm1, x.size() * sizeof(double)));
+      TWG_CUDA(cudaMemcpy(c.d_exp_neg, e.data(), e.size() * sizeof(double), cudaMemcpyHostToDevice));
+      TWG_CUDA(cudaMemcpy(c.d_expm1, x.data(), x.size() * sizeof(double), cudaMemcpyHostToDevice));
+      TWG_CUDA(cudaMallocHost(&c.h_pinned, 64 * sizeof(u64)));
+      TWG_CUDA(cudaMalloc(&c.d_scalars, 64 * sizeof(u64)));
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int twg_ctx_destroy(twg_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    Ctx& c = ctx->c;
+    cudaStreamSynchronize(c.stream);
+    cudaFree(c.d_exp_neg);
+    cudaFree(c.d_expm1);
+    cudaFree(c.d_scalars);
+    cudaFreeHost(c.h_pinned);
+    cudaStreamDestroy(c.stream);
+    delete ctx;
+  });
+}
+
+int twg_ctx_sync(twg_ctx* ctx) {
+  return guarded([&] { sync(ctx->c); });
+}
+
+int twg_ctx_stream(twg_ctx* ctx, void** stream) {
+  return guarded([&] { *stream = static_cast<void*>(ctx->c.stream); });
+}
+
+int twg_ctx_launch_count(twg_ctx* ctx, uint64_t* count) {
+  return guarded([&] { *count = ctx->c.launches; });
+}
+
+// ---- store ------------------------------------------------------------------
+
+int twg_store_build(twg_ctx* ctx, const twg_edge* edges, uint64_t n, int mode, const twg_build_opts* opts,
+                    twg_store** out) {
+  return guarded([&] {
+    Ctx& c = ctx->c;
+    if (n >= 0xffffffffull / 2) fail(TWG_EINVAL, "edge store: edge count exceeds 32-bit reference space");
+    SoA soa;
+    upload_edges(c, edges, n, soa);
+    Store* s = build_store(c, EdgesSoA{soa.s.p, soa.d.p, soa.t.p, n}, mode, to_opts(opts));
+    sync(c);
+    *out = new twg_store{s};
+  });
+}
+
+int twg_store_build_device(twg_ctx* ctx, const int64_t* d_src, const int64_t* d_dst, const int64_t* d_t, uint64_t n,
+                           int mode, const twg_build_opts* opts, twg_store** out) {
+  return guarded([&] {
+    Store* s = build_store(ctx->c, EdgesSoA{d_src, d_dst, d_t, n}, mode, to_opts(opts));
+    *out = new twg_store{s};
+  });
+}
+
+int twg_store_retain(twg_store* s) {
+  return guarded([&] { s->s->refs.fetch_add(1); });
+}
+
+int twg_store_release(twg_store* s) {
+  return guarded([&] {
+    if (!s) return;
+    release_store(s->s);
+    delete s;
+  });
+}
+
+int twg_store_get_info(twg_store* h, twg_store_info* out) {
+  return guarded([&] {
+    const Store& s = *h->s;
+    twg_store_info i{};
+    i.edges = s.m;
+    i.nodes = s.V;
+    i.ts_groups = s.Z;
+    i.entries = s.P;
+    i.node_groups = s.Q;
+    i.adjacency = s.has_adjacency ? s.A : 0;
+    i.mode = s.mode;
+    i.has_weights = s.has_weights;
+    i.has_adjacency = s.has_adjacency;
+    i.device_bytes = s.device_bytes();
+    *out = i;
+  });
+}
+
+namespace {
+__global__ void k_widen_u32(const u32* in, u64 n, u64* out) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<u64>(gridDim.x) * blockDim.x)
+    out[i] = in[i];
+}
+__global__ void k_ext_of(const u32* ids, const i64* ext, u64 n, i64* out) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<u64>(gridDim.x) * blockDim.x)
+    out[i] = ext[ids[i]];
+}
+__global__ void k_meta_field(const uint2* meta, u64 n, int which, u64* out) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<u64>(gridDim.x) * blockDim.x)
+    out[i] = which ? meta[i].y : meta[i].x;
+}
+__global__ void k_entry_field(const Entry* ent, u64 n, int which, u32* out) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<u64>(gridDim.x) * blockDim.x)
+    out[i] = which ? ent[i].nbr : ent[i].edge;
+}
+}  // namespace
+
+int twg_store_download(twg_store* h, int field, void* dst) {
+  return guarded([&] {
+    Store& s = *h->s;
+    Ctx& c = *s.ctx;
+    cudaStream_t st = c.stream;
+    const unsigned g = grid_for(s.P + s.m + s.V + 1, 256, c.sm_count * 16);
+    switch (field) {
+      case 0: case 1: {
+        DevBuf<i64> tmp(s.m ? s.m : 1, st);
+        if (s.m) {
+          k_ext_of<<<g, 256, 0, st>>>(field == 0 ? s.e_src.p : s.e_dst.p, s.ext.p, s.m, tmp.p);
+          TWG_LAUNCHED(c);
+        }
+        d2h(c, static_cast<i64*>(dst), tmp.p, s.m);
+        sync(c);
+        break;
+      }
+      case 2: d2h(c, static_cast<i64*>(dst), s.e_t.p, s.m); break;
+      case 3: d2h(c, static_cast<u32*>(dst), s.e_src.p, s.m); break;
+      case 4: d2h(c, static_cast<u32*>(dst), s.e_dst.p, s.m); break;
+      case 5: {
+        DevBuf<u64> tmp(s.Z + 1, st);
+        k_widen_u32<<<g, 256, 0, st>>>(s.ts_off.p, s.Z + 1, tmp.p);
+        TWG_LAUNCHED(c);
+        d2h(c, static_cast<u64*>(dst), tmp.p, s.Z + 1);
+        sync(c);
+        break;
+      }
+      case 6: d2h(c, static_cast<i64*>(dst), s.ts_time.p, s.Z); break;
+      case 7: ensure_weights(c, s); d2h(c, static_cast<double*>(dst), s.ts_w.p, s.Z); break;
+      case 8: case 9: {
+        DevBuf<u64> tmp(s.V + 1, st);
+        k_meta_field<<<g, 256, 0, st>>>(s.nmeta.p, s.V + 1, field == 9, tmp.p);
+        TWG_LAUNCHED(c);
+        d2h(c, static_cast<u64*>(dst), tmp.p, s.V + 1);
+        sync(c);
+        break;
+      }
+      case 10: d2h(c, static_cast<i64*>(dst), s.mk_time.p, s.Q); break;
+      case 11: d2h(c, static_cast<u32*>(dst), s.mk_start.p, s.Q); break;
+      case 12: case 15: {
+        DevBuf<u32> tmp(s.P ? s.P : 1, st);
+        if (s.P) {
+          k_entry_field<<<g, 256, 0, st>>>(s.ent.p, s.P, field == 15, tmp.p);
+          TWG_LAUNCHED(c);
+        }
+        d2h(c, static_cast<u32*>(dst), tmp.p, s.P);
+        sync(c);
+        break;
+      }
+      case 13: ensure_weights(c, s); d2h(c, static_cast<double*>(dst), s.wp.p, s.P); break;
+      case 14: d2h(c, static_cast<i64*>(dst), s.ext.p, s.V); break;
+      case 16: {
+        ensure_adjacency(c, s);
+        DevBuf<u64> tmp(s.V + 1, st);
+        k_widen_u32<<<g, 256, 0, st>>>(s.adj_off.p, s.V + 1, tmp.p);
+        TWG_LAUNCHED(c);
+        d2h(c, static_cast<u64*>(dst), tmp.p, s.V + 1);
+        sync(c);
+        break;
+      }
+      case 17: ensure_adjacency(c, s); d2h(c, static_cast<u32*>(dst), s.adj.p, s.A); break;
+      default: fail(TWG_EINVAL, "twg_store_download: unknown field");
+    }
+    sync(c);
+  });
+}
+
+int twg_store_neighborhood(twg_store* h, const int64_t* v_ext, const int64_t* t, uint64_t n, int dir,
+                           uint64_t* out3) {
+  return guarded([&] {
+    Store& s = *h->s;
+    Ctx& c = *s.ctx;
+    DevBuf<i64> dv, dt;
+    h2d(c, dv, v_ext, n);
+    h2d(c, dt, t, n);
+    DevBuf<u64> o(3 * n + 1, c.stream);
+    neighborhood_batch(c, s, dv.p, dt.p, n, dir, o.p);
+    d2h(c, out3, o.p, 3 * n);
+    sync(c);
+  });
+}
+
+int twg_store_find_nodes(twg_store* h, const int64_t* v_ext, uint64_t n, uint32_t* internal, uint8_t* found) {
+  return guarded([&] {
+    Store& s = *h->s;
+    Ctx& c = *s.ctx;
+    DevBuf<i64> dv;
+    h2d(c, dv, v_ext, n);
+    DevBuf<u32> di(n + 1, c.stream);
+    DevBuf<u8> df(n + 1, c.stream);
+    find_nodes_batch(c, s, dv.p, n, di.p, df.p);
+    d2h(c, internal, di.p, n);
+    d2h(c, found, df.p, n);
+    sync(c);
+  });
+}
+
+int twg_store_adjacent(twg_store* h, const uint32_t* a, const uint32_t* b, uint64_t n, int temporal,
+                       const int64_t* t, int dir, uint8_t* out) {
+  return guarded([&] {
+    Store& s = *h->s;
+    Ctx& c = *s.ctx;
+    for (u64 i = 0; i < n; ++i) require(a[i] < s.V && b[i] < s.V, "twg_store_adjacent: node id out of range");
+    DevBuf<u32> da, db;
+    DevBuf<i64> dt;
+    h2d(c, da, a, n);
+    h2d(c, db, b, n);
+    if (temporal) h2d(c, dt, t, n);
+    DevBuf<u8> o(n + 1, c.stream);
+    adjacent_batch(c, s, da.p, db.p, n, temporal, dt.p, dir, o.p);
+    d2h(c, out, o.p, n);
+    sync(c);
+  });
+}
+
+// ---- window -------------------------------------------------------------------
+
+int twg_window_create(twg_ctx* ctx, int64_t duration, int mode, const twg_build_opts* opts, twg_window** out) {
+  return guarded([&] {
+    Window* w = window_create(ctx->c, duration, mode, to_opts(opts));
+    *out = new twg_window{w, ctx};
+  });
+}
+
+int twg_window_destroy(twg_window* w) {
+  return guarded([&] {
+    if (!w) return;
+    window_destroy(w->w);
+    delete w;
+  });
+}
+
+int twg_window_ingest(twg_window* w, const twg_edge* batch, uint64_t n, twg_batch_stats* out) {
+  return guarded([&] {
+    Ctx& c = *w->w->ctx;
+    SoA soa;
+    upload_edges(c, batch, n, soa);
+    window_ingest(*w->w, soa.s.p, soa.d.p, soa.t.p, n, out);
+    sync(c);
+  });
+}
+
+int twg_window_ingest_device(twg_window* w, const int64_t* d_src, const int64_t* d_dst, const int64_t* d_t,
+                             uint64_t n, twg_batch_stats* out) {
+  return guarded([&] { window_ingest(*w->w, d_src, d_dst, d_t, n, out); });
+}
+
+int twg_window_snapshot(twg_window* w, twg_store** out) {
+  return guarded([&] {
+    w->w->store->refs.fetch_add(1);
+    *out = new twg_store{w->w->store};
+  });
+}
+
+int twg_window_bounds(twg_window* w, int64_t* lo, int64_t* hi) {
+  return guarded([&] {
+    const Window& x = *w->w;
+    if (x.batch_count == 0 || x.t_high == kTimeUnset)  // window_manager.cpp:65-66
+      fail(TWG_ELOGIC, "window_bounds: no batch ingested yet");
+    *lo = x.cutoff_for(x.t_high);
+    *hi = x.t_high;
+  });
+}
+
+int twg_window_state(twg_window* w, int64_t* t_high, uint64_t* batch_count, twg_batch_stats* last) {
+  return guarded([&] {
+    if (t_high) *t_high = w->w->t_high;
+    if (batch_count) *batch_count = w->w->batch_count;
+    if (last) *last = w->w->stats;
+  });
+}
+
+// ---- walks -----------------------------------------------------------------------
+
+int twg_generate(twg_ctx* ctx, twg_store* s, const twg_walk_config* config, const twg_thresholds* thresholds,
+                 int variant, twg_walkset** out, twg_walk_stats* stats) {
+  return guarded([&] {
+    require(variant >= 0 && variant <= 2, "generate_walks: unknown variant");
+    const twg_thresholds th = thresholds ? *thresholds : twg_thresholds{4, 256, 8192, 512, 4096};
+    WalkSetDev* w = generate_walks(ctx->c, *s->s, *config, th, variant, stats);
+    *out = new twg_walkset{w};
+  });
+}
+
+int twg_walkset_destroy(twg_walkset* w) {
+  return guarded([&] {
+    if (!w) return;
+    delete w->w;
+    delete w;
+  });
+}
+
+int twg_walkset_info(twg_walkset* w, uint32_t* stride, uint64_t* walk_count, uint64_t* first_walk, uint64_t* hops) {
+  return guarded([&] {
+    if (stride) *stride = w->w->stride;
+    if (walk_count) *walk_count = w->w->count;
+    if (first_walk) *first_walk = w->w->first;
+    if (hops) *hops = w->w->hops;
+  });
+}
+
+int twg_walkset_download(twg_walkset* w, int64_t* nodes, int64_t* times, uint32_t* lengths) {
+  return guarded([&] {
+    WalkSetDev& x = *w->w;
+    Ctx& c = *x.ctx;
+    if (nodes || times) zero_walk_tails(c, x);
+    const u64 cells = x.count * x.stride;
+    if (nodes) d2h(c, nodes, x.nodes.p, cells);
+    if (times) d2h(c, times, x.times.p, cells);
+    if (lengths) d2h(c, lengths, x.lengths.p, x.count);
+    sync(c);
+  });
+}
+
+int twg_walkset_download_compact(twg_walkset* w, uint64_t* offsets, int64_t* nodes, int64_t* times) {
+  return guarded([&] {
+    WalkSetDev& x = *w->w;
+    Ctx& c = *x.ctx;
+    DevBuf<u64> offs;
+    DevBuf<i64> cn, ct;
+    u64 total = 0;
+    compact_walks(c, x, offs, cn, ct, &total);
+    if (offsets) d2h(c, offsets, offs.p, x.count + 1);
+    if (nodes) d2h(c, nodes, cn.p, total);
+    if (times) d2h(c, times, ct.p, total);
+    sync(c);
+  });
+}
+
+int twg_walkset_device(twg_walkset* w, int64_t** d_nodes, int64_t** d_times, uint32_t** d_lengths) {
+  return guarded([&] {
+    if (d_nodes) *d_nodes = w->w->nodes.p;
+    if (d_times) *d_times = w->w->times.p;
+    if (d_lengths) *d_lengths = w->w->lengths.p;
+  });
+}
+
+int twg_sample_start_edges(twg_store* h, int bias, const double* u1, const double* u2, uint64_t n, uint64_t* out) {
+  return guarded([&] {
+    Store& s = *h->s;
+    Ctx& c = *s.ctx;
+    for (u64 i = 0; i < n; ++i)
+      require(u1[i] >= 0.0 && u1[i] < 1.0 && u2[i] >= 0.0 && u2[i] < 1.0, "picker: u outside [0,1)");
+    DevBuf<double> a, b;
+    h2d(c, a, u1, n);
+    h2d(c, b, u2, n);
+    DevBuf<u64> o(n + 1, c.stream);
+    sample_start_edges(c, s, bias, a.p, b.p, n, o.p);
+    d2h(c, out, o.p, n);
+    sync(c);
+  });
+}
+
+int twg_schedule_step(twg_store* h, const uint32_t* node_of_walk, const uint8_t* alive, uint64_t n,
+                      const twg_thresholds* thresholds, uint64_t* sizes5, uint32_t* rows, uint64_t cap,
+                      uint32_t* walk_ids) {
+  return guarded([&] {
+    Store& s = *h->s;
+    Ctx& c = *s.ctx;
+    const twg_thresholds th = thresholds ? *thresholds : twg_thresholds{4, 256, 8192, 512, 4096};
+    for (u64 i = 0; i < n; ++i) require(node_of_walk[i] < s.V, "schedule_step: node id out of range");
+    DevBuf<u32> dn;
+    DevBuf<u8> da;
+    h2d(c, dn, node_of_walk, n);
+    h2d(c, da, alive, n);
+    schedule_step_explicit(c, s, dn.p, da.p, n, th, sizes5, rows, cap, walk_ids);
+  });
+}
+
+int twg_pick_index(twg_ctx* ctx, int kind, const double* u, const uint64_t* n, uint64_t count, uint64_t* out) {
+  return guarded([&] {
+    require(kind >= 0 && kind <= 2, "twg_pick_index: kind");
+    for (u64 i = 0; i < count; ++i) {  // samplers.cpp:10-13
+      if (n[i] == 0) fail(TWG_EINVAL, "picker: empty candidate set");
+      if (!(u[i] >= 0.0) || u[i] >= 1.0) fail(TWG_EINVAL, "picker: u outside [0,1)");
+    }
+    Ctx& c = ctx->c;
+    DevBuf<double> du;
+    DevBuf<u64> dn;
+    h2d(c, du, u, count);
+    h2d(c, dn, n, count);
+    DevBuf<u64> o(count + 1, c.stream);
+    pick_index_batch(c, kind, du.p, dn.p, count, o.p);
+    d2h(c, out, o.p, count);
+    sync(c);
+  });
+}
+
+int twg_pick_weighted_range(twg_ctx* ctx, const double* u, const double* prefix, uint64_t len, const uint64_t* begin,
+                            const uint64_t* end, const double* base, uint64_t count, uint64_t* out) {
+  return guarded([&] {
+    for (u64 i = 0; i < count; ++i) require(begin[i] < end[i] && end[i] <= len, "pick_weighted_range: bad range");
+    Ctx& c = ctx->c;
+    DevBuf<double> du, dp, db;
+    DevBuf<u64> dbeg, dend;
+    h2d(c, du, u, count);
+    h2d(c, dp, prefix, len);
+    h2d(c, db, base, count);
+    h2d(c, dbeg, begin, count);
+    h2d(c, dend, end, count);
+    DevBuf<u64> o(count + 1, c.stream);
+    pick_weighted_range_batch(c, du.p, dp.p, dbeg.p, dend.p, db.p, count, o.p);
+    d2h(c, out, o.p, count);
+    sync(c);
+  });
+}
+
+int twg_rng_bits(twg_ctx* ctx, int rng, uint64_t seed, const uint64_t* walk, const uint64_t* hop,
+                 const uint64_t* ordinal, uint64_t count, uint64_t* out) {
+  return guarded([&] {
+    require(rng == TWG_RNG_SPLITMIX || rng == TWG_RNG_PHILOX, "twg_rng_bits: rng");
+    Ctx& c = ctx->c;
+    DevBuf<u64> dw, dh, dor;
+    h2d(c, dw, walk, count);
+    h2d(c, dh, hop, count);
+    h2d(c, dor, ordinal, count);
+    DevBuf<u64> o(count + 1, c.stream);
+    rng_bits_batch(c, rng, seed, dw.p, dh.p, dor.p, count, o.p);
+    d2h(c, out, o.p, count);
+    sync(c);
+  });
+}
+
+// ---- synthetic inputs -----------------------------------------------------------------
+
+int twg_synth_stream_host(uint64_t nodes, uint64_t first, uint64_t count, uint64_t seed, twg_edge* out) {
+  return guarded([&] {
+    require(nodes > 0, "twg_synth_stream_host: nodes");
+    const u64 key = mix64_host(seed);
+#pragma omp parallel for schedule(static)
+    for (long long k = 0; k < static_cast<long long>(count); ++k)
+      stream_edge(nodes, first + static_cast<u64>(k), key, &out[k].src, &out[k].dst, &out[k].t);
+  });
+}
+
+int twg_synth_stream_device(twg_ctx* ctx, uint64_t nodes, uint64_t first, uint64_t count, uint64_t seed,
+                            int64_t* d_src, int64_t* d_dst, int64_t* d_t) {
+  return guarded([&] {
+    require(nodes > 0, "twg_synth_stream_device: nodes");
+    Ctx& c = ctx->c;
+    if (!count) return;
+    k_synth_stream<<<grid_for(count, 256, c.sm_count * 32), 256, 0, c.stream>>>(nodes, first, count, mix64_host(seed),
+                                                                                d_src, d_dst, d_t);
+    TWG_LAUNCHED(c);
+  });
+}
+
+int twg_synth_uniform_device(twg_ctx* ctx, uint64_t nodes, uint64_t count, int64_t t_max, uint64_t seed,
+                             int64_t* d_src, int64_t* d_dst, int64_t* d_t) {
+  return guarded([&] {
+    require(nodes > 0 && t_max >= 0, "twg_synth_uniform_device: args");
+    Ctx& c = ctx->c;
+    if (!count) return;
+    k_synth_uniform<<<grid_for(count, 256, c.sm_count * 32), 256, 0, c.stream>>>(nodes, count, t_max,
+                                                                                 mix64_host(seed), d_src, d_dst, d_t);
+    TWG_LAUNCHED(c);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,121 @@
+// Shared host/device plumbing for libtimewalk_b200: errors, the per-context
+// stream + stream-ordered pool, device buffers, launch accounting.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <utility>
+
+#include "twg.h"
+
+namespace twg {
+
+using u8 = uint8_t;
+using u32 = uint32_t;
+using u64 = uint64_t;
+using i64 = int64_t;
+
+constexpr i64 kTimeUnset = INT64_MIN;     // types.hpp:23
+constexpr i64 kTimeInfinite = INT64_MAX;  // types.hpp:25
+constexpr int kExpTableSize = 746;        // exp(-k), k = 0..745 (glibc); exp(-746) == +0
+
+// Error carrying a TWG_* status (mapped onto the reference exception types).
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e != cudaSuccess) {
+    char buf[512];
+    std::snprintf(buf, sizeof buf, "%s failed at %s:%d: %s", what, file, line,
+                  cudaGetErrorString(e));
+    fail(e == cudaErrorMemoryAllocation ? TWG_ENOMEM : TWG_ECUDA, buf);
+  }
+}
+#define TWG_CUDA(x) ::twg::cuda_check((x), #x, __FILE__, __LINE__)
+#define TWG_LAUNCHED(ctx) \
+  do {                    \
+    ::twg::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__); \
+    (ctx).launches++;     \
+  } while (0)
+
+struct Ctx {
+  int device = 0;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+  cudaMemPool_t pool = nullptr;
+  u64 launches = 0;
+  // glibc exp(-k) for k = 0..745 and expm1(n) for n = 0..700, computed on the
+  // host by the same libm the reference links (App. A of SURVEY.md).
+  double* d_exp_neg = nullptr;
+  double* d_expm1 = nullptr;
+  // pinned scratch for small device->host reads
+  u64* h_pinned = nullptr;
+  u64* d_scalars = nullptr;  // 64 u64 scratch scalars on the device
+};
+
+// Stream-ordered device buffer (cudaMallocAsync on the ctx stream).
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+
+  DevBuf() = default;
+  DevBuf(size_t count, cudaStream_t stream) { alloc(count, stream); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p; n = o.n; s = o.s;
+      o.p = nullptr; o.n = 0;
+    }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+
+  void alloc(size_t count, cudaStream_t stream) {
+    release();
+    s = stream;
+    n = count;
+    if (count) TWG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), stream));
+  }
+  // grow-only reallocation (contents not preserved)
+  void reserve(size_t count, cudaStream_t stream) {
+    if (count > n || p == nullptr) alloc(count < 1 ? 1 : count, stream);
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  size_t bytes() const { return n * sizeof(T); }
+  T* get() const { return p; }
+};
+
+inline int bit_width_u64(u64 x) {
+  int b = 0;
+  while (x) { ++b; x >>= 1; }
+  return b;
+}
+
+inline unsigned grid_for(u64 n, unsigned block, unsigned cap = 1u << 20) {
+  u64 g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return static_cast<unsigned>(g);
+}
+
+// small synchronous device -> host read of n u64 scalars via pinned memory
+void read_scalars(Ctx& ctx, const u64* d_src, u64* host_dst, int n);
+
+}  // namespace twg

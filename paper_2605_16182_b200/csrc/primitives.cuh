@@ -1,0 +1,258 @@
+// Device-wide data-parallel primitives for the index build and the walk
+// scheduler (the sm_100a replacements of the reference's CPU primitives,
+// primitives.cpp:24-148 — radix_sort_pairs, exclusive_scan,
+// run_length_encode, partition_flagged — and of the CUB calls the paper's
+// GPU engine uses):
+//
+//  * exclusive_scan: three-phase tile scan (tile sums -> recursive scan of
+//    the sums -> rescan + write), input supplied by a functor so flag
+//    computations fuse into the scan's loads;
+//  * radix_sort_pairs: stable LSD radix sort of (u32|u64 key, u32 value),
+//    8-bit digits, pass count from the key's actual bit width (the
+//    reference's constant-digit skip, primitives.cpp:47-56, made static).
+//    Per pass: tile histogram -> scan of the digit-major count matrix ->
+//    stable tile ranking with warp match/ballot + shared-memory staging so
+//    the global scatter is written in digit-contiguous, coalesced runs.
+#pragma once
+
+#include "common.cuh"
+
+namespace twg {
+
+constexpr int kScanBlock = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanBlock * kScanItems;
+
+constexpr int kSortBlock = 256;
+constexpr int kSortItems = 8;
+constexpr int kSortTile = kSortBlock * kSortItems;
+constexpr int kRadixBits = 8;
+constexpr int kRadix = 1 << kRadixBits;
+
+// ---------------------------------------------------------------- scan ----
+
+template <class T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const T n = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += n;
+  }
+  return v;
+}
+
+// Block-wide exclusive scan of one value per thread; returns the exclusive
+// prefix, *total = block sum. blockDim.x == kScanBlock.
+template <class T>
+__device__ __forceinline__ T block_excl_scan(T v, T* total) {
+  __shared__ T warp_sums[kScanBlock / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const T incl = warp_incl_scan(v);
+  if (lane == 31) warp_sums[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    T s = lane < kScanBlock / 32 ? warp_sums[lane] : T(0);
+    s = warp_incl_scan(s);
+    if (lane < kScanBlock / 32) warp_sums[lane] = s;
+  }
+  __syncthreads();
+  const T warp_prefix = warp == 0 ? T(0) : warp_sums[warp - 1];
+  *total = warp_sums[kScanBlock / 32 - 1];
+  __syncthreads();
+  return warp_prefix + incl - v;
+}
+
+template <class T, class In>
+__global__ void __launch_bounds__(kScanBlock) k_scan_tile_sums(In in, u64 n, T* tile_sums) {
+  const u64 base = static_cast<u64>(blockIdx.x) * kScanTile;
+  T s = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    const u64 i = base + static_cast<u64>(threadIdx.x) * kScanItems + j;
+    if (i < n) s += in(i);
+  }
+  T total;
+  block_excl_scan<T>(s, &total);
+  if (threadIdx.x == 0) tile_sums[blockIdx.x] = total;
+}
+
+template <class T, class In>
+__global__ void __launch_bounds__(kScanBlock) k_scan_tiles(In in, u64 n, const T* tile_offsets, T* out) {
+  const u64 base = static_cast<u64>(blockIdx.x) * kScanTile;
+  T v[kScanItems];
+  T s = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    const u64 i = base + static_cast<u64>(threadIdx.x) * kScanItems + j;
+    v[j] = i < n ? in(i) : T(0);
+    s += v[j];
+  }
+  T total;
+  T run = block_excl_scan<T>(s, &total) + (tile_offsets ? tile_offsets[blockIdx.x] : T(0));
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    const u64 i = base + static_cast<u64>(threadIdx.x) * kScanItems + j;
+    if (i < n) out[i] = run;
+    run += v[j];
+  }
+  // out[n] = grand total, written by the block owning element n-1 (or n == 0)
+  if (threadIdx.x == kScanBlock - 1 && base < n && n - base <= kScanTile) out[n] = run;
+}
+
+template <class T>
+struct LoadFn {
+  const T* p;
+  __device__ __forceinline__ T operator()(u64 i) const { return p[i]; }
+};
+
+// out[0..n] : out[i] = sum_{j<i} in(j), out[n] = total. T = u32 or u64.
+template <class T, class In>
+void exclusive_scan(Ctx& ctx, In in, u64 n, T* out) {
+  cudaStream_t st = ctx.stream;
+  if (n == 0) {
+    TWG_CUDA(cudaMemsetAsync(out, 0, sizeof(T), st));
+    return;
+  }
+  const u64 tiles = (n + kScanTile - 1) / kScanTile;
+  if (tiles == 1) {
+    k_scan_tiles<T, In><<<1, kScanBlock, 0, st>>>(in, n, nullptr, out);
+    TWG_LAUNCHED(ctx);
+    return;
+  }
+  DevBuf<T> sums(tiles + 1, st);
+  k_scan_tile_sums<T, In><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(in, n, sums.p);
+  TWG_LAUNCHED(ctx);
+  DevBuf<T> offs(tiles + 1, st);
+  exclusive_scan<T>(ctx, LoadFn<T>{sums.p}, tiles, offs.p);
+  k_scan_tiles<T, In><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(in, n, offs.p, out);
+  TWG_LAUNCHED(ctx);
+}
+
+// --------------------------------------------------------------- radix ----
+
+template <class K>
+__global__ void __launch_bounds__(kSortBlock) k_radix_hist(const K* __restrict__ keys, u64 n, int shift,
+                                                           u32* __restrict__ counts, u64 tiles) {
+  __shared__ u32 hist[kRadix];
+  for (int b = threadIdx.x; b < kRadix; b += kSortBlock) hist[b] = 0;
+  __syncthreads();
+  const u64 base = static_cast<u64>(blockIdx.x) * kSortTile;
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const u64 i = base + static_cast<u64>(j) * kSortBlock + threadIdx.x;
+    if (i < n) atomicAdd(&hist[static_cast<u32>(keys[i] >> shift) & (kRadix - 1)], 1u);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < kRadix; b += kSortBlock) counts[static_cast<u64>(b) * tiles + blockIdx.x] = hist[b];
+}
+
+// Stable tile rank + coalesced scatter. Item order inside a tile is
+// (round j, warp, lane) == input order, which keeps the sort stable.
+template <class K>
+__global__ void __launch_bounds__(kSortBlock) k_radix_scatter(const K* __restrict__ keys_in,
+                                                              const u32* __restrict__ vals_in,
+                                                              K* __restrict__ keys_out,
+                                                              u32* __restrict__ vals_out, u64 n,
+                                                              int shift, const u32* __restrict__ offsets,
+                                                              u64 tiles) {
+  constexpr int kWarps = kSortBlock / 32;
+  __shared__ u32 wcount[kWarps][kRadix];
+  __shared__ u32 running[kRadix];
+  __shared__ u32 tile_start[kRadix];
+  __shared__ K skeys[kSortTile];
+  __shared__ u32 svals[kSortTile];
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const u64 base = static_cast<u64>(blockIdx.x) * kSortTile;
+  const u32 lanemask_lt = (1u << lane) - 1u;
+  for (int b = threadIdx.x; b < kRadix; b += kSortBlock) running[b] = 0;
+
+  K key[kSortItems];
+  u32 val[kSortItems];
+  u32 rank[kSortItems];
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const u64 i = base + static_cast<u64>(j) * kSortBlock + threadIdx.x;
+    const bool valid = i < n;
+    key[j] = valid ? keys_in[i] : K(0);
+    val[j] = (valid && vals_in) ? vals_in[i] : 0u;
+    const u32 d = valid ? (static_cast<u32>(key[j] >> shift) & (kRadix - 1)) : (kRadix + lane);
+    for (int b = threadIdx.x; b < kWarps * kRadix; b += kSortBlock) (&wcount[0][0])[b] = 0;
+    __syncthreads();
+    const u32 peers = __match_any_sync(0xffffffffu, d);
+    const u32 r_in_warp = __popc(peers & lanemask_lt);
+    if (valid && r_in_warp == 0) wcount[warp][d] = __popc(peers);
+    __syncthreads();
+    for (int b = threadIdx.x; b < kRadix; b += kSortBlock) {
+      u32 acc = running[b];
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        const u32 c = wcount[w][b];
+        wcount[w][b] = acc;
+        acc += c;
+      }
+      running[b] = acc;
+    }
+    __syncthreads();
+    rank[j] = valid ? wcount[warp][d] + r_in_warp : 0u;
+    __syncthreads();
+  }
+  // digit starts inside the tile
+  {
+    u32 total;
+    const u32 c = threadIdx.x < kRadix ? running[threadIdx.x] : 0u;
+    const u32 ex = block_excl_scan<u32>(c, &total);
+    if (threadIdx.x < kRadix) tile_start[threadIdx.x] = ex;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const u64 i = base + static_cast<u64>(j) * kSortBlock + threadIdx.x;
+    if (i < n) {
+      const u32 d = static_cast<u32>(key[j] >> shift) & (kRadix - 1);
+      const u32 pos = tile_start[d] + rank[j];
+      skeys[pos] = key[j];
+      if (vals_in) svals[pos] = val[j];
+    }
+  }
+  __syncthreads();
+  const u64 tile_n = n - base < static_cast<u64>(kSortTile) ? n - base : static_cast<u64>(kSortTile);
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const u32 pos = static_cast<u32>(j) * kSortBlock + threadIdx.x;
+    if (pos < tile_n) {
+      const K k = skeys[pos];
+      const u32 d = static_cast<u32>(k >> shift) & (kRadix - 1);
+      const u64 dst = static_cast<u64>(offsets[static_cast<u64>(d) * tiles + blockIdx.x]) + (pos - tile_start[d]);
+      keys_out[dst] = k;
+      if (vals_in) vals_out[dst] = svals[pos];
+    }
+  }
+}
+
+// Stable LSD sort of (keys, vals) by the low `bits` bits of the key. Sorted
+// output lands in (*keys, *vals); the alt buffers are scratch of the same
+// size. Pointers are swapped as passes ping-pong. n < 2^32. Keys-only when
+// *vals == nullptr.
+template <class K>
+void radix_sort_pairs(Ctx& ctx, K** keys, K** keys_alt, u32** vals, u32** vals_alt, u64 n, int bits) {
+  if (n < 2 || bits <= 0) return;
+  cudaStream_t st = ctx.stream;
+  const u64 tiles = (n + kSortTile - 1) / kSortTile;
+  if (tiles * kRadix >= (1ull << 32)) fail(TWG_EINVAL, "radix_sort_pairs: input too large");
+  DevBuf<u32> counts(tiles * kRadix + 1, st);
+  DevBuf<u32> offsets(tiles * kRadix + 1, st);
+  for (int shift = 0; shift < bits; shift += kRadixBits) {
+    k_radix_hist<K><<<static_cast<unsigned>(tiles), kSortBlock, 0, st>>>(*keys, n, shift, counts.p, tiles);
+    TWG_LAUNCHED(ctx);
+    exclusive_scan<u32>(ctx, LoadFn<u32>{counts.p}, tiles * kRadix, offsets.p);
+    k_radix_scatter<K><<<static_cast<unsigned>(tiles), kSortBlock, 0, st>>>(
+        *keys, *vals, *keys_alt, *vals_alt, n, shift, offsets.p, tiles);
+    TWG_LAUNCHED(ctx);
+    std::swap(*keys, *keys_alt);
+    std::swap(*vals, *vals_alt);
+  }
+}
+
+}  // namespace twg

@@ -1,0 +1,290 @@
+// Batched device evaluation of the reference's scalar query/sampler API:
+// temporal_neighborhood (edge_store.cpp:270-302), find_node (:264-268),
+// adjacent / adjacent_after (:310-323), sample_start_edge
+// (walk_engine.cpp:284-299), schedule_step (walk_engine.cpp:301-345) on
+// explicit walk populations, and the closed-form pickers (samplers.cpp).
+// These serve the drop-in façade's accessors and the parity tests; they are
+// not on the measured path.
+#include <cstring>
+#include <vector>
+
+#include "primitives.cuh"
+#include "rng.cuh"
+#include "samplers.cuh"
+#include "walk.cuh"
+
+namespace twg {
+
+namespace {
+
+constexpr int kBlock = 256;
+
+__device__ __forceinline__ bool find_ext(const StoreView& s, i64 v, u32* out) {
+  u64 lo = 0, hi = s.V;
+  while (lo < hi) {
+    const u64 mid = (lo + hi) >> 1;
+    if (static_cast<u64>(s.ext[mid]) < static_cast<u64>(v)) lo = mid + 1;
+    else hi = mid;
+  }
+  if (lo < s.V && s.ext[lo] == v) {
+    *out = static_cast<u32>(lo);
+    return true;
+  }
+  return false;
+}
+
+__global__ void k_neighborhood(StoreView s, const i64* v, const i64* t, u64 n, int dir, u64* out3) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    u32 iv;
+    u64 a = 0, b = 0, g = 0;
+    if (find_ext(s, v[i], &iv)) {
+      const uint2 na = s.nmeta[iv], nb = s.nmeta[iv + 1];
+      if (na.x == nb.x) {
+        a = b = na.x;
+      } else if (dir == 0) {
+        const u32 k = ub_i64(s.mk_time, na.y, nb.y, t[i]);
+        a = k == nb.y ? nb.x : s.mk_start[k];
+        b = nb.x;
+        g = nb.y - k;
+      } else {
+        const u32 k = lb_i64(s.mk_time, na.y, nb.y, t[i]);
+        a = na.x;
+        b = k == nb.y ? nb.x : s.mk_start[k];
+        g = k - na.y;
+      }
+    }
+    out3[3 * i] = a;
+    out3[3 * i + 1] = b;
+    out3[3 * i + 2] = g;
+  }
+}
+
+__global__ void k_find_nodes(StoreView s, const i64* v, u64 n, u32* internal, u8* found) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    u32 iv = 0;
+    const bool f = find_ext(s, v[i], &iv);
+    internal[i] = iv;
+    found[i] = f ? 1 : 0;
+  }
+}
+
+__global__ void k_adjacent(StoreView s, const u32* a, const u32* b, u64 n, int temporal, const i64* t, int dir,
+                           u8* out) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    bool r = false;
+    if (!temporal) {
+      u32 lo = s.adj_off[a[i]], hi = s.adj_off[a[i] + 1];
+      const u32 end = hi;
+      while (lo < hi) {
+        const u32 mid = lo + ((hi - lo) >> 1);
+        if (s.adj[mid] < b[i]) lo = mid + 1;
+        else hi = mid;
+      }
+      r = lo < end && s.adj[lo] == b[i];
+    } else {
+      const uint2 na = s.nmeta[a[i]], nb = s.nmeta[a[i] + 1];
+      u32 c, e;
+      if (dir == 0) {
+        const u32 k = ub_i64(s.mk_time, na.y, nb.y, t[i]);
+        c = k == nb.y ? nb.x : s.mk_start[k];
+        e = nb.x;
+      } else {
+        const u32 k = lb_i64(s.mk_time, na.y, nb.y, t[i]);
+        c = na.x;
+        e = k == nb.y ? nb.x : s.mk_start[k];
+      }
+      for (u32 p = c; p < e && !r; ++p) r = s.ent[p].nbr == b[i];
+    }
+    out[i] = r ? 1 : 0;
+  }
+}
+
+__global__ void k_sample_start(StoreView s, int bias, const double* u1, const double* u2, u64 n,
+                               const double* expm1_tab, u64* out) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    u32 amb = 0;
+    const u64 Z = s.Z;
+    u64 g;
+    switch (bias) {
+      case TWG_UNIFORM: g = pick_uniform(u1[i], Z); break;
+      case TWG_LINEAR: g = pick_linear(u1[i], Z); break;
+      case TWG_EXPINDEX: g = pick_exponential(u1[i], Z, expm1_tab, &amb); break;
+      default: g = pick_weighted(u1[i], s.ts_w, Z); break;
+    }
+    const u64 lo = s.ts_off[g], hi = s.ts_off[g + 1];
+    u64 off = __double2ull_rz(__dmul_rn(u2[i], __ull2double_rn(hi - lo)));
+    if (off >= hi - lo) off = hi - lo - 1;
+    out[i] = lo + off;
+  }
+}
+
+__global__ void k_pick_index(int kind, const double* u, const u64* n, u64 count, const double* expm1_tab, u64* out) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    u32 amb = 0;
+    u64 r;
+    if (kind == 0) r = pick_uniform(u[i], n[i]);
+    else if (kind == 1) r = pick_linear(u[i], n[i]);
+    else r = pick_exponential(u[i], n[i], expm1_tab, &amb);
+    out[i] = r;
+  }
+}
+
+__global__ void k_pick_weighted_range(const double* u, const double* prefix, const u64* begin, const u64* end,
+                                      const double* base, u64 count, u64* out) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<u64>(gridDim.x) * blockDim.x)
+    out[i] = pick_weighted_range(u[i], prefix, begin[i], end[i], base[i]);
+}
+
+__global__ void k_rng_bits(Rng rng, const u64* w, const u64* h, const u64* o, u64 count, u64* out) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<u64>(gridDim.x) * blockDim.x)
+    out[i] = rng.bits(w[i], h[i], o[i]);
+}
+
+unsigned grid(Ctx& ctx, u64 n) { return grid_for(n, kBlock, static_cast<unsigned>(ctx.sm_count) * 16); }
+
+// schedule_step pieces
+struct AliveFlagFn {
+  const u8* alive;
+  __device__ __forceinline__ u32 operator()(u64 i) const { return alive[i] ? 1u : 0u; }
+};
+
+__global__ void k_compact_explicit(const u32* nodes, const u8* alive, const u32* pos, u64 n, u32* keys, u32* vals) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    if (alive[i]) {
+      keys[pos[i]] = nodes[i];
+      vals[pos[i]] = static_cast<u32>(i);
+    }
+  }
+}
+
+}  // namespace
+
+void neighborhood_batch(Ctx& ctx, Store& s, const i64* d_v, const i64* d_t, u64 n, int dir, u64* d_out3) {
+  const bool supports = s.mode == TWG_UNDIRECTED || ((s.mode == TWG_FORWARD) == (dir == 0));
+  if (!supports)
+    fail(TWG_EINVAL,
+         "temporal_neighborhood: walk direction not served by this store's direction mode");
+  if (!n) return;
+  k_neighborhood<<<grid(ctx, n), kBlock, 0, ctx.stream>>>(s.view(), d_v, d_t, n, dir, d_out3);
+  TWG_LAUNCHED(ctx);
+}
+
+void find_nodes_batch(Ctx& ctx, Store& s, const i64* d_v, u64 n, u32* d_internal, u8* d_found) {
+  if (!n) return;
+  k_find_nodes<<<grid(ctx, n), kBlock, 0, ctx.stream>>>(s.view(), d_v, n, d_internal, d_found);
+  TWG_LAUNCHED(ctx);
+}
+
+void adjacent_batch(Ctx& ctx, Store& s, const u32* d_a, const u32* d_b, u64 n, int temporal, const i64* d_t,
+                    int dir, u8* d_out) {
+  if (!temporal) ensure_adjacency(ctx, s);
+  if (!n) return;
+  k_adjacent<<<grid(ctx, n), kBlock, 0, ctx.stream>>>(s.view(), d_a, d_b, n, temporal, d_t, dir, d_out);
+  TWG_LAUNCHED(ctx);
+}
+
+void sample_start_edges(Ctx& ctx, Store& s, int bias, const double* d_u1, const double* d_u2, u64 n, u64* d_out) {
+  if (s.m == 0) fail(TWG_EINVAL, "sample_start_edge: empty store");
+  if (bias < 0 || bias > 3) fail(TWG_ELOGIC, "sample_start_edge: unknown bias");
+  if (bias == TWG_EXPWEIGHT) ensure_weights(ctx, s);
+  if (!n) return;
+  k_sample_start<<<grid(ctx, n), kBlock, 0, ctx.stream>>>(s.view(), bias, d_u1, d_u2, n, ctx.d_expm1, d_out);
+  TWG_LAUNCHED(ctx);
+}
+
+void pick_index_batch(Ctx& ctx, int kind, const double* d_u, const u64* d_n, u64 count, u64* d_out) {
+  if (!count) return;
+  k_pick_index<<<grid(ctx, count), kBlock, 0, ctx.stream>>>(kind, d_u, d_n, count, ctx.d_expm1, d_out);
+  TWG_LAUNCHED(ctx);
+}
+
+void pick_weighted_range_batch(Ctx& ctx, const double* d_u, const double* d_prefix, const u64* d_begin,
+                               const u64* d_end, const double* d_base, u64 count, u64* d_out) {
+  if (!count) return;
+  k_pick_weighted_range<<<grid(ctx, count), kBlock, 0, ctx.stream>>>(d_u, d_prefix, d_begin, d_end, d_base, count,
+                                                                     d_out);
+  TWG_LAUNCHED(ctx);
+}
+
+void rng_bits_batch(Ctx& ctx, int rng, u64 seed, const u64* d_walk, const u64* d_hop, const u64* d_ord, u64 count,
+                    u64* d_out) {
+  if (!count) return;
+  k_rng_bits<<<grid(ctx, count), kBlock, 0, ctx.stream>>>(Rng::make(rng, seed), d_walk, d_hop, d_ord, count, d_out);
+  TWG_LAUNCHED(ctx);
+}
+
+// schedule_step (walk_engine.cpp:301-345) on an explicit population: the
+// device compaction + stable sort by node, then the dispatch plane on the
+// host-visible runs (this entry point exists for the unit-test fixtures).
+void schedule_step_explicit(Ctx& ctx, Store& s, const u32* d_nodes, const u8* d_alive, u64 n,
+                            const twg_thresholds& th, u64* sizes5, u32* rows, u64 cap, u32* walk_ids) {
+  if (th.w_warp < 1 || th.w_warp > th.block_dim || th.block_dim > th.w_max)
+    fail(TWG_EINVAL, "tier thresholds: need 1 <= w_warp <= block_dim <= w_max");
+  if (th.g_warp_cap > th.g_block_cap) fail(TWG_EINVAL, "tier thresholds: need g_warp_cap <= g_block_cap");
+  cudaStream_t st = ctx.stream;
+  for (int k = 0; k < 5; ++k) sizes5[k] = 0;
+  if (n == 0) return;
+  DevBuf<u32> pos(n + 1, st), k0(n, st), k1(n, st), v0(n, st), v1(n, st);
+  exclusive_scan<u32>(ctx, AliveFlagFn{d_alive}, n, pos.p);
+  u64 sc[1];
+  TWG_CUDA(cudaMemsetAsync(ctx.d_scalars, 0, 8, st));
+  TWG_CUDA(cudaMemcpyAsync(ctx.d_scalars, pos.p + n, 4, cudaMemcpyDeviceToDevice, st));
+  read_scalars(ctx, ctx.d_scalars, sc, 1);
+  const u64 alive = sc[0];
+  if (alive == 0) return;
+  k_compact_explicit<<<grid(ctx, n), kBlock, 0, st>>>(d_nodes, d_alive, pos.p, n, k0.p, v0.p);
+  TWG_LAUNCHED(ctx);
+  u32* kp = k0.p;
+  u32* ka = k1.p;
+  u32* vp = v0.p;
+  u32* va = v1.p;
+  const int vb = s.V > 1 ? bit_width_u64(s.V - 1) : 0;
+  radix_sort_pairs<u32>(ctx, &kp, &ka, &vp, &va, alive, vb);
+  std::vector<u32> keys(alive), ids(alive);
+  std::vector<uint2> meta(s.V + 1);
+  TWG_CUDA(cudaMemcpyAsync(keys.data(), kp, alive * 4, cudaMemcpyDeviceToHost, st));
+  TWG_CUDA(cudaMemcpyAsync(ids.data(), vp, alive * 4, cudaMemcpyDeviceToHost, st));
+  TWG_CUDA(cudaMemcpyAsync(meta.data(), s.nmeta.p, (s.V + 1) * sizeof(uint2), cudaMemcpyDeviceToHost, st));
+  TWG_CUDA(cudaStreamSynchronize(st));
+  if (walk_ids) std::memcpy(walk_ids, ids.data(), alive * 4);
+  std::vector<u32> lists[5];  // rows (6 u32 each)
+  for (u64 i = 0; i < alive;) {
+    u64 j = i + 1;
+    while (j < alive && keys[j] == keys[i]) ++j;
+    const u32 v = keys[i];
+    const u32 W = static_cast<u32>(j - i);
+    const u32 G = meta[v + 1].y - meta[v].y;
+    auto push = [&](int tier, u32 b, u32 e, u32 sub, u32 cnt) {
+      lists[tier].insert(lists[tier].end(), {v, b, e, sub, cnt, static_cast<u32>(tier)});
+    };
+    if (W < th.w_warp) push(0, i, j, 0, 1);
+    else if (W <= th.block_dim) push(G <= th.g_warp_cap ? 1 : 2, i, j, 0, 1);
+    else {
+      const int tier = G <= th.g_block_cap ? 3 : 4;
+      if (W <= th.w_max) push(tier, i, j, 0, 1);
+      else {
+        const u32 pieces = (W + th.w_max - 1) / th.w_max;
+        for (u32 p = 0; p < pieces; ++p) {
+          const u32 b = static_cast<u32>(i) + p * th.w_max;
+          push(tier, b, std::min(static_cast<u32>(j), b + th.w_max), p, pieces);
+        }
+      }
+    }
+    i = j;
+  }
+  u64 r = 0;
+  for (int k = 0; k < 5; ++k) {
+    sizes5[k] = lists[k].size() / 6;
+    for (u64 x = 0; x < lists[k].size() / 6 && r < cap; ++x, ++r) std::memcpy(rows + 6 * r, &lists[k][6 * x], 24);
+  }
+}
+
+}  // namespace twg

@@ -1,0 +1,805 @@
+// Walk generation on sm_100a (walk_engine.cpp:147-434).
+//
+// Variants (walk_engine.hpp:31-34), byte-identical outputs (the reference's
+// scheduler-neutrality invariant, test_walk_engine.cpp:294-316):
+//  * FullWalk  — k_fullwalk: one thread per walk, init fused, walk to
+//                completion in registers (walk_engine.cpp:380-392).
+//  * Coop      — the hierarchical cooperative scheduler (Alg. 1,
+//                walk_engine.cpp:301-345): per step, compact alive walks
+//                (flag+scan), stable radix sort by current node, run-length
+//                encode, classify runs on the (W, G) dispatch plane, split
+//                mega-hub runs into ceil(W/w_max) sub-tasks, and launch the
+//                five terminal tiers: solo (thread per task), warp (warp per
+//                task) and block (CTA per (sub-)task), the cached flavours
+//                staging the node's timestamp-group marks in shared memory.
+//  * CoopDirect — Coop with staging disabled (direct global reads).
+//
+// Per-hop semantics are hop_walk (walk_engine.cpp:88-145): causal slice by
+// binary search over the node's marks, draw keyed (walk, length, ordinal),
+// closed-form / weighted pick, node2vec rejection with <=64 retries.
+#include <chrono>
+#include <cstring>
+
+#include "primitives.cuh"
+#include "rng.cuh"
+#include "samplers.cuh"
+#include "walk.cuh"
+
+namespace twg {
+
+namespace {
+
+constexpr int kBlock = 256;
+constexpr u32 kNode2VecMaxRetries = 64;  // samplers.hpp:89
+
+struct WalkParams {
+  StoreView s;
+  Rng rng;
+  int bias;
+  int dir;  // 0 forward, 1 backward
+  int node2vec;
+  int temporal_adj;
+  double inv_p, inv_q, bmax;
+  u32 stride;
+  u64 walk_begin;
+  i64* nodes;
+  i64* times;
+  const double* exp_neg;
+  const double* expm1_tab;
+};
+
+// ---- per-hop pieces -------------------------------------------------------
+
+// walk_engine.cpp:18-34 over marks mt/ms[glo, ghi) of a region [lo, hi)
+__device__ __forceinline__ void causal_slice(const i64* mt, const u32* ms, u32 glo, u32 ghi, u32 lo, u32 hi,
+                                             i64 t, int dir, u32& c, u32& e) {
+  if (dir == 0) {
+    const u32 g = ub_i64(mt, glo, ghi, t);
+    c = g == ghi ? hi : ms[g];
+    e = hi;
+  } else {
+    const u32 g = lb_i64(mt, glo, ghi, t);
+    c = lo;
+    e = g == ghi ? hi : ms[g];
+  }
+}
+
+// walk_engine.cpp:49-63
+__device__ u64 draw_weighted_local(const WalkParams& P, double u, u32 c, u32 e) {
+  const i64 anchor = P.s.ent[e - 1].t;
+  double total = 0.0;
+  for (u32 pos = c; pos < e; ++pos) total = __dadd_rn(total, exp_nonpos(P.s.ent[pos].t - anchor, P.exp_neg));
+  const double r = __dmul_rn(u, total);
+  double cum = 0.0;
+  for (u32 pos = c; pos < e; ++pos) {
+    cum = __dadd_rn(cum, exp_nonpos(P.s.ent[pos].t - anchor, P.exp_neg));
+    if (r < cum) return pos - c;
+  }
+  return e - 1 - c;
+}
+
+// walk_engine.cpp:65-84
+__device__ __forceinline__ u64 draw_index(const WalkParams& P, double u, u32 lo, u32 c, u32 e, u32* amb) {
+  const u64 n = e - c;
+  switch (P.bias) {
+    case TWG_UNIFORM: return pick_uniform(u, n);
+    case TWG_LINEAR: return pick_linear(u, n);
+    case TWG_EXPINDEX: return pick_exponential(u, n, P.expm1_tab, amb);
+    default: {
+      const double base = c > lo ? P.s.wp[c - 1] : 0.0;
+      const double mass = __dsub_rn(P.s.wp[e - 1], base);
+      if (!(mass > 0.0) || !isfinite(mass)) return draw_weighted_local(P, u, c, e);
+      return pick_weighted_range(u, P.s.wp, c, e, base);
+    }
+  }
+}
+
+// edge_store.cpp:310-314
+__device__ __forceinline__ bool adjacent(const StoreView& s, u32 a, u32 b) {
+  u32 lo = s.adj_off[a], hi = s.adj_off[a + 1];
+  const u32 end = hi;
+  while (lo < hi) {
+    const u32 mid = lo + ((hi - lo) >> 1);
+    if (s.adj[mid] < b) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo < end && s.adj[lo] == b;
+}
+
+// edge_store.cpp:316-323
+__device__ bool adjacent_after(const StoreView& s, u32 a, u32 b, i64 t, int dir) {
+  const uint2 na = s.nmeta[a], nb = s.nmeta[a + 1];
+  u32 c, e;
+  causal_slice(s.mk_time, s.mk_start, na.y, nb.y, na.x, nb.x, t, dir, c, e);
+  for (u32 pos = c; pos < e; ++pos)
+    if (s.ent[pos].nbr == b) return true;
+  return false;
+}
+
+struct WalkReg {
+  u32 cur;
+  u32 prev;
+  i64 t;
+  u32 len;
+  u32 has_prev;
+};
+
+// One hop (walk_engine.cpp:88-145). mt/ms: the marks to search, either the
+// global arrays (glo/ghi = node group range) or a shared-memory copy
+// (glo = 0). Returns false when the causal slice is empty (walk dies).
+__device__ __forceinline__ bool hop(const WalkParams& P, u64 wl, WalkReg& r, const i64* mt, const u32* ms, u32 glo,
+                                    u32 ghi, u32 lo, u32 hi, u32* amb) {
+  u32 c, e;
+  causal_slice(mt, ms, glo, ghi, lo, hi, r.t, P.dir, c, e);
+  if (c == e) return false;
+  const u64 w = P.walk_begin + wl;
+  const u64 hop_index = r.len;
+  u64 idx;
+  if (P.node2vec && r.has_prev) {
+    idx = 0;
+    for (u32 k = 0; k < kNode2VecMaxRetries; ++k) {
+      const double u = P.rng.uniform(w, hop_index, 2ull * k);
+      idx = draw_index(P, u, lo, c, e, amb);
+      const u32 cand = P.s.ent[c + idx].nbr;
+      const double ua = P.rng.uniform(w, hop_index, 2ull * k + 1);
+      double beta;  // samplers.hpp:74-86
+      if (cand == r.prev) beta = P.inv_p;
+      else if (P.temporal_adj ? adjacent_after(P.s, r.prev, cand, r.t, P.dir) : adjacent(P.s, r.prev, cand))
+        beta = 1.0;
+      else beta = P.inv_q;
+      if (ua < __ddiv_rn(beta, P.bmax)) break;
+    }
+  } else {
+    const double u = P.rng.uniform(w, hop_index, 0);
+    idx = draw_index(P, u, lo, c, e, amb);
+  }
+  const Entry x = P.s.ent[c + idx];
+  const u64 slot = wl * P.stride + r.len;
+  P.nodes[slot] = P.s.ext[x.nbr];
+  P.times[slot] = x.t;
+  r.len += 1;
+  if (P.node2vec) {
+    r.prev = r.cur;
+    r.has_prev = 1;
+  }
+  r.cur = x.nbr;
+  r.t = x.t;
+  return true;
+}
+
+// walk_engine.cpp:284-299
+__device__ __forceinline__ u64 sample_start_edge_dev(const StoreView& s, int bias, double u1, double u2,
+                                                     const double* expm1_tab, u32* amb) {
+  const u64 Z = s.Z;
+  u64 g;
+  switch (bias) {
+    case TWG_UNIFORM: g = pick_uniform(u1, Z); break;
+    case TWG_LINEAR: g = pick_linear(u1, Z); break;
+    case TWG_EXPINDEX: g = pick_exponential(u1, Z, expm1_tab, amb); break;
+    default: g = pick_weighted(u1, s.ts_w, Z); break;
+  }
+  const u64 lo = s.ts_off[g], hi = s.ts_off[g + 1];
+  u64 off = __double2ull_rz(__dmul_rn(u2, __ull2double_rn(hi - lo)));
+  if (off >= hi - lo) off = hi - lo - 1;
+  return lo + off;
+}
+
+struct InitParams {
+  int start_mode;
+  u32 walks_per_node;
+  int start_bias;
+  const u32* start_nodes;
+  i64 sentinel;
+};
+
+// seed_walk + init_walks (walk_engine.cpp:147-155, :247-279)
+__device__ __forceinline__ void init_walk(const WalkParams& P, const InitParams& I, u64 wl, WalkReg& r, u32* amb) {
+  const u64 w = P.walk_begin + wl;
+  const u64 base = wl * P.stride;
+  r.prev = 0;
+  r.has_prev = 0;
+  if (I.start_mode == 0) {
+    const u32 v = I.start_nodes[w / I.walks_per_node];
+    P.nodes[base] = P.s.ext[v];
+    P.times[base] = I.sentinel;
+    r.cur = v;
+    r.t = I.sentinel;
+    r.len = 1;
+  } else {
+    const double u1 = P.rng.uniform(w, 0, 0);
+    const double u2 = P.rng.uniform(w, 0, 1);
+    const u64 eidx = sample_start_edge_dev(P.s, I.start_bias, u1, u2, P.expm1_tab, amb);
+    const u32 sv = P.s.e_src[eidx], dv = P.s.e_dst[eidx];
+    const i64 t = P.s.e_t[eidx];
+    const u32 from = P.dir == 0 ? sv : dv;
+    const u32 to = P.dir == 0 ? dv : sv;
+    P.nodes[base] = P.s.ext[from];
+    P.times[base] = I.sentinel;
+    P.nodes[base + 1] = P.s.ext[to];
+    P.times[base + 1] = t;
+    r.len = 2;
+    r.cur = to;
+    r.t = t;
+    if (P.node2vec) {
+      r.prev = from;
+      r.has_prev = 1;
+    }
+  }
+}
+
+// stats[0] walks, [1] hops, [2] max hops (fullwalk steps), [3] ambiguous
+__device__ __forceinline__ void add_stats(u64* stats, u32 len, u32 init_len, u32 amb, bool active) {
+  u64 walks = active && len >= 2 ? 1 : 0;
+  u64 hops = active && len >= 2 ? len - 1 : 0;
+  u64 steps = active ? len - init_len : 0;
+  u64 a = amb;
+  for (int o = 16; o > 0; o >>= 1) {
+    walks += __shfl_xor_sync(0xffffffffu, walks, o);
+    hops += __shfl_xor_sync(0xffffffffu, hops, o);
+    steps = max(steps, __shfl_xor_sync(0xffffffffu, steps, o));
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (walks) atomicAdd(reinterpret_cast<unsigned long long*>(&stats[0]), walks);
+    if (hops) atomicAdd(reinterpret_cast<unsigned long long*>(&stats[1]), hops);
+    if (steps) atomicMax(reinterpret_cast<unsigned long long*>(&stats[2]), steps);
+    if (a) atomicAdd(reinterpret_cast<unsigned long long*>(&stats[3]), a);
+  }
+}
+
+// ---- FullWalk -----------------------------------------------------------------
+
+__global__ void __launch_bounds__(kBlock) k_fullwalk(WalkParams P, InitParams I, u64 count, u32* lengths, u64* stats) {
+  const u64 wl = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x;
+  const bool active = wl < count;
+  u32 amb = 0;
+  u32 init_len = 0;
+  WalkReg r{};
+  if (active) {
+    init_walk(P, I, wl, r, &amb);
+    init_len = r.len;
+    while (r.len < P.stride) {
+      const uint2 a = P.s.nmeta[r.cur], b = P.s.nmeta[r.cur + 1];
+      if (!hop(P, wl, r, P.s.mk_time, P.s.mk_start, a.y, b.y, a.x, b.x, &amb)) break;
+    }
+    lengths[wl] = r.len;
+  }
+  add_stats(stats, r.len, init_len, amb, active);
+}
+
+// ---- Coop scheduler -------------------------------------------------------------
+
+struct StateArrays {
+  u32* cur;
+  u32* prev;
+  i64* t;
+  u32* len;
+  u8* flags;  // bit0 alive, bit1 has_prev
+};
+
+__global__ void __launch_bounds__(kBlock) k_init_states(WalkParams P, InitParams I, u64 count, StateArrays S,
+                                                        u64* stats) {
+  const u64 wl = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x;
+  u32 amb = 0;
+  if (wl < count) {
+    WalkReg r{};
+    init_walk(P, I, wl, r, &amb);
+    S.cur[wl] = r.cur;
+    S.prev[wl] = r.prev;
+    S.t[wl] = r.t;
+    S.len[wl] = r.len;
+    S.flags[wl] = static_cast<u8>((r.len < P.stride ? 1 : 0) | (r.has_prev ? 2 : 0));
+  }
+  for (int o = 16; o > 0; o >>= 1) amb += __shfl_xor_sync(0xffffffffu, amb, o);
+  if ((threadIdx.x & 31) == 0 && amb) atomicAdd(reinterpret_cast<unsigned long long*>(&stats[3]), (u64)amb);
+}
+
+struct AliveFn {
+  const u32* ids;
+  const u8* flags;
+  __device__ __forceinline__ u32 operator()(u64 i) const { return flags[ids[i]] & 1u; }
+};
+
+__global__ void k_compact_alive(const u32* ids, u64 n, const u8* flags, const u32* cur, const u32* pos, u32* keys,
+                                u32* vals) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const u32 w = ids[i];
+    if (flags[w] & 1u) {
+      keys[pos[i]] = cur[w];
+      vals[pos[i]] = w;
+    }
+  }
+}
+
+struct RunFlagFn {
+  const u32* keys;
+  __device__ __forceinline__ u32 operator()(u64 i) const { return (i == 0 || keys[i] != keys[i - 1]) ? 1u : 0u; }
+};
+
+// DispatchTask (walk_engine.hpp:87-94)
+struct Task {
+  u32 node;
+  u32 begin;  // slice of the step's grouped walk ids
+  u32 end;
+  u32 sub;    // sub_task_index
+};
+
+struct TaskLists {
+  Task* list[5];     // solo, warp_cached, warp_direct, block_cached, block_direct
+  u32* subcount[5];  // sub_task_count per task
+  // count[0..4] tasks per list; count[5] / count[6] split pieces in the
+  // block-cached / block-direct lists (booked as multi_block, :157-161)
+  u32* count;
+};
+
+struct OneFn {
+  __device__ __forceinline__ u32 operator()(u64) const { return 1u; }
+};
+
+// Classify runs on the dispatch plane (walk_engine.cpp:314-343).
+__global__ void k_classify(const u32* keys, u64 n, StoreView s, twg_thresholds th, TaskLists T) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    if (!(i == 0 || keys[i] != keys[i - 1])) continue;
+    // run [i, end): galloping search for the first j > i with keys[j] != keys[i]
+    const u32 v = keys[i];
+    u64 lo = i + 1, step = 1, hi = i + 1;
+    while (hi < n && keys[hi] == v) {
+      lo = hi + 1;
+      hi = i + 1 + step;
+      step <<= 1;
+    }
+    if (hi > n) hi = n;
+    while (lo < hi) {  // first j in [lo, hi) with keys[j] != v
+      const u64 mid = (lo + hi) >> 1;
+      if (keys[mid] == v) lo = mid + 1;
+      else hi = mid;
+    }
+    const u64 end = lo;
+    const u32 W = static_cast<u32>(end - i);
+    const u32 G = s.nmeta[v + 1].y - s.nmeta[v].y;
+    int tier;
+    u32 pieces = 1;
+    if (W < th.w_warp) tier = 0;
+    else if (W <= th.block_dim) tier = G <= th.g_warp_cap ? 1 : 2;
+    else {
+      tier = G <= th.g_block_cap ? 3 : 4;
+      if (W > th.w_max) pieces = (W + th.w_max - 1) / th.w_max;
+    }
+    const u32 slot = atomicAdd(&T.count[tier], pieces);
+    if (pieces > 1) atomicAdd(&T.count[tier == 3 ? 5 : 6], pieces);
+    for (u32 p = 0; p < pieces; ++p) {
+      Task task;
+      task.node = v;
+      task.begin = static_cast<u32>(i) + p * th.w_max;
+      task.end = pieces > 1 ? min(static_cast<u32>(end), task.begin + th.w_max) : static_cast<u32>(end);
+      task.sub = p;
+      T.list[tier][slot + p] = task;
+      T.subcount[tier][slot + p] = pieces;
+    }
+  }
+}
+
+__device__ __forceinline__ void load_state(const StateArrays& S, u32 w, WalkReg& r) {
+  r.cur = S.cur[w];
+  r.prev = S.prev[w];
+  r.t = S.t[w];
+  r.len = S.len[w];
+  r.has_prev = (S.flags[w] >> 1) & 1u;
+}
+
+__device__ __forceinline__ void store_state(const StateArrays& S, u32 w, const WalkReg& r, bool alive, u32 stride) {
+  S.cur[w] = r.cur;
+  S.prev[w] = r.prev;
+  S.t[w] = r.t;
+  S.len[w] = r.len;
+  S.flags[w] = static_cast<u8>(((alive && r.len < stride) ? 1 : 0) | (r.has_prev ? 2 : 0));
+}
+
+__device__ __forceinline__ void hop_member(const WalkParams& P, const StateArrays& S, u32 w, const i64* mt,
+                                           const u32* ms, u32 glo, u32 ghi, u32 lo, u32 hi, u32* amb) {
+  WalkReg r;
+  load_state(S, w, r);
+  const bool alive = hop(P, w, r, mt, ms, glo, ghi, lo, hi, amb);
+  store_state(S, w, r, alive, P.stride);
+}
+
+// solo tier: one thread per task (W < w_warp), global marks
+__global__ void __launch_bounds__(kBlock) k_tier_solo(WalkParams P, StateArrays S, const u32* ids, const Task* tasks,
+                                                      const u32* count, u64* stats) {
+  const u32 n = *count;
+  u32 amb = 0;
+  for (u32 k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const Task task = tasks[k];
+    const uint2 a = P.s.nmeta[task.node], b = P.s.nmeta[task.node + 1];
+    for (u32 i = task.begin; i < task.end; ++i)
+      hop_member(P, S, ids[i], P.s.mk_time, P.s.mk_start, a.y, b.y, a.x, b.x, &amb);
+  }
+  for (int o = 16; o > 0; o >>= 1) amb += __shfl_xor_sync(0xffffffffu, amb, o);
+  if ((threadIdx.x & 31) == 0 && amb) atomicAdd(reinterpret_cast<unsigned long long*>(&stats[3]), (u64)amb);
+}
+
+// warp tiers: one warp per task; cached => the node's marks staged in this
+// warp's shared-memory slice (G <= cap)
+template <bool kCached>
+__global__ void __launch_bounds__(kBlock) k_tier_warp(WalkParams P, StateArrays S, const u32* ids, const Task* tasks,
+                                                      const u32* count, u32 cap, u64* stats) {
+  extern __shared__ unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const u32 n = *count;
+  i64* smt = reinterpret_cast<i64*>(smem_raw) + static_cast<u64>(warp) * cap;
+  u32* sms = reinterpret_cast<u32*>(reinterpret_cast<i64*>(smem_raw) + static_cast<u64>(kBlock / 32) * cap) +
+             static_cast<u64>(warp) * cap;
+  u32 amb = 0;
+  for (u32 k = blockIdx.x * (kBlock / 32) + warp; k < n; k += gridDim.x * (kBlock / 32)) {
+    const Task task = tasks[k];
+    const uint2 a = P.s.nmeta[task.node], b = P.s.nmeta[task.node + 1];
+    const u32 G = b.y - a.y;
+    if (kCached && G <= cap) {
+      for (u32 g = lane; g < G; g += 32) {
+        smt[g] = P.s.mk_time[a.y + g];
+        sms[g] = P.s.mk_start[a.y + g];
+      }
+      __syncwarp();
+      for (u32 i = task.begin + lane; i < task.end; i += 32)
+        hop_member(P, S, ids[i], smt, sms, 0, G, a.x, b.x, &amb);
+      __syncwarp();
+    } else {
+      for (u32 i = task.begin + lane; i < task.end; i += 32)
+        hop_member(P, S, ids[i], P.s.mk_time, P.s.mk_start, a.y, b.y, a.x, b.x, &amb);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) amb += __shfl_xor_sync(0xffffffffu, amb, o);
+  if (lane == 0 && amb) atomicAdd(reinterpret_cast<unsigned long long*>(&stats[3]), (u64)amb);
+}
+
+// block tiers: one CTA per (sub-)task; cached => marks staged in the CTA's
+// shared memory (G <= cap). Mega-hub sub-tasks each reload the panel
+// (PAPER.md:187).
+template <bool kCached>
+__global__ void __launch_bounds__(kBlock) k_tier_block(WalkParams P, StateArrays S, const u32* ids, const Task* tasks,
+                                                       const u32* count, u32 cap, u64* stats) {
+  extern __shared__ unsigned char smem_raw[];
+  i64* smt = reinterpret_cast<i64*>(smem_raw);
+  u32* sms = reinterpret_cast<u32*>(smt + cap);
+  const u32 n = *count;
+  u32 amb = 0;
+  for (u32 k = blockIdx.x; k < n; k += gridDim.x) {
+    const Task task = tasks[k];
+    const uint2 a = P.s.nmeta[task.node], b = P.s.nmeta[task.node + 1];
+    const u32 G = b.y - a.y;
+    if (kCached && G <= cap) {
+      __syncthreads();
+      for (u32 g = threadIdx.x; g < G; g += blockDim.x) {
+        smt[g] = P.s.mk_time[a.y + g];
+        sms[g] = P.s.mk_start[a.y + g];
+      }
+      __syncthreads();
+      for (u32 i = task.begin + threadIdx.x; i < task.end; i += blockDim.x)
+        hop_member(P, S, ids[i], smt, sms, 0, G, a.x, b.x, &amb);
+    } else {
+      for (u32 i = task.begin + threadIdx.x; i < task.end; i += blockDim.x)
+        hop_member(P, S, ids[i], P.s.mk_time, P.s.mk_start, a.y, b.y, a.x, b.x, &amb);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) amb += __shfl_xor_sync(0xffffffffu, amb, o);
+  if ((threadIdx.x & 31) == 0 && amb) atomicAdd(reinterpret_cast<unsigned long long*>(&stats[3]), (u64)amb);
+}
+
+__global__ void k_finalize(const StateArrays S, u64 count, u32* lengths, u64* stats) {
+  const u64 wl = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x;
+  const bool active = wl < count;
+  const u32 len = active ? S.len[wl] : 0;
+  if (active) lengths[wl] = len;
+  add_stats(stats, len, len, 0, active);
+}
+
+__global__ void k_start_flags(const uint2* nmeta, u64 V, u32* flags) {
+  for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < V;
+       v += static_cast<u64>(gridDim.x) * blockDim.x)
+    flags[v] = nmeta[v].x != nmeta[v + 1].x ? 1u : 0u;
+}
+
+__global__ void k_start_nodes(const u32* flags, const u32* pos, u64 V, u32* out) {
+  for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < V;
+       v += static_cast<u64>(gridDim.x) * blockDim.x)
+    if (flags[v]) out[pos[v]] = static_cast<u32>(v);
+}
+
+__global__ void k_zero_tails(i64* nodes, i64* times, const u32* lengths, u64 count, u32 stride) {
+  const u64 total = count * stride;
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const u64 w = i / stride;
+    const u32 slot = static_cast<u32>(i - w * stride);
+    if (slot >= lengths[w]) {
+      nodes[i] = 0;
+      times[i] = 0;
+    }
+  }
+}
+
+struct LenFn {
+  const u32* len;
+  __device__ __forceinline__ u64 operator()(u64 i) const { return len[i]; }
+};
+
+__global__ void k_compact_walks(const i64* nodes, const i64* times, const u32* lengths, const u64* offs, u64 count,
+                                u32 stride, i64* cn, i64* ct) {
+  for (u64 w = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; w < count;
+       w += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const u64 o = offs[w];
+    for (u32 j = 0; j < lengths[w]; ++j) {
+      cn[o + j] = nodes[w * stride + j];
+      ct[o + j] = times[w * stride + j];
+    }
+  }
+}
+
+unsigned grid(Ctx& ctx, u64 n) { return grid_for(n, kBlock, static_cast<unsigned>(ctx.sm_count) * 32); }
+
+WalkParams make_params(Ctx& ctx, Store& s, const twg_walk_config& cfg, u32 stride, u64 walk_begin, WalkSetDev& out) {
+  WalkParams P;
+  P.s = s.view();
+  P.rng = Rng::make(cfg.rng, cfg.seed);
+  P.bias = cfg.bias;
+  P.dir = cfg.direction;
+  P.node2vec = cfg.node2vec;
+  P.temporal_adj = cfg.temporal_adjacency;
+  if (cfg.node2vec) {
+    P.inv_p = 1.0 / cfg.p;
+    P.inv_q = 1.0 / cfg.q;
+    P.bmax = P.inv_p;  // samplers.hpp:27-29 max({1/p, 1, 1/q})
+    if (1.0 > P.bmax) P.bmax = 1.0;
+    if (P.inv_q > P.bmax) P.bmax = P.inv_q;
+  } else {
+    P.inv_p = P.inv_q = P.bmax = 1.0;
+  }
+  P.stride = stride;
+  P.walk_begin = walk_begin;
+  P.nodes = out.nodes.p;
+  P.times = out.times.p;
+  P.exp_neg = ctx.d_exp_neg;
+  P.expm1_tab = ctx.d_expm1;
+  return P;
+}
+
+}  // namespace
+
+void zero_walk_tails(Ctx& ctx, WalkSetDev& w) {
+  if (w.tails_zeroed || w.count == 0) return;
+  k_zero_tails<<<grid(ctx, w.count * w.stride), kBlock, 0, ctx.stream>>>(w.nodes.p, w.times.p, w.lengths.p, w.count,
+                                                                          w.stride);
+  TWG_LAUNCHED(ctx);
+  w.tails_zeroed = true;
+}
+
+void compact_walks(Ctx& ctx, const WalkSetDev& w, DevBuf<u64>& offsets, DevBuf<i64>& nodes, DevBuf<i64>& times,
+                   u64* total) {
+  offsets.alloc(w.count + 1, ctx.stream);
+  exclusive_scan<u64>(ctx, LenFn{w.lengths.p}, w.count, offsets.p);
+  u64 tot[1];
+  read_scalars(ctx, offsets.p + w.count, tot, 1);
+  *total = tot[0];
+  nodes.alloc(tot[0] ? tot[0] : 1, ctx.stream);
+  times.alloc(tot[0] ? tot[0] : 1, ctx.stream);
+  if (w.count) {
+    k_compact_walks<<<grid(ctx, w.count), kBlock, 0, ctx.stream>>>(w.nodes.p, w.times.p, w.lengths.p, offsets.p,
+                                                                    w.count, w.stride, nodes.p, times.p);
+    TWG_LAUNCHED(ctx);
+  }
+}
+
+WalkSetDev* generate_walks(Ctx& ctx, Store& s, const twg_walk_config& cfg, const twg_thresholds& th, int variant,
+                           twg_walk_stats* stats_out) {
+  using clock = std::chrono::steady_clock;
+  const auto started = clock::now();
+  cudaStream_t st = ctx.stream;
+  // WalkConfig::validate (walk_engine.cpp:198-206), TierThresholds::validate (:189-196)
+  if (cfg.walk_length < 1) fail(TWG_EINVAL, "walk config: walk_length must be >= 1");
+  if (cfg.start_mode == 0 && cfg.walks_per_node == 0) fail(TWG_EINVAL, "walk config: walks_per_node must be positive");
+  if (cfg.node2vec && (cfg.p <= 0.0 || cfg.q <= 0.0)) fail(TWG_EINVAL, "walk config: node2vec p and q must be positive");
+  if (th.w_warp < 1 || th.w_warp > th.block_dim || th.block_dim > th.w_max)
+    fail(TWG_EINVAL, "tier thresholds: need 1 <= w_warp <= block_dim <= w_max");
+  if (th.g_warp_cap > th.g_block_cap) fail(TWG_EINVAL, "tier thresholds: need g_warp_cap <= g_block_cap");
+  if (cfg.bias < 0 || cfg.bias > 3 || cfg.start_bias < 0 || cfg.start_bias > 3) fail(TWG_EINVAL, "walk config: bias");
+  if (cfg.direction != 0 && cfg.direction != 1) fail(TWG_EINVAL, "walk config: direction");
+  if (cfg.rng != TWG_RNG_SPLITMIX && cfg.rng != TWG_RNG_PHILOX) fail(TWG_EINVAL, "walk config: rng");
+  // EdgeStore::supports (edge_store.hpp:60-63), walk_engine.cpp:368-370
+  const bool supports = s.mode == TWG_UNDIRECTED || ((s.mode == TWG_FORWARD) == (cfg.direction == 0));
+  if (!supports)
+    fail(TWG_EINVAL, "generate_walks: store direction mode does not serve the requested walk direction");
+  if (cfg.bias == TWG_EXPWEIGHT || cfg.start_bias == TWG_EXPWEIGHT) ensure_weights(ctx, s);
+  if (cfg.node2vec && !cfg.temporal_adjacency) ensure_adjacency(ctx, s);
+
+  auto out = std::make_unique<WalkSetDev>();
+  out->ctx = &ctx;
+  // init_walks (walk_engine.cpp:208-245)
+  u64 total = 0;
+  DevBuf<u32> start_nodes;
+  if (cfg.start_mode == 0) {
+    DevBuf<u32> flags(s.V ? s.V : 1, st), pos(s.V + 1, st);
+    if (s.V) {
+      k_start_flags<<<grid(ctx, s.V), kBlock, 0, st>>>(s.nmeta.p, s.V, flags.p);
+      TWG_LAUNCHED(ctx);
+    }
+    exclusive_scan<u32>(ctx, LoadFn<u32>{flags.p}, s.V, pos.p);
+    u64 sc[1];
+    TWG_CUDA(cudaMemsetAsync(ctx.d_scalars, 0, 8, st));
+    TWG_CUDA(cudaMemcpyAsync(ctx.d_scalars, pos.p + s.V, 4, cudaMemcpyDeviceToDevice, st));
+    read_scalars(ctx, ctx.d_scalars, sc, 1);
+    start_nodes.alloc(sc[0] ? sc[0] : 1, st);
+    if (s.V) {
+      k_start_nodes<<<grid(ctx, s.V), kBlock, 0, st>>>(flags.p, pos.p, s.V, start_nodes.p);
+      TWG_LAUNCHED(ctx);
+    }
+    total = sc[0] * static_cast<u64>(cfg.walks_per_node);
+    out->stride = cfg.walk_length;
+  } else {
+    if (s.m == 0) fail(TWG_EINVAL, "init_walks: sampled starts need a non-empty store");
+    total = cfg.total_walks;
+    out->stride = cfg.walk_length > 2 ? cfg.walk_length : 2;
+  }
+  if (total >= 0xffffffffull) fail(TWG_EINVAL, "init_walks: walk count exceeds 32-bit id space");
+  u64 wb = cfg.walk_begin, we = cfg.walk_end;
+  if (wb == 0 && we == 0) we = total;
+  if (we > total) we = total;
+  if (wb > we) wb = we;
+  const u64 count = we - wb;
+  out->first = wb;
+  out->count = count;
+  out->nodes.alloc(count * out->stride ? count * out->stride : 1, st);
+  out->times.alloc(count * out->stride ? count * out->stride : 1, st);
+  out->lengths.alloc(count ? count : 1, st);
+
+  DevBuf<u64> stats(8, st);
+  TWG_CUDA(cudaMemsetAsync(stats.p, 0, stats.bytes(), st));
+  WalkParams P = make_params(ctx, s, cfg, out->stride, wb, *out);
+  InitParams I;
+  I.start_mode = cfg.start_mode;
+  I.walks_per_node = cfg.walks_per_node;
+  I.start_bias = cfg.start_bias;
+  I.start_nodes = start_nodes.p;
+  I.sentinel = cfg.direction == 0 ? kTimeUnset : kTimeInfinite;  // types.hpp:47-49
+
+  u64 tiers[6] = {0, 0, 0, 0, 0, 0};
+  u64 coop_steps = 0;
+  if (count == 0) {
+    // nothing to do
+  } else if (variant == TWG_FULLWALK) {
+    k_fullwalk<<<grid_for(count, kBlock, 0xffffffffu), kBlock, 0, st>>>(P, I, count, out->lengths.p, stats.p);
+    TWG_LAUNCHED(ctx);
+  } else {
+    const bool cache = variant == TWG_COOP;
+    DevBuf<u32> cur(count, st), prev(count, st), len(count, st);
+    DevBuf<i64> tt(count, st);
+    DevBuf<u8> flags(count, st);
+    StateArrays S{cur.p, prev.p, tt.p, len.p, flags.p};
+    k_init_states<<<grid_for(count, kBlock, 0xffffffffu), kBlock, 0, st>>>(P, I, count, S, stats.p);
+    TWG_LAUNCHED(ctx);
+    DevBuf<u32> ids(count, st), pos(count + 1, st), k0(count, st), k1(count, st), v0(count, st), v1(count, st);
+    DevBuf<Task> tasks(5 * count, st);
+    DevBuf<u32> subcount(5 * count, st);
+    DevBuf<u32> counters(8, st);
+    // candidates = iota (walk_engine.cpp:395-398), as the scan of all-ones
+    exclusive_scan<u32>(ctx, OneFn{}, count, ids.p);
+    u64 n_cand = count;
+    const int vb = s.V > 1 ? bit_width_u64(s.V - 1) : 0;
+    TaskLists T;
+    for (int k = 0; k < 5; ++k) {
+      T.list[k] = tasks.p + k * count;
+      T.subcount[k] = subcount.p + k * count;
+    }
+    T.count = counters.p;
+    const u32 warp_cap = th.g_warp_cap;
+    u32 block_cap = th.g_block_cap;
+    const size_t warp_smem = static_cast<size_t>(warp_cap) * 12 * (kBlock / 32);
+    const bool warp_stage = cache && warp_smem <= 200 * 1024;
+    if (block_cap * 12ull > 200 * 1024) block_cap = 200 * 1024 / 12;
+    const size_t block_smem = static_cast<size_t>(block_cap) * 12;
+    if (warp_stage)
+      TWG_CUDA(cudaFuncSetAttribute(k_tier_warp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(warp_smem)));
+    if (cache)
+      TWG_CUDA(cudaFuncSetAttribute(k_tier_block<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(block_smem)));
+    while (true) {
+      // 1. flag + compact alive (partition_flagged, primitives.cpp:140-148)
+      exclusive_scan<u32>(ctx, AliveFn{ids.p, flags.p}, n_cand, pos.p);
+      u64 sc[1];
+      TWG_CUDA(cudaMemsetAsync(ctx.d_scalars, 0, 8, st));
+      TWG_CUDA(cudaMemcpyAsync(ctx.d_scalars, pos.p + n_cand, 4, cudaMemcpyDeviceToDevice, st));
+      read_scalars(ctx, ctx.d_scalars, sc, 1);
+      const u64 n = sc[0];
+      if (n == 0) break;
+      ++coop_steps;
+      k_compact_alive<<<grid(ctx, n_cand), kBlock, 0, st>>>(ids.p, n_cand, flags.p, cur.p, pos.p, k0.p, v0.p);
+      TWG_LAUNCHED(ctx);
+      // 2. stable sort (node, walk) by node
+      u32* kp = k0.p;
+      u32* ka = k1.p;
+      u32* vp = v0.p;
+      u32* va = v1.p;
+      radix_sort_pairs<u32>(ctx, &kp, &ka, &vp, &va, n, vb);
+      // 3-5. RLE + dispatch plane + mega-hub split
+      TWG_CUDA(cudaMemsetAsync(counters.p, 0, counters.bytes(), st));
+      k_classify<<<grid(ctx, n), kBlock, 0, st>>>(kp, n, s.view(), th, T);
+      TWG_LAUNCHED(ctx);
+      u32 cnt[8];
+      TWG_CUDA(cudaMemcpyAsync(ctx.h_pinned, counters.p, 8 * sizeof(u32), cudaMemcpyDeviceToHost, st));
+      TWG_CUDA(cudaStreamSynchronize(st));
+      std::memcpy(cnt, ctx.h_pinned, sizeof cnt);
+      // tier counts (count_tier, walk_engine.cpp:157-169): split pieces count as multi_block
+      for (int k = 0; k < 3; ++k) tiers[k] += cnt[k];
+      tiers[3] += cnt[3] - cnt[5];
+      tiers[4] += cnt[4] - cnt[6];
+      tiers[5] += cnt[5] + cnt[6];
+      // 6. terminal tiers
+      if (cnt[0]) {
+        k_tier_solo<<<grid(ctx, cnt[0]), kBlock, 0, st>>>(P, S, vp, T.list[0], counters.p + 0, stats.p);
+        TWG_LAUNCHED(ctx);
+      }
+      if (cnt[1]) {
+        if (warp_stage) {
+          k_tier_warp<true><<<static_cast<unsigned>(std::min<u64>((cnt[1] + 7) / 8, 1u << 20)), kBlock, warp_smem, st>>>(
+              P, S, vp, T.list[1], counters.p + 1, warp_cap, stats.p);
+        } else {
+          k_tier_warp<false><<<static_cast<unsigned>(std::min<u64>((cnt[1] + 7) / 8, 1u << 20)), kBlock, 0, st>>>(
+              P, S, vp, T.list[1], counters.p + 1, 0, stats.p);
+        }
+        TWG_LAUNCHED(ctx);
+      }
+      if (cnt[2]) {
+        k_tier_warp<false><<<static_cast<unsigned>(std::min<u64>((cnt[2] + 7) / 8, 1u << 20)), kBlock, 0, st>>>(
+            P, S, vp, T.list[2], counters.p + 2, 0, stats.p);
+        TWG_LAUNCHED(ctx);
+      }
+      if (cnt[3]) {
+        if (cache) {
+          k_tier_block<true><<<static_cast<unsigned>(std::min<u64>(cnt[3], 1u << 20)), kBlock, block_smem, st>>>(
+              P, S, vp, T.list[3], counters.p + 3, block_cap, stats.p);
+        } else {
+          k_tier_block<false><<<static_cast<unsigned>(std::min<u64>(cnt[3], 1u << 20)), kBlock, 0, st>>>(
+              P, S, vp, T.list[3], counters.p + 3, 0, stats.p);
+        }
+        TWG_LAUNCHED(ctx);
+      }
+      if (cnt[4]) {
+        k_tier_block<false><<<static_cast<unsigned>(std::min<u64>(cnt[4], 1u << 20)), kBlock, 0, st>>>(
+            P, S, vp, T.list[4], counters.p + 4, 0, stats.p);
+        TWG_LAUNCHED(ctx);
+      }
+      // next candidates = this step's grouped order (walk_engine.cpp:416)
+      TWG_CUDA(cudaMemcpyAsync(ids.p, vp, n * sizeof(u32), cudaMemcpyDeviceToDevice, st));
+      n_cand = n;
+    }
+    k_finalize<<<grid_for(count, kBlock, 0xffffffffu), kBlock, 0, st>>>(S, count, out->lengths.p, stats.p);
+    TWG_LAUNCHED(ctx);
+  }
+  u64 hs[4];
+  read_scalars(ctx, stats.p, hs, 4);
+  out->hops = hs[1];
+  if (stats_out) {
+    twg_walk_stats w{};
+    w.walks = hs[0];
+    w.hops = hs[1];
+    w.ambiguous_draws = hs[3];
+    if (variant == TWG_FULLWALK) {
+      w.steps = hs[2];
+    } else {
+      w.steps = coop_steps;
+      w.solo = tiers[0];
+      w.warp_cached = tiers[1];
+      w.warp_direct = tiers[2];
+      w.block_cached = tiers[3];
+      w.block_direct = tiers[4];
+      w.multi_block = tiers[5];
+    }
+    w.wall_seconds = std::chrono::duration<double>(clock::now() - started).count();
+    *stats_out = w;
+  }
+  return out.release();
+}
+
+}  // namespace twg

@@ -1,0 +1,51 @@
+// Walk generation on the device (walk_engine.cpp:147-434).
+#pragma once
+
+#include "store.cuh"
+
+namespace twg {
+
+struct WalkSetDev {
+  Ctx* ctx = nullptr;
+  u32 stride = 0;
+  u64 count = 0;       // walks in this shard
+  u64 first = 0;       // global id of local walk 0
+  u64 hops = 0;
+  DevBuf<i64> nodes;   // [count * stride] walk-major, external ids
+  DevBuf<i64> times;   // [count * stride]
+  DevBuf<u32> lengths; // [count]
+  bool tails_zeroed = false;
+};
+
+// Validates like walk_engine.cpp:189-206 / :366-370 (throws Error(TWG_EINVAL)).
+WalkSetDev* generate_walks(Ctx& ctx, Store& s, const twg_walk_config& cfg, const twg_thresholds& th,
+                           int variant, twg_walk_stats* stats);
+
+// zero the unused slots so the fixed-stride image equals the reference's
+// zero-initialised WalkSet (walk_engine.cpp:237-239)
+void zero_walk_tails(Ctx& ctx, WalkSetDev& w);
+
+// compact (CSR) image on the device: offsets[count+1], nodes/times[total]
+void compact_walks(Ctx& ctx, const WalkSetDev& w, DevBuf<u64>& offsets, DevBuf<i64>& nodes,
+                   DevBuf<i64>& times, u64* total);
+
+void sample_start_edges(Ctx& ctx, Store& s, int bias, const double* d_u1, const double* d_u2, u64 n,
+                        u64* d_out);
+
+// schedule_step over explicit populations; returns list sizes + rows (host)
+void schedule_step_explicit(Ctx& ctx, Store& s, const u32* d_nodes, const u8* d_alive, u64 n,
+                            const twg_thresholds& th, u64* sizes5, u32* rows, u64 cap, u32* walk_ids);
+
+void pick_index_batch(Ctx& ctx, int kind, const double* d_u, const u64* d_n, u64 count, u64* d_out);
+void pick_weighted_range_batch(Ctx& ctx, const double* d_u, const double* d_prefix, const u64* d_begin,
+                               const u64* d_end, const double* d_base, u64 count, u64* d_out);
+void rng_bits_batch(Ctx& ctx, int rng, u64 seed, const u64* d_walk, const u64* d_hop, const u64* d_ord,
+                    u64 count, u64* d_out);
+
+// batched queries on a store
+void neighborhood_batch(Ctx& ctx, Store& s, const i64* d_v, const i64* d_t, u64 n, int dir, u64* d_out3);
+void find_nodes_batch(Ctx& ctx, Store& s, const i64* d_v, u64 n, u32* d_internal, u8* d_found);
+void adjacent_batch(Ctx& ctx, Store& s, const u32* d_a, const u32* d_b, u64 n, int temporal, const i64* d_t,
+                    int dir, u8* d_out);
+
+}  // namespace twg

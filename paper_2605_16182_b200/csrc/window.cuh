@@ -1,0 +1,29 @@
+// Sliding-window ingestion on the device (window_manager.cpp:9-69).
+#pragma once
+
+#include "store.cuh"
+
+namespace twg {
+
+struct Window {
+  Ctx* ctx = nullptr;
+  i64 duration = 0;
+  int mode = 0;
+  BuildOpts opts;
+  Store* store = nullptr;     // current snapshot (holds one reference)
+  Store* previous = nullptr;  // exactly one retired snapshot (window_manager.hpp:40, :57-58)
+  i64 t_high = kTimeUnset;
+  u64 batch_count = 0;
+  twg_batch_stats stats{};
+
+  i64 cutoff_for(i64 high) const { return high > duration ? high - duration : 0; }  // window_manager.hpp:51-53
+};
+
+void release_store(Store* s);
+
+Window* window_create(Ctx& ctx, i64 duration, int mode, BuildOpts opts);
+void window_destroy(Window* w);
+// Device-resident SoA batch. stats may be null.
+void window_ingest(Window& w, const i64* d_src, const i64* d_dst, const i64* d_t, u64 n, twg_batch_stats* out);
+
+}  // namespace twg
