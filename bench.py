@@ -1,0 +1,551 @@
+#!/usr/bin/env python3
+"""Benchmark of the streaming temporal-walk hot path (BASELINE.json metric:
+walk steps/sec + edges ingested/sec over a 1B-edge sliding-window stream).
+
+Workload (BASELINE configs[4]): synthetic power-law stream,
+edge i = (src = bits(1,i,0) % N, dst = floor(N*u^3), t = floor(i/4)),
+N = 10M nodes, seed 5; batches of 50M edges (batch_duration 12.5M time
+units), sliding window Δ = floor(span/3) = 83,333,333 (≈333M-edge window),
+ExponentialIndex bias, 10M sampled walks per batch per GPU, L = 80.
+One bench "step" = one batch: sliding-window ingest (eviction + full dual
+index rebuild on the device) + walk generation on the fresh snapshot.
+
+The window is pre-filled (untimed) to steady state, then W warm-up steps,
+then K timed steps (default 7 + 3 + 10 = 20 batches = the 1B-edge stream).
+
+  value      walk steps / s over the timed steps, inputs already in HBM
+             (batches pre-generated on the device); edges/s beside it.
+  e2e        the same through the reference-facing C ABI with HOST buffers:
+             pinned host batch -> twg_window_ingest (H2D inside) ->
+             twg_generate -> compact walk download to pinned host memory.
+  roofline   walk kernel (k_fullwalk): algorithmic bytes (SURVEY §8d
+             B_hop = 80 + 8*ceil(log2(G_v+1)) summed per hop on the device)
+             / walk-phase device time, against MEASURED_PEAKS.json hbm_gbs.
+
+Multi-GPU (torchrun): every batch is H2D'd / generated once on rank 0 and
+broadcast over NVLink (NCCL) into each rank's replica window; each rank
+generates its own 10M walks (disjoint global walk ids) -> weak scaling.
+`--impl reference` times the reference's own CPU implementation
+(oracle/_ref, unmodified proj/core) on a bounded sample of this workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "walk steps/sec + edges ingested/sec, 1B-edge sliding-window stream, 1–8 B200"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scale", type=float, default=1.0, help="workload scale (1.0 = C5)")
+    ap.add_argument("--variant", default="fullwalk", choices=["fullwalk", "coop", "coopdirect"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+class Workload:
+    def __init__(self, scale: float):
+        self.nodes = max(1000, int(10_000_000 * scale))
+        self.batch_edges = max(4000, int(50_000_000 * scale))
+        self.batch_duration = self.batch_edges // 4          # t = floor(i/4)
+        self.total_edges = 20 * self.batch_edges              # 1B at scale 1
+        span = self.total_edges // 4
+        self.window = span // 3                               # Δ = floor(span/3) (main.cpp:186)
+        self.prefill = math.ceil(self.window / self.batch_duration)  # batches to reach steady state
+        self.walks = max(1000, int(10_000_000 * scale))
+        self.walk_length = 80
+        self.seed = 5
+
+    def describe(self, scale):
+        return {"workload": "C5: 1B-edge power-law stream, sliding window, exp-index walks"
+                if scale == 1.0 else f"C5 shape at scale {scale}",
+                "nodes": self.nodes, "batch_edges": self.batch_edges, "window_duration": self.window,
+                "window_edges": self.window * 4, "walks_per_batch_per_gpu": self.walks,
+                "walk_length": self.walk_length, "bias": "ExponentialIndex", "start": "sampled edges",
+                "direction": "DirectedForward", "prefill_batches": self.prefill,
+                "l2": "inputs larger than L2 (window ~16 GB at scale 1)"}
+
+
+# --------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+
+    def start(self):
+        # nvidia-smi's start-up holds driver locks that stall CUDA API calls:
+        # let it initialise (first sample written) before the timed region.
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.first = self.proc.stdout.readline()
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        out = (getattr(self, "first", "") or "") + out
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- ours
+
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2605_16182_b200 as tw
+
+    torch.cuda.set_device(local_rank)
+    wl = Workload(args.scale)
+    ctx = tw.Context(local_rank)
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    variant = {"fullwalk": tw.Variant.FullWalk, "coop": tw.Variant.Coop, "coopdirect": tw.Variant.CoopDirect}[
+        args.variant]
+    B = wl.batch_edges
+
+    def walk_cfg():
+        return tw.WalkConfig(walk_length=wl.walk_length, start_mode=tw.StartMode.Sampled,
+                             total_walks=wl.walks * world, bias=tw.BiasKind.ExponentialIndex,
+                             start_bias=tw.BiasKind.UniformIndex, seed=wl.seed,
+                             walk_begin=rank * wl.walks, walk_end=(rank + 1) * wl.walks)
+
+    lib = tw._abi.load()
+
+    def synth(buf, b):
+        # batch b of the stream, generated on this device (rank 0 only in multi-GPU)
+        rc = lib.twg_synth_stream_device(ctx.handle, wl.nodes, b * B, B, wl.seed, buf[0].data_ptr(),
+                                         buf[1].data_ptr(), buf[2].data_ptr())
+        assert rc == 0, lib.twg_last_error()
+
+    def bcast(buf):
+        if world > 1:
+            with torch.cuda.stream(stream):
+                for x in buf:
+                    dist.broadcast(x, src=0)
+
+    def new_buf():
+        return [torch.empty(B, dtype=torch.int64, device=f"cuda:{local_rank}") for _ in range(3)]
+
+    def step(window, buf):
+        window.ingest_batch_device(buf[0].data_ptr(), buf[1].data_ptr(), buf[2].data_ptr(), B, stats=False)
+        snap = window.snapshot()
+        st = tw.WalkStats()
+        ws = tw.generate_walks(snap, walk_cfg(), variant=variant, stats=st)
+        return st, ws
+
+    # ---- device-resident pass ------------------------------------------------------
+    window = tw.WindowManager(wl.window, tw.DirectionMode.DirectedForward, weights=False, adjacency=False, ctx=ctx)
+    buf = new_buf()
+    b = 0
+    for _ in range(wl.prefill):
+        if rank == 0:
+            synth(buf, b)
+        bcast(buf)
+        window.ingest_batch_device(buf[0].data_ptr(), buf[1].data_ptr(), buf[2].data_ptr(), B, stats=False)
+        b += 1
+    for _ in range(args.warmup):
+        if rank == 0:
+            synth(buf, b)
+        bcast(buf)
+        st, ws = step(window, buf)
+        del ws
+        b += 1
+    # pre-generate the K timed batches into HBM (inputs resident before timing)
+    bufs = []
+    for k in range(args.steps):
+        x = new_buf()
+        if rank == 0:
+            synth(x, b + k)
+        bufs.append(x)
+    ctx.sync()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    launches0 = ctx.launches
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3 * args.steps + 2)]
+    hops = 0
+    alg_bytes = 0
+    ev[0].record(stream)
+    for k in range(args.steps):
+        bcast(bufs[k])
+        ev[1 + 3 * k].record(stream)
+        window.ingest_batch_device(bufs[k][0].data_ptr(), bufs[k][1].data_ptr(), bufs[k][2].data_ptr(), B,
+                                   stats=False)
+        ev[2 + 3 * k].record(stream)
+        snap = window.snapshot()
+        st = tw.WalkStats()
+        ws = tw.generate_walks(snap, walk_cfg(), variant=variant, stats=st)
+        ev[3 + 3 * k].record(stream)
+        hops += st.hops
+        alg_bytes += st.alg_bytes if hasattr(st, "alg_bytes") else 0
+        del ws, snap
+    ev[-1].record(stream)
+    ctx.sync()
+    torch.cuda.synchronize()
+    launches = ctx.launches - launches0
+    clk = clocks.stop()
+    total_ms = ev[0].elapsed_time(ev[-1])
+    ingest_ms = sum(ev[1 + 3 * k].elapsed_time(ev[2 + 3 * k]) for k in range(args.steps))
+    walk_ms = sum(ev[2 + 3 * k].elapsed_time(ev[3 + 3 * k]) for k in range(args.steps))
+    del bufs
+
+    def allmax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local_rank}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def allsum(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local_rank}")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    total_ms = allmax(total_ms)
+    ingest_ms = allmax(ingest_ms)
+    walk_ms = allmax(walk_ms)
+    hops_all = allsum(hops)
+    edges_all = B * args.steps  # each batch ingested once (replicated on every GPU)
+    result = dict(total_ms=total_ms, ingest_ms=ingest_ms, walk_ms=walk_ms, hops=hops_all, edges=edges_all,
+                  launches=launches, clocks=clk, alg_bytes=allsum(alg_bytes))
+
+    # ---- e2e pass through the C ABI with host buffers -----------------------------------
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, tw, ctx, wl, rank, world, local_rank, variant, walk_cfg)
+    return result, e2e, wl
+
+
+def run_e2e(args, tw, ctx, wl, rank, world, local_rank, variant, walk_cfg):
+    import ctypes as C
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    lib = tw._abi.load()
+    B = wl.batch_edges
+    window = tw.WindowManager(wl.window, tw.DirectionMode.DirectedForward, weights=False, adjacency=False, ctx=ctx)
+    host = torch.empty((B, 3), dtype=torch.int64, pin_memory=True)
+    dev = [torch.empty(B, dtype=torch.int64, device=f"cuda:{local_rank}") for _ in range(3)]
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    b = 0
+    for _ in range(wl.prefill):  # untimed prefill via the device generator
+        if rank == 0:
+            lib.twg_synth_stream_device(ctx.handle, wl.nodes, b * B, B, wl.seed, dev[0].data_ptr(),
+                                        dev[1].data_ptr(), dev[2].data_ptr())
+        if world > 1:
+            with torch.cuda.stream(stream):
+                for x in dev:
+                    dist.broadcast(x, src=0)
+        window.ingest_batch_device(dev[0].data_ptr(), dev[1].data_ptr(), dev[2].data_ptr(), B, stats=False)
+        b += 1
+    cap = None
+    out_off = out_n = out_t = None
+    step_s, hops, h2d, d2h = [], 0, 0, 0
+    for k in range(args.warmup + args.steps):
+        if rank == 0:  # host-side generation of this batch: outside the timed step
+            rc = lib.twg_synth_stream_host(wl.nodes, b * B, B, wl.seed, C.c_void_p(host.data_ptr()))
+            assert rc == 0
+        b += 1
+        ctx.sync()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        if world == 1:
+            st = tw._abi.twg_batch_stats()
+            rc = lib.twg_window_ingest(window.handle, C.c_void_p(host.data_ptr()), B, C.byref(st))
+            assert rc == 0, lib.twg_last_error()
+            in_bytes = B * 24
+        else:
+            # rank 0: pinned H2D; then NCCL broadcast over NVLink into every replica
+            if rank == 0:
+                with torch.cuda.stream(stream):
+                    d = host.to(f"cuda:{local_rank}", non_blocking=True)
+                    for i, x in enumerate(dev):
+                        x.copy_(d[:, i])
+            with torch.cuda.stream(stream):
+                for x in dev:
+                    dist.broadcast(x, src=0)
+            window.ingest_batch_device(dev[0].data_ptr(), dev[1].data_ptr(), dev[2].data_ptr(), B, stats=False)
+            in_bytes = B * 24 if rank == 0 else 0
+        snap = window.snapshot()
+        wst = tw.WalkStats()
+        ws = tw.generate_walks(snap, walk_cfg(), variant=variant, stats=wst)
+        total = int(ws.total_hops + 2 * ws.walk_count)  # upper bound of recorded entries
+        if cap is None or total > cap:
+            cap = int(total * 1.25) + 1
+            out_off = torch.empty(ws.walk_count + 1, dtype=torch.int64, pin_memory=True)
+            out_n = torch.empty(cap, dtype=torch.int64, pin_memory=True)
+            out_t = torch.empty(cap, dtype=torch.int64, pin_memory=True)
+        rc = lib.twg_walkset_download_compact(ws.handle, C.c_void_p(out_off.data_ptr()), C.c_void_p(out_n.data_ptr()),
+                                              C.c_void_p(out_t.data_ptr()))
+        assert rc == 0, lib.twg_last_error()
+        entries = int(out_off[ws.walk_count].item())
+        if world > 1:
+            dist.barrier()
+        dt = time.perf_counter() - t0
+        if k >= args.warmup:
+            step_s.append(dt)
+            hops += wst.hops
+            h2d += in_bytes
+            d2h += 8 * (ws.walk_count + 1) + 16 * entries
+        del ws, snap
+
+    def allmax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local_rank}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def allsum(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local_rank}")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    total_s = allmax(sum(step_s))
+    return dict(total_s=total_s, hops=allsum(hops), edges=B * args.steps,
+                h2d=allsum(h2d) / args.steps, d2h=allsum(d2h) / args.steps)
+
+
+# --------------------------------------------------------------------------- reference / CPU
+
+def cpu_sample_workload():
+    """Bounded sample of the C5 workload for the CPU reference: same stream
+    law and window/batch ratios at 1/100 scale (N=100K nodes, 500K-edge
+    batches, Δ=span/3 -> ~3.3M-edge window, 100K walks per batch, L=80)."""
+    return Workload(0.01)
+
+
+def run_cpu(steps: int, warmup: int, which: str = "reference"):
+    """Time the reference's own CPU implementation (oracle/_ref: the
+    unmodified proj/core, -O3 -fopenmp, all host threads) on the sample.
+    Per step: WindowManager::ingest_batch + generate_walks (Coop, the
+    reference default). Times from the reference's own timers
+    (BatchStats::rebuild_duration, WalkStats::wall_seconds)."""
+    import ctypes as C
+
+    import numpy as np
+
+    from oracle.py import BatchStatsC, Cfg, COracle, RefOracle, ThresholdsC, WalkStatsC, _p, ref_available
+
+    wl = cpu_sample_workload()
+    co = COracle()
+    use_ref = which == "reference" and ref_available()
+    R = RefOracle() if use_ref else None
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    B = wl.batch_edges
+    cfg = Cfg(walk_length=wl.walk_length, start_mode=1, total_walks=wl.walks, bias=2, start_bias=0, seed=wl.seed)
+    ingest_s = walk_s = 0.0
+    hops = edges = 0
+    if use_ref:
+        L = R.L
+        st = C.c_int()
+        w = L.twref_window_create(wl.window, 0, C.byref(st))
+        for b in range(wl.prefill + warmup + steps):
+            e = co.gen_stream(wl.nodes, b * B, B, wl.seed)
+            bs = BatchStatsC()
+            rc = L.twref_window_ingest(w, _p(e), B, C.byref(bs))
+            assert rc == 0
+            if b < wl.prefill:
+                continue
+            snap = L.twref_window_snapshot(w)
+            ws = WalkStatsC()
+            status = C.c_int()
+            th = ThresholdsC(4, 256, 8192, 512, 4096)
+            wh = L.twref_generate(snap, C.byref(cfg.c()), C.byref(th), 0, C.byref(ws), C.byref(status))
+            L.twref_walks_free(wh)
+            L.twref_store_free(snap)
+            if b >= wl.prefill + warmup:
+                ingest_s += bs.rebuild_duration
+                walk_s += ws.wall_seconds
+                hops += ws.hops
+                edges += B
+        L.twref_window_free(w)
+        kind = "reference"
+    else:  # C restatement (scalar port)
+        st = C.c_int()
+        Lc = co.L
+        w = Lc.two_window_create(wl.window, 0, C.byref(st))
+        for b in range(wl.prefill + warmup + steps):
+            e = co.gen_stream(wl.nodes, b * B, B, wl.seed)
+            bs = BatchStatsC()
+            Lc.two_window_ingest(w, _p(e), B, C.byref(bs))
+            if b < wl.prefill:
+                continue
+            from oracle.py import two_window, two_walkset
+            store = C.cast(w, C.POINTER(two_window)).contents.store
+            out = two_walkset()
+            ws = WalkStatsC()
+            Lc.two_generate(store, C.byref(cfg.c()), None, 2, C.byref(out), C.byref(ws))
+            Lc.two_walkset_free(C.byref(out))
+            if b >= wl.prefill + warmup:
+                ingest_s += bs.rebuild_duration
+                walk_s += ws.wall_seconds
+                hops += ws.hops
+                edges += B
+        Lc.two_window_free(w)
+        kind = "port"
+        cores = 1
+    total = ingest_s + walk_s
+    cpu_model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                cpu_model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return dict(value=hops / total if total else 0.0, edges_per_s=edges / total if total else 0.0,
+                ingest_edges_per_s=edges / ingest_s if ingest_s else 0.0,
+                walk_steps_per_s=hops / walk_s if walk_s else 0.0, total_s=total, hops=hops, edges=edges,
+                kind=kind, cores=cores, cpu_model=cpu_model,
+                sample=f"C5 law at 1/100 scale: N={wl.nodes} nodes, {B}-edge batches, window {wl.window} "
+                       f"time units (~{4 * wl.window} edges), {wl.walks} exp-index walks/batch, L=80; "
+                       f"{steps} timed batches after {wl.prefill} prefill + {warmup} warm-up")
+
+
+# --------------------------------------------------------------------------- main
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        r = run_cpu(args.steps, args.warmup, "reference")
+        ms = 1000.0 * r["total_s"] / max(args.steps, 1)
+        line = {"metric": METRIC, "value": r["value"], "unit": "walk steps/s", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+                "impl": "reference", "edges_per_s": r["edges_per_s"],
+                "config": {**cpu_sample_workload().describe(0.01), "parallelism": "CPU OpenMP"},
+                "cpu_baseline": {"value": r["value"], "unit": "walk steps/s", "cores": r["cores"], "kind": r["kind"],
+                                 "sample": r["sample"], "cpu_model": r["cpu_model"]},
+                "e2e": {"value": r["value"], "unit": "walk steps/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0},
+                "phases": {"ingest_edges_per_s": r["ingest_edges_per_s"],
+                           "walk_steps_per_s": r["walk_steps_per_s"]}}
+        print(json.dumps(line), flush=True)
+        return
+
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+
+    res, e2e, wl = run_ours(args, rank, world, local_rank)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = run_cpu(2, 0, "reference")
+        except Exception as ex:  # the baseline is reported, never the product path
+            cpu = {"value": None, "kind": "unavailable", "cores": 0, "sample": str(ex)}
+
+    if rank == 0:
+        peak, peak_src = peaks()
+        total_s = res["total_ms"] / 1000.0
+        value = res["hops"] / total_s
+        walk_s = res["walk_ms"] / 1000.0
+        alg = res["alg_bytes"]
+        achieved = alg / walk_s / 1e9 if walk_s and alg else None
+        line = {
+            "metric": METRIC, "value": value, "unit": "walk steps/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": res["total_ms"] / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "edges_per_s": res["edges"] / total_s,
+            "config": {**wl.describe(args.scale), "variant": args.variant, "parallelism": f"replicas{world}+walk-shards",
+                       "global_walks_per_batch": wl.walks * world},
+            "phases": {"ingest_ms_per_step": res["ingest_ms"] / args.steps,
+                       "walk_ms_per_step": res["walk_ms"] / args.steps,
+                       "ingest_edges_per_s": res["edges"] / (res["ingest_ms"] / 1000.0),
+                       "walk_steps_per_s": res["hops"] / walk_s, "hops_per_step": res["hops"] / args.steps},
+            "roofline": {"bound": "hbm", "kernel": "k_fullwalk (walk phase)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": None,
+                         "peak_source": peak_src},
+            "gpu_launches": res["launches"],
+            "clocks": res["clocks"],
+        }
+        if e2e:
+            line["e2e"] = {"value": e2e["hops"] / e2e["total_s"], "unit": "walk steps/s",
+                           "edges_per_s": e2e["edges"] / e2e["total_s"],
+                           "h2d_bytes_per_step": int(e2e["h2d"]), "d2h_bytes_per_step": int(e2e["d2h"])}
+        if cpu:
+            line["cpu_baseline"] = {"value": cpu.get("value"), "unit": "walk steps/s", "cores": cpu.get("cores"),
+                                    "kind": cpu.get("kind"), "sample": cpu.get("sample"),
+                                    "edges_per_s": cpu.get("edges_per_s"), "cpu_model": cpu.get("cpu_model")}
+        print(json.dumps(line), flush=True)
+
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -208,6 +208,7 @@ typedef struct twg_walk_stats {
   uint64_t solo, warp_cached, warp_direct, block_cached, block_direct, multi_block;
   double wall_seconds;
   uint64_t ambiguous_draws;
+  uint64_t alg_bytes;  /* SURVEY §8(d) algorithmic bytes summed over the hops (roofline numerator) */
 } twg_walk_stats;
 
 /* generate_walks. The WalkSet stays on the device until downloaded.

@@ -61,7 +61,7 @@ class twg_walk_stats(C.Structure):
         ("walks", C.c_uint64), ("hops", C.c_uint64), ("steps", C.c_uint64),
         ("solo", C.c_uint64), ("warp_cached", C.c_uint64), ("warp_direct", C.c_uint64),
         ("block_cached", C.c_uint64), ("block_direct", C.c_uint64), ("multi_block", C.c_uint64),
-        ("wall_seconds", C.c_double), ("ambiguous_draws", C.c_uint64),
+        ("wall_seconds", C.c_double), ("ambiguous_draws", C.c_uint64), ("alg_bytes", C.c_uint64),
     ]
 
 

@@ -116,6 +116,17 @@ __device__ bool adjacent_after(const StoreView& s, u32 a, u32 b, i64 t, int dir)
   return false;
 }
 
+// Per-thread instrumentation: ambiguous exp-index draws, and the algorithmic
+// bytes of SURVEY §8(d) (B_hop = 80 + 8*ceil(log2(G_v+1)) for the index
+// pickers, +16 + 8*ceil(log2 n) for the weighted picker; 24 B per sampled
+// start) summed exactly per hop for the roofline.
+struct Ctr {
+  u32 amb;
+  u64 bytes;
+};
+
+__device__ __forceinline__ u32 ceil_log2p1(u32 g) { return g ? 32u - __clz(g) : 0u; }  // ceil(log2(g+1))
+
 struct WalkReg {
   u32 cur;
   u32 prev;
@@ -128,10 +139,13 @@ struct WalkReg {
 // global arrays (glo/ghi = node group range) or a shared-memory copy
 // (glo = 0). Returns false when the causal slice is empty (walk dies).
 __device__ __forceinline__ bool hop(const WalkParams& P, u64 wl, WalkReg& r, const i64* mt, const u32* ms, u32 glo,
-                                    u32 ghi, u32 lo, u32 hi, u32* amb) {
+                                    u32 ghi, u32 lo, u32 hi, Ctr* cn) {
+  u32* amb = &cn->amb;
   u32 c, e;
   causal_slice(mt, ms, glo, ghi, lo, hi, r.t, P.dir, c, e);
   if (c == e) return false;
+  cn->bytes += 80u + 8u * ceil_log2p1(ghi - glo) +
+               (P.bias == TWG_EXPWEIGHT ? 16u + 8u * ceil_log2p1(e - c - 1) : 0u);
   const u64 w = P.walk_begin + wl;
   const u64 hop_index = r.len;
   u64 idx;
@@ -193,7 +207,7 @@ struct InitParams {
 };
 
 // seed_walk + init_walks (walk_engine.cpp:147-155, :247-279)
-__device__ __forceinline__ void init_walk(const WalkParams& P, const InitParams& I, u64 wl, WalkReg& r, u32* amb) {
+__device__ __forceinline__ void init_walk(const WalkParams& P, const InitParams& I, u64 wl, WalkReg& r, Ctr* cn) {
   const u64 w = P.walk_begin + wl;
   const u64 base = wl * P.stride;
   r.prev = 0;
@@ -208,7 +222,8 @@ __device__ __forceinline__ void init_walk(const WalkParams& P, const InitParams&
   } else {
     const double u1 = P.rng.uniform(w, 0, 0);
     const double u2 = P.rng.uniform(w, 0, 1);
-    const u64 eidx = sample_start_edge_dev(P.s, I.start_bias, u1, u2, P.expm1_tab, amb);
+    const u64 eidx = sample_start_edge_dev(P.s, I.start_bias, u1, u2, P.expm1_tab, &cn->amb);
+    cn->bytes += 24u + (I.start_bias == TWG_EXPWEIGHT ? 8u * (64u - __clzll(P.s.Z)) : 0u);
     const u32 sv = P.s.e_src[eidx], dv = P.s.e_dst[eidx];
     const i64 t = P.s.e_t[eidx];
     const u32 from = P.dir == 0 ? sv : dv;
@@ -227,24 +242,34 @@ __device__ __forceinline__ void init_walk(const WalkParams& P, const InitParams&
   }
 }
 
-// stats[0] walks, [1] hops, [2] max hops (fullwalk steps), [3] ambiguous
-__device__ __forceinline__ void add_stats(u64* stats, u32 len, u32 init_len, u32 amb, bool active) {
+// stats[0] walks, [1] hops, [2] max hops (fullwalk steps), [3] ambiguous, [4] algorithmic bytes
+__device__ __forceinline__ void add_counters(u64* stats, const Ctr& cn) {
+  u64 a = cn.amb, b = cn.bytes;
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (a) atomicAdd(reinterpret_cast<unsigned long long*>(&stats[3]), a);
+    if (b) atomicAdd(reinterpret_cast<unsigned long long*>(&stats[4]), b);
+  }
+}
+
+__device__ __forceinline__ void add_stats(u64* stats, u32 len, u32 init_len, const Ctr& cn, bool active) {
   u64 walks = active && len >= 2 ? 1 : 0;
   u64 hops = active && len >= 2 ? len - 1 : 0;
   u64 steps = active ? len - init_len : 0;
-  u64 a = amb;
   for (int o = 16; o > 0; o >>= 1) {
     walks += __shfl_xor_sync(0xffffffffu, walks, o);
     hops += __shfl_xor_sync(0xffffffffu, hops, o);
     steps = max(steps, __shfl_xor_sync(0xffffffffu, steps, o));
-    a += __shfl_xor_sync(0xffffffffu, a, o);
   }
   if ((threadIdx.x & 31) == 0) {
     if (walks) atomicAdd(reinterpret_cast<unsigned long long*>(&stats[0]), walks);
     if (hops) atomicAdd(reinterpret_cast<unsigned long long*>(&stats[1]), hops);
     if (steps) atomicMax(reinterpret_cast<unsigned long long*>(&stats[2]), steps);
-    if (a) atomicAdd(reinterpret_cast<unsigned long long*>(&stats[3]), a);
   }
+  add_counters(stats, cn);
 }
 
 // ---- FullWalk -----------------------------------------------------------------
@@ -252,19 +277,19 @@ __device__ __forceinline__ void add_stats(u64* stats, u32 len, u32 init_len, u32
 __global__ void __launch_bounds__(kBlock) k_fullwalk(WalkParams P, InitParams I, u64 count, u32* lengths, u64* stats) {
   const u64 wl = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x;
   const bool active = wl < count;
-  u32 amb = 0;
+  Ctr cn{0, 0};
   u32 init_len = 0;
   WalkReg r{};
   if (active) {
-    init_walk(P, I, wl, r, &amb);
+    init_walk(P, I, wl, r, &cn);
     init_len = r.len;
     while (r.len < P.stride) {
       const uint2 a = P.s.nmeta[r.cur], b = P.s.nmeta[r.cur + 1];
-      if (!hop(P, wl, r, P.s.mk_time, P.s.mk_start, a.y, b.y, a.x, b.x, &amb)) break;
+      if (!hop(P, wl, r, P.s.mk_time, P.s.mk_start, a.y, b.y, a.x, b.x, &cn)) break;
     }
     lengths[wl] = r.len;
   }
-  add_stats(stats, r.len, init_len, amb, active);
+  add_stats(stats, r.len, init_len, cn, active);
 }
 
 // ---- Coop scheduler -------------------------------------------------------------
@@ -280,18 +305,17 @@ struct StateArrays {
 __global__ void __launch_bounds__(kBlock) k_init_states(WalkParams P, InitParams I, u64 count, StateArrays S,
                                                         u64* stats) {
   const u64 wl = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x;
-  u32 amb = 0;
+  Ctr cn{0, 0};
   if (wl < count) {
     WalkReg r{};
-    init_walk(P, I, wl, r, &amb);
+    init_walk(P, I, wl, r, &cn);
     S.cur[wl] = r.cur;
     S.prev[wl] = r.prev;
     S.t[wl] = r.t;
     S.len[wl] = r.len;
     S.flags[wl] = static_cast<u8>((r.len < P.stride ? 1 : 0) | (r.has_prev ? 2 : 0));
   }
-  for (int o = 16; o > 0; o >>= 1) amb += __shfl_xor_sync(0xffffffffu, amb, o);
-  if ((threadIdx.x & 31) == 0 && amb) atomicAdd(reinterpret_cast<unsigned long long*>(&stats[3]), (u64)amb);
+  add_counters(stats, cn);
 }
 
 struct AliveFn {
@@ -398,7 +422,7 @@ __device__ __forceinline__ void store_state(const StateArrays& S, u32 w, const W
 }
 
 __device__ __forceinline__ void hop_member(const WalkParams& P, const StateArrays& S, u32 w, const i64* mt,
-                                           const u32* ms, u32 glo, u32 ghi, u32 lo, u32 hi, u32* amb) {
+                                           const u32* ms, u32 glo, u32 ghi, u32 lo, u32 hi, Ctr* amb) {
   WalkReg r;
   load_state(S, w, r);
   const bool alive = hop(P, w, r, mt, ms, glo, ghi, lo, hi, amb);
@@ -409,15 +433,14 @@ __device__ __forceinline__ void hop_member(const WalkParams& P, const StateArray
 __global__ void __launch_bounds__(kBlock) k_tier_solo(WalkParams P, StateArrays S, const u32* ids, const Task* tasks,
                                                       const u32* count, u64* stats) {
   const u32 n = *count;
-  u32 amb = 0;
+  Ctr amb{0, 0};
   for (u32 k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const Task task = tasks[k];
     const uint2 a = P.s.nmeta[task.node], b = P.s.nmeta[task.node + 1];
     for (u32 i = task.begin; i < task.end; ++i)
       hop_member(P, S, ids[i], P.s.mk_time, P.s.mk_start, a.y, b.y, a.x, b.x, &amb);
   }
-  for (int o = 16; o > 0; o >>= 1) amb += __shfl_xor_sync(0xffffffffu, amb, o);
-  if ((threadIdx.x & 31) == 0 && amb) atomicAdd(reinterpret_cast<unsigned long long*>(&stats[3]), (u64)amb);
+  add_counters(stats, amb);
 }
 
 // warp tiers: one warp per task; cached => the node's marks staged in this
@@ -431,7 +454,7 @@ __global__ void __launch_bounds__(kBlock) k_tier_warp(WalkParams P, StateArrays 
   i64* smt = reinterpret_cast<i64*>(smem_raw) + static_cast<u64>(warp) * cap;
   u32* sms = reinterpret_cast<u32*>(reinterpret_cast<i64*>(smem_raw) + static_cast<u64>(kBlock / 32) * cap) +
              static_cast<u64>(warp) * cap;
-  u32 amb = 0;
+  Ctr amb{0, 0};
   for (u32 k = blockIdx.x * (kBlock / 32) + warp; k < n; k += gridDim.x * (kBlock / 32)) {
     const Task task = tasks[k];
     const uint2 a = P.s.nmeta[task.node], b = P.s.nmeta[task.node + 1];
@@ -450,8 +473,7 @@ __global__ void __launch_bounds__(kBlock) k_tier_warp(WalkParams P, StateArrays 
         hop_member(P, S, ids[i], P.s.mk_time, P.s.mk_start, a.y, b.y, a.x, b.x, &amb);
     }
   }
-  for (int o = 16; o > 0; o >>= 1) amb += __shfl_xor_sync(0xffffffffu, amb, o);
-  if (lane == 0 && amb) atomicAdd(reinterpret_cast<unsigned long long*>(&stats[3]), (u64)amb);
+  add_counters(stats, amb);
 }
 
 // block tiers: one CTA per (sub-)task; cached => marks staged in the CTA's
@@ -464,7 +486,7 @@ __global__ void __launch_bounds__(kBlock) k_tier_block(WalkParams P, StateArrays
   i64* smt = reinterpret_cast<i64*>(smem_raw);
   u32* sms = reinterpret_cast<u32*>(smt + cap);
   const u32 n = *count;
-  u32 amb = 0;
+  Ctr amb{0, 0};
   for (u32 k = blockIdx.x; k < n; k += gridDim.x) {
     const Task task = tasks[k];
     const uint2 a = P.s.nmeta[task.node], b = P.s.nmeta[task.node + 1];
@@ -483,8 +505,7 @@ __global__ void __launch_bounds__(kBlock) k_tier_block(WalkParams P, StateArrays
         hop_member(P, S, ids[i], P.s.mk_time, P.s.mk_start, a.y, b.y, a.x, b.x, &amb);
     }
   }
-  for (int o = 16; o > 0; o >>= 1) amb += __shfl_xor_sync(0xffffffffu, amb, o);
-  if ((threadIdx.x & 31) == 0 && amb) atomicAdd(reinterpret_cast<unsigned long long*>(&stats[3]), (u64)amb);
+  add_counters(stats, amb);
 }
 
 __global__ void k_finalize(const StateArrays S, u64 count, u32* lengths, u64* stats) {
@@ -492,7 +513,7 @@ __global__ void k_finalize(const StateArrays S, u64 count, u32* lengths, u64* st
   const bool active = wl < count;
   const u32 len = active ? S.len[wl] : 0;
   if (active) lengths[wl] = len;
-  add_stats(stats, len, len, 0, active);
+  add_stats(stats, len, len, Ctr{0, 0}, active);
 }
 
 __global__ void k_start_flags(const uint2* nmeta, u64 V, u32* flags) {
@@ -777,14 +798,15 @@ WalkSetDev* generate_walks(Ctx& ctx, Store& s, const twg_walk_config& cfg, const
     k_finalize<<<grid_for(count, kBlock, 0xffffffffu), kBlock, 0, st>>>(S, count, out->lengths.p, stats.p);
     TWG_LAUNCHED(ctx);
   }
-  u64 hs[4];
-  read_scalars(ctx, stats.p, hs, 4);
+  u64 hs[5];
+  read_scalars(ctx, stats.p, hs, 5);
   out->hops = hs[1];
   if (stats_out) {
     twg_walk_stats w{};
     w.walks = hs[0];
     w.hops = hs[1];
     w.ambiguous_draws = hs[3];
+    w.alg_bytes = hs[4];
     if (variant == TWG_FULLWALK) {
       w.steps = hs[2];
     } else {

@@ -542,6 +542,7 @@ class WalkStats:
     tiers: TierCounts = field(default_factory=TierCounts)
     wall_seconds: float = 0.0
     ambiguous_draws: int = 0
+    alg_bytes: int = 0
 
     def fill(self, s: _abi.twg_walk_stats) -> None:
         self.walks, self.hops, self.steps = s.walks, s.hops, s.steps
@@ -549,6 +550,7 @@ class WalkStats:
                                 s.multi_block)
         self.wall_seconds = s.wall_seconds
         self.ambiguous_draws = s.ambiguous_draws
+        self.alg_bytes = s.alg_bytes
 
 
 class WalkSet:
