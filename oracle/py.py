@@ -313,13 +313,15 @@ class COracle:
             self.L.two_store_free(h)
 
     # window ------------------------------------------------------------------------
-    def window_run(self, batches, duration, mode):
+    def window_run(self, batches, duration, mode, every=False):
+        """Ingest batches; returns ([(stats, bounds)], final dump) or, with
+        every=True, ([(stats, bounds)], [dump after each batch])."""
         st = I()
         w = self.L.two_window_create(duration, mode, C.byref(st))
         if not w:
             raise OracleError(st.value)
         try:
-            stats = []
+            stats, dumps = [], []
             for b in batches:
                 e = edges_array(b)
                 bs = BatchStatsC()
@@ -329,6 +331,10 @@ class COracle:
                 lo, hi = I64(), I64()
                 rcb = self.L.two_window_bounds(w, C.byref(lo), C.byref(hi))
                 stats.append((stats_dict(bs), (lo.value, hi.value) if rcb == 0 else None))
+                if every:
+                    dumps.append(self.dump_handle(C.cast(w, C.POINTER(two_window)).contents.store))
+            if every:
+                return stats, dumps
             store = C.cast(w, C.POINTER(two_window)).contents.store
             return stats, self.dump_handle(store)
         finally:

@@ -1,0 +1,124 @@
+// Per-stream caching device allocator (see common.cuh). Size classes: powers
+// of two up to 1 MiB, then 8 classes per octave. A freed block goes back to
+// its class list and is handed to the next request of that class on the same
+// stream — stream order makes the reuse safe without events. On an
+// allocation failure every cached block of every class is released and the
+// request retried once.
+#include <map>
+#include <mutex>
+#include <unordered_map>
+#include <vector>
+
+#include "common.cuh"
+
+namespace twg {
+
+namespace {
+
+struct Arena {
+  std::map<size_t, std::vector<void*>> free_lists;
+  size_t in_use = 0;
+  size_t reserved = 0;
+};
+
+std::mutex g_mu;
+std::unordered_map<cudaStream_t, Arena*>& arenas() {
+  static auto* m = new std::unordered_map<cudaStream_t, Arena*>;
+  return *m;
+}
+
+size_t size_class(size_t bytes) {
+  if (bytes <= 256) return 256;
+  if (bytes <= (1u << 20)) {
+    size_t c = 256;
+    while (c < bytes) c <<= 1;
+    return c;
+  }
+  int top = 63 - __builtin_clzll(bytes);
+  const size_t step = size_t(1) << (top - 3);
+  return (bytes + step - 1) / step * step;
+}
+
+Arena* find(cudaStream_t s) {
+  auto it = arenas().find(s);
+  return it == arenas().end() ? nullptr : it->second;
+}
+
+}  // namespace
+
+void arena_register(cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!find(s)) arenas()[s] = new Arena;
+}
+
+void arena_unregister(cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  Arena* a = find(s);
+  if (!a) return;
+  cudaStreamSynchronize(s);
+  for (auto& kv : a->free_lists)
+    for (void* p : kv.second) cudaFree(p);
+  arenas().erase(s);
+  delete a;
+}
+
+void* arena_alloc(cudaStream_t s, size_t bytes) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  Arena* a = find(s);
+  const size_t c = size_class(bytes);
+  if (a) {
+    auto it = a->free_lists.find(c);
+    if (it != a->free_lists.end() && !it->second.empty()) {
+      void* p = it->second.back();
+      it->second.pop_back();
+      a->in_use += c;
+      return p;
+    }
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, c);
+  if (e == cudaErrorMemoryAllocation && a) {
+    cudaGetLastError();
+    cudaStreamSynchronize(s);
+    for (auto& kv : a->free_lists) {
+      for (void* q : kv.second) {
+        cudaFree(q);
+        a->reserved -= kv.first;
+      }
+      kv.second.clear();
+    }
+    e = cudaMalloc(&p, c);
+  }
+  cuda_check(e, "cudaMalloc (arena)", __FILE__, __LINE__);
+  if (a) {
+    a->in_use += c;
+    a->reserved += c;
+  }
+  return p;
+}
+
+void arena_free(cudaStream_t s, void* p, size_t bytes) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  Arena* a = find(s);
+  if (!a) {  // ctx already gone: release for real
+    cudaFree(p);
+    return;
+  }
+  const size_t c = size_class(bytes);
+  a->free_lists[c].push_back(p);
+  a->in_use -= c;
+}
+
+size_t arena_bytes_in_use(cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  Arena* a = find(s);
+  return a ? a->in_use : 0;
+}
+
+size_t arena_bytes_reserved(cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  Arena* a = find(s);
+  return a ? a->reserved : 0;
+}
+
+}  // namespace twg

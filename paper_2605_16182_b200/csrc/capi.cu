@@ -162,9 +162,7 @@ int twg_ctx_create(int device, twg_ctx** out) {
       TWG_CUDA(cudaSetDevice(device));
       TWG_CUDA(cudaDeviceGetAttribute(&c.sm_count, cudaDevAttrMultiProcessorCount, device));
       TWG_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
-      TWG_CUDA(cudaDeviceGetDefaultMemPool(&c.pool, device));
-      u64 threshold = ~0ull;
-      TWG_CUDA(cudaMemPoolSetAttribute(c.pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+      arena_register(c.stream);
       // glibc tables: same libm as the reference
       std::vector<double> e(kExpTableSize), x(701);
       for (int k = 0; k < kExpTableSize; ++k) e[k] = std::exp(static_cast<double>(-k));
@@ -192,6 +190,7 @@ int twg_ctx_destroy(twg_ctx* ctx) {
     cudaFree(c.d_expm1);
     cudaFree(c.d_scalars);
     cudaFreeHost(c.h_pinned);
+    arena_unregister(c.stream);
     cudaStreamDestroy(c.stream);
     delete ctx;
   });

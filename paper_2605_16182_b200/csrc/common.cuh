@@ -61,7 +61,19 @@ struct Ctx {
   u64* d_scalars = nullptr;  // 64 u64 scratch scalars on the device
 };
 
-// Stream-ordered device buffer (cudaMallocAsync on the ctx stream).
+// Per-stream caching allocator (arena.cu). Every ctx owns one, keyed by its
+// stream. Blocks are rounded to size classes (<= 12.5% slack) and recycled
+// in stream order, so the steady-state ingest/walk loop performs no device
+// allocation at all (cudaMallocAsync pool growth cost up to 200 ms per batch
+// in round-1 measurements, profiles/r1_baseline_fullrebuild.md).
+void arena_register(cudaStream_t s);
+void arena_unregister(cudaStream_t s);
+void* arena_alloc(cudaStream_t s, size_t bytes);
+void arena_free(cudaStream_t s, void* p, size_t bytes);
+size_t arena_bytes_in_use(cudaStream_t s);
+size_t arena_bytes_reserved(cudaStream_t s);
+
+// Device buffer allocated from the ctx arena of `stream`.
 template <class T>
 struct DevBuf {
   T* p = nullptr;
@@ -87,14 +99,14 @@ struct DevBuf {
     release();
     s = stream;
     n = count;
-    if (count) TWG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), stream));
+    if (count) p = static_cast<T*>(arena_alloc(stream, count * sizeof(T)));
   }
   // grow-only reallocation (contents not preserved)
   void reserve(size_t count, cudaStream_t stream) {
     if (count > n || p == nullptr) alloc(count < 1 ? 1 : count, stream);
   }
   void release() {
-    if (p) cudaFreeAsync(p, s);
+    if (p) arena_free(s, p, n * sizeof(T));
     p = nullptr;
     n = 0;
   }

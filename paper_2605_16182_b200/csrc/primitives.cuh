@@ -231,6 +231,85 @@ __global__ void __launch_bounds__(kSortBlock) k_radix_scatter(const K* __restric
   }
 }
 
+// --------------------------------------------------------------- merge ----
+//
+// Merge-path merge of two sorted sequences A (na) and B (nb), A first on
+// ties (stable). Keys come from functors ka(i) / kb(j) returning a type with
+// operator<; the emitter receives (output index, from_a, source index, key)
+// and writes whatever payload columns the caller needs. One tile of
+// kMergeTile outputs per CTA: a global diagonal search per tile boundary,
+// the tile's keys staged in shared memory, then a per-thread diagonal
+// search and an 8-element sequential merge.
+constexpr int kMergeBlock = 256;
+constexpr int kMergeItems = 8;
+constexpr int kMergeTile = kMergeBlock * kMergeItems;
+
+template <class KA, class KB>
+__global__ void k_merge_partition(KA ka, u64 na, KB kb, u64 nb, u64 ntiles, u64* part) {
+  for (u64 t = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; t <= ntiles;
+       t += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const u64 d = t * kMergeTile < na + nb ? t * kMergeTile : na + nb;
+    u64 lo = d > nb ? d - nb : 0, hi = d < na ? d : na;
+    while (lo < hi) {
+      const u64 mid = (lo + hi) >> 1;
+      if (kb(d - 1 - mid) < ka(mid)) hi = mid;
+      else lo = mid + 1;
+    }
+    part[t] = lo;
+  }
+}
+
+template <class K, class KA, class KB, class Emit>
+__global__ void __launch_bounds__(kMergeBlock) k_merge_tiles(KA ka, u64 na, KB kb, u64 nb, const u64* part,
+                                                             Emit emit) {
+  __shared__ K sk[kMergeTile];
+  const u64 t = blockIdx.x;
+  const u64 d0 = t * kMergeTile;
+  const u64 d1 = d0 + kMergeTile < na + nb ? d0 + kMergeTile : na + nb;
+  const u64 a0 = part[t], a1 = part[t + 1];
+  const u64 b0 = d0 - a0, b1 = d1 - a1;
+  const u32 nal = static_cast<u32>(a1 - a0), nbl = static_cast<u32>(b1 - b0), tot = nal + nbl;
+  for (u32 k = threadIdx.x; k < tot; k += blockDim.x) sk[k] = k < nal ? ka(a0 + k) : kb(b0 + (k - nal));
+  __syncthreads();
+  const K* A = sk;
+  const K* B = sk + nal;
+  const u32 dl = threadIdx.x * kMergeItems;
+  if (dl >= tot) return;
+  u32 lo = dl > nbl ? dl - nbl : 0, hi = dl < nal ? dl : nal;
+  while (lo < hi) {
+    const u32 mid = (lo + hi) >> 1;
+    if (B[dl - 1 - mid] < A[mid]) hi = mid;
+    else lo = mid + 1;
+  }
+  u32 i = lo, j = dl - lo;
+#pragma unroll
+  for (int k = 0; k < kMergeItems; ++k) {
+    if (dl + k >= tot) break;
+    const bool take_a = j >= nbl || (i < nal && !(B[j] < A[i]));
+    if (take_a) {
+      emit(d0 + dl + k, true, a0 + i, A[i]);
+      ++i;
+    } else {
+      emit(d0 + dl + k, false, b0 + j, B[j]);
+      ++j;
+    }
+  }
+}
+
+template <class K, class KA, class KB, class Emit>
+void merge_path(Ctx& ctx, KA ka, u64 na, KB kb, u64 nb, Emit emit) {
+  const u64 total = na + nb;
+  if (total == 0) return;
+  cudaStream_t st = ctx.stream;
+  const u64 ntiles = (total + kMergeTile - 1) / kMergeTile;
+  DevBuf<u64> part(ntiles + 1, st);
+  k_merge_partition<KA, KB><<<grid_for(ntiles + 1, 256, 1u << 16), 256, 0, st>>>(ka, na, kb, nb, ntiles, part.p);
+  TWG_LAUNCHED(ctx);
+  k_merge_tiles<K, KA, KB, Emit><<<static_cast<unsigned>(ntiles), kMergeBlock, 0, st>>>(ka, na, kb, nb, part.p,
+                                                                                        emit);
+  TWG_LAUNCHED(ctx);
+}
+
 // Stable LSD sort of (keys, vals) by the low `bits` bits of the key. Sorted
 // output lands in (*keys, *vals); the alt buffers are scratch of the same
 // size. Pointers are swapped as passes ping-pong. n < 2^32. Keys-only when

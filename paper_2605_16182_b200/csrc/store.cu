@@ -420,6 +420,90 @@ void ensure_adjacency(Ctx& ctx, Store& s) {
   build_adjacency(ctx, s, owners.p);
 }
 
+
+// Canonical (time, src, dst) order of n edges given dense internal ids
+// (edge_store.cpp:42-55; ties between identical triples are content-equal).
+void sort_canonical(Ctx& ctx, const u32* src_i, const u32* dst_i, const i64* t, u64 m, i64 tmin, i64 tmax, int vb,
+                    u32* o_src, u32* o_dst, i64* o_t) {
+  if (m == 0) return;
+  cudaStream_t st = ctx.stream;
+  const int tb = bit_width_u64(static_cast<u64>(tmax - tmin));
+  DevBuf<u64> k0(m, st), k1(m, st);
+  u64* kp = k0.p;
+  u64* ka = k1.p;
+  if (tb + 2 * vb <= 64) {
+    DevBuf<u32> v0(m, st);
+    k_pack_canonical<<<grid(ctx, m), kBlock, 0, st>>>(src_i, dst_i, t, m, tmin, vb, kp, v0.p);
+    TWG_LAUNCHED(ctx);
+    u32* vnull = nullptr;
+    u32* vnull2 = nullptr;
+    radix_sort_pairs<u64>(ctx, &kp, &ka, &vnull, &vnull2, m, tb + 2 * vb);
+    k_unpack_canonical<<<grid(ctx, m), kBlock, 0, st>>>(kp, m, tmin, vb, o_src, o_dst, o_t);
+    TWG_LAUNCHED(ctx);
+  } else {
+    DevBuf<u32> v0(m, st), v1(m, st);
+    u32* vp = v0.p;
+    u32* va = v1.p;
+    k_pack_pair<<<grid(ctx, m), kBlock, 0, st>>>(src_i, dst_i, m, vb, kp, vp);
+    TWG_LAUNCHED(ctx);
+    radix_sort_pairs<u64>(ctx, &kp, &ka, &vp, &va, m, 2 * vb);
+    k_gather_time_key<<<grid(ctx, m), kBlock, 0, st>>>(t, vp, m, tmin, kp);
+    TWG_LAUNCHED(ctx);
+    radix_sort_pairs<u64>(ctx, &kp, &ka, &vp, &va, m, tb);
+    k_gather_edges<<<grid(ctx, m), kBlock, 0, st>>>(src_i, dst_i, t, vp, m, o_src, o_dst, o_t);
+    TWG_LAUNCHED(ctx);
+  }
+}
+
+// ts_off / ts_time from the canonical time column (edge_store.cpp:91-98)
+void build_ts_view(Ctx& ctx, Store& s) {
+  cudaStream_t st = ctx.stream;
+  const u64 m = s.m;
+  u64 sc[1];
+  DevBuf<u32> gscan(m + 1, st);
+  exclusive_scan<u32>(ctx, TimeChangeFn{s.e_t.p}, m, gscan.p);
+  TWG_CUDA(cudaMemcpyAsync(ctx.d_scalars, gscan.p + m, sizeof(u32), cudaMemcpyDeviceToDevice, st));
+  TWG_CUDA(cudaMemsetAsync(reinterpret_cast<char*>(ctx.d_scalars) + 4, 0, 4, st));
+  read_scalars(ctx, ctx.d_scalars, sc, 1);
+  s.Z = sc[0];
+  s.ts_off.alloc(s.Z + 1, st);
+  s.ts_time.alloc(s.Z ? s.Z : 1, st);
+  if (m) {
+    k_ts_fill<<<grid(ctx, m), kBlock, 0, st>>>(s.e_t.p, gscan.p, m, s.ts_off.p, s.ts_time.p);
+    TWG_LAUNCHED(ctx);
+  }
+}
+
+// Region bounds, timestamp-group marks and group offsets from the node-sorted
+// owner column + entries (edge_store.cpp:164-214), then the optional views.
+void finish_node_view(Ctx& ctx, Store& s, BuildOpts opts) {
+  cudaStream_t st = ctx.stream;
+  const u64 P = s.P, V = s.V;
+  u64 sc[1];
+  const u32* okp = s.owner.p;
+  s.nmeta.alloc(V + 1, st);
+  k_region_bounds<<<grid(ctx, P + 1), kBlock, 0, st>>>(okp, P, V, s.nmeta.p);
+  TWG_LAUNCHED(ctx);
+  DevBuf<u32> gscan(P + 1, st);
+  exclusive_scan<u32>(ctx, GroupStartFn{okp, s.ent.p}, P, gscan.p);
+  TWG_CUDA(cudaMemcpyAsync(ctx.d_scalars, gscan.p + P, sizeof(u32), cudaMemcpyDeviceToDevice, st));
+  TWG_CUDA(cudaMemsetAsync(reinterpret_cast<char*>(ctx.d_scalars) + 4, 0, 4, st));
+  read_scalars(ctx, ctx.d_scalars, sc, 1);
+  s.Q = sc[0];
+  s.mk_time.alloc(s.Q ? s.Q : 1, st);
+  s.mk_start.alloc(s.Q ? s.Q : 1, st);
+  if (P) {
+    k_marks<<<grid(ctx, P), kBlock, 0, st>>>(okp, s.ent.p, gscan.p, P, s.mk_time.p, s.mk_start.p);
+    TWG_LAUNCHED(ctx);
+  }
+  k_group_offsets<<<grid(ctx, V + 1), kBlock, 0, st>>>(gscan.p, P, V, s.nmeta.p);
+  TWG_LAUNCHED(ctx);
+  s.has_weights = false;
+  s.has_adjacency = false;
+  if (opts.weights) ensure_weights(ctx, s);
+  if (opts.adjacency) build_adjacency(ctx, s, okp);
+}
+
 Store* build_store(Ctx& ctx, EdgesSoA in, int mode, BuildOpts opts, u64* scratch_peak) {
   cudaStream_t st = ctx.stream;
   const u64 m = in.n;
@@ -508,53 +592,17 @@ Store* build_store(Ctx& ctx, EdgesSoA in, int mode, BuildOpts opts, u64* scratch
   // 3. canonical (time, src, dst) order (edge_store.cpp:42-55)
   const int vb = V > 1 ? bit_width_u64(V - 1) : 0;
   const int tb = bit_width_u64(static_cast<u64>(tmax - tmin));
+  (void)tb;
   s->e_src.alloc(m, st);
   s->e_dst.alloc(m, st);
   s->e_t.alloc(m, st);
-  {
-    DevBuf<u64> k0(m, st), k1(m, st);
-    DevBuf<u32> v0(m, st), v1(m, st);
-    scratch += 24 * m;
-    u64* kp = k0.p;
-    u64* ka = k1.p;
-    u32* vp = v0.p;
-    u32* va = v1.p;
-    if (tb + 2 * vb <= 64) {
-      k_pack_canonical<<<grid(ctx, m), kBlock, 0, st>>>(src_i.p, dst_i.p, in.t, m, tmin, vb, kp, vp);
-      TWG_LAUNCHED(ctx);
-      u32* vnull = nullptr;
-      u32* vnull2 = nullptr;
-      radix_sort_pairs<u64>(ctx, &kp, &ka, &vnull, &vnull2, m, tb + 2 * vb);
-      k_unpack_canonical<<<grid(ctx, m), kBlock, 0, st>>>(kp, m, tmin, vb, s->e_src.p, s->e_dst.p, s->e_t.p);
-      TWG_LAUNCHED(ctx);
-    } else {
-      k_pack_pair<<<grid(ctx, m), kBlock, 0, st>>>(src_i.p, dst_i.p, m, vb, kp, vp);
-      TWG_LAUNCHED(ctx);
-      radix_sort_pairs<u64>(ctx, &kp, &ka, &vp, &va, m, 2 * vb);
-      k_gather_time_key<<<grid(ctx, m), kBlock, 0, st>>>(in.t, vp, m, tmin, kp);
-      TWG_LAUNCHED(ctx);
-      radix_sort_pairs<u64>(ctx, &kp, &ka, &vp, &va, m, tb);
-      k_gather_edges<<<grid(ctx, m), kBlock, 0, st>>>(src_i.p, dst_i.p, in.t, vp, m, s->e_src.p, s->e_dst.p,
-                                                       s->e_t.p);
-      TWG_LAUNCHED(ctx);
-    }
-  }
+  scratch += 24 * m;
+  sort_canonical(ctx, src_i.p, dst_i.p, in.t, m, tmin, tmax, vb, s->e_src.p, s->e_dst.p, s->e_t.p);
   src_i.release();
   dst_i.release();
 
   // 4. timestamp-grouped view (edge_store.cpp:91-110)
-  {
-    DevBuf<u32> gscan(m + 1, st);
-    exclusive_scan<u32>(ctx, TimeChangeFn{s->e_t.p}, m, gscan.p);
-    TWG_CUDA(cudaMemcpyAsync(ctx.d_scalars, gscan.p + m, sizeof(u32), cudaMemcpyDeviceToDevice, st));
-    TWG_CUDA(cudaMemsetAsync(reinterpret_cast<char*>(ctx.d_scalars) + 4, 0, 4, st));
-    read_scalars(ctx, ctx.d_scalars, sc, 1);
-    s->Z = sc[0];
-    s->ts_off.alloc(s->Z + 1, st);
-    s->ts_time.alloc(s->Z, st);
-    k_ts_fill<<<grid(ctx, m), kBlock, 0, st>>>(s->e_t.p, gscan.p, m, s->ts_off.p, s->ts_time.p);
-    TWG_LAUNCHED(ctx);
-  }
+  build_ts_view(ctx, *s);
 
   // 5. node-and-timestamp-grouped view (edge_store.cpp:112-214)
   DevBuf<u32> ok0(P, st), ok1(P, st), ov0(P, st), ov1(P, st);
@@ -569,27 +617,9 @@ Store* build_store(Ctx& ctx, EdgesSoA in, int mode, BuildOpts opts, u64* scratch
   s->ent.alloc(P, st);
   k_entries<<<grid(ctx, P), kBlock, 0, st>>>(okp, ovp, P, mode, s->e_src.p, s->e_dst.p, s->e_t.p, s->ent.p);
   TWG_LAUNCHED(ctx);
-  s->nmeta.alloc(V + 1, st);
-  k_region_bounds<<<grid(ctx, P + 1), kBlock, 0, st>>>(okp, P, V, s->nmeta.p);
-  TWG_LAUNCHED(ctx);
-  {
-    DevBuf<u32> gscan(P + 1, st);
-    exclusive_scan<u32>(ctx, GroupStartFn{okp, s->ent.p}, P, gscan.p);
-    TWG_CUDA(cudaMemcpyAsync(ctx.d_scalars, gscan.p + P, sizeof(u32), cudaMemcpyDeviceToDevice, st));
-    TWG_CUDA(cudaMemsetAsync(reinterpret_cast<char*>(ctx.d_scalars) + 4, 0, 4, st));
-    read_scalars(ctx, ctx.d_scalars, sc, 1);
-    s->Q = sc[0];
-    s->mk_time.alloc(s->Q, st);
-    s->mk_start.alloc(s->Q, st);
-    k_marks<<<grid(ctx, P), kBlock, 0, st>>>(okp, s->ent.p, gscan.p, P, s->mk_time.p, s->mk_start.p);
-    TWG_LAUNCHED(ctx);
-    k_group_offsets<<<grid(ctx, V + 1), kBlock, 0, st>>>(gscan.p, P, V, s->nmeta.p);
-    TWG_LAUNCHED(ctx);
-  }
-
-  // 6-7. optional views
-  if (opts.weights) ensure_weights(ctx, *s);
-  if (opts.adjacency) build_adjacency(ctx, *s, okp);
+  // owners of the sorted entries become the store's owner column
+  s->owner = std::move(okp == ok0.p ? ok0 : ok1);
+  finish_node_view(ctx, *s, opts);
   if (scratch_peak) *scratch_peak = scratch;
   return s.release();
 }

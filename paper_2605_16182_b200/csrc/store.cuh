@@ -73,6 +73,7 @@ struct Store {
   DevBuf<Entry> ent;
   DevBuf<double> wp;
   DevBuf<u32> adj_off, adj;
+  DevBuf<u32> owner;  // owner node of each node-view entry (drives the next batch's merge)
 
   StoreView view() const {
     return StoreView{mode,     m,         V,         Z,          P,         Q,       A,
@@ -83,9 +84,18 @@ struct Store {
   u64 device_bytes() const {
     return e_src.bytes() + e_dst.bytes() + e_t.bytes() + ext.bytes() + ts_off.bytes() +
            ts_time.bytes() + ts_w.bytes() + nmeta.bytes() + mk_time.bytes() + mk_start.bytes() +
-           ent.bytes() + wp.bytes() + adj_off.bytes() + adj.bytes();
+           ent.bytes() + wp.bytes() + adj_off.bytes() + adj.bytes() + owner.bytes();
   }
 };
+
+// canonical (t, src, dst) order of edges with dense internal ids (edge_store.cpp:42-55)
+void sort_canonical(Ctx& ctx, const u32* src_i, const u32* dst_i, const i64* t, u64 m, i64 tmin, i64 tmax, int vb,
+                    u32* o_src, u32* o_dst, i64* o_t);
+// ts_off / ts_time from s.e_t (edge_store.cpp:91-98)
+void build_ts_view(Ctx& ctx, Store& s);
+// nmeta / marks / group offsets (+ optional weights, adjacency) from the
+// node-sorted s.owner and s.ent (edge_store.cpp:164-250)
+void finish_node_view(Ctx& ctx, Store& s, BuildOpts opts);
 
 // Canonical-order edges of a build input, device SoA, external ids.
 struct EdgesSoA {

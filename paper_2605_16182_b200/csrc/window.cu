@@ -1,13 +1,30 @@
-// WindowManager on the device (window_manager.cpp:9-69).
+// WindowManager on the device (window_manager.cpp:9-69), streaming design.
 //
-// Per batch: batch_high by a device max-reduction; cutoff_for(new_high)
-// (window_manager.hpp:51-53); survivors = the suffix of the time-sorted
-// store at lower_bound(e_t, cutoff) (export_suffix, edge_store.cpp:325-332),
-// gathered back to external ids on the device; admitted batch edges
-// (t >= cutoff, window_manager.cpp:39-46) compacted by flag+scan behind them;
-// then the full dual-index rebuild over the merged set. Snapshot swap keeps
-// exactly one retired snapshot alive (window_manager.cpp:56-57); callers may
-// hold any snapshot longer through the store's reference count.
+// Semantics are the reference's: batch_high / new_high / cutoff_for
+// (window_manager.cpp:30-33, .hpp:51-53); survivors = the time-sorted suffix
+// at lower_bound(time, cutoff) (export_suffix, edge_store.cpp:325-332);
+// batch edges with t >= cutoff admitted, the rest dropped_late (:39-46);
+// the snapshot is rebuilt with re-densified ids (edge_store.cpp:57-89) and
+// exactly one retired snapshot is kept (:56-57).
+//
+// What changes is the cost: instead of re-sorting the whole window
+// (O(W log W) per batch, the reference's and our v1 path), only the batch is
+// sorted and then MERGED into the survivors, which are already in canonical
+// order:
+//   1. ids: presence flags over the external-id range from (a) the old nodes
+//      still referenced by a survivor and (b) admitted batch endpoints; an
+//      exclusive scan gives the new dense ids (= ranks, as the reference);
+//      old->new id table for the survivors.
+//   2. canonical order: radix sort of the admitted batch by (t, src, dst),
+//      merge-path merge with the survivors -> new edge columns + the new
+//      position of every survivor / batch edge.
+//   3. node view: the old node view's surviving entries (a suffix of every
+//      region) keep their order; re-keyed (new owner, new position) they are
+//      merged with the batch's entries (stable-sorted by owner) -> the new
+//      node view with payloads carried, no gathers.
+//   4. marks / offsets / ts view by flag + scan as in the full build.
+// Ids outside the dense fast path (huge or sparse external ids) take the v1
+// route: gather survivors back to external ids and run the full build.
 #include <chrono>
 
 #include "primitives.cuh"
@@ -19,15 +36,32 @@ namespace {
 
 constexpr int kBlock = 256;
 
-__global__ void k_init_max(i64* v) { *v = kTimeUnset; }
+unsigned grid(Ctx& ctx, u64 n) { return grid_for(n, kBlock, static_cast<unsigned>(ctx.sm_count) * 16); }
 
-__global__ void k_batch_max(const i64* t, u64 n, i64* out) {
-  i64 m = kTimeUnset;
+// scal: [0] batch max t (i64), [1] max non-negative id, [2] from, [3] admitted, [4] admitted negative id flag,
+//       [5] V_new, [6] max present id
+__global__ void k_init_scalars(u64* s) {
+  reinterpret_cast<i64*>(s)[0] = kTimeUnset;
+  for (int i = 1; i < 8; ++i) s[i] = 0;
+}
+
+__global__ void k_batch_stats(const i64* bs, const i64* bd, const i64* bt, u64 n, u64* scal) {
+  i64 mt = kTimeUnset;
+  u64 mid = 0;
   for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<u64>(gridDim.x) * blockDim.x)
-    m = max(m, t[i]);
-  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<long long*>(out), static_cast<long long>(m));
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    mt = max(mt, bt[i]);
+    if (bs[i] > 0) mid = max(mid, static_cast<u64>(bs[i]));
+    if (bd[i] > 0) mid = max(mid, static_cast<u64>(bd[i]));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mt = max(mt, __shfl_xor_sync(0xffffffffu, mt, o));
+    mid = max(mid, __shfl_xor_sync(0xffffffffu, mid, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(reinterpret_cast<long long*>(&scal[0]), static_cast<long long>(mt));
+    atomicMax(reinterpret_cast<unsigned long long*>(&scal[1]), mid);
+  }
 }
 
 // lower_bound(time_, cutoff) (edge_store.cpp:326)
@@ -41,6 +75,20 @@ __global__ void k_lower_bound(const i64* t, u64 m, i64 cutoff, u64* out) {
   *out = lo;
 }
 
+struct AdmitFn {
+  const i64* t;
+  i64 cutoff;
+  __device__ __forceinline__ u32 operator()(u64 i) const { return t[i] >= cutoff ? 1u : 0u; }
+};
+
+__global__ void k_admitted_neg(const i64* bs, const i64* bd, const i64* bt, u64 n, i64 cutoff, u64* flag) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<u64>(gridDim.x) * blockDim.x)
+    if (bt[i] >= cutoff && (bs[i] < 0 || bd[i] < 0)) atomicOr(reinterpret_cast<unsigned long long*>(flag), 1ull);
+}
+
+// ---- v1 route (full rebuild) -------------------------------------------------
+
 __global__ void k_gather_survivors(StoreView s, u64 from, i64* src, i64* dst, i64* t) {
   const u64 n = s.m - from;
   for (u64 k = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; k < n;
@@ -51,12 +99,6 @@ __global__ void k_gather_survivors(StoreView s, u64 from, i64* src, i64* dst, i6
     t[k] = s.e_t[i];
   }
 }
-
-struct AdmitFn {
-  const i64* t;
-  i64 cutoff;
-  __device__ __forceinline__ u32 operator()(u64 i) const { return t[i] >= cutoff ? 1u : 0u; }
-};
 
 __global__ void k_compact_batch(const i64* bs, const i64* bd, const i64* bt, u64 n, i64 cutoff, const u32* pos,
                                 u64 base, i64* src, i64* dst, i64* t) {
@@ -71,7 +113,330 @@ __global__ void k_compact_batch(const i64* bs, const i64* bd, const i64* bt, u64
   }
 }
 
-unsigned grid(Ctx& ctx, u64 n) { return grid_for(n, kBlock, static_cast<unsigned>(ctx.sm_count) * 16); }
+// ---- streaming route ---------------------------------------------------------------
+
+// old nodes referenced by a surviving edge (check-before-write: hub slots are
+// hammered by many edges; a plain store from each would serialise in L2)
+__global__ void k_flag_survivor_nodes(const u32* e_src, const u32* e_dst, u64 from, u64 m, u8* alive) {
+  for (u64 i = from + blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const u32 a = e_src[i], b = e_dst[i];
+    if (!alive[a]) alive[a] = 1;
+    if (!alive[b]) alive[b] = 1;
+  }
+}
+
+__global__ void k_present_old(const u8* alive, const i64* ext, u64 V, u8* present, u64* max_id) {
+  u64 mx = 0;
+  for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < V;
+       v += static_cast<u64>(gridDim.x) * blockDim.x) {
+    if (alive[v]) {
+      present[ext[v]] = 1;
+      mx = max(mx, static_cast<u64>(ext[v]));
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(reinterpret_cast<unsigned long long*>(max_id), mx);
+}
+
+__global__ void k_present_batch(const i64* bs, const i64* bd, const i64* bt, u64 n, i64 cutoff, u8* present,
+                                u64* max_id) {
+  u64 mx = 0;
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    if (bt[i] >= cutoff) {
+      const u64 a = static_cast<u64>(bs[i]), b = static_cast<u64>(bd[i]);
+      if (!present[a]) present[a] = 1;
+      if (!present[b]) present[b] = 1;
+      mx = max(mx, max(a, b));
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(reinterpret_cast<unsigned long long*>(max_id), mx);
+}
+
+struct U8Fn {
+  const u8* p;
+  __device__ __forceinline__ u32 operator()(u64 i) const { return p[i]; }
+};
+
+__global__ void k_fill_ext_u8(const u8* present, const u32* rank, u64 range, i64* ext) {
+  for (u64 id = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; id < range;
+       id += static_cast<u64>(gridDim.x) * blockDim.x)
+    if (present[id]) ext[rank[id]] = static_cast<i64>(id);
+}
+
+__global__ void k_old_to_new(const u8* alive, const i64* ext, const u32* rank, u64 V, u32* o2n) {
+  for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < V;
+       v += static_cast<u64>(gridDim.x) * blockDim.x)
+    o2n[v] = alive[v] ? rank[ext[v]] : 0xffffffffu;
+}
+
+__global__ void k_batch_internal(const i64* bs, const i64* bd, const i64* bt, u64 n, i64 cutoff, const u32* pos,
+                                 const u32* rank, u32* s_i, u32* d_i, i64* t_c) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    if (bt[i] >= cutoff) {
+      const u32 k = pos[i];
+      s_i[k] = rank[bs[i]];
+      d_i[k] = rank[bd[i]];
+      t_c[k] = bt[i];
+    }
+  }
+}
+
+// canonical key (t, src, dst) with new internal ids
+struct K3 {
+  i64 t;
+  u64 sd;
+  __device__ __forceinline__ bool operator<(const K3& o) const { return t < o.t || (t == o.t && sd < o.sd); }
+};
+
+struct SurvivorKey {
+  const u32* e_src;
+  const u32* e_dst;
+  const i64* e_t;
+  const u32* o2n;
+  u64 from;
+  __device__ __forceinline__ K3 operator()(u64 i) const {
+    const u64 p = from + i;
+    return K3{e_t[p], (static_cast<u64>(o2n[e_src[p]]) << 32) | o2n[e_dst[p]]};
+  }
+};
+
+struct BatchKey {
+  const u32* s;
+  const u32* d;
+  const i64* t;
+  __device__ __forceinline__ K3 operator()(u64 j) const {
+    return K3{t[j], (static_cast<u64>(s[j]) << 32) | d[j]};
+  }
+};
+
+struct CanonicalEmit {
+  u32* e_src;
+  u32* e_dst;
+  i64* e_t;
+  u32* spos;
+  u32* bpos;
+  __device__ __forceinline__ void operator()(u64 o, bool from_a, u64 idx, const K3& k) const {
+    e_src[o] = static_cast<u32>(k.sd >> 32);
+    e_dst[o] = static_cast<u32>(k.sd);
+    e_t[o] = k.t;
+    if (from_a) spos[idx] = static_cast<u32>(o);
+    else bpos[idx] = static_cast<u32>(o);
+  }
+};
+
+struct SurvivingEntryFn {
+  const Entry* ent;
+  u32 from;
+  __device__ __forceinline__ u32 operator()(u64 p) const { return ent[p].edge >= from ? 1u : 0u; }
+};
+
+// X: the old node view's surviving entries, re-keyed (new owner, new pos)
+__global__ void k_make_x(const Entry* ent, const u32* owner, u64 P, u32 from, const u32* xpos, const u32* o2n,
+                         const u32* spos, u64* xkey, u32* xnbr, i64* xt) {
+  for (u64 p = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; p < P;
+       p += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const Entry e = ent[p];
+    if (e.edge >= from) {
+      const u32 k = xpos[p];
+      xkey[k] = (static_cast<u64>(o2n[owner[p]]) << 32) | spos[e.edge - from];
+      xnbr[k] = o2n[e.nbr];
+      xt[k] = e.t;
+    }
+  }
+}
+
+// batch entries in canonical order: j -> owner (edge_store.cpp:120-124)
+__global__ void k_batch_owner_keys(const u32* s, const u32* d, u64 A, int mode, u32* keys, u32* vals) {
+  const u64 P = mode == TWG_UNDIRECTED ? 2 * A : A;
+  for (u64 j = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; j < P;
+       j += static_cast<u64>(gridDim.x) * blockDim.x) {
+    u32 o;
+    if (mode == TWG_UNDIRECTED) o = (j & 1) ? d[j >> 1] : s[j >> 1];
+    else if (mode == TWG_BACKWARD) o = d[j];
+    else o = s[j];
+    keys[j] = o;
+    vals[j] = static_cast<u32>(j);
+  }
+}
+
+__global__ void k_make_y(const u32* owners, const u32* jidx, u64 P, int mode, const u32* s, const u32* d,
+                         const i64* t, const u32* bpos, u64* ykey, u32* ynbr, i64* yt) {
+  for (u64 q = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; q < P;
+       q += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const u32 j = jidx[q];
+    const u32 k = mode == TWG_UNDIRECTED ? (j >> 1) : j;
+    const u32 o = owners[q];
+    u32 nbr;
+    if (mode == TWG_FORWARD) nbr = d[k];
+    else if (mode == TWG_BACKWARD) nbr = s[k];
+    else nbr = (j & 1) ? s[k] : d[k];
+    ykey[q] = (static_cast<u64>(o) << 32) | bpos[k];
+    ynbr[q] = nbr;
+    yt[q] = t[k];
+  }
+}
+
+struct U64Key {
+  const u64* k;
+  __device__ __forceinline__ u64 operator()(u64 i) const { return k[i]; }
+};
+
+struct EntryEmit {
+  const u32* xnbr;
+  const i64* xt;
+  const u32* ynbr;
+  const i64* yt;
+  u32* owner;
+  Entry* ent;
+  __device__ __forceinline__ void operator()(u64 o, bool from_a, u64 idx, const u64& key) const {
+    Entry e;
+    e.nbr = from_a ? xnbr[idx] : ynbr[idx];
+    e.edge = static_cast<u32>(key);
+    e.t = from_a ? xt[idx] : yt[idx];
+    ent[o] = e;
+    owner[o] = static_cast<u32>(key >> 32);
+  }
+};
+
+u64 read_u32_total(Ctx& ctx, const u32* p) {
+  u64 v[1];
+  TWG_CUDA(cudaMemsetAsync(ctx.d_scalars + 8, 0, 8, ctx.stream));
+  TWG_CUDA(cudaMemcpyAsync(ctx.d_scalars + 8, p, 4, cudaMemcpyDeviceToDevice, ctx.stream));
+  read_scalars(ctx, ctx.d_scalars + 8, v, 1);
+  return v[0];
+}
+
+// The streaming rebuild (file header, steps 1-4). `pos` = admitted-batch
+// compaction offsets. Returns the new snapshot.
+Store* ingest_streaming(Window& w, const i64* bs, const i64* bd, const i64* bt, u64 n, i64 cutoff, u64 from,
+                        u64 A, u64 R, const u32* pos, u64* scratch_out) {
+  Ctx& ctx = *w.ctx;
+  cudaStream_t st = ctx.stream;
+  const Store& O = *w.store;
+  const u64 S = O.m - from;
+  const u64 Vo = O.V;
+  u64 scratch = 0;
+
+  // 1. new dense ids
+  DevBuf<u8> alive(Vo ? Vo : 1, st);
+  DevBuf<u8> present(R, st);
+  DevBuf<u32> rank(R + 1, st);
+  scratch += Vo + 5 * R;
+  if (Vo) TWG_CUDA(cudaMemsetAsync(alive.p, 0, Vo, st));
+  TWG_CUDA(cudaMemsetAsync(present.p, 0, R, st));
+  TWG_CUDA(cudaMemsetAsync(ctx.d_scalars + 6, 0, 8, st));
+  if (S) {
+    k_flag_survivor_nodes<<<grid(ctx, S), kBlock, 0, st>>>(O.e_src.p, O.e_dst.p, from, O.m, alive.p);
+    TWG_LAUNCHED(ctx);
+  }
+  if (Vo) {
+    k_present_old<<<grid(ctx, Vo), kBlock, 0, st>>>(alive.p, O.ext.p, Vo, present.p, ctx.d_scalars + 6);
+    TWG_LAUNCHED(ctx);
+  }
+  if (A) {
+    k_present_batch<<<grid(ctx, n), kBlock, 0, st>>>(bs, bd, bt, n, cutoff, present.p, ctx.d_scalars + 6);
+    TWG_LAUNCHED(ctx);
+  }
+  exclusive_scan<u32>(ctx, U8Fn{present.p}, R, rank.p);
+  TWG_CUDA(cudaMemsetAsync(ctx.d_scalars + 5, 0, 8, st));
+  TWG_CUDA(cudaMemcpyAsync(ctx.d_scalars + 5, rank.p + R, 4, cudaMemcpyDeviceToDevice, st));
+  u64 sc[2];
+  read_scalars(ctx, ctx.d_scalars + 5, sc, 2);
+  const u64 Vn = sc[0];
+  w.max_ext = static_cast<i64>(sc[1]);
+
+  auto s = std::make_unique<Store>();
+  s->ctx = &ctx;
+  s->mode = w.mode;
+  s->m = S + A;
+  s->V = Vn;
+  s->ext.alloc(Vn ? Vn : 1, st);
+  k_fill_ext_u8<<<grid(ctx, R), kBlock, 0, st>>>(present.p, rank.p, R, s->ext.p);
+  TWG_LAUNCHED(ctx);
+  DevBuf<u32> o2n(Vo ? Vo : 1, st);
+  if (Vo) {
+    k_old_to_new<<<grid(ctx, Vo), kBlock, 0, st>>>(alive.p, O.ext.p, rank.p, Vo, o2n.p);
+    TWG_LAUNCHED(ctx);
+  }
+  present.release();
+  alive.release();
+
+  // 2. canonical order: sort the admitted batch, merge with the survivors
+  const int vb = Vn > 1 ? bit_width_u64(Vn - 1) : 0;
+  DevBuf<u32> bsi(A ? A : 1, st), bdi(A ? A : 1, st);
+  DevBuf<i64> btc(A ? A : 1, st);
+  DevBuf<u32> bS(A ? A : 1, st), bD(A ? A : 1, st);
+  DevBuf<i64> bT(A ? A : 1, st);
+  scratch += 32 * A;
+  if (A) {
+    k_batch_internal<<<grid(ctx, n), kBlock, 0, st>>>(bs, bd, bt, n, cutoff, pos, rank.p, bsi.p, bdi.p, btc.p);
+    TWG_LAUNCHED(ctx);
+    i64 tmax = cutoff;
+    {
+      // batch time range bound: [cutoff, new_high]
+      tmax = w.t_high_pending;
+    }
+    sort_canonical(ctx, bsi.p, bdi.p, btc.p, A, cutoff, tmax, vb, bS.p, bD.p, bT.p);
+  }
+  rank.release();
+  bsi.release();
+  bdi.release();
+  btc.release();
+  s->e_src.alloc(s->m ? s->m : 1, st);
+  s->e_dst.alloc(s->m ? s->m : 1, st);
+  s->e_t.alloc(s->m ? s->m : 1, st);
+  DevBuf<u32> spos(S ? S : 1, st), bpos(A ? A : 1, st);
+  scratch += 4 * (S + A);
+  merge_path<K3>(ctx, SurvivorKey{O.e_src.p, O.e_dst.p, O.e_t.p, o2n.p, from}, S, BatchKey{bS.p, bD.p, bT.p}, A,
+                 CanonicalEmit{s->e_src.p, s->e_dst.p, s->e_t.p, spos.p, bpos.p});
+  build_ts_view(ctx, *s);
+
+  // 3. node view: surviving old entries (X) merged with the batch's entries (Y)
+  const u64 Po = O.P;
+  DevBuf<u32> xpos(Po + 1, st);
+  exclusive_scan<u32>(ctx, SurvivingEntryFn{O.ent.p, static_cast<u32>(from)}, Po, xpos.p);
+  const u64 Xn = read_u32_total(ctx, xpos.p + Po);
+  DevBuf<u64> xkey(Xn ? Xn : 1, st);
+  DevBuf<u32> xnbr(Xn ? Xn : 1, st);
+  DevBuf<i64> xt(Xn ? Xn : 1, st);
+  scratch += 20 * Xn;
+  if (Po) {
+    k_make_x<<<grid(ctx, Po), kBlock, 0, st>>>(O.ent.p, O.owner.p, Po, static_cast<u32>(from), xpos.p, o2n.p, spos.p,
+                                               xkey.p, xnbr.p, xt.p);
+    TWG_LAUNCHED(ctx);
+  }
+  xpos.release();
+  const u64 Yn = w.mode == TWG_UNDIRECTED ? 2 * A : A;
+  DevBuf<u64> ykey(Yn ? Yn : 1, st);
+  DevBuf<u32> ynbr(Yn ? Yn : 1, st);
+  DevBuf<i64> yt(Yn ? Yn : 1, st);
+  scratch += 36 * Yn;
+  if (Yn) {
+    DevBuf<u32> k0(Yn, st), k1(Yn, st), v0(Yn, st), v1(Yn, st);
+    u32* kp = k0.p;
+    u32* ka = k1.p;
+    u32* vp = v0.p;
+    u32* va = v1.p;
+    k_batch_owner_keys<<<grid(ctx, Yn), kBlock, 0, st>>>(bS.p, bD.p, A, w.mode, kp, vp);
+    TWG_LAUNCHED(ctx);
+    radix_sort_pairs<u32>(ctx, &kp, &ka, &vp, &va, Yn, vb);
+    k_make_y<<<grid(ctx, Yn), kBlock, 0, st>>>(kp, vp, Yn, w.mode, bS.p, bD.p, bT.p, bpos.p, ykey.p, ynbr.p, yt.p);
+    TWG_LAUNCHED(ctx);
+  }
+  s->P = Xn + Yn;
+  s->ent.alloc(s->P ? s->P : 1, st);
+  s->owner.alloc(s->P ? s->P : 1, st);
+  merge_path<u64>(ctx, U64Key{xkey.p}, Xn, U64Key{ykey.p}, Yn,
+                  EntryEmit{xnbr.p, xt.p, ynbr.p, yt.p, s->owner.p, s->ent.p});
+  // 4. marks, offsets, optional views
+  finish_node_view(ctx, *s, w.opts);
+  if (scratch_out) *scratch_out = scratch;
+  return s.release();
+}
 
 }  // namespace
 
@@ -118,50 +483,69 @@ void window_ingest(Window& w, const i64* d_src, const i64* d_dst, const i64* d_t
     if (out) *out = stats;
     return;
   }
-  // batch_high, new_high, cutoff (window_manager.cpp:30-33)
-  k_init_max<<<1, 1, 0, st>>>(reinterpret_cast<i64*>(ctx.d_scalars));
-  TWG_LAUNCHED(ctx);
-  k_batch_max<<<grid(ctx, n), kBlock, 0, st>>>(d_t, n, reinterpret_cast<i64*>(ctx.d_scalars));
-  TWG_LAUNCHED(ctx);
   const Store& old = *w.store;
-  u64 sc[1];
-  read_scalars(ctx, ctx.d_scalars, sc, 1);
+  // batch_high, new_high, cutoff (window_manager.cpp:30-33)
+  k_init_scalars<<<1, 1, 0, st>>>(ctx.d_scalars);
+  TWG_LAUNCHED(ctx);
+  k_batch_stats<<<grid(ctx, n), kBlock, 0, st>>>(d_src, d_dst, d_t, n, ctx.d_scalars);
+  TWG_LAUNCHED(ctx);
+  u64 sc[2];
+  read_scalars(ctx, ctx.d_scalars, sc, 2);
   const i64 batch_high = static_cast<i64>(sc[0]);
+  const u64 batch_max_id = sc[1];
   const i64 new_high = w.t_high > batch_high ? w.t_high : batch_high;
   const i64 cutoff = w.cutoff_for(new_high);
 
-  // survivors: suffix of the old time-sorted store (export_suffix)
-  k_lower_bound<<<1, 1, 0, st>>>(old.e_t.p, old.m, cutoff, ctx.d_scalars + 1);
+  // survivors (export_suffix) and admitted batch edges
+  k_lower_bound<<<1, 1, 0, st>>>(old.e_t.p, old.m, cutoff, ctx.d_scalars + 2);
   TWG_LAUNCHED(ctx);
   DevBuf<u32> pos(n + 1, st);
   exclusive_scan<u32>(ctx, AdmitFn{d_t, cutoff}, n, pos.p);
-  TWG_CUDA(cudaMemsetAsync(ctx.d_scalars + 2, 0, 8, st));
-  TWG_CUDA(cudaMemcpyAsync(ctx.d_scalars + 2, pos.p + n, 4, cudaMemcpyDeviceToDevice, st));
+  TWG_CUDA(cudaMemcpyAsync(ctx.d_scalars + 3, pos.p + n, 4, cudaMemcpyDeviceToDevice, st));
+  k_admitted_neg<<<grid(ctx, n), kBlock, 0, st>>>(d_src, d_dst, d_t, n, cutoff, ctx.d_scalars + 4);
+  TWG_LAUNCHED(ctx);
   u64 r[3];
-  read_scalars(ctx, ctx.d_scalars, r, 3);
-  const u64 from = r[1];
+  read_scalars(ctx, ctx.d_scalars + 2, r, 3);
+  const u64 from = r[0];
+  const u64 admitted = r[1] & 0xffffffffull;
+  if (r[2]) fail(TWG_EINVAL, "edge store: negative node id");  // edge_store.cpp:37, state unchanged
   const u64 survivors = old.m - from;
-  const u64 admitted = r[2];
   stats.evicted = old.m - survivors;
   stats.dropped_late = n - admitted;
-
   const u64 total = survivors + admitted;
-  DevBuf<i64> ms(total ? total : 1, st), md(total ? total : 1, st), mt(total ? total : 1, st);
-  if (survivors) {
-    k_gather_survivors<<<grid(ctx, survivors), kBlock, 0, st>>>(old.view(), from, ms.p, md.p, mt.p);
-    TWG_LAUNCHED(ctx);
-  }
-  if (admitted) {
-    k_compact_batch<<<grid(ctx, n), kBlock, 0, st>>>(d_src, d_dst, d_t, n, cutoff, pos.p, survivors, ms.p, md.p,
-                                                     mt.p);
-    TWG_LAUNCHED(ctx);
-  }
-  pos.release();
+  if (total >= 0xffffffffull / 2) fail(TWG_EINVAL, "edge store: edge count exceeds 32-bit reference space");
+
+  // dense id fast path: the external-id range is compact
+  const u64 R = std::max<u64>(w.max_ext >= 0 ? static_cast<u64>(w.max_ext) : 0, batch_max_id) + 1;
+  const bool dense = R < (1ull << 31) && R <= std::max<u64>(8 * total, 1ull << 22);
   u64 scratch = 0;
-  Store* rebuilt = build_store(ctx, EdgesSoA{ms.p, md.p, mt.p, total}, w.mode, w.opts, &scratch);
+  Store* rebuilt = nullptr;
+  if (dense) {
+    w.t_high_pending = new_high;
+    rebuilt = ingest_streaming(w, d_src, d_dst, d_t, n, cutoff, from, admitted, R, pos.p, &scratch);
+  } else {
+    DevBuf<i64> ms(total ? total : 1, st), md(total ? total : 1, st), mt(total ? total : 1, st);
+    if (survivors) {
+      k_gather_survivors<<<grid(ctx, survivors), kBlock, 0, st>>>(old.view(), from, ms.p, md.p, mt.p);
+      TWG_LAUNCHED(ctx);
+    }
+    if (admitted) {
+      k_compact_batch<<<grid(ctx, n), kBlock, 0, st>>>(d_src, d_dst, d_t, n, cutoff, pos.p, survivors, ms.p, md.p,
+                                                       mt.p);
+      TWG_LAUNCHED(ctx);
+    }
+    pos.release();
+    rebuilt = build_store(ctx, EdgesSoA{ms.p, md.p, mt.p, total}, w.mode, w.opts, &scratch);
+    scratch += 24 * total;
+    if (rebuilt->V) {
+      u64 mx[1];
+      read_scalars(ctx, reinterpret_cast<const u64*>(rebuilt->ext.p + rebuilt->V - 1), mx, 1);
+      w.max_ext = static_cast<i64>(mx[0]);
+    }
+  }
 
   stats.retained = rebuilt->m;
-  stats.peak_bytes = old.device_bytes() + 24 * total + rebuilt->device_bytes() + scratch;
+  stats.peak_bytes = old.device_bytes() + rebuilt->device_bytes() + scratch;
   TWG_CUDA(cudaStreamSynchronize(st));
   stats.rebuild_duration = std::chrono::duration<double>(clock::now() - started).count();
   release_store(w.previous);

@@ -15,6 +15,8 @@ struct Window {
   i64 t_high = kTimeUnset;
   u64 batch_count = 0;
   twg_batch_stats stats{};
+  i64 max_ext = -1;            // largest external id in the current snapshot (dense-id fast path)
+  i64 t_high_pending = 0;      // new_high of the batch being ingested
 
   i64 cutoff_for(i64 high) const { return high > duration ? high - duration : 0; }  // window_manager.hpp:51-53
 };

@@ -202,6 +202,69 @@ def test_window_sequence_parity(tw, co, mode):
     assert_store(w.snapshot(), exp_dump)
 
 
+def _stream_batches(seed, nb, n, nodes, span, step, ids=None, dup=True):
+    """Random batches with late edges, duplicates and self-loops."""
+    rs = np.random.default_rng(seed)
+    out, base = [], 0
+    for b in range(nb):
+        t = base + rs.integers(0, span, n)
+        s = rs.integers(0, nodes, n)
+        d = rs.integers(0, nodes, n)
+        d[: n // 50] = s[: n // 50]  # self-loops
+        e = np.stack([s, d, t], 1)
+        if dup:
+            e[n // 2: n // 2 + n // 20] = e[: n // 20]  # exact duplicates
+        if ids is not None:
+            e[:, 0] = ids[e[:, 0]]
+            e[:, 1] = ids[e[:, 1]]
+        out.append(e)
+        base += step
+    return out
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("sparse", [False, True])
+def test_window_every_batch_bit_exact(tw, co, mode, sparse):
+    """Streaming merge path (dense ids) and full-rebuild path (sparse 62-bit
+    ids): the whole dual index after EVERY batch equals the oracle's."""
+    ids = np.random.default_rng(9).integers(0, 2**62, 400) if sparse else None
+    batches = _stream_batches(11 + mode, 12, 3000, 400, 300, 120, ids)
+    batches.insert(4, np.zeros((0, 3), np.int64))
+    exp_stats, exp_dumps = co.window_run(batches, 500, mode, every=True)
+    w = tw.WindowManager(500, tw.DirectionMode(mode))
+    for b, (es, eb), ed in zip(batches, exp_stats, exp_dumps):
+        st = w.ingest_batch(b)
+        assert (st.ingested, st.dropped_late, st.evicted, st.retained) == (
+            es["ingested"], es["dropped_late"], es["evicted"], es["retained"])
+        assert w.window_bounds() == eb
+        assert_store(w.snapshot(), ed)
+
+
+def test_window_c2_replay_state(tw, co):
+    """C2 shape: C1 edges sorted by time, 10 batches, Δ = span/3; every
+    post-eviction snapshot bit-exact (weights included: exp-weight default)."""
+    g = co.gen_uniform(100000, 1000000, 1000000, 1)
+    g = g[np.argsort(g[:, 2], kind="stable")]
+    bounds = tw.split_batches(g[:, 2], 100000)
+    batches = [g[a:b] for a, b in bounds]
+    assert len(batches) == 10
+    exp_stats, exp_dumps = co.window_run(batches, 333333, 0, every=True)
+    w = tw.WindowManager(333333)
+    for b, ed in zip(batches, exp_dumps):
+        w.ingest_batch(b)
+        assert_store(w.snapshot(), ed)
+
+
+def test_window_rejects_negative_admitted_id(tw):
+    w = tw.WindowManager(10)
+    w.ingest_batch([(1, 2, 5)])
+    with pytest.raises(ValueError):
+        w.ingest_batch([(-1, 2, 6)])
+    assert w.batch_count() == 1 and w.snapshot().edge_count() == 1
+    st = w.ingest_batch([(-1, 2, -7), (3, 4, 8)])  # negative edge is late: dropped, not an error
+    assert st.dropped_late == 1 and st.retained == 2
+
+
 # ------------------------------------------------------------------ walks
 
 @pytest.mark.parametrize("mode,direction", [(0, 0), (1, 1), (2, 0), (2, 1)])
