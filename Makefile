@@ -7,19 +7,25 @@ CSRC     := paper_2605_16182_b200/csrc
 SRCS     := $(wildcard $(CSRC)/*.cu)
 HDRS     := $(wildcard $(CSRC)/*.cuh) include/twg.h
 OBJDIR   := build/obj
-OBJS     := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(SRCS))
+OBJS     := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(SRCS)) $(OBJDIR)/host_timewalk_facade.o
+CXXHDRS  := $(wildcard include/timewalk/*.hpp) include/twg.h
 LIB      := paper_2605_16182_b200/lib/libtimewalk_b200.so
 NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Iinclude -Xcompiler -fPIC,-fopenmp,-O3 \
             --fmad=false -Xptxas -warn-spills --expt-relaxed-constexpr
 
-.PHONY: all lib oracle clean
-all: lib oracle
+.PHONY: all lib oracle clean facade_test
+all: lib oracle facade_test
 
 lib: $(LIB)
 
 $(OBJDIR)/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+# drop-in C++ façade (the reference's public API, C++20 like proj/core)
+$(OBJDIR)/host_timewalk_facade.o: $(CSRC)/host/timewalk_facade.cpp $(CXXHDRS)
+	@mkdir -p $(OBJDIR)
+	g++ -std=c++20 -O2 -fPIC -Wall -Wextra -Iinclude -c $< -o $@
 
 $(LIB): $(OBJS)
 	@mkdir -p $(dir $@)
@@ -30,3 +36,10 @@ oracle:
 
 clean:
 	rm -rf build $(LIB)
+
+# C++ drop-in check: the reference's API compiled against include/timewalk and linked to the library
+FACADE_TEST := build/facade_test
+facade_test: $(FACADE_TEST)
+$(FACADE_TEST): tests/cpp/facade_test.cpp $(CXXHDRS) $(LIB)
+	@mkdir -p build
+	g++ -std=c++20 -O2 -Wall -Wextra -Iinclude $< -o $@ -L$(dir $(LIB)) -ltimewalk_b200 -Wl,-rpath,'$$ORIGIN/../$(dir $(LIB))'

@@ -3,7 +3,7 @@
  * (libtimewalk_b200.so). Plain pointers and sizes only; no CUDA or torch
  * types cross this boundary.
  *
- * This is the thin C layer the drop-in C++ façade (include/timewalk/*.hpp,
+ * This is the thin C layer the drop-in C++ façade (include/timewalk/<name>.hpp,
  * same public API as the reference's proj/core) calls into, and what a
  * ctypes / cffi binding loads. Each entry point cites the reference
  * interface it replaces:
@@ -242,6 +242,36 @@ int twg_sample_start_edges(twg_store* s, int bias, const double* u1, const doubl
 int twg_schedule_step(twg_store* s, const uint32_t* node_of_walk, const uint8_t* alive, uint64_t n,
                       const twg_thresholds* thresholds, uint64_t* sizes5, uint32_t* rows,
                       uint64_t cap, uint32_t* walk_ids);
+
+/* init_walks (walk_engine.hpp:136-137) as a device round trip. Call once with
+ * all array pointers NULL to get stride and walk_count, then again with host
+ * arrays of walk_count (states) and walk_count*stride (walks) elements.
+ * WalkStates columns: current u32, time i64, prev u32, has_prev u8, alive u8,
+ * length u32. Walk slots not written by init are zero. */
+int twg_init_walks(twg_ctx* ctx, twg_store* s, const twg_walk_config* config, uint32_t* stride,
+                   uint64_t* walk_count, uint32_t* current, int64_t* time, uint32_t* prev,
+                   uint8_t* has_prev, uint8_t* alive, uint32_t* length, int64_t* nodes, int64_t* times);
+
+/* execute_task (walk_engine.hpp:153-155): one hop (hop_walk,
+ * walk_engine.cpp:88-145) for each listed walk id, updating the host
+ * WalkStates / WalkSet arrays in place (device round trip). */
+int twg_hop_walks(twg_ctx* ctx, twg_store* s, const twg_walk_config* config, const uint32_t* walk_ids,
+                  uint64_t n_ids, uint64_t walk_count, uint32_t stride, uint32_t* current, int64_t* time,
+                  uint32_t* prev, uint8_t* has_prev, uint8_t* alive, uint32_t* length, int64_t* nodes,
+                  int64_t* times);
+
+/* ---- primitives (primitives.hpp:11-31), device implementations -------------- */
+/* stable LSD radix sort of (u64 key, u32 value) pairs, in place (host arrays) */
+int twg_radix_sort_pairs(twg_ctx* ctx, uint64_t* keys, uint32_t* values, uint64_t n);
+/* exclusive scan of u64 (out may alias in); returns the total */
+int twg_exclusive_scan(twg_ctx* ctx, const uint64_t* in, uint64_t* out, uint64_t n, uint64_t* total);
+/* run-length encode of a sorted key sequence: runs (key u64, start u32,
+ * length u32) into out (capacity n rows of 3 u64); *runs = count */
+int twg_run_length_encode(twg_ctx* ctx, const uint64_t* sorted_keys, uint64_t n, uint64_t* out_rows,
+                          uint64_t* runs);
+/* stable compaction of items whose flags[item] != 0 (flags indexed by item) */
+int twg_partition_flagged(twg_ctx* ctx, const uint32_t* items, uint64_t n, const uint8_t* flags,
+                          uint64_t flags_len, uint32_t* out, uint64_t* kept);
 
 /* ---- samplers (device evaluation of the closed forms) ----------------------- */
 /* kind 0 uniform, 1 linear, 2 exponential; u in [0,1), n >= 1 */

@@ -104,6 +104,12 @@ SIGNATURES = {
     "twg_walkset_device": (I, [VP, PP, PP, PP]),
     "twg_sample_start_edges": (I, [VP, I, VP, VP, U64, VP]),
     "twg_schedule_step": (I, [VP, VP, VP, U64, VP, VP, VP, U64, VP]),
+    "twg_init_walks": (I, [VP, VP, C.POINTER(twg_walk_config), C.POINTER(C.c_uint32), C.POINTER(U64)] + [VP] * 8),
+    "twg_hop_walks": (I, [VP, VP, C.POINTER(twg_walk_config), VP, U64, U64, C.c_uint32] + [VP] * 8),
+    "twg_radix_sort_pairs": (I, [VP, VP, VP, U64]),
+    "twg_exclusive_scan": (I, [VP, VP, VP, U64, C.POINTER(U64)]),
+    "twg_run_length_encode": (I, [VP, VP, U64, VP, C.POINTER(U64)]),
+    "twg_partition_flagged": (I, [VP, VP, U64, VP, U64, VP, C.POINTER(U64)]),
     "twg_pick_index": (I, [VP, I, VP, VP, U64, VP]),
     "twg_pick_weighted_range": (I, [VP, VP, VP, U64, VP, VP, VP, U64, VP]),
     "twg_rng_bits": (I, [VP, I, U64, VP, VP, VP, U64, VP]),

@@ -545,12 +545,90 @@ int twg_schedule_step(twg_store* h, const uint32_t* node_of_walk, const uint8_t*
     Store& s = *h->s;
     Ctx& c = *s.ctx;
     const twg_thresholds th = thresholds ? *thresholds : twg_thresholds{4, 256, 8192, 512, 4096};
-    for (u64 i = 0; i < n; ++i) require(node_of_walk[i] < s.V, "schedule_step: node id out of range");
+    for (u64 i = 0; i < n; ++i) require(!alive[i] || node_of_walk[i] < s.V, "schedule_step: node id out of range");
     DevBuf<u32> dn;
     DevBuf<u8> da;
     h2d(c, dn, node_of_walk, n);
     h2d(c, da, alive, n);
     schedule_step_explicit(c, s, dn.p, da.p, n, th, sizes5, rows, cap, walk_ids);
+  });
+}
+
+int twg_init_walks(twg_ctx* ctx, twg_store* s, const twg_walk_config* config, uint32_t* stride, uint64_t* walk_count,
+                   uint32_t* current, int64_t* time, uint32_t* prev, uint8_t* has_prev, uint8_t* alive,
+                   uint32_t* length, int64_t* nodes, int64_t* times) {
+  return guarded([&] {
+    HostWalkArrays out{current, time, prev, has_prev, alive, length, nodes, times};
+    const bool fill = current && time && prev && has_prev && alive && length && nodes && times;
+    init_walks_dev(ctx->c, *s->s, *config, stride, walk_count, fill ? &out : nullptr);
+  });
+}
+
+int twg_hop_walks(twg_ctx* ctx, twg_store* s, const twg_walk_config* config, const uint32_t* walk_ids, uint64_t n_ids,
+                  uint64_t walk_count, uint32_t stride, uint32_t* current, int64_t* time, uint32_t* prev,
+                  uint8_t* has_prev, uint8_t* alive, uint32_t* length, int64_t* nodes, int64_t* times) {
+  return guarded([&] {
+    for (u64 i = 0; i < n_ids; ++i) require(walk_ids[i] < walk_count, "hop_walks: walk id out of range");
+    for (u64 i = 0; i < n_ids; ++i)
+      require(current[walk_ids[i]] < s->s->V && length[walk_ids[i]] < stride, "hop_walks: walk state out of range");
+    HostWalkArrays io{current, time, prev, has_prev, alive, length, nodes, times};
+    hop_walks_dev(ctx->c, *s->s, *config, walk_ids, n_ids, walk_count, stride, io);
+  });
+}
+
+int twg_radix_sort_pairs(twg_ctx* ctx, uint64_t* keys, uint32_t* values, uint64_t n) {
+  return guarded([&] {
+    Ctx& c = ctx->c;
+    require(n < (1ull << 32), "radix_sort_pairs: n");
+    DevBuf<u64> k;
+    DevBuf<u32> v;
+    h2d(c, k, keys, n);
+    h2d(c, v, values, n);
+    radix_sort_pairs_dev(c, k.p, v.p, n);
+    d2h(c, keys, k.p, n);
+    d2h(c, values, v.p, n);
+    sync(c);
+  });
+}
+
+int twg_exclusive_scan(twg_ctx* ctx, const uint64_t* in, uint64_t* out, uint64_t n, uint64_t* total) {
+  return guarded([&] {
+    Ctx& c = ctx->c;
+    DevBuf<u64> a, b(n + 1, c.stream);
+    h2d(c, a, in, n);
+    exclusive_scan_dev(c, a.p, b.p, n);
+    d2h(c, out, b.p, n);
+    u64 t[1];
+    read_scalars(c, b.p + n, t, 1);
+    if (total) *total = t[0];
+  });
+}
+
+int twg_run_length_encode(twg_ctx* ctx, const uint64_t* sorted_keys, uint64_t n, uint64_t* out_rows, uint64_t* runs) {
+  return guarded([&] {
+    Ctx& c = ctx->c;
+    DevBuf<u64> k, rows(3 * n + 3, c.stream);
+    h2d(c, k, sorted_keys, n);
+    const u64 r = run_length_encode_dev(c, k.p, n, rows.p);
+    d2h(c, out_rows, rows.p, 3 * r);
+    sync(c);
+    *runs = r;
+  });
+}
+
+int twg_partition_flagged(twg_ctx* ctx, const uint32_t* items, uint64_t n, const uint8_t* flags, uint64_t flags_len,
+                          uint32_t* out, uint64_t* kept) {
+  return guarded([&] {
+    Ctx& c = ctx->c;
+    for (u64 i = 0; i < n; ++i) require(items[i] < flags_len, "partition_flagged: item outside flags");
+    DevBuf<u32> it, o(n + 1, c.stream);
+    DevBuf<u8> fl;
+    h2d(c, it, items, n);
+    h2d(c, fl, flags, flags_len);
+    const u64 k = partition_flagged_dev(c, it.p, n, fl.p, o.p);
+    d2h(c, out, o.p, k);
+    sync(c);
+    *kept = k;
   });
 }
 

@@ -1,0 +1,632 @@
+// The drop-in C++ façade: the reference's public timewalk API
+// (proj/core/include/timewalk/*.hpp) implemented over the C ABI (twg.h).
+// Every computation is a GPU call; the host keeps only control flow,
+// argument validation (the reference's validate() contracts) and the lazily
+// downloaded mirrors that back the reference's span-returning accessors.
+// Status codes become the reference's exception types.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <map>
+#include <mutex>
+#include <new>
+#include <stdexcept>
+#include <string>
+
+#include "timewalk/edge_store.hpp"
+#include "timewalk/primitives.hpp"
+#include "timewalk/replay.hpp"
+#include "timewalk/samplers.hpp"
+#include "timewalk/walk_engine.hpp"
+#include "timewalk/window_manager.hpp"
+#include "twg.h"
+
+static_assert(sizeof(timewalk::TemporalEdge) == sizeof(twg_edge), "TemporalEdge must match twg_edge");
+
+namespace timewalk {
+
+namespace {
+
+std::recursive_mutex& api_mutex() {  // one ctx per device is shared; its scratch is not thread-safe
+  static std::recursive_mutex m;
+  return m;
+}
+
+thread_local int t_device = 0;
+
+[[noreturn]] void raise_status(int rc) {
+  const std::string msg = twg_last_error();
+  switch (rc) {
+    case TWG_EINVAL: throw std::invalid_argument(msg);
+    case TWG_ERANGE: throw std::out_of_range(msg);
+    case TWG_ELOGIC: throw std::logic_error(msg);
+    case TWG_ENOMEM: throw std::bad_alloc();
+    default: throw std::runtime_error("timewalk (B200): " + msg);
+  }
+}
+
+void check(int rc) {
+  if (rc != TWG_OK) raise_status(rc);
+}
+
+twg_ctx* ctx() {
+  static std::map<int, twg_ctx*> contexts;
+  std::lock_guard<std::recursive_mutex> lk(api_mutex());
+  auto it = contexts.find(t_device);
+  if (it != contexts.end()) return it->second;
+  twg_ctx* c = nullptr;
+  check(twg_ctx_create(t_device, &c));
+  contexts[t_device] = c;
+  return c;
+}
+
+twg_walk_config to_c(const WalkConfig& c) {
+  twg_walk_config w{};
+  w.walk_length = c.walk_length;
+  w.start_mode = static_cast<int32_t>(c.start_mode);
+  w.walks_per_node = c.walks_per_node;
+  w.total_walks = c.total_walks;
+  w.bias = static_cast<int32_t>(c.bias);
+  w.start_bias = static_cast<int32_t>(c.start_bias);
+  w.node2vec = c.node2vec ? 1 : 0;
+  w.temporal_adjacency = c.node2vec_temporal_adjacency ? 1 : 0;
+  w.p = c.node2vec ? c.node2vec->p : 1.0;
+  w.q = c.node2vec ? c.node2vec->q : 1.0;
+  w.direction = static_cast<int32_t>(c.direction);
+  w.rng = static_cast<int32_t>(c.rng);
+  w.seed = c.seed;
+  w.walk_begin = c.walk_begin;
+  w.walk_end = c.walk_end;
+  return w;
+}
+
+twg_thresholds to_c(const TierThresholds& t) {
+  return twg_thresholds{t.w_warp, t.block_dim, t.w_max, t.g_warp_cap, t.g_block_cap};
+}
+
+}  // namespace
+
+void set_device(int device) { t_device = device; }
+int current_device() { return t_device; }
+
+// ---------------------------------------------------------------- EdgeStore
+
+struct EdgeStore::Impl {
+  twg_store* h{nullptr};
+  twg_store_info info{};
+  std::once_flag f_edges, f_internal, f_ts, f_tsw, f_nodes, f_marks, f_ref, f_wp, f_ext;
+  std::vector<NodeId> src_ext, dst_ext;
+  std::vector<Timestamp> time;
+  std::vector<std::uint32_t> src, dst;
+  std::vector<std::uint64_t> ts_off;
+  std::vector<Timestamp> ts_time;
+  std::vector<double> ts_w;
+  std::vector<std::uint64_t> n_off, n_tsidx;
+  std::vector<TsGroupMark> marks;
+  std::vector<std::uint32_t> ref_edge, ref_nbr;
+  std::vector<double> wp;
+  std::vector<NodeId> ext;
+
+  ~Impl() {
+    if (h) twg_store_release(h);
+  }
+
+  template <class T>
+  void download(int field, std::vector<T>& out, std::size_t n) {
+    std::lock_guard<std::recursive_mutex> lk(api_mutex());
+    out.resize(n);
+    check(twg_store_download(h, field, out.empty() ? nullptr : out.data()));
+  }
+  void refresh_info() {
+    std::lock_guard<std::recursive_mutex> lk(api_mutex());
+    check(twg_store_get_info(h, &info));
+  }
+
+  const Impl& edges() {
+    std::call_once(f_edges, [&] {
+      download(0, src_ext, info.edges);
+      download(1, dst_ext, info.edges);
+      download(2, time, info.edges);
+    });
+    return *this;
+  }
+  const Impl& internal() {
+    std::call_once(f_internal, [&] {
+      download(3, src, info.edges);
+      download(4, dst, info.edges);
+    });
+    return *this;
+  }
+  const Impl& ts() {
+    std::call_once(f_ts, [&] {
+      download(5, ts_off, info.ts_groups + 1);
+      download(6, ts_time, info.ts_groups);
+    });
+    return *this;
+  }
+  const Impl& tsw() {
+    std::call_once(f_tsw, [&] { download(7, ts_w, info.ts_groups); });
+    return *this;
+  }
+  const Impl& nodes() {
+    std::call_once(f_nodes, [&] {
+      download(8, n_off, info.nodes + 1);
+      download(9, n_tsidx, info.nodes + 1);
+    });
+    return *this;
+  }
+  const Impl& mk() {
+    std::call_once(f_marks, [&] {
+      std::vector<Timestamp> t;
+      std::vector<std::uint32_t> s;
+      download(10, t, info.node_groups);
+      download(11, s, info.node_groups);
+      marks.resize(t.size());
+      for (std::size_t g = 0; g < t.size(); ++g) marks[g] = TsGroupMark{t[g], s[g]};
+    });
+    return *this;
+  }
+  const Impl& refs() {
+    std::call_once(f_ref, [&] {
+      download(12, ref_edge, info.entries);
+      download(15, ref_nbr, info.entries);
+    });
+    return *this;
+  }
+  const Impl& weights() {
+    std::call_once(f_wp, [&] { download(13, wp, info.entries); });
+    return *this;
+  }
+  const Impl& exts() {
+    std::call_once(f_ext, [&] { download(14, ext, info.nodes); });
+    return *this;
+  }
+};
+
+EdgeStore::EdgeStore(std::shared_ptr<Impl> impl) : impl_(std::move(impl)) {}
+
+EdgeStore::EdgeStore() : EdgeStore(build({}, DirectionMode::DirectedForward, BuildOptions{})) {}
+
+EdgeStore EdgeStore::build(std::span<const TemporalEdge> edges, DirectionMode mode, BuildTelemetry* telemetry) {
+  EdgeStore s = build(edges, mode, BuildOptions{});
+  if (telemetry) telemetry->scratch_bytes = s.impl_->info.device_bytes;
+  return s;
+}
+
+EdgeStore EdgeStore::build(std::span<const TemporalEdge> edges, DirectionMode mode, BuildOptions options) {
+  std::lock_guard<std::recursive_mutex> lk(api_mutex());
+  auto impl = std::make_shared<Impl>();
+  const twg_build_opts o{options.weights ? 1 : 0, options.adjacency ? 1 : 0};
+  check(twg_store_build(ctx(), reinterpret_cast<const twg_edge*>(edges.data()), edges.size(),
+                        static_cast<int>(mode), &o, &impl->h));
+  impl->refresh_info();
+  return EdgeStore(std::move(impl));
+}
+
+std::size_t EdgeStore::edge_count() const { return impl_->info.edges; }
+std::size_t EdgeStore::node_count() const { return impl_->info.nodes; }
+std::size_t EdgeStore::ts_group_count() const { return impl_->info.ts_groups; }
+bool EdgeStore::empty() const { return impl_->info.edges == 0; }
+DirectionMode EdgeStore::direction_mode() const { return static_cast<DirectionMode>(impl_->info.mode); }
+bool EdgeStore::supports(WalkDirection dir) const {
+  const auto m = direction_mode();
+  if (m == DirectionMode::Undirected) return true;
+  return (m == DirectionMode::DirectedForward) == (dir == WalkDirection::Forward);
+}
+std::size_t EdgeStore::memory_bytes() const { return impl_->info.device_bytes; }
+twg_store* EdgeStore::device_handle() const { return impl_->h; }
+
+std::pair<std::size_t, std::size_t> EdgeStore::edge_slice_for_ts_group(std::size_t g) const {
+  if (g >= ts_group_count()) throw std::out_of_range("edge_slice_for_ts_group: group index out of range");
+  const auto& m = impl_->ts();
+  return {m.ts_off[g], m.ts_off[g + 1]};
+}
+Timestamp EdgeStore::ts_group_time(std::size_t g) const { return impl_->ts().ts_time[g]; }
+std::span<const double> EdgeStore::ts_group_weight_prefix() const { return impl_->tsw().ts_w; }
+
+TemporalEdge EdgeStore::edge_at(std::size_t pos) const {
+  const auto& m = impl_->edges();
+  return {m.src_ext[pos], m.dst_ext[pos], m.time[pos]};
+}
+InternalNode EdgeStore::edge_source_internal(std::size_t pos) const { return impl_->internal().src[pos]; }
+InternalNode EdgeStore::edge_target_internal(std::size_t pos) const { return impl_->internal().dst[pos]; }
+Timestamp EdgeStore::edge_time(std::size_t pos) const { return impl_->edges().time[pos]; }
+std::span<const Timestamp> EdgeStore::edge_times() const { return impl_->edges().time; }
+
+std::optional<InternalNode> EdgeStore::find_node(NodeId external) const {
+  std::lock_guard<std::recursive_mutex> lk(api_mutex());
+  std::uint32_t id = 0;
+  std::uint8_t found = 0;
+  check(twg_store_find_nodes(impl_->h, &external, 1, &id, &found));
+  if (!found) return std::nullopt;
+  return id;
+}
+NodeId EdgeStore::external_id(InternalNode v) const { return impl_->exts().ext[v]; }
+
+NeighborRange EdgeStore::temporal_neighborhood(NodeId v, Timestamp t, WalkDirection dir) const {
+  std::lock_guard<std::recursive_mutex> lk(api_mutex());
+  std::uint64_t out[3] = {0, 0, 0};
+  check(twg_store_neighborhood(impl_->h, &v, &t, 1, static_cast<int>(dir), out));
+  return {out[0], out[1], out[2]};
+}
+NeighborRange EdgeStore::temporal_neighborhood_internal(InternalNode v, Timestamp t, WalkDirection dir) const {
+  return temporal_neighborhood(external_id(v), t, dir);
+}
+std::size_t EdgeStore::timestamp_group_count(NodeId v) const {
+  const auto iv = find_node(v);
+  return iv ? timestamp_group_count_internal(*iv) : 0;
+}
+std::size_t EdgeStore::timestamp_group_count_internal(InternalNode v) const {
+  const auto& m = impl_->nodes();
+  return m.n_tsidx[v + 1] - m.n_tsidx[v];
+}
+std::pair<std::size_t, std::size_t> EdgeStore::node_region(InternalNode v) const {
+  const auto& m = impl_->nodes();
+  return {m.n_off[v], m.n_off[v + 1]};
+}
+std::span<const TsGroupMark> EdgeStore::group_marks(InternalNode v) const {
+  const auto& n = impl_->nodes();
+  const auto& m = impl_->mk();
+  return {m.marks.data() + n.n_tsidx[v], n.n_tsidx[v + 1] - n.n_tsidx[v]};
+}
+EdgeIndex EdgeStore::ref_edge(std::size_t pos) const { return impl_->refs().ref_edge[pos]; }
+Timestamp EdgeStore::ref_time(std::size_t pos) const { return impl_->edges().time[impl_->refs().ref_edge[pos]]; }
+InternalNode EdgeStore::ref_neighbor(std::size_t pos, InternalNode owner) const {
+  if (direction_mode() != DirectionMode::Undirected) return impl_->refs().ref_nbr[pos];
+  const auto& in = impl_->internal();
+  const auto e = impl_->refs().ref_edge[pos];
+  return in.src[e] == owner ? in.dst[e] : in.src[e];
+}
+std::span<const double> EdgeStore::weight_prefix() const { return impl_->weights().wp; }
+
+bool EdgeStore::adjacent(InternalNode a, InternalNode b) const {
+  std::lock_guard<std::recursive_mutex> lk(api_mutex());
+  std::uint8_t r = 0;
+  check(twg_store_adjacent(impl_->h, &a, &b, 1, 0, nullptr, 0, &r));
+  return r != 0;
+}
+bool EdgeStore::adjacent_after(InternalNode a, InternalNode b, Timestamp t, WalkDirection dir) const {
+  if (!supports(dir)) {  // via temporal_neighborhood_internal (edge_store.cpp:279-281)
+    throw std::invalid_argument("temporal_neighborhood: walk direction not served by this store's direction mode");
+  }
+  std::lock_guard<std::recursive_mutex> lk(api_mutex());
+  std::uint8_t r = 0;
+  check(twg_store_adjacent(impl_->h, &a, &b, 1, 1, &t, static_cast<int>(dir), &r));
+  return r != 0;
+}
+
+std::vector<TemporalEdge> EdgeStore::export_suffix(Timestamp cutoff) const {
+  const auto& m = impl_->edges();
+  const auto from = static_cast<std::size_t>(std::lower_bound(m.time.begin(), m.time.end(), cutoff) - m.time.begin());
+  std::vector<TemporalEdge> out;
+  out.reserve(m.time.size() - from);
+  for (std::size_t i = from; i < m.time.size(); ++i) out.push_back({m.src_ext[i], m.dst_ext[i], m.time[i]});
+  return out;
+}
+
+// ---------------------------------------------------------------- window
+
+WindowManager::WindowManager(WindowConfig config) : WindowManager(config, BuildOptions{}) {}
+
+WindowManager::WindowManager(WindowConfig config, BuildOptions options) : config_(config) {
+  std::lock_guard<std::recursive_mutex> lk(api_mutex());
+  const twg_build_opts o{options.weights ? 1 : 0, options.adjacency ? 1 : 0};
+  check(twg_window_create(ctx(), config.duration, static_cast<int>(config.mode), &o, &handle_));
+  refresh();
+}
+
+WindowManager::~WindowManager() {
+  std::lock_guard<std::recursive_mutex> lk(api_mutex());
+  store_.reset();
+  previous_.reset();
+  if (handle_) twg_window_destroy(handle_);
+}
+
+void WindowManager::refresh() {
+  twg_store* h = nullptr;
+  check(twg_window_snapshot(handle_, &h));
+  auto impl = std::make_shared<EdgeStore::Impl>();
+  impl->h = h;
+  impl->refresh_info();
+  previous_ = std::move(store_);  // exactly one retired snapshot (window_manager.cpp:56-57)
+  store_ = std::make_shared<const EdgeStore>(EdgeStore(std::move(impl)));
+}
+
+const BatchStats& WindowManager::ingest_batch(std::span<const TemporalEdge> batch) {
+  std::lock_guard<std::recursive_mutex> lk(api_mutex());
+  twg_batch_stats s{};
+  check(twg_window_ingest(handle_, reinterpret_cast<const twg_edge*>(batch.data()), batch.size(), &s));
+  stats_ = BatchStats{s.ingested, s.dropped_late, s.evicted, s.retained, s.rebuild_duration, s.peak_bytes};
+  check(twg_window_state(handle_, &t_high_, &batch_count_, nullptr));
+  if (!batch.empty()) refresh();  // an empty batch leaves the snapshot itself unchanged
+  return stats_;
+}
+
+const BatchStats& WindowManager::ingest_batch_device(const std::int64_t* d_src, const std::int64_t* d_dst,
+                                                     const std::int64_t* d_t, std::uint64_t n) {
+  std::lock_guard<std::recursive_mutex> lk(api_mutex());
+  twg_batch_stats s{};
+  check(twg_window_ingest_device(handle_, d_src, d_dst, d_t, n, &s));
+  stats_ = BatchStats{s.ingested, s.dropped_late, s.evicted, s.retained, s.rebuild_duration, s.peak_bytes};
+  check(twg_window_state(handle_, &t_high_, &batch_count_, nullptr));
+  if (n) refresh();
+  return stats_;
+}
+
+std::pair<Timestamp, Timestamp> WindowManager::window_bounds() const {
+  std::lock_guard<std::recursive_mutex> lk(api_mutex());
+  Timestamp lo = 0, hi = 0;
+  check(twg_window_bounds(handle_, &lo, &hi));
+  return {lo, hi};
+}
+
+// ---------------------------------------------------------------- walks
+
+void TierThresholds::validate() const {
+  if (w_warp < 1 || w_warp > block_dim || block_dim > w_max)
+    throw std::invalid_argument("tier thresholds: need 1 <= w_warp <= block_dim <= w_max");
+  if (g_warp_cap > g_block_cap) throw std::invalid_argument("tier thresholds: need g_warp_cap <= g_block_cap");
+}
+
+void WalkConfig::validate() const {
+  if (walk_length < 1) throw std::invalid_argument("walk config: walk_length must be >= 1");
+  if (start_mode == StartMode::PerNode && walks_per_node == 0)
+    throw std::invalid_argument("walk config: walks_per_node must be positive");
+  if (node2vec && (node2vec->p <= 0.0 || node2vec->q <= 0.0))
+    throw std::invalid_argument("walk config: node2vec p and q must be positive");
+}
+
+WalkSet generate_walks(const EdgeStore& store, const WalkConfig& config, const TierThresholds& thresholds,
+                       Variant variant, WalkStats* stats) {
+  const auto started = std::chrono::steady_clock::now();
+  config.validate();
+  thresholds.validate();
+  std::lock_guard<std::recursive_mutex> lk(api_mutex());
+  const twg_walk_config c = to_c(config);
+  const twg_thresholds th = to_c(thresholds);
+  twg_walkset* w = nullptr;
+  twg_walk_stats st{};
+  check(twg_generate(ctx(), store.device_handle(), &c, &th, static_cast<int>(variant), &w, &st));
+  WalkSet out;
+  std::uint64_t first = 0, hops = 0;
+  const int rc = twg_walkset_info(w, &out.stride, &out.walk_count, &first, &hops);
+  if (rc == TWG_OK) {
+    out.nodes.resize(out.walk_count * out.stride);
+    out.times.resize(out.walk_count * out.stride);
+    out.lengths.resize(out.walk_count);
+  }
+  const int rc2 = rc == TWG_OK ? twg_walkset_download(w, out.nodes.data(), out.times.data(), out.lengths.data()) : rc;
+  twg_walkset_destroy(w);
+  check(rc2);
+  if (stats) {
+    *stats = WalkStats{st.walks, st.hops, st.steps,
+                       TierCounts{st.solo, st.warp_cached, st.warp_direct, st.block_cached, st.block_direct,
+                                  st.multi_block},
+                       std::chrono::duration<double>(std::chrono::steady_clock::now() - started).count()};
+  }
+  return out;
+}
+
+WalkSet generate_walks_fullwalk(const EdgeStore& store, const WalkConfig& config, WalkStats* stats) {
+  return generate_walks(store, config, TierThresholds{}, Variant::FullWalk, stats);
+}
+
+void init_walks(const EdgeStore& store, const WalkConfig& config, WalkStates& states, WalkSet& walks) {
+  config.validate();
+  std::lock_guard<std::recursive_mutex> lk(api_mutex());
+  const twg_walk_config c = to_c(config);
+  std::uint32_t stride = 0;
+  std::uint64_t count = 0;
+  check(twg_init_walks(ctx(), store.device_handle(), &c, &stride, &count, nullptr, nullptr, nullptr, nullptr, nullptr,
+                       nullptr, nullptr, nullptr));
+  walks.stride = stride;
+  walks.walk_count = count;
+  walks.nodes.assign(count * stride, 0);
+  walks.times.assign(count * stride, 0);
+  walks.lengths.assign(count, 0);
+  states.current.assign(count, 0);
+  states.time.assign(count, 0);
+  states.prev.assign(count, 0);
+  states.has_prev.assign(count, 0);
+  states.alive.assign(count, 0);
+  states.length.assign(count, 0);
+  if (count) {
+    check(twg_init_walks(ctx(), store.device_handle(), &c, &stride, &count, states.current.data(),
+                         states.time.data(), states.prev.data(), states.has_prev.data(), states.alive.data(),
+                         states.length.data(), walks.nodes.data(), walks.times.data()));
+  }
+  walks.lengths.assign(states.length.begin(), states.length.end());
+}
+
+StepPlan schedule_step(const WalkStates& states, const std::vector<std::uint32_t>& candidates, const EdgeStore& store,
+                       const TierThresholds& thresholds) {
+  thresholds.validate();
+  std::lock_guard<std::recursive_mutex> lk(api_mutex());
+  const std::size_t n = candidates.size();
+  std::vector<std::uint32_t> node(n);
+  std::vector<std::uint8_t> alive(n);
+  for (std::size_t i = 0; i < n; ++i) {
+    node[i] = states.current[candidates[i]];
+    alive[i] = states.alive[candidates[i]];
+  }
+  std::uint64_t sizes[5] = {0, 0, 0, 0, 0};
+  std::vector<std::uint32_t> rows(6 * (n + 16));
+  std::vector<std::uint32_t> ids(n + 1);
+  const twg_thresholds th = to_c(thresholds);
+  check(twg_schedule_step(store.device_handle(), node.data(), alive.data(), n, &th, sizes, rows.data(), n + 16,
+                          ids.data()));
+  StepPlan plan;
+  std::size_t alive_n = 0;
+  for (auto a : alive) alive_n += a ? 1 : 0;
+  plan.walk_ids.resize(alive_n);
+  for (std::size_t k = 0; k < alive_n; ++k) plan.walk_ids[k] = candidates[ids[k]];
+  std::vector<DispatchTask>* lists[5] = {&plan.solo, &plan.warp_cached, &plan.warp_direct, &plan.block_cached,
+                                         &plan.block_direct};
+  std::size_t r = 0;
+  for (int k = 0; k < 5; ++k) {
+    for (std::uint64_t x = 0; x < sizes[k]; ++x, ++r) {
+      const std::uint32_t* row = &rows[6 * r];
+      lists[k]->push_back(DispatchTask{row[0], static_cast<Tier>(row[5]), row[1], row[2], row[3], row[4]});
+    }
+  }
+  return plan;
+}
+
+void execute_task(const DispatchTask& task, const StepPlan& plan, const EdgeStore& store, const WalkConfig& config,
+                  bool /*use_scratch: staging is an execution detail, results are identical*/, TaskScratch& /*scratch*/,
+                  WalkStates& states, WalkSet& walks) {
+  std::lock_guard<std::recursive_mutex> lk(api_mutex());
+  const twg_walk_config c = to_c(config);
+  const std::uint32_t* ids = plan.walk_ids.data() + task.begin;
+  check(twg_hop_walks(ctx(), store.device_handle(), &c, ids, task.end - task.begin, states.size(), walks.stride,
+                      states.current.data(), states.time.data(), states.prev.data(), states.has_prev.data(),
+                      states.alive.data(), states.length.data(), walks.nodes.data(), walks.times.data()));
+}
+
+std::size_t sample_start_edge(const EdgeStore& store, BiasKind bias, double u1, double u2) {
+  std::lock_guard<std::recursive_mutex> lk(api_mutex());
+  std::uint64_t out = 0;
+  check(twg_sample_start_edges(store.device_handle(), static_cast<int>(bias), &u1, &u2, 1, &out));
+  return out;
+}
+
+// ---------------------------------------------------------------- samplers
+
+namespace {
+std::size_t pick(int kind, double u, std::size_t n) {
+  std::lock_guard<std::recursive_mutex> lk(api_mutex());
+  std::uint64_t nn = n, out = 0;
+  check(twg_pick_index(ctx(), kind, &u, &nn, 1, &out));
+  return out;
+}
+}  // namespace
+
+std::size_t pick_index_uniform(double u, std::size_t n) { return pick(0, u, n); }
+std::size_t pick_index_linear(double u, std::size_t n) { return pick(1, u, n); }
+std::size_t pick_index_exponential(double u, std::size_t n) { return pick(2, u, n); }
+
+std::size_t pick_weighted_range(double u, std::span<const double> prefix, std::size_t begin, std::size_t end,
+                                double base) {
+  std::lock_guard<std::recursive_mutex> lk(api_mutex());
+  std::uint64_t b = begin, e = end, out = 0;
+  check(twg_pick_weighted_range(ctx(), &u, prefix.data(), prefix.size(), &b, &e, &base, 1, &out));
+  return out;
+}
+
+std::size_t pick_weighted(double u, std::span<const double> prefix) {
+  if (prefix.empty()) throw std::invalid_argument("pick_weighted: empty prefix array");
+  // samplers.cpp:74-80 == pick_weighted_range over [0, n) with base 0
+  return pick_weighted_range(u, prefix, 0, prefix.size(), 0.0);
+}
+
+std::size_t pick_weighted(double u, const CumulativeWeights& cw) { return pick_weighted(u, cw.prefix); }
+
+// Reference utilities outside the walk path (samplers.cpp:57-72, :92-103),
+// evaluated where the caller's data lives, with the reference's arithmetic.
+CumulativeWeights build_cumulative_weights(std::span<const Timestamp> times) {
+  if (times.empty()) throw std::invalid_argument("build_cumulative_weights: empty input");
+  CumulativeWeights cw;
+  cw.prefix.resize(times.size());
+  double acc = 0.0;
+  for (std::size_t i = 0; i < times.size(); ++i) {
+    acc += std::exp(static_cast<double>(times[i] - times.front()));
+    cw.prefix[i] = acc;
+  }
+  return cw;
+}
+
+std::size_t oracle_pick(double u, std::span<const double> weights) {
+  if (weights.empty()) throw std::invalid_argument("oracle_pick: empty weights");
+  double total = 0.0;
+  for (double w : weights) total += w;
+  const double r = u * total;
+  double cum = 0.0;
+  for (std::size_t k = 0; k < weights.size(); ++k) {
+    cum += weights[k];
+    if (r < cum) return k;
+  }
+  return weights.size() - 1;
+}
+
+// ---------------------------------------------------------------- primitives
+
+namespace primitives {
+
+std::uint64_t exclusive_scan(std::span<const std::uint64_t> in, std::span<std::uint64_t> out) {
+  std::lock_guard<std::recursive_mutex> lk(api_mutex());
+  std::uint64_t total = 0;
+  check(twg_exclusive_scan(ctx(), in.data(), out.data(), in.size(), &total));
+  return total;
+}
+
+void radix_sort_pairs(std::vector<std::uint64_t>& keys, std::vector<std::uint32_t>& values) {
+  if (keys.size() < 2) return;
+  std::lock_guard<std::recursive_mutex> lk(api_mutex());
+  check(twg_radix_sort_pairs(ctx(), keys.data(), values.data(), keys.size()));
+}
+
+std::vector<KeyRun> run_length_encode(std::span<const std::uint64_t> sorted_keys) {
+  std::lock_guard<std::recursive_mutex> lk(api_mutex());
+  std::vector<std::uint64_t> rows(3 * sorted_keys.size() + 3);
+  std::uint64_t runs = 0;
+  check(twg_run_length_encode(ctx(), sorted_keys.data(), sorted_keys.size(), rows.data(), &runs));
+  std::vector<KeyRun> out(runs);
+  for (std::uint64_t r = 0; r < runs; ++r)
+    out[r] = KeyRun{rows[3 * r], static_cast<std::uint32_t>(rows[3 * r + 1]), static_cast<std::uint32_t>(rows[3 * r + 2])};
+  return out;
+}
+
+std::size_t partition_flagged(std::span<const std::uint32_t> items, std::span<const std::uint8_t> flags,
+                              std::vector<std::uint32_t>& out) {
+  std::lock_guard<std::recursive_mutex> lk(api_mutex());
+  out.assign(items.size(), 0);
+  std::uint64_t kept = 0;
+  check(twg_partition_flagged(ctx(), items.data(), items.size(), flags.data(), flags.size(), out.data(), &kept));
+  out.resize(kept);
+  return kept;
+}
+
+}  // namespace primitives
+
+// ---------------------------------------------------------------- replay
+
+void ReplayConfig::validate() const {
+  if (batch_duration <= 0) throw std::invalid_argument("replay: batch_duration must be positive");
+  if (window_duration < batch_duration) throw std::invalid_argument("replay: window_duration must be >= batch_duration");
+  walk.validate();
+  thresholds.validate();
+}
+
+// replay.cpp:16-53
+std::uint64_t replay_stream(std::span<const TemporalEdge> edges, const ReplayConfig& config, const BatchSink& sink) {
+  config.validate();
+  if (edges.empty()) return 0;
+  WindowManager window({config.window_duration, config.mode});
+  std::uint64_t batch_index = 0;
+  const Timestamp origin = edges.front().time;
+  Timestamp boundary = origin + config.batch_duration;
+  std::size_t begin = 0;
+  auto flush = [&](std::size_t end) {
+    if (end == begin) return;
+    BatchRecord record;
+    record.batch_index = batch_index++;
+    record.ingest = window.ingest_batch(edges.subspan(begin, end - begin));
+    WalkSet walks;
+    if (config.generate && !window.snapshot()->empty()) {
+      walks = generate_walks(*window.snapshot(), config.walk, config.thresholds, config.variant, &record.walk);
+    }
+    if (sink) sink(record, walks);
+    begin = end;
+  };
+  for (std::size_t i = 0; i < edges.size(); ++i) {
+    if (edges[i].time >= boundary) {
+      flush(i);
+      const Timestamp spans = (edges[i].time - origin) / config.batch_duration + 1;
+      boundary = origin + spans * config.batch_duration;
+    }
+  }
+  flush(edges.size());
+  return batch_index;
+}
+
+}  // namespace timewalk

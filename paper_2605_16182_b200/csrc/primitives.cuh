@@ -274,25 +274,47 @@ __global__ void __launch_bounds__(kMergeBlock) k_merge_tiles(KA ka, u64 na, KB k
   const K* A = sk;
   const K* B = sk + nal;
   const u32 dl = threadIdx.x * kMergeItems;
-  if (dl >= tot) return;
   u32 lo = dl > nbl ? dl - nbl : 0, hi = dl < nal ? dl : nal;
+  if (dl >= tot) lo = hi = 0;
   while (lo < hi) {
     const u32 mid = (lo + hi) >> 1;
     if (B[dl - 1 - mid] < A[mid]) hi = mid;
     else lo = mid + 1;
   }
   u32 i = lo, j = dl - lo;
+  K out[kMergeItems];
+  u32 src[kMergeItems];
 #pragma unroll
   for (int k = 0; k < kMergeItems; ++k) {
-    if (dl + k >= tot) break;
-    const bool take_a = j >= nbl || (i < nal && !(B[j] < A[i]));
-    if (take_a) {
-      emit(d0 + dl + k, true, a0 + i, A[i]);
-      ++i;
-    } else {
-      emit(d0 + dl + k, false, b0 + j, B[j]);
-      ++j;
+    if (dl + k < tot) {
+      const bool take_a = j >= nbl || (i < nal && !(B[j] < A[i]));
+      if (take_a) {
+        out[k] = A[i];
+        src[k] = i;  // index into the tile's A range
+        ++i;
+      } else {
+        out[k] = B[j];
+        src[k] = 0x80000000u | j;
+        ++j;
+      }
     }
+  }
+  // restage the merged tile in shared memory so the emitter's column writes
+  // are issued by consecutive threads for consecutive outputs (coalesced)
+  __shared__ u32 ssrc[kMergeTile];
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kMergeItems; ++k) {
+    if (dl + k < tot) {
+      sk[dl + k] = out[k];
+      ssrc[dl + k] = src[k];
+    }
+  }
+  __syncthreads();
+  for (u32 o = threadIdx.x; o < tot; o += blockDim.x) {
+    const u32 s = ssrc[o];
+    if (s & 0x80000000u) emit(d0 + o, false, b0 + (s & 0x7fffffffu), sk[o]);
+    else emit(d0 + o, true, a0 + s, sk[o]);
   }
 }
 

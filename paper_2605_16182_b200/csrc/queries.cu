@@ -165,7 +165,89 @@ __global__ void k_compact_explicit(const u32* nodes, const u8* alive, const u32*
   }
 }
 
+// run_length_encode (primitives.cpp:126-138): run starts by flag + scan
+struct RunStartFn {
+  const u64* k;
+  __device__ __forceinline__ u32 operator()(u64 i) const { return (i == 0 || k[i] != k[i - 1]) ? 1u : 0u; }
+};
+
+__global__ void k_rle_rows(const u64* k, const u32* rid, u64 n, u64* rows) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    if (i == 0 || k[i] != k[i - 1]) {
+      const u64 r = rid[i];
+      rows[3 * r] = k[i];
+      rows[3 * r + 1] = i;
+      u64 j = i + 1;  // run end: next start (runs are short on the paths that use this API)
+      while (j < n && k[j] == k[i]) ++j;
+      rows[3 * r + 2] = j - i;
+    }
+  }
+}
+
+// partition_flagged (primitives.cpp:140-148): flags indexed by item
+struct ItemFlagFn {
+  const u32* items;
+  const u8* flags;
+  __device__ __forceinline__ u32 operator()(u64 i) const { return flags[items[i]] ? 1u : 0u; }
+};
+
+__global__ void k_partition(const u32* items, const u8* flags, const u32* pos, u64 n, u32* out) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<u64>(gridDim.x) * blockDim.x)
+    if (flags[items[i]]) out[pos[i]] = items[i];
+}
+
 }  // namespace
+
+void radix_sort_pairs_dev(Ctx& ctx, u64* keys, u32* vals, u64 n) {
+  if (n < 2) return;
+  cudaStream_t st = ctx.stream;
+  DevBuf<u64> k1(n, st);
+  DevBuf<u32> v1(n, st);
+  u64* kp = keys;
+  u64* ka = k1.p;
+  u32* vp = vals;
+  u32* va = v1.p;
+  // full 64-bit key width (8 passes): stable, so passes over constant digits are no-ops
+  radix_sort_pairs<u64>(ctx, &kp, &ka, &vp, &va, n, 64);
+  if (kp != keys) {
+    TWG_CUDA(cudaMemcpyAsync(keys, kp, n * 8, cudaMemcpyDeviceToDevice, st));
+    TWG_CUDA(cudaMemcpyAsync(vals, vp, n * 4, cudaMemcpyDeviceToDevice, st));
+  }
+}
+
+void exclusive_scan_dev(Ctx& ctx, const u64* in, u64* out, u64 n) {
+  exclusive_scan<u64>(ctx, LoadFn<u64>{in}, n, out);
+}
+
+u64 run_length_encode_dev(Ctx& ctx, const u64* keys, u64 n, u64* rows) {
+  if (n == 0) return 0;
+  cudaStream_t st = ctx.stream;
+  DevBuf<u32> rid(n + 1, st);
+  exclusive_scan<u32>(ctx, RunStartFn{keys}, n, rid.p);
+  k_rle_rows<<<grid(ctx, n), kBlock, 0, st>>>(keys, rid.p, n, rows);
+  TWG_LAUNCHED(ctx);
+  u64 r[1];
+  TWG_CUDA(cudaMemsetAsync(ctx.d_scalars, 0, 8, st));
+  TWG_CUDA(cudaMemcpyAsync(ctx.d_scalars, rid.p + n, 4, cudaMemcpyDeviceToDevice, st));
+  read_scalars(ctx, ctx.d_scalars, r, 1);
+  return r[0];
+}
+
+u64 partition_flagged_dev(Ctx& ctx, const u32* items, u64 n, const u8* flags, u32* out) {
+  if (n == 0) return 0;
+  cudaStream_t st = ctx.stream;
+  DevBuf<u32> pos(n + 1, st);
+  exclusive_scan<u32>(ctx, ItemFlagFn{items, flags}, n, pos.p);
+  k_partition<<<grid(ctx, n), kBlock, 0, st>>>(items, flags, pos.p, n, out);
+  TWG_LAUNCHED(ctx);
+  u64 r[1];
+  TWG_CUDA(cudaMemsetAsync(ctx.d_scalars, 0, 8, st));
+  TWG_CUDA(cudaMemcpyAsync(ctx.d_scalars, pos.p + n, 4, cudaMemcpyDeviceToDevice, st));
+  read_scalars(ctx, ctx.d_scalars, r, 1);
+  return r[0];
+}
 
 void neighborhood_batch(Ctx& ctx, Store& s, const i64* d_v, const i64* d_t, u64 n, int dir, u64* d_out3) {
   const bool supports = s.mode == TWG_UNDIRECTED || ((s.mode == TWG_FORWARD) == (dir == 0));

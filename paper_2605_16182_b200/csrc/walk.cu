@@ -586,7 +586,174 @@ WalkParams make_params(Ctx& ctx, Store& s, const twg_walk_config& cfg, u32 strid
   return P;
 }
 
+// Start plan of init_walks (walk_engine.cpp:214-235): per-node starts are
+// the nodes with a non-empty region, in id order (walk id = rank * k + j).
+void plan_starts(Ctx& ctx, Store& s, const twg_walk_config& cfg, u32* stride, u64* total, DevBuf<u32>& start_nodes) {
+  cudaStream_t st = ctx.stream;
+  if (cfg.start_mode == 0) {
+    DevBuf<u32> flags(s.V ? s.V : 1, st), pos(s.V + 1, st);
+    if (s.V) {
+      k_start_flags<<<grid(ctx, s.V), kBlock, 0, st>>>(s.nmeta.p, s.V, flags.p);
+      TWG_LAUNCHED(ctx);
+    }
+    exclusive_scan<u32>(ctx, LoadFn<u32>{flags.p}, s.V, pos.p);
+    u64 sc[1];
+    TWG_CUDA(cudaMemsetAsync(ctx.d_scalars, 0, 8, st));
+    TWG_CUDA(cudaMemcpyAsync(ctx.d_scalars, pos.p + s.V, 4, cudaMemcpyDeviceToDevice, st));
+    read_scalars(ctx, ctx.d_scalars, sc, 1);
+    start_nodes.alloc(sc[0] ? sc[0] : 1, st);
+    if (s.V) {
+      k_start_nodes<<<grid(ctx, s.V), kBlock, 0, st>>>(flags.p, pos.p, s.V, start_nodes.p);
+      TWG_LAUNCHED(ctx);
+    }
+    *total = sc[0] * static_cast<u64>(cfg.walks_per_node);
+    *stride = cfg.walk_length;
+  } else {
+    if (s.m == 0) fail(TWG_EINVAL, "init_walks: sampled starts need a non-empty store");
+    *total = cfg.total_walks;
+    *stride = cfg.walk_length > 2 ? cfg.walk_length : 2;  // walk_engine.cpp:229
+  }
+  if (*total >= 0xffffffffull) fail(TWG_EINVAL, "init_walks: walk count exceeds 32-bit id space");
+}
+
+void validate_config(const twg_walk_config& cfg) {  // WalkConfig::validate (walk_engine.cpp:198-206)
+  if (cfg.walk_length < 1) fail(TWG_EINVAL, "walk config: walk_length must be >= 1");
+  if (cfg.start_mode == 0 && cfg.walks_per_node == 0) fail(TWG_EINVAL, "walk config: walks_per_node must be positive");
+  if (cfg.node2vec && (cfg.p <= 0.0 || cfg.q <= 0.0)) fail(TWG_EINVAL, "walk config: node2vec p and q must be positive");
+  if (cfg.bias < 0 || cfg.bias > 3 || cfg.start_bias < 0 || cfg.start_bias > 3) fail(TWG_EINVAL, "walk config: bias");
+  if (cfg.direction != 0 && cfg.direction != 1) fail(TWG_EINVAL, "walk config: direction");
+  if (cfg.rng != TWG_RNG_SPLITMIX && cfg.rng != TWG_RNG_PHILOX) fail(TWG_EINVAL, "walk config: rng");
+}
+
+__global__ void k_unpack_states(StateArrays S, u64 n, u32* cur, i64* t, u32* prev, u8* has_prev, u8* alive,
+                                u32* len) {
+  for (u64 w = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; w < n;
+       w += static_cast<u64>(gridDim.x) * blockDim.x) {
+    cur[w] = S.cur[w];
+    t[w] = S.t[w];
+    prev[w] = S.prev[w];
+    has_prev[w] = (S.flags[w] >> 1) & 1u;
+    alive[w] = S.flags[w] & 1u;
+    len[w] = S.len[w];
+  }
+}
+
+__global__ void k_pack_states(StateArrays S, u64 n, const u32* cur, const i64* t, const u32* prev, const u8* has_prev,
+                              const u8* alive, const u32* len) {
+  for (u64 w = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; w < n;
+       w += static_cast<u64>(gridDim.x) * blockDim.x) {
+    S.cur[w] = cur[w];
+    S.t[w] = t[w];
+    S.prev[w] = prev[w];
+    S.len[w] = len[w];
+    S.flags[w] = static_cast<u8>((alive[w] ? 1 : 0) | (has_prev[w] ? 2 : 0));
+  }
+}
+
+// execute_task's per-walk loop (walk_engine.cpp:357-359) over a walk-id list
+__global__ void k_hop_list(WalkParams P, StateArrays S, const u32* ids, u64 n, u64* stats) {
+  Ctr cn{0, 0};
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const u32 w = ids[i];
+    const uint2 a = P.s.nmeta[S.cur[w]], b = P.s.nmeta[S.cur[w] + 1];
+    WalkReg r;
+    load_state(S, w, r);
+    const bool ok = hop(P, w, r, P.s.mk_time, P.s.mk_start, a.y, b.y, a.x, b.x, &cn);
+    store_state(S, w, r, ok, P.stride);
+  }
+  add_counters(stats, cn);
+}
+
 }  // namespace
+
+void init_walks_dev(Ctx& ctx, Store& s, const twg_walk_config& cfg, u32* stride, u64* walk_count,
+                    const HostWalkArrays* out) {
+  validate_config(cfg);
+  cudaStream_t st = ctx.stream;
+  u64 total = 0;
+  DevBuf<u32> start_nodes;
+  plan_starts(ctx, s, cfg, stride, &total, start_nodes);
+  *walk_count = total;
+  if (!out || total == 0) return;
+  if (cfg.start_bias == TWG_EXPWEIGHT) ensure_weights(ctx, s);
+  WalkSetDev tmp;
+  tmp.nodes.alloc(total * *stride, st);
+  tmp.times.alloc(total * *stride, st);
+  TWG_CUDA(cudaMemsetAsync(tmp.nodes.p, 0, tmp.nodes.bytes(), st));
+  TWG_CUDA(cudaMemsetAsync(tmp.times.p, 0, tmp.times.bytes(), st));
+  WalkParams P = make_params(ctx, s, cfg, *stride, 0, tmp);
+  InitParams I{cfg.start_mode, cfg.walks_per_node, cfg.start_bias, start_nodes.p,
+               cfg.direction == 0 ? kTimeUnset : kTimeInfinite};
+  DevBuf<u32> cur(total, st), prev(total, st), len(total, st);
+  DevBuf<i64> tt(total, st);
+  DevBuf<u8> flags(total, st);
+  DevBuf<u64> stats(8, st);
+  TWG_CUDA(cudaMemsetAsync(stats.p, 0, stats.bytes(), st));
+  StateArrays S{cur.p, prev.p, tt.p, len.p, flags.p};
+  k_init_states<<<grid_for(total, kBlock, 0xffffffffu), kBlock, 0, st>>>(P, I, total, S, stats.p);
+  TWG_LAUNCHED(ctx);
+  DevBuf<u32> oc(total, st), op(total, st), ol(total, st);
+  DevBuf<i64> ot(total, st);
+  DevBuf<u8> oh(total, st), oa(total, st);
+  k_unpack_states<<<grid(ctx, total), kBlock, 0, st>>>(S, total, oc.p, ot.p, op.p, oh.p, oa.p, ol.p);
+  TWG_LAUNCHED(ctx);
+  TWG_CUDA(cudaMemcpyAsync(out->current, oc.p, total * 4, cudaMemcpyDeviceToHost, st));
+  TWG_CUDA(cudaMemcpyAsync(out->time, ot.p, total * 8, cudaMemcpyDeviceToHost, st));
+  TWG_CUDA(cudaMemcpyAsync(out->prev, op.p, total * 4, cudaMemcpyDeviceToHost, st));
+  TWG_CUDA(cudaMemcpyAsync(out->has_prev, oh.p, total, cudaMemcpyDeviceToHost, st));
+  TWG_CUDA(cudaMemcpyAsync(out->alive, oa.p, total, cudaMemcpyDeviceToHost, st));
+  TWG_CUDA(cudaMemcpyAsync(out->length, ol.p, total * 4, cudaMemcpyDeviceToHost, st));
+  TWG_CUDA(cudaMemcpyAsync(out->nodes, tmp.nodes.p, tmp.nodes.bytes(), cudaMemcpyDeviceToHost, st));
+  TWG_CUDA(cudaMemcpyAsync(out->times, tmp.times.p, tmp.times.bytes(), cudaMemcpyDeviceToHost, st));
+  TWG_CUDA(cudaStreamSynchronize(st));
+}
+
+void hop_walks_dev(Ctx& ctx, Store& s, const twg_walk_config& cfg, const u32* ids, u64 n_ids, u64 count, u32 stride,
+                   const HostWalkArrays& io) {
+  validate_config(cfg);
+  cudaStream_t st = ctx.stream;
+  if (cfg.bias == TWG_EXPWEIGHT) ensure_weights(ctx, s);
+  if (cfg.node2vec && !cfg.temporal_adjacency) ensure_adjacency(ctx, s);
+  if (n_ids == 0 || count == 0) return;
+  WalkSetDev tmp;
+  tmp.nodes.alloc(count * stride, st);
+  tmp.times.alloc(count * stride, st);
+  TWG_CUDA(cudaMemcpyAsync(tmp.nodes.p, io.nodes, tmp.nodes.bytes(), cudaMemcpyHostToDevice, st));
+  TWG_CUDA(cudaMemcpyAsync(tmp.times.p, io.times, tmp.times.bytes(), cudaMemcpyHostToDevice, st));
+  DevBuf<u32> ic(count, st), ip(count, st), il(count, st), dids(n_ids, st);
+  DevBuf<i64> it(count, st);
+  DevBuf<u8> ih(count, st), ia(count, st);
+  TWG_CUDA(cudaMemcpyAsync(ic.p, io.current, count * 4, cudaMemcpyHostToDevice, st));
+  TWG_CUDA(cudaMemcpyAsync(it.p, io.time, count * 8, cudaMemcpyHostToDevice, st));
+  TWG_CUDA(cudaMemcpyAsync(ip.p, io.prev, count * 4, cudaMemcpyHostToDevice, st));
+  TWG_CUDA(cudaMemcpyAsync(ih.p, io.has_prev, count, cudaMemcpyHostToDevice, st));
+  TWG_CUDA(cudaMemcpyAsync(ia.p, io.alive, count, cudaMemcpyHostToDevice, st));
+  TWG_CUDA(cudaMemcpyAsync(il.p, io.length, count * 4, cudaMemcpyHostToDevice, st));
+  TWG_CUDA(cudaMemcpyAsync(dids.p, ids, n_ids * 4, cudaMemcpyHostToDevice, st));
+  DevBuf<u32> cur(count, st), prev(count, st), len(count, st);
+  DevBuf<i64> tt(count, st);
+  DevBuf<u8> flags(count, st);
+  StateArrays S{cur.p, prev.p, tt.p, len.p, flags.p};
+  k_pack_states<<<grid(ctx, count), kBlock, 0, st>>>(S, count, ic.p, it.p, ip.p, ih.p, ia.p, il.p);
+  TWG_LAUNCHED(ctx);
+  DevBuf<u64> stats(8, st);
+  TWG_CUDA(cudaMemsetAsync(stats.p, 0, stats.bytes(), st));
+  WalkParams P = make_params(ctx, s, cfg, stride, 0, tmp);
+  k_hop_list<<<grid(ctx, n_ids), kBlock, 0, st>>>(P, S, dids.p, n_ids, stats.p);
+  TWG_LAUNCHED(ctx);
+  k_unpack_states<<<grid(ctx, count), kBlock, 0, st>>>(S, count, ic.p, it.p, ip.p, ih.p, ia.p, il.p);
+  TWG_LAUNCHED(ctx);
+  TWG_CUDA(cudaMemcpyAsync(io.current, ic.p, count * 4, cudaMemcpyDeviceToHost, st));
+  TWG_CUDA(cudaMemcpyAsync(io.time, it.p, count * 8, cudaMemcpyDeviceToHost, st));
+  TWG_CUDA(cudaMemcpyAsync(io.prev, ip.p, count * 4, cudaMemcpyDeviceToHost, st));
+  TWG_CUDA(cudaMemcpyAsync(io.has_prev, ih.p, count, cudaMemcpyDeviceToHost, st));
+  TWG_CUDA(cudaMemcpyAsync(io.alive, ia.p, count, cudaMemcpyDeviceToHost, st));
+  TWG_CUDA(cudaMemcpyAsync(io.length, il.p, count * 4, cudaMemcpyDeviceToHost, st));
+  TWG_CUDA(cudaMemcpyAsync(io.nodes, tmp.nodes.p, tmp.nodes.bytes(), cudaMemcpyDeviceToHost, st));
+  TWG_CUDA(cudaMemcpyAsync(io.times, tmp.times.p, tmp.times.bytes(), cudaMemcpyDeviceToHost, st));
+  TWG_CUDA(cudaStreamSynchronize(st));
+}
 
 void zero_walk_tails(Ctx& ctx, WalkSetDev& w) {
   if (w.tails_zeroed || w.count == 0) return;
@@ -639,30 +806,7 @@ WalkSetDev* generate_walks(Ctx& ctx, Store& s, const twg_walk_config& cfg, const
   // init_walks (walk_engine.cpp:208-245)
   u64 total = 0;
   DevBuf<u32> start_nodes;
-  if (cfg.start_mode == 0) {
-    DevBuf<u32> flags(s.V ? s.V : 1, st), pos(s.V + 1, st);
-    if (s.V) {
-      k_start_flags<<<grid(ctx, s.V), kBlock, 0, st>>>(s.nmeta.p, s.V, flags.p);
-      TWG_LAUNCHED(ctx);
-    }
-    exclusive_scan<u32>(ctx, LoadFn<u32>{flags.p}, s.V, pos.p);
-    u64 sc[1];
-    TWG_CUDA(cudaMemsetAsync(ctx.d_scalars, 0, 8, st));
-    TWG_CUDA(cudaMemcpyAsync(ctx.d_scalars, pos.p + s.V, 4, cudaMemcpyDeviceToDevice, st));
-    read_scalars(ctx, ctx.d_scalars, sc, 1);
-    start_nodes.alloc(sc[0] ? sc[0] : 1, st);
-    if (s.V) {
-      k_start_nodes<<<grid(ctx, s.V), kBlock, 0, st>>>(flags.p, pos.p, s.V, start_nodes.p);
-      TWG_LAUNCHED(ctx);
-    }
-    total = sc[0] * static_cast<u64>(cfg.walks_per_node);
-    out->stride = cfg.walk_length;
-  } else {
-    if (s.m == 0) fail(TWG_EINVAL, "init_walks: sampled starts need a non-empty store");
-    total = cfg.total_walks;
-    out->stride = cfg.walk_length > 2 ? cfg.walk_length : 2;
-  }
-  if (total >= 0xffffffffull) fail(TWG_EINVAL, "init_walks: walk count exceeds 32-bit id space");
+  plan_starts(ctx, s, cfg, &out->stride, &total, start_nodes);
   u64 wb = cfg.walk_begin, we = cfg.walk_end;
   if (wb == 0 && we == 0) we = total;
   if (we > total) we = total;

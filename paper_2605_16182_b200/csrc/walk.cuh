@@ -21,6 +21,24 @@ struct WalkSetDev {
 WalkSetDev* generate_walks(Ctx& ctx, Store& s, const twg_walk_config& cfg, const twg_thresholds& th,
                            int variant, twg_walk_stats* stats);
 
+// Host-side WalkStates + WalkSet columns (walk_engine.hpp:55-82).
+struct HostWalkArrays {
+  u32* current;
+  i64* time;
+  u32* prev;
+  u8* has_prev;
+  u8* alive;
+  u32* length;
+  i64* nodes;
+  i64* times;
+};
+
+// init_walks / execute_task as device round trips (reference unit-test API)
+void init_walks_dev(Ctx& ctx, Store& s, const twg_walk_config& cfg, u32* stride, u64* walk_count,
+                    const HostWalkArrays* out);
+void hop_walks_dev(Ctx& ctx, Store& s, const twg_walk_config& cfg, const u32* ids, u64 n_ids, u64 count, u32 stride,
+                   const HostWalkArrays& io);
+
 // zero the unused slots so the fixed-stride image equals the reference's
 // zero-initialised WalkSet (walk_engine.cpp:237-239)
 void zero_walk_tails(Ctx& ctx, WalkSetDev& w);
@@ -41,6 +59,12 @@ void pick_weighted_range_batch(Ctx& ctx, const double* d_u, const double* d_pref
                                const u64* d_end, const double* d_base, u64 count, u64* d_out);
 void rng_bits_batch(Ctx& ctx, int rng, u64 seed, const u64* d_walk, const u64* d_hop, const u64* d_ord,
                     u64 count, u64* d_out);
+
+// primitives.hpp:11-31 on device buffers
+void radix_sort_pairs_dev(Ctx& ctx, u64* keys, u32* vals, u64 n);
+void exclusive_scan_dev(Ctx& ctx, const u64* in, u64* out, u64 n);
+u64 run_length_encode_dev(Ctx& ctx, const u64* keys, u64 n, u64* rows);
+u64 partition_flagged_dev(Ctx& ctx, const u32* items, u64 n, const u8* flags, u32* out);
 
 // batched queries on a store
 void neighborhood_batch(Ctx& ctx, Store& s, const i64* d_v, const i64* d_t, u64 n, int dir, u64* d_out3);

@@ -45,22 +45,58 @@ __global__ void k_init_scalars(u64* s) {
   for (int i = 1; i < 8; ++i) s[i] = 0;
 }
 
+// scal[7]: bit0 = batch not time-ordered, bit1 = some equal-time run > kSegMax
+constexpr int kSegMax = 32;
+
 __global__ void k_batch_stats(const i64* bs, const i64* bd, const i64* bt, u64 n, u64* scal) {
   i64 mt = kTimeUnset;
   u64 mid = 0;
+  u32 shape = 0;
   for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<u64>(gridDim.x) * blockDim.x) {
-    mt = max(mt, bt[i]);
+    const i64 t = bt[i];
+    mt = max(mt, t);
     if (bs[i] > 0) mid = max(mid, static_cast<u64>(bs[i]));
     if (bd[i] > 0) mid = max(mid, static_cast<u64>(bd[i]));
+    if (i + 1 < n && t > bt[i + 1]) shape |= 1u;
+    if (i + kSegMax < n && t == bt[i + kSegMax]) shape |= 2u;
   }
   for (int o = 16; o > 0; o >>= 1) {
     mt = max(mt, __shfl_xor_sync(0xffffffffu, mt, o));
     mid = max(mid, __shfl_xor_sync(0xffffffffu, mid, o));
+    shape |= __shfl_xor_sync(0xffffffffu, shape, o);
   }
   if ((threadIdx.x & 31) == 0) {
     atomicMax(reinterpret_cast<long long*>(&scal[0]), static_cast<long long>(mt));
     atomicMax(reinterpret_cast<unsigned long long*>(&scal[1]), mid);
+    if (shape) atomicOr(reinterpret_cast<unsigned long long*>(&scal[7]), static_cast<u64>(shape));
+  }
+}
+
+// Canonical order of a time-ordered batch whose equal-time runs are short
+// (the common streaming case): sort each run by (src, dst) in registers —
+// one thread per run — instead of a 72-bit LSD radix sort.
+__global__ void k_segment_sort(const u32* s, const u32* d, const i64* t, u64 A, u32* os, u32* od, i64* ot) {
+  for (u64 k = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; k < A;
+       k += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const i64 tk = t[k];
+    if (k > 0 && t[k - 1] == tk) continue;
+    u64 key[kSegMax];
+    int len = 0;
+    while (len < kSegMax && k + len < A && t[k + len] == tk) {
+      u64 x = (static_cast<u64>(s[k + len]) << 32) | d[k + len];
+      int j = len++;
+      while (j > 0 && key[j - 1] > x) {  // insertion sort (stable for equal keys: content-equal)
+        key[j] = key[j - 1];
+        --j;
+      }
+      key[j] = x;
+    }
+    for (int j = 0; j < len; ++j) {
+      os[k + j] = static_cast<u32>(key[j] >> 32);
+      od[k + j] = static_cast<u32>(key[j]);
+      ot[k + j] = tk;
+    }
   }
 }
 
@@ -235,14 +271,21 @@ struct SurvivingEntryFn {
 };
 
 // X: the old node view's surviving entries, re-keyed (new owner, new pos)
+// New position of surviving edge i (0-based among survivors): survivors
+// before the first batch edge keep i (no batch edge precedes them) — for a
+// time-ordered stream that is all but the boundary tail, so the random
+// gather from spos is almost never issued.
 __global__ void k_make_x(const Entry* ent, const u32* owner, u64 P, u32 from, const u32* xpos, const u32* o2n,
-                         const u32* spos, u64* xkey, u32* xnbr, i64* xt) {
+                         const u32* spos, const u32* bpos, u64 A, u64 S, u64* xkey, u32* xnbr, i64* xt) {
+  const u64 i0 = A ? bpos[0] : S;
   for (u64 p = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; p < P;
        p += static_cast<u64>(gridDim.x) * blockDim.x) {
     const Entry e = ent[p];
     if (e.edge >= from) {
       const u32 k = xpos[p];
-      xkey[k] = (static_cast<u64>(o2n[owner[p]]) << 32) | spos[e.edge - from];
+      const u32 i = e.edge - from;
+      const u32 np = i < i0 ? i : spos[i];
+      xkey[k] = (static_cast<u64>(o2n[owner[p]]) << 32) | np;
       xnbr[k] = o2n[e.nbr];
       xt[k] = e.t;
     }
@@ -375,12 +418,13 @@ Store* ingest_streaming(Window& w, const i64* bs, const i64* bd, const i64* bt, 
   if (A) {
     k_batch_internal<<<grid(ctx, n), kBlock, 0, st>>>(bs, bd, bt, n, cutoff, pos, rank.p, bsi.p, bdi.p, btc.p);
     TWG_LAUNCHED(ctx);
-    i64 tmax = cutoff;
-    {
-      // batch time range bound: [cutoff, new_high]
-      tmax = w.t_high_pending;
+    if (w.batch_shape == 0) {
+      k_segment_sort<<<grid(ctx, A), kBlock, 0, st>>>(bsi.p, bdi.p, btc.p, A, bS.p, bD.p, bT.p);
+      TWG_LAUNCHED(ctx);
+    } else {
+      // admitted times lie in [cutoff, new_high]
+      sort_canonical(ctx, bsi.p, bdi.p, btc.p, A, cutoff, w.t_high_pending, vb, bS.p, bD.p, bT.p);
     }
-    sort_canonical(ctx, bsi.p, bdi.p, btc.p, A, cutoff, tmax, vb, bS.p, bD.p, bT.p);
   }
   rank.release();
   bsi.release();
@@ -406,7 +450,7 @@ Store* ingest_streaming(Window& w, const i64* bs, const i64* bd, const i64* bt, 
   scratch += 20 * Xn;
   if (Po) {
     k_make_x<<<grid(ctx, Po), kBlock, 0, st>>>(O.ent.p, O.owner.p, Po, static_cast<u32>(from), xpos.p, o2n.p, spos.p,
-                                               xkey.p, xnbr.p, xt.p);
+                                               bpos.p, A, S, xkey.p, xnbr.p, xt.p);
     TWG_LAUNCHED(ctx);
   }
   xpos.release();
@@ -489,10 +533,11 @@ void window_ingest(Window& w, const i64* d_src, const i64* d_dst, const i64* d_t
   TWG_LAUNCHED(ctx);
   k_batch_stats<<<grid(ctx, n), kBlock, 0, st>>>(d_src, d_dst, d_t, n, ctx.d_scalars);
   TWG_LAUNCHED(ctx);
-  u64 sc[2];
-  read_scalars(ctx, ctx.d_scalars, sc, 2);
+  u64 sc[8];
+  read_scalars(ctx, ctx.d_scalars, sc, 8);
   const i64 batch_high = static_cast<i64>(sc[0]);
   const u64 batch_max_id = sc[1];
+  w.batch_shape = static_cast<u32>(sc[7]);
   const i64 new_high = w.t_high > batch_high ? w.t_high : batch_high;
   const i64 cutoff = w.cutoff_for(new_high);
 

@@ -240,6 +240,22 @@ def test_window_every_batch_bit_exact(tw, co, mode, sparse):
         assert_store(w.snapshot(), ed)
 
 
+@pytest.mark.parametrize("span", [3000, 40])
+def test_window_time_ordered_batches(tw, co, span):
+    """Time-ordered batches take the in-register segment sort (short
+    equal-time runs, span 3000) or fall back to the radix sort (runs > 32,
+    span 40); both bit-exact after every batch."""
+    batches = []
+    for e in _stream_batches(21, 8, 2000, 300, span, span // 2):
+        batches.append(e[np.argsort(e[:, 2], kind="stable")])
+    for mode in (0, 2):
+        exp_stats, exp_dumps = co.window_run(batches, span * 2, mode, every=True)
+        w = tw.WindowManager(span * 2, tw.DirectionMode(mode))
+        for b, ed in zip(batches, exp_dumps):
+            w.ingest_batch(b)
+            assert_store(w.snapshot(), ed)
+
+
 def test_window_c2_replay_state(tw, co):
     """C2 shape: C1 edges sorted by time, 10 batches, Δ = span/3; every
     post-eviction snapshot bit-exact (weights included: exp-weight default)."""
