@@ -145,11 +145,13 @@ def run_ours(args, rank, world, local_rank):
         args.variant]
     B = wl.batch_edges
 
+    from paper_2605_16182_b200.dist import broadcast_batch, shard_config
+
     def walk_cfg():
-        return tw.WalkConfig(walk_length=wl.walk_length, start_mode=tw.StartMode.Sampled,
-                             total_walks=wl.walks * world, bias=tw.BiasKind.ExponentialIndex,
-                             start_bias=tw.BiasKind.UniformIndex, seed=wl.seed,
-                             walk_begin=rank * wl.walks, walk_end=(rank + 1) * wl.walks)
+        # weak scaling: every rank generates wl.walks walks of the global id space
+        base = tw.WalkConfig(walk_length=wl.walk_length, start_mode=tw.StartMode.Sampled, total_walks=wl.walks,
+                             bias=tw.BiasKind.ExponentialIndex, start_bias=tw.BiasKind.UniformIndex, seed=wl.seed)
+        return shard_config(base, rank, world, walks_per_rank=wl.walks)
 
     lib = tw._abi.load()
 
@@ -160,10 +162,9 @@ def run_ours(args, rank, world, local_rank):
         assert rc == 0, lib.twg_last_error()
 
     def bcast(buf):
-        if world > 1:
+        if world > 1:  # one copy of the batch over NVLink into every replica (NCCL)
             with torch.cuda.stream(stream):
-                for x in buf:
-                    dist.broadcast(x, src=0)
+                broadcast_batch(buf, src=0)
 
     def new_buf():
         return [torch.empty(B, dtype=torch.int64, device=f"cuda:{local_rank}") for _ in range(3)]
