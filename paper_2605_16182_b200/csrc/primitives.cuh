@@ -231,6 +231,118 @@ __global__ void __launch_bounds__(kSortBlock) k_radix_scatter(const K* __restric
   }
 }
 
+// ---------------------------------------------------- single-pass scan ----
+//
+// Flag -> exclusive scan -> scatter in ONE pass over the input (decoupled
+// look-back): each CTA takes a tile by ticket, scans its 2048 flags, posts
+// its aggregate, resolves its global prefix from its predecessors' posts,
+// and hands every item (index, exclusive prefix, flag) to the scatter
+// functor. Replaces the three-kernel chains (tile sums, rescan, scatter)
+// that read the input twice. The grand total lands in *total.
+constexpr u64 kLbAggregate = 1ull << 62;
+constexpr u64 kLbInclusive = 2ull << 62;
+constexpr u64 kLbValueMask = (1ull << 62) - 1;
+
+// Flags are 0/1. Each warp owns 256 consecutive items (8 rounds of 32), so
+// every flag load and every scatter is issued by 32 lanes for 32 consecutive
+// items (coalesced); in-warp prefixes come from ballot + popc.
+template <class FlagFn, class Scatter>
+__global__ void __launch_bounds__(kScanBlock) k_scan_scatter(FlagFn flag, u64 n, u64* tile_state, u32* ticket,
+                                                             u64* total, Scatter scatter) {
+  __shared__ u32 s_tile;
+  __shared__ u64 s_prefix;
+  __shared__ u32 s_warp[kScanBlock / 32 + 1];
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const u64 tile = s_tile;
+  const u64 base = tile * kScanTile;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const u32 lt = (1u << lane) - 1u;
+  const u64 wbase = base + static_cast<u64>(warp) * (32 * kScanItems);
+  u32 f[kScanItems];
+  u32 bal[kScanItems];
+  u32 wsum = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    const u64 i = wbase + j * 32 + lane;
+    f[j] = i < n ? flag(i) : 0u;
+  }
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    bal[j] = __ballot_sync(0xffffffffu, f[j] != 0);
+    wsum += __popc(bal[j]);
+  }
+  if (lane == 0) s_warp[warp] = wsum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    u32 acc = 0;
+    for (int w = 0; w < kScanBlock / 32; ++w) {
+      const u32 c = s_warp[w];
+      s_warp[w] = acc;
+      acc += c;
+    }
+    s_warp[kScanBlock / 32] = acc;
+  }
+  __syncthreads();
+  const u32 agg = s_warp[kScanBlock / 32];
+  if (warp == 0) {
+    // warp-parallel decoupled look-back: 32 predecessors per round
+    volatile u64* st = tile_state;
+    u64 prefix = 0;
+    if (tile == 0) {
+      if (lane == 0) st[0] = kLbInclusive | agg;
+    } else {
+      if (lane == 0) st[tile] = kLbAggregate | agg;
+      long long p = static_cast<long long>(tile) - 1;
+      while (true) {
+        const long long idx = p - lane;
+        u64 s = kLbInclusive;  // before tile 0: inclusive zero
+        if (idx >= 0) {
+          do {
+            s = st[idx];
+          } while ((s >> 62) == 0);
+        }
+        const u32 incl = __ballot_sync(0xffffffffu, (s >> 62) == 2);
+        const int stop = incl ? __ffs(incl) - 1 : 31;  // closest predecessor holding a full prefix
+        u64 v = lane <= stop ? (s & kLbValueMask) : 0;
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        prefix += v;
+        if (incl) break;
+        p -= 32;
+      }
+      if (lane == 0) st[tile] = kLbInclusive | (prefix + agg);
+    }
+    if (lane == 0) {
+      s_prefix = prefix;
+      if (base + kScanTile >= n) *total = prefix + agg;
+    }
+  }
+  __syncthreads();
+  u64 run = s_prefix + s_warp[warp];
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    const u64 i = wbase + j * 32 + lane;
+    if (i < n) scatter(i, run + __popc(bal[j] & lt), f[j]);
+    run += __popc(bal[j]);
+  }
+}
+
+// total -> *d_total (device). n == 0 writes 0.
+template <class FlagFn, class Scatter>
+void scan_scatter(Ctx& ctx, FlagFn flag, u64 n, u64* d_total, Scatter scatter) {
+  cudaStream_t st = ctx.stream;
+  if (n == 0) {
+    TWG_CUDA(cudaMemsetAsync(d_total, 0, sizeof(u64), st));
+    return;
+  }
+  const u64 tiles = (n + kScanTile - 1) / kScanTile;
+  DevBuf<u64> state(tiles + 1, st);
+  TWG_CUDA(cudaMemsetAsync(state.p, 0, state.bytes(), st));  // +1 word holds the ticket
+  k_scan_scatter<FlagFn, Scatter><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(
+      flag, n, state.p, reinterpret_cast<u32*>(state.p + tiles), d_total, scatter);
+  TWG_LAUNCHED(ctx);
+}
+
 // --------------------------------------------------------------- merge ----
 //
 // Merge-path merge of two sorted sequences A (na) and B (nb), A first on
@@ -269,7 +381,21 @@ __global__ void __launch_bounds__(kMergeBlock) k_merge_tiles(KA ka, u64 na, KB k
   const u64 a0 = part[t], a1 = part[t + 1];
   const u64 b0 = d0 - a0, b1 = d1 - a1;
   const u32 nal = static_cast<u32>(a1 - a0), nbl = static_cast<u32>(b1 - b0), tot = nal + nbl;
-  for (u32 k = threadIdx.x; k < tot; k += blockDim.x) sk[k] = k < nal ? ka(a0 + k) : kb(b0 + (k - nal));
+  {
+    // all of a thread's key loads issued before any is consumed (ILP for the
+    // dependent id-remap gathers inside ka)
+    K tmp[kMergeItems];
+#pragma unroll
+    for (int r = 0; r < kMergeItems; ++r) {
+      const u32 k = r * kMergeBlock + threadIdx.x;
+      if (k < tot) tmp[r] = k < nal ? ka(a0 + k) : kb(b0 + (k - nal));
+    }
+#pragma unroll
+    for (int r = 0; r < kMergeItems; ++r) {
+      const u32 k = r * kMergeBlock + threadIdx.x;
+      if (k < tot) sk[k] = tmp[r];
+    }
+  }
   __syncthreads();
   const K* A = sk;
   const K* B = sk + nal;

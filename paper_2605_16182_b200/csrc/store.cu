@@ -455,23 +455,64 @@ void sort_canonical(Ctx& ctx, const u32* src_i, const u32* dst_i, const i64* t, 
   }
 }
 
-// ts_off / ts_time from the canonical time column (edge_store.cpp:91-98)
+namespace {
+
+// ts view scatter (edge_store.cpp:91-98): group starts -> ts_off / ts_time
+struct TsScatter {
+  const i64* t;
+  u32* ts_off;
+  i64* ts_time;
+  __device__ __forceinline__ void operator()(u64 i, u64 g, u32 f) const {
+    if (f) {
+      ts_off[g] = static_cast<u32>(i);
+      ts_time[g] = t[i];
+    }
+  }
+};
+
+__global__ void k_ts_tail(const u64* Z, u64 m, u32* ts_off) { ts_off[*Z] = static_cast<u32>(m); }
+
+// node view scatter (edge_store.cpp:164-214): per-node timestamp-group
+// marks, and at every region start the (entry, group) offsets of the node
+// and of the empty-region nodes before it
+struct NodeViewScatter {
+  const u32* owner;
+  const Entry* ent;
+  i64* mk_time;
+  u32* mk_start;
+  uint2* nmeta;
+  __device__ __forceinline__ void operator()(u64 p, u64 g, u32 f) const {
+    if (!f) return;
+    mk_time[g] = ent[p].t;
+    mk_start[g] = static_cast<u32>(p);
+    if (p == 0 || owner[p] != owner[p - 1]) {
+      const u64 lo = p == 0 ? 0 : static_cast<u64>(owner[p - 1]) + 1;
+      for (u64 v = lo; v <= owner[p]; ++v) nmeta[v] = make_uint2(static_cast<u32>(p), static_cast<u32>(g));
+    }
+  }
+};
+
+__global__ void k_node_tail(const u32* owner, u64 P, u64 V, const u64* Q, uint2* nmeta) {
+  const u64 lo = P ? static_cast<u64>(owner[P - 1]) + 1 : 0;
+  const uint2 x = make_uint2(static_cast<u32>(P), static_cast<u32>(*Q));
+  for (u64 v = lo + blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v <= V;
+       v += static_cast<u64>(gridDim.x) * blockDim.x)
+    nmeta[v] = x;
+}
+
+}  // namespace
+
+// ts_off / ts_time from the canonical time column (edge_store.cpp:91-98).
+// One pass (flag + look-back scan + scatter); Z stays on the device in
+// ctx.d_scalars[16] until finish_node_view reads Z and Q together.
 void build_ts_view(Ctx& ctx, Store& s) {
   cudaStream_t st = ctx.stream;
   const u64 m = s.m;
-  u64 sc[1];
-  DevBuf<u32> gscan(m + 1, st);
-  exclusive_scan<u32>(ctx, TimeChangeFn{s.e_t.p}, m, gscan.p);
-  TWG_CUDA(cudaMemcpyAsync(ctx.d_scalars, gscan.p + m, sizeof(u32), cudaMemcpyDeviceToDevice, st));
-  TWG_CUDA(cudaMemsetAsync(reinterpret_cast<char*>(ctx.d_scalars) + 4, 0, 4, st));
-  read_scalars(ctx, ctx.d_scalars, sc, 1);
-  s.Z = sc[0];
-  s.ts_off.alloc(s.Z + 1, st);
-  s.ts_time.alloc(s.Z ? s.Z : 1, st);
-  if (m) {
-    k_ts_fill<<<grid(ctx, m), kBlock, 0, st>>>(s.e_t.p, gscan.p, m, s.ts_off.p, s.ts_time.p);
-    TWG_LAUNCHED(ctx);
-  }
+  s.ts_off.alloc(m + 1, st);
+  s.ts_time.alloc(m ? m : 1, st);
+  scan_scatter(ctx, TimeChangeFn{s.e_t.p}, m, ctx.d_scalars + 16, TsScatter{s.e_t.p, s.ts_off.p, s.ts_time.p});
+  k_ts_tail<<<1, 1, 0, st>>>(ctx.d_scalars + 16, m, s.ts_off.p);
+  TWG_LAUNCHED(ctx);
 }
 
 // Region bounds, timestamp-group marks and group offsets from the node-sorted
@@ -479,25 +520,18 @@ void build_ts_view(Ctx& ctx, Store& s) {
 void finish_node_view(Ctx& ctx, Store& s, BuildOpts opts) {
   cudaStream_t st = ctx.stream;
   const u64 P = s.P, V = s.V;
-  u64 sc[1];
   const u32* okp = s.owner.p;
   s.nmeta.alloc(V + 1, st);
-  k_region_bounds<<<grid(ctx, P + 1), kBlock, 0, st>>>(okp, P, V, s.nmeta.p);
+  s.mk_time.alloc(P ? P : 1, st);  // Q <= P
+  s.mk_start.alloc(P ? P : 1, st);
+  scan_scatter(ctx, GroupStartFn{okp, s.ent.p}, P, ctx.d_scalars + 17,
+               NodeViewScatter{okp, s.ent.p, s.mk_time.p, s.mk_start.p, s.nmeta.p});
+  k_node_tail<<<grid(ctx, V + 1), kBlock, 0, st>>>(okp, P, V, ctx.d_scalars + 17, s.nmeta.p);
   TWG_LAUNCHED(ctx);
-  DevBuf<u32> gscan(P + 1, st);
-  exclusive_scan<u32>(ctx, GroupStartFn{okp, s.ent.p}, P, gscan.p);
-  TWG_CUDA(cudaMemcpyAsync(ctx.d_scalars, gscan.p + P, sizeof(u32), cudaMemcpyDeviceToDevice, st));
-  TWG_CUDA(cudaMemsetAsync(reinterpret_cast<char*>(ctx.d_scalars) + 4, 0, 4, st));
-  read_scalars(ctx, ctx.d_scalars, sc, 1);
-  s.Q = sc[0];
-  s.mk_time.alloc(s.Q ? s.Q : 1, st);
-  s.mk_start.alloc(s.Q ? s.Q : 1, st);
-  if (P) {
-    k_marks<<<grid(ctx, P), kBlock, 0, st>>>(okp, s.ent.p, gscan.p, P, s.mk_time.p, s.mk_start.p);
-    TWG_LAUNCHED(ctx);
-  }
-  k_group_offsets<<<grid(ctx, V + 1), kBlock, 0, st>>>(gscan.p, P, V, s.nmeta.p);
-  TWG_LAUNCHED(ctx);
+  u64 zq[2];
+  read_scalars(ctx, ctx.d_scalars + 16, zq, 2);  // the build's one read-back of Z and Q
+  s.Z = zq[0];
+  s.Q = zq[1];
   s.has_weights = false;
   s.has_adjacency = false;
   if (opts.weights) ensure_weights(ctx, s);

@@ -274,7 +274,69 @@ struct SurvivingEntryFn {
 // New position of surviving edge i (0-based among survivors): survivors
 // before the first batch edge keep i (no batch edge precedes them) — for a
 // time-ordered stream that is all but the boundary tail, so the random
-// gather from spos is almost never issued.
+// gather from spos is almost never issued. Fused into the compaction scan.
+struct XScatter {
+  const Entry* ent;
+  const u32* owner;
+  u32 from;
+  const u32* o2n;
+  const u32* spos;
+  const u32* bpos;
+  u64 A, S;
+  u64* xkey;
+  u32* xnbr;
+  i64* xt;
+  __device__ __forceinline__ void operator()(u64 p, u64 k, u32 f) const {
+    if (!f) return;
+    const Entry e = ent[p];
+    const u64 i0 = A ? bpos[0] : S;
+    const u32 i = e.edge - from;
+    const u32 np = i < i0 ? i : spos[i];
+    xkey[k] = (static_cast<u64>(o2n[owner[p]]) << 32) | np;
+    xnbr[k] = o2n[e.nbr];
+    xt[k] = e.t;
+  }
+};
+
+// one 24-byte record per sorted batch edge, so the node-view entries of the
+// batch gather one sector instead of four
+struct BatchRec {
+  u32 pos;
+  u32 src;
+  u32 dst;
+  u32 pad;
+  i64 t;
+};
+
+__global__ void k_pack_batch_rec(const u32* s, const u32* d, const i64* t, const u32* bpos, u64 A, BatchRec* rec) {
+  for (u64 k = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; k < A;
+       k += static_cast<u64>(gridDim.x) * blockDim.x) {
+    BatchRec r;
+    r.pos = bpos[k];
+    r.src = s[k];
+    r.dst = d[k];
+    r.pad = 0;
+    r.t = t[k];
+    rec[k] = r;
+  }
+}
+
+__global__ void k_make_y_rec(const u32* owners, const u32* jidx, u64 P, int mode, const BatchRec* rec, u64* ykey,
+                             u32* ynbr, i64* yt) {
+  for (u64 q = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; q < P;
+       q += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const u32 j = jidx[q];
+    const BatchRec r = rec[mode == TWG_UNDIRECTED ? (j >> 1) : j];
+    u32 nbr;
+    if (mode == TWG_FORWARD) nbr = r.dst;
+    else if (mode == TWG_BACKWARD) nbr = r.src;
+    else nbr = (j & 1) ? r.src : r.dst;
+    ykey[q] = (static_cast<u64>(owners[q]) << 32) | r.pos;
+    ynbr[q] = nbr;
+    yt[q] = r.t;
+  }
+}
+
 __global__ void k_make_x(const Entry* ent, const u32* owner, u64 P, u32 from, const u32* xpos, const u32* o2n,
                          const u32* spos, const u32* bpos, u64 A, u64 S, u64* xkey, u32* xnbr, i64* xt) {
   const u64 i0 = A ? bpos[0] : S;
@@ -441,25 +503,24 @@ Store* ingest_streaming(Window& w, const i64* bs, const i64* bd, const i64* bt, 
 
   // 3. node view: surviving old entries (X) merged with the batch's entries (Y)
   const u64 Po = O.P;
-  DevBuf<u32> xpos(Po + 1, st);
-  exclusive_scan<u32>(ctx, SurvivingEntryFn{O.ent.p, static_cast<u32>(from)}, Po, xpos.p);
-  const u64 Xn = read_u32_total(ctx, xpos.p + Po);
+  const u64 sides = w.mode == TWG_UNDIRECTED ? 2 : 1;
+  const u64 Xn = Po - sides * from;  // every surviving edge keeps all of its entries
   DevBuf<u64> xkey(Xn ? Xn : 1, st);
   DevBuf<u32> xnbr(Xn ? Xn : 1, st);
   DevBuf<i64> xt(Xn ? Xn : 1, st);
   scratch += 20 * Xn;
-  if (Po) {
-    k_make_x<<<grid(ctx, Po), kBlock, 0, st>>>(O.ent.p, O.owner.p, Po, static_cast<u32>(from), xpos.p, o2n.p, spos.p,
-                                               bpos.p, A, S, xkey.p, xnbr.p, xt.p);
-    TWG_LAUNCHED(ctx);
-  }
-  xpos.release();
-  const u64 Yn = w.mode == TWG_UNDIRECTED ? 2 * A : A;
+  scan_scatter(ctx, SurvivingEntryFn{O.ent.p, static_cast<u32>(from)}, Po, ctx.d_scalars + 9,
+               XScatter{O.ent.p, O.owner.p, static_cast<u32>(from), o2n.p, spos.p, bpos.p, A, S, xkey.p, xnbr.p,
+                        xt.p});
+  const u64 Yn = sides * A;
   DevBuf<u64> ykey(Yn ? Yn : 1, st);
   DevBuf<u32> ynbr(Yn ? Yn : 1, st);
   DevBuf<i64> yt(Yn ? Yn : 1, st);
   scratch += 36 * Yn;
   if (Yn) {
+    DevBuf<BatchRec> rec(A, st);
+    k_pack_batch_rec<<<grid(ctx, A), kBlock, 0, st>>>(bS.p, bD.p, bT.p, bpos.p, A, rec.p);
+    TWG_LAUNCHED(ctx);
     DevBuf<u32> k0(Yn, st), k1(Yn, st), v0(Yn, st), v1(Yn, st);
     u32* kp = k0.p;
     u32* ka = k1.p;
@@ -468,7 +529,7 @@ Store* ingest_streaming(Window& w, const i64* bs, const i64* bd, const i64* bt, 
     k_batch_owner_keys<<<grid(ctx, Yn), kBlock, 0, st>>>(bS.p, bD.p, A, w.mode, kp, vp);
     TWG_LAUNCHED(ctx);
     radix_sort_pairs<u32>(ctx, &kp, &ka, &vp, &va, Yn, vb);
-    k_make_y<<<grid(ctx, Yn), kBlock, 0, st>>>(kp, vp, Yn, w.mode, bS.p, bD.p, bT.p, bpos.p, ykey.p, ynbr.p, yt.p);
+    k_make_y_rec<<<grid(ctx, Yn), kBlock, 0, st>>>(kp, vp, Yn, w.mode, rec.p, ykey.p, ynbr.p, yt.p);
     TWG_LAUNCHED(ctx);
   }
   s->P = Xn + Yn;
