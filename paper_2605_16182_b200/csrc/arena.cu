@@ -17,6 +17,7 @@ namespace {
 
 struct Arena {
   std::map<size_t, std::vector<void*>> free_lists;
+  std::unordered_map<void*, size_t> owned;  // live block -> its class
   size_t in_use = 0;
   size_t reserved = 0;
 };
@@ -67,12 +68,17 @@ void* arena_alloc(cudaStream_t s, size_t bytes) {
   Arena* a = find(s);
   const size_t c = size_class(bytes);
   if (a) {
-    auto it = a->free_lists.find(c);
-    if (it != a->free_lists.end() && !it->second.empty()) {
-      void* p = it->second.back();
-      it->second.pop_back();
-      a->in_use += c;
-      return p;
+    // smallest cached block of class in [c, 2c): batch-to-batch size jitter
+    // (a few more nodes or groups) must not trigger a fresh cudaMalloc,
+    // which synchronises the device
+    for (auto it = a->free_lists.lower_bound(c); it != a->free_lists.end() && it->first < 2 * c; ++it) {
+      if (!it->second.empty()) {
+        void* p = it->second.back();
+        it->second.pop_back();
+        a->in_use += it->first;
+        a->owned[p] = it->first;
+        return p;
+      }
     }
   }
   void* p = nullptr;
@@ -93,6 +99,7 @@ void* arena_alloc(cudaStream_t s, size_t bytes) {
   if (a) {
     a->in_use += c;
     a->reserved += c;
+    a->owned[p] = c;
   }
   return p;
 }
@@ -104,7 +111,9 @@ void arena_free(cudaStream_t s, void* p, size_t bytes) {
     cudaFree(p);
     return;
   }
-  const size_t c = size_class(bytes);
+  auto it = a->owned.find(p);
+  const size_t c = it != a->owned.end() ? it->second : size_class(bytes);
+  if (it != a->owned.end()) a->owned.erase(it);
   a->free_lists[c].push_back(p);
   a->in_use -= c;
 }

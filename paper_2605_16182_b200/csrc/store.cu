@@ -304,6 +304,17 @@ __global__ void k_node_weights(StoreView s, const double* exp_neg, double* wp) {
   }
 }
 
+// newest incident time per node (check-before-max: hub slots are hot)
+__global__ void k_node_last_t(const u32* s, const u32* d, const i64* t, u64 m, i64* last) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const i64 ti = t[i];
+    const u32 a = s[i], b = d[i];
+    if (last[a] < ti) atomicMax(reinterpret_cast<long long*>(last + a), static_cast<long long>(ti));
+    if (last[b] < ti) atomicMax(reinterpret_cast<long long*>(last + b), static_cast<long long>(ti));
+  }
+}
+
 __global__ void k_adj_keys(const u32* owners, const Entry* ent, u64 P, int vb, u64* keys) {
   for (u64 p = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; p < P;
        p += static_cast<u64>(gridDim.x) * blockDim.x) {
@@ -632,6 +643,10 @@ Store* build_store(Ctx& ctx, EdgesSoA in, int mode, BuildOpts opts, u64* scratch
   s->e_t.alloc(m, st);
   scratch += 24 * m;
   sort_canonical(ctx, src_i.p, dst_i.p, in.t, m, tmin, tmax, vb, s->e_src.p, s->e_dst.p, s->e_t.p);
+  s->last_t.alloc(V, st);
+  TWG_CUDA(cudaMemsetAsync(s->last_t.p, 0xff, s->last_t.bytes(), st));  // -1: before every (non-negative) time
+  k_node_last_t<<<grid(ctx, m), kBlock, 0, st>>>(src_i.p, dst_i.p, in.t, m, s->last_t.p);
+  TWG_LAUNCHED(ctx);
   src_i.release();
   dst_i.release();
 

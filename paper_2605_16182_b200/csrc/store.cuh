@@ -74,6 +74,7 @@ struct Store {
   DevBuf<double> wp;
   DevBuf<u32> adj_off, adj;
   DevBuf<u32> owner;  // owner node of each node-view entry (drives the next batch's merge)
+  DevBuf<i64> last_t; // newest incident edge time per node: v survives a cutoff c iff last_t[v] >= c
 
   StoreView view() const {
     return StoreView{mode,     m,         V,         Z,          P,         Q,       A,

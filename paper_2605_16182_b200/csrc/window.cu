@@ -153,27 +153,76 @@ __global__ void k_compact_batch(const i64* bs, const i64* bd, const i64* bt, u64
 
 // old nodes referenced by a surviving edge (check-before-write: hub slots are
 // hammered by many edges; a plain store from each would serialise in L2)
+// 4 survivors per thread per iteration: the id loads are independent, so a
+// thread keeps 8 alive-flag probes in flight instead of 2
 __global__ void k_flag_survivor_nodes(const u32* e_src, const u32* e_dst, u64 from, u64 m, u8* alive) {
-  for (u64 i = from + blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < m;
-       i += static_cast<u64>(gridDim.x) * blockDim.x) {
-    const u32 a = e_src[i], b = e_dst[i];
-    if (!alive[a]) alive[a] = 1;
-    if (!alive[b]) alive[b] = 1;
+  const u64 n = m - from;
+  const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+  for (u64 k = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; k < (n + 3) / 4; k += stride) {
+    u32 ids[8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const u64 i = from + 4 * k + j;
+      ids[2 * j] = i < m ? e_src[i] : 0xffffffffu;
+      ids[2 * j + 1] = i < m ? e_dst[i] : 0xffffffffu;
+    }
+    u8 seen[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) seen[j] = ids[j] != 0xffffffffu ? alive[ids[j]] : 1;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (!seen[j]) alive[ids[j]] = 1;
   }
 }
 
-__global__ void k_present_old(const u8* alive, const i64* ext, u64 V, u8* present, u64* max_id) {
-  u64 mx = 0;
+// old node v is an endpoint of a surviving edge iff its newest incident
+// edge is not evicted (all of v's edges are in the old window)
+__global__ void k_alive_from_last(const i64* last, u64 V, i64 cutoff, u8* alive) {
+  for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < V;
+       v += static_cast<u64>(gridDim.x) * blockDim.x)
+    alive[v] = last[v] >= cutoff ? 1 : 0;
+}
+
+__global__ void k_carry_last_t(const i64* old_last, const u8* alive, const u32* o2n, u64 V, i64* new_last) {
+  for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < V;
+       v += static_cast<u64>(gridDim.x) * blockDim.x)
+    if (alive[v]) new_last[o2n[v]] = old_last[v];
+}
+
+__global__ void k_batch_last_t(const u32* s, const u32* d, const i64* t, u64 m, i64* last) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const i64 ti = t[i];
+    if (last[s[i]] < ti) atomicMax(reinterpret_cast<long long*>(last + s[i]), static_cast<long long>(ti));
+    if (last[d[i]] < ti) atomicMax(reinterpret_cast<long long*>(last + d[i]), static_cast<long long>(ti));
+  }
+}
+
+// present[ext[v]] for the old nodes still referenced; counts them
+// (scal[0] max present id, scal[4] alive count)
+__global__ void k_present_old(const u8* alive, const i64* ext, u64 V, u8* present, u64* scal) {
+  u64 mx = 0, cnt = 0;
   for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < V;
        v += static_cast<u64>(gridDim.x) * blockDim.x) {
     if (alive[v]) {
       present[ext[v]] = 1;
       mx = max(mx, static_cast<u64>(ext[v]));
+      ++cnt;
     }
   }
-  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if ((threadIdx.x & 31) == 0 && mx) atomicMax(reinterpret_cast<unsigned long long*>(max_id), mx);
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (mx) atomicMax(reinterpret_cast<unsigned long long*>(scal), mx);
+    if (cnt) atomicAdd(reinterpret_cast<unsigned long long*>(scal + 4), cnt);
+  }
 }
+
+// old->new id: identity when the node set is unchanged (the common steady
+// state of a stream over a fixed population), then kernels skip the remap
+__device__ __forceinline__ u32 remap(const u32* o2n, u32 v) { return o2n ? o2n[v] : v; }
 
 __global__ void k_present_batch(const i64* bs, const i64* bd, const i64* bt, u64 n, i64 cutoff, u8* present,
                                 u64* max_id) {
@@ -236,7 +285,7 @@ struct SurvivorKey {
   u64 from;
   __device__ __forceinline__ K3 operator()(u64 i) const {
     const u64 p = from + i;
-    return K3{e_t[p], (static_cast<u64>(o2n[e_src[p]]) << 32) | o2n[e_dst[p]]};
+    return K3{e_t[p], (static_cast<u64>(remap(o2n, e_src[p])) << 32) | remap(o2n, e_dst[p])};
   }
 };
 
@@ -292,8 +341,8 @@ struct XScatter {
     const u64 i0 = A ? bpos[0] : S;
     const u32 i = e.edge - from;
     const u32 np = i < i0 ? i : spos[i];
-    xkey[k] = (static_cast<u64>(o2n[owner[p]]) << 32) | np;
-    xnbr[k] = o2n[e.nbr];
+    xkey[k] = (static_cast<u64>(remap(o2n, owner[p])) << 32) | np;
+    xnbr[k] = remap(o2n, e.nbr);
     xt[k] = e.t;
   }
 };
@@ -431,13 +480,13 @@ Store* ingest_streaming(Window& w, const i64* bs, const i64* bd, const i64* bt, 
   DevBuf<u8> present(R, st);
   DevBuf<u32> rank(R + 1, st);
   scratch += Vo + 5 * R;
-  if (Vo) TWG_CUDA(cudaMemsetAsync(alive.p, 0, Vo, st));
   TWG_CUDA(cudaMemsetAsync(present.p, 0, R, st));
   TWG_CUDA(cudaMemsetAsync(ctx.d_scalars + 6, 0, 8, st));
-  if (S) {
-    k_flag_survivor_nodes<<<grid(ctx, S), kBlock, 0, st>>>(O.e_src.p, O.e_dst.p, from, O.m, alive.p);
+  if (Vo) {  // O(V) instead of a pass over every survivor's endpoints
+    k_alive_from_last<<<grid(ctx, Vo), kBlock, 0, st>>>(O.last_t.p, Vo, cutoff, alive.p);
     TWG_LAUNCHED(ctx);
   }
+  TWG_CUDA(cudaMemsetAsync(ctx.d_scalars + 10, 0, 8, st));
   if (Vo) {
     k_present_old<<<grid(ctx, Vo), kBlock, 0, st>>>(alive.p, O.ext.p, Vo, present.p, ctx.d_scalars + 6);
     TWG_LAUNCHED(ctx);
@@ -449,10 +498,12 @@ Store* ingest_streaming(Window& w, const i64* bs, const i64* bd, const i64* bt, 
   exclusive_scan<u32>(ctx, U8Fn{present.p}, R, rank.p);
   TWG_CUDA(cudaMemsetAsync(ctx.d_scalars + 5, 0, 8, st));
   TWG_CUDA(cudaMemcpyAsync(ctx.d_scalars + 5, rank.p + R, 4, cudaMemcpyDeviceToDevice, st));
-  u64 sc[2];
-  read_scalars(ctx, ctx.d_scalars + 5, sc, 2);
+  u64 sc[6];
+  read_scalars(ctx, ctx.d_scalars + 5, sc, 6);
   const u64 Vn = sc[0];
   w.max_ext = static_cast<i64>(sc[1]);
+  // every old node survives and none is new <=> the ranks are unchanged
+  const bool identity = Vo > 0 && sc[5] == Vo && Vn == Vo;
 
   auto s = std::make_unique<Store>();
   s->ctx = &ctx;
@@ -462,10 +513,24 @@ Store* ingest_streaming(Window& w, const i64* bs, const i64* bd, const i64* bt, 
   s->ext.alloc(Vn ? Vn : 1, st);
   k_fill_ext_u8<<<grid(ctx, R), kBlock, 0, st>>>(present.p, rank.p, R, s->ext.p);
   TWG_LAUNCHED(ctx);
-  DevBuf<u32> o2n(Vo ? Vo : 1, st);
-  if (Vo) {
-    k_old_to_new<<<grid(ctx, Vo), kBlock, 0, st>>>(alive.p, O.ext.p, rank.p, Vo, o2n.p);
+  DevBuf<u32> o2n_buf;
+  const u32* o2n = nullptr;  // null = identity remap
+  if (Vo && !identity) {
+    o2n_buf.alloc(Vo, st);
+    k_old_to_new<<<grid(ctx, Vo), kBlock, 0, st>>>(alive.p, O.ext.p, rank.p, Vo, o2n_buf.p);
     TWG_LAUNCHED(ctx);
+    o2n = o2n_buf.p;
+  }
+  // newest incident time per new node: survivors carry theirs, the batch maxes in below
+  s->last_t.alloc(Vn ? Vn : 1, st);
+  if (identity) {
+    TWG_CUDA(cudaMemcpyAsync(s->last_t.p, O.last_t.p, Vn * sizeof(i64), cudaMemcpyDeviceToDevice, st));
+  } else {
+    TWG_CUDA(cudaMemsetAsync(s->last_t.p, 0xff, s->last_t.bytes(), st));
+    if (Vo) {
+      k_carry_last_t<<<grid(ctx, Vo), kBlock, 0, st>>>(O.last_t.p, alive.p, o2n, Vo, s->last_t.p);
+      TWG_LAUNCHED(ctx);
+    }
   }
   present.release();
   alive.release();
@@ -479,6 +544,8 @@ Store* ingest_streaming(Window& w, const i64* bs, const i64* bd, const i64* bt, 
   scratch += 32 * A;
   if (A) {
     k_batch_internal<<<grid(ctx, n), kBlock, 0, st>>>(bs, bd, bt, n, cutoff, pos, rank.p, bsi.p, bdi.p, btc.p);
+    TWG_LAUNCHED(ctx);
+    k_batch_last_t<<<grid(ctx, A), kBlock, 0, st>>>(bsi.p, bdi.p, btc.p, A, s->last_t.p);
     TWG_LAUNCHED(ctx);
     if (w.batch_shape == 0) {
       k_segment_sort<<<grid(ctx, A), kBlock, 0, st>>>(bsi.p, bdi.p, btc.p, A, bS.p, bD.p, bT.p);
@@ -497,7 +564,7 @@ Store* ingest_streaming(Window& w, const i64* bs, const i64* bd, const i64* bt, 
   s->e_t.alloc(s->m ? s->m : 1, st);
   DevBuf<u32> spos(S ? S : 1, st), bpos(A ? A : 1, st);
   scratch += 4 * (S + A);
-  merge_path<K3>(ctx, SurvivorKey{O.e_src.p, O.e_dst.p, O.e_t.p, o2n.p, from}, S, BatchKey{bS.p, bD.p, bT.p}, A,
+  merge_path<K3>(ctx, SurvivorKey{O.e_src.p, O.e_dst.p, O.e_t.p, o2n, from}, S, BatchKey{bS.p, bD.p, bT.p}, A,
                  CanonicalEmit{s->e_src.p, s->e_dst.p, s->e_t.p, spos.p, bpos.p});
   build_ts_view(ctx, *s);
 
@@ -510,7 +577,7 @@ Store* ingest_streaming(Window& w, const i64* bs, const i64* bd, const i64* bt, 
   DevBuf<i64> xt(Xn ? Xn : 1, st);
   scratch += 20 * Xn;
   scan_scatter(ctx, SurvivingEntryFn{O.ent.p, static_cast<u32>(from)}, Po, ctx.d_scalars + 9,
-               XScatter{O.ent.p, O.owner.p, static_cast<u32>(from), o2n.p, spos.p, bpos.p, A, S, xkey.p, xnbr.p,
+               XScatter{O.ent.p, O.owner.p, static_cast<u32>(from), o2n, spos.p, bpos.p, A, S, xkey.p, xnbr.p,
                         xt.p});
   const u64 Yn = sides * A;
   DevBuf<u64> ykey(Yn ? Yn : 1, st);

@@ -256,6 +256,19 @@ def test_window_time_ordered_batches(tw, co, span):
             assert_store(w.snapshot(), ed)
 
 
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_window_stable_node_set(tw, co, mode):
+    """Fixed small population: every batch after the first keeps the node set
+    (identity id remap fast path); bit-exact after every batch."""
+    batches = _stream_batches(31, 8, 3000, 20, 200, 100)
+    exp_stats, exp_dumps = co.window_run(batches, 300, mode, every=True)
+    w = tw.WindowManager(300, tw.DirectionMode(mode))
+    for b, ed in zip(batches, exp_dumps):
+        w.ingest_batch(b)
+        assert w.snapshot().node_count() == 20
+        assert_store(w.snapshot(), ed)
+
+
 def test_window_c2_replay_state(tw, co):
     """C2 shape: C1 edges sorted by time, 10 batches, Δ = span/3; every
     post-eviction snapshot bit-exact (weights included: exp-weight default)."""
