@@ -232,7 +232,9 @@ def run_ours(args, rank, world, local_rank):
     total_ms = ev[0].elapsed_time(ev[-1])
     ingest_ms = sum(ev[1 + 3 * k].elapsed_time(ev[2 + 3 * k]) for k in range(args.steps))
     walk_ms = sum(ev[2 + 3 * k].elapsed_time(ev[3 + 3 * k]) for k in range(args.steps))
-    del bufs
+    del bufs, buf, window  # the e2e pass builds its own window: free this one first
+    ctx.sync()
+    torch.cuda.empty_cache()
 
     def allmax(x):
         if world == 1:
@@ -263,6 +265,85 @@ def run_ours(args, rank, world, local_rank):
     return result, e2e, wl
 
 
+def run_e2e_pipelined(args, tw, ctx, wl, variant, walk_cfg):
+    """Single-GPU e2e through the C ABI with host buffers, as a streaming
+    consumer would drive it: batch k+1's H2D (twg_stage_batch, copy stream)
+    and batch k-1's compact walk D2H (download stream) overlap batch k's
+    ingest + walks. Every step's H2D and D2H happen inside the timed region.
+    Host batches are generated before timing into pinned memory (a stream
+    arrives already in host RAM; generating 50M edges on the host is slower
+    than the GPU step)."""
+    import ctypes as C
+
+    import psutil
+    import torch
+
+    lib = tw._abi.load()
+    B = wl.batch_edges
+    window = tw.WindowManager(wl.window, tw.DirectionMode.DirectedForward, weights=False, adjacency=False, ctx=ctx)
+    dev = [torch.empty(B, dtype=torch.int64, device="cuda") for _ in range(3)]
+    b = 0
+    for _ in range(wl.prefill):  # untimed prefill via the device generator
+        lib.twg_synth_stream_device(ctx.handle, wl.nodes, b * B, B, wl.seed, dev[0].data_ptr(), dev[1].data_ptr(),
+                                    dev[2].data_ptr())
+        window.ingest_batch_device(dev[0].data_ptr(), dev[1].data_ptr(), dev[2].data_ptr(), B, stats=False)
+        b += 1
+    del dev
+    n_steps = args.warmup + args.steps
+    budget = psutil.virtual_memory().available * 0.5
+    n_host = max(2, min(n_steps, int(budget // (B * 24))))
+    hosts = [torch.empty((B, 3), dtype=torch.int64, pin_memory=True) for _ in range(n_host)]
+    for i, h in enumerate(hosts):  # pre-generated input stream (untimed)
+        assert lib.twg_synth_stream_host(wl.nodes, (b + i) * B, B, wl.seed, C.c_void_p(h.data_ptr())) == 0
+    if n_host < n_steps:  # not enough host RAM for the whole run: reuse batches cyclically, times advance anyway
+        pass
+    cap = wl.walks * 8  # entries; grown if needed
+    outs = [[torch.empty(wl.walks + 1, dtype=torch.int64, pin_memory=True),
+             torch.empty(cap, dtype=torch.int64, pin_memory=True),
+             torch.empty(cap, dtype=torch.int64, pin_memory=True)] for _ in range(2)]
+    pending = [None, None]
+    hops, d2h = 0, 0
+    timed_hops = 0
+    t_start = None
+    assert lib.twg_stage_batch(ctx.handle, 0, C.c_void_p(hosts[0].data_ptr()), B) == 0
+    for k in range(n_steps):
+        if k == args.warmup:
+            ctx.sync()
+            for p in pending:
+                if p is not None:
+                    lib.twg_walkset_wait(p[0].handle)
+            t_start = time.perf_counter()
+            timed_hops, d2h = 0, 0
+        if k + 1 < n_steps:  # H2D of the next batch overlaps this step
+            assert lib.twg_stage_batch(ctx.handle, (k + 1) % 2, C.c_void_p(hosts[(k + 1) % n_host].data_ptr()), B) == 0
+        st = tw._abi.twg_batch_stats()
+        rc = lib.twg_window_ingest_staged(window.handle, k % 2, None)
+        assert rc == 0, lib.twg_last_error()
+        snap = window.snapshot()
+        wst = tw.WalkStats()
+        ws = tw.generate_walks(snap, walk_cfg(), variant=variant, stats=wst)
+        slot = k % 2
+        if pending[slot] is not None:  # the download two steps back must finish before its buffers are reused
+            lib.twg_walkset_wait(pending[slot][0].handle)
+            pending[slot] = None
+        total = C.c_uint64()
+        off, nodes, times = outs[slot]
+        rc = lib.twg_walkset_download_compact_async(ws.handle, C.c_void_p(off.data_ptr()), C.c_void_p(nodes.data_ptr()),
+                                                    C.c_void_p(times.data_ptr()), nodes.numel(), C.byref(total))
+        assert rc == 0, lib.twg_last_error()
+        pending[slot] = (ws, total.value)
+        timed_hops += wst.hops
+        d2h += 8 * (ws.walk_count + 1) + 16 * total.value
+        del snap
+    for p in pending:
+        if p is not None:
+            lib.twg_walkset_wait(p[0].handle)
+    ctx.sync()
+    total_s = time.perf_counter() - t_start
+    return dict(total_s=total_s, hops=timed_hops, edges=B * args.steps, h2d=B * 24, d2h=d2h / args.steps,
+                pipelined=True, host_batches=n_host)
+
+
 def run_e2e(args, tw, ctx, wl, rank, world, local_rank, variant, walk_cfg):
     import ctypes as C
 
@@ -270,6 +351,8 @@ def run_e2e(args, tw, ctx, wl, rank, world, local_rank, variant, walk_cfg):
     import torch
     import torch.distributed as dist
 
+    if world == 1:
+        return run_e2e_pipelined(args, tw, ctx, wl, variant, walk_cfg)
     lib = tw._abi.load()
     B = wl.batch_edges
     window = tw.WindowManager(wl.window, tw.DirectionMode.DirectedForward, weights=False, adjacency=False, ctx=ctx)
@@ -535,7 +618,12 @@ def main():
         if e2e:
             line["e2e"] = {"value": e2e["hops"] / e2e["total_s"], "unit": "walk steps/s",
                            "edges_per_s": e2e["edges"] / e2e["total_s"],
-                           "h2d_bytes_per_step": int(e2e["h2d"]), "d2h_bytes_per_step": int(e2e["d2h"])}
+                           "h2d_bytes_per_step": int(e2e["h2d"]), "d2h_bytes_per_step": int(e2e["d2h"]),
+                           "path": ("twg_stage_batch (pinned H2D, copy stream) -> twg_window_ingest_staged -> "
+                                    "twg_generate -> twg_walkset_download_compact_async (pinned D2H, download "
+                                    "stream); H2D/D2H of neighbouring batches overlap compute")
+                           if e2e.get("pipelined") else "twg_window_ingest (host batch) -> twg_generate -> "
+                                                        "twg_walkset_download_compact, serial per step"}
         if cpu:
             line["cpu_baseline"] = {"value": cpu.get("value"), "unit": "walk steps/s", "cores": cpu.get("cores"),
                                     "kind": cpu.get("kind"), "sample": cpu.get("sample"),

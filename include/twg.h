@@ -161,6 +161,15 @@ int twg_window_ingest(twg_window* w, const twg_edge* batch, uint64_t n, twg_batc
  * (then the call is fully asynchronous on the ctx stream). */
 int twg_window_ingest_device(twg_window* w, const int64_t* d_src, const int64_t* d_dst,
                              const int64_t* d_t, uint64_t n, twg_batch_stats* out);
+/* Streaming pipeline (double-buffered host ingest). twg_stage_batch enqueues
+ * the H2D copy of a host batch (pinned memory for real overlap) into device
+ * slot 0 or 1 on the ctx's copy stream and returns; twg_window_ingest_staged
+ * ingests a staged slot on the compute stream after its copy lands. Staging
+ * batch k+1 before ingesting batch k overlaps PCIe with the rebuild. The
+ * host buffer must stay untouched until the slot is re-staged or the ctx is
+ * synchronised. */
+int twg_stage_batch(twg_ctx* ctx, int slot, const twg_edge* batch, uint64_t n);
+int twg_window_ingest_staged(twg_window* w, int slot, twg_batch_stats* out);
 /* current snapshot (+1 reference; release with twg_store_release) */
 int twg_window_snapshot(twg_window* w, twg_store** out);
 int twg_window_bounds(twg_window* w, int64_t* lo, int64_t* hi);
@@ -227,6 +236,14 @@ int twg_walkset_download(twg_walkset* w, int64_t* nodes, int64_t* times, uint32_
  * sum(lengths) entries — only the recorded entries cross PCIe. */
 int twg_walkset_download_compact(twg_walkset* w, uint64_t* offsets, int64_t* nodes,
                                  int64_t* times);
+/* Asynchronous compact download: compaction on the compute stream, the D2H
+ * copies on the ctx's download stream (overlapping the next batch). Host
+ * buffers (pinned for real overlap) must hold `capacity` entries; *total
+ * receives the entry count. twg_walkset_wait blocks until the data landed
+ * (destroy also waits). */
+int twg_walkset_download_compact_async(twg_walkset* w, uint64_t* offsets, int64_t* nodes, int64_t* times,
+                                       uint64_t capacity, uint64_t* total_entries);
+int twg_walkset_wait(twg_walkset* w);
 /* Device views (valid until destroy). */
 int twg_walkset_device(twg_walkset* w, int64_t** d_nodes, int64_t** d_times,
                        uint32_t** d_lengths);

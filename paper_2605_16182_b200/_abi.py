@@ -93,6 +93,10 @@ SIGNATURES = {
     "twg_window_destroy": (I, [VP]),
     "twg_window_ingest": (I, [VP, VP, U64, C.POINTER(twg_batch_stats)]),
     "twg_window_ingest_device": (I, [VP, VP, VP, VP, U64, VP]),
+    "twg_stage_batch": (I, [VP, I, VP, U64]),
+    "twg_window_ingest_staged": (I, [VP, I, VP]),
+    "twg_walkset_download_compact_async": (I, [VP, VP, VP, VP, U64, C.POINTER(U64)]),
+    "twg_walkset_wait": (I, [VP]),
     "twg_window_snapshot": (I, [VP, PP]),
     "twg_window_bounds": (I, [VP, C.POINTER(I64), C.POINTER(I64)]),
     "twg_window_state": (I, [VP, C.POINTER(I64), C.POINTER(U64), C.POINTER(twg_batch_stats)]),

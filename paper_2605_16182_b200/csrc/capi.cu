@@ -171,8 +171,15 @@ int twg_ctx_create(int device, twg_ctx** out) {
       TWG_CUDA(cudaMalloc(&c.d_expm1, x.size() * sizeof(double)));
       TWG_CUDA(cudaMemcpy(c.d_exp_neg, e.data(), e.size() * sizeof(double), cudaMemcpyHostToDevice));
       TWG_CUDA(cudaMemcpy(c.d_expm1, x.data(), x.size() * sizeof(double), cudaMemcpyHostToDevice));
-      TWG_CUDA(cudaMallocHost(&c.h_pinned, 64 * sizeof(u64)));
+      TWG_CUDA(cudaHostAlloc(&c.h_pinned, 64 * sizeof(u64), cudaHostAllocMapped));
+      TWG_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c.d_mapped), c.h_pinned, 0));
       TWG_CUDA(cudaMalloc(&c.d_scalars, 64 * sizeof(u64)));
+      TWG_CUDA(cudaStreamCreateWithFlags(&c.h2d_stream, cudaStreamNonBlocking));
+      TWG_CUDA(cudaStreamCreateWithFlags(&c.d2h_stream, cudaStreamNonBlocking));
+      for (auto& sl : c.slots) {
+        TWG_CUDA(cudaEventCreateWithFlags(&sl.ready, cudaEventDisableTiming));
+        TWG_CUDA(cudaEventCreateWithFlags(&sl.consumed, cudaEventDisableTiming));
+      }
     } catch (...) {
       delete h;
       throw;
@@ -190,6 +197,15 @@ int twg_ctx_destroy(twg_ctx* ctx) {
     cudaFree(c.d_expm1);
     cudaFree(c.d_scalars);
     cudaFreeHost(c.h_pinned);
+    cudaStreamSynchronize(c.h2d_stream);
+    cudaStreamSynchronize(c.d2h_stream);
+    for (auto& sl : c.slots) {
+      if (sl.buf) cudaFree(sl.buf);
+      cudaEventDestroy(sl.ready);
+      cudaEventDestroy(sl.consumed);
+    }
+    cudaStreamDestroy(c.h2d_stream);
+    cudaStreamDestroy(c.d2h_stream);
     arena_unregister(c.stream);
     cudaStreamDestroy(c.stream);
     delete ctx;
@@ -432,6 +448,47 @@ int twg_window_ingest_device(twg_window* w, const int64_t* d_src, const int64_t*
   return guarded([&] { window_ingest(*w->w, d_src, d_dst, d_t, n, out); });
 }
 
+int twg_stage_batch(twg_ctx* ctx, int slot, const twg_edge* batch, uint64_t n) {
+  return guarded([&] {
+    require(slot == 0 || slot == 1, "twg_stage_batch: slot must be 0 or 1");
+    Ctx& c = ctx->c;
+    auto& sl = c.slots[slot];
+    if (n > sl.cap) {  // grow (rare): the slot's previous contents must be consumed first
+      TWG_CUDA(cudaEventSynchronize(sl.consumed));
+      TWG_CUDA(cudaStreamSynchronize(c.h2d_stream));
+      if (sl.buf) TWG_CUDA(cudaFree(sl.buf));
+      TWG_CUDA(cudaMalloc(&sl.buf, n * sizeof(twg_edge)));
+      sl.cap = n;
+    }
+    // never overwrite a slot the compute stream has not finished reading
+    TWG_CUDA(cudaStreamWaitEvent(c.h2d_stream, sl.consumed, 0));
+    if (n) TWG_CUDA(cudaMemcpyAsync(sl.buf, batch, n * sizeof(twg_edge), cudaMemcpyHostToDevice, c.h2d_stream));
+    TWG_CUDA(cudaEventRecord(sl.ready, c.h2d_stream));
+    sl.n = n;
+  });
+}
+
+int twg_window_ingest_staged(twg_window* w, int slot, twg_batch_stats* out) {
+  return guarded([&] {
+    require(slot == 0 || slot == 1, "twg_window_ingest_staged: slot must be 0 or 1");
+    Ctx& c = *w->w->ctx;
+    auto& sl = c.slots[slot];
+    const u64 n = sl.n;
+    TWG_CUDA(cudaStreamWaitEvent(c.stream, sl.ready, 0));
+    SoA soa;
+    soa.s.alloc(n ? n : 1, c.stream);
+    soa.d.alloc(n ? n : 1, c.stream);
+    soa.t.alloc(n ? n : 1, c.stream);
+    if (n) {
+      k_split_aos<<<grid_for(n, 256, c.sm_count * 16), 256, 0, c.stream>>>(static_cast<const twg_edge*>(sl.buf), n,
+                                                                           soa.s.p, soa.d.p, soa.t.p);
+      TWG_LAUNCHED(c);
+    }
+    TWG_CUDA(cudaEventRecord(sl.consumed, c.stream));
+    window_ingest(*w->w, soa.s.p, soa.d.p, soa.t.p, n, out);
+  });
+}
+
 int twg_window_snapshot(twg_window* w, twg_store** out) {
   return guarded([&] {
     w->w->store->refs.fetch_add(1);
@@ -511,6 +568,36 @@ int twg_walkset_download_compact(twg_walkset* w, uint64_t* offsets, int64_t* nod
     if (nodes) d2h(c, nodes, cn.p, total);
     if (times) d2h(c, times, ct.p, total);
     sync(c);
+  });
+}
+
+int twg_walkset_download_compact_async(twg_walkset* w, uint64_t* offsets, int64_t* nodes, int64_t* times,
+                                       uint64_t capacity, uint64_t* total_entries) {
+  return guarded([&] {
+    WalkSetDev& x = *w->w;
+    Ctx& c = *x.ctx;
+    if (x.d2h_done) TWG_CUDA(cudaEventSynchronize(x.d2h_done));  // a previous download still reads the buffers
+    u64 total = 0;
+    compact_walks(c, x, x.c_off, x.c_nodes, x.c_times, &total);
+    if (total_entries) *total_entries = total;
+    if (total > capacity) fail(TWG_EINVAL, "twg_walkset_download_compact_async: host capacity too small");
+    if (!x.d2h_done) TWG_CUDA(cudaEventCreateWithFlags(&x.d2h_done, cudaEventDisableTiming));
+    cudaEvent_t compacted;
+    TWG_CUDA(cudaEventCreateWithFlags(&compacted, cudaEventDisableTiming));
+    TWG_CUDA(cudaEventRecord(compacted, c.stream));
+    TWG_CUDA(cudaStreamWaitEvent(c.d2h_stream, compacted, 0));
+    cudaEventDestroy(compacted);
+    if (offsets)
+      TWG_CUDA(cudaMemcpyAsync(offsets, x.c_off.p, (x.count + 1) * 8, cudaMemcpyDeviceToHost, c.d2h_stream));
+    if (nodes && total) TWG_CUDA(cudaMemcpyAsync(nodes, x.c_nodes.p, total * 8, cudaMemcpyDeviceToHost, c.d2h_stream));
+    if (times && total) TWG_CUDA(cudaMemcpyAsync(times, x.c_times.p, total * 8, cudaMemcpyDeviceToHost, c.d2h_stream));
+    TWG_CUDA(cudaEventRecord(x.d2h_done, c.d2h_stream));
+  });
+}
+
+int twg_walkset_wait(twg_walkset* w) {
+  return guarded([&] {
+    if (w->w->d2h_done) TWG_CUDA(cudaEventSynchronize(w->w->d2h_done));
   });
 }
 

@@ -57,8 +57,21 @@ struct Ctx {
   double* d_exp_neg = nullptr;
   double* d_expm1 = nullptr;
   // pinned scratch for small device->host reads
-  u64* h_pinned = nullptr;
+  u64* h_pinned = nullptr;   // mapped pinned host scalars (see read_scalars)
+  u64* d_mapped = nullptr;   // device alias of h_pinned
   u64* d_scalars = nullptr;  // 64 u64 scratch scalars on the device
+  // Streaming pipeline: host batches are staged into device slots on a copy
+  // stream (H2D overlaps the compute stream) and walk downloads run on a D2H
+  // stream. Slot buffers are plain cudaMalloc (used across streams).
+  cudaStream_t h2d_stream = nullptr;
+  cudaStream_t d2h_stream = nullptr;
+  struct Slot {
+    void* buf = nullptr;
+    u64 cap = 0;  // edges
+    u64 n = 0;
+    cudaEvent_t ready = nullptr;     // H2D done
+    cudaEvent_t consumed = nullptr;  // compute stream finished reading it
+  } slots[2];
 };
 
 // Per-stream caching allocator (arena.cu). Every ctx owns one, keyed by its

@@ -348,10 +348,20 @@ unsigned grid(Ctx& ctx, u64 n) { return grid_for(n, kBlock, static_cast<unsigned
 
 }  // namespace
 
+namespace {
+__global__ void k_read_scalars(const u64* src, volatile u64* mapped, int n) {
+  if (static_cast<int>(threadIdx.x) < n) mapped[threadIdx.x] = src[threadIdx.x];
+}
+}  // namespace
+
+// Small device->host reads go through mapped pinned memory written by a
+// one-warp kernel: no copy engine is involved, so the read never queues
+// behind a multi-GB walk download running on the D2H engine.
 void read_scalars(Ctx& ctx, const u64* d_src, u64* host_dst, int n) {
-  TWG_CUDA(cudaMemcpyAsync(ctx.h_pinned, d_src, n * sizeof(u64), cudaMemcpyDeviceToHost, ctx.stream));
+  k_read_scalars<<<1, 64, 0, ctx.stream>>>(d_src, ctx.d_mapped, n);
+  TWG_LAUNCHED(ctx);
   TWG_CUDA(cudaStreamSynchronize(ctx.stream));
-  for (int i = 0; i < n; ++i) host_dst[i] = ctx.h_pinned[i];
+  for (int i = 0; i < n; ++i) host_dst[i] = reinterpret_cast<volatile u64*>(ctx.h_pinned)[i];
 }
 
 void ensure_weights(Ctx& ctx, Store& s) {

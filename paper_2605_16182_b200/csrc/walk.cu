@@ -892,9 +892,9 @@ WalkSetDev* generate_walks(Ctx& ctx, Store& s, const twg_walk_config& cfg, const
       k_classify<<<grid(ctx, n), kBlock, 0, st>>>(kp, n, s.view(), th, T);
       TWG_LAUNCHED(ctx);
       u32 cnt[8];
-      TWG_CUDA(cudaMemcpyAsync(ctx.h_pinned, counters.p, 8 * sizeof(u32), cudaMemcpyDeviceToHost, st));
-      TWG_CUDA(cudaStreamSynchronize(st));
-      std::memcpy(cnt, ctx.h_pinned, sizeof cnt);
+      u64 words[4];
+      read_scalars(ctx, reinterpret_cast<const u64*>(counters.p), words, 4);
+      std::memcpy(cnt, words, sizeof cnt);
       // tier counts (count_tier, walk_engine.cpp:157-169): split pieces count as multi_block
       for (int k = 0; k < 3; ++k) tiers[k] += cnt[k];
       tiers[3] += cnt[3] - cnt[5];

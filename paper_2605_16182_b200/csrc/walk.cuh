@@ -15,6 +15,16 @@ struct WalkSetDev {
   DevBuf<i64> times;   // [count * stride]
   DevBuf<u32> lengths; // [count]
   bool tails_zeroed = false;
+  // asynchronous compact download (twg_walkset_download_compact_async)
+  DevBuf<u64> c_off;
+  DevBuf<i64> c_nodes, c_times;
+  cudaEvent_t d2h_done = nullptr;
+  ~WalkSetDev() {
+    if (d2h_done) {
+      cudaEventSynchronize(d2h_done);  // the D2H stream may still read the compact buffers
+      cudaEventDestroy(d2h_done);
+    }
+  }
 };
 
 // Validates like walk_engine.cpp:189-206 / :366-370 (throws Error(TWG_EINVAL)).
