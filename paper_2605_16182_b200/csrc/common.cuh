@@ -6,6 +6,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -125,6 +126,46 @@ struct DevBuf {
   }
   size_t bytes() const { return n * sizeof(T); }
   T* get() const { return p; }
+};
+
+// Opt-in phase timing (TWG_PHASES=1): CUDA events on the ctx stream between
+// named phases, printed to stderr at the end of the scope. Zero cost when off.
+struct PhaseTimer {
+  Ctx& ctx;
+  const char* scope;
+  bool on;
+  int n = 0;
+  cudaEvent_t ev[48];
+  const char* name[48];
+  PhaseTimer(Ctx& c, const char* s) : ctx(c), scope(s) {
+    static const bool enabled = [] {
+      const char* e = std::getenv("TWG_PHASES");
+      return e && e[0] == '1';
+    }();
+    on = enabled;
+    mark("start");
+  }
+  void mark(const char* what) {
+    if (!on || n >= 48) return;
+    cudaEventCreate(&ev[n]);
+    cudaEventRecord(ev[n], ctx.stream);
+    name[n++] = what;
+  }
+  ~PhaseTimer() {
+    if (!on) return;
+    mark("end");
+    cudaEventSynchronize(ev[n - 1]);
+    std::fprintf(stderr, "[twg phases] %s:", scope);
+    float total = 0.f;
+    for (int i = 1; i < n; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+      total += ms;
+      std::fprintf(stderr, " %s=%.2f", name[i], ms);
+    }
+    std::fprintf(stderr, " | total=%.2f ms\n", total);
+    for (int i = 0; i < n; ++i) cudaEventDestroy(ev[i]);
+  }
 };
 
 inline int bit_width_u64(u64 x) {

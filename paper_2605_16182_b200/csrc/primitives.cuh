@@ -168,36 +168,47 @@ __global__ void __launch_bounds__(kSortBlock) k_radix_scatter(const K* __restric
   const u32 lanemask_lt = (1u << lane) - 1u;
   for (int b = threadIdx.x; b < kRadix; b += kSortBlock) running[b] = 0;
 
+  // Warp-private ranking: warp w owns the tile's items [w*256, (w+1)*256) in
+  // 8 rounds of 32 lanes, so its digit counters need no block barrier
+  // between rounds; one cross-warp scan per digit at the end.
   K key[kSortItems];
   u32 val[kSortItems];
   u32 rank[kSortItems];
+  for (int b = threadIdx.x; b < kWarps * kRadix; b += kSortBlock) (&wcount[0][0])[b] = 0;
+  __syncthreads();
+  const u64 wbase = base + static_cast<u64>(warp) * (32 * kSortItems);
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
-    const u64 i = base + static_cast<u64>(j) * kSortBlock + threadIdx.x;
+    const u64 i = wbase + static_cast<u64>(j) * 32 + lane;
     const bool valid = i < n;
     key[j] = valid ? keys_in[i] : K(0);
     val[j] = (valid && vals_in) ? vals_in[i] : 0u;
-    const u32 d = valid ? (static_cast<u32>(key[j] >> shift) & (kRadix - 1)) : (kRadix + lane);
-    for (int b = threadIdx.x; b < kWarps * kRadix; b += kSortBlock) (&wcount[0][0])[b] = 0;
-    __syncthreads();
-    const u32 peers = __match_any_sync(0xffffffffu, d);
-    const u32 r_in_warp = __popc(peers & lanemask_lt);
-    if (valid && r_in_warp == 0) wcount[warp][d] = __popc(peers);
-    __syncthreads();
-    for (int b = threadIdx.x; b < kRadix; b += kSortBlock) {
-      u32 acc = running[b];
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) {
-        const u32 c = wcount[w][b];
-        wcount[w][b] = acc;
-        acc += c;
-      }
-      running[b] = acc;
-    }
-    __syncthreads();
-    rank[j] = valid ? wcount[warp][d] + r_in_warp : 0u;
-    __syncthreads();
   }
+#pragma unroll
+  for (int j = 0; j < kSortItems; ++j) {
+    const u64 i = wbase + static_cast<u64>(j) * 32 + lane;
+    const bool valid = i < n;
+    const u32 d = valid ? (static_cast<u32>(key[j] >> shift) & (kRadix - 1)) : (kRadix + lane);
+    const u32 peers = __match_any_sync(0xffffffffu, d);
+    const u32 r_in_round = __popc(peers & lanemask_lt);
+    const u32 before = valid ? wcount[warp][d] : 0u;
+    __syncwarp();
+    if (valid && r_in_round == 0) wcount[warp][d] = before + __popc(peers);
+    __syncwarp();
+    rank[j] = before + r_in_round;
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < kRadix; b += kSortBlock) {  // per digit: exclusive scan across warps
+    u32 acc = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const u32 c = wcount[w][b];
+      wcount[w][b] = acc;
+      acc += c;
+    }
+    running[b] = acc;
+  }
+  __syncthreads();
   // digit starts inside the tile
   {
     u32 total;
@@ -208,10 +219,10 @@ __global__ void __launch_bounds__(kSortBlock) k_radix_scatter(const K* __restric
   __syncthreads();
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
-    const u64 i = base + static_cast<u64>(j) * kSortBlock + threadIdx.x;
+    const u64 i = wbase + static_cast<u64>(j) * 32 + lane;
     if (i < n) {
       const u32 d = static_cast<u32>(key[j] >> shift) & (kRadix - 1);
-      const u32 pos = tile_start[d] + rank[j];
+      const u32 pos = tile_start[d] + wcount[warp][d] + rank[j];
       skeys[pos] = key[j];
       if (vals_in) svals[pos] = val[j];
     }

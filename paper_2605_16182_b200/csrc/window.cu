@@ -347,6 +347,156 @@ struct XScatter {
   }
 };
 
+// ---- node view by placement (time-ordered append case) ---------------------------
+//
+// When the canonical merge is a concatenation, every batch entry of a node
+// follows all of its surviving entries, so the new region of v is
+// [survivors of v in old order | batch entries of v in position order].
+// Region sizes = old size - evicted entries + batch entries (two count
+// passes), one scan gives the new regions, survivors are written straight to
+// their final slots (no compaction scan, no merge), batch entries are placed
+// with per-node cursors and each node's (short) batch segment is re-sorted by
+// position. Falls back to the sort + merge route when a node receives more
+// than kYSegMax batch entries.
+constexpr u32 kYSegMax = 32;
+
+__device__ __forceinline__ u32 owner_of_side(int mode, u32 s, u32 d, int side) {
+  if (mode == TWG_UNDIRECTED) return side ? d : s;
+  return mode == TWG_BACKWARD ? d : s;
+}
+
+// warp-aggregated increment: lanes with the same key add once
+__device__ __forceinline__ void agg_inc(u32* cnt, u32 key, bool valid) {
+  const u32 peers = __match_any_sync(0xffffffffu, valid ? key : 0xffffffffu);
+  if (valid && (__ffs(peers) - 1) == static_cast<int>(threadIdx.x & 31)) atomicAdd(cnt + key, __popc(peers));
+}
+
+__global__ void k_count_evicted(const u32* e_src, const u32* e_dst, u64 from, int mode, u32* evicted) {
+  const int sides = mode == TWG_UNDIRECTED ? 2 : 1;
+  const u64 n = from * sides;
+  for (u64 j = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; j < ((n + 31) & ~31ull);
+       j += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const bool valid = j < n;
+    const u64 i = sides == 2 ? (j >> 1) : j;
+    const u32 o = valid ? owner_of_side(mode, e_src[i], e_dst[i], sides == 2 ? static_cast<int>(j & 1) : 0) : 0;
+    agg_inc(evicted, o, valid);
+  }
+}
+
+__global__ void k_count_y(const u32* s, const u32* d, u64 A, int mode, u32* ycnt) {
+  const int sides = mode == TWG_UNDIRECTED ? 2 : 1;
+  const u64 n = A * sides;
+  for (u64 j = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; j < ((n + 31) & ~31ull);
+       j += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const bool valid = j < n;
+    const u64 k = sides == 2 ? (j >> 1) : j;
+    const u32 o = valid ? owner_of_side(mode, s[k], d[k], sides == 2 ? static_cast<int>(j & 1) : 0) : 0;
+    agg_inc(ycnt, o, valid);
+  }
+}
+
+// new region sizes (surviving entries + batch entries) per new node; the
+// survivors' count is written at the NEW id; max batch segment -> scal[0]
+__global__ void k_region_sizes(const uint2* old_meta, const u32* evicted, const u8* alive_or_null, const u32* o2n,
+                               u64 Vo, u32* xcnt_new) {
+  for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < Vo;
+       v += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const u32 x = old_meta[v + 1].x - old_meta[v].x - evicted[v];
+    if (x) xcnt_new[remap(o2n, static_cast<u32>(v))] = x;
+  }
+}
+
+__global__ void k_cursor_init(const u32* new_off, const u32* xcnt, u64 V, u32* cursor) {
+  for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < V;
+       v += static_cast<u64>(gridDim.x) * blockDim.x)
+    cursor[v] = new_off[v] + xcnt[v];
+}
+
+struct SizeFn {
+  const u32* x;
+  const u32* y;
+  __device__ __forceinline__ u32 operator()(u64 v) const { return x[v] + y[v]; }
+};
+
+__global__ void k_max_u32(const u32* a, u64 n, u64* out) {
+  u32 m = 0;
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<u64>(gridDim.x) * blockDim.x)
+    m = max(m, a[i]);
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(reinterpret_cast<unsigned long long*>(out), static_cast<u64>(m));
+}
+
+// survivors straight to their final slots: slot = new_off[v'] + (p - first surviving entry of v)
+__global__ void k_place_x(const Entry* ent, const u32* owner, u64 Po, u32 from, const uint2* old_meta,
+                          const u32* evicted, const u32* o2n, const u32* new_off, Entry* out_ent, u32* out_owner) {
+  for (u64 p = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; p < Po;
+       p += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const Entry e = ent[p];
+    if (e.edge < from) continue;
+    const u32 v = owner[p];
+    const u32 vn = remap(o2n, v);
+    const u64 slot = new_off[vn] + (p - (old_meta[v].x + evicted[v]));
+    Entry x;
+    x.nbr = remap(o2n, e.nbr);
+    x.edge = e.edge - from;  // concatenation: survivors keep their index
+    x.t = e.t;
+    out_ent[slot] = x;
+    out_owner[slot] = vn;
+  }
+}
+
+// batch entries via per-node cursors (order fixed up by k_sort_y_segments)
+__global__ void k_place_y(const u32* s, const u32* d, const i64* t, u64 A, u64 S, int mode, u32* cursor, Entry* out_ent,
+                          u32* out_owner) {
+  const int sides = mode == TWG_UNDIRECTED ? 2 : 1;
+  const u64 n = A * sides;
+  for (u64 j = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; j < n;
+       j += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const u64 k = sides == 2 ? (j >> 1) : j;
+    const int side = sides == 2 ? static_cast<int>(j & 1) : 0;
+    const u32 o = owner_of_side(mode, s[k], d[k], side);
+    u32 nbr;
+    if (mode == TWG_FORWARD) nbr = d[k];
+    else if (mode == TWG_BACKWARD) nbr = s[k];
+    else nbr = side ? s[k] : d[k];
+    const u32 slot = atomicAdd(cursor + o, 1u);
+    Entry x;
+    x.nbr = nbr;
+    x.edge = static_cast<u32>(S + k);
+    x.t = t[k];
+    out_ent[slot] = x;
+    out_owner[slot] = o;
+  }
+}
+
+// each node's batch segment [new_off + xcnt, new_off + xcnt + ycnt) sorted by
+// (position, side) — the reference's entry order (edge_store.cpp:196-210)
+__global__ void k_sort_y_segments(const u32* new_off, const u32* xcnt, const u32* ycnt, u64 V, Entry* ent) {
+  for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < V;
+       v += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const u32 len = ycnt[v];
+    if (len < 2) continue;
+    Entry* seg = ent + new_off[v] + xcnt[v];
+    Entry buf[kYSegMax];
+    for (u32 i = 0; i < len; ++i) {
+      Entry x = seg[i];
+      u32 j = i;
+      // undirected self-loops give two identical entries: any order is equal content
+      while (j > 0 && buf[j - 1].edge > x.edge) {
+        buf[j] = buf[j - 1];
+        --j;
+      }
+      buf[j] = x;
+    }
+    for (u32 i = 0; i < len; ++i) seg[i] = buf[i];
+  }
+}
+
+struct BatchRec;
+__global__ void k_place_y_sorted(const u32* owners, const u32* jidx, u64 Yn, int mode, const BatchRec* rec,
+                                 const u32* new_off, const u32* xcnt, const u32* ystart, Entry* out_ent, u32* out_owner);
+
 // one 24-byte record per sorted batch edge, so the node-view entries of the
 // batch gather one sector instead of four
 struct BatchRec {
@@ -357,16 +507,55 @@ struct BatchRec {
   i64 t;
 };
 
-__global__ void k_pack_batch_rec(const u32* s, const u32* d, const i64* t, const u32* bpos, u64 A, BatchRec* rec) {
+// the canonical merge degenerates to a concatenation iff the first batch
+// edge does not sort before the last survivor (survivors first on ties)
+__global__ void k_concat_check(SurvivorKey ka, u64 S, BatchKey kb, u64* out) { *out = (kb(0) < ka(S - 1)) ? 0 : 1; }
+
+__global__ void k_copy_survivors(const u32* s, const u32* d, const i64* t, const u32* o2n, u64 n, u32* os, u32* od,
+                                 i64* ot) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    os[i] = remap(o2n, s[i]);
+    od[i] = remap(o2n, d[i]);
+    ot[i] = t[i];
+  }
+}
+
+__global__ void k_pack_batch_rec(const u32* s, const u32* d, const i64* t, const u32* bpos, u64 S, u64 A,
+                                 BatchRec* rec) {
   for (u64 k = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; k < A;
        k += static_cast<u64>(gridDim.x) * blockDim.x) {
     BatchRec r;
-    r.pos = bpos[k];
+    r.pos = bpos ? bpos[k] : static_cast<u32>(S + k);
     r.src = s[k];
     r.dst = d[k];
     r.pad = 0;
     r.t = t[k];
     rec[k] = r;
+  }
+}
+
+// batch entries (stable-sorted by owner) to their final slots: after the
+// node's survivors, in position order; consecutive q write consecutive slots
+__global__ void k_place_y_sorted(const u32* owners, const u32* jidx, u64 Yn, int mode, const BatchRec* rec,
+                                 const u32* new_off, const u32* xcnt, const u32* ystart, Entry* out_ent,
+                                 u32* out_owner) {
+  for (u64 q = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; q < Yn;
+       q += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const u32 o = owners[q];
+    const u32 j = jidx[q];
+    const BatchRec r = rec[mode == TWG_UNDIRECTED ? (j >> 1) : j];
+    u32 nbr;
+    if (mode == TWG_FORWARD) nbr = r.dst;
+    else if (mode == TWG_BACKWARD) nbr = r.src;
+    else nbr = (j & 1) ? r.src : r.dst;
+    const u64 slot = static_cast<u64>(new_off[o]) + xcnt[o] + (q - ystart[o]);
+    Entry x;
+    x.nbr = nbr;
+    x.edge = r.pos;
+    x.t = r.t;
+    out_ent[slot] = x;
+    out_owner[slot] = o;
   }
 }
 
@@ -474,6 +663,7 @@ Store* ingest_streaming(Window& w, const i64* bs, const i64* bd, const i64* bt, 
   const u64 S = O.m - from;
   const u64 Vo = O.V;
   u64 scratch = 0;
+  PhaseTimer pt(ctx, "ingest_streaming");
 
   // 1. new dense ids
   DevBuf<u8> alive(Vo ? Vo : 1, st);
@@ -559,34 +749,123 @@ Store* ingest_streaming(Window& w, const i64* bs, const i64* bd, const i64* bt, 
   bsi.release();
   bdi.release();
   btc.release();
+  pt.mark("ids+batch_sort");
   s->e_src.alloc(s->m ? s->m : 1, st);
   s->e_dst.alloc(s->m ? s->m : 1, st);
   s->e_t.alloc(s->m ? s->m : 1, st);
-  DevBuf<u32> spos(S ? S : 1, st), bpos(A ? A : 1, st);
-  scratch += 4 * (S + A);
-  merge_path<K3>(ctx, SurvivorKey{O.e_src.p, O.e_dst.p, O.e_t.p, o2n, from}, S, BatchKey{bS.p, bD.p, bT.p}, A,
-                 CanonicalEmit{s->e_src.p, s->e_dst.p, s->e_t.p, spos.p, bpos.p});
+  // A time-ordered stream appends: if the first batch edge does not sort
+  // before the last survivor, the merge is a concatenation (survivors keep
+  // their index, batch edge k lands at S + k) — two streaming copies instead
+  // of a merge-path pass.
+  bool concat = A == 0 || S == 0;
+  if (!concat) {
+    k_concat_check<<<1, 1, 0, st>>>(SurvivorKey{O.e_src.p, O.e_dst.p, O.e_t.p, o2n, from}, S, BatchKey{bS.p, bD.p, bT.p},
+                                    ctx.d_scalars + 11);
+    TWG_LAUNCHED(ctx);
+    u64 c[1];
+    read_scalars(ctx, ctx.d_scalars + 11, c, 1);
+    concat = c[0] != 0;
+  }
+  DevBuf<u32> spos, bpos;
+  if (concat) {
+    if (S) {
+      k_copy_survivors<<<grid(ctx, S), kBlock, 0, st>>>(O.e_src.p + from, O.e_dst.p + from, O.e_t.p + from, o2n, S,
+                                                        s->e_src.p, s->e_dst.p, s->e_t.p);
+      TWG_LAUNCHED(ctx);
+    }
+    if (A) {
+      k_copy_survivors<<<grid(ctx, A), kBlock, 0, st>>>(bS.p, bD.p, bT.p, nullptr, A, s->e_src.p + S, s->e_dst.p + S,
+                                                        s->e_t.p + S);
+      TWG_LAUNCHED(ctx);
+    }
+  } else {
+    spos.alloc(S ? S : 1, st);
+    bpos.alloc(A ? A : 1, st);
+    scratch += 4 * (S + A);
+    merge_path<K3>(ctx, SurvivorKey{O.e_src.p, O.e_dst.p, O.e_t.p, o2n, from}, S, BatchKey{bS.p, bD.p, bT.p}, A,
+                   CanonicalEmit{s->e_src.p, s->e_dst.p, s->e_t.p, spos.p, bpos.p});
+  }
+  pt.mark(concat ? "canonical_concat" : "canonical_merge");
   build_ts_view(ctx, *s);
+  pt.mark("ts_view");
 
   // 3. node view: surviving old entries (X) merged with the batch's entries (Y)
   const u64 Po = O.P;
   const u64 sides = w.mode == TWG_UNDIRECTED ? 2 : 1;
   const u64 Xn = Po - sides * from;  // every surviving edge keeps all of its entries
+  const u64 Yn = sides * A;
+  bool placed = false;
+  if (concat && Vn > 0) {
+    DevBuf<u32> evicted(Vo ? Vo : 1, st), ycnt(Vn, st), xcnt(Vn, st);
+    if (Vo) TWG_CUDA(cudaMemsetAsync(evicted.p, 0, Vo * 4, st));
+    TWG_CUDA(cudaMemsetAsync(ycnt.p, 0, Vn * 4, st));
+    TWG_CUDA(cudaMemsetAsync(xcnt.p, 0, Vn * 4, st));
+    TWG_CUDA(cudaMemsetAsync(ctx.d_scalars + 12, 0, 8, st));
+    if (from) {
+      k_count_evicted<<<grid(ctx, sides * from), kBlock, 0, st>>>(O.e_src.p, O.e_dst.p, from, w.mode, evicted.p);
+      TWG_LAUNCHED(ctx);
+    }
+    if (A) {
+      k_count_y<<<grid(ctx, Yn), kBlock, 0, st>>>(bS.p, bD.p, A, w.mode, ycnt.p);
+      TWG_LAUNCHED(ctx);
+    }
+    pt.mark("place_counts");
+    {
+      if (Vo) {
+        k_region_sizes<<<grid(ctx, Vo), kBlock, 0, st>>>(O.nmeta.p, evicted.p, nullptr, o2n, Vo, xcnt.p);
+        TWG_LAUNCHED(ctx);
+      }
+      DevBuf<u32> new_off(Vn + 1, st), ystart(Vn + 1, st);
+      exclusive_scan<u32>(ctx, SizeFn{xcnt.p, ycnt.p}, Vn, new_off.p);
+      s->P = Xn + Yn;
+      s->ent.alloc(s->P ? s->P : 1, st);
+      s->owner.alloc(s->P ? s->P : 1, st);
+      pt.mark("place_offsets");
+      if (Po) {
+        k_place_x<<<grid(ctx, Po), kBlock, 0, st>>>(O.ent.p, O.owner.p, Po, static_cast<u32>(from), O.nmeta.p,
+                                                    evicted.p, o2n, new_off.p, s->ent.p, s->owner.p);
+        TWG_LAUNCHED(ctx);
+      }
+      pt.mark("place_x");
+      if (Yn) {
+        // batch entries stable-sorted by owner: rank within owner = q - ystart[owner]
+        exclusive_scan<u32>(ctx, LoadFn<u32>{ycnt.p}, Vn, ystart.p);
+        DevBuf<BatchRec> rec(A, st);
+        k_pack_batch_rec<<<grid(ctx, A), kBlock, 0, st>>>(bS.p, bD.p, bT.p, nullptr, S, A, rec.p);
+        TWG_LAUNCHED(ctx);
+        DevBuf<u32> k0(Yn, st), k1(Yn, st), v0(Yn, st), v1(Yn, st);
+        u32* kp = k0.p;
+        u32* ka = k1.p;
+        u32* vp = v0.p;
+        u32* va = v1.p;
+        k_batch_owner_keys<<<grid(ctx, Yn), kBlock, 0, st>>>(bS.p, bD.p, A, w.mode, kp, vp);
+        TWG_LAUNCHED(ctx);
+        radix_sort_pairs<u32>(ctx, &kp, &ka, &vp, &va, Yn, vb);
+        pt.mark("place_y_sort");
+        k_place_y_sorted<<<grid(ctx, Yn), kBlock, 0, st>>>(kp, vp, Yn, w.mode, rec.p, new_off.p, xcnt.p, ystart.p,
+                                                           s->ent.p, s->owner.p);
+        TWG_LAUNCHED(ctx);
+      }
+      placed = true;
+      pt.mark("place_y");
+    }
+  }
+  if (!placed) {
   DevBuf<u64> xkey(Xn ? Xn : 1, st);
   DevBuf<u32> xnbr(Xn ? Xn : 1, st);
   DevBuf<i64> xt(Xn ? Xn : 1, st);
   scratch += 20 * Xn;
   scan_scatter(ctx, SurvivingEntryFn{O.ent.p, static_cast<u32>(from)}, Po, ctx.d_scalars + 9,
-               XScatter{O.ent.p, O.owner.p, static_cast<u32>(from), o2n, spos.p, bpos.p, A, S, xkey.p, xnbr.p,
-                        xt.p});
-  const u64 Yn = sides * A;
+               XScatter{O.ent.p, O.owner.p, static_cast<u32>(from), o2n, spos.p, concat ? nullptr : bpos.p,
+                        concat ? 0 : A, S, xkey.p, xnbr.p, xt.p});
+  pt.mark("node_x");
   DevBuf<u64> ykey(Yn ? Yn : 1, st);
   DevBuf<u32> ynbr(Yn ? Yn : 1, st);
   DevBuf<i64> yt(Yn ? Yn : 1, st);
   scratch += 36 * Yn;
   if (Yn) {
     DevBuf<BatchRec> rec(A, st);
-    k_pack_batch_rec<<<grid(ctx, A), kBlock, 0, st>>>(bS.p, bD.p, bT.p, bpos.p, A, rec.p);
+    k_pack_batch_rec<<<grid(ctx, A), kBlock, 0, st>>>(bS.p, bD.p, bT.p, concat ? nullptr : bpos.p, S, A, rec.p);
     TWG_LAUNCHED(ctx);
     DevBuf<u32> k0(Yn, st), k1(Yn, st), v0(Yn, st), v1(Yn, st);
     u32* kp = k0.p;
@@ -599,13 +878,17 @@ Store* ingest_streaming(Window& w, const i64* bs, const i64* bd, const i64* bt, 
     k_make_y_rec<<<grid(ctx, Yn), kBlock, 0, st>>>(kp, vp, Yn, w.mode, rec.p, ykey.p, ynbr.p, yt.p);
     TWG_LAUNCHED(ctx);
   }
+  pt.mark("node_y");
   s->P = Xn + Yn;
   s->ent.alloc(s->P ? s->P : 1, st);
   s->owner.alloc(s->P ? s->P : 1, st);
   merge_path<u64>(ctx, U64Key{xkey.p}, Xn, U64Key{ykey.p}, Yn,
                   EntryEmit{xnbr.p, xt.p, ynbr.p, yt.p, s->owner.p, s->ent.p});
+  pt.mark("node_merge");
+  }
   // 4. marks, offsets, optional views
   finish_node_view(ctx, *s, w.opts);
+  pt.mark("marks+views");
   if (scratch_out) *scratch_out = scratch;
   return s.release();
 }

@@ -248,7 +248,7 @@ def test_window_time_ordered_batches(tw, co, span):
     batches = []
     for e in _stream_batches(21, 8, 2000, 300, span, span // 2):
         batches.append(e[np.argsort(e[:, 2], kind="stable")])
-    for mode in (0, 2):
+    for mode in (0, 1, 2):
         exp_stats, exp_dumps = co.window_run(batches, span * 2, mode, every=True)
         w = tw.WindowManager(span * 2, tw.DirectionMode(mode))
         for b, ed in zip(batches, exp_dumps):
