@@ -210,19 +210,21 @@ def run_ours(args, rank, world, local_rank):
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3 * args.steps + 2)]
     hops = 0
     alg_bytes = 0
+    ingest_alg = 0
     ev[0].record(stream)
     for k in range(args.steps):
         bcast(bufs[k])
         ev[1 + 3 * k].record(stream)
-        window.ingest_batch_device(bufs[k][0].data_ptr(), bufs[k][1].data_ptr(), bufs[k][2].data_ptr(), B,
-                                   stats=False)
+        bst = window.ingest_batch_device(bufs[k][0].data_ptr(), bufs[k][1].data_ptr(), bufs[k][2].data_ptr(), B,
+                                         stats=True)
         ev[2 + 3 * k].record(stream)
         snap = window.snapshot()
         st = tw.WalkStats()
         ws = tw.generate_walks(snap, walk_cfg(), variant=variant, stats=st)
         ev[3 + 3 * k].record(stream)
         hops += st.hops
-        alg_bytes += st.alg_bytes if hasattr(st, "alg_bytes") else 0
+        alg_bytes += st.alg_bytes
+        ingest_alg += batch_alg_bytes(snap.info, bst, B)
         del ws, snap
     ev[-1].record(stream)
     ctx.sync()
@@ -256,7 +258,7 @@ def run_ours(args, rank, world, local_rank):
     hops_all = allsum(hops)
     edges_all = B * args.steps  # each batch ingested once (replicated on every GPU)
     result = dict(total_ms=total_ms, ingest_ms=ingest_ms, walk_ms=walk_ms, hops=hops_all, edges=edges_all,
-                  launches=launches, clocks=clk, alg_bytes=allsum(alg_bytes))
+                  launches=launches, clocks=clk, alg_bytes=allsum(alg_bytes), ingest_alg=ingest_alg)
 
     # ---- e2e pass through the C ABI with host buffers -----------------------------------
     e2e = None
@@ -541,6 +543,32 @@ def run_cpu(steps: int, warmup: int, which: str = "reference"):
 
 # --------------------------------------------------------------------------- main
 
+def batch_alg_bytes(info, bst, batch_edges, weights=False, adjacency=False) -> int:
+    """SURVEY §8(d) algorithmic bytes of one ingest: 24B (input triples) + 16S
+    (survivors read) + 32W (merged window written + read for the node view)
+    + 12P + 12Q + 12Z + 16V [+ 8P + 8Z weights] [+ 4P + 4V adjacency]."""
+    admitted = batch_edges - bst.dropped_late
+    W = int(info.edges)
+    S = W - admitted
+    P, Q, Z, V = int(info.entries), int(info.node_groups), int(info.ts_groups), int(info.nodes)
+    b = 24 * batch_edges + 16 * S + 32 * W + 12 * P + 12 * Q + 12 * Z + 16 * V
+    if weights:
+        b += 8 * P + 8 * Z
+    if adjacency:
+        b += 4 * P + 4 * V
+    return b
+
+
+def walk_traffic(kernel: str = "k_fullwalk"):
+    """DRAM bytes per launch of the walk kernel from the committed ncu --set
+    full capture (profiles/walk_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "walk_traffic.json")) as f:
+            return json.load(f).get(kernel)
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -608,10 +636,19 @@ def main():
                        "walk_ms_per_step": res["walk_ms"] / args.steps,
                        "ingest_edges_per_s": res["edges"] / (res["ingest_ms"] / 1000.0),
                        "walk_steps_per_s": res["hops"] / walk_s, "hops_per_step": res["hops"] / args.steps},
-            "roofline": {"bound": "hbm", "kernel": "k_fullwalk (walk phase)",
+            "roofline": {"bound": "hbm", "kernel": "k_fullwalk (one launch per step; CUDA events around twg_generate)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": (achieved / peak) if achieved else None, "traffic": None,
+                         "frac": (achieved / peak) if achieved else None,
+                         "traffic": walk_traffic() if args.scale == 1.0 and args.variant == "fullwalk" else None,
+                         "algorithmic_bytes_per_launch": alg / args.steps,
+                         "per_unit": "B_hop = 80 + 8*ceil(log2(G_v+1)) per hop + 24 per sampled start, summed on device",
                          "peak_source": peak_src},
+            "ingest_roofline": {"bound": "hbm", "scope": "whole ingest phase (twg_window_ingest_device)",
+                                "achieved": res["ingest_alg"] / (res["ingest_ms"] / 1000.0) / 1e9, "peak": peak,
+                                "unit": "GB/s",
+                                "frac": res["ingest_alg"] / (res["ingest_ms"] / 1000.0) / 1e9 / peak,
+                                "algorithmic_bytes_per_batch": res["ingest_alg"] / args.steps,
+                                "per_unit": "24B + 16S + 32W + 12P + 12Q + 12Z + 16V (SURVEY 8d)"},
             "gpu_launches": res["launches"],
             "clocks": res["clocks"],
         }
