@@ -244,7 +244,9 @@ int twg_walkset_download_compact(twg_walkset* w, uint64_t* offsets, int64_t* nod
 int twg_walkset_download_compact_async(twg_walkset* w, uint64_t* offsets, int64_t* nodes, int64_t* times,
                                        uint64_t capacity, uint64_t* total_entries);
 int twg_walkset_wait(twg_walkset* w);
-/* Device views (valid until destroy). */
+/* Device views (valid until destroy). The device layout is SLOT-MAJOR:
+ * cell (walk w, slot j) is at [j * walk_count + w]; slots >= lengths[w] are
+ * undefined. (The downloads above produce the walk-major images.) */
 int twg_walkset_device(twg_walkset* w, int64_t** d_nodes, int64_t** d_times,
                        uint32_t** d_lengths);
 

@@ -547,10 +547,11 @@ int twg_walkset_download(twg_walkset* w, int64_t* nodes, int64_t* times, uint32_
   return guarded([&] {
     WalkSetDev& x = *w->w;
     Ctx& c = *x.ctx;
-    if (nodes || times) zero_walk_tails(c, x);
     const u64 cells = x.count * x.stride;
-    if (nodes) d2h(c, nodes, x.nodes.p, cells);
-    if (times) d2h(c, times, x.times.p, cells);
+    DevBuf<i64> wn, wt;
+    if (nodes || times) walk_major_image(c, x, wn, wt);  // device layout is slot-major
+    if (nodes) d2h(c, nodes, wn.p, cells);
+    if (times) d2h(c, times, wt.p, cells);
     if (lengths) d2h(c, lengths, x.lengths.p, x.count);
     sync(c);
   });

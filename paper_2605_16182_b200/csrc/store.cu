@@ -643,6 +643,7 @@ Store* build_store(Ctx& ctx, EdgesSoA in, int mode, BuildOpts opts, u64* scratch
     TWG_LAUNCHED(ctx);
   }
   s->V = V;
+  s->ext_identity = V > 0 && V == max_id + 1;  // every id 0..max present: rank == id
 
   // 3. canonical (time, src, dst) order (edge_store.cpp:42-55)
   const int vb = V > 1 ? bit_width_u64(V - 1) : 0;

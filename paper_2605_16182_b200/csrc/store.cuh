@@ -49,6 +49,7 @@ struct StoreView {
   const double* wp;
   const u32* adj_off;
   const u32* adj;
+  int ext_identity;  // ext[v] == v for all v (the id map can be skipped)
 };
 
 struct BuildOpts {
@@ -62,6 +63,7 @@ struct Store {
   int mode = 0;
   u64 m = 0, V = 0, Z = 0, P = 0, Q = 0, A = 0;
   bool has_weights = false, has_adjacency = false;
+  bool ext_identity = false;
   DevBuf<u32> e_src, e_dst;
   DevBuf<i64> e_t, ext;
   DevBuf<u32> ts_off;
@@ -80,7 +82,7 @@ struct Store {
     return StoreView{mode,     m,         V,         Z,          P,         Q,       A,
                      e_src.p,  e_dst.p,   e_t.p,     ext.p,      ts_off.p,  ts_time.p,
                      ts_w.p,   nmeta.p,   mk_time.p, mk_start.p, ent.p,     wp.p,
-                     adj_off.p, adj.p};
+                     adj_off.p, adj.p,  ext_identity ? 1 : 0};
   }
   u64 device_bytes() const {
     return e_src.bytes() + e_dst.bytes() + e_t.bytes() + ext.bytes() + ts_off.bytes() +

@@ -42,11 +42,27 @@ struct WalkParams {
   double inv_p, inv_q, bmax;
   u32 stride;
   u64 walk_begin;
+  u64 count;        // walks in this output
+  int slot_major;   // device WalkSet layout: [slot][walk] (coalesced hop writes) vs [walk][slot]
   i64* nodes;
   i64* times;
   const double* exp_neg;
   const double* expm1_tab;
 };
+
+// Output cell of (local walk, slot). The device-resident WalkSet is
+// slot-major: the 32 lanes of a warp writing slot j of 32 consecutive walks
+// hit 256 contiguous bytes instead of 32 rows 640 bytes apart. The
+// reference's walk-major image is produced at download.
+__device__ __forceinline__ u64 out_index(const WalkParams& P, u64 wl, u32 slot) {
+  return P.slot_major ? static_cast<u64>(slot) * P.count + wl : wl * P.stride + slot;
+}
+
+// internal -> external id; skipped when the id map is the identity (the
+// snapshot holds exactly the ids 0..V-1, e.g. the C5 stream's population)
+__device__ __forceinline__ i64 ext_of(const StoreView& s, u32 v) {
+  return s.ext_identity ? static_cast<i64>(v) : s.ext[v];
+}
 
 // ---- per-hop pieces -------------------------------------------------------
 
@@ -168,8 +184,8 @@ __device__ __forceinline__ bool hop(const WalkParams& P, u64 wl, WalkReg& r, con
     idx = draw_index(P, u, lo, c, e, amb);
   }
   const Entry x = P.s.ent[c + idx];
-  const u64 slot = wl * P.stride + r.len;
-  P.nodes[slot] = P.s.ext[x.nbr];
+  const u64 slot = out_index(P, wl, r.len);
+  P.nodes[slot] = ext_of(P.s, x.nbr);
   P.times[slot] = x.t;
   r.len += 1;
   if (P.node2vec) {
@@ -209,12 +225,12 @@ struct InitParams {
 // seed_walk + init_walks (walk_engine.cpp:147-155, :247-279)
 __device__ __forceinline__ void init_walk(const WalkParams& P, const InitParams& I, u64 wl, WalkReg& r, Ctr* cn) {
   const u64 w = P.walk_begin + wl;
-  const u64 base = wl * P.stride;
+  const u64 base = out_index(P, wl, 0), base1 = out_index(P, wl, 1);
   r.prev = 0;
   r.has_prev = 0;
   if (I.start_mode == 0) {
     const u32 v = I.start_nodes[w / I.walks_per_node];
-    P.nodes[base] = P.s.ext[v];
+    P.nodes[base] = ext_of(P.s, v);
     P.times[base] = I.sentinel;
     r.cur = v;
     r.t = I.sentinel;
@@ -228,10 +244,10 @@ __device__ __forceinline__ void init_walk(const WalkParams& P, const InitParams&
     const i64 t = P.s.e_t[eidx];
     const u32 from = P.dir == 0 ? sv : dv;
     const u32 to = P.dir == 0 ? dv : sv;
-    P.nodes[base] = P.s.ext[from];
+    P.nodes[base] = ext_of(P.s, from);
     P.times[base] = I.sentinel;
-    P.nodes[base + 1] = P.s.ext[to];
-    P.times[base + 1] = t;
+    P.nodes[base1] = ext_of(P.s, to);
+    P.times[base1] = t;
     r.len = 2;
     r.cur = to;
     r.t = t;
@@ -528,16 +544,18 @@ __global__ void k_start_nodes(const u32* flags, const u32* pos, u64 V, u32* out)
     if (flags[v]) out[pos[v]] = static_cast<u32>(v);
 }
 
-__global__ void k_zero_tails(i64* nodes, i64* times, const u32* lengths, u64 count, u32 stride) {
+// slot-major device layout -> the reference's walk-major fixed-stride image
+// with zeroed unused slots (walk_engine.cpp:237-239)
+__global__ void k_to_walk_major(const i64* nodes, const i64* times, const u32* lengths, u64 count, u32 stride,
+                                i64* wn, i64* wt) {
   const u64 total = count * stride;
   for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<u64>(gridDim.x) * blockDim.x) {
     const u64 w = i / stride;
     const u32 slot = static_cast<u32>(i - w * stride);
-    if (slot >= lengths[w]) {
-      nodes[i] = 0;
-      times[i] = 0;
-    }
+    const bool used = slot < lengths[w];
+    wn[i] = used ? nodes[static_cast<u64>(slot) * count + w] : 0;
+    wt[i] = used ? times[static_cast<u64>(slot) * count + w] : 0;
   }
 }
 
@@ -546,22 +564,28 @@ struct LenFn {
   __device__ __forceinline__ u64 operator()(u64 i) const { return len[i]; }
 };
 
+// compact CSR image from the slot-major layout: thread per walk, reads of
+// slot j are coalesced across consecutive walks
 __global__ void k_compact_walks(const i64* nodes, const i64* times, const u32* lengths, const u64* offs, u64 count,
                                 u32 stride, i64* cn, i64* ct) {
   for (u64 w = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; w < count;
        w += static_cast<u64>(gridDim.x) * blockDim.x) {
     const u64 o = offs[w];
     for (u32 j = 0; j < lengths[w]; ++j) {
-      cn[o + j] = nodes[w * stride + j];
-      ct[o + j] = times[w * stride + j];
+      cn[o + j] = nodes[static_cast<u64>(j) * count + w];
+      ct[o + j] = times[static_cast<u64>(j) * count + w];
     }
   }
+  (void)stride;
 }
 
 unsigned grid(Ctx& ctx, u64 n) { return grid_for(n, kBlock, static_cast<unsigned>(ctx.sm_count) * 32); }
 
-WalkParams make_params(Ctx& ctx, Store& s, const twg_walk_config& cfg, u32 stride, u64 walk_begin, WalkSetDev& out) {
+WalkParams make_params(Ctx& ctx, Store& s, const twg_walk_config& cfg, u32 stride, u64 walk_begin, WalkSetDev& out,
+                       bool slot_major = false, u64 count = 0) {
   WalkParams P;
+  P.slot_major = slot_major ? 1 : 0;
+  P.count = count;
   P.s = s.view();
   P.rng = Rng::make(cfg.rng, cfg.seed);
   P.bias = cfg.bias;
@@ -755,12 +779,14 @@ void hop_walks_dev(Ctx& ctx, Store& s, const twg_walk_config& cfg, const u32* id
   TWG_CUDA(cudaStreamSynchronize(st));
 }
 
-void zero_walk_tails(Ctx& ctx, WalkSetDev& w) {
-  if (w.tails_zeroed || w.count == 0) return;
-  k_zero_tails<<<grid(ctx, w.count * w.stride), kBlock, 0, ctx.stream>>>(w.nodes.p, w.times.p, w.lengths.p, w.count,
-                                                                          w.stride);
+void walk_major_image(Ctx& ctx, const WalkSetDev& w, DevBuf<i64>& nodes, DevBuf<i64>& times) {
+  const u64 cells = w.count * w.stride;
+  nodes.alloc(cells ? cells : 1, ctx.stream);
+  times.alloc(cells ? cells : 1, ctx.stream);
+  if (!cells) return;
+  k_to_walk_major<<<grid(ctx, cells), kBlock, 0, ctx.stream>>>(w.nodes.p, w.times.p, w.lengths.p, w.count, w.stride,
+                                                                nodes.p, times.p);
   TWG_LAUNCHED(ctx);
-  w.tails_zeroed = true;
 }
 
 void compact_walks(Ctx& ctx, const WalkSetDev& w, DevBuf<u64>& offsets, DevBuf<i64>& nodes, DevBuf<i64>& times,
@@ -820,7 +846,7 @@ WalkSetDev* generate_walks(Ctx& ctx, Store& s, const twg_walk_config& cfg, const
 
   DevBuf<u64> stats(8, st);
   TWG_CUDA(cudaMemsetAsync(stats.p, 0, stats.bytes(), st));
-  WalkParams P = make_params(ctx, s, cfg, out->stride, wb, *out);
+  WalkParams P = make_params(ctx, s, cfg, out->stride, wb, *out, /*slot_major=*/true, count);
   InitParams I;
   I.start_mode = cfg.start_mode;
   I.walks_per_node = cfg.walks_per_node;

@@ -51,7 +51,7 @@ void hop_walks_dev(Ctx& ctx, Store& s, const twg_walk_config& cfg, const u32* id
 
 // zero the unused slots so the fixed-stride image equals the reference's
 // zero-initialised WalkSet (walk_engine.cpp:237-239)
-void zero_walk_tails(Ctx& ctx, WalkSetDev& w);
+void walk_major_image(Ctx& ctx, const WalkSetDev& w, DevBuf<i64>& nodes, DevBuf<i64>& times);
 
 // compact (CSR) image on the device: offsets[count+1], nodes/times[total]
 void compact_walks(Ctx& ctx, const WalkSetDev& w, DevBuf<u64>& offsets, DevBuf<i64>& nodes,

@@ -189,12 +189,38 @@ __global__ void k_carry_last_t(const i64* old_last, const u8* alive, const u32* 
     if (alive[v]) new_last[o2n[v]] = old_last[v];
 }
 
+// max-combine (node, t) pairs of a warp before touching memory: hub nodes
+// (dst = floor(N u^3) puts ~0.5% of a batch on node 0) otherwise serialise
+// in the L2 atomic unit
+// time_ordered: lanes hold non-decreasing times, so the highest peer lane
+// carries the group's max and is the only one to touch memory
+template <bool kTimeOrdered>
+__device__ __forceinline__ void agg_max(i64* last, u32 key, i64 t, bool valid) {
+  const u32 peers = __match_any_sync(0xffffffffu, valid ? key : 0xffffffffu);
+  i64 m = t;
+  int leader;
+  if (kTimeOrdered) {
+    leader = 31 - __clz(peers);
+  } else {
+#pragma unroll
+    for (int src = 0; src < 32; ++src) {
+      const i64 v = __shfl_sync(0xffffffffu, t, src);
+      if ((peers >> src) & 1u) m = v > m ? v : m;
+    }
+    leader = __ffs(peers) - 1;
+  }
+  if (valid && leader == static_cast<int>(threadIdx.x & 31) && last[key] < m)
+    atomicMax(reinterpret_cast<long long*>(last + key), static_cast<long long>(m));
+}
+
+template <bool kTimeOrdered>
 __global__ void k_batch_last_t(const u32* s, const u32* d, const i64* t, u64 m, i64* last) {
-  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < m;
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < ((m + 31) & ~31ull);
        i += static_cast<u64>(gridDim.x) * blockDim.x) {
-    const i64 ti = t[i];
-    if (last[s[i]] < ti) atomicMax(reinterpret_cast<long long*>(last + s[i]), static_cast<long long>(ti));
-    if (last[d[i]] < ti) atomicMax(reinterpret_cast<long long*>(last + d[i]), static_cast<long long>(ti));
+    const bool valid = i < m;
+    const i64 ti = valid ? t[i] : 0;
+    agg_max<kTimeOrdered>(last, valid ? s[i] : 0u, ti, valid);
+    agg_max<kTimeOrdered>(last, valid ? d[i] : 0u, ti, valid);
   }
 }
 
@@ -700,6 +726,7 @@ Store* ingest_streaming(Window& w, const i64* bs, const i64* bd, const i64* bt, 
   s->mode = w.mode;
   s->m = S + A;
   s->V = Vn;
+  s->ext_identity = Vn > 0 && w.max_ext >= 0 && static_cast<u64>(w.max_ext) == Vn - 1;
   s->ext.alloc(Vn ? Vn : 1, st);
   k_fill_ext_u8<<<grid(ctx, R), kBlock, 0, st>>>(present.p, rank.p, R, s->ext.p);
   TWG_LAUNCHED(ctx);
@@ -735,7 +762,10 @@ Store* ingest_streaming(Window& w, const i64* bs, const i64* bd, const i64* bt, 
   if (A) {
     k_batch_internal<<<grid(ctx, n), kBlock, 0, st>>>(bs, bd, bt, n, cutoff, pos, rank.p, bsi.p, bdi.p, btc.p);
     TWG_LAUNCHED(ctx);
-    k_batch_last_t<<<grid(ctx, A), kBlock, 0, st>>>(bsi.p, bdi.p, btc.p, A, s->last_t.p);
+    if ((w.batch_shape & 1u) == 0)  // admitted edges in time order
+      k_batch_last_t<true><<<grid(ctx, A), kBlock, 0, st>>>(bsi.p, bdi.p, btc.p, A, s->last_t.p);
+    else
+      k_batch_last_t<false><<<grid(ctx, A), kBlock, 0, st>>>(bsi.p, bdi.p, btc.p, A, s->last_t.p);
     TWG_LAUNCHED(ctx);
     if (w.batch_shape == 0) {
       k_segment_sort<<<grid(ctx, A), kBlock, 0, st>>>(bsi.p, bdi.p, btc.p, A, bS.p, bD.p, bT.p);
