@@ -114,7 +114,7 @@ typedef struct twg_store_info {
   int32_t mode;
   int32_t has_weights;
   int32_t has_adjacency;
-  int32_t _pad;
+  int32_t streaming;     /* 1: slice of the shared append log / node arena (time-ordered stream fast path) */
   uint64_t device_bytes; /* bytes held by the snapshot's device arrays */
 } twg_store_info;
 int twg_store_get_info(twg_store* s, twg_store_info* out);

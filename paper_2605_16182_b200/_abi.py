@@ -28,7 +28,7 @@ class twg_store_info(C.Structure):
         ("edges", C.c_uint64), ("nodes", C.c_uint64), ("ts_groups", C.c_uint64),
         ("entries", C.c_uint64), ("node_groups", C.c_uint64), ("adjacency", C.c_uint64),
         ("mode", C.c_int32), ("has_weights", C.c_int32), ("has_adjacency", C.c_int32),
-        ("_pad", C.c_int32), ("device_bytes", C.c_uint64),
+        ("streaming", C.c_int32), ("device_bytes", C.c_uint64),
     ]
 
 

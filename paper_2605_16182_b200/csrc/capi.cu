@@ -268,10 +268,13 @@ int twg_store_get_info(twg_store* h, twg_store_info* out) {
     i.ts_groups = s.Z;
     i.entries = s.P;
     i.node_groups = s.Q;
-    i.adjacency = s.has_adjacency ? s.A : 0;
+    // a streaming store's optional views live on its contiguous form
+    const Store& v = s.gapped && s.compact ? *s.compact : s;
+    i.adjacency = v.has_adjacency ? v.A : 0;
     i.mode = s.mode;
-    i.has_weights = s.has_weights;
-    i.has_adjacency = s.has_adjacency;
+    i.has_weights = v.has_weights;
+    i.has_adjacency = v.has_adjacency;
+    i.streaming = s.gapped ? 1 : 0;
     i.device_bytes = s.device_bytes();
     *out = i;
   });
@@ -302,7 +305,7 @@ __global__ void k_entry_field(const Entry* ent, u64 n, int which, u32* out) {
 
 int twg_store_download(twg_store* h, int field, void* dst) {
   return guarded([&] {
-    Store& s = *h->s;
+    Store& s = ensure_compact(*h->s->ctx, *h->s);  // reference layout for accessors
     Ctx& c = *s.ctx;
     cudaStream_t st = c.stream;
     const unsigned g = grid_for(s.P + s.m + s.V + 1, 256, c.sm_count * 16);
@@ -371,7 +374,7 @@ int twg_store_download(twg_store* h, int field, void* dst) {
 int twg_store_neighborhood(twg_store* h, const int64_t* v_ext, const int64_t* t, uint64_t n, int dir,
                            uint64_t* out3) {
   return guarded([&] {
-    Store& s = *h->s;
+    Store& s = ensure_compact(*h->s->ctx, *h->s);  // reference layout for accessors
     Ctx& c = *s.ctx;
     DevBuf<i64> dv, dt;
     h2d(c, dv, v_ext, n);
@@ -385,7 +388,7 @@ int twg_store_neighborhood(twg_store* h, const int64_t* v_ext, const int64_t* t,
 
 int twg_store_find_nodes(twg_store* h, const int64_t* v_ext, uint64_t n, uint32_t* internal, uint8_t* found) {
   return guarded([&] {
-    Store& s = *h->s;
+    Store& s = ensure_compact(*h->s->ctx, *h->s);  // reference layout for accessors
     Ctx& c = *s.ctx;
     DevBuf<i64> dv;
     h2d(c, dv, v_ext, n);
@@ -401,7 +404,7 @@ int twg_store_find_nodes(twg_store* h, const int64_t* v_ext, uint64_t n, uint32_
 int twg_store_adjacent(twg_store* h, const uint32_t* a, const uint32_t* b, uint64_t n, int temporal,
                        const int64_t* t, int dir, uint8_t* out) {
   return guarded([&] {
-    Store& s = *h->s;
+    Store& s = ensure_compact(*h->s->ctx, *h->s);  // reference layout for accessors
     Ctx& c = *s.ctx;
     for (u64 i = 0; i < n; ++i) require(a[i] < s.V && b[i] < s.V, "twg_store_adjacent: node id out of range");
     DevBuf<u32> da, db;
@@ -612,7 +615,7 @@ int twg_walkset_device(twg_walkset* w, int64_t** d_nodes, int64_t** d_times, uin
 
 int twg_sample_start_edges(twg_store* h, int bias, const double* u1, const double* u2, uint64_t n, uint64_t* out) {
   return guarded([&] {
-    Store& s = *h->s;
+    Store& s = ensure_compact(*h->s->ctx, *h->s);  // reference layout for accessors
     Ctx& c = *s.ctx;
     for (u64 i = 0; i < n; ++i)
       require(u1[i] >= 0.0 && u1[i] < 1.0 && u2[i] >= 0.0 && u2[i] < 1.0, "picker: u outside [0,1)");
@@ -630,7 +633,7 @@ int twg_schedule_step(twg_store* h, const uint32_t* node_of_walk, const uint8_t*
                       const twg_thresholds* thresholds, uint64_t* sizes5, uint32_t* rows, uint64_t cap,
                       uint32_t* walk_ids) {
   return guarded([&] {
-    Store& s = *h->s;
+    Store& s = ensure_compact(*h->s->ctx, *h->s);  // reference layout for accessors
     Ctx& c = *s.ctx;
     const twg_thresholds th = thresholds ? *thresholds : twg_thresholds{4, 256, 8192, 512, 4096};
     for (u64 i = 0; i < n; ++i) require(!alive[i] || node_of_walk[i] < s.V, "schedule_step: node id out of range");

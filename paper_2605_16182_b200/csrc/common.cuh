@@ -93,24 +93,33 @@ struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
   cudaStream_t s = nullptr;
+  bool own = true;  // false: a view into memory owned elsewhere (shared logs / arenas)
 
   DevBuf() = default;
   DevBuf(size_t count, cudaStream_t stream) { alloc(count, stream); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s), own(o.own) { o.p = nullptr; o.n = 0; o.own = true; }
   DevBuf& operator=(DevBuf&& o) noexcept {
     if (this != &o) {
       release();
-      p = o.p; n = o.n; s = o.s;
-      o.p = nullptr; o.n = 0;
+      p = o.p; n = o.n; s = o.s; own = o.own;
+      o.p = nullptr; o.n = 0; o.own = true;
     }
     return *this;
   }
   ~DevBuf() { release(); }
 
+  // non-owning view of count elements at q (the owner outlives this buffer)
+  void alias(T* q, size_t count) {
+    release();
+    p = q;
+    n = count;
+    own = false;
+  }
   void alloc(size_t count, cudaStream_t stream) {
     release();
+    own = true;
     s = stream;
     n = count;
     if (count) p = static_cast<T*>(arena_alloc(stream, count * sizeof(T)));
@@ -120,9 +129,10 @@ struct DevBuf {
     if (count > n || p == nullptr) alloc(count < 1 ? 1 : count, stream);
   }
   void release() {
-    if (p) arena_free(s, p, n * sizeof(T));
+    if (p && own) arena_free(s, p, n * sizeof(T));
     p = nullptr;
     n = 0;
+    own = true;
   }
   size_t bytes() const { return n * sizeof(T); }
   T* get() const { return p; }

@@ -115,7 +115,8 @@ __global__ void k_sample_start(StoreView s, int bias, const double* u1, const do
       case TWG_EXPINDEX: g = pick_exponential(u1[i], Z, expm1_tab, &amb); break;
       default: g = pick_weighted(u1[i], s.ts_w, Z); break;
     }
-    const u64 lo = s.ts_off[g], hi = s.ts_off[g + 1];
+    u64 lo, hi;
+    ts_group_range(s, g, lo, hi);
     u64 off = __double2ull_rz(__dmul_rn(u2[i], __ull2double_rn(hi - lo)));
     if (off >= hi - lo) off = hi - lo - 1;
     out[i] = lo + off;

@@ -366,6 +366,7 @@ void read_scalars(Ctx& ctx, const u64* d_src, u64* host_dst, int n) {
 
 void ensure_weights(Ctx& ctx, Store& s) {
   if (s.has_weights) return;
+  if (s.gapped) fail(TWG_ELOGIC, "ensure_weights: streaming store (use ensure_compact)");
   cudaStream_t st = ctx.stream;
   s.ts_w.alloc(s.Z ? s.Z : 1, st);
   TWG_CUDA(cudaMemsetAsync(s.ts_w.p, 0, s.ts_w.bytes(), st));
@@ -423,6 +424,59 @@ static void build_adjacency(Ctx& ctx, Store& s, const u32* owners) {
 }
 
 namespace {
+__global__ void k_nm_from_nmeta(const uint2* nmeta, u64 V, uint4* nm) {
+  for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < V;
+       v += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const uint2 a = nmeta[v], b = nmeta[v + 1];
+    nm[v] = make_uint4(a.x, b.x, a.y, b.y);
+  }
+}
+
+struct EntSizeFn {
+  const uint4* nm;
+  __device__ __forceinline__ u32 operator()(u64 v) const { return nm[v].y - nm[v].x; }
+};
+struct MarkSizeFn {
+  const uint4* nm;
+  __device__ __forceinline__ u32 operator()(u64 v) const { return nm[v].w - nm[v].z; }
+};
+
+__global__ void k_pack_nmeta(const u32* off, const u32* goff, u64 V, uint2* nmeta) {
+  for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v <= V;
+       v += static_cast<u64>(gridDim.x) * blockDim.x)
+    nmeta[v] = make_uint2(off[v], goff[v]);
+}
+
+__global__ void k_ts_rebase(const u32* ts_off, u64 Z, u32 seq0, u64 m, u32* out) {
+  for (u64 g = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; g <= Z;
+       g += static_cast<u64>(gridDim.x) * blockDim.x)
+    out[g] = g < Z ? ts_off[g] - seq0 : static_cast<u32>(m);
+}
+
+// gapped regions -> contiguous regions, one warp per node (lanes stride the
+// region): entries get snapshot-relative edge indices, marks contiguous
+// positions, and every entry its owner.
+__global__ void k_compact_regions(const uint4* nm, u64 V, const Entry* ent, const i64* mk_time, const u32* mk_start,
+                                  u32 seq0, const uint2* nmeta, Entry* ent_c, u32* owner_c, i64* mk_time_c,
+                                  u32* mk_start_c) {
+  const int lane = threadIdx.x & 31;
+  const u64 warps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
+  for (u64 v = (blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x) >> 5; v < V; v += warps) {
+    const uint4 r = nm[v];
+    const uint2 o = nmeta[v];
+    for (u32 i = lane; i < r.y - r.x; i += 32) {
+      Entry e = ent[r.x + i];
+      e.edge -= seq0;
+      ent_c[o.x + i] = e;
+      owner_c[o.x + i] = static_cast<u32>(v);
+    }
+    for (u32 i = lane; i < r.w - r.z; i += 32) {
+      mk_time_c[o.y + i] = mk_time[r.z + i];
+      mk_start_c[o.y + i] = mk_start[r.z + i] - r.x + o.x;
+    }
+  }
+}
+
 __global__ void k_entry_owners(const uint2* nmeta, u64 V, u32* owners) {
   for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < V;
        v += static_cast<u64>(gridDim.x) * blockDim.x) {
@@ -431,8 +485,71 @@ __global__ void k_entry_owners(const uint2* nmeta, u64 V, u32* owners) {
 }
 }  // namespace
 
+void build_nm(Ctx& ctx, Store& s) {
+  s.nm.alloc(s.V ? s.V : 1, ctx.stream);
+  if (s.V) {
+    k_nm_from_nmeta<<<grid(ctx, s.V), kBlock, 0, ctx.stream>>>(s.nmeta.p, s.V, s.nm.p);
+    TWG_LAUNCHED(ctx);
+  }
+}
+
+Store& ensure_compact(Ctx& ctx, const Store& g) {
+  if (!g.gapped) return const_cast<Store&>(g);
+  std::lock_guard<std::mutex> lock(g.compact_mu);
+  if (g.compact) return *g.compact;
+  cudaStream_t st = ctx.stream;
+  auto c = std::make_unique<Store>();
+  c->ctx = &ctx;
+  c->mode = g.mode;
+  c->m = g.m;
+  c->V = g.V;
+  c->Z = g.Z;
+  c->P = g.P;
+  c->ext_identity = g.ext_identity;
+  c->seq0 = 0;
+  c->e_src.alias(g.e_src.p, g.e_src.n);
+  c->e_dst.alias(g.e_dst.p, g.e_dst.n);
+  c->e_t.alias(g.e_t.p, g.e_t.n);
+  c->ext.alias(g.ext.p, g.ext.n);
+  c->last_t.alias(g.last_t.p, g.last_t.n);
+  c->ts_time.alias(g.ts_time.p, g.ts_time.n);
+  c->ts_off.alloc(g.Z + 1, st);
+  k_ts_rebase<<<grid(ctx, g.Z + 1), kBlock, 0, st>>>(g.ts_off.p, g.Z, g.seq0, g.m, c->ts_off.p);
+  TWG_LAUNCHED(ctx);
+  const u64 V = g.V;
+  DevBuf<u32> off(V + 1, st), goff(V + 1, st);
+  exclusive_scan<u32>(ctx, EntSizeFn{g.nm.p}, V, off.p);
+  exclusive_scan<u32>(ctx, MarkSizeFn{g.nm.p}, V, goff.p);
+  c->nmeta.alloc(V + 1, st);
+  k_pack_nmeta<<<grid(ctx, V + 1), kBlock, 0, st>>>(off.p, goff.p, V, c->nmeta.p);
+  TWG_LAUNCHED(ctx);
+  TWG_CUDA(cudaMemsetAsync(ctx.d_scalars + 18, 0, 16, st));
+  TWG_CUDA(cudaMemcpyAsync(ctx.d_scalars + 18, off.p + V, 4, cudaMemcpyDeviceToDevice, st));
+  TWG_CUDA(cudaMemcpyAsync(ctx.d_scalars + 19, goff.p + V, 4, cudaMemcpyDeviceToDevice, st));
+  u64 pq[2];
+  read_scalars(ctx, ctx.d_scalars + 18, pq, 2);
+  if (pq[0] != g.P) fail(TWG_ECUDA, "ensure_compact: region sizes do not add up to the entry count");
+  c->Q = pq[1];
+  c->ent.alloc(g.P ? g.P : 1, st);
+  c->owner.alloc(g.P ? g.P : 1, st);
+  c->mk_time.alloc(c->Q ? c->Q : 1, st);
+  c->mk_start.alloc(c->Q ? c->Q : 1, st);
+  if (V) {
+    k_compact_regions<<<grid(ctx, 32 * V), kBlock, 0, st>>>(g.nm.p, V, g.ent.p, g.mk_time.p, g.mk_start.p, g.seq0,
+                                                            c->nmeta.p, c->ent.p, c->owner.p, c->mk_time.p,
+                                                            c->mk_start.p);
+    TWG_LAUNCHED(ctx);
+  }
+  build_nm(ctx, *c);
+  c->has_weights = false;
+  c->has_adjacency = false;
+  g.compact = std::move(c);
+  return *g.compact;
+}
+
 void ensure_adjacency(Ctx& ctx, Store& s) {
   if (s.has_adjacency) return;
+  if (s.gapped) fail(TWG_ELOGIC, "ensure_adjacency: streaming store (use ensure_compact)");
   DevBuf<u32> owners(s.P ? s.P : 1, ctx.stream);
   if (s.P) {
     k_entry_owners<<<grid(ctx, s.V), kBlock, 0, ctx.stream>>>(s.nmeta.p, s.V, owners.p);
@@ -549,6 +666,7 @@ void finish_node_view(Ctx& ctx, Store& s, BuildOpts opts) {
                NodeViewScatter{okp, s.ent.p, s.mk_time.p, s.mk_start.p, s.nmeta.p});
   k_node_tail<<<grid(ctx, V + 1), kBlock, 0, st>>>(okp, P, V, ctx.d_scalars + 17, s.nmeta.p);
   TWG_LAUNCHED(ctx);
+  build_nm(ctx, s);
   u64 zq[2];
   read_scalars(ctx, ctx.d_scalars + 16, zq, 2);  // the build's one read-back of Z and Q
   s.Z = zq[0];
@@ -575,6 +693,8 @@ Store* build_store(Ctx& ctx, EdgesSoA in, int mode, BuildOpts opts, u64* scratch
   if (m == 0) {
     s->nmeta.alloc(1, st);
     TWG_CUDA(cudaMemsetAsync(s->nmeta.p, 0, sizeof(uint2), st));
+    s->nm.alloc(1, st);
+    TWG_CUDA(cudaMemsetAsync(s->nm.p, 0, sizeof(uint4), st));
     s->ts_off.alloc(1, st);
     TWG_CUDA(cudaMemsetAsync(s->ts_off.p, 0, sizeof(u32), st));
     s->adj_off.alloc(1, st);

@@ -19,6 +19,7 @@
 
 #include <atomic>
 #include <memory>
+#include <mutex>
 
 #include "common.cuh"
 
@@ -32,6 +33,12 @@ struct Entry {
 static_assert(sizeof(Entry) == 16, "Entry must be 16 bytes");
 
 // Raw pointers + counts of one snapshot, passed by value to kernels.
+//
+// Edge numbering: entry .edge fields and ts_off hold edge SEQUENCE numbers
+// (u32, wrapping); the snapshot's edge i has sequence seq0 + i. Contiguous
+// (built) stores have seq0 == 0, so the values are the reference's 0-based
+// indices; streaming stores share an append-only edge log whose numbering
+// runs across batches (store.cuh EdgeLog).
 struct StoreView {
   int mode;
   u64 m, V, Z, P, Q, A;
@@ -39,10 +46,11 @@ struct StoreView {
   const u32* e_dst;
   const i64* e_t;
   const i64* ext;
-  const u32* ts_off;
+  const u32* ts_off;   // group start sequence numbers, Z (+1 terminal in contiguous stores, unused)
   const i64* ts_time;
   const double* ts_w;
-  const uint2* nmeta;  // {entry offset, group offset}, V+1
+  const uint2* nmeta;  // {entry offset, group offset}, V+1 (contiguous stores only)
+  const uint4* nm;     // {entry begin, entry end, mark begin, mark end} per node (every store)
   const i64* mk_time;
   const u32* mk_start;
   const Entry* ent;
@@ -50,11 +58,56 @@ struct StoreView {
   const u32* adj_off;
   const u32* adj;
   int ext_identity;  // ext[v] == v for all v (the id map can be skipped)
+  u32 seq0;
 };
+
+// Edge range [lo, hi) (snapshot-relative) of timestamp group g < Z.
+__device__ __forceinline__ void ts_group_range(const StoreView& s, u64 g, u64& lo, u64& hi) {
+  lo = static_cast<u32>(s.ts_off[g] - s.seq0);
+  hi = g + 1 < s.Z ? static_cast<u64>(static_cast<u32>(s.ts_off[g + 1] - s.seq0)) : s.m;
+}
 
 struct BuildOpts {
   bool weights = true;
   bool adjacency = true;
+};
+
+// ---- streaming (append) representation ------------------------------------
+//
+// A time-ordered stream only ever appends to the window's newest end and
+// evicts from its oldest end, per node as well as globally. The streaming
+// snapshots therefore share two append-only structures instead of
+// rewriting the whole window every batch:
+//  * EdgeLog: the canonical edge columns and the timestamp-group view; a
+//    snapshot is a contiguous slice of it.
+//  * NodeArena: per-node regions with slack; node v's entries live in
+//    [eb, ee) and its timestamp marks in [gb, ge) (parallel arrays, the
+//    marks of a region never outgrow its entries), new entries are placed
+//    at ee, eviction advances eb/gb. A region that runs out of slack is
+//    relocated to fresh arena space; when the arena is exhausted the live
+//    regions are repacked into a new one.
+// Nothing a published snapshot can read is ever overwritten: writes go only
+// past every published snapshot's ends, and a replaced log/arena stays alive
+// (shared_ptr) while any snapshot references it.
+struct EdgeLog {
+  DevBuf<u32> src, dst;
+  DevBuf<i64> t;
+  DevBuf<u32> ts_off;  // group start sequence numbers
+  DevBuf<i64> ts_time;
+  u64 cap = 0;     // edges (and groups)
+  u64 len = 0;     // edges written
+  u64 zlen = 0;    // groups written
+  u32 seq0 = 0;    // sequence number of log index 0
+};
+
+struct NodeArena {
+  DevBuf<Entry> ent;
+  DevBuf<i64> mk_time;
+  DevBuf<u32> mk_start;
+  DevBuf<u32> rend;  // per node: end of its region's capacity (writer state)
+  u64 cap = 0;       // slots
+  u64 used = 0;      // bump pointer (host copy, updated after each ingest)
+  u64 V = 0;
 };
 
 struct Store {
@@ -77,17 +130,30 @@ struct Store {
   DevBuf<u32> adj_off, adj;
   DevBuf<u32> owner;  // owner node of each node-view entry (drives the next batch's merge)
   DevBuf<i64> last_t; // newest incident edge time per node: v survives a cutoff c iff last_t[v] >= c
+  DevBuf<uint4> nm;   // {eb, ee, gb, ge} per node: the walk kernels' node meta (every store)
+  u32 seq0 = 0;       // sequence number of edge 0 (StoreView)
+  // streaming representation (gapped == true): slices of a shared log/arena
+  bool gapped = false;
+  std::shared_ptr<EdgeLog> log;
+  std::shared_ptr<NodeArena> arena;
+  u64 log_first = 0;  // log index of edge 0
+  u64 ts_first = 0;   // log group index of group 0
+  // contiguous materialisation of a gapped store (reference layout), built on
+  // first use by the accessors / downloads / weighted views (ensure_compact)
+  mutable std::unique_ptr<Store> compact;
+  mutable std::mutex compact_mu;
 
   StoreView view() const {
-    return StoreView{mode,     m,         V,         Z,          P,         Q,       A,
+    return StoreView{mode,     m,         V,         Z,          P,         Q,        A,
                      e_src.p,  e_dst.p,   e_t.p,     ext.p,      ts_off.p,  ts_time.p,
-                     ts_w.p,   nmeta.p,   mk_time.p, mk_start.p, ent.p,     wp.p,
-                     adj_off.p, adj.p,  ext_identity ? 1 : 0};
+                     ts_w.p,   nmeta.p,   nm.p,      mk_time.p,  mk_start.p, ent.p,   wp.p,
+                     adj_off.p, adj.p,  ext_identity ? 1 : 0, seq0};
   }
   u64 device_bytes() const {
     return e_src.bytes() + e_dst.bytes() + e_t.bytes() + ext.bytes() + ts_off.bytes() +
            ts_time.bytes() + ts_w.bytes() + nmeta.bytes() + mk_time.bytes() + mk_start.bytes() +
-           ent.bytes() + wp.bytes() + adj_off.bytes() + adj.bytes() + owner.bytes();
+           ent.bytes() + wp.bytes() + adj_off.bytes() + adj.bytes() + owner.bytes() + nm.bytes() +
+           last_t.bytes();
   }
 };
 
@@ -116,6 +182,11 @@ Store* build_store(Ctx& ctx, EdgesSoA in, int mode, BuildOpts opts, u64* scratch
 // Lazily complete optional views.
 void ensure_weights(Ctx& ctx, Store& s);
 void ensure_adjacency(Ctx& ctx, Store& s);
+// nm from nmeta (contiguous stores)
+void build_nm(Ctx& ctx, Store& s);
+// The contiguous (reference-layout) form of s: s itself unless s is gapped,
+// else its lazily built contiguous copy (sharing the edge columns).
+Store& ensure_compact(Ctx& ctx, const Store& s);
 
 // Device binary-search helpers shared by the walk and query kernels.
 __device__ __forceinline__ u32 ub_i64(const i64* a, u32 lo, u32 hi, i64 x) {

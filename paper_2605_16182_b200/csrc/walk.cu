@@ -124,9 +124,9 @@ __device__ __forceinline__ bool adjacent(const StoreView& s, u32 a, u32 b) {
 
 // edge_store.cpp:316-323
 __device__ bool adjacent_after(const StoreView& s, u32 a, u32 b, i64 t, int dir) {
-  const uint2 na = s.nmeta[a], nb = s.nmeta[a + 1];
+  const uint4 na = s.nm[a];
   u32 c, e;
-  causal_slice(s.mk_time, s.mk_start, na.y, nb.y, na.x, nb.x, t, dir, c, e);
+  causal_slice(s.mk_time, s.mk_start, na.z, na.w, na.x, na.y, t, dir, c, e);
   for (u32 pos = c; pos < e; ++pos)
     if (s.ent[pos].nbr == b) return true;
   return false;
@@ -208,7 +208,8 @@ __device__ __forceinline__ u64 sample_start_edge_dev(const StoreView& s, int bia
     case TWG_EXPINDEX: g = pick_exponential(u1, Z, expm1_tab, amb); break;
     default: g = pick_weighted(u1, s.ts_w, Z); break;
   }
-  const u64 lo = s.ts_off[g], hi = s.ts_off[g + 1];
+  u64 lo, hi;
+  ts_group_range(s, g, lo, hi);
   u64 off = __double2ull_rz(__dmul_rn(u2, __ull2double_rn(hi - lo)));
   if (off >= hi - lo) off = hi - lo - 1;
   return lo + off;
@@ -300,8 +301,8 @@ __global__ void __launch_bounds__(kBlock) k_fullwalk(WalkParams P, InitParams I,
     init_walk(P, I, wl, r, &cn);
     init_len = r.len;
     while (r.len < P.stride) {
-      const uint2 a = P.s.nmeta[r.cur], b = P.s.nmeta[r.cur + 1];
-      if (!hop(P, wl, r, P.s.mk_time, P.s.mk_start, a.y, b.y, a.x, b.x, &cn)) break;
+      const uint4 a = P.s.nm[r.cur];
+      if (!hop(P, wl, r, P.s.mk_time, P.s.mk_start, a.z, a.w, a.x, a.y, &cn)) break;
     }
     lengths[wl] = r.len;
   }
@@ -398,7 +399,8 @@ __global__ void k_classify(const u32* keys, u64 n, StoreView s, twg_thresholds t
     }
     const u64 end = lo;
     const u32 W = static_cast<u32>(end - i);
-    const u32 G = s.nmeta[v + 1].y - s.nmeta[v].y;
+    const uint4 nv = s.nm[v];
+    const u32 G = nv.w - nv.z;
     int tier;
     u32 pieces = 1;
     if (W < th.w_warp) tier = 0;
@@ -452,9 +454,9 @@ __global__ void __launch_bounds__(kBlock) k_tier_solo(WalkParams P, StateArrays 
   Ctr amb{0, 0};
   for (u32 k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const Task task = tasks[k];
-    const uint2 a = P.s.nmeta[task.node], b = P.s.nmeta[task.node + 1];
+    const uint4 a = P.s.nm[task.node];
     for (u32 i = task.begin; i < task.end; ++i)
-      hop_member(P, S, ids[i], P.s.mk_time, P.s.mk_start, a.y, b.y, a.x, b.x, &amb);
+      hop_member(P, S, ids[i], P.s.mk_time, P.s.mk_start, a.z, a.w, a.x, a.y, &amb);
   }
   add_counters(stats, amb);
 }
@@ -473,20 +475,20 @@ __global__ void __launch_bounds__(kBlock) k_tier_warp(WalkParams P, StateArrays 
   Ctr amb{0, 0};
   for (u32 k = blockIdx.x * (kBlock / 32) + warp; k < n; k += gridDim.x * (kBlock / 32)) {
     const Task task = tasks[k];
-    const uint2 a = P.s.nmeta[task.node], b = P.s.nmeta[task.node + 1];
-    const u32 G = b.y - a.y;
+    const uint4 a = P.s.nm[task.node];
+    const u32 G = a.w - a.z;
     if (kCached && G <= cap) {
       for (u32 g = lane; g < G; g += 32) {
-        smt[g] = P.s.mk_time[a.y + g];
-        sms[g] = P.s.mk_start[a.y + g];
+        smt[g] = P.s.mk_time[a.z + g];
+        sms[g] = P.s.mk_start[a.z + g];
       }
       __syncwarp();
       for (u32 i = task.begin + lane; i < task.end; i += 32)
-        hop_member(P, S, ids[i], smt, sms, 0, G, a.x, b.x, &amb);
+        hop_member(P, S, ids[i], smt, sms, 0, G, a.x, a.y, &amb);
       __syncwarp();
     } else {
       for (u32 i = task.begin + lane; i < task.end; i += 32)
-        hop_member(P, S, ids[i], P.s.mk_time, P.s.mk_start, a.y, b.y, a.x, b.x, &amb);
+        hop_member(P, S, ids[i], P.s.mk_time, P.s.mk_start, a.z, a.w, a.x, a.y, &amb);
     }
   }
   add_counters(stats, amb);
@@ -505,20 +507,20 @@ __global__ void __launch_bounds__(kBlock) k_tier_block(WalkParams P, StateArrays
   Ctr amb{0, 0};
   for (u32 k = blockIdx.x; k < n; k += gridDim.x) {
     const Task task = tasks[k];
-    const uint2 a = P.s.nmeta[task.node], b = P.s.nmeta[task.node + 1];
-    const u32 G = b.y - a.y;
+    const uint4 a = P.s.nm[task.node];
+    const u32 G = a.w - a.z;
     if (kCached && G <= cap) {
       __syncthreads();
       for (u32 g = threadIdx.x; g < G; g += blockDim.x) {
-        smt[g] = P.s.mk_time[a.y + g];
-        sms[g] = P.s.mk_start[a.y + g];
+        smt[g] = P.s.mk_time[a.z + g];
+        sms[g] = P.s.mk_start[a.z + g];
       }
       __syncthreads();
       for (u32 i = task.begin + threadIdx.x; i < task.end; i += blockDim.x)
-        hop_member(P, S, ids[i], smt, sms, 0, G, a.x, b.x, &amb);
+        hop_member(P, S, ids[i], smt, sms, 0, G, a.x, a.y, &amb);
     } else {
       for (u32 i = task.begin + threadIdx.x; i < task.end; i += blockDim.x)
-        hop_member(P, S, ids[i], P.s.mk_time, P.s.mk_start, a.y, b.y, a.x, b.x, &amb);
+        hop_member(P, S, ids[i], P.s.mk_time, P.s.mk_start, a.z, a.w, a.x, a.y, &amb);
     }
   }
   add_counters(stats, amb);
@@ -532,10 +534,10 @@ __global__ void k_finalize(const StateArrays S, u64 count, u32* lengths, u64* st
   add_stats(stats, len, len, Ctr{0, 0}, active);
 }
 
-__global__ void k_start_flags(const uint2* nmeta, u64 V, u32* flags) {
+__global__ void k_start_flags(const uint4* nm, u64 V, u32* flags) {
   for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < V;
        v += static_cast<u64>(gridDim.x) * blockDim.x)
-    flags[v] = nmeta[v].x != nmeta[v + 1].x ? 1u : 0u;
+    flags[v] = nm[v].x != nm[v].y ? 1u : 0u;
 }
 
 __global__ void k_start_nodes(const u32* flags, const u32* pos, u64 V, u32* out) {
@@ -581,6 +583,16 @@ __global__ void k_compact_walks(const i64* nodes, const i64* times, const u32* l
 
 unsigned grid(Ctx& ctx, u64 n) { return grid_for(n, kBlock, static_cast<unsigned>(ctx.sm_count) * 32); }
 
+// The store a walk runs on: streaming (gapped) stores serve the index and
+// exponential-index pickers directly; the weight prefixes and the node2vec
+// adjacency are defined over the contiguous layout, so those configurations
+// run on the store's contiguous form.
+Store& walk_store(Ctx& ctx, Store& s, const twg_walk_config& cfg) {
+  const bool needs = cfg.bias == TWG_EXPWEIGHT || cfg.start_bias == TWG_EXPWEIGHT ||
+                     (cfg.node2vec && !cfg.temporal_adjacency);
+  return s.gapped && needs ? ensure_compact(ctx, s) : s;
+}
+
 WalkParams make_params(Ctx& ctx, Store& s, const twg_walk_config& cfg, u32 stride, u64 walk_begin, WalkSetDev& out,
                        bool slot_major = false, u64 count = 0) {
   WalkParams P;
@@ -617,7 +629,7 @@ void plan_starts(Ctx& ctx, Store& s, const twg_walk_config& cfg, u32* stride, u6
   if (cfg.start_mode == 0) {
     DevBuf<u32> flags(s.V ? s.V : 1, st), pos(s.V + 1, st);
     if (s.V) {
-      k_start_flags<<<grid(ctx, s.V), kBlock, 0, st>>>(s.nmeta.p, s.V, flags.p);
+      k_start_flags<<<grid(ctx, s.V), kBlock, 0, st>>>(s.nm.p, s.V, flags.p);
       TWG_LAUNCHED(ctx);
     }
     exclusive_scan<u32>(ctx, LoadFn<u32>{flags.p}, s.V, pos.p);
@@ -680,10 +692,10 @@ __global__ void k_hop_list(WalkParams P, StateArrays S, const u32* ids, u64 n, u
   for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<u64>(gridDim.x) * blockDim.x) {
     const u32 w = ids[i];
-    const uint2 a = P.s.nmeta[S.cur[w]], b = P.s.nmeta[S.cur[w] + 1];
+    const uint4 a = P.s.nm[S.cur[w]];
     WalkReg r;
     load_state(S, w, r);
-    const bool ok = hop(P, w, r, P.s.mk_time, P.s.mk_start, a.y, b.y, a.x, b.x, &cn);
+    const bool ok = hop(P, w, r, P.s.mk_time, P.s.mk_start, a.z, a.w, a.x, a.y, &cn);
     store_state(S, w, r, ok, P.stride);
   }
   add_counters(stats, cn);
@@ -691,9 +703,10 @@ __global__ void k_hop_list(WalkParams P, StateArrays S, const u32* ids, u64 n, u
 
 }  // namespace
 
-void init_walks_dev(Ctx& ctx, Store& s, const twg_walk_config& cfg, u32* stride, u64* walk_count,
+void init_walks_dev(Ctx& ctx, Store& s_in, const twg_walk_config& cfg, u32* stride, u64* walk_count,
                     const HostWalkArrays* out) {
   validate_config(cfg);
+  Store& s = walk_store(ctx, s_in, cfg);
   cudaStream_t st = ctx.stream;
   u64 total = 0;
   DevBuf<u32> start_nodes;
@@ -733,9 +746,10 @@ void init_walks_dev(Ctx& ctx, Store& s, const twg_walk_config& cfg, u32* stride,
   TWG_CUDA(cudaStreamSynchronize(st));
 }
 
-void hop_walks_dev(Ctx& ctx, Store& s, const twg_walk_config& cfg, const u32* ids, u64 n_ids, u64 count, u32 stride,
+void hop_walks_dev(Ctx& ctx, Store& s_in, const twg_walk_config& cfg, const u32* ids, u64 n_ids, u64 count, u32 stride,
                    const HostWalkArrays& io) {
   validate_config(cfg);
+  Store& s = walk_store(ctx, s_in, cfg);
   cudaStream_t st = ctx.stream;
   if (cfg.bias == TWG_EXPWEIGHT) ensure_weights(ctx, s);
   if (cfg.node2vec && !cfg.temporal_adjacency) ensure_adjacency(ctx, s);
@@ -805,8 +819,9 @@ void compact_walks(Ctx& ctx, const WalkSetDev& w, DevBuf<u64>& offsets, DevBuf<i
   }
 }
 
-WalkSetDev* generate_walks(Ctx& ctx, Store& s, const twg_walk_config& cfg, const twg_thresholds& th, int variant,
+WalkSetDev* generate_walks(Ctx& ctx, Store& s_in, const twg_walk_config& cfg, const twg_thresholds& th, int variant,
                            twg_walk_stats* stats_out) {
+  Store& s = walk_store(ctx, s_in, cfg);
   using clock = std::chrono::steady_clock;
   const auto started = clock::now();
   cudaStream_t st = ctx.stream;

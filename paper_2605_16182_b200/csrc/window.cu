@@ -685,9 +685,9 @@ Store* ingest_streaming(Window& w, const i64* bs, const i64* bd, const i64* bt, 
                         u64 A, u64 R, const u32* pos, u64* scratch_out) {
   Ctx& ctx = *w.ctx;
   cudaStream_t st = ctx.stream;
-  const Store& O = *w.store;
-  const u64 S = O.m - from;
-  const u64 Vo = O.V;
+  const Store& Og = *w.store;
+  const u64 S = Og.m - from;
+  const u64 Vo = Og.V;
   u64 scratch = 0;
   PhaseTimer pt(ctx, "ingest_streaming");
 
@@ -699,12 +699,12 @@ Store* ingest_streaming(Window& w, const i64* bs, const i64* bd, const i64* bt, 
   TWG_CUDA(cudaMemsetAsync(present.p, 0, R, st));
   TWG_CUDA(cudaMemsetAsync(ctx.d_scalars + 6, 0, 8, st));
   if (Vo) {  // O(V) instead of a pass over every survivor's endpoints
-    k_alive_from_last<<<grid(ctx, Vo), kBlock, 0, st>>>(O.last_t.p, Vo, cutoff, alive.p);
+    k_alive_from_last<<<grid(ctx, Vo), kBlock, 0, st>>>(Og.last_t.p, Vo, cutoff, alive.p);
     TWG_LAUNCHED(ctx);
   }
   TWG_CUDA(cudaMemsetAsync(ctx.d_scalars + 10, 0, 8, st));
   if (Vo) {
-    k_present_old<<<grid(ctx, Vo), kBlock, 0, st>>>(alive.p, O.ext.p, Vo, present.p, ctx.d_scalars + 6);
+    k_present_old<<<grid(ctx, Vo), kBlock, 0, st>>>(alive.p, Og.ext.p, Vo, present.p, ctx.d_scalars + 6);
     TWG_LAUNCHED(ctx);
   }
   if (A) {
@@ -734,18 +734,18 @@ Store* ingest_streaming(Window& w, const i64* bs, const i64* bd, const i64* bt, 
   const u32* o2n = nullptr;  // null = identity remap
   if (Vo && !identity) {
     o2n_buf.alloc(Vo, st);
-    k_old_to_new<<<grid(ctx, Vo), kBlock, 0, st>>>(alive.p, O.ext.p, rank.p, Vo, o2n_buf.p);
+    k_old_to_new<<<grid(ctx, Vo), kBlock, 0, st>>>(alive.p, Og.ext.p, rank.p, Vo, o2n_buf.p);
     TWG_LAUNCHED(ctx);
     o2n = o2n_buf.p;
   }
   // newest incident time per new node: survivors carry theirs, the batch maxes in below
   s->last_t.alloc(Vn ? Vn : 1, st);
   if (identity) {
-    TWG_CUDA(cudaMemcpyAsync(s->last_t.p, O.last_t.p, Vn * sizeof(i64), cudaMemcpyDeviceToDevice, st));
+    TWG_CUDA(cudaMemcpyAsync(s->last_t.p, Og.last_t.p, Vn * sizeof(i64), cudaMemcpyDeviceToDevice, st));
   } else {
     TWG_CUDA(cudaMemsetAsync(s->last_t.p, 0xff, s->last_t.bytes(), st));
     if (Vo) {
-      k_carry_last_t<<<grid(ctx, Vo), kBlock, 0, st>>>(O.last_t.p, alive.p, o2n, Vo, s->last_t.p);
+      k_carry_last_t<<<grid(ctx, Vo), kBlock, 0, st>>>(Og.last_t.p, alive.p, o2n, Vo, s->last_t.p);
       TWG_LAUNCHED(ctx);
     }
   }
@@ -780,22 +780,30 @@ Store* ingest_streaming(Window& w, const i64* bs, const i64* bd, const i64* bt, 
   bdi.release();
   btc.release();
   pt.mark("ids+batch_sort");
-  s->e_src.alloc(s->m ? s->m : 1, st);
-  s->e_dst.alloc(s->m ? s->m : 1, st);
-  s->e_t.alloc(s->m ? s->m : 1, st);
   // A time-ordered stream appends: if the first batch edge does not sort
   // before the last survivor, the merge is a concatenation (survivors keep
   // their index, batch edge k lands at S + k) — two streaming copies instead
   // of a merge-path pass.
   bool concat = A == 0 || S == 0;
   if (!concat) {
-    k_concat_check<<<1, 1, 0, st>>>(SurvivorKey{O.e_src.p, O.e_dst.p, O.e_t.p, o2n, from}, S, BatchKey{bS.p, bD.p, bT.p},
+    k_concat_check<<<1, 1, 0, st>>>(SurvivorKey{Og.e_src.p, Og.e_dst.p, Og.e_t.p, o2n, from}, S, BatchKey{bS.p, bD.p, bT.p},
                                     ctx.d_scalars + 11);
     TWG_LAUNCHED(ctx);
     u64 c[1];
     read_scalars(ctx, ctx.d_scalars + 11, c, 1);
     concat = c[0] != 0;
   }
+  // Time-ordered batch over an unchanged node population: append to the
+  // shared log / node arena instead of rewriting the window (append.cu).
+  if (concat && identity && A > 0 && append_ingest_enabled()) {
+    pt.mark("append_handoff");
+    if (scratch_out) *scratch_out = scratch + 48 * (w.mode == TWG_UNDIRECTED ? 2 * A : A) + 40 * Vn;
+    return ingest_append(w, Og, std::move(s), bS.p, bD.p, bT.p, A, from, cutoff);
+  }
+  const Store& O = ensure_compact(ctx, Og);  // the rewrite routes below read the contiguous node view
+  s->e_src.alloc(s->m ? s->m : 1, st);
+  s->e_dst.alloc(s->m ? s->m : 1, st);
+  s->e_t.alloc(s->m ? s->m : 1, st);
   DevBuf<u32> spos, bpos;
   if (concat) {
     if (S) {

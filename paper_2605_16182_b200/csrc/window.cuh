@@ -24,6 +24,13 @@ struct Window {
 
 void release_store(Store* s);
 
+// Streaming append ingest (append.cu): the time-ordered, stable-population
+// fast path. s carries the new snapshot's ids (ext, last_t, V); bS/bD/bT
+// is the admitted batch in canonical order with internal ids.
+bool append_ingest_enabled();
+Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const u32* bS, const u32* bD,
+                     const i64* bT, u64 A, u64 from, i64 cutoff);
+
 Window* window_create(Ctx& ctx, i64 duration, int mode, BuildOpts opts);
 void window_destroy(Window* w);
 // Device-resident SoA batch. stats may be null.

@@ -245,6 +245,11 @@ class EdgeStore:
     def node_count(self) -> int:
         return int(self.info.nodes)
 
+    def is_streaming(self) -> bool:
+        """True when the snapshot is a slice of the window's append log / node
+        arena (the time-ordered streaming fast path, csrc/append.cu)."""
+        return bool(self.info.streaming)
+
     def ts_group_count(self) -> int:
         return int(self.info.ts_groups)
 

@@ -1,0 +1,134 @@
+"""GPU parity of the streaming append ingest (csrc/append.cu): time-ordered
+batches over a stable node population take the shared log / node-arena
+path (the snapshot reports is_streaming()); after EVERY batch the whole
+dual index must equal the oracle's full rebuild of the same window
+(WindowManager::ingest_batch, window_manager.cpp:14-62 +
+EdgeStore::build, edge_store.cpp:27-254), including region relocation,
+arena repacks, equal-time batch boundaries and hub-sized regions, and
+walks on the streaming snapshots must equal the oracle's walks."""
+import numpy as np
+import pytest
+
+from oracle.py import Cfg
+from tests.test_gpu_parity import STORE_KEYS, assert_store, assert_walks, to_cfg
+
+pytestmark = pytest.mark.gpu
+
+
+def _ordered_stream(seed, nb, n, nodes, step, skew=False, tie_boundary=False):
+    """Time-ordered batches: batch b covers times [b*step, (b+1)*step). With
+    tie_boundary the first edge of every batch repeats the previous batch's
+    last time with the largest ids (so the canonical concatenation still
+    holds and the boundary groups/marks must merge)."""
+    rs = np.random.default_rng(seed)
+    out, last_t = [], None
+    for b in range(nb):
+        t = np.sort(b * step + rs.integers(0, step, n))
+        s = rs.integers(0, nodes, n)
+        if skew:
+            d = np.minimum((nodes * rs.random(n) ** 3).astype(np.int64), nodes - 1)
+        else:
+            d = rs.integers(0, nodes, n)
+        d[: n // 40] = s[: n // 40]  # self-loops
+        e = np.stack([s, d, t], 1)
+        e = e[np.lexsort((e[:, 1], e[:, 0], e[:, 2]))]
+        if tie_boundary and last_t is not None:
+            e[0] = (nodes - 1, nodes - 1, last_t)
+        last_t = int(e[-1, 2])
+        out.append(e)
+    return out
+
+
+def _run(tw, co, batches, duration, mode, check_walks=False):
+    exp_stats, exp_dumps = co.window_run(batches, duration, mode, every=True)
+    w = tw.WindowManager(duration, tw.DirectionMode(mode))
+    streaming = 0
+    for i, (b, (es, eb), ed) in enumerate(zip(batches, exp_stats, exp_dumps)):
+        st = w.ingest_batch(b)
+        assert (st.ingested, st.dropped_late, st.evicted, st.retained) == (
+            es["ingested"], es["dropped_late"], es["evicted"], es["retained"])
+        assert w.window_bounds() == eb
+        snap = w.snapshot()
+        streaming += snap.is_streaming()
+        assert_store(snap, ed)
+        if check_walks and i in (3, len(batches) - 1):
+            _check_walks(tw, co, snap, ed, mode)
+    return streaming
+
+
+def _check_walks(tw, co, snap, ed, mode):
+    edges = np.stack([ed["src_ext"], ed["dst_ext"], ed["t"]], 1)
+    dirs = [0, 1] if mode == 2 else [0 if mode == 0 else 1]
+    for direction in dirs:
+        for bias in (0, 1, 2, 3):
+            for start_mode in (0, 1):
+                c = Cfg(walk_length=12, start_mode=start_mode, walks_per_node=2, total_walks=700, bias=bias,
+                        start_bias=bias, direction=direction, seed=5)
+                exp, _ = co.generate(edges, mode, c)
+                # fresh handle each time: the weighted configurations run on
+                # the snapshot's contiguous form, the others on the slices
+                ws = tw.generate_walks(snap, to_cfg(tw, c))
+                assert_walks(ws, exp)
+        c = Cfg(walk_length=10, start_mode=1, total_walks=500, bias=3, start_bias=0, node2vec=1, p=0.5, q=2.0,
+                direction=direction, seed=9)
+        exp, _ = co.generate(edges, mode, c)
+        assert_walks(tw.generate_walks(snap, to_cfg(tw, c)), exp)
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_append_every_batch_bit_exact(tw, co, mode):
+    """14 batches over 200 nodes: relocations every few batches, arena
+    repacks; every snapshot after the first is a streaming one."""
+    batches = _ordered_stream(41 + mode, 14, 3000, 200, 100)
+    n = _run(tw, co, batches, 250, mode, check_walks=True)
+    assert n == len(batches) - 1
+
+
+@pytest.mark.parametrize("mode", [0, 2])
+def test_append_tie_boundary(tw, co, mode):
+    """Batch boundaries sharing a timestamp: the first batch group and the
+    first batch mark of a node merge with the survivors' last ones."""
+    batches = _ordered_stream(7, 10, 2000, 150, 60, tie_boundary=True)
+    n = _run(tw, co, batches, 150, mode)
+    assert n == len(batches) - 1
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_append_hub_regions(tw, co, mode):
+    """Skewed destinations (dst = N*u^3): the hub regions exceed the big-copy
+    threshold (2048 live entries), so relocations use the CTA-grid copy."""
+    batches = _ordered_stream(3, 8, 20000, 300, 1000, skew=True)
+    n = _run(tw, co, batches, 2500, mode)
+    assert n == len(batches) - 1
+
+
+def test_append_population_change_falls_back(tw, co):
+    """A node leaving the window (or a new one arriving) changes the dense
+    ids: that batch takes the rewrite route from the streaming snapshot's
+    contiguous form, the following ones resume appending."""
+    batches = _ordered_stream(5, 8, 2000, 100, 50)
+    # batch 4 introduces a brand-new node 1000
+    batches[4] = batches[4].copy()
+    batches[4][-1] = (1000, 3, batches[4][-1, 2])
+    exp_stats, exp_dumps = co.window_run(batches, 120, 0, every=True)
+    w = tw.WindowManager(120)
+    kinds = []
+    for b, ed in zip(batches, exp_dumps):
+        w.ingest_batch(b)
+        kinds.append(w.snapshot().is_streaming())
+        assert_store(w.snapshot(), ed)
+    assert kinds[4] is False and kinds[3] is True
+
+
+def test_append_held_snapshots_stay_valid(tw, co):
+    """The retired snapshot stays readable while the next batches append."""
+    batches = _ordered_stream(13, 6, 2000, 100, 50)
+    exp_stats, exp_dumps = co.window_run(batches, 120, 0, every=True)
+    w = tw.WindowManager(120)
+    snaps = []
+    for b in batches:
+        w.ingest_batch(b)
+        snaps.append(w.snapshot())
+    # every held snapshot (not only the current one) still reads back exactly
+    for s, ed in zip(snaps, exp_dumps):
+        assert_store(s, ed, keys=["src_ext", "dst_ext", "t", "ts_off", "n_off", "mk_time", "mk_start", "ref_edge"])
