@@ -32,8 +32,11 @@ namespace twg {
 namespace {
 
 constexpr int kBlock = 256;
-constexpr u32 kBigRegion = 2048;  // relocations larger than this get a CTA grid each
-constexpr u32 kSmallRun = 32;     // batch runs up to this length: placed by one thread per node
+constexpr int kPB = 256;           // nodes per bucket = threads per placement CTA
+constexpr u32 kBucketShift = 8;
+constexpr int kChunk = 1024;       // bucket entries staged per placement round
+constexpr int kChunkItems = kChunk / kPB;
+static_assert(kPB == 1 << kBucketShift, "one thread per bucket node");
 
 __device__ __forceinline__ u32 owner_of(int mode, const u32* s, const u32* d, u64 j) {
   if (mode == TWG_UNDIRECTED) return (j & 1) ? d[j >> 1] : s[j >> 1];
@@ -100,25 +103,16 @@ struct BatchGroupScatter {
 
 __global__ void k_zbase(u64 Z, const u64* g_cut, u64* out) { *out = Z - *g_cut; }
 
-// run bounds of the owner-sorted batch entries: [ystart[v], yend[v])
-__global__ void k_runs(const u32* keys, u64 Yn, u32* ystart, u32* yend) {
-  for (u64 q = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; q < Yn;
-       q += static_cast<u64>(gridDim.x) * blockDim.x) {
-    const u32 v = keys[q];
-    if (q == 0 || keys[q - 1] != v) ystart[v] = static_cast<u32>(q);
-    if (q + 1 == Yn || keys[q + 1] != v) yend[v] = static_cast<u32>(q + 1);
-  }
-}
-
-// first pos in [lo, hi) with ent[pos].t >= x, galloping from lo (eviction
-// removes a short prefix of most regions)
-__device__ __forceinline__ u32 gallop_ent(const Entry* e, u32 lo, u32 hi, i64 x) {
-  if (lo >= hi || e[lo].t >= x) return lo;
+// first logical x in [lo, hi) with time >= c, galloping from lo through
+// the node's ring (eviction removes a short prefix of most regions)
+template <class TimeAt>
+__device__ __forceinline__ u32 gallop_lb(TimeAt at, u32 lo, u32 hi, i64 c) {
+  if (lo >= hi || at(lo) >= c) return lo;
   u32 prev = lo, step = 1, bound = hi;
-  while (true) {  // e[prev].t < x
+  while (true) {  // at(prev) < c
     const u64 nx = static_cast<u64>(prev) + step;
     if (nx >= hi) break;
-    if (e[nx].t >= x) {
+    if (at(static_cast<u32>(nx)) >= c) {
       bound = static_cast<u32>(nx);
       break;
     }
@@ -128,134 +122,10 @@ __device__ __forceinline__ u32 gallop_ent(const Entry* e, u32 lo, u32 hi, i64 x)
   u32 a = prev + 1, b = bound;
   while (a < b) {
     const u32 mid = a + ((b - a) >> 1);
-    if (e[mid].t < x) a = mid + 1;
+    if (at(mid) < c) a = mid + 1;
     else b = mid;
   }
   return a;
-}
-
-__device__ __forceinline__ u32 gallop_time(const i64* t, u32 lo, u32 hi, i64 x) {
-  if (lo >= hi || t[lo] >= x) return lo;
-  u32 prev = lo, step = 1, bound = hi;
-  while (true) {
-    const u64 nx = static_cast<u64>(prev) + step;
-    if (nx >= hi) break;
-    if (t[nx] >= x) {
-      bound = static_cast<u32>(nx);
-      break;
-    }
-    prev = static_cast<u32>(nx);
-    step <<= 1;
-  }
-  u32 a = prev + 1, b = bound;
-  while (a < b) {
-    const u32 mid = a + ((b - a) >> 1);
-    if (t[mid] < x) a = mid + 1;
-    else b = mid;
-  }
-  return a;
-}
-
-struct Reloc {
-  u32 v, src_e, src_g, live, glive, dst;
-};
-
-// Per node: eviction bounds, room check, relocation plan. relocate_all ==
-// repack every region into a fresh arena (rend_old == nullptr).
-// scal: [0] bump (u64), [1] overflow flag, [2] relocations, [3] big relocations,
-//       [10] nodes with a long batch run, [11] their batch entries
-__global__ void __launch_bounds__(kBlock) k_plan(const uint4* onm, u64 V, const Entry* oent, const i64* omk_time,
-                                                 const u32* rend_old, const u32* ystart, const u32* yend, i64 cutoff,
-                                                 u64 cap, u32* rend_new, uint4* nm_new, u32* cur0, u32* gcur0,
-                                                 Reloc* list, Reloc* big, u32* bignodes, u64* scal) {
-  __shared__ u64 s_base;
-  __shared__ u32 s_lbase, s_bbase, s_nbase;
-  for (u64 base = static_cast<u64>(blockIdx.x) * kBlock; base < V; base += static_cast<u64>(gridDim.x) * kBlock) {
-    const u64 v = base + threadIdx.x;
-    const bool valid = v < V;
-    uint4 o = make_uint4(0, 0, 0, 0);
-    u32 y = 0, eb = 0, gb = 0, req = 0;
-    bool move = false;
-    if (valid) {
-      o = onm[v];
-      y = yend[v] - ystart[v];
-      eb = gallop_ent(oent, o.x, o.y, cutoff);
-      gb = gallop_time(omk_time, o.z, o.w, cutoff);
-      const u32 need = (o.y - eb) + y;
-      move = rend_old == nullptr || static_cast<u64>(o.y) + y > rend_old[v];
-      if (move) req = need + (need >> 1) + (need ? 2u : 0u);
-    }
-    const bool is_big = move && req && (o.y - eb) > kBigRegion;
-    const bool is_small = move && req && !is_big;
-    const bool is_long = y > kSmallRun;
-    u32 tot;
-    const u32 off = block_excl_scan<u32>(req, &tot);  // u32: one block's slack never overflows
-    u32 mtot;
-    const u32 midx = block_excl_scan<u32>(is_small ? 1u : 0u, &mtot);
-    u32 btot;
-    const u32 bidx = block_excl_scan<u32>(is_big ? 1u : 0u, &btot);
-    u32 ntot;
-    const u32 nidx = block_excl_scan<u32>(is_long ? 1u : 0u, &ntot);
-    u32 ytot;
-    block_excl_scan<u32>(is_long ? y : 0u, &ytot);
-    if (threadIdx.x == 0) {
-      s_base = tot ? atomicAdd(reinterpret_cast<unsigned long long*>(&scal[0]), static_cast<unsigned long long>(tot))
-                   : 0ull;
-      s_lbase = mtot ? atomicAdd(reinterpret_cast<unsigned int*>(&scal[2]), mtot) : 0u;
-      s_bbase = btot ? atomicAdd(reinterpret_cast<unsigned int*>(&scal[3]), btot) : 0u;
-      s_nbase = ntot ? atomicAdd(reinterpret_cast<unsigned int*>(&scal[10]), ntot) : 0u;
-      if (ytot) atomicAdd(reinterpret_cast<unsigned long long*>(&scal[11]), static_cast<unsigned long long>(ytot));
-    }
-    __syncthreads();
-    if (valid) {
-      const u32 live = o.y - eb, glive = o.w - gb;
-      if (is_long) bignodes[s_nbase + nidx] = static_cast<u32>(v);
-      if (!move) {
-        cur0[v] = o.y;
-        gcur0[v] = o.w;
-        nm_new[v] = make_uint4(eb, 0, gb, 0);
-      } else {
-        const u64 dst = s_base + off;
-        if (dst + req > cap) {
-          atomicOr(reinterpret_cast<unsigned long long*>(&scal[1]), 1ull);
-        } else {
-          const u32 d = static_cast<u32>(dst);
-          rend_new[v] = d + req;
-          cur0[v] = d + live;
-          gcur0[v] = d + glive;
-          nm_new[v] = make_uint4(d, 0, d, 0);
-          const Reloc r{static_cast<u32>(v), eb, gb, live, glive, d};
-          if (is_big) big[s_bbase + bidx] = r;
-          else if (is_small) list[s_lbase + midx] = r;
-        }
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// relocation copies: one warp per region (small), a CTA row per region (big)
-__device__ __forceinline__ void copy_region(const Reloc& r, u32 i0, u32 stride, const Entry* oent, const i64* omt,
-                                            const u32* oms, Entry* ent, i64* mt, u32* ms) {
-  for (u32 i = i0; i < r.live; i += stride) ent[r.dst + i] = oent[r.src_e + i];
-  for (u32 i = i0; i < r.glive; i += stride) {
-    mt[r.dst + i] = omt[r.src_g + i];
-    ms[r.dst + i] = oms[r.src_g + i] - r.src_e + r.dst;
-  }
-}
-
-__global__ void k_relocate(const Reloc* list, const u64* scal, const Entry* oent, const i64* omt, const u32* oms,
-                           Entry* ent, i64* mt, u32* ms) {
-  const u32 n = static_cast<u32>(scal[2]);
-  const u64 warps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
-  for (u64 k = (blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x) >> 5; k < n; k += warps)
-    copy_region(list[k], threadIdx.x & 31, 32, oent, omt, oms, ent, mt, ms);
-}
-
-__global__ void k_relocate_big(const Reloc* big, const Entry* oent, const i64* omt, const u32* oms, Entry* ent,
-                               i64* mt, u32* ms) {
-  copy_region(big[blockIdx.y], blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, oent, omt, oms, ent, mt,
-              ms);
 }
 
 __device__ __forceinline__ u32 entry_edge(int mode, u32 j) { return mode == TWG_UNDIRECTED ? (j >> 1) : j; }
@@ -294,143 +164,321 @@ __global__ void k_owner_keys(const u32* s, const u32* d, u64 A, int mode, u32* k
   }
 }
 
-// Short runs, one thread per node: the run [ystart, yend) of the
-// owner-sorted entries is already in canonical order; copy it to the region
-// end, append the marks (the first merges with the last surviving mark when
-// the times agree), publish {eb, ee, gb, ge}; Q += ge - gb.
-__global__ void __launch_bounds__(kBlock) k_place_runs(u64 V, const u32* ystart, const u32* yend, const u32* vals,
-                                                       const Rec* rec, int mode, u32 seq_b, const u32* cur0,
-                                                       const u32* gcur0, Entry* ent, i64* mk_time, u32* mk_start,
-                                                       uint4* nm_new, u64* q_total) {
-  u64 acc = 0;
-  for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < V;
-       v += static_cast<u64>(gridDim.x) * blockDim.x) {
-    const u32 ys = ystart[v], y = yend[v] - ys;
-    if (y > kSmallRun) continue;
-    uint4 r = nm_new[v];
-    const u32 c0 = cur0[v];
-    u32 g = gcur0[v];
-    bool has = c0 > r.x;
-    i64 prev = has ? ent[c0 - 1].t : 0;
-    for (u32 i = 0; i < y; ++i) {
-      const u32 j = vals[ys + i];
-      const u32 k = entry_edge(mode, j);
-      const Rec b = rec[k];
-      Entry e;
-      e.nbr = nbr_of(mode, b, j);
-      e.edge = seq_b + k;
-      e.t = b.t;
-      ent[c0 + i] = e;
-      if (!has || b.t != prev) {
-        mk_time[g] = b.t;
-        mk_start[g] = c0 + i;
-        ++g;
+// bucket b = owner >> 8 of the bucket-sorted entries starts at bstart[b]
+// (empty buckets included); bstart[nb] = Yn
+__global__ void k_bucket_bounds(const u32* keys, u64 Yn, u64 nb, u32* bstart) {
+  for (u64 q = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; q <= Yn;
+       q += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const i64 prev = q == 0 ? -1 : static_cast<i64>(keys[q - 1] >> kBucketShift);
+    const i64 cur = q == Yn ? static_cast<i64>(nb) : static_cast<i64>(keys[q] >> kBucketShift);
+    for (i64 b = prev + 1; b <= cur; ++b) bstart[b] = static_cast<u32>(q);
+  }
+}
+
+// per-node batch counts from the bucket-sorted keys (one CTA per bucket)
+__global__ void __launch_bounds__(kPB) k_bucket_count(const u32* keys, const u32* bstart, u64 V, u32* y) {
+  __shared__ u32 cnt[kPB];
+  const u64 bkt = blockIdx.x;
+  cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const u32 bs = bstart[bkt], be = bstart[bkt + 1];
+  for (u32 q = bs + threadIdx.x; q < be; q += kPB) atomicAdd(&cnt[keys[q] & (kPB - 1)], 1u);
+  __syncthreads();
+  const u64 v = (bkt << kBucketShift) + threadIdx.x;
+  if (v < V) y[v] = cnt[threadIdx.x];
+}
+
+// Eviction bound: first logical x in [lo, hi) with time >= c. The eight
+// times after lo are loaded at once (independent loads, one round trip):
+// a batch evicts only a few entries of a typical node; longer prefixes
+// continue by galloping.
+template <class TimeAt>
+__device__ __forceinline__ u32 evict_lb(TimeAt at, u32 lo, u32 hi, i64 c) {
+  constexpr u32 kAhead = 8;
+  const u32 k = min(hi - lo, kAhead);
+  i64 tt[kAhead];
+#pragma unroll
+  for (u32 i = 0; i < kAhead; ++i) tt[i] = i < k ? at(lo + i) : c;
+  u32 n = 0;
+#pragma unroll
+  for (u32 i = 0; i < kAhead; ++i) n += tt[i] < c ? 1u : 0u;
+  if (n < k || k == hi - lo) return lo + n;
+  return gallop_lb(at, lo + kAhead, hi, c);
+}
+
+__device__ __forceinline__ u32 adjust_org(u32 org, u32 x, u32 cap) {  // org' = org (mod cap), 0 <= x - org' < cap
+  return x - org >= cap ? org + cap : org;
+}
+
+struct Reloc {
+  u32 v, src_e, src_g;
+};
+
+struct PlanArgs {
+  const NodeMeta* onm;  // the current snapshot
+  const NodeMeta* rnm;  // the retired one when it shares the arena (its rings stay readable), else null
+  u64 V;
+  const Entry* oent;
+  const i64* omt;
+  const u32* y;
+  i64 cutoff;
+  int relocate_all;     // repack every ring into a fresh arena
+  u64 arena_cap;
+  NodeMeta* plan;       // new bounds / ring; ee, ge = where the batch's entries / marks start
+  i64* last_t;          // time of the last live entry (valid iff plan.ee > plan.eb)
+  Reloc* reloc;
+  u64* scal;            // [0] bump, [1] overflow, [2] relocations
+};
+
+// Per node: eviction (cutoff lower bound on the ring's entry and mark
+// times), room check against the oldest live begin in the ring (the retired
+// snapshot's, while it shares the ring), otherwise a new ring from the bump
+// allocator (CTA-aggregated) with logical positions rebased to 0.
+__global__ void __launch_bounds__(kBlock) k_plan(PlanArgs a) {
+  __shared__ u64 s_base;
+  __shared__ u32 s_rbase;
+  for (u64 b0 = static_cast<u64>(blockIdx.x) * kBlock; b0 < a.V; b0 += static_cast<u64>(gridDim.x) * kBlock) {
+    const u64 v = b0 + threadIdx.x;
+    const bool valid = v < a.V;
+    NodeMeta o{};
+    u32 eb = 0, gb = 0, req = 0, y = 0;
+    bool fits = true;
+    if (valid) {
+      o = a.onm[v];
+      y = a.y[v];
+      const Ring oer = entry_ring(o), omr = mark_ring(o);
+      const i64 c = a.cutoff;
+      eb = evict_lb([&](u32 x) { return a.oent[oer(x)].t; }, o.eb, o.ee, c);
+      gb = evict_lb([&](u32 x) { return a.omt[omr(x)]; }, o.gb, o.ge, c);
+      u32 low = o.eb;
+      if (a.rnm) {
+        const NodeMeta r = a.rnm[v];
+        if (r.base == o.base && r.cap == o.cap) low = r.eb;  // same ring: the retired snapshot reads [r.eb, ..)
       }
-      prev = b.t;
-      has = true;
+      fits = !a.relocate_all && static_cast<u64>(o.ee - low) + y <= o.cap;
+      if (!fits) {
+        const u32 need = (o.ee - eb) + y;
+        req = need + (a.relocate_all ? need / 2 : need) + 4;
+      }
+      if (o.ee > eb) a.last_t[v] = a.oent[oer(o.ee - 1)].t;
     }
-    r.y = c0 + y;
-    r.w = g;
-    nm_new[v] = r;
-    acc += r.w - r.z;
+    u32 tot, mtot;
+    const u32 off = block_excl_scan<u32>(req, &tot);
+    const u32 midx = block_excl_scan<u32>(fits ? 0u : 1u, &mtot);
+    if (threadIdx.x == 0) {
+      s_base = tot ? atomicAdd(reinterpret_cast<unsigned long long*>(&a.scal[0]), static_cast<unsigned long long>(tot))
+                   : 0ull;
+      s_rbase = mtot ? atomicAdd(reinterpret_cast<unsigned int*>(&a.scal[2]), mtot) : 0u;
+    }
+    __syncthreads();
+    if (valid) {
+      if (fits) {
+        a.plan[v] = NodeMeta{eb, o.ee, gb, o.ge, o.base, o.cap, adjust_org(o.eorg, eb, o.cap),
+                             adjust_org(o.gorg, gb, o.cap)};
+      } else {
+        const u64 dst = s_base + off;
+        if (dst + req > a.arena_cap) atomicOr(reinterpret_cast<unsigned long long*>(&a.scal[1]), 1ull);
+        a.plan[v] = NodeMeta{0u, o.ee - eb, 0u, o.ge - gb, static_cast<u32>(dst), req, 0u, 0u};
+        a.reloc[s_rbase + midx] = Reloc{static_cast<u32>(v), eb, gb};
+      }
+    }
+    __syncthreads();
   }
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(reinterpret_cast<unsigned long long*>(q_total), acc);
 }
 
-__device__ __forceinline__ bool long_run(const u32* ystart, const u32* yend, u32 v) {
-  return yend[v] - ystart[v] > kSmallRun;
+// live entries and marks into the new rings (rebased to logical 0), one warp per ring
+__global__ void k_reloc_copy(const Reloc* list, const u64* scal, const NodeMeta* onm, const NodeMeta* plan,
+                             const Entry* oent, const i64* omt, const u32* oms, Entry* ent, i64* mt, u32* ms) {
+  const u64 n = scal[2] & 0xffffffffull;
+  const u64 warps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
+  const u32 lane = threadIdx.x & 31;
+  for (u64 k = (blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x) >> 5; k < n; k += warps) {
+    const Reloc r = list[k];
+    const NodeMeta on = onm[r.v], p = plan[r.v];
+    const Ring er = entry_ring(on), mr = mark_ring(on);
+    for (u32 j = lane; j < p.ee; j += 32) ent[p.base + j] = oent[er(r.src_e + j)];
+    for (u32 j = lane; j < p.ge; j += 32) {
+      mt[p.base + j] = omt[mr(r.src_g + j)];
+      ms[p.base + j] = oms[mr(r.src_g + j)] - r.src_e;
+    }
+  }
 }
 
-// Long runs, pass A flag: q starts a new timestamp mark of its (long-run) node
-struct MarkFlagFn {
-  const u32* keys;
+struct PlaceArgs {
+  u64 V;
+  const NodeMeta* plan;
+  const i64* last_t;
+  const u32* keys;      // batch entries bucket-sorted (owner >> 8), canonical order inside a bucket
   const u32* vals;
-  const Rec* rec;
-  int mode;
-  const u32* ystart;
-  const u32* yend;
-  const u32* cur0;
-  const uint4* nm_new;  // .x = region begin after eviction / relocation
-  const Entry* ent;
-  __device__ __forceinline__ u32 operator()(u64 q) const {
-    const u32 v = keys[q];
-    if (!long_run(ystart, yend, v)) return 0u;
-    const i64 t = rec[entry_edge(mode, vals[q])].t;
-    if (q > 0 && keys[q - 1] == v) return t != rec[entry_edge(mode, vals[q - 1])].t ? 1u : 0u;
-    const u32 c = cur0[v];
-    return (c > nm_new[v].x && ent[c - 1].t == t) ? 0u : 1u;
-  }
-};
-
-struct MarkTmp {
-  i64 t;
-  u32 pos;
-  u32 v;
-};
-
-// Long runs, pass A scatter: place the entry at its region end, record the
-// mark prefix (every q: the long runs' bounds read it)
-struct PlaceScatter {
-  const u32* keys;
-  const u32* vals;
+  const u32* bstart;
   const Rec* rec;
   int mode;
   u32 seq_b;
-  u64 Yn;
-  const u32* ystart;
-  const u32* yend;
-  const u32* cur0;
   Entry* ent;
-  u32* mscan;
-  MarkTmp* mtmp;
-  __device__ __forceinline__ void operator()(u64 q, u64 g, u32 f) const {
-    mscan[q] = static_cast<u32>(g);
-    if (q + 1 == Yn) mscan[Yn] = static_cast<u32>(g + f);
-    const u32 v = keys[q];
-    if (!long_run(ystart, yend, v)) return;
-    const u32 j = vals[q];
-    const u32 k = entry_edge(mode, j);
-    const Rec b = rec[k];
-    const u32 pos = cur0[v] + static_cast<u32>(q - ystart[v]);
-    Entry e;
-    e.nbr = nbr_of(mode, b, j);
-    e.edge = seq_b + k;
-    e.t = b.t;
-    ent[pos] = e;
-    if (f) mtmp[g] = MarkTmp{e.t, pos, v};
-  }
+  i64* mt;
+  u32* ms;
+  NodeMeta* nm_new;
+  u64* q_total;
 };
 
-// Pass B: new marks to their region slots
-__global__ void k_marks_scatter(const MarkTmp* mtmp, const u64* nmarks, const u32* ystart, const u32* mscan,
-                                const u32* gcur0, i64* mk_time, u32* mk_start) {
-  const u64 n = *nmarks;
-  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<u64>(gridDim.x) * blockDim.x) {
-    const MarkTmp m = mtmp[i];
-    const u32 g = gcur0[m.v] + static_cast<u32>(i) - mscan[ystart[m.v]];
-    mk_time[g] = m.t;
-    mk_start[g] = m.pos;
-  }
-}
+struct PlaceSmem {
+  u32 wcnt[kPB / 32][kPB];
+  u32 off[kPB + 1];
+  u32 cur[kPB], gcur[kPB], base[kPB], cap[kPB], eorg[kPB], gorg[kPB];
+  i64 last_t[kPB];
+  u32 has_last[kPB];
+  u32 mtotal;
+  u8 key[kChunk];
+  u8 snode[kChunk];
+  u8 flag[kChunk];
+  u32 val[kChunk];
+  u32 mscan[kChunk];
+  Entry sent[kChunk];
+};
 
-__global__ void __launch_bounds__(kBlock) k_big_finish(const u32* nodes, u64 n, const u32* ystart, const u32* yend,
-                                                       const u32* mscan, const u32* cur0, const u32* gcur0,
-                                                       uint4* nm_new, u64* q_total) {
-  u64 acc = 0;
-  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<u64>(gridDim.x) * blockDim.x) {
-    const u32 v = nodes[i];
-    const u32 ys = ystart[v], ye = yend[v];
-    uint4 r = nm_new[v];
-    r.y = cur0[v] + (ye - ys);
-    r.w = gcur0[v] + (mscan[ye] - mscan[ys]);
-    nm_new[v] = r;
-    acc += r.w - r.z;
+// One CTA per bucket of 256 nodes (thread t <-> node (bucket << 8) + t):
+// the bucket's entries in rounds of kChunk: stable rank per node
+// (warp-private match/ballot counters + cross-warp scan), records gathered
+// and staged in node order in shared memory, mark flags + block scan, then
+// written in node order (a node's new entries / marks are contiguous in its
+// ring, so the stores coalesce); finally publish {eb, ee, gb, ge, ring}.
+__global__ void __launch_bounds__(kPB) k_bucket_place(PlaceArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PlaceSmem& sm = *reinterpret_cast<PlaceSmem*>(smem_raw);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const u64 bkt = blockIdx.x;
+  const u64 v = (bkt << kBucketShift) + t;
+  const bool valid = v < a.V;
+  const u32 bs = a.bstart[bkt], be = a.bstart[bkt + 1];
+  NodeMeta p{};
+  if (valid) p = a.plan[v];
+  sm.cur[t] = p.ee;
+  sm.gcur[t] = p.ge;
+  sm.base[t] = p.base;
+  sm.cap[t] = p.cap;
+  sm.eorg[t] = p.eorg;
+  sm.gorg[t] = p.gorg;
+  const bool has = valid && p.ee > p.eb && be > bs;
+  sm.has_last[t] = has ? 1u : 0u;
+  sm.last_t[t] = has ? a.last_t[v] : 0;
+
+  const u32 lt = (1u << lane) - 1u;
+  for (u32 c0 = bs; c0 < be; c0 += kChunk) {
+    const u32 n = min(static_cast<u32>(kChunk), be - c0);
+    __syncthreads();
+    for (u32 i = t; i < n; i += kPB) {
+      sm.key[i] = static_cast<u8>(a.keys[c0 + i] & (kPB - 1));
+      sm.val[i] = a.vals[c0 + i];
+    }
+    for (int i = t; i < (kPB / 32) * kPB; i += kPB) (&sm.wcnt[0][0])[i] = 0;
+    __syncthreads();
+    // stable rank: warp w owns items [w*R*32, (w+1)*R*32) in R rounds of 32
+    u32 rank[kChunkItems];
+#pragma unroll
+    for (int r = 0; r < kChunkItems; ++r) {
+      const u32 i = warp * (32 * kChunkItems) + r * 32 + lane;
+      const bool ok = i < n;
+      const u32 d = ok ? sm.key[i] : kPB + lane;
+      const u32 peers = __match_any_sync(0xffffffffu, d);
+      const u32 before = ok ? sm.wcnt[warp][d] : 0u;
+      __syncwarp();
+      if (ok && (__ffs(peers) - 1) == lane) sm.wcnt[warp][d] = before + __popc(peers);
+      __syncwarp();
+      rank[r] = before + __popc(peers & lt);
+    }
+    __syncthreads();
+    {  // per node: exclusive prefix across warps, node offset in the staged order
+      u32 acc = 0;
+#pragma unroll
+      for (int w = 0; w < kPB / 32; ++w) {
+        const u32 c = sm.wcnt[w][t];
+        sm.wcnt[w][t] = acc;
+        acc += c;
+      }
+      u32 total;
+      sm.off[t] = block_excl_scan<u32>(acc, &total);
+      if (t == 0) sm.off[kPB] = total;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kChunkItems; ++r) {
+      const u32 i = warp * (32 * kChunkItems) + r * 32 + lane;
+      if (i < n) {
+        const u32 nd = sm.key[i];
+        const u32 sp = sm.off[nd] + sm.wcnt[warp][nd] + rank[r];
+        const u32 j = sm.val[i];
+        const u32 k = entry_edge(a.mode, j);
+        const Rec b = a.rec[k];
+        Entry e;
+        e.nbr = nbr_of(a.mode, b, j);
+        e.edge = a.seq_b + k;
+        e.t = b.t;
+        sm.sent[sp] = e;
+        sm.snode[sp] = static_cast<u8>(nd);
+      }
+    }
+    __syncthreads();
+    // mark flags over the staged order + block scan (consecutive items per thread)
+    u32 fsum = 0;
+#pragma unroll
+    for (int r = 0; r < kChunkItems; ++r) {
+      const u32 i = t * kChunkItems + r;
+      u32 f = 0;
+      if (i < n) {
+        const u32 nd = sm.snode[i];
+        const i64 ti = sm.sent[i].t;
+        if (i == sm.off[nd]) f = (!sm.has_last[nd] || ti != sm.last_t[nd]) ? 1u : 0u;
+        else f = ti != sm.sent[i - 1].t ? 1u : 0u;
+      }
+      sm.flag[i] = static_cast<u8>(f);
+      fsum += f;
+    }
+    u32 mtot;
+    u32 run = block_excl_scan<u32>(fsum, &mtot);
+#pragma unroll
+    for (int r = 0; r < kChunkItems; ++r) {
+      const u32 i = t * kChunkItems + r;
+      sm.mscan[i] = run;
+      run += sm.flag[i];
+    }
+    if (t == 0) sm.mtotal = mtot;
+    __syncthreads();
+    // write out in staged (node) order
+    for (u32 i = t; i < n; i += kPB) {
+      const u32 nd = sm.snode[i];
+      const u32 pos = sm.cur[nd] + (i - sm.off[nd]);
+      const Ring er{sm.base[nd], sm.cap[nd], sm.eorg[nd]};
+      const Entry e = sm.sent[i];
+      a.ent[er(pos)] = e;
+      if (sm.flag[i]) {
+        const Ring mr{sm.base[nd], sm.cap[nd], sm.gorg[nd]};
+        const u32 g = sm.gcur[nd] + (sm.mscan[i] - sm.mscan[sm.off[nd]]);
+        a.mt[mr(g)] = e.t;
+        a.ms[mr(g)] = pos;
+      }
+    }
+    __syncthreads();
+    {  // advance the node cursors
+      const u32 o1 = sm.off[t], c = sm.off[t + 1] - o1;
+      if (c) {
+        const u32 mend = o1 + c < n ? sm.mscan[o1 + c] : sm.mtotal;
+        sm.cur[t] += c;
+        sm.gcur[t] += mend - sm.mscan[o1];
+        sm.last_t[t] = sm.sent[o1 + c - 1].t;
+        sm.has_last[t] = 1u;
+      }
+    }
   }
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(reinterpret_cast<unsigned long long*>(q_total), acc);
+  __syncthreads();
+
+  u64 q = 0;
+  if (valid) {
+    const NodeMeta r{p.eb, sm.cur[t], p.gb, sm.gcur[t], p.base, p.cap, p.eorg, p.gorg};
+    a.nm_new[v] = r;
+    q = r.ge - r.gb;
+  }
+  for (int o2 = 16; o2 > 0; o2 >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o2);
+  if (lane == 0 && q) atomicAdd(reinterpret_cast<unsigned long long*>(a.q_total), q);
 }
 
 bool append_enabled() {
@@ -504,9 +552,11 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
                BatchGroupScatter{bT, seq_b, zbase, zbase_dev, log->ts_off.p, log->ts_time.p});
   pt.mark("log+ts");
 
-  // 2. batch entries grouped by owner: stable radix sort of (owner, entry)
-  //    pairs; run bounds per node
+  // 2. batch entries grouped into 256-node buckets: stable radix sort of
+  //    (owner, entry) pairs on the owner bits above the bucket (canonical
+  //    order inside a bucket), bucket bounds
   const int vb = V > 1 ? bit_width_u64(V - 1) : 0;
+  const u64 nb = (V + kPB - 1) / kPB;
   DevBuf<u32> k0(Yn, st), k1(Yn, st), v0(Yn, st), v1(Yn, st);
   u32* kp = k0.p;
   u32* ka = k1.p;
@@ -514,100 +564,104 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
   u32* va = v1.p;
   k_owner_keys<<<grid(ctx, Yn), kBlock, 0, st>>>(bS, bD, A, mode, kp, vp);
   TWG_LAUNCHED(ctx);
-  radix_sort_pairs<u32>(ctx, &kp, &ka, &vp, &va, Yn, vb);
-  DevBuf<u32> ystart(V, st), yend(V, st);
-  TWG_CUDA(cudaMemsetAsync(ystart.p, 0, V * 4, st));
-  TWG_CUDA(cudaMemsetAsync(yend.p, 0, V * 4, st));
-  k_runs<<<grid(ctx, Yn), kBlock, 0, st>>>(kp, Yn, ystart.p, yend.p);
+  if (vb > static_cast<int>(kBucketShift)) radix_sort_pairs<u32>(ctx, &kp, &ka, &vp, &va, Yn, vb, kBucketShift);
+  DevBuf<u32> bstart(nb + 1, st);
+  k_bucket_bounds<<<grid(ctx, Yn + 1), kBlock, 0, st>>>(kp, Yn, nb, bstart.p);
   TWG_LAUNCHED(ctx);
   (kp == k0.p ? k1 : k0).release();  // the pass count decides which buffer holds the result
   (vp == v0.p ? v1 : v0).release();
-  pt.mark("owner_sort");
+  pt.mark("bucket_sort");
 
-  // 3. eviction + room per node; relocation / repack
-  DevBuf<u32> cur0(V, st), gcur0(V, st), bignodes(V, st);
+  // 3. per node: eviction, ring room / relocation; then per bucket:
+  //    placement, marks, publish
   s->nm.alloc(V, st);
+  DevBuf<u32> ycnt(V, st);
+  k_bucket_count<<<static_cast<unsigned>(nb), kPB, 0, st>>>(kp, bstart.p, V, ycnt.p);
+  TWG_LAUNCHED(ctx);
   std::shared_ptr<NodeArena> arena = O.gapped ? O.arena : nullptr;
-  DevBuf<Reloc> list, big;
-  u64 plan[6] = {0, 0, 0, 0, 0, 0};
-  auto run_plan = [&](NodeArena& dst, const u32* rend_old) {
-    TWG_CUDA(cudaMemsetAsync(sc, 0, 4 * sizeof(u64), st));
-    TWG_CUDA(cudaMemsetAsync(sc + 10, 0, 2 * sizeof(u64), st));
-    TWG_CUDA(cudaMemcpyAsync(sc, &dst.used, sizeof(u64), cudaMemcpyHostToDevice, st));
-    k_plan<<<grid(ctx, V), kBlock, 0, st>>>(O.nm.p, V, O.ent.p, O.mk_time.p, rend_old, ystart.p, yend.p, cutoff,
-                                            dst.cap, dst.rend.p, s->nm.p, cur0.p, gcur0.p, list.p, big.p,
-                                            bignodes.p, sc);
-    TWG_LAUNCHED(ctx);
-    u64 all[12];
-    read_scalars(ctx, sc, all, 12);
-    for (int i = 0; i < 4; ++i) plan[i] = all[i];
-    plan[4] = all[10];  // long-run nodes
-    plan[5] = all[11];  // their entries
-  };
-  list.alloc(V, st);
-  big.alloc(V, st);
-  bool fresh = false;
+  const Store* R = w.previous;
+  // a snapshot older than the retired one still holding this arena may read
+  // any slot: then nothing of it is reused (fresh arena)
   if (arena) {
-    run_plan(*arena, arena->rend.p);
-    if (plan[1]) {
-      arena.reset();  // exhausted: repack below
-    }
+    const long expected = 2 + ((R && R->gapped && R->arena == arena) ? 1 : 0);  // O, R, this local copy
+    if (arena.use_count() > expected) arena.reset();
   }
-  if (!arena) {
+  DevBuf<NodeMeta> plan(V, st);
+  DevBuf<i64> last_t(V, st);
+  DevBuf<Reloc> reloc(V, st);
+  auto run_plan = [&](NodeArena& dst, bool all) {
+    TWG_CUDA(cudaMemsetAsync(sc, 0, 3 * sizeof(u64), st));
+    TWG_CUDA(cudaMemcpyAsync(sc, &dst.used, sizeof(u64), cudaMemcpyHostToDevice, st));
+    PlanArgs pa;
+    pa.onm = O.nm.p;
+    pa.rnm = (!all && R && R->gapped && R->arena.get() == &dst) ? R->nm.p : nullptr;
+    pa.V = V;
+    pa.oent = O.ent.p;
+    pa.omt = O.mk_time.p;
+    pa.y = ycnt.p;
+    pa.cutoff = cutoff;
+    pa.relocate_all = all ? 1 : 0;
+    pa.arena_cap = dst.cap;
+    pa.plan = plan.p;
+    pa.last_t = last_t.p;
+    pa.reloc = reloc.p;
+    pa.scal = sc;
+    k_plan<<<grid(ctx, V), kBlock, 0, st>>>(pa);
+    TWG_LAUNCHED(ctx);
+    u64 r3[3];
+    read_scalars(ctx, sc, r3, 3);
+    dst.used = r3[0];
+    return r3[1] == 0 ? static_cast<u64>(r3[2] & 0xffffffffull) + 1 : 0;  // relocations + 1, 0 = exhausted
+  };
+  bool fresh = false;
+  u64 nrel = arena ? run_plan(*arena, false) : 0;
+  if (nrel == 0) {
     auto na = std::make_shared<NodeArena>();
     na->V = V;
-    na->cap = std::min<u64>((5 * s->P) / 2 + 4 * V + 1024, 0xffffff00ull);  // u32 positions
+    na->cap = std::min<u64>(2 * s->P + 12 * V + 1024, 0xffffff00ull);  // >= 1.5 P + 4 V: the repack always fits
     na->ent.alloc(na->cap, st);
     na->mk_time.alloc(na->cap, st);
     na->mk_start.alloc(na->cap, st);
-    na->rend.alloc(V, st);
     na->used = 0;
     arena = std::move(na);
-    run_plan(*arena, nullptr);
-    if (plan[1]) fail(TWG_ENOMEM, "ingest: node arena sized below the live regions");
+    nrel = run_plan(*arena, true);
+    if (nrel == 0) fail(TWG_ENOMEM, "ingest: node arena sized below the live regions");
     fresh = true;
   }
-  arena->used = plan[0];
-  if (plan[2]) {
-    k_relocate<<<grid(ctx, 32 * plan[2]), kBlock, 0, st>>>(list.p, sc, O.ent.p, O.mk_time.p, O.mk_start.p,
-                                                           arena->ent.p, arena->mk_time.p, arena->mk_start.p);
+  --nrel;
+  if (nrel) {
+    k_reloc_copy<<<grid(ctx, 32 * nrel), kBlock, 0, st>>>(reloc.p, sc, O.nm.p, plan.p, O.ent.p, O.mk_time.p,
+                                                          O.mk_start.p, arena->ent.p, arena->mk_time.p,
+                                                          arena->mk_start.p);
     TWG_LAUNCHED(ctx);
   }
-  for (u64 b0 = 0; b0 < plan[3]; b0 += 65535) {
-    const unsigned rows = static_cast<unsigned>(std::min<u64>(65535, plan[3] - b0));
-    k_relocate_big<<<dim3(32, rows), kBlock, 0, st>>>(big.p + b0, O.ent.p, O.mk_time.p, O.mk_start.p, arena->ent.p,
-                                                      arena->mk_time.p, arena->mk_start.p);
-    TWG_LAUNCHED(ctx);
+  reloc.release();
+  pt.mark(fresh ? "plan+repack" : "plan");
+  static bool attr_set = false;
+  if (!attr_set) {
+    TWG_CUDA(cudaFuncSetAttribute(k_bucket_place, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sizeof(PlaceSmem))));
+    attr_set = true;
   }
-  list.release();
-  big.release();
-  pt.mark(fresh ? "plan+repack" : "plan+relocate");
-
-  // 4a. short runs (the streaming common case): one thread per node copies
-  //     its run (canonical order) to the region end, appends its marks and
-  //     publishes {eb, ee, gb, ge}
-  k_place_runs<<<grid(ctx, V), kBlock, 0, st>>>(V, ystart.p, yend.p, vp, brec.p, mode, seq_b, cur0.p, gcur0.p,
-                                                arena->ent.p, arena->mk_time.p, arena->mk_start.p, s->nm.p, sc + 7);
+  PlaceArgs pl;
+  pl.V = V;
+  pl.plan = plan.p;
+  pl.last_t = last_t.p;
+  pl.keys = kp;
+  pl.vals = vp;
+  pl.bstart = bstart.p;
+  pl.rec = brec.p;
+  pl.mode = mode;
+  pl.seq_b = seq_b;
+  pl.ent = arena->ent.p;
+  pl.mt = arena->mk_time.p;
+  pl.ms = arena->mk_start.p;
+  pl.nm_new = s->nm.p;
+  pl.q_total = sc + 7;
+  TWG_CUDA(cudaMemsetAsync(sc + 7, 0, sizeof(u64), st));
+  k_bucket_place<<<static_cast<unsigned>(nb), kPB, sizeof(PlaceSmem), st>>>(pl);
   TWG_LAUNCHED(ctx);
-  pt.mark("place_runs");
-
-  // 4b. long runs (hub owners): one decoupled-look-back pass over the sorted
-  //     entries places them and numbers their new marks (other nodes' flags
-  //     are 0), a per-mark pass scatters the marks, a per-node pass publishes
-  if (plan[4]) {
-    DevBuf<u32> mscan(Yn + 1, st);
-    DevBuf<MarkTmp> mtmp(plan[5], st);
-    scan_scatter(ctx, MarkFlagFn{kp, vp, brec.p, mode, ystart.p, yend.p, cur0.p, s->nm.p, arena->ent.p}, Yn, sc + 6,
-                 PlaceScatter{kp, vp, brec.p, mode, seq_b, Yn, ystart.p, yend.p, cur0.p, arena->ent.p, mscan.p,
-                              mtmp.p});
-    k_marks_scatter<<<grid(ctx, plan[5]), kBlock, 0, st>>>(mtmp.p, sc + 6, ystart.p, mscan.p, gcur0.p,
-                                                           arena->mk_time.p, arena->mk_start.p);
-    TWG_LAUNCHED(ctx);
-    k_big_finish<<<grid(ctx, plan[4]), kBlock, 0, st>>>(bignodes.p, plan[4], ystart.p, yend.p, mscan.p, cur0.p,
-                                                        gcur0.p, s->nm.p, sc + 7);
-    TWG_LAUNCHED(ctx);
-    pt.mark("place_long_runs");
-  }
+  pt.mark("place");
 
   // the one closing read-back: g_cut, batch groups, Q
   u64 r[4];

@@ -469,19 +469,19 @@ void merge_path(Ctx& ctx, KA ka, u64 na, KB kb, u64 nb, Emit emit) {
   TWG_LAUNCHED(ctx);
 }
 
-// Stable LSD sort of (keys, vals) by the low `bits` bits of the key. Sorted
+// Stable LSD sort of (keys, vals) by key bits [lo_bit, bits). Sorted
 // output lands in (*keys, *vals); the alt buffers are scratch of the same
 // size. Pointers are swapped as passes ping-pong. n < 2^32. Keys-only when
 // *vals == nullptr.
 template <class K>
-void radix_sort_pairs(Ctx& ctx, K** keys, K** keys_alt, u32** vals, u32** vals_alt, u64 n, int bits) {
-  if (n < 2 || bits <= 0) return;
+void radix_sort_pairs(Ctx& ctx, K** keys, K** keys_alt, u32** vals, u32** vals_alt, u64 n, int bits, int lo_bit = 0) {
+  if (n < 2 || bits <= lo_bit) return;
   cudaStream_t st = ctx.stream;
   const u64 tiles = (n + kSortTile - 1) / kSortTile;
   if (tiles * kRadix >= (1ull << 32)) fail(TWG_EINVAL, "radix_sort_pairs: input too large");
   DevBuf<u32> counts(tiles * kRadix + 1, st);
   DevBuf<u32> offsets(tiles * kRadix + 1, st);
-  for (int shift = 0; shift < bits; shift += kRadixBits) {
+  for (int shift = lo_bit; shift < bits; shift += kRadixBits) {
     k_radix_hist<K><<<static_cast<unsigned>(tiles), kSortBlock, 0, st>>>(*keys, n, shift, counts.p, tiles);
     TWG_LAUNCHED(ctx);
     exclusive_scan<u32>(ctx, LoadFn<u32>{counts.p}, tiles * kRadix, offsets.p);

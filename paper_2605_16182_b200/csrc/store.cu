@@ -424,21 +424,21 @@ static void build_adjacency(Ctx& ctx, Store& s, const u32* owners) {
 }
 
 namespace {
-__global__ void k_nm_from_nmeta(const uint2* nmeta, u64 V, uint4* nm) {
+__global__ void k_nm_from_nmeta(const uint2* nmeta, u64 V, NodeMeta* nm) {
   for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < V;
        v += static_cast<u64>(gridDim.x) * blockDim.x) {
     const uint2 a = nmeta[v], b = nmeta[v + 1];
-    nm[v] = make_uint4(a.x, b.x, a.y, b.y);
+    nm[v] = NodeMeta{a.x, b.x, a.y, b.y, 0u, kIdentityCap, 0u, 0u};
   }
 }
 
 struct EntSizeFn {
-  const uint4* nm;
-  __device__ __forceinline__ u32 operator()(u64 v) const { return nm[v].y - nm[v].x; }
+  const NodeMeta* nm;
+  __device__ __forceinline__ u32 operator()(u64 v) const { return nm[v].ee - nm[v].eb; }
 };
 struct MarkSizeFn {
-  const uint4* nm;
-  __device__ __forceinline__ u32 operator()(u64 v) const { return nm[v].w - nm[v].z; }
+  const NodeMeta* nm;
+  __device__ __forceinline__ u32 operator()(u64 v) const { return nm[v].ge - nm[v].gb; }
 };
 
 __global__ void k_pack_nmeta(const u32* off, const u32* goff, u64 V, uint2* nmeta) {
@@ -456,23 +456,24 @@ __global__ void k_ts_rebase(const u32* ts_off, u64 Z, u32 seq0, u64 m, u32* out)
 // gapped regions -> contiguous regions, one warp per node (lanes stride the
 // region): entries get snapshot-relative edge indices, marks contiguous
 // positions, and every entry its owner.
-__global__ void k_compact_regions(const uint4* nm, u64 V, const Entry* ent, const i64* mk_time, const u32* mk_start,
-                                  u32 seq0, const uint2* nmeta, Entry* ent_c, u32* owner_c, i64* mk_time_c,
-                                  u32* mk_start_c) {
+__global__ void k_compact_regions(const NodeMeta* nm, u64 V, const Entry* ent, const i64* mk_time,
+                                  const u32* mk_start, u32 seq0, const uint2* nmeta, Entry* ent_c, u32* owner_c,
+                                  i64* mk_time_c, u32* mk_start_c) {
   const int lane = threadIdx.x & 31;
   const u64 warps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
   for (u64 v = (blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x) >> 5; v < V; v += warps) {
-    const uint4 r = nm[v];
+    const NodeMeta r = nm[v];
+    const Ring er = entry_ring(r), mr = mark_ring(r);
     const uint2 o = nmeta[v];
-    for (u32 i = lane; i < r.y - r.x; i += 32) {
-      Entry e = ent[r.x + i];
+    for (u32 i = lane; i < r.ee - r.eb; i += 32) {
+      Entry e = ent[er(r.eb + i)];
       e.edge -= seq0;
       ent_c[o.x + i] = e;
       owner_c[o.x + i] = static_cast<u32>(v);
     }
-    for (u32 i = lane; i < r.w - r.z; i += 32) {
-      mk_time_c[o.y + i] = mk_time[r.z + i];
-      mk_start_c[o.y + i] = mk_start[r.z + i] - r.x + o.x;
+    for (u32 i = lane; i < r.ge - r.gb; i += 32) {
+      mk_time_c[o.y + i] = mk_time[mr(r.gb + i)];
+      mk_start_c[o.y + i] = mk_start[mr(r.gb + i)] - r.eb + o.x;
     }
   }
 }
@@ -694,7 +695,7 @@ Store* build_store(Ctx& ctx, EdgesSoA in, int mode, BuildOpts opts, u64* scratch
     s->nmeta.alloc(1, st);
     TWG_CUDA(cudaMemsetAsync(s->nmeta.p, 0, sizeof(uint2), st));
     s->nm.alloc(1, st);
-    TWG_CUDA(cudaMemsetAsync(s->nm.p, 0, sizeof(uint4), st));
+    TWG_CUDA(cudaMemsetAsync(s->nm.p, 0, sizeof(NodeMeta), st));
     s->ts_off.alloc(1, st);
     TWG_CUDA(cudaMemsetAsync(s->ts_off.p, 0, sizeof(u32), st));
     s->adj_off.alloc(1, st);

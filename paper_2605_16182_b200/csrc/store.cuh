@@ -32,6 +32,30 @@ struct Entry {
 };
 static_assert(sizeof(Entry) == 16, "Entry must be 16 bytes");
 
+// Per-node view of one snapshot (32 bytes: one sector per hop). Positions
+// are LOGICAL: node v's entries are [eb, ee), its timestamp marks [gb, ge),
+// and mark starts hold logical entry positions. They live in a ring of
+// `cap` slots at `base` (entries and marks in parallel arrays): logical x
+// maps to base + ((x - org) mod cap), with org chosen per snapshot so that
+// x - org < 2 cap for every live x (one compare + select, no division).
+// Contiguous stores use the identity ring {base 0, cap 2^32-1, org 0}.
+struct alignas(32) NodeMeta {
+  u32 eb, ee, gb, ge;
+  u32 base, cap, eorg, gorg;
+};
+static_assert(sizeof(NodeMeta) == 32, "NodeMeta must be one 32-byte sector");
+
+struct Ring {
+  u32 base, cap, org;
+  __device__ __forceinline__ u32 operator()(u32 x) const {
+    const u32 d = x - org;
+    return base + (d >= cap ? d - cap : d);
+  }
+};
+__device__ __forceinline__ Ring entry_ring(const NodeMeta& m) { return Ring{m.base, m.cap, m.eorg}; }
+__device__ __forceinline__ Ring mark_ring(const NodeMeta& m) { return Ring{m.base, m.cap, m.gorg}; }
+constexpr u32 kIdentityCap = 0xffffffffu;
+
 // Raw pointers + counts of one snapshot, passed by value to kernels.
 //
 // Edge numbering: entry .edge fields and ts_off hold edge SEQUENCE numbers
@@ -50,7 +74,7 @@ struct StoreView {
   const i64* ts_time;
   const double* ts_w;
   const uint2* nmeta;  // {entry offset, group offset}, V+1 (contiguous stores only)
-  const uint4* nm;     // {entry begin, entry end, mark begin, mark end} per node (every store)
+  const NodeMeta* nm;  // per-node bounds + ring (every store)
   const i64* mk_time;
   const u32* mk_start;
   const Entry* ent;
@@ -80,15 +104,15 @@ struct BuildOpts {
 // rewriting the whole window every batch:
 //  * EdgeLog: the canonical edge columns and the timestamp-group view; a
 //    snapshot is a contiguous slice of it.
-//  * NodeArena: per-node regions with slack; node v's entries live in
-//    [eb, ee) and its timestamp marks in [gb, ge) (parallel arrays, the
-//    marks of a region never outgrow its entries), new entries are placed
-//    at ee, eviction advances eb/gb. A region that runs out of slack is
-//    relocated to fresh arena space; when the arena is exhausted the live
-//    regions are repacked into a new one.
-// Nothing a published snapshot can read is ever overwritten: writes go only
-// past every published snapshot's ends, and a replaced log/arena stays alive
-// (shared_ptr) while any snapshot references it.
+//  * NodeArena: one ring per node (NodeMeta); new entries and marks are
+//    written at the logical ends ee/ge, eviction advances eb/gb, and the
+//    slots freed by eviction are reused once no live snapshot can read them.
+//    A ring without room is relocated to fresh arena space (bigger); when
+//    the arena is exhausted, or a snapshot older than the retired one is
+//    still held, every live ring is repacked into a new arena.
+// Nothing a live snapshot can read is ever overwritten: a ring only accepts
+// new entries while ee + y - (oldest live eb in that ring) <= cap, and a
+// replaced log/arena stays alive (shared_ptr) while any snapshot uses it.
 struct EdgeLog {
   DevBuf<u32> src, dst;
   DevBuf<i64> t;
@@ -104,7 +128,6 @@ struct NodeArena {
   DevBuf<Entry> ent;
   DevBuf<i64> mk_time;
   DevBuf<u32> mk_start;
-  DevBuf<u32> rend;  // per node: end of its region's capacity (writer state)
   u64 cap = 0;       // slots
   u64 used = 0;      // bump pointer (host copy, updated after each ingest)
   u64 V = 0;
@@ -130,7 +153,7 @@ struct Store {
   DevBuf<u32> adj_off, adj;
   DevBuf<u32> owner;  // owner node of each node-view entry (drives the next batch's merge)
   DevBuf<i64> last_t; // newest incident edge time per node: v survives a cutoff c iff last_t[v] >= c
-  DevBuf<uint4> nm;   // {eb, ee, gb, ge} per node: the walk kernels' node meta (every store)
+  DevBuf<NodeMeta> nm;  // per-node bounds + ring: the walk kernels' node meta (every store)
   u32 seq0 = 0;       // sequence number of edge 0 (StoreView)
   // streaming representation (gapped == true): slices of a shared log/arena
   bool gapped = false;

@@ -66,21 +66,40 @@ __device__ __forceinline__ i64 ext_of(const StoreView& s, u32 v) {
 
 // ---- per-hop pieces -------------------------------------------------------
 
-// walk_engine.cpp:18-34 over marks mt/ms[glo, ghi) of a region [lo, hi)
-__device__ __forceinline__ void causal_slice(const i64* mt, const u32* ms, u32 glo, u32 ghi, u32 lo, u32 hi,
+// first logical g in [lo, hi) with x < a[ring(g)] / with a[ring(g)] >= x
+__device__ __forceinline__ u32 ub_ring(const i64* a, Ring r, u32 lo, u32 hi, i64 x) {
+  while (lo < hi) {
+    const u32 mid = lo + ((hi - lo) >> 1);
+    if (x < a[r(mid)]) hi = mid;
+    else lo = mid + 1;
+  }
+  return lo;
+}
+__device__ __forceinline__ u32 lb_ring(const i64* a, Ring r, u32 lo, u32 hi, i64 x) {
+  while (lo < hi) {
+    const u32 mid = lo + ((hi - lo) >> 1);
+    if (a[r(mid)] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// walk_engine.cpp:18-34 over marks mt/ms (logical [glo, ghi) through ring mr)
+// of a region [lo, hi); c/e are logical entry positions
+__device__ __forceinline__ void causal_slice(const i64* mt, const u32* ms, Ring mr, u32 glo, u32 ghi, u32 lo, u32 hi,
                                              i64 t, int dir, u32& c, u32& e) {
   if (dir == 0) {
-    const u32 g = ub_i64(mt, glo, ghi, t);
-    c = g == ghi ? hi : ms[g];
+    const u32 g = ub_ring(mt, mr, glo, ghi, t);
+    c = g == ghi ? hi : ms[mr(g)];
     e = hi;
   } else {
-    const u32 g = lb_i64(mt, glo, ghi, t);
+    const u32 g = lb_ring(mt, mr, glo, ghi, t);
     c = lo;
-    e = g == ghi ? hi : ms[g];
+    e = g == ghi ? hi : ms[mr(g)];
   }
 }
 
-// walk_engine.cpp:49-63
+// walk_engine.cpp:49-63 (contiguous stores: the weighted views exist only there)
 __device__ u64 draw_weighted_local(const WalkParams& P, double u, u32 c, u32 e) {
   const i64 anchor = P.s.ent[e - 1].t;
   double total = 0.0;
@@ -124,11 +143,12 @@ __device__ __forceinline__ bool adjacent(const StoreView& s, u32 a, u32 b) {
 
 // edge_store.cpp:316-323
 __device__ bool adjacent_after(const StoreView& s, u32 a, u32 b, i64 t, int dir) {
-  const uint4 na = s.nm[a];
+  const NodeMeta na = s.nm[a];
+  const Ring er = entry_ring(na);
   u32 c, e;
-  causal_slice(s.mk_time, s.mk_start, na.z, na.w, na.x, na.y, t, dir, c, e);
+  causal_slice(s.mk_time, s.mk_start, mark_ring(na), na.gb, na.ge, na.eb, na.ee, t, dir, c, e);
   for (u32 pos = c; pos < e; ++pos)
-    if (s.ent[pos].nbr == b) return true;
+    if (s.ent[er(pos)].nbr == b) return true;
   return false;
 }
 
@@ -151,14 +171,15 @@ struct WalkReg {
   u32 has_prev;
 };
 
-// One hop (walk_engine.cpp:88-145). mt/ms: the marks to search, either the
-// global arrays (glo/ghi = node group range) or a shared-memory copy
-// (glo = 0). Returns false when the causal slice is empty (walk dies).
-__device__ __forceinline__ bool hop(const WalkParams& P, u64 wl, WalkReg& r, const i64* mt, const u32* ms, u32 glo,
-                                    u32 ghi, u32 lo, u32 hi, Ctr* cn) {
+// One hop (walk_engine.cpp:88-145). mt/ms: the marks to search (logical
+// [glo, ghi) through ring mr), either the global arrays or a shared-memory
+// copy; entries [lo, hi) through ring er. Returns false when the causal
+// slice is empty (walk dies).
+__device__ __forceinline__ bool hop(const WalkParams& P, u64 wl, WalkReg& r, const i64* mt, const u32* ms, Ring mr,
+                                    u32 glo, u32 ghi, Ring er, u32 lo, u32 hi, Ctr* cn) {
   u32* amb = &cn->amb;
   u32 c, e;
-  causal_slice(mt, ms, glo, ghi, lo, hi, r.t, P.dir, c, e);
+  causal_slice(mt, ms, mr, glo, ghi, lo, hi, r.t, P.dir, c, e);
   if (c == e) return false;
   cn->bytes += 80u + 8u * ceil_log2p1(ghi - glo) +
                (P.bias == TWG_EXPWEIGHT ? 16u + 8u * ceil_log2p1(e - c - 1) : 0u);
@@ -170,7 +191,7 @@ __device__ __forceinline__ bool hop(const WalkParams& P, u64 wl, WalkReg& r, con
     for (u32 k = 0; k < kNode2VecMaxRetries; ++k) {
       const double u = P.rng.uniform(w, hop_index, 2ull * k);
       idx = draw_index(P, u, lo, c, e, amb);
-      const u32 cand = P.s.ent[c + idx].nbr;
+      const u32 cand = P.s.ent[er(c + static_cast<u32>(idx))].nbr;
       const double ua = P.rng.uniform(w, hop_index, 2ull * k + 1);
       double beta;  // samplers.hpp:74-86
       if (cand == r.prev) beta = P.inv_p;
@@ -183,7 +204,7 @@ __device__ __forceinline__ bool hop(const WalkParams& P, u64 wl, WalkReg& r, con
     const double u = P.rng.uniform(w, hop_index, 0);
     idx = draw_index(P, u, lo, c, e, amb);
   }
-  const Entry x = P.s.ent[c + idx];
+  const Entry x = P.s.ent[er(c + static_cast<u32>(idx))];
   const u64 slot = out_index(P, wl, r.len);
   P.nodes[slot] = ext_of(P.s, x.nbr);
   P.times[slot] = x.t;
@@ -301,8 +322,8 @@ __global__ void __launch_bounds__(kBlock) k_fullwalk(WalkParams P, InitParams I,
     init_walk(P, I, wl, r, &cn);
     init_len = r.len;
     while (r.len < P.stride) {
-      const uint4 a = P.s.nm[r.cur];
-      if (!hop(P, wl, r, P.s.mk_time, P.s.mk_start, a.z, a.w, a.x, a.y, &cn)) break;
+      const NodeMeta a = P.s.nm[r.cur];
+      if (!hop(P, wl, r, P.s.mk_time, P.s.mk_start, mark_ring(a), a.gb, a.ge, entry_ring(a), a.eb, a.ee, &cn)) break;
     }
     lengths[wl] = r.len;
   }
@@ -399,8 +420,8 @@ __global__ void k_classify(const u32* keys, u64 n, StoreView s, twg_thresholds t
     }
     const u64 end = lo;
     const u32 W = static_cast<u32>(end - i);
-    const uint4 nv = s.nm[v];
-    const u32 G = nv.w - nv.z;
+    const NodeMeta nv = s.nm[v];
+    const u32 G = nv.ge - nv.gb;
     int tier;
     u32 pieces = 1;
     if (W < th.w_warp) tier = 0;
@@ -440,10 +461,11 @@ __device__ __forceinline__ void store_state(const StateArrays& S, u32 w, const W
 }
 
 __device__ __forceinline__ void hop_member(const WalkParams& P, const StateArrays& S, u32 w, const i64* mt,
-                                           const u32* ms, u32 glo, u32 ghi, u32 lo, u32 hi, Ctr* amb) {
+                                           const u32* ms, Ring mr, u32 glo, u32 ghi, Ring er, u32 lo, u32 hi,
+                                           Ctr* amb) {
   WalkReg r;
   load_state(S, w, r);
-  const bool alive = hop(P, w, r, mt, ms, glo, ghi, lo, hi, amb);
+  const bool alive = hop(P, w, r, mt, ms, mr, glo, ghi, er, lo, hi, amb);
   store_state(S, w, r, alive, P.stride);
 }
 
@@ -454,9 +476,9 @@ __global__ void __launch_bounds__(kBlock) k_tier_solo(WalkParams P, StateArrays 
   Ctr amb{0, 0};
   for (u32 k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const Task task = tasks[k];
-    const uint4 a = P.s.nm[task.node];
+    const NodeMeta a = P.s.nm[task.node];
     for (u32 i = task.begin; i < task.end; ++i)
-      hop_member(P, S, ids[i], P.s.mk_time, P.s.mk_start, a.z, a.w, a.x, a.y, &amb);
+      hop_member(P, S, ids[i], P.s.mk_time, P.s.mk_start, mark_ring(a), a.gb, a.ge, entry_ring(a), a.eb, a.ee, &amb);
   }
   add_counters(stats, amb);
 }
@@ -475,20 +497,22 @@ __global__ void __launch_bounds__(kBlock) k_tier_warp(WalkParams P, StateArrays 
   Ctr amb{0, 0};
   for (u32 k = blockIdx.x * (kBlock / 32) + warp; k < n; k += gridDim.x * (kBlock / 32)) {
     const Task task = tasks[k];
-    const uint4 a = P.s.nm[task.node];
-    const u32 G = a.w - a.z;
+    const NodeMeta a = P.s.nm[task.node];
+    const Ring mr = mark_ring(a), er = entry_ring(a);
+    const u32 G = a.ge - a.gb;
     if (kCached && G <= cap) {
       for (u32 g = lane; g < G; g += 32) {
-        smt[g] = P.s.mk_time[a.z + g];
-        sms[g] = P.s.mk_start[a.z + g];
+        smt[g] = P.s.mk_time[mr(a.gb + g)];
+        sms[g] = P.s.mk_start[mr(a.gb + g)];
       }
       __syncwarp();
+      const Ring staged{0u, kIdentityCap, a.gb};
       for (u32 i = task.begin + lane; i < task.end; i += 32)
-        hop_member(P, S, ids[i], smt, sms, 0, G, a.x, a.y, &amb);
+        hop_member(P, S, ids[i], smt, sms, staged, a.gb, a.ge, er, a.eb, a.ee, &amb);
       __syncwarp();
     } else {
       for (u32 i = task.begin + lane; i < task.end; i += 32)
-        hop_member(P, S, ids[i], P.s.mk_time, P.s.mk_start, a.z, a.w, a.x, a.y, &amb);
+        hop_member(P, S, ids[i], P.s.mk_time, P.s.mk_start, mr, a.gb, a.ge, er, a.eb, a.ee, &amb);
     }
   }
   add_counters(stats, amb);
@@ -507,20 +531,22 @@ __global__ void __launch_bounds__(kBlock) k_tier_block(WalkParams P, StateArrays
   Ctr amb{0, 0};
   for (u32 k = blockIdx.x; k < n; k += gridDim.x) {
     const Task task = tasks[k];
-    const uint4 a = P.s.nm[task.node];
-    const u32 G = a.w - a.z;
+    const NodeMeta a = P.s.nm[task.node];
+    const Ring mr = mark_ring(a), er = entry_ring(a);
+    const u32 G = a.ge - a.gb;
     if (kCached && G <= cap) {
       __syncthreads();
       for (u32 g = threadIdx.x; g < G; g += blockDim.x) {
-        smt[g] = P.s.mk_time[a.z + g];
-        sms[g] = P.s.mk_start[a.z + g];
+        smt[g] = P.s.mk_time[mr(a.gb + g)];
+        sms[g] = P.s.mk_start[mr(a.gb + g)];
       }
       __syncthreads();
+      const Ring staged{0u, kIdentityCap, a.gb};
       for (u32 i = task.begin + threadIdx.x; i < task.end; i += blockDim.x)
-        hop_member(P, S, ids[i], smt, sms, 0, G, a.x, a.y, &amb);
+        hop_member(P, S, ids[i], smt, sms, staged, a.gb, a.ge, er, a.eb, a.ee, &amb);
     } else {
       for (u32 i = task.begin + threadIdx.x; i < task.end; i += blockDim.x)
-        hop_member(P, S, ids[i], P.s.mk_time, P.s.mk_start, a.z, a.w, a.x, a.y, &amb);
+        hop_member(P, S, ids[i], P.s.mk_time, P.s.mk_start, mr, a.gb, a.ge, er, a.eb, a.ee, &amb);
     }
   }
   add_counters(stats, amb);
@@ -534,10 +560,10 @@ __global__ void k_finalize(const StateArrays S, u64 count, u32* lengths, u64* st
   add_stats(stats, len, len, Ctr{0, 0}, active);
 }
 
-__global__ void k_start_flags(const uint4* nm, u64 V, u32* flags) {
+__global__ void k_start_flags(const NodeMeta* nm, u64 V, u32* flags) {
   for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < V;
        v += static_cast<u64>(gridDim.x) * blockDim.x)
-    flags[v] = nm[v].x != nm[v].y ? 1u : 0u;
+    flags[v] = nm[v].eb != nm[v].ee ? 1u : 0u;
 }
 
 __global__ void k_start_nodes(const u32* flags, const u32* pos, u64 V, u32* out) {
@@ -692,10 +718,10 @@ __global__ void k_hop_list(WalkParams P, StateArrays S, const u32* ids, u64 n, u
   for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<u64>(gridDim.x) * blockDim.x) {
     const u32 w = ids[i];
-    const uint4 a = P.s.nm[S.cur[w]];
+    const NodeMeta a = P.s.nm[S.cur[w]];
     WalkReg r;
     load_state(S, w, r);
-    const bool ok = hop(P, w, r, P.s.mk_time, P.s.mk_start, a.z, a.w, a.x, a.y, &cn);
+    const bool ok = hop(P, w, r, P.s.mk_time, P.s.mk_start, mark_ring(a), a.gb, a.ge, entry_ring(a), a.eb, a.ee, &cn);
     store_state(S, w, r, ok, P.stride);
   }
   add_counters(stats, cn);

@@ -42,34 +42,42 @@ unsigned grid(Ctx& ctx, u64 n) { return grid_for(n, kBlock, static_cast<unsigned
 //       [5] V_new, [6] max present id
 __global__ void k_init_scalars(u64* s) {
   reinterpret_cast<i64*>(s)[0] = kTimeUnset;
-  for (int i = 1; i < 8; ++i) s[i] = 0;
+  for (int i = 1; i < 10; ++i) s[i] = 0;
+  reinterpret_cast<i64*>(s)[8] = kTimeInfinite;
 }
 
 // scal[7]: bit0 = batch not time-ordered, bit1 = some equal-time run > kSegMax
 constexpr int kSegMax = 32;
 
+// scal[8]: batch min t, scal[9]: some id negative
 __global__ void k_batch_stats(const i64* bs, const i64* bd, const i64* bt, u64 n, u64* scal) {
-  i64 mt = kTimeUnset;
+  i64 mt = kTimeUnset, lt = kTimeInfinite;
   u64 mid = 0;
-  u32 shape = 0;
+  u32 shape = 0, neg = 0;
   for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<u64>(gridDim.x) * blockDim.x) {
-    const i64 t = bt[i];
+    const i64 t = bt[i], a = bs[i], b = bd[i];
     mt = max(mt, t);
-    if (bs[i] > 0) mid = max(mid, static_cast<u64>(bs[i]));
-    if (bd[i] > 0) mid = max(mid, static_cast<u64>(bd[i]));
+    lt = min(lt, t);
+    if (a > 0) mid = max(mid, static_cast<u64>(a));
+    if (b > 0) mid = max(mid, static_cast<u64>(b));
+    if (a < 0 || b < 0) neg = 1;
     if (i + 1 < n && t > bt[i + 1]) shape |= 1u;
     if (i + kSegMax < n && t == bt[i + kSegMax]) shape |= 2u;
   }
   for (int o = 16; o > 0; o >>= 1) {
     mt = max(mt, __shfl_xor_sync(0xffffffffu, mt, o));
+    lt = min(lt, __shfl_xor_sync(0xffffffffu, lt, o));
     mid = max(mid, __shfl_xor_sync(0xffffffffu, mid, o));
     shape |= __shfl_xor_sync(0xffffffffu, shape, o);
+    neg |= __shfl_xor_sync(0xffffffffu, neg, o);
   }
   if ((threadIdx.x & 31) == 0) {
     atomicMax(reinterpret_cast<long long*>(&scal[0]), static_cast<long long>(mt));
+    atomicMin(reinterpret_cast<long long*>(&scal[8]), static_cast<long long>(lt));
     atomicMax(reinterpret_cast<unsigned long long*>(&scal[1]), mid);
     if (shape) atomicOr(reinterpret_cast<unsigned long long*>(&scal[7]), static_cast<u64>(shape));
+    if (neg) atomicOr(reinterpret_cast<unsigned long long*>(&scal[9]), 1ull);
   }
 }
 
@@ -98,6 +106,52 @@ __global__ void k_segment_sort(const u32* s, const u32* d, const i64* t, u64 A, 
       ot[k + j] = tk;
     }
   }
+}
+
+// Fast append route, batch side in one pass: a time-ordered batch over the
+// existing population 0..V-1 (internal id == external id): canonical order
+// by sorting each short equal-time run by (src, dst) in registers (one
+// thread per run), and the newest-incident-time update of both endpoints.
+template <bool kTimeOrdered>
+__device__ __forceinline__ void agg_max(i64* last, u32 key, i64 t, bool valid);
+
+__global__ void k_batch_fast(const i64* bs, const i64* bd, const i64* bt, u64 n, u32* os, u32* od, i64* ot,
+                             i64* last) {
+  for (u64 k0 = blockIdx.x * static_cast<u64>(blockDim.x); k0 < n; k0 += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const u64 k = k0 + threadIdx.x;
+    const bool valid = k < n;
+    const i64 tk = valid ? bt[k] : 0;
+    if (valid && !(k > 0 && bt[k - 1] == tk)) {
+      u64 key[kSegMax];
+      int len = 0;
+      while (len < kSegMax && k + len < n && bt[k + len] == tk) {
+        const u64 x = (static_cast<u64>(bs[k + len]) << 32) | static_cast<u64>(bd[k + len]);
+        int j = len++;
+        while (j > 0 && key[j - 1] > x) {
+          key[j] = key[j - 1];
+          --j;
+        }
+        key[j] = x;
+      }
+      for (int j = 0; j < len; ++j) {
+        os[k + j] = static_cast<u32>(key[j] >> 32);
+        od[k + j] = static_cast<u32>(key[j]);
+        ot[k + j] = tk;
+      }
+    }
+    agg_max<true>(last, valid ? static_cast<u32>(bs[k < n ? k : 0]) : 0u, tk, valid);
+    agg_max<true>(last, valid ? static_cast<u32>(bd[k < n ? k : 0]) : 0u, tk, valid);
+  }
+}
+
+// nodes whose newest incident edge falls before the cutoff (they would leave the snapshot)
+__global__ void k_count_dead(const i64* last, u64 V, i64 cutoff, u64* dead) {
+  u64 c = 0;
+  for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < V;
+       v += static_cast<u64>(gridDim.x) * blockDim.x)
+    c += last[v] < cutoff ? 1u : 0u;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(reinterpret_cast<unsigned long long*>(dead), c);
 }
 
 // lower_bound(time_, cutoff) (edge_store.cpp:326)
@@ -931,6 +985,55 @@ Store* ingest_streaming(Window& w, const i64* bs, const i64* bd, const i64* bt, 
   return s.release();
 }
 
+// The fast append route (append.cu) when the batch shape allows it from
+// the batch statistics alone: time-ordered with short equal-time runs, all
+// admitted (min t >= cutoff), strictly after the window's newest time (the
+// canonical merge is a concatenation), ids inside the current dense
+// population 0..V-1 (internal == external), and no old node leaving the
+// window (checked on the device after the newest-time update; otherwise the
+// general route runs from scratch and the speculative work is discarded).
+Store* ingest_fast(Window& w, const i64* bs, const i64* bd, const i64* bt, u64 n, const u64* sc, i64 cutoff,
+                   twg_batch_stats* stats) {
+  Ctx& ctx = *w.ctx;
+  cudaStream_t st = ctx.stream;
+  const Store& O = *w.store;
+  const i64 batch_min = static_cast<i64>(sc[8]);
+  const u32 shape = static_cast<u32>(sc[7]);
+  if (!append_ingest_enabled() || O.m == 0 || O.V == 0 || !O.ext_identity || shape != 0 || sc[9] ||
+      batch_min < cutoff || batch_min <= w.t_high || sc[1] >= O.V || n >= 0xffffffffull / 2)
+    return nullptr;
+  PhaseTimer pt(ctx, "ingest_fast");
+  const u64 V = O.V;
+  auto s = std::make_unique<Store>();
+  s->ctx = &ctx;
+  s->mode = w.mode;
+  s->V = V;
+  s->ext_identity = true;
+  s->ext.alloc(V, st);
+  TWG_CUDA(cudaMemcpyAsync(s->ext.p, O.ext.p, V * sizeof(i64), cudaMemcpyDeviceToDevice, st));
+  s->last_t.alloc(V, st);
+  TWG_CUDA(cudaMemcpyAsync(s->last_t.p, O.last_t.p, V * sizeof(i64), cudaMemcpyDeviceToDevice, st));
+  DevBuf<u32> bS(n, st), bD(n, st);
+  DevBuf<i64> bT(n, st);
+  TWG_CUDA(cudaMemsetAsync(ctx.d_scalars + 12, 0, 16, st));
+  k_lower_bound<<<1, 1, 0, st>>>(O.e_t.p, O.m, cutoff, ctx.d_scalars + 12);
+  TWG_LAUNCHED(ctx);
+  k_batch_fast<<<grid(ctx, n), kBlock, 0, st>>>(bs, bd, bt, n, bS.p, bD.p, bT.p, s->last_t.p);
+  TWG_LAUNCHED(ctx);
+  k_count_dead<<<grid(ctx, V), kBlock, 0, st>>>(s->last_t.p, V, cutoff, ctx.d_scalars + 13);
+  TWG_LAUNCHED(ctx);
+  u64 r[2];
+  read_scalars(ctx, ctx.d_scalars + 12, r, 2);
+  pt.mark("batch_fast");
+  if (r[1]) return nullptr;  // a node leaves: dense ids change
+  const u64 from = r[0];
+  s->m = O.m - from + n;
+  stats->evicted = from;
+  stats->dropped_late = 0;
+  w.max_ext = static_cast<i64>(V - 1);
+  return ingest_append(w, O, std::move(s), bS.p, bD.p, bT.p, n, from, cutoff);
+}
+
 }  // namespace
 
 void release_store(Store* s) {
@@ -982,13 +1085,27 @@ void window_ingest(Window& w, const i64* d_src, const i64* d_dst, const i64* d_t
   TWG_LAUNCHED(ctx);
   k_batch_stats<<<grid(ctx, n), kBlock, 0, st>>>(d_src, d_dst, d_t, n, ctx.d_scalars);
   TWG_LAUNCHED(ctx);
-  u64 sc[8];
-  read_scalars(ctx, ctx.d_scalars, sc, 8);
+  u64 sc[10];
+  read_scalars(ctx, ctx.d_scalars, sc, 10);
   const i64 batch_high = static_cast<i64>(sc[0]);
   const u64 batch_max_id = sc[1];
   w.batch_shape = static_cast<u32>(sc[7]);
   const i64 new_high = w.t_high > batch_high ? w.t_high : batch_high;
   const i64 cutoff = w.cutoff_for(new_high);
+  if (Store* fast = ingest_fast(w, d_src, d_dst, d_t, n, sc, cutoff, &stats)) {
+    stats.retained = fast->m;
+    stats.peak_bytes = old.device_bytes() + fast->device_bytes();
+    TWG_CUDA(cudaStreamSynchronize(st));
+    stats.rebuild_duration = std::chrono::duration<double>(clock::now() - started).count();
+    release_store(w.previous);
+    w.previous = w.store;
+    w.store = fast;
+    w.t_high = new_high;
+    w.stats = stats;
+    ++w.batch_count;
+    if (out) *out = stats;
+    return;
+  }
 
   // survivors (export_suffix) and admitted batch edges
   k_lower_bound<<<1, 1, 0, st>>>(old.e_t.p, old.m, cutoff, ctx.d_scalars + 2);
