@@ -234,6 +234,10 @@ def run_ours(args, rank, world, local_rank):
     total_ms = ev[0].elapsed_time(ev[-1])
     ingest_ms = sum(ev[1 + 3 * k].elapsed_time(ev[2 + 3 * k]) for k in range(args.steps))
     walk_ms = sum(ev[2 + 3 * k].elapsed_time(ev[3 + 3 * k]) for k in range(args.steps))
+    if os.environ.get("TWG_BENCH_VERBOSE") == "1":
+        for k in range(args.steps):
+            print(f"step {k}: ingest {ev[1 + 3 * k].elapsed_time(ev[2 + 3 * k]):7.2f} ms  "
+                  f"walk {ev[2 + 3 * k].elapsed_time(ev[3 + 3 * k]):7.2f} ms", file=sys.stderr)
     del bufs, buf, window  # the e2e pass builds its own window: free this one first
     ctx.sync()
     torch.cuda.empty_cache()

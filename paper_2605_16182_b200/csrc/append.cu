@@ -45,33 +45,37 @@ __device__ __forceinline__ u32 owner_of(int mode, const u32* s, const u32* d, u6
 
 unsigned grid(Ctx& ctx, u64 n) { return grid_for(n, kBlock, static_cast<unsigned>(ctx.sm_count) * 16); }
 
-// first k in [0, n) with t[k] >= x (one thread)
-__global__ void k_lb_time(const i64* t, u64 n, i64 x, u64* out) {
+// first k in [0, n) with t[zr(k)] >= x (one thread)
+__global__ void k_lb_time(const i64* t, Ring zr, u64 n, i64 x, u64* out) {
   u64 lo = 0, hi = n;
   while (lo < hi) {
     const u64 mid = (lo + hi) >> 1;
-    if (t[mid] < x) lo = mid + 1;
+    if (t[zr(static_cast<u32>(mid))] < x) lo = mid + 1;
     else hi = mid;
   }
   *out = lo;
 }
 
-__global__ void k_copy_cols(const u32* s, const u32* d, const i64* t, u64 n, u32* os, u32* od, i64* ot) {
+// survivors [from, from + n) of a snapshot (edge ring er) -> the start of a new log
+__global__ void k_copy_cols(const u32* s, const u32* d, const i64* t, Ring er, u64 from, u64 n, u32* os, u32* od,
+                            i64* ot) {
   for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<u64>(gridDim.x) * blockDim.x) {
-    os[i] = s[i];
-    od[i] = d[i];
-    ot[i] = t[i];
+    const u32 p = er(static_cast<u32>(from + i));
+    os[i] = s[p];
+    od[i] = d[p];
+    ot[i] = t[p];
   }
 }
 
 // surviving ts groups [g_cut, Z) of the old snapshot -> a fresh log
-__global__ void k_copy_groups(const u32* off, const i64* tt, u64 Z, const u64* g_cut, u32* ooff, i64* ott) {
+__global__ void k_copy_groups(const u32* off, const i64* tt, Ring zr, u64 Z, const u64* g_cut, u32* ooff, i64* ott) {
   const u64 g0 = *g_cut;
   for (u64 g = g0 + blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; g < Z;
        g += static_cast<u64>(gridDim.x) * blockDim.x) {
-    ooff[g - g0] = off[g];
-    ott[g - g0] = tt[g];
+    const u32 p = zr(static_cast<u32>(g));
+    ooff[g - g0] = off[p];
+    ott[g - g0] = tt[p];
   }
 }
 
@@ -79,25 +83,29 @@ __global__ void k_copy_groups(const u32* off, const i64* tt, u64 Z, const u64* g
 // the last survivor's time
 struct BatchGroupFn {
   const i64* t;
+  Ring br;                     // batch index -> slot of t
   const i64* last_survivor_t;  // null when there are no survivors
   __device__ __forceinline__ u32 operator()(u64 k) const {
-    if (k == 0) return last_survivor_t ? (t[0] != *last_survivor_t ? 1u : 0u) : 1u;
-    return t[k] != t[k - 1] ? 1u : 0u;
+    const i64 tk = t[br(static_cast<u32>(k))];
+    if (k == 0) return last_survivor_t ? (tk != *last_survivor_t ? 1u : 0u) : 1u;
+    return tk != t[br(static_cast<u32>(k - 1))] ? 1u : 0u;
   }
 };
 
 struct BatchGroupScatter {
   const i64* t;
+  Ring br;
   u32 seq_b;
-  u64 zbase;              // host-known write position, or
+  u64 zbase;              // host-known logical write position, or
   const u64* zbase_dev;   // device-resident one (fresh log: Z_old - g_cut)
+  u64 cap;                // ring slots
   u32* ts_off;
   i64* ts_time;
   __device__ __forceinline__ void operator()(u64 k, u64 g, u32 f) const {
     if (!f) return;
-    const u64 z = (zbase_dev ? *zbase_dev : zbase) + g;
+    const u64 z = ((zbase_dev ? *zbase_dev : zbase) + g) % cap;
     ts_off[z] = seq_b + static_cast<u32>(k);
-    ts_time[z] = t[k];
+    ts_time[z] = t[br(static_cast<u32>(k))];
   }
 };
 
@@ -130,22 +138,21 @@ __device__ __forceinline__ u32 gallop_lb(TimeAt at, u32 lo, u32 hi, i64 c) {
 
 __device__ __forceinline__ u32 entry_edge(int mode, u32 j) { return mode == TWG_UNDIRECTED ? (j >> 1) : j; }
 
-struct Rec {
-  u32 src, dst;
-  i64 t;
-};
+using Rec = BatchRec16;
 
 // the sorted batch into the log, plus a 16-byte record per edge for the
 // owner-ordered gathers
-__global__ void k_append_batch(const u32* s, const u32* d, const i64* t, u64 n, u32* os, u32* od, i64* ot, Rec* rec) {
+__global__ void k_append_batch(const u32* s, const u32* d, const i64* t, Ring br, u64 n, u32* os, u32* od, i64* ot,
+                               Ring wr, Rec* rec) {
   for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<u64>(gridDim.x) * blockDim.x) {
-    const u32 a = s[i], b = d[i];
-    const i64 x = t[i];
-    os[i] = a;
-    od[i] = b;
-    ot[i] = x;
-    rec[i] = Rec{a, b, x};
+    const u32 q = br(static_cast<u32>(i)), p = wr(static_cast<u32>(i));
+    const u32 a = s[q], b = d[q];
+    const i64 x = t[q];
+    os[p] = a;
+    od[p] = b;
+    ot[p] = x;
+    if (rec) rec[i] = Rec{a, b, x};
   }
 }
 
@@ -155,11 +162,13 @@ __device__ __forceinline__ u32 nbr_of(int mode, const Rec& r, u32 j) {
   return (j & 1) ? r.src : r.dst;  // side 1 (owner dst) -> src; self-loops give the owner
 }
 
-__global__ void k_owner_keys(const u32* s, const u32* d, u64 A, int mode, u32* keys, u32* vals) {
+__global__ void k_owner_keys(const Rec* rec, u64 A, int mode, u32* keys, u32* vals) {
   const u64 Yn = mode == TWG_UNDIRECTED ? 2 * A : A;
   for (u64 j = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; j < Yn;
        j += static_cast<u64>(gridDim.x) * blockDim.x) {
-    keys[j] = owner_of(mode, s, d, j);
+    const u32 k = mode == TWG_UNDIRECTED ? static_cast<u32>(j >> 1) : static_cast<u32>(j);
+    const Rec r = rec[k];
+    keys[j] = mode == TWG_UNDIRECTED ? ((j & 1) ? r.dst : r.src) : (mode == TWG_BACKWARD ? r.dst : r.src);
     vals[j] = static_cast<u32>(j);
   }
 }
@@ -220,12 +229,14 @@ struct PlanArgs {
   u64 V;
   const Entry* oent;
   const i64* omt;
+  const u32* oms;
   const u32* y;
   i64 cutoff;
+  int need_last;        // a batch time may equal a node's newest live time (mark merge)
   int relocate_all;     // repack every ring into a fresh arena
   u64 arena_cap;
   NodeMeta* plan;       // new bounds / ring; ee, ge = where the batch's entries / marks start
-  i64* last_t;          // time of the last live entry (valid iff plan.ee > plan.eb)
+  i64* last_t;          // time of the last live entry (valid iff need_last and plan.ee > plan.eb)
   Reloc* reloc;
   u64* scal;            // [0] bump, [1] overflow, [2] relocations
 };
@@ -247,9 +258,11 @@ __global__ void __launch_bounds__(kBlock) k_plan(PlanArgs a) {
       o = a.onm[v];
       y = a.y[v];
       const Ring oer = entry_ring(o), omr = mark_ring(o);
-      const i64 c = a.cutoff;
-      eb = evict_lb([&](u32 x) { return a.oent[oer(x)].t; }, o.eb, o.ee, c);
-      gb = evict_lb([&](u32 x) { return a.omt[omr(x)]; }, o.gb, o.ge, c);
+      // the first surviving mark starts the first surviving entry (a group is
+      // evicted whole: eviction is by time), so one search over the marks
+      // gives both bounds
+      gb = evict_lb([&](u32 x) { return a.omt[omr(x)]; }, o.gb, o.ge, a.cutoff);
+      eb = gb == o.ge ? o.ee : a.oms[omr(gb)];
       u32 low = o.eb;
       if (a.rnm) {
         const NodeMeta r = a.rnm[v];
@@ -260,7 +273,7 @@ __global__ void __launch_bounds__(kBlock) k_plan(PlanArgs a) {
         const u32 need = (o.ee - eb) + y;
         req = need + (a.relocate_all ? need / 2 : need) + 4;
       }
-      if (o.ee > eb) a.last_t[v] = a.oent[oer(o.ee - 1)].t;
+      if (a.need_last && o.ee > eb) a.last_t[v] = a.oent[oer(o.ee - 1)].t;
     }
     u32 tot, mtot;
     const u32 off = block_excl_scan<u32>(req, &tot);
@@ -358,7 +371,7 @@ __global__ void __launch_bounds__(kPB) k_bucket_place(PlaceArgs a) {
   sm.cap[t] = p.cap;
   sm.eorg[t] = p.eorg;
   sm.gorg[t] = p.gorg;
-  const bool has = valid && p.ee > p.eb && be > bs;
+  const bool has = valid && a.last_t && p.ee > p.eb && be > bs;
   sm.has_last[t] = has ? 1u : 0u;
   sm.last_t[t] = has ? a.last_t[v] : 0;
 
@@ -366,9 +379,22 @@ __global__ void __launch_bounds__(kPB) k_bucket_place(PlaceArgs a) {
   for (u32 c0 = bs; c0 < be; c0 += kChunk) {
     const u32 n = min(static_cast<u32>(kChunk), be - c0);
     __syncthreads();
-    for (u32 i = t; i < n; i += kPB) {
-      sm.key[i] = static_cast<u8>(a.keys[c0 + i] & (kPB - 1));
-      sm.val[i] = a.vals[c0 + i];
+    {
+      u32 kk[kChunkItems], vv[kChunkItems];
+#pragma unroll
+      for (int r = 0; r < kChunkItems; ++r) {
+        const u32 i = t + r * kPB;
+        kk[r] = i < n ? a.keys[c0 + i] : 0u;
+        vv[r] = i < n ? a.vals[c0 + i] : 0u;
+      }
+#pragma unroll
+      for (int r = 0; r < kChunkItems; ++r) {
+        const u32 i = t + r * kPB;
+        if (i < n) {
+          sm.key[i] = static_cast<u8>(kk[r] & (kPB - 1));
+          sm.val[i] = vv[r];
+        }
+      }
     }
     for (int i = t; i < (kPB / 32) * kPB; i += kPB) (&sm.wcnt[0][0])[i] = 0;
     __syncthreads();
@@ -400,21 +426,28 @@ __global__ void __launch_bounds__(kPB) k_bucket_place(PlaceArgs a) {
       if (t == 0) sm.off[kPB] = total;
     }
     __syncthreads();
+    {  // all gathers in flight before the staging stores
+      Rec b[kChunkItems];
+      u32 jj[kChunkItems];
 #pragma unroll
-    for (int r = 0; r < kChunkItems; ++r) {
-      const u32 i = warp * (32 * kChunkItems) + r * 32 + lane;
-      if (i < n) {
-        const u32 nd = sm.key[i];
-        const u32 sp = sm.off[nd] + sm.wcnt[warp][nd] + rank[r];
-        const u32 j = sm.val[i];
-        const u32 k = entry_edge(a.mode, j);
-        const Rec b = a.rec[k];
-        Entry e;
-        e.nbr = nbr_of(a.mode, b, j);
-        e.edge = a.seq_b + k;
-        e.t = b.t;
-        sm.sent[sp] = e;
-        sm.snode[sp] = static_cast<u8>(nd);
+      for (int r = 0; r < kChunkItems; ++r) {
+        const u32 i = warp * (32 * kChunkItems) + r * 32 + lane;
+        jj[r] = i < n ? sm.val[i] : 0u;
+        if (i < n) b[r] = a.rec[entry_edge(a.mode, jj[r])];
+      }
+#pragma unroll
+      for (int r = 0; r < kChunkItems; ++r) {
+        const u32 i = warp * (32 * kChunkItems) + r * 32 + lane;
+        if (i < n) {
+          const u32 nd = sm.key[i];
+          const u32 sp = sm.off[nd] + sm.wcnt[warp][nd] + rank[r];
+          Entry e;
+          e.nbr = nbr_of(a.mode, b[r], jj[r]);
+          e.edge = a.seq_b + entry_edge(a.mode, jj[r]);
+          e.t = b[r].t;
+          sm.sent[sp] = e;
+          sm.snode[sp] = static_cast<u8>(nd);
+        }
       }
     }
     __syncthreads();
@@ -493,8 +526,29 @@ bool append_enabled() {
 
 bool append_ingest_enabled() { return append_enabled(); }
 
+// O's log can take A more edges (and up to A groups) in place: O is the
+// log's newest slice, no snapshot older than the retired one holds it, and
+// the ring slots the batch reuses lie before every live slice (O, and the
+// retired R when it shares the log).
+bool log_room(const Store& O, const Store* R, u64 A) {
+  const EdgeLog* L = O.gapped ? O.log.get() : nullptr;
+  if (!L || L->len != O.log_first + O.m) return false;
+  const bool shared = R && R->gapped && R->log.get() == L;
+  if (O.log.use_count() > (shared ? 2 : 1)) return false;
+  const u64 lo = shared ? std::min(O.log_first, R->log_first) : O.log_first;
+  const u64 zlo = shared ? std::min(O.ts_first, R->ts_first) : O.ts_first;
+  return (L->len + A) - lo <= L->cap && (L->zlen + A) - zlo <= L->cap;
+}
+
+bool append_log_slot(const Store& O, const Store* R, u64 A, Ring* wr) {
+  if (!log_room(O, R, A)) return false;
+  *wr = log_ring(O.log->cap, O.log_first + O.m);  // == the new slice start (O.log_first + from) + survivors
+  return true;
+}
+
 Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const u32* bS, const u32* bD,
-                     const i64* bT, u64 A, u64 from, i64 cutoff) {
+                     const i64* bT, Ring bring, u64 A, u64 from, i64 cutoff, bool no_ties, const BatchRec16* rec_in,
+                     bool in_log) {
   Ctx& ctx = *w.ctx;
   cudaStream_t st = ctx.stream;
   PhaseTimer pt(ctx, "ingest_append");
@@ -508,34 +562,40 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
   u64* sc = ctx.d_scalars + 32;  // 32..47 private to this path
   TWG_CUDA(cudaMemsetAsync(sc, 0, 16 * sizeof(u64), st));
   const u64* d_gcut = sc + 9;  // first surviving ts group of O
-  k_lb_time<<<1, 1, 0, st>>>(O.ts_time.p, O.Z, cutoff, sc + 9);
+  k_lb_time<<<1, 1, 0, st>>>(O.ts_time.p, O.view().zrg, O.Z, cutoff, sc + 9);
   TWG_LAUNCHED(ctx);
 
   // 1. edge log + ts groups
-  std::shared_ptr<EdgeLog> log = O.gapped ? O.log : nullptr;
-  const bool in_place = log && log->len == O.log_first + O.m && log->len + A <= log->cap;
+  const Store* R = w.previous;
+  const bool in_place = log_room(O, R, A);
+  if (in_log && !in_place) fail(TWG_ECUDA, "ingest_append: batch staged in a log without room");
+  std::shared_ptr<EdgeLog> log = in_place ? O.log : nullptr;
   const u32 seq0 = O.seq0 + static_cast<u32>(from);
   const u32 seq_b = seq0 + static_cast<u32>(S);
+  const StoreView ov = O.view();
   u64 zbase = 0;
   const u64* zbase_dev = nullptr;
   if (in_place) {
     s->log_first = O.log_first + from;
     zbase = log->zlen;
-  } else {
+  } else {  // a new log (first streaming batch, window growth, or an older snapshot holding the log)
     auto nl = std::make_shared<EdgeLog>();
-    nl->cap = m + 8 * A;
+    nl->cap = std::max<u64>((3 * m) / 2 + 2 * A, 1024);
     nl->src.alloc(nl->cap, st);
     nl->dst.alloc(nl->cap, st);
     nl->t.alloc(nl->cap, st);
     nl->ts_off.alloc(nl->cap, st);
     nl->ts_time.alloc(nl->cap, st);
-    nl->seq0 = seq0;
-    k_copy_cols<<<grid(ctx, S), kBlock, 0, st>>>(O.e_src.p + from, O.e_dst.p + from, O.e_t.p + from, S, nl->src.p,
-                                                 nl->dst.p, nl->t.p);
-    TWG_LAUNCHED(ctx);
-    k_copy_groups<<<grid(ctx, O.Z), kBlock, 0, st>>>(O.ts_off.p, O.ts_time.p, O.Z, d_gcut, nl->ts_off.p,
-                                                     nl->ts_time.p);
-    TWG_LAUNCHED(ctx);
+    if (S) {
+      k_copy_cols<<<grid(ctx, S), kBlock, 0, st>>>(O.e_src.p, O.e_dst.p, O.e_t.p, ov.erg, from, S, nl->src.p,
+                                                   nl->dst.p, nl->t.p);
+      TWG_LAUNCHED(ctx);
+    }
+    if (O.Z) {
+      k_copy_groups<<<grid(ctx, O.Z), kBlock, 0, st>>>(O.ts_off.p, O.ts_time.p, ov.zrg, O.Z, d_gcut, nl->ts_off.p,
+                                                       nl->ts_time.p);
+      TWG_LAUNCHED(ctx);
+    }
     k_zbase<<<1, 1, 0, st>>>(O.Z, d_gcut, sc + 4);
     TWG_LAUNCHED(ctx);
     zbase_dev = sc + 4;
@@ -543,13 +603,21 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
     log = std::move(nl);
     s->log_first = 0;
   }
-  const u64 lpos = s->log_first + S;  // log index of batch edge 0
-  DevBuf<Rec> brec(A, st);  // one 16-byte gather per placed entry
-  k_append_batch<<<grid(ctx, A), kBlock, 0, st>>>(bS, bD, bT, A, log->src.p + lpos, log->dst.p + lpos,
-                                                  log->t.p + lpos, brec.p);
-  TWG_LAUNCHED(ctx);
-  scan_scatter(ctx, BatchGroupFn{bT, S ? O.e_t.p + (O.m - 1) : nullptr}, A, sc + 5,
-               BatchGroupScatter{bT, seq_b, zbase, zbase_dev, log->ts_off.p, log->ts_time.p});
+  const u64 lpos = s->log_first + S;  // logical log position of batch edge 0
+  const Ring wr = log_ring(log->cap, lpos);
+  DevBuf<Rec> brec_own;
+  const Rec* brec = rec_in;
+  if (!brec || !in_log) {
+    if (!brec) brec_own.alloc(A, st);
+    k_append_batch<<<grid(ctx, A), kBlock, 0, st>>>(bS, bD, bT, bring, A, log->src.p, log->dst.p, log->t.p, wr,
+                                                    brec ? nullptr : brec_own.p);
+    TWG_LAUNCHED(ctx);
+    if (!brec) brec = brec_own.p;
+  }
+  const i64* last_surv = nullptr;  // the last survivor's time: the first batch group merges with it on a tie
+  if (S) last_surv = O.e_t.p + (O.gapped ? (O.log_first + O.m - 1) % O.log->cap : O.m - 1);
+  scan_scatter(ctx, BatchGroupFn{bT, bring, last_surv}, A, sc + 5,
+               BatchGroupScatter{bT, bring, seq_b, zbase, zbase_dev, log->cap, log->ts_off.p, log->ts_time.p});
   pt.mark("log+ts");
 
   // 2. batch entries grouped into 256-node buckets: stable radix sort of
@@ -562,7 +630,7 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
   u32* ka = k1.p;
   u32* vp = v0.p;
   u32* va = v1.p;
-  k_owner_keys<<<grid(ctx, Yn), kBlock, 0, st>>>(bS, bD, A, mode, kp, vp);
+  k_owner_keys<<<grid(ctx, Yn), kBlock, 0, st>>>(brec, A, mode, kp, vp);
   TWG_LAUNCHED(ctx);
   if (vb > static_cast<int>(kBucketShift)) radix_sort_pairs<u32>(ctx, &kp, &ka, &vp, &va, Yn, vb, kBucketShift);
   DevBuf<u32> bstart(nb + 1, st);
@@ -579,7 +647,6 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
   k_bucket_count<<<static_cast<unsigned>(nb), kPB, 0, st>>>(kp, bstart.p, V, ycnt.p);
   TWG_LAUNCHED(ctx);
   std::shared_ptr<NodeArena> arena = O.gapped ? O.arena : nullptr;
-  const Store* R = w.previous;
   // a snapshot older than the retired one still holding this arena may read
   // any slot: then nothing of it is reused (fresh arena)
   if (arena) {
@@ -598,7 +665,9 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
     pa.V = V;
     pa.oent = O.ent.p;
     pa.omt = O.mk_time.p;
+    pa.oms = O.mk_start.p;
     pa.y = ycnt.p;
+    pa.need_last = no_ties ? 0 : 1;
     pa.cutoff = cutoff;
     pa.relocate_all = all ? 1 : 0;
     pa.arena_cap = dst.cap;
@@ -646,11 +715,11 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
   PlaceArgs pl;
   pl.V = V;
   pl.plan = plan.p;
-  pl.last_t = last_t.p;
+  pl.last_t = no_ties ? nullptr : last_t.p;
   pl.keys = kp;
   pl.vals = vp;
   pl.bstart = bstart.p;
-  pl.rec = brec.p;
+  pl.rec = brec;
   pl.mode = mode;
   pl.seq_b = seq_b;
   pl.ent = arena->ent.p;
@@ -678,11 +747,16 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
   s->m = m;
   s->Z = Z;
   s->Q = Q;
-  s->e_src.alias(log->src.p + s->log_first, m);
-  s->e_dst.alias(log->dst.p + s->log_first, m);
-  s->e_t.alias(log->t.p + s->log_first, m);
-  s->ts_off.alias(log->ts_off.p + s->ts_first, Z);
-  s->ts_time.alias(log->ts_time.p + s->ts_first, Z);
+  s->e_src.alias(log->src.p, log->cap);
+  s->e_dst.alias(log->dst.p, log->cap);
+  s->e_t.alias(log->t.p, log->cap);
+  s->ts_off.alias(log->ts_off.p, log->cap);
+  s->ts_time.alias(log->ts_time.p, log->cap);
+  const Ring er = log_ring(log->cap, s->log_first), zr = log_ring(log->cap, s->ts_first);
+  s->e_cap = er.cap;
+  s->e_org = er.org;
+  s->z_cap = zr.cap;
+  s->z_org = zr.org;
   s->ent.alias(arena->ent.p, arena->cap);
   s->mk_time.alias(arena->mk_time.p, arena->cap);
   s->mk_start.alias(arena->mk_start.p, arena->cap);

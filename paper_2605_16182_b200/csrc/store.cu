@@ -447,10 +447,24 @@ __global__ void k_pack_nmeta(const u32* off, const u32* goff, u64 V, uint2* nmet
     nmeta[v] = make_uint2(off[v], goff[v]);
 }
 
-__global__ void k_ts_rebase(const u32* ts_off, u64 Z, u32 seq0, u64 m, u32* out) {
+__global__ void k_ts_rebase(const u32* ts_off, const i64* ts_time, Ring zr, u64 Z, u32 seq0, u64 m, u32* out,
+                            i64* tout) {
   for (u64 g = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; g <= Z;
-       g += static_cast<u64>(gridDim.x) * blockDim.x)
-    out[g] = g < Z ? ts_off[g] - seq0 : static_cast<u32>(m);
+       g += static_cast<u64>(gridDim.x) * blockDim.x) {
+    out[g] = g < Z ? ts_off[zr(static_cast<u32>(g))] - seq0 : static_cast<u32>(m);
+    if (g < Z) tout[g] = ts_time[zr(static_cast<u32>(g))];
+  }
+}
+
+// ring slice of the edge log -> contiguous columns
+__global__ void k_unring_edges(const u32* s, const u32* d, const i64* t, Ring er, u64 m, u32* os, u32* od, i64* ot) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < m;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const u32 p = er(static_cast<u32>(i));
+    os[i] = s[p];
+    od[i] = d[p];
+    ot[i] = t[p];
+  }
 }
 
 // gapped regions -> contiguous regions, one warp per node (lanes stride the
@@ -508,14 +522,20 @@ Store& ensure_compact(Ctx& ctx, const Store& g) {
   c->P = g.P;
   c->ext_identity = g.ext_identity;
   c->seq0 = 0;
-  c->e_src.alias(g.e_src.p, g.e_src.n);
-  c->e_dst.alias(g.e_dst.p, g.e_dst.n);
-  c->e_t.alias(g.e_t.p, g.e_t.n);
   c->ext.alias(g.ext.p, g.ext.n);
   c->last_t.alias(g.last_t.p, g.last_t.n);
-  c->ts_time.alias(g.ts_time.p, g.ts_time.n);
+  c->e_src.alloc(g.m ? g.m : 1, st);
+  c->e_dst.alloc(g.m ? g.m : 1, st);
+  c->e_t.alloc(g.m ? g.m : 1, st);
+  if (g.m) {
+    k_unring_edges<<<grid(ctx, g.m), kBlock, 0, st>>>(g.e_src.p, g.e_dst.p, g.e_t.p, Ring{0u, g.e_cap, g.e_org}, g.m,
+                                                      c->e_src.p, c->e_dst.p, c->e_t.p);
+    TWG_LAUNCHED(ctx);
+  }
+  c->ts_time.alloc(g.Z ? g.Z : 1, st);
   c->ts_off.alloc(g.Z + 1, st);
-  k_ts_rebase<<<grid(ctx, g.Z + 1), kBlock, 0, st>>>(g.ts_off.p, g.Z, g.seq0, g.m, c->ts_off.p);
+  k_ts_rebase<<<grid(ctx, g.Z + 1), kBlock, 0, st>>>(g.ts_off.p, g.ts_time.p, Ring{0u, g.z_cap, g.z_org}, g.Z, g.seq0,
+                                                     g.m, c->ts_off.p, c->ts_time.p);
   TWG_LAUNCHED(ctx);
   const u64 V = g.V;
   DevBuf<u32> off(V + 1, st), goff(V + 1, st);

@@ -83,12 +83,20 @@ struct StoreView {
   const u32* adj;
   int ext_identity;  // ext[v] == v for all v (the id map can be skipped)
   u32 seq0;
+  Ring erg;  // snapshot edge i -> slot erg(i) of e_src/e_dst/e_t (identity in contiguous stores)
+  Ring zrg;  // snapshot ts group g -> slot zrg(g) of ts_off/ts_time
 };
 
 // Edge range [lo, hi) (snapshot-relative) of timestamp group g < Z.
 __device__ __forceinline__ void ts_group_range(const StoreView& s, u64 g, u64& lo, u64& hi) {
-  lo = static_cast<u32>(s.ts_off[g] - s.seq0);
-  hi = g + 1 < s.Z ? static_cast<u64>(static_cast<u32>(s.ts_off[g + 1] - s.seq0)) : s.m;
+  lo = static_cast<u32>(s.ts_off[s.zrg(static_cast<u32>(g))] - s.seq0);
+  hi = g + 1 < s.Z ? static_cast<u64>(static_cast<u32>(s.ts_off[s.zrg(static_cast<u32>(g + 1))] - s.seq0)) : s.m;
+}
+
+// host: the ring slot of relative index i of a log slice starting at logical
+// position `first` (slots = logical mod cap)
+inline Ring log_ring(u64 cap, u64 first) {
+  return Ring{0u, static_cast<u32>(cap), static_cast<u32>(0u - static_cast<u32>(first % cap))};
 }
 
 struct BuildOpts {
@@ -113,15 +121,14 @@ struct BuildOpts {
 // Nothing a live snapshot can read is ever overwritten: a ring only accepts
 // new entries while ee + y - (oldest live eb in that ring) <= cap, and a
 // replaced log/arena stays alive (shared_ptr) while any snapshot uses it.
-struct EdgeLog {
+struct EdgeLog {  // two rings of `cap` slots; positions are logical (slot = position mod cap)
   DevBuf<u32> src, dst;
   DevBuf<i64> t;
   DevBuf<u32> ts_off;  // group start sequence numbers
   DevBuf<i64> ts_time;
   u64 cap = 0;     // edges (and groups)
-  u64 len = 0;     // edges written
-  u64 zlen = 0;    // groups written
-  u32 seq0 = 0;    // sequence number of log index 0
+  u64 len = 0;     // edges written (logical end)
+  u64 zlen = 0;    // groups written (logical end)
 };
 
 struct NodeArena {
@@ -159,8 +166,9 @@ struct Store {
   bool gapped = false;
   std::shared_ptr<EdgeLog> log;
   std::shared_ptr<NodeArena> arena;
-  u64 log_first = 0;  // log index of edge 0
-  u64 ts_first = 0;   // log group index of group 0
+  u64 log_first = 0;  // logical log position of edge 0
+  u64 ts_first = 0;   // logical log group position of group 0
+  u32 e_cap = kIdentityCap, e_org = 0, z_cap = kIdentityCap, z_org = 0;  // StoreView::erg / zrg
   // contiguous materialisation of a gapped store (reference layout), built on
   // first use by the accessors / downloads / weighted views (ensure_compact)
   mutable std::unique_ptr<Store> compact;
@@ -170,7 +178,8 @@ struct Store {
     return StoreView{mode,     m,         V,         Z,          P,         Q,        A,
                      e_src.p,  e_dst.p,   e_t.p,     ext.p,      ts_off.p,  ts_time.p,
                      ts_w.p,   nmeta.p,   nm.p,      mk_time.p,  mk_start.p, ent.p,   wp.p,
-                     adj_off.p, adj.p,  ext_identity ? 1 : 0, seq0};
+                     adj_off.p, adj.p,  ext_identity ? 1 : 0, seq0,
+                     Ring{0u, e_cap, e_org}, Ring{0u, z_cap, z_org}};
   }
   u64 device_bytes() const {
     return e_src.bytes() + e_dst.bytes() + e_t.bytes() + ext.bytes() + ts_off.bytes() +

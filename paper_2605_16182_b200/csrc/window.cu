@@ -116,7 +116,7 @@ template <bool kTimeOrdered>
 __device__ __forceinline__ void agg_max(i64* last, u32 key, i64 t, bool valid);
 
 __global__ void k_batch_fast(const i64* bs, const i64* bd, const i64* bt, u64 n, u32* os, u32* od, i64* ot,
-                             i64* last) {
+                             Ring orr, BatchRec16* rec, i64* last) {
   for (u64 k0 = blockIdx.x * static_cast<u64>(blockDim.x); k0 < n; k0 += static_cast<u64>(gridDim.x) * blockDim.x) {
     const u64 k = k0 + threadIdx.x;
     const bool valid = k < n;
@@ -134,9 +134,12 @@ __global__ void k_batch_fast(const i64* bs, const i64* bd, const i64* bt, u64 n,
         key[j] = x;
       }
       for (int j = 0; j < len; ++j) {
-        os[k + j] = static_cast<u32>(key[j] >> 32);
-        od[k + j] = static_cast<u32>(key[j]);
-        ot[k + j] = tk;
+        const u32 a = static_cast<u32>(key[j] >> 32), b = static_cast<u32>(key[j]);
+        const u32 p = orr(static_cast<u32>(k + j));
+        os[p] = a;
+        od[p] = b;
+        ot[p] = tk;
+        rec[k + j] = BatchRec16{a, b, tk};
       }
     }
     agg_max<true>(last, valid ? static_cast<u32>(bs[k < n ? k : 0]) : 0u, tk, valid);
@@ -154,12 +157,12 @@ __global__ void k_count_dead(const i64* last, u64 V, i64 cutoff, u64* dead) {
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(reinterpret_cast<unsigned long long*>(dead), c);
 }
 
-// lower_bound(time_, cutoff) (edge_store.cpp:326)
-__global__ void k_lower_bound(const i64* t, u64 m, i64 cutoff, u64* out) {
+// lower_bound(time_, cutoff) (edge_store.cpp:326) over the snapshot's edge ring
+__global__ void k_lower_bound(const i64* t, Ring er, u64 m, i64 cutoff, u64* out) {
   u64 lo = 0, hi = m;
   while (lo < hi) {
     const u64 mid = (lo + hi) >> 1;
-    if (t[mid] < cutoff) lo = mid + 1;
+    if (t[er(static_cast<u32>(mid))] < cutoff) lo = mid + 1;
     else hi = mid;
   }
   *out = lo;
@@ -363,8 +366,9 @@ struct SurvivorKey {
   const i64* e_t;
   const u32* o2n;
   u64 from;
+  Ring er;
   __device__ __forceinline__ K3 operator()(u64 i) const {
-    const u64 p = from + i;
+    const u32 p = er(static_cast<u32>(from + i));
     return K3{e_t[p], (static_cast<u64>(remap(o2n, e_src[p])) << 32) | remap(o2n, e_dst[p])};
   }
 };
@@ -840,7 +844,8 @@ Store* ingest_streaming(Window& w, const i64* bs, const i64* bd, const i64* bt, 
   // of a merge-path pass.
   bool concat = A == 0 || S == 0;
   if (!concat) {
-    k_concat_check<<<1, 1, 0, st>>>(SurvivorKey{Og.e_src.p, Og.e_dst.p, Og.e_t.p, o2n, from}, S, BatchKey{bS.p, bD.p, bT.p},
+    k_concat_check<<<1, 1, 0, st>>>(SurvivorKey{Og.e_src.p, Og.e_dst.p, Og.e_t.p, o2n, from, Og.view().erg}, S,
+                                    BatchKey{bS.p, bD.p, bT.p},
                                     ctx.d_scalars + 11);
     TWG_LAUNCHED(ctx);
     u64 c[1];
@@ -852,7 +857,7 @@ Store* ingest_streaming(Window& w, const i64* bs, const i64* bd, const i64* bt, 
   if (concat && identity && A > 0 && append_ingest_enabled()) {
     pt.mark("append_handoff");
     if (scratch_out) *scratch_out = scratch + 48 * (w.mode == TWG_UNDIRECTED ? 2 * A : A) + 40 * Vn;
-    return ingest_append(w, Og, std::move(s), bS.p, bD.p, bT.p, A, from, cutoff);
+    return ingest_append(w, Og, std::move(s), bS.p, bD.p, bT.p, Ring{0u, kIdentityCap, 0u}, A, from, cutoff, false);
   }
   const Store& O = ensure_compact(ctx, Og);  // the rewrite routes below read the contiguous node view
   s->e_src.alloc(s->m ? s->m : 1, st);
@@ -874,7 +879,8 @@ Store* ingest_streaming(Window& w, const i64* bs, const i64* bd, const i64* bt, 
     spos.alloc(S ? S : 1, st);
     bpos.alloc(A ? A : 1, st);
     scratch += 4 * (S + A);
-    merge_path<K3>(ctx, SurvivorKey{O.e_src.p, O.e_dst.p, O.e_t.p, o2n, from}, S, BatchKey{bS.p, bD.p, bT.p}, A,
+    merge_path<K3>(ctx, SurvivorKey{O.e_src.p, O.e_dst.p, O.e_t.p, o2n, from, O.view().erg}, S,
+                   BatchKey{bS.p, bD.p, bT.p}, A,
                    CanonicalEmit{s->e_src.p, s->e_dst.p, s->e_t.p, spos.p, bpos.p});
   }
   pt.mark(concat ? "canonical_concat" : "canonical_merge");
@@ -1013,12 +1019,30 @@ Store* ingest_fast(Window& w, const i64* bs, const i64* bd, const i64* bt, u64 n
   TWG_CUDA(cudaMemcpyAsync(s->ext.p, O.ext.p, V * sizeof(i64), cudaMemcpyDeviceToDevice, st));
   s->last_t.alloc(V, st);
   TWG_CUDA(cudaMemcpyAsync(s->last_t.p, O.last_t.p, V * sizeof(i64), cudaMemcpyDeviceToDevice, st));
-  DevBuf<u32> bS(n, st), bD(n, st);
-  DevBuf<i64> bT(n, st);
+  // the canonical batch goes straight into the shared log when it has room
+  Ring wring{0u, kIdentityCap, 0u};
+  const bool in_log = append_log_slot(O, w.previous, n, &wring);
+  DevBuf<u32> tS, tD;
+  DevBuf<i64> tT;
+  u32 *bS, *bD;
+  i64* bT;
+  if (in_log) {
+    bS = O.log->src.p;
+    bD = O.log->dst.p;
+    bT = O.log->t.p;
+  } else {
+    tS.alloc(n, st);
+    tD.alloc(n, st);
+    tT.alloc(n, st);
+    bS = tS.p;
+    bD = tD.p;
+    bT = tT.p;
+  }
+  DevBuf<BatchRec16> rec(n, st);
   TWG_CUDA(cudaMemsetAsync(ctx.d_scalars + 12, 0, 16, st));
-  k_lower_bound<<<1, 1, 0, st>>>(O.e_t.p, O.m, cutoff, ctx.d_scalars + 12);
+  k_lower_bound<<<1, 1, 0, st>>>(O.e_t.p, O.view().erg, O.m, cutoff, ctx.d_scalars + 12);
   TWG_LAUNCHED(ctx);
-  k_batch_fast<<<grid(ctx, n), kBlock, 0, st>>>(bs, bd, bt, n, bS.p, bD.p, bT.p, s->last_t.p);
+  k_batch_fast<<<grid(ctx, n), kBlock, 0, st>>>(bs, bd, bt, n, bS, bD, bT, wring, rec.p, s->last_t.p);
   TWG_LAUNCHED(ctx);
   k_count_dead<<<grid(ctx, V), kBlock, 0, st>>>(s->last_t.p, V, cutoff, ctx.d_scalars + 13);
   TWG_LAUNCHED(ctx);
@@ -1031,7 +1055,7 @@ Store* ingest_fast(Window& w, const i64* bs, const i64* bd, const i64* bt, u64 n
   stats->evicted = from;
   stats->dropped_late = 0;
   w.max_ext = static_cast<i64>(V - 1);
-  return ingest_append(w, O, std::move(s), bS.p, bD.p, bT.p, n, from, cutoff);
+  return ingest_append(w, O, std::move(s), bS, bD, bT, wring, n, from, cutoff, true, rec.p, in_log);
 }
 
 }  // namespace
@@ -1108,7 +1132,7 @@ void window_ingest(Window& w, const i64* d_src, const i64* d_dst, const i64* d_t
   }
 
   // survivors (export_suffix) and admitted batch edges
-  k_lower_bound<<<1, 1, 0, st>>>(old.e_t.p, old.m, cutoff, ctx.d_scalars + 2);
+  k_lower_bound<<<1, 1, 0, st>>>(old.e_t.p, old.view().erg, old.m, cutoff, ctx.d_scalars + 2);
   TWG_LAUNCHED(ctx);
   DevBuf<u32> pos(n + 1, st);
   exclusive_scan<u32>(ctx, AdmitFn{d_t, cutoff}, n, pos.p);
@@ -1137,7 +1161,8 @@ void window_ingest(Window& w, const i64* d_src, const i64* d_dst, const i64* d_t
   } else {
     DevBuf<i64> ms(total ? total : 1, st), md(total ? total : 1, st), mt(total ? total : 1, st);
     if (survivors) {
-      k_gather_survivors<<<grid(ctx, survivors), kBlock, 0, st>>>(old.view(), from, ms.p, md.p, mt.p);
+      k_gather_survivors<<<grid(ctx, survivors), kBlock, 0, st>>>(ensure_compact(ctx, old).view(), from, ms.p, md.p,
+                                                                  mt.p);
       TWG_LAUNCHED(ctx);
     }
     if (admitted) {
