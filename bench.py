@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--scale", type=float, default=1.0, help="workload scale (1.0 = C5)")
     ap.add_argument("--variant", default="fullwalk", choices=["fullwalk", "coop", "coopdirect"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--pipelined", action="store_true",
+                    help="headline pass with the walks of batch k overlapping the ingest of k+1 on a second stream "
+                         "(measured slower than back to back on B200: both phases compete for HBM)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -139,8 +142,10 @@ def run_ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     wl = Workload(args.scale)
-    ctx = tw.Context(local_rank)
+    ctx = tw.Context(local_rank, priority=1)  # ingest: the pipeline's critical path
     stream = torch.cuda.ExternalStream(ctx.stream)
+    ctx_w = tw.Context(local_rank)  # walk stream: overlaps the next batch's ingest in the pipelined pass
+    wstream = torch.cuda.ExternalStream(ctx_w.stream)
     variant = {"fullwalk": tw.Variant.FullWalk, "coop": tw.Variant.Coop, "coopdirect": tw.Variant.CoopDirect}[
         args.variant]
     B = wl.batch_edges
@@ -193,52 +198,127 @@ def run_ours(args, rank, world, local_rank):
         st, ws = step(window, buf)
         del ws
         b += 1
-    # pre-generate the K timed batches into HBM (inputs resident before timing)
-    bufs = []
-    for k in range(args.steps):
-        x = new_buf()
-        if rank == 0:
-            synth(x, b + k)
-        bufs.append(x)
-    ctx.sync()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    clocks = ClockSampler(local_rank)
-    clocks.start()
-    launches0 = ctx.launches
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3 * args.steps + 2)]
-    hops = 0
-    alg_bytes = 0
-    ingest_alg = 0
-    ev[0].record(stream)
-    for k in range(args.steps):
-        bcast(bufs[k])
-        ev[1 + 3 * k].record(stream)
-        bst = window.ingest_batch_device(bufs[k][0].data_ptr(), bufs[k][1].data_ptr(), bufs[k][2].data_ptr(), B,
-                                         stats=True)
-        ev[2 + 3 * k].record(stream)
-        snap = window.snapshot()
-        st = tw.WalkStats()
-        ws = tw.generate_walks(snap, walk_cfg(), variant=variant, stats=st)
-        ev[3 + 3 * k].record(stream)
-        hops += st.hops
-        alg_bytes += st.alg_bytes
-        ingest_alg += batch_alg_bytes(snap.info, bst, B)
-        del ws, snap
-    ev[-1].record(stream)
-    ctx.sync()
-    torch.cuda.synchronize()
-    launches = ctx.launches - launches0
-    clk = clocks.stop()
-    total_ms = ev[0].elapsed_time(ev[-1])
-    ingest_ms = sum(ev[1 + 3 * k].elapsed_time(ev[2 + 3 * k]) for k in range(args.steps))
-    walk_ms = sum(ev[2 + 3 * k].elapsed_time(ev[3 + 3 * k]) for k in range(args.steps))
-    if os.environ.get("TWG_BENCH_VERBOSE") == "1":
+    def timed_pass(pipelined, b):
+        """K steps of batches b..b+K-1, inputs pre-generated in HBM, timed with
+        device events. Sequential: ingest then walks per batch on one stream.
+        Pipelined: the walks of batch k run on a second stream (own context)
+        while batch k+1 is ingested; ingest k+2 waits for walks k (the window
+        protects only the current and the retired snapshot). Every batch is
+        ingested and walked in full either way."""
+        bufs = []
         for k in range(args.steps):
-            print(f"step {k}: ingest {ev[1 + 3 * k].elapsed_time(ev[2 + 3 * k]):7.2f} ms  "
-                  f"walk {ev[2 + 3 * k].elapsed_time(ev[3 + 3 * k]):7.2f} ms", file=sys.stderr)
-    del bufs, buf, window  # the e2e pass builds its own window: free this one first
+            x = new_buf()
+            if rank == 0:
+                synth(x, b + k)
+            bufs.append(x)
+        ctx.sync()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        clocks = ClockSampler(local_rank)
+        clocks.start()
+        launches0 = ctx.launches + ctx_w.launches
+        hops = alg_bytes = ingest_alg = 0
+        if not pipelined:
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3 * args.steps + 2)]
+            ev[0].record(stream)
+            for k in range(args.steps):
+                bcast(bufs[k])
+                ev[1 + 3 * k].record(stream)
+                bst = window.ingest_batch_device(bufs[k][0].data_ptr(), bufs[k][1].data_ptr(),
+                                                 bufs[k][2].data_ptr(), B, stats=True)
+                ev[2 + 3 * k].record(stream)
+                snap = window.snapshot()
+                st = tw.WalkStats()
+                ws = tw.generate_walks(snap, walk_cfg(), variant=variant, stats=st)
+                ev[3 + 3 * k].record(stream)
+                hops += st.hops
+                alg_bytes += st.alg_bytes
+                ingest_alg += batch_alg_bytes(snap.info, bst, B)
+                del ws, snap
+            ev[-1].record(stream)
+            ctx.sync()
+            torch.cuda.synchronize()
+            total_ms = ev[0].elapsed_time(ev[-1])
+            ing_ms = [ev[1 + 3 * k].elapsed_time(ev[2 + 3 * k]) for k in range(args.steps)]
+            walk_ms_k = [ev[2 + 3 * k].elapsed_time(ev[3 + 3 * k]) for k in range(args.steps)]
+        else:
+            import queue
+            import threading
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            iev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(args.steps)]
+            wev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(args.steps)]
+            ready = queue.Queue()
+            done = [threading.Event() for _ in range(args.steps)]
+            res = [None] * args.steps
+            err = []
+
+            def walker():
+                try:
+                    for k in range(args.steps):
+                        snap, bst = ready.get()
+                        wev[k][0].record(wstream)
+                        st = tw.WalkStats()
+                        ws = tw.generate_walks(snap, walk_cfg(), variant=variant, stats=st, ctx=ctx_w)
+                        wev[k][1].record(wstream)
+                        res[k] = (st.hops, st.alg_bytes, batch_alg_bytes(snap.info, bst, B))
+                        del ws, snap
+                        done[k].set()
+                except Exception as e:  # surfaced in the main thread
+                    err.append(e)
+                    for d in done:
+                        d.set()
+
+            th = threading.Thread(target=walker, daemon=True)
+            ev0.record(stream)
+            th.start()
+            for k in range(args.steps):
+                if k >= 2:
+                    done[k - 2].wait()
+                bcast(bufs[k])
+                iev[k][0].record(stream)
+                bst = window.ingest_batch_device(bufs[k][0].data_ptr(), bufs[k][1].data_ptr(),
+                                                 bufs[k][2].data_ptr(), B, stats=True)
+                iev[k][1].record(stream)
+                ready.put((window.snapshot(), bst))
+            th.join()
+            if err:
+                raise err[0]
+            stream.wait_event(wev[-1][1])
+            ev1.record(stream)
+            ctx.sync()
+            ctx_w.sync()
+            torch.cuda.synchronize()
+            total_ms = ev0.elapsed_time(ev1)
+            ing_ms = [iev[k][0].elapsed_time(iev[k][1]) for k in range(args.steps)]
+            walk_ms_k = [wev[k][0].elapsed_time(wev[k][1]) for k in range(args.steps)]
+            for h, a, ia in res:
+                hops += h
+                alg_bytes += a
+                ingest_alg += ia
+        launches = ctx.launches + ctx_w.launches - launches0
+        clk = clocks.stop()
+        if os.environ.get("TWG_BENCH_VERBOSE") == "1":
+            for k in range(args.steps):
+                print(f"{'pipelined' if pipelined else 'sequential'} step {k}: ingest {ing_ms[k]:7.2f} ms  "
+                      f"walk {walk_ms_k[k]:7.2f} ms", file=sys.stderr)
+        del bufs
+        return dict(total_ms=total_ms, ingest_ms=sum(ing_ms), walk_ms=sum(walk_ms_k), hops=hops,
+                    alg_bytes=alg_bytes, ingest_alg=ingest_alg, launches=launches, clocks=clk)
+
+    # sequential pass: the headline, per-phase times and the rooflines (each
+    # kernel alone on the GPU); --pipelined adds an overlapped headline pass
+    seq = timed_pass(False, b)
+    b += args.steps
+    head = timed_pass(True, b) if args.pipelined else seq
+    total_ms, launches, clk = head["total_ms"], head["launches"], head["clocks"]
+    hops, alg_bytes, ingest_alg = head["hops"], seq["alg_bytes"], seq["ingest_alg"]
+    ingest_ms, walk_ms = seq["ingest_ms"], seq["walk_ms"]
+    seq_total_ms, seq_hops = seq["total_ms"], seq["hops"]
+    ctx_w.sync()
+    del buf, window  # the e2e pass builds its own window: free this one first
     ctx.sync()
     torch.cuda.empty_cache()
 
@@ -262,7 +342,8 @@ def run_ours(args, rank, world, local_rank):
     hops_all = allsum(hops)
     edges_all = B * args.steps  # each batch ingested once (replicated on every GPU)
     result = dict(total_ms=total_ms, ingest_ms=ingest_ms, walk_ms=walk_ms, hops=hops_all, edges=edges_all,
-                  launches=launches, clocks=clk, alg_bytes=allsum(alg_bytes), ingest_alg=ingest_alg)
+                  launches=launches, clocks=clk, alg_bytes=allsum(alg_bytes), ingest_alg=ingest_alg,
+                  seq_total_ms=allmax(seq_total_ms), seq_hops=allsum(seq_hops), pipelined=bool(args.pipelined))
 
     # ---- e2e pass through the C ABI with host buffers -----------------------------------
     e2e = None
@@ -636,10 +717,13 @@ def main():
             "edges_per_s": res["edges"] / total_s,
             "config": {**wl.describe(args.scale), "variant": args.variant, "parallelism": f"replicas{world}+walk-shards",
                        "global_walks_per_batch": wl.walks * world},
-            "phases": {"ingest_ms_per_step": res["ingest_ms"] / args.steps,
+            "pipelined": res["pipelined"],
+            "phases": {"source": "sequential pass (ingest then walks per batch, one stream, device events)",
+                       "ms_per_step": res["seq_total_ms"] / args.steps,
+                       "ingest_ms_per_step": res["ingest_ms"] / args.steps,
                        "walk_ms_per_step": res["walk_ms"] / args.steps,
                        "ingest_edges_per_s": res["edges"] / (res["ingest_ms"] / 1000.0),
-                       "walk_steps_per_s": res["hops"] / walk_s, "hops_per_step": res["hops"] / args.steps},
+                       "walk_steps_per_s": res["seq_hops"] / walk_s, "hops_per_step": res["hops"] / args.steps},
             "roofline": {"bound": "hbm", "kernel": "k_fullwalk (one launch per step; CUDA events around twg_generate)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None,

@@ -81,6 +81,9 @@ const char* twg_last_error(void);
 
 /* ---- context: device, stream, stream-ordered memory pool ---------------- */
 int twg_ctx_create(int device, twg_ctx** out);
+/* priority > 0: the compute stream gets the device's greatest priority (e.g.
+ * the ingest context of a pipeline whose walks run on a second context). */
+int twg_ctx_create_prio(int device, int priority, twg_ctx** out);
 int twg_ctx_destroy(twg_ctx* ctx);
 int twg_ctx_sync(twg_ctx* ctx);
 /* the cudaStream_t (as void*) all calls on ctx are ordered on */

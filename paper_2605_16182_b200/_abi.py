@@ -76,6 +76,7 @@ SIGNATURES = {
     "twg_abi_version": (I, []),
     "twg_last_error": (C.c_char_p, []),
     "twg_ctx_create": (I, [I, PP]),
+    "twg_ctx_create_prio": (I, [I, I, PP]),
     "twg_ctx_destroy": (I, [VP]),
     "twg_ctx_sync": (I, [VP]),
     "twg_ctx_stream": (I, [VP, PP]),

@@ -404,8 +404,8 @@ __global__ void __launch_bounds__(kPB) k_bucket_place(PlaceArgs a) {
     for (int r = 0; r < kChunkItems; ++r) {
       const u32 i = warp * (32 * kChunkItems) + r * 32 + lane;
       const bool ok = i < n;
-      const u32 d = ok ? sm.key[i] : kPB + lane;
-      const u32 peers = __match_any_sync(0xffffffffu, d);
+      const u32 d = ok ? sm.key[i] : 0u;
+      const u32 peers = digit_peers<kBucketShift>(d, ok);
       const u32 before = ok ? sm.wcnt[warp][d] : 0u;
       __syncwarp();
       if (ok && (__ffs(peers) - 1) == lane) sm.wcnt[warp][d] = before + __popc(peers);

@@ -153,7 +153,9 @@ extern "C" {
 int twg_abi_version(void) { return TWG_ABI_VERSION; }
 const char* twg_last_error(void) { return g_error.c_str(); }
 
-int twg_ctx_create(int device, twg_ctx** out) {
+int twg_ctx_create(int device, twg_ctx** out) { return twg_ctx_create_prio(device, 0, out); }
+
+int twg_ctx_create_prio(int device, int priority, twg_ctx** out) {
   return guarded([&] {
     auto* h = new twg_ctx;
     Ctx& c = h->c;
@@ -161,7 +163,13 @@ int twg_ctx_create(int device, twg_ctx** out) {
       c.device = device;
       TWG_CUDA(cudaSetDevice(device));
       TWG_CUDA(cudaDeviceGetAttribute(&c.sm_count, cudaDevAttrMultiProcessorCount, device));
-      TWG_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+      if (priority > 0) {  // the device's greatest priority: its kernels' blocks dispatch first
+        int least = 0, greatest = 0;
+        TWG_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        TWG_CUDA(cudaStreamCreateWithPriority(&c.stream, cudaStreamNonBlocking, greatest));
+      } else {
+        TWG_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+      }
       arena_register(c.stream);
       // glibc tables: same libm as the reference
       std::vector<double> e(kExpTableSize), x(701);

@@ -25,7 +25,7 @@
 
 namespace twg {
 
-struct Entry {
+struct alignas(16) Entry {  // one 128-bit load per hop
   u32 nbr;   // ref_neighbor(pos, owner)
   u32 edge;  // ref_edge(pos): index into the time-sorted edge array
   i64 t;     // time_[ref_edge(pos)]

@@ -100,9 +100,9 @@ def _ptr(a: np.ndarray) -> C.c_void_p:
 class Context:
     """One device + stream + stream-ordered pool (twg_ctx)."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, priority: int = 0):
         h = C.c_void_p()
-        _call("twg_ctx_create", device, C.byref(h))
+        _call("twg_ctx_create_prio", device, int(priority), C.byref(h))
         self.handle = h
         self.device = device
 
@@ -630,17 +630,21 @@ class WalkSet:
 
 
 def generate_walks(store: EdgeStore, config: WalkConfig, thresholds: Optional[TierThresholds] = None,
-                   variant: Variant = Variant.Coop, stats: Optional[WalkStats] = None) -> WalkSet:
-    """walk_engine.hpp:165-167."""
+                   variant: Variant = Variant.Coop, stats: Optional[WalkStats] = None,
+                   ctx: Optional[Context] = None) -> WalkSet:
+    """walk_engine.hpp:165-167. ctx: run on another context's stream (e.g. a
+    walk stream overlapping the next batch's ingest; the window protects the
+    current and the retired snapshot while it ingests)."""
+    ctx = ctx or store.ctx
     th = (thresholds or TierThresholds()).c()
     cfg = config.c()
     h = C.c_void_p()
     st = _abi.twg_walk_stats()
-    _call("twg_generate", store.ctx.handle, store.handle, C.byref(cfg), C.byref(th), int(variant), C.byref(h),
+    _call("twg_generate", ctx.handle, store.handle, C.byref(cfg), C.byref(th), int(variant), C.byref(h),
           C.byref(st))
     if stats is not None:
         stats.fill(st)
-    return WalkSet(h, store.ctx)
+    return WalkSet(h, ctx)
 
 
 def generate_walks_fullwalk(store: EdgeStore, config: WalkConfig, stats: Optional[WalkStats] = None) -> WalkSet:
