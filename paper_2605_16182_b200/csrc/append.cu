@@ -184,17 +184,43 @@ __global__ void k_bucket_bounds(const u32* keys, u64 Yn, u64 nb, u32* bstart) {
   }
 }
 
-// per-node batch counts from the bucket-sorted keys (one CTA per bucket)
-__global__ void __launch_bounds__(kPB) k_bucket_count(const u32* keys, const u32* bstart, u64 V, u32* y) {
+// Per-node batch counts from the bucket-sorted keys (one CTA per bucket),
+// and the owner side of the newest-incident-time update: a node's last entry
+// in the (canonical) bucket order carries its newest batch time.
+__global__ void __launch_bounds__(kPB) k_bucket_count(const u32* keys, const u32* vals, const u32* bstart, u64 V,
+                                                      const Rec* rec, int mode, u32* y, i64* last_t) {
   __shared__ u32 cnt[kPB];
+  __shared__ u32 lastq[kPB];
   const u64 bkt = blockIdx.x;
   cnt[threadIdx.x] = 0;
+  lastq[threadIdx.x] = 0;
   __syncthreads();
   const u32 bs = bstart[bkt], be = bstart[bkt + 1];
-  for (u32 q = bs + threadIdx.x; q < be; q += kPB) atomicAdd(&cnt[keys[q] & (kPB - 1)], 1u);
+  for (u32 q = bs + threadIdx.x; q < be; q += kPB) {
+    const u32 nd = keys[q] & (kPB - 1);
+    atomicAdd(&cnt[nd], 1u);
+    atomicMax(&lastq[nd], q + 1);
+  }
   __syncthreads();
   const u64 v = (bkt << kBucketShift) + threadIdx.x;
-  if (v < V) y[v] = cnt[threadIdx.x];
+  if (v < V) {
+    y[v] = cnt[threadIdx.x];
+    if (last_t && cnt[threadIdx.x]) {
+      const u32 j = vals[lastq[threadIdx.x] - 1];
+      const i64 t = rec[mode == TWG_UNDIRECTED ? (j >> 1) : j].t;
+      if (last_t[v] < t) last_t[v] = t;
+    }
+  }
+}
+
+// nodes whose newest incident edge falls before the cutoff (they would leave the snapshot)
+__global__ void k_count_dead(const i64* last, u64 V, i64 cutoff, u64* dead) {
+  u64 c = 0;
+  for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < V;
+       v += static_cast<u64>(gridDim.x) * blockDim.x)
+    c += last[v] < cutoff ? 1u : 0u;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(reinterpret_cast<unsigned long long*>(dead), c);
 }
 
 // Eviction bound: first logical x in [lo, hi) with time >= c. The eight
@@ -548,7 +574,7 @@ bool append_log_slot(const Store& O, const Store* R, u64 A, Ring* wr) {
 
 Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const u32* bS, const u32* bD,
                      const i64* bT, Ring bring, u64 A, u64 from, i64 cutoff, bool no_ties, const BatchRec16* rec_in,
-                     bool in_log) {
+                     bool in_log, bool check_dead) {
   Ctx& ctx = *w.ctx;
   cudaStream_t st = ctx.stream;
   PhaseTimer pt(ctx, "ingest_append");
@@ -644,8 +670,16 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
   //    placement, marks, publish
   s->nm.alloc(V, st);
   DevBuf<u32> ycnt(V, st);
-  k_bucket_count<<<static_cast<unsigned>(nb), kPB, 0, st>>>(kp, bstart.p, V, ycnt.p);
+  k_bucket_count<<<static_cast<unsigned>(nb), kPB, 0, st>>>(kp, vp, bstart.p, V, brec, mode, ycnt.p, s->last_t.p);
   TWG_LAUNCHED(ctx);
+  if (check_dead) {  // fast route: the population must not shrink (nothing is published yet)
+    TWG_CUDA(cudaMemsetAsync(sc + 13, 0, sizeof(u64), st));
+    k_count_dead<<<grid(ctx, V), kBlock, 0, st>>>(s->last_t.p, V, cutoff, sc + 13);
+    TWG_LAUNCHED(ctx);
+    u64 dead[1];
+    read_scalars(ctx, sc + 13, dead, 1);
+    if (dead[0]) return nullptr;
+  }
   std::shared_ptr<NodeArena> arena = O.gapped ? O.arena : nullptr;
   // a snapshot older than the retired one still holding this arena may read
   // any slot: then nothing of it is reused (fresh arena)

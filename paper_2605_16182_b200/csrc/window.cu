@@ -115,7 +115,7 @@ __global__ void k_segment_sort(const u32* s, const u32* d, const i64* t, u64 A, 
 template <bool kTimeOrdered>
 __device__ __forceinline__ void agg_max(i64* last, u32 key, i64 t, bool valid);
 
-__global__ void k_batch_fast(const i64* bs, const i64* bd, const i64* bt, u64 n, u32* os, u32* od, i64* ot,
+__global__ void k_batch_fast(const i64* bs, const i64* bd, const i64* bt, u64 n, int mode, u32* os, u32* od, i64* ot,
                              Ring orr, BatchRec16* rec, i64* last) {
   for (u64 k0 = blockIdx.x * static_cast<u64>(blockDim.x); k0 < n; k0 += static_cast<u64>(gridDim.x) * blockDim.x) {
     const u64 k = k0 + threadIdx.x;
@@ -142,19 +142,10 @@ __global__ void k_batch_fast(const i64* bs, const i64* bd, const i64* bt, u64 n,
         rec[k + j] = BatchRec16{a, b, tk};
       }
     }
-    agg_max<true>(last, valid ? static_cast<u32>(bs[k < n ? k : 0]) : 0u, tk, valid);
-    agg_max<true>(last, valid ? static_cast<u32>(bd[k < n ? k : 0]) : 0u, tk, valid);
+    // the non-owner endpoint; the owner side is merged by the placement's counts
+    if (mode == TWG_FORWARD) agg_max<true>(last, valid ? static_cast<u32>(bd[k < n ? k : 0]) : 0u, tk, valid);
+    else if (mode == TWG_BACKWARD) agg_max<true>(last, valid ? static_cast<u32>(bs[k < n ? k : 0]) : 0u, tk, valid);
   }
-}
-
-// nodes whose newest incident edge falls before the cutoff (they would leave the snapshot)
-__global__ void k_count_dead(const i64* last, u64 V, i64 cutoff, u64* dead) {
-  u64 c = 0;
-  for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < V;
-       v += static_cast<u64>(gridDim.x) * blockDim.x)
-    c += last[v] < cutoff ? 1u : 0u;
-  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd(reinterpret_cast<unsigned long long*>(dead), c);
 }
 
 // lower_bound(time_, cutoff) (edge_store.cpp:326) over the snapshot's edge ring
@@ -1042,20 +1033,22 @@ Store* ingest_fast(Window& w, const i64* bs, const i64* bd, const i64* bt, u64 n
   TWG_CUDA(cudaMemsetAsync(ctx.d_scalars + 12, 0, 16, st));
   k_lower_bound<<<1, 1, 0, st>>>(O.e_t.p, O.view().erg, O.m, cutoff, ctx.d_scalars + 12);
   TWG_LAUNCHED(ctx);
-  k_batch_fast<<<grid(ctx, n), kBlock, 0, st>>>(bs, bd, bt, n, bS, bD, bT, wring, rec.p, s->last_t.p);
+  k_batch_fast<<<grid(ctx, n), kBlock, 0, st>>>(bs, bd, bt, n, w.mode, bS, bD, bT, wring, rec.p, s->last_t.p);
   TWG_LAUNCHED(ctx);
-  k_count_dead<<<grid(ctx, V), kBlock, 0, st>>>(s->last_t.p, V, cutoff, ctx.d_scalars + 13);
-  TWG_LAUNCHED(ctx);
-  u64 r[2];
-  read_scalars(ctx, ctx.d_scalars + 12, r, 2);
+  u64 r[1];
+  read_scalars(ctx, ctx.d_scalars + 12, r, 1);
   pt.mark("batch_fast");
-  if (r[1]) return nullptr;  // a node leaves: dense ids change
   const u64 from = r[0];
   s->m = O.m - from + n;
   stats->evicted = from;
   stats->dropped_late = 0;
   w.max_ext = static_cast<i64>(V - 1);
-  return ingest_append(w, O, std::move(s), bS, bD, bT, wring, n, from, cutoff, true, rec.p, in_log);
+  Store* out = ingest_append(w, O, std::move(s), bS, bD, bT, wring, n, from, cutoff, true, rec.p, in_log, true);
+  if (!out) {  // an old node leaves the window: the general route recomputes everything
+    stats->evicted = stats->dropped_late = 0;
+    return nullptr;
+  }
+  return out;
 }
 
 }  // namespace

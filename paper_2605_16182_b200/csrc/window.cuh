@@ -40,9 +40,12 @@ bool append_log_slot(const Store& O, const Store* R, u64 A, Ring* wr);
 // bS/bD/bT[bring(k)] = batch edge k. rec / in_log: the caller already
 // produced the records / wrote the batch into O's log through the ring
 // append_log_slot returned (bS, bD, bT are then the log's columns).
+// check_dead: s->last_t holds only the non-owner side of the batch; the owner
+// side is merged here and the ingest returns null (nothing published) when an
+// old node would leave the window.
 Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const u32* bS, const u32* bD,
                      const i64* bT, Ring bring, u64 A, u64 from, i64 cutoff, bool no_ties,
-                     const BatchRec16* rec = nullptr, bool in_log = false);
+                     const BatchRec16* rec = nullptr, bool in_log = false, bool check_dead = false);
 
 Window* window_create(Ctx& ctx, i64 duration, int mode, BuildOpts opts);
 void window_destroy(Window* w);

@@ -132,3 +132,25 @@ def test_append_held_snapshots_stay_valid(tw, co):
     # every held snapshot (not only the current one) still reads back exactly
     for s, ed in zip(snaps, exp_dumps):
         assert_store(s, ed, keys=["src_ext", "dst_ext", "t", "ts_off", "n_off", "mk_time", "mk_start", "ref_edge"])
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_append_node_leaves_window(tw, co, mode):
+    """Node 7 stops appearing after batch 2: once its last edge is evicted the
+    fast route's population check aborts (nothing published) and the general
+    route re-densifies the ids; bit-exact after every batch."""
+    batches = _ordered_stream(19, 9, 2000, 100, 50)
+    for b in range(3, 9):
+        e = batches[b].copy()
+        e[e[:, 0] == 7, 0] = 8
+        e[e[:, 1] == 7, 1] = 9
+        batches[b] = e[np.lexsort((e[:, 1], e[:, 0], e[:, 2]))]
+    exp_stats, exp_dumps = co.window_run(batches, 120, mode, every=True)
+    w = tw.WindowManager(120, tw.DirectionMode(mode))
+    counts = []
+    for b, (es, eb), ed in zip(batches, exp_stats, exp_dumps):
+        st = w.ingest_batch(b)
+        assert (st.evicted, st.retained) == (es["evicted"], es["retained"])
+        counts.append(w.snapshot().node_count())
+        assert_store(w.snapshot(), ed)
+    assert counts[0] == 100 and counts[-1] == 99
