@@ -162,14 +162,20 @@ __device__ __forceinline__ u32 nbr_of(int mode, const Rec& r, u32 j) {
   return (j & 1) ? r.src : r.dst;  // side 1 (owner dst) -> src; self-loops give the owner
 }
 
-__global__ void k_owner_keys(const Rec* rec, u64 A, int mode, u32* keys, u32* vals) {
+// batch entry j: key = owner, payload = the finished node-view entry (carried
+// through the bucket sort, so the placement reads it in order)
+__global__ void k_owner_keys(const Rec* rec, u64 A, int mode, u32 seq_b, u32* keys, Entry* vals) {
   const u64 Yn = mode == TWG_UNDIRECTED ? 2 * A : A;
   for (u64 j = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; j < Yn;
        j += static_cast<u64>(gridDim.x) * blockDim.x) {
     const u32 k = mode == TWG_UNDIRECTED ? static_cast<u32>(j >> 1) : static_cast<u32>(j);
     const Rec r = rec[k];
     keys[j] = mode == TWG_UNDIRECTED ? ((j & 1) ? r.dst : r.src) : (mode == TWG_BACKWARD ? r.dst : r.src);
-    vals[j] = static_cast<u32>(j);
+    Entry e;
+    e.nbr = nbr_of(mode, r, static_cast<u32>(j));
+    e.edge = seq_b + k;
+    e.t = r.t;
+    vals[j] = e;
   }
 }
 
@@ -187,8 +193,8 @@ __global__ void k_bucket_bounds(const u32* keys, u64 Yn, u64 nb, u32* bstart) {
 // Per-node batch counts from the bucket-sorted keys (one CTA per bucket),
 // and the owner side of the newest-incident-time update: a node's last entry
 // in the (canonical) bucket order carries its newest batch time.
-__global__ void __launch_bounds__(kPB) k_bucket_count(const u32* keys, const u32* vals, const u32* bstart, u64 V,
-                                                      const Rec* rec, int mode, u32* y, i64* last_t) {
+__global__ void __launch_bounds__(kPB) k_bucket_count(const u32* keys, const Entry* vals, const u32* bstart, u64 V,
+                                                      u32* y, i64* last_t) {
   __shared__ u32 cnt[kPB];
   __shared__ u32 lastq[kPB];
   const u64 bkt = blockIdx.x;
@@ -206,8 +212,7 @@ __global__ void __launch_bounds__(kPB) k_bucket_count(const u32* keys, const u32
   if (v < V) {
     y[v] = cnt[threadIdx.x];
     if (last_t && cnt[threadIdx.x]) {
-      const u32 j = vals[lastq[threadIdx.x] - 1];
-      const i64 t = rec[mode == TWG_UNDIRECTED ? (j >> 1) : j].t;
+      const i64 t = vals[lastq[threadIdx.x] - 1].t;
       if (last_t[v] < t) last_t[v] = t;
     }
   }
@@ -348,11 +353,8 @@ struct PlaceArgs {
   const NodeMeta* plan;
   const i64* last_t;
   const u32* keys;      // batch entries bucket-sorted (owner >> 8), canonical order inside a bucket
-  const u32* vals;
+  const Entry* vals;    // their node-view entries
   const u32* bstart;
-  const Rec* rec;
-  int mode;
-  u32 seq_b;
   Entry* ent;
   i64* mt;
   u32* ms;
@@ -367,10 +369,8 @@ struct PlaceSmem {
   i64 last_t[kPB];
   u32 has_last[kPB];
   u32 mtotal;
-  u8 key[kChunk];
   u8 snode[kChunk];
   u8 flag[kChunk];
-  u32 val[kChunk];
   u32 mscan[kChunk];
   Entry sent[kChunk];
 };
@@ -405,22 +405,14 @@ __global__ void __launch_bounds__(kPB) k_bucket_place(PlaceArgs a) {
   for (u32 c0 = bs; c0 < be; c0 += kChunk) {
     const u32 n = min(static_cast<u32>(kChunk), be - c0);
     __syncthreads();
-    {
-      u32 kk[kChunkItems], vv[kChunkItems];
+    // item i = warp*R*32 + r*32 + lane of the chunk belongs to this lane in round r
+    u32 dk[kChunkItems];
+    Entry pe[kChunkItems];
 #pragma unroll
-      for (int r = 0; r < kChunkItems; ++r) {
-        const u32 i = t + r * kPB;
-        kk[r] = i < n ? a.keys[c0 + i] : 0u;
-        vv[r] = i < n ? a.vals[c0 + i] : 0u;
-      }
-#pragma unroll
-      for (int r = 0; r < kChunkItems; ++r) {
-        const u32 i = t + r * kPB;
-        if (i < n) {
-          sm.key[i] = static_cast<u8>(kk[r] & (kPB - 1));
-          sm.val[i] = vv[r];
-        }
-      }
+    for (int r = 0; r < kChunkItems; ++r) {
+      const u32 i = warp * (32 * kChunkItems) + r * 32 + lane;
+      dk[r] = i < n ? (a.keys[c0 + i] & (kPB - 1)) : 0u;
+      if (i < n) pe[r] = a.vals[c0 + i];
     }
     for (int i = t; i < (kPB / 32) * kPB; i += kPB) (&sm.wcnt[0][0])[i] = 0;
     __syncthreads();
@@ -430,7 +422,7 @@ __global__ void __launch_bounds__(kPB) k_bucket_place(PlaceArgs a) {
     for (int r = 0; r < kChunkItems; ++r) {
       const u32 i = warp * (32 * kChunkItems) + r * 32 + lane;
       const bool ok = i < n;
-      const u32 d = ok ? sm.key[i] : 0u;
+      const u32 d = dk[r];
       const u32 peers = digit_peers<kBucketShift>(d, ok);
       const u32 before = ok ? sm.wcnt[warp][d] : 0u;
       __syncwarp();
@@ -452,28 +444,14 @@ __global__ void __launch_bounds__(kPB) k_bucket_place(PlaceArgs a) {
       if (t == 0) sm.off[kPB] = total;
     }
     __syncthreads();
-    {  // all gathers in flight before the staging stores
-      Rec b[kChunkItems];
-      u32 jj[kChunkItems];
 #pragma unroll
-      for (int r = 0; r < kChunkItems; ++r) {
-        const u32 i = warp * (32 * kChunkItems) + r * 32 + lane;
-        jj[r] = i < n ? sm.val[i] : 0u;
-        if (i < n) b[r] = a.rec[entry_edge(a.mode, jj[r])];
-      }
-#pragma unroll
-      for (int r = 0; r < kChunkItems; ++r) {
-        const u32 i = warp * (32 * kChunkItems) + r * 32 + lane;
-        if (i < n) {
-          const u32 nd = sm.key[i];
-          const u32 sp = sm.off[nd] + sm.wcnt[warp][nd] + rank[r];
-          Entry e;
-          e.nbr = nbr_of(a.mode, b[r], jj[r]);
-          e.edge = a.seq_b + entry_edge(a.mode, jj[r]);
-          e.t = b[r].t;
-          sm.sent[sp] = e;
-          sm.snode[sp] = static_cast<u8>(nd);
-        }
+    for (int r = 0; r < kChunkItems; ++r) {
+      const u32 i = warp * (32 * kChunkItems) + r * 32 + lane;
+      if (i < n) {
+        const u32 nd = dk[r];
+        const u32 sp = sm.off[nd] + sm.wcnt[warp][nd] + rank[r];
+        sm.sent[sp] = pe[r];
+        sm.snode[sp] = static_cast<u8>(nd);
       }
     }
     __syncthreads();
@@ -651,14 +629,16 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
   //    order inside a bucket), bucket bounds
   const int vb = V > 1 ? bit_width_u64(V - 1) : 0;
   const u64 nb = (V + kPB - 1) / kPB;
-  DevBuf<u32> k0(Yn, st), k1(Yn, st), v0(Yn, st), v1(Yn, st);
+  DevBuf<u32> k0(Yn, st), k1(Yn, st);
+  DevBuf<Entry> v0(Yn, st), v1(Yn, st);
   u32* kp = k0.p;
   u32* ka = k1.p;
-  u32* vp = v0.p;
-  u32* va = v1.p;
-  k_owner_keys<<<grid(ctx, Yn), kBlock, 0, st>>>(brec, A, mode, kp, vp);
+  Entry* vp = v0.p;
+  Entry* va = v1.p;
+  k_owner_keys<<<grid(ctx, Yn), kBlock, 0, st>>>(brec, A, mode, seq_b, kp, vp);
   TWG_LAUNCHED(ctx);
-  if (vb > static_cast<int>(kBucketShift)) radix_sort_pairs<u32>(ctx, &kp, &ka, &vp, &va, Yn, vb, kBucketShift);
+  if (vb > static_cast<int>(kBucketShift))
+    radix_sort_pairs<u32, Entry>(ctx, &kp, &ka, &vp, &va, Yn, vb, kBucketShift);
   DevBuf<u32> bstart(nb + 1, st);
   k_bucket_bounds<<<grid(ctx, Yn + 1), kBlock, 0, st>>>(kp, Yn, nb, bstart.p);
   TWG_LAUNCHED(ctx);
@@ -670,7 +650,7 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
   //    placement, marks, publish
   s->nm.alloc(V, st);
   DevBuf<u32> ycnt(V, st);
-  k_bucket_count<<<static_cast<unsigned>(nb), kPB, 0, st>>>(kp, vp, bstart.p, V, brec, mode, ycnt.p, s->last_t.p);
+  k_bucket_count<<<static_cast<unsigned>(nb), kPB, 0, st>>>(kp, vp, bstart.p, V, ycnt.p, s->last_t.p);
   TWG_LAUNCHED(ctx);
   if (check_dead) {  // fast route: the population must not shrink (nothing is published yet)
     TWG_CUDA(cudaMemsetAsync(sc + 13, 0, sizeof(u64), st));
@@ -753,9 +733,6 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
   pl.keys = kp;
   pl.vals = vp;
   pl.bstart = bstart.p;
-  pl.rec = brec;
-  pl.mode = mode;
-  pl.seq_b = seq_b;
   pl.ent = arena->ent.p;
   pl.mt = arena->mk_time.p;
   pl.ms = arena->mk_start.p;

@@ -147,15 +147,16 @@ void exclusive_scan(Ctx& ctx, In in, u64 n, T* out) {
 
 // --------------------------------------------------------------- radix ----
 
-template <class K>
+template <class K, int kItems = kSortItems>
 __global__ void __launch_bounds__(kSortBlock) k_radix_hist(const K* __restrict__ keys, u64 n, int shift,
                                                            u32* __restrict__ counts, u64 tiles) {
+  constexpr int kTile = kSortBlock * kItems;
   __shared__ u32 hist[kRadix];
   for (int b = threadIdx.x; b < kRadix; b += kSortBlock) hist[b] = 0;
   __syncthreads();
-  const u64 base = static_cast<u64>(blockIdx.x) * kSortTile;
+  const u64 base = static_cast<u64>(blockIdx.x) * kTile;
 #pragma unroll
-  for (int j = 0; j < kSortItems; ++j) {
+  for (int j = 0; j < kItems; ++j) {
     const u64 i = base + static_cast<u64>(j) * kSortBlock + threadIdx.x;
     if (i < n) atomicAdd(&hist[static_cast<u32>(keys[i] >> shift) & (kRadix - 1)], 1u);
   }
@@ -164,44 +165,47 @@ __global__ void __launch_bounds__(kSortBlock) k_radix_hist(const K* __restrict__
 }
 
 // Stable tile rank + coalesced scatter. Item order inside a tile is
-// (round j, warp, lane) == input order, which keeps the sort stable.
-template <class K>
+// (round j, warp, lane) == input order, which keeps the sort stable. V is
+// the value type (u32 indices, or a 16-byte payload carried through the
+// passes so the consumer reads it in order instead of gathering it).
+template <class K, class V, int kItems>
 __global__ void __launch_bounds__(kSortBlock) k_radix_scatter(const K* __restrict__ keys_in,
-                                                              const u32* __restrict__ vals_in,
+                                                              const V* __restrict__ vals_in,
                                                               K* __restrict__ keys_out,
-                                                              u32* __restrict__ vals_out, u64 n,
+                                                              V* __restrict__ vals_out, u64 n,
                                                               int shift, const u32* __restrict__ offsets,
                                                               u64 tiles) {
   constexpr int kWarps = kSortBlock / 32;
+  constexpr int kTile = kSortBlock * kItems;
   __shared__ u32 wcount[kWarps][kRadix];
   __shared__ u32 running[kRadix];
   __shared__ u32 tile_start[kRadix];
-  __shared__ K skeys[kSortTile];
-  __shared__ u32 svals[kSortTile];
+  __shared__ K skeys[kTile];
+  __shared__ V svals[kTile];
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const u64 base = static_cast<u64>(blockIdx.x) * kSortTile;
+  const u64 base = static_cast<u64>(blockIdx.x) * kTile;
   const u32 lanemask_lt = (1u << lane) - 1u;
   for (int b = threadIdx.x; b < kRadix; b += kSortBlock) running[b] = 0;
 
-  // Warp-private ranking: warp w owns the tile's items [w*256, (w+1)*256) in
-  // 8 rounds of 32 lanes, so its digit counters need no block barrier
+  // Warp-private ranking: warp w owns the tile's items [w*32*kItems, ...) in
+  // kItems rounds of 32 lanes, so its digit counters need no block barrier
   // between rounds; one cross-warp scan per digit at the end.
-  K key[kSortItems];
-  u32 val[kSortItems];
-  u32 rank[kSortItems];
+  K key[kItems];
+  V val[kItems];
+  u32 rank[kItems];
   for (int b = threadIdx.x; b < kWarps * kRadix; b += kSortBlock) (&wcount[0][0])[b] = 0;
   __syncthreads();
-  const u64 wbase = base + static_cast<u64>(warp) * (32 * kSortItems);
+  const u64 wbase = base + static_cast<u64>(warp) * (32 * kItems);
 #pragma unroll
-  for (int j = 0; j < kSortItems; ++j) {
+  for (int j = 0; j < kItems; ++j) {
     const u64 i = wbase + static_cast<u64>(j) * 32 + lane;
     const bool valid = i < n;
     key[j] = valid ? keys_in[i] : K(0);
-    val[j] = (valid && vals_in) ? vals_in[i] : 0u;
+    if (vals_in && valid) val[j] = vals_in[i];
   }
 #pragma unroll
-  for (int j = 0; j < kSortItems; ++j) {
+  for (int j = 0; j < kItems; ++j) {
     const u64 i = wbase + static_cast<u64>(j) * 32 + lane;
     const bool valid = i < n;
     const u32 d = valid ? (static_cast<u32>(key[j] >> shift) & (kRadix - 1)) : 0u;
@@ -234,7 +238,7 @@ __global__ void __launch_bounds__(kSortBlock) k_radix_scatter(const K* __restric
   }
   __syncthreads();
 #pragma unroll
-  for (int j = 0; j < kSortItems; ++j) {
+  for (int j = 0; j < kItems; ++j) {
     const u64 i = wbase + static_cast<u64>(j) * 32 + lane;
     if (i < n) {
       const u32 d = static_cast<u32>(key[j] >> shift) & (kRadix - 1);
@@ -244,9 +248,9 @@ __global__ void __launch_bounds__(kSortBlock) k_radix_scatter(const K* __restric
     }
   }
   __syncthreads();
-  const u64 tile_n = n - base < static_cast<u64>(kSortTile) ? n - base : static_cast<u64>(kSortTile);
+  const u64 tile_n = n - base < static_cast<u64>(kTile) ? n - base : static_cast<u64>(kTile);
 #pragma unroll
-  for (int j = 0; j < kSortItems; ++j) {
+  for (int j = 0; j < kItems; ++j) {
     const u32 pos = static_cast<u32>(j) * kSortBlock + threadIdx.x;
     if (pos < tile_n) {
       const K k = skeys[pos];
@@ -489,19 +493,22 @@ void merge_path(Ctx& ctx, KA ka, u64 na, KB kb, u64 nb, Emit emit) {
 // output lands in (*keys, *vals); the alt buffers are scratch of the same
 // size. Pointers are swapped as passes ping-pong. n < 2^32. Keys-only when
 // *vals == nullptr.
-template <class K>
-void radix_sort_pairs(Ctx& ctx, K** keys, K** keys_alt, u32** vals, u32** vals_alt, u64 n, int bits, int lo_bit = 0) {
+template <class K, class V = u32>
+void radix_sort_pairs(Ctx& ctx, K** keys, K** keys_alt, V** vals, V** vals_alt, u64 n, int bits, int lo_bit = 0) {
   if (n < 2 || bits <= lo_bit) return;
+  // 16-byte payloads: half the items per thread keeps the staging under 48 KB
+  constexpr int kItems = sizeof(V) > 4 ? kSortItems / 2 : kSortItems;
+  constexpr int kTile = kSortBlock * kItems;
   cudaStream_t st = ctx.stream;
-  const u64 tiles = (n + kSortTile - 1) / kSortTile;
+  const u64 tiles = (n + kTile - 1) / kTile;
   if (tiles * kRadix >= (1ull << 32)) fail(TWG_EINVAL, "radix_sort_pairs: input too large");
   DevBuf<u32> counts(tiles * kRadix + 1, st);
   DevBuf<u32> offsets(tiles * kRadix + 1, st);
   for (int shift = lo_bit; shift < bits; shift += kRadixBits) {
-    k_radix_hist<K><<<static_cast<unsigned>(tiles), kSortBlock, 0, st>>>(*keys, n, shift, counts.p, tiles);
+    k_radix_hist<K, kItems><<<static_cast<unsigned>(tiles), kSortBlock, 0, st>>>(*keys, n, shift, counts.p, tiles);
     TWG_LAUNCHED(ctx);
     exclusive_scan<u32>(ctx, LoadFn<u32>{counts.p}, tiles * kRadix, offsets.p);
-    k_radix_scatter<K><<<static_cast<unsigned>(tiles), kSortBlock, 0, st>>>(
+    k_radix_scatter<K, V, kItems><<<static_cast<unsigned>(tiles), kSortBlock, 0, st>>>(
         *keys, *vals, *keys_alt, *vals_alt, n, shift, offsets.p, tiles);
     TWG_LAUNCHED(ctx);
     std::swap(*keys, *keys_alt);
