@@ -56,16 +56,11 @@ __global__ void k_lb_time(const i64* t, Ring zr, u64 n, i64 x, u64* out) {
   *out = lo;
 }
 
-// survivors [from, from + n) of a snapshot (edge ring er) -> the start of a new log
-__global__ void k_copy_cols(const u32* s, const u32* d, const i64* t, Ring er, u64 from, u64 n, u32* os, u32* od,
-                            i64* ot) {
+// survivors [from, from + n) of a snapshot -> the start of a new log
+__global__ void k_copy_cols(StoreView v, u64 from, u64 n, EdgeRec* out) {
   for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<u64>(gridDim.x) * blockDim.x) {
-    const u32 p = er(static_cast<u32>(from + i));
-    os[i] = s[p];
-    od[i] = d[p];
-    ot[i] = t[p];
-  }
+       i += static_cast<u64>(gridDim.x) * blockDim.x)
+    out[i] = edge_at(v, from + i);
 }
 
 // surviving ts groups [g_cut, Z) of the old snapshot -> a fresh log
@@ -82,18 +77,18 @@ __global__ void k_copy_groups(const u32* off, const i64* tt, Ring zr, u64 Z, con
 // batch group starts: the first batch edge starts a group unless it shares
 // the last survivor's time
 struct BatchGroupFn {
-  const i64* t;
-  Ring br;                     // batch index -> slot of t
+  const EdgeRec* b;
+  Ring br;                     // batch index -> slot of b
   const i64* last_survivor_t;  // null when there are no survivors
   __device__ __forceinline__ u32 operator()(u64 k) const {
-    const i64 tk = t[br(static_cast<u32>(k))];
+    const i64 tk = b[br(static_cast<u32>(k))].t;
     if (k == 0) return last_survivor_t ? (tk != *last_survivor_t ? 1u : 0u) : 1u;
-    return tk != t[br(static_cast<u32>(k - 1))] ? 1u : 0u;
+    return tk != b[br(static_cast<u32>(k - 1))].t ? 1u : 0u;
   }
 };
 
 struct BatchGroupScatter {
-  const i64* t;
+  const EdgeRec* b;
   Ring br;
   u32 seq_b;
   u64 zbase;              // host-known logical write position, or
@@ -105,7 +100,7 @@ struct BatchGroupScatter {
     if (!f) return;
     const u64 z = ((zbase_dev ? *zbase_dev : zbase) + g) % cap;
     ts_off[z] = seq_b + static_cast<u32>(k);
-    ts_time[z] = t[br(static_cast<u32>(k))];
+    ts_time[z] = b[br(static_cast<u32>(k))].t;
   }
 };
 
@@ -142,18 +137,10 @@ using Rec = BatchRec16;
 
 // the sorted batch into the log, plus a 16-byte record per edge for the
 // owner-ordered gathers
-__global__ void k_append_batch(const u32* s, const u32* d, const i64* t, Ring br, u64 n, u32* os, u32* od, i64* ot,
-                               Ring wr, Rec* rec) {
+__global__ void k_append_batch(const EdgeRec* b, Ring br, u64 n, EdgeRec* log, Ring wr) {
   for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<u64>(gridDim.x) * blockDim.x) {
-    const u32 q = br(static_cast<u32>(i)), p = wr(static_cast<u32>(i));
-    const u32 a = s[q], b = d[q];
-    const i64 x = t[q];
-    os[p] = a;
-    od[p] = b;
-    ot[p] = x;
-    if (rec) rec[i] = Rec{a, b, x};
-  }
+       i += static_cast<u64>(gridDim.x) * blockDim.x)
+    log[wr(static_cast<u32>(i))] = b[br(static_cast<u32>(i))];
 }
 
 __device__ __forceinline__ u32 nbr_of(int mode, const Rec& r, u32 j) {
@@ -164,12 +151,12 @@ __device__ __forceinline__ u32 nbr_of(int mode, const Rec& r, u32 j) {
 
 // batch entry j: key = owner, payload = the finished node-view entry (carried
 // through the bucket sort, so the placement reads it in order)
-__global__ void k_owner_keys(const Rec* rec, u64 A, int mode, u32 seq_b, u32* keys, Entry* vals) {
+__global__ void k_owner_keys(const Rec* rec, Ring br, u64 A, int mode, u32 seq_b, u32* keys, Entry* vals) {
   const u64 Yn = mode == TWG_UNDIRECTED ? 2 * A : A;
   for (u64 j = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; j < Yn;
        j += static_cast<u64>(gridDim.x) * blockDim.x) {
     const u32 k = mode == TWG_UNDIRECTED ? static_cast<u32>(j >> 1) : static_cast<u32>(j);
-    const Rec r = rec[k];
+    const Rec r = rec[br(k)];
     keys[j] = mode == TWG_UNDIRECTED ? ((j & 1) ? r.dst : r.src) : (mode == TWG_BACKWARD ? r.dst : r.src);
     Entry e;
     e.nbr = nbr_of(mode, r, static_cast<u32>(j));
@@ -550,9 +537,8 @@ bool append_log_slot(const Store& O, const Store* R, u64 A, Ring* wr) {
   return true;
 }
 
-Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const u32* bS, const u32* bD,
-                     const i64* bT, Ring bring, u64 A, u64 from, i64 cutoff, bool no_ties, const BatchRec16* rec_in,
-                     bool in_log, bool check_dead) {
+Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const EdgeRec* batch, Ring bring, u64 A,
+                     u64 from, i64 cutoff, bool no_ties, bool in_log, bool check_dead) {
   Ctx& ctx = *w.ctx;
   cudaStream_t st = ctx.stream;
   PhaseTimer pt(ctx, "ingest_append");
@@ -585,14 +571,11 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
   } else {  // a new log (first streaming batch, window growth, or an older snapshot holding the log)
     auto nl = std::make_shared<EdgeLog>();
     nl->cap = std::max<u64>((3 * m) / 2 + 2 * A, 1024);
-    nl->src.alloc(nl->cap, st);
-    nl->dst.alloc(nl->cap, st);
-    nl->t.alloc(nl->cap, st);
+    nl->rec.alloc(nl->cap, st);
     nl->ts_off.alloc(nl->cap, st);
     nl->ts_time.alloc(nl->cap, st);
     if (S) {
-      k_copy_cols<<<grid(ctx, S), kBlock, 0, st>>>(O.e_src.p, O.e_dst.p, O.e_t.p, ov.erg, from, S, nl->src.p,
-                                                   nl->dst.p, nl->t.p);
+      k_copy_cols<<<grid(ctx, S), kBlock, 0, st>>>(ov, from, S, nl->rec.p);
       TWG_LAUNCHED(ctx);
     }
     if (O.Z) {
@@ -609,19 +592,15 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
   }
   const u64 lpos = s->log_first + S;  // logical log position of batch edge 0
   const Ring wr = log_ring(log->cap, lpos);
-  DevBuf<Rec> brec_own;
-  const Rec* brec = rec_in;
-  if (!brec || !in_log) {
-    if (!brec) brec_own.alloc(A, st);
-    k_append_batch<<<grid(ctx, A), kBlock, 0, st>>>(bS, bD, bT, bring, A, log->src.p, log->dst.p, log->t.p, wr,
-                                                    brec ? nullptr : brec_own.p);
+  if (!in_log) {  // the batch into the log ring (the fast route wrote it there already)
+    k_append_batch<<<grid(ctx, A), kBlock, 0, st>>>(batch, bring, A, log->rec.p, wr);
     TWG_LAUNCHED(ctx);
-    if (!brec) brec = brec_own.p;
   }
+  const Rec* brec = log->rec.p;  // batch edge k at log slot wr(k) from here on
   const i64* last_surv = nullptr;  // the last survivor's time: the first batch group merges with it on a tie
-  if (S) last_surv = O.e_t.p + (O.gapped ? (O.log_first + O.m - 1) % O.log->cap : O.m - 1);
-  scan_scatter(ctx, BatchGroupFn{bT, bring, last_surv}, A, sc + 5,
-               BatchGroupScatter{bT, bring, seq_b, zbase, zbase_dev, log->cap, log->ts_off.p, log->ts_time.p});
+  if (S) last_surv = O.gapped ? &O.e_rec.p[(O.log_first + O.m - 1) % O.log->cap].t : O.e_t.p + (O.m - 1);
+  scan_scatter(ctx, BatchGroupFn{brec, wr, last_surv}, A, sc + 5,
+               BatchGroupScatter{brec, wr, seq_b, zbase, zbase_dev, log->cap, log->ts_off.p, log->ts_time.p});
   pt.mark("log+ts");
 
   // 2. batch entries grouped into 256-node buckets: stable radix sort of
@@ -635,7 +614,7 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
   u32* ka = k1.p;
   Entry* vp = v0.p;
   Entry* va = v1.p;
-  k_owner_keys<<<grid(ctx, Yn), kBlock, 0, st>>>(brec, A, mode, seq_b, kp, vp);
+  k_owner_keys<<<grid(ctx, Yn), kBlock, 0, st>>>(brec, wr, A, mode, seq_b, kp, vp);
   TWG_LAUNCHED(ctx);
   if (vb > static_cast<int>(kBucketShift))
     radix_sort_pairs<u32, Entry>(ctx, &kp, &ka, &vp, &va, Yn, vb, kBucketShift);
@@ -758,9 +737,7 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
   s->m = m;
   s->Z = Z;
   s->Q = Q;
-  s->e_src.alias(log->src.p, log->cap);
-  s->e_dst.alias(log->dst.p, log->cap);
-  s->e_t.alias(log->t.p, log->cap);
+  s->e_rec.alias(log->rec.p, log->cap);
   s->ts_off.alias(log->ts_off.p, log->cap);
   s->ts_time.alias(log->ts_time.p, log->cap);
   const Ring er = log_ring(log->cap, s->log_first), zr = log_ring(log->cap, s->ts_first);

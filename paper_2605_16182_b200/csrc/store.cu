@@ -457,13 +457,13 @@ __global__ void k_ts_rebase(const u32* ts_off, const i64* ts_time, Ring zr, u64 
 }
 
 // ring slice of the edge log -> contiguous columns
-__global__ void k_unring_edges(const u32* s, const u32* d, const i64* t, Ring er, u64 m, u32* os, u32* od, i64* ot) {
+__global__ void k_unring_edges(StoreView v, u64 m, u32* os, u32* od, i64* ot) {
   for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < m;
        i += static_cast<u64>(gridDim.x) * blockDim.x) {
-    const u32 p = er(static_cast<u32>(i));
-    os[i] = s[p];
-    od[i] = d[p];
-    ot[i] = t[p];
+    const EdgeRec r = edge_at(v, i);
+    os[i] = r.src;
+    od[i] = r.dst;
+    ot[i] = r.t;
   }
 }
 
@@ -528,8 +528,7 @@ Store& ensure_compact(Ctx& ctx, const Store& g) {
   c->e_dst.alloc(g.m ? g.m : 1, st);
   c->e_t.alloc(g.m ? g.m : 1, st);
   if (g.m) {
-    k_unring_edges<<<grid(ctx, g.m), kBlock, 0, st>>>(g.e_src.p, g.e_dst.p, g.e_t.p, Ring{0u, g.e_cap, g.e_org}, g.m,
-                                                      c->e_src.p, c->e_dst.p, c->e_t.p);
+    k_unring_edges<<<grid(ctx, g.m), kBlock, 0, st>>>(g.view(), g.m, c->e_src.p, c->e_dst.p, c->e_t.p);
     TWG_LAUNCHED(ctx);
   }
   c->ts_time.alloc(g.Z ? g.Z : 1, st);

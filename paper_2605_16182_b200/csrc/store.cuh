@@ -25,6 +25,13 @@
 
 namespace twg {
 
+// One edge of the streaming log (internal ids): the AoS record a walk start
+// reads in one 128-bit load.
+struct alignas(16) EdgeRec {
+  u32 src, dst;
+  i64 t;
+};
+
 struct alignas(16) Entry {  // one 128-bit load per hop
   u32 nbr;   // ref_neighbor(pos, owner)
   u32 edge;  // ref_edge(pos): index into the time-sorted edge array
@@ -66,9 +73,10 @@ constexpr u32 kIdentityCap = 0xffffffffu;
 struct StoreView {
   int mode;
   u64 m, V, Z, P, Q, A;
-  const u32* e_src;
+  const u32* e_src;    // contiguous stores: SoA edge columns
   const u32* e_dst;
   const i64* e_t;
+  const EdgeRec* erec; // streaming stores: the log's AoS records (e_* null)
   const i64* ext;
   const u32* ts_off;   // group start sequence numbers, Z (+1 terminal in contiguous stores, unused)
   const i64* ts_time;
@@ -86,6 +94,17 @@ struct StoreView {
   Ring erg;  // snapshot edge i -> slot erg(i) of e_src/e_dst/e_t (identity in contiguous stores)
   Ring zrg;  // snapshot ts group g -> slot zrg(g) of ts_off/ts_time
 };
+
+// snapshot edge i
+__device__ __forceinline__ i64 edge_time(const StoreView& s, u64 i) {
+  const u32 p = s.erg(static_cast<u32>(i));
+  return s.erec ? s.erec[p].t : s.e_t[p];
+}
+__device__ __forceinline__ EdgeRec edge_at(const StoreView& s, u64 i) {
+  const u32 p = s.erg(static_cast<u32>(i));
+  if (s.erec) return s.erec[p];
+  return EdgeRec{s.e_src[p], s.e_dst[p], s.e_t[p]};
+}
 
 // Edge range [lo, hi) (snapshot-relative) of timestamp group g < Z.
 __device__ __forceinline__ void ts_group_range(const StoreView& s, u64 g, u64& lo, u64& hi) {
@@ -122,8 +141,7 @@ struct BuildOpts {
 // new entries while ee + y - (oldest live eb in that ring) <= cap, and a
 // replaced log/arena stays alive (shared_ptr) while any snapshot uses it.
 struct EdgeLog {  // two rings of `cap` slots; positions are logical (slot = position mod cap)
-  DevBuf<u32> src, dst;
-  DevBuf<i64> t;
+  DevBuf<EdgeRec> rec;
   DevBuf<u32> ts_off;  // group start sequence numbers
   DevBuf<i64> ts_time;
   u64 cap = 0;     // edges (and groups)
@@ -149,6 +167,7 @@ struct Store {
   bool ext_identity = false;
   DevBuf<u32> e_src, e_dst;
   DevBuf<i64> e_t, ext;
+  DevBuf<EdgeRec> e_rec;  // streaming stores: alias of the log's records
   DevBuf<u32> ts_off;
   DevBuf<i64> ts_time;
   DevBuf<double> ts_w;
@@ -176,13 +195,13 @@ struct Store {
 
   StoreView view() const {
     return StoreView{mode,     m,         V,         Z,          P,         Q,        A,
-                     e_src.p,  e_dst.p,   e_t.p,     ext.p,      ts_off.p,  ts_time.p,
+                     e_src.p,  e_dst.p,   e_t.p,     e_rec.p,    ext.p,     ts_off.p,  ts_time.p,
                      ts_w.p,   nmeta.p,   nm.p,      mk_time.p,  mk_start.p, ent.p,   wp.p,
                      adj_off.p, adj.p,  ext_identity ? 1 : 0, seq0,
                      Ring{0u, e_cap, e_org}, Ring{0u, z_cap, z_org}};
   }
   u64 device_bytes() const {
-    return e_src.bytes() + e_dst.bytes() + e_t.bytes() + ext.bytes() + ts_off.bytes() +
+    return e_src.bytes() + e_dst.bytes() + e_t.bytes() + e_rec.bytes() + ext.bytes() + ts_off.bytes() +
            ts_time.bytes() + ts_w.bytes() + nmeta.bytes() + mk_time.bytes() + mk_start.bytes() +
            ent.bytes() + wp.bytes() + adj_off.bytes() + adj.bytes() + owner.bytes() + nm.bytes() +
            last_t.bytes();

@@ -284,9 +284,9 @@ __device__ __forceinline__ void init_walk(const WalkParams& P, const InitParams&
     const double u2 = P.rng.uniform(w, 0, 1);
     const u64 eidx = sample_start_edge_dev(P.s, I.start_bias, u1, u2, P.expm1_tab, &cn->amb);
     cn->bytes += 24u + (I.start_bias == TWG_EXPWEIGHT ? 8u * (64u - __clzll(P.s.Z)) : 0u);
-    const u32 pe = P.s.erg(static_cast<u32>(eidx));
-    const u32 sv = P.s.e_src[pe], dv = P.s.e_dst[pe];
-    const i64 t = P.s.e_t[pe];
+    const EdgeRec er = edge_at(P.s, eidx);  // one 128-bit load on streaming stores
+    const u32 sv = er.src, dv = er.dst;
+    const i64 t = er.t;
     const u32 from = P.dir == 0 ? sv : dv;
     const u32 to = P.dir == 0 ? dv : sv;
     P.nodes[base] = ext_of(P.s, from);

@@ -115,8 +115,8 @@ __global__ void k_segment_sort(const u32* s, const u32* d, const i64* t, u64 A, 
 template <bool kTimeOrdered>
 __device__ __forceinline__ void agg_max(i64* last, u32 key, i64 t, bool valid);
 
-__global__ void k_batch_fast(const i64* bs, const i64* bd, const i64* bt, u64 n, int mode, u32* os, u32* od, i64* ot,
-                             Ring orr, BatchRec16* rec, i64* last) {
+__global__ void k_batch_fast(const i64* bs, const i64* bd, const i64* bt, u64 n, int mode, EdgeRec* rec, Ring orr,
+                             i64* last) {
   for (u64 k0 = blockIdx.x * static_cast<u64>(blockDim.x); k0 < n; k0 += static_cast<u64>(gridDim.x) * blockDim.x) {
     const u64 k = k0 + threadIdx.x;
     const bool valid = k < n;
@@ -134,12 +134,7 @@ __global__ void k_batch_fast(const i64* bs, const i64* bd, const i64* bt, u64 n,
         key[j] = x;
       }
       for (int j = 0; j < len; ++j) {
-        const u32 a = static_cast<u32>(key[j] >> 32), b = static_cast<u32>(key[j]);
-        const u32 p = orr(static_cast<u32>(k + j));
-        os[p] = a;
-        od[p] = b;
-        ot[p] = tk;
-        rec[k + j] = BatchRec16{a, b, tk};
+        rec[orr(static_cast<u32>(k + j))] = EdgeRec{static_cast<u32>(key[j] >> 32), static_cast<u32>(key[j]), tk};
       }
     }
     // the non-owner endpoint; the owner side is merged by the placement's counts
@@ -148,12 +143,18 @@ __global__ void k_batch_fast(const i64* bs, const i64* bd, const i64* bt, u64 n,
   }
 }
 
-// lower_bound(time_, cutoff) (edge_store.cpp:326) over the snapshot's edge ring
-__global__ void k_lower_bound(const i64* t, Ring er, u64 m, i64 cutoff, u64* out) {
-  u64 lo = 0, hi = m;
+__global__ void k_pack_rec(const u32* s, const u32* d, const i64* t, u64 n, EdgeRec* out) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<u64>(gridDim.x) * blockDim.x)
+    out[i] = EdgeRec{s[i], d[i], t[i]};
+}
+
+// lower_bound(time_, cutoff) (edge_store.cpp:326) over the snapshot's edges
+__global__ void k_lower_bound(StoreView s, i64 cutoff, u64* out) {
+  u64 lo = 0, hi = s.m;
   while (lo < hi) {
     const u64 mid = (lo + hi) >> 1;
-    if (t[er(static_cast<u32>(mid))] < cutoff) lo = mid + 1;
+    if (edge_time(s, mid) < cutoff) lo = mid + 1;
     else hi = mid;
   }
   *out = lo;
@@ -352,14 +353,23 @@ struct K3 {
 };
 
 struct SurvivorKey {
+  StoreView s;
+  const u32* o2n;
+  u64 from;
+  __device__ __forceinline__ K3 operator()(u64 i) const {
+    const EdgeRec r = edge_at(s, from + i);
+    return K3{r.t, (static_cast<u64>(remap(o2n, r.src)) << 32) | remap(o2n, r.dst)};
+  }
+};
+
+struct SurvivorKeySoA {  // contiguous stores (the merge route)
   const u32* e_src;
   const u32* e_dst;
   const i64* e_t;
   const u32* o2n;
   u64 from;
-  Ring er;
   __device__ __forceinline__ K3 operator()(u64 i) const {
-    const u32 p = er(static_cast<u32>(from + i));
+    const u64 p = from + i;
     return K3{e_t[p], (static_cast<u64>(remap(o2n, e_src[p])) << 32) | remap(o2n, e_dst[p])};
   }
 };
@@ -835,8 +845,7 @@ Store* ingest_streaming(Window& w, const i64* bs, const i64* bd, const i64* bt, 
   // of a merge-path pass.
   bool concat = A == 0 || S == 0;
   if (!concat) {
-    k_concat_check<<<1, 1, 0, st>>>(SurvivorKey{Og.e_src.p, Og.e_dst.p, Og.e_t.p, o2n, from, Og.view().erg}, S,
-                                    BatchKey{bS.p, bD.p, bT.p},
+    k_concat_check<<<1, 1, 0, st>>>(SurvivorKey{Og.view(), o2n, from}, S, BatchKey{bS.p, bD.p, bT.p},
                                     ctx.d_scalars + 11);
     TWG_LAUNCHED(ctx);
     u64 c[1];
@@ -848,7 +857,10 @@ Store* ingest_streaming(Window& w, const i64* bs, const i64* bd, const i64* bt, 
   if (concat && identity && A > 0 && append_ingest_enabled()) {
     pt.mark("append_handoff");
     if (scratch_out) *scratch_out = scratch + 48 * (w.mode == TWG_UNDIRECTED ? 2 * A : A) + 40 * Vn;
-    return ingest_append(w, Og, std::move(s), bS.p, bD.p, bT.p, Ring{0u, kIdentityCap, 0u}, A, from, cutoff, false);
+    DevBuf<EdgeRec> brec(A, st);
+    k_pack_rec<<<grid(ctx, A), kBlock, 0, st>>>(bS.p, bD.p, bT.p, A, brec.p);
+    TWG_LAUNCHED(ctx);
+    return ingest_append(w, Og, std::move(s), brec.p, Ring{0u, kIdentityCap, 0u}, A, from, cutoff, false);
   }
   const Store& O = ensure_compact(ctx, Og);  // the rewrite routes below read the contiguous node view
   s->e_src.alloc(s->m ? s->m : 1, st);
@@ -870,8 +882,7 @@ Store* ingest_streaming(Window& w, const i64* bs, const i64* bd, const i64* bt, 
     spos.alloc(S ? S : 1, st);
     bpos.alloc(A ? A : 1, st);
     scratch += 4 * (S + A);
-    merge_path<K3>(ctx, SurvivorKey{O.e_src.p, O.e_dst.p, O.e_t.p, o2n, from, O.view().erg}, S,
-                   BatchKey{bS.p, bD.p, bT.p}, A,
+    merge_path<K3>(ctx, SurvivorKeySoA{O.e_src.p, O.e_dst.p, O.e_t.p, o2n, from}, S, BatchKey{bS.p, bD.p, bT.p}, A,
                    CanonicalEmit{s->e_src.p, s->e_dst.p, s->e_t.p, spos.p, bpos.p});
   }
   pt.mark(concat ? "canonical_concat" : "canonical_merge");
@@ -1013,27 +1024,18 @@ Store* ingest_fast(Window& w, const i64* bs, const i64* bd, const i64* bt, u64 n
   // the canonical batch goes straight into the shared log when it has room
   Ring wring{0u, kIdentityCap, 0u};
   const bool in_log = append_log_slot(O, w.previous, n, &wring);
-  DevBuf<u32> tS, tD;
-  DevBuf<i64> tT;
-  u32 *bS, *bD;
-  i64* bT;
+  DevBuf<EdgeRec> tmp;
+  EdgeRec* rec;
   if (in_log) {
-    bS = O.log->src.p;
-    bD = O.log->dst.p;
-    bT = O.log->t.p;
+    rec = O.log->rec.p;
   } else {
-    tS.alloc(n, st);
-    tD.alloc(n, st);
-    tT.alloc(n, st);
-    bS = tS.p;
-    bD = tD.p;
-    bT = tT.p;
+    tmp.alloc(n, st);
+    rec = tmp.p;
   }
-  DevBuf<BatchRec16> rec(n, st);
   TWG_CUDA(cudaMemsetAsync(ctx.d_scalars + 12, 0, 16, st));
-  k_lower_bound<<<1, 1, 0, st>>>(O.e_t.p, O.view().erg, O.m, cutoff, ctx.d_scalars + 12);
+  k_lower_bound<<<1, 1, 0, st>>>(O.view(), cutoff, ctx.d_scalars + 12);
   TWG_LAUNCHED(ctx);
-  k_batch_fast<<<grid(ctx, n), kBlock, 0, st>>>(bs, bd, bt, n, w.mode, bS, bD, bT, wring, rec.p, s->last_t.p);
+  k_batch_fast<<<grid(ctx, n), kBlock, 0, st>>>(bs, bd, bt, n, w.mode, rec, wring, s->last_t.p);
   TWG_LAUNCHED(ctx);
   u64 r[1];
   read_scalars(ctx, ctx.d_scalars + 12, r, 1);
@@ -1043,7 +1045,7 @@ Store* ingest_fast(Window& w, const i64* bs, const i64* bd, const i64* bt, u64 n
   stats->evicted = from;
   stats->dropped_late = 0;
   w.max_ext = static_cast<i64>(V - 1);
-  Store* out = ingest_append(w, O, std::move(s), bS, bD, bT, wring, n, from, cutoff, true, rec.p, in_log, true);
+  Store* out = ingest_append(w, O, std::move(s), rec, wring, n, from, cutoff, true, in_log, true);
   if (!out) {  // an old node leaves the window: the general route recomputes everything
     stats->evicted = stats->dropped_late = 0;
     return nullptr;
@@ -1125,7 +1127,7 @@ void window_ingest(Window& w, const i64* d_src, const i64* d_dst, const i64* d_t
   }
 
   // survivors (export_suffix) and admitted batch edges
-  k_lower_bound<<<1, 1, 0, st>>>(old.e_t.p, old.view().erg, old.m, cutoff, ctx.d_scalars + 2);
+  k_lower_bound<<<1, 1, 0, st>>>(old.view(), cutoff, ctx.d_scalars + 2);
   TWG_LAUNCHED(ctx);
   DevBuf<u32> pos(n + 1, st);
   exclusive_scan<u32>(ctx, AdmitFn{d_t, cutoff}, n, pos.p);

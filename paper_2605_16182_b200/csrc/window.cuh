@@ -29,23 +29,18 @@ void release_store(Store* s);
 // is the admitted batch in canonical order with internal ids; no_ties:
 // every batch time is newer than every window time (no mark merges).
 bool append_ingest_enabled();
-// one 16-byte record per admitted batch edge (internal ids): the placement's gathers
-struct alignas(16) BatchRec16 {
-  u32 src, dst;
-  i64 t;
-};
+using BatchRec16 = EdgeRec;  // one record per admitted batch edge (internal ids)
 // when the shared log of O can take A more edges in place: the ring that
 // maps batch edge k to its log slot (the batch can be written there directly)
 bool append_log_slot(const Store& O, const Store* R, u64 A, Ring* wr);
-// bS/bD/bT[bring(k)] = batch edge k. rec / in_log: the caller already
-// produced the records / wrote the batch into O's log through the ring
-// append_log_slot returned (bS, bD, bT are then the log's columns).
+// batch[bring(k)] = admitted batch edge k (canonical order, internal ids).
+// in_log: the batch already sits in O's log through the ring append_log_slot
+// returned (batch is then the log's record array).
 // check_dead: s->last_t holds only the non-owner side of the batch; the owner
 // side is merged here and the ingest returns null (nothing published) when an
 // old node would leave the window.
-Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const u32* bS, const u32* bD,
-                     const i64* bT, Ring bring, u64 A, u64 from, i64 cutoff, bool no_ties,
-                     const BatchRec16* rec = nullptr, bool in_log = false, bool check_dead = false);
+Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const EdgeRec* batch, Ring bring, u64 A,
+                     u64 from, i64 cutoff, bool no_ties, bool in_log = false, bool check_dead = false);
 
 Window* window_create(Ctx& ctx, i64 duration, int mode, BuildOpts opts);
 void window_destroy(Window* w);
