@@ -179,6 +179,7 @@ struct Store {
   DevBuf<u32> adj_off, adj;
   DevBuf<u32> owner;  // owner node of each node-view entry (drives the next batch's merge)
   DevBuf<i64> last_t; // newest incident edge time per node: v survives a cutoff c iff last_t[v] >= c
+  bool last_t_exact = true;  // false: a lower bound (the streaming route tracks only the owner side)
   DevBuf<NodeMeta> nm;  // per-node bounds + ring: the walk kernels' node meta (every store)
   u32 seq0 = 0;       // sequence number of edge 0 (StoreView)
   // streaming representation (gapped == true): slices of a shared log/arena

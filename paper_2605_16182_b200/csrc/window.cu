@@ -111,12 +111,11 @@ __global__ void k_segment_sort(const u32* s, const u32* d, const i64* t, u64 A, 
 // Fast append route, batch side in one pass: a time-ordered batch over the
 // existing population 0..V-1 (internal id == external id): canonical order
 // by sorting each short equal-time run by (src, dst) in registers (one
-// thread per run), and the newest-incident-time update of both endpoints.
+// thread per run), written as log records through the ring.
 template <bool kTimeOrdered>
 __device__ __forceinline__ void agg_max(i64* last, u32 key, i64 t, bool valid);
 
-__global__ void k_batch_fast(const i64* bs, const i64* bd, const i64* bt, u64 n, int mode, EdgeRec* rec, Ring orr,
-                             i64* last) {
+__global__ void k_batch_fast(const i64* bs, const i64* bd, const i64* bt, u64 n, EdgeRec* rec, Ring orr) {
   for (u64 k0 = blockIdx.x * static_cast<u64>(blockDim.x); k0 < n; k0 += static_cast<u64>(gridDim.x) * blockDim.x) {
     const u64 k = k0 + threadIdx.x;
     const bool valid = k < n;
@@ -137,9 +136,6 @@ __global__ void k_batch_fast(const i64* bs, const i64* bd, const i64* bt, u64 n,
         rec[orr(static_cast<u32>(k + j))] = EdgeRec{static_cast<u32>(key[j] >> 32), static_cast<u32>(key[j]), tk};
       }
     }
-    // the non-owner endpoint; the owner side is merged by the placement's counts
-    if (mode == TWG_FORWARD) agg_max<true>(last, valid ? static_cast<u32>(bd[k < n ? k : 0]) : 0u, tk, valid);
-    else if (mode == TWG_BACKWARD) agg_max<true>(last, valid ? static_cast<u32>(bs[k < n ? k : 0]) : 0u, tk, valid);
   }
 }
 
@@ -230,6 +226,16 @@ __global__ void k_alive_from_last(const i64* last, u64 V, i64 cutoff, u8* alive)
   for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < V;
        v += static_cast<u64>(gridDim.x) * blockDim.x)
     alive[v] = last[v] >= cutoff ? 1 : 0;
+}
+
+// exact newest incident time of every node of a snapshot (over all its edges)
+__global__ void k_store_last_t(StoreView s, i64* last) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < s.m;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const EdgeRec r = edge_at(s, i);
+    if (last[r.src] < r.t) atomicMax(reinterpret_cast<long long*>(last + r.src), static_cast<long long>(r.t));
+    if (last[r.dst] < r.t) atomicMax(reinterpret_cast<long long*>(last + r.dst), static_cast<long long>(r.t));
+  }
 }
 
 __global__ void k_carry_last_t(const i64* old_last, const u8* alive, const u32* o2n, u64 V, i64* new_last) {
@@ -757,8 +763,19 @@ Store* ingest_streaming(Window& w, const i64* bs, const i64* bd, const i64* bt, 
   scratch += Vo + 5 * R;
   TWG_CUDA(cudaMemsetAsync(present.p, 0, R, st));
   TWG_CUDA(cudaMemsetAsync(ctx.d_scalars + 6, 0, 8, st));
+  // O's newest incident times; exact ones recomputed from its edges when the
+  // streaming route left a lower bound (directed modes)
+  DevBuf<i64> exact_last;
+  const i64* o_last = Og.last_t.p;
+  if (Vo && !Og.last_t_exact) {
+    exact_last.alloc(Vo, st);
+    TWG_CUDA(cudaMemsetAsync(exact_last.p, 0xff, Vo * sizeof(i64), st));
+    k_store_last_t<<<grid(ctx, Og.m), kBlock, 0, st>>>(Og.view(), exact_last.p);
+    TWG_LAUNCHED(ctx);
+    o_last = exact_last.p;
+  }
   if (Vo) {  // O(V) instead of a pass over every survivor's endpoints
-    k_alive_from_last<<<grid(ctx, Vo), kBlock, 0, st>>>(Og.last_t.p, Vo, cutoff, alive.p);
+    k_alive_from_last<<<grid(ctx, Vo), kBlock, 0, st>>>(o_last, Vo, cutoff, alive.p);
     TWG_LAUNCHED(ctx);
   }
   TWG_CUDA(cudaMemsetAsync(ctx.d_scalars + 10, 0, 8, st));
@@ -800,11 +817,11 @@ Store* ingest_streaming(Window& w, const i64* bs, const i64* bd, const i64* bt, 
   // newest incident time per new node: survivors carry theirs, the batch maxes in below
   s->last_t.alloc(Vn ? Vn : 1, st);
   if (identity) {
-    TWG_CUDA(cudaMemcpyAsync(s->last_t.p, Og.last_t.p, Vn * sizeof(i64), cudaMemcpyDeviceToDevice, st));
+    TWG_CUDA(cudaMemcpyAsync(s->last_t.p, o_last, Vn * sizeof(i64), cudaMemcpyDeviceToDevice, st));
   } else {
     TWG_CUDA(cudaMemsetAsync(s->last_t.p, 0xff, s->last_t.bytes(), st));
     if (Vo) {
-      k_carry_last_t<<<grid(ctx, Vo), kBlock, 0, st>>>(Og.last_t.p, alive.p, o2n, Vo, s->last_t.p);
+      k_carry_last_t<<<grid(ctx, Vo), kBlock, 0, st>>>(o_last, alive.p, o2n, Vo, s->last_t.p);
       TWG_LAUNCHED(ctx);
     }
   }
@@ -1019,8 +1036,14 @@ Store* ingest_fast(Window& w, const i64* bs, const i64* bd, const i64* bt, u64 n
   s->ext_identity = true;
   s->ext.alloc(V, st);
   TWG_CUDA(cudaMemcpyAsync(s->ext.p, O.ext.p, V * sizeof(i64), cudaMemcpyDeviceToDevice, st));
+  // newest incident time: only the owner side is tracked here (merged by the
+  // placement's bucket counts); in directed modes the non-owner side would
+  // cost one random atomic per edge, so last_t becomes a lower bound — the
+  // population check stays sound (a node it cannot prove alive sends the
+  // batch to the general route, which recomputes exact times)
   s->last_t.alloc(V, st);
   TWG_CUDA(cudaMemcpyAsync(s->last_t.p, O.last_t.p, V * sizeof(i64), cudaMemcpyDeviceToDevice, st));
+  s->last_t_exact = w.mode == TWG_UNDIRECTED && O.last_t_exact;
   // the canonical batch goes straight into the shared log when it has room
   Ring wring{0u, kIdentityCap, 0u};
   const bool in_log = append_log_slot(O, w.previous, n, &wring);
@@ -1035,7 +1058,7 @@ Store* ingest_fast(Window& w, const i64* bs, const i64* bd, const i64* bt, u64 n
   TWG_CUDA(cudaMemsetAsync(ctx.d_scalars + 12, 0, 16, st));
   k_lower_bound<<<1, 1, 0, st>>>(O.view(), cutoff, ctx.d_scalars + 12);
   TWG_LAUNCHED(ctx);
-  k_batch_fast<<<grid(ctx, n), kBlock, 0, st>>>(bs, bd, bt, n, w.mode, rec, wring, s->last_t.p);
+  k_batch_fast<<<grid(ctx, n), kBlock, 0, st>>>(bs, bd, bt, n, rec, wring);
   TWG_LAUNCHED(ctx);
   u64 r[1];
   read_scalars(ctx, ctx.d_scalars + 12, r, 1);
