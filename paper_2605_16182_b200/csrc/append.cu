@@ -349,8 +349,8 @@ struct PlaceArgs {
   u64* q_total;
 };
 
-struct PlaceSmem {
-  u32 wcnt[kPB / 32][kPB];
+struct PlaceSmem {  // ~34 KB: 6 CTAs per SM
+  u16 wcnt[kPB / 32][kPB];  // chunk counts fit 16 bits (kChunk <= 65535)
   u32 off[kPB + 1];
   u32 cur[kPB], gcur[kPB], base[kPB], cap[kPB], eorg[kPB], gorg[kPB];
   i64 last_t[kPB];
@@ -358,9 +358,10 @@ struct PlaceSmem {
   u32 mtotal;
   u8 snode[kChunk];
   u8 flag[kChunk];
-  u32 mscan[kChunk];
+  u16 mscan[kChunk];
   Entry sent[kChunk];
 };
+static_assert(kChunk < 65536, "16-bit chunk counters");
 
 // One CTA per bucket of 256 nodes (thread t <-> node (bucket << 8) + t):
 // the bucket's entries in rounds of kChunk: stable rank per node
@@ -413,7 +414,7 @@ __global__ void __launch_bounds__(kPB) k_bucket_place(PlaceArgs a) {
       const u32 peers = digit_peers<kBucketShift>(d, ok);
       const u32 before = ok ? sm.wcnt[warp][d] : 0u;
       __syncwarp();
-      if (ok && (__ffs(peers) - 1) == lane) sm.wcnt[warp][d] = before + __popc(peers);
+      if (ok && (__ffs(peers) - 1) == lane) sm.wcnt[warp][d] = static_cast<u16>(before + __popc(peers));
       __syncwarp();
       rank[r] = before + __popc(peers & lt);
     }
@@ -423,7 +424,7 @@ __global__ void __launch_bounds__(kPB) k_bucket_place(PlaceArgs a) {
 #pragma unroll
       for (int w = 0; w < kPB / 32; ++w) {
         const u32 c = sm.wcnt[w][t];
-        sm.wcnt[w][t] = acc;
+        sm.wcnt[w][t] = static_cast<u16>(acc);
         acc += c;
       }
       u32 total;
@@ -462,7 +463,7 @@ __global__ void __launch_bounds__(kPB) k_bucket_place(PlaceArgs a) {
 #pragma unroll
     for (int r = 0; r < kChunkItems; ++r) {
       const u32 i = t * kChunkItems + r;
-      sm.mscan[i] = run;
+      sm.mscan[i] = static_cast<u16>(run);
       run += sm.flag[i];
     }
     if (t == 0) sm.mtotal = mtot;
