@@ -356,6 +356,7 @@ struct PlaceSmem {  // ~34 KB: 6 CTAs per SM
   i64 last_t[kPB];
   u32 has_last[kPB];
   u32 mtotal;
+  u32 rwcnt[kChunkItems][kPB / 32];
   u8 snode[kChunk];
   u8 flag[kChunk];
   u16 mscan[kChunk];
@@ -443,11 +444,12 @@ __global__ void __launch_bounds__(kPB) k_bucket_place(PlaceArgs a) {
       }
     }
     __syncthreads();
-    // mark flags over the staged order + block scan (consecutive items per thread)
-    u32 fsum = 0;
+    // mark flags over the staged order; item i = r*256 + t (conflict-free
+    // smem reads), prefixes from per-(round, warp) ballot counts
+    u32 fl[kChunkItems];
 #pragma unroll
     for (int r = 0; r < kChunkItems; ++r) {
-      const u32 i = t * kChunkItems + r;
+      const u32 i = r * kPB + t;
       u32 f = 0;
       if (i < n) {
         const u32 nd = sm.snode[i];
@@ -455,18 +457,23 @@ __global__ void __launch_bounds__(kPB) k_bucket_place(PlaceArgs a) {
         if (i == sm.off[nd]) f = (!sm.has_last[nd] || ti != sm.last_t[nd]) ? 1u : 0u;
         else f = ti != sm.sent[i - 1].t ? 1u : 0u;
       }
-      sm.flag[i] = static_cast<u8>(f);
-      fsum += f;
+      fl[r] = __ballot_sync(0xffffffffu, f != 0);
+      if (lane == 0) sm.rwcnt[r][warp] = __popc(fl[r]);
     }
-    u32 mtot;
-    u32 run = block_excl_scan<u32>(fsum, &mtot);
+    __syncthreads();
+    if (warp == 0) {  // exclusive scan of the kChunkItems x 8 counts in item order
+      const u32 c = lane < kChunkItems * (kPB / 32) ? (&sm.rwcnt[0][0])[lane] : 0u;
+      const u32 incl = warp_incl_scan(c);
+      if (lane < kChunkItems * (kPB / 32)) (&sm.rwcnt[0][0])[lane] = incl - c;
+      if (lane == 31) sm.mtotal = incl;
+    }
+    __syncthreads();
 #pragma unroll
     for (int r = 0; r < kChunkItems; ++r) {
-      const u32 i = t * kChunkItems + r;
-      sm.mscan[i] = static_cast<u16>(run);
-      run += sm.flag[i];
+      const u32 i = r * kPB + t;
+      sm.mscan[i] = static_cast<u16>(sm.rwcnt[r][warp] + __popc(fl[r] & lt));
+      sm.flag[i] = static_cast<u8>((fl[r] >> lane) & 1u);
     }
-    if (t == 0) sm.mtotal = mtot;
     __syncthreads();
     // write out in staged (node) order
     for (u32 i = t; i < n; i += kPB) {

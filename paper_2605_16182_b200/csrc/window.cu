@@ -116,26 +116,22 @@ template <bool kTimeOrdered>
 __device__ __forceinline__ void agg_max(i64* last, u32 key, i64 t, bool valid);
 
 __global__ void k_batch_fast(const i64* bs, const i64* bd, const i64* bt, u64 n, EdgeRec* rec, Ring orr) {
-  for (u64 k0 = blockIdx.x * static_cast<u64>(blockDim.x); k0 < n; k0 += static_cast<u64>(gridDim.x) * blockDim.x) {
-    const u64 k = k0 + threadIdx.x;
-    const bool valid = k < n;
-    const i64 tk = valid ? bt[k] : 0;
-    if (valid && !(k > 0 && bt[k - 1] == tk)) {
-      u64 key[kSegMax];
-      int len = 0;
-      while (len < kSegMax && k + len < n && bt[k + len] == tk) {
-        const u64 x = (static_cast<u64>(bs[k + len]) << 32) | static_cast<u64>(bd[k + len]);
-        int j = len++;
-        while (j > 0 && key[j - 1] > x) {
-          key[j] = key[j - 1];
-          --j;
-        }
-        key[j] = x;
-      }
-      for (int j = 0; j < len; ++j) {
-        rec[orr(static_cast<u32>(k + j))] = EdgeRec{static_cast<u32>(key[j] >> 32), static_cast<u32>(key[j]), tk};
-      }
+  // one thread per edge: its rank by (src, dst) inside its equal-time run
+  // (runs are <= kSegMax long: the batch shape check), neighbours from L1
+  for (u64 k = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const i64 tk = bt[k];
+    u64 lo = k, hi = k + 1;
+    while (lo > 0 && bt[lo - 1] == tk) --lo;
+    while (hi < n && bt[hi] == tk) ++hi;
+    const u64 sk = static_cast<u64>(bs[k]), dk = static_cast<u64>(bd[k]);
+    const u64 key = (sk << 32) | dk;
+    u32 rank = 0;
+    for (u64 q = lo; q < hi; ++q) {
+      const u64 kq = (static_cast<u64>(bs[q]) << 32) | static_cast<u64>(bd[q]);
+      rank += (kq < key || (kq == key && q < k)) ? 1u : 0u;  // equal keys: content-equal, any stable order
     }
+    rec[orr(static_cast<u32>(lo + rank))] = EdgeRec{static_cast<u32>(sk), static_cast<u32>(dk), tk};
   }
 }
 
