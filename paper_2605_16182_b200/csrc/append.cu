@@ -166,6 +166,28 @@ __global__ void k_owner_keys(const Rec* rec, Ring br, u64 A, int mode, u32 seq_b
   }
 }
 
+// (owner, node-view entry) of batch entry j, computed from the log records
+struct OwnerIn {
+  const Rec* rec;
+  Ring br;
+  int mode;
+  u32 seq_b;
+  __device__ __forceinline__ u32 key(u64 j) const {
+    const Rec r = rec[br(mode == TWG_UNDIRECTED ? static_cast<u32>(j >> 1) : static_cast<u32>(j))];
+    return mode == TWG_UNDIRECTED ? ((j & 1) ? r.dst : r.src) : (mode == TWG_BACKWARD ? r.dst : r.src);
+  }
+  __device__ __forceinline__ Entry val(u64 j) const {
+    const u32 k = mode == TWG_UNDIRECTED ? static_cast<u32>(j >> 1) : static_cast<u32>(j);
+    const Rec r = rec[br(k)];
+    Entry e;
+    e.nbr = nbr_of(mode, r, static_cast<u32>(j));
+    e.edge = seq_b + k;
+    e.t = r.t;
+    return e;
+  }
+  __device__ __forceinline__ bool has_val() const { return true; }
+};
+
 // bucket b = owner >> 8 of the bucket-sorted entries starts at bstart[b]
 // (empty buckets included); bstart[nb] = Yn
 __global__ void k_bucket_bounds(const u32* keys, u64 Yn, u64 nb, u32* bstart) {
@@ -622,10 +644,13 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
   u32* ka = k1.p;
   Entry* vp = v0.p;
   Entry* va = v1.p;
-  k_owner_keys<<<grid(ctx, Yn), kBlock, 0, st>>>(brec, wr, A, mode, seq_b, kp, vp);
-  TWG_LAUNCHED(ctx);
-  if (vb > static_cast<int>(kBucketShift))
-    radix_sort_pairs<u32, Entry>(ctx, &kp, &ka, &vp, &va, Yn, vb, kBucketShift);
+  if (vb > static_cast<int>(kBucketShift)) {  // the first pass builds (owner, entry) from the log records
+    radix_sort_pairs_from<u32, Entry>(ctx, OwnerIn{brec, wr, mode, seq_b}, &kp, &ka, &vp, &va, Yn, vb,
+                                      kBucketShift);
+  } else {
+    k_owner_keys<<<grid(ctx, Yn), kBlock, 0, st>>>(brec, wr, A, mode, seq_b, kp, vp);
+    TWG_LAUNCHED(ctx);
+  }
   DevBuf<u32> bstart(nb + 1, st);
   k_bucket_bounds<<<grid(ctx, Yn + 1), kBlock, 0, st>>>(kp, Yn, nb, bstart.p);
   TWG_LAUNCHED(ctx);

@@ -147,9 +147,20 @@ void exclusive_scan(Ctx& ctx, In in, u64 n, T* out) {
 
 // --------------------------------------------------------------- radix ----
 
-template <class K, int kItems = kSortItems>
-__global__ void __launch_bounds__(kSortBlock) k_radix_hist(const K* __restrict__ keys, u64 n, int shift,
-                                                           u32* __restrict__ counts, u64 tiles) {
+// Input of a radix pass: arrays, or (first pass) a functor computing the
+// (key, value) of item i from some other layout (In::key(i), In::val(i)).
+template <class K, class V>
+struct ArrayIn {
+  const K* k;
+  const V* v;
+  __device__ __forceinline__ K key(u64 i) const { return k[i]; }
+  __device__ __forceinline__ V val(u64 i) const { return v[i]; }
+  __device__ __forceinline__ bool has_val() const { return v != nullptr; }
+};
+
+template <class K, int kItems = kSortItems, class In = ArrayIn<K, u32>>
+__global__ void __launch_bounds__(kSortBlock) k_radix_hist(In in, u64 n, int shift, u32* __restrict__ counts,
+                                                           u64 tiles) {
   constexpr int kTile = kSortBlock * kItems;
   __shared__ u32 hist[kRadix];
   for (int b = threadIdx.x; b < kRadix; b += kSortBlock) hist[b] = 0;
@@ -158,7 +169,7 @@ __global__ void __launch_bounds__(kSortBlock) k_radix_hist(const K* __restrict__
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
     const u64 i = base + static_cast<u64>(j) * kSortBlock + threadIdx.x;
-    if (i < n) atomicAdd(&hist[static_cast<u32>(keys[i] >> shift) & (kRadix - 1)], 1u);
+    if (i < n) atomicAdd(&hist[static_cast<u32>(in.key(i) >> shift) & (kRadix - 1)], 1u);
   }
   __syncthreads();
   for (int b = threadIdx.x; b < kRadix; b += kSortBlock) counts[static_cast<u64>(b) * tiles + blockIdx.x] = hist[b];
@@ -168,13 +179,12 @@ __global__ void __launch_bounds__(kSortBlock) k_radix_hist(const K* __restrict__
 // (round j, warp, lane) == input order, which keeps the sort stable. V is
 // the value type (u32 indices, or a 16-byte payload carried through the
 // passes so the consumer reads it in order instead of gathering it).
-template <class K, class V, int kItems>
-__global__ void __launch_bounds__(kSortBlock) k_radix_scatter(const K* __restrict__ keys_in,
-                                                              const V* __restrict__ vals_in,
-                                                              K* __restrict__ keys_out,
+template <class K, class V, int kItems, class In = ArrayIn<K, V>>
+__global__ void __launch_bounds__(kSortBlock) k_radix_scatter(In in, K* __restrict__ keys_out,
                                                               V* __restrict__ vals_out, u64 n,
                                                               int shift, const u32* __restrict__ offsets,
                                                               u64 tiles) {
+  const bool has_val = in.has_val();
   constexpr int kWarps = kSortBlock / 32;
   constexpr int kTile = kSortBlock * kItems;
   __shared__ u32 wcount[kWarps][kRadix];
@@ -201,8 +211,8 @@ __global__ void __launch_bounds__(kSortBlock) k_radix_scatter(const K* __restric
   for (int j = 0; j < kItems; ++j) {
     const u64 i = wbase + static_cast<u64>(j) * 32 + lane;
     const bool valid = i < n;
-    key[j] = valid ? keys_in[i] : K(0);
-    if (vals_in && valid) val[j] = vals_in[i];
+    key[j] = valid ? in.key(i) : K(0);
+    if (has_val && valid) val[j] = in.val(i);
   }
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
@@ -244,7 +254,7 @@ __global__ void __launch_bounds__(kSortBlock) k_radix_scatter(const K* __restric
       const u32 d = static_cast<u32>(key[j] >> shift) & (kRadix - 1);
       const u32 pos = tile_start[d] + wcount[warp][d] + rank[j];
       skeys[pos] = key[j];
-      if (vals_in) svals[pos] = val[j];
+      if (has_val) svals[pos] = val[j];
     }
   }
   __syncthreads();
@@ -257,7 +267,7 @@ __global__ void __launch_bounds__(kSortBlock) k_radix_scatter(const K* __restric
       const u32 d = static_cast<u32>(k >> shift) & (kRadix - 1);
       const u64 dst = static_cast<u64>(offsets[static_cast<u64>(d) * tiles + blockIdx.x]) + (pos - tile_start[d]);
       keys_out[dst] = k;
-      if (vals_in) vals_out[dst] = svals[pos];
+      if (has_val) vals_out[dst] = svals[pos];
     }
   }
 }
@@ -493,27 +503,41 @@ void merge_path(Ctx& ctx, KA ka, u64 na, KB kb, u64 nb, Emit emit) {
 // output lands in (*keys, *vals); the alt buffers are scratch of the same
 // size. Pointers are swapped as passes ping-pong. n < 2^32. Keys-only when
 // *vals == nullptr.
-template <class K, class V = u32>
-void radix_sort_pairs(Ctx& ctx, K** keys, K** keys_alt, V** vals, V** vals_alt, u64 n, int bits, int lo_bit = 0) {
-  if (n < 2 || bits <= lo_bit) return;
-  // 16-byte payloads: half the items per thread keeps the staging under 48 KB
-  constexpr int kItems = sizeof(V) > 4 ? kSortItems / 2 : kSortItems;
+// One LSD pass over digit `shift`: (in) -> (keys_out, vals_out).
+template <class K, class V, class In>
+void radix_pass(Ctx& ctx, In in, K* keys_out, V* vals_out, u64 n, int shift) {
+  constexpr int kItems = sizeof(V) > 4 ? kSortItems / 2 : kSortItems;  // 16-B payloads: staging < 48 KB
   constexpr int kTile = kSortBlock * kItems;
   cudaStream_t st = ctx.stream;
   const u64 tiles = (n + kTile - 1) / kTile;
   if (tiles * kRadix >= (1ull << 32)) fail(TWG_EINVAL, "radix_sort_pairs: input too large");
   DevBuf<u32> counts(tiles * kRadix + 1, st);
   DevBuf<u32> offsets(tiles * kRadix + 1, st);
+  k_radix_hist<K, kItems, In><<<static_cast<unsigned>(tiles), kSortBlock, 0, st>>>(in, n, shift, counts.p, tiles);
+  TWG_LAUNCHED(ctx);
+  exclusive_scan<u32>(ctx, LoadFn<u32>{counts.p}, tiles * kRadix, offsets.p);
+  k_radix_scatter<K, V, kItems, In><<<static_cast<unsigned>(tiles), kSortBlock, 0, st>>>(in, keys_out, vals_out, n,
+                                                                                          shift, offsets.p, tiles);
+  TWG_LAUNCHED(ctx);
+}
+
+template <class K, class V = u32>
+void radix_sort_pairs(Ctx& ctx, K** keys, K** keys_alt, V** vals, V** vals_alt, u64 n, int bits, int lo_bit = 0) {
+  if (n < 2 || bits <= lo_bit) return;
   for (int shift = lo_bit; shift < bits; shift += kRadixBits) {
-    k_radix_hist<K, kItems><<<static_cast<unsigned>(tiles), kSortBlock, 0, st>>>(*keys, n, shift, counts.p, tiles);
-    TWG_LAUNCHED(ctx);
-    exclusive_scan<u32>(ctx, LoadFn<u32>{counts.p}, tiles * kRadix, offsets.p);
-    k_radix_scatter<K, V, kItems><<<static_cast<unsigned>(tiles), kSortBlock, 0, st>>>(
-        *keys, *vals, *keys_alt, *vals_alt, n, shift, offsets.p, tiles);
-    TWG_LAUNCHED(ctx);
+    radix_pass<K, V>(ctx, ArrayIn<K, V>{*keys, *vals}, *keys_alt, *vals_alt, n, shift);
     std::swap(*keys, *keys_alt);
     std::swap(*vals, *vals_alt);
   }
+}
+
+// Same, the first pass reading its items through `in` (sorted result in
+// (*keys, *vals); n >= 1).
+template <class K, class V, class In>
+void radix_sort_pairs_from(Ctx& ctx, In in, K** keys, K** keys_alt, V** vals, V** vals_alt, u64 n, int bits,
+                           int lo_bit) {
+  radix_pass<K, V>(ctx, in, *keys, *vals, n, lo_bit);
+  radix_sort_pairs<K, V>(ctx, keys, keys_alt, vals, vals_alt, n, bits, lo_bit + kRadixBits);
 }
 
 }  // namespace twg
