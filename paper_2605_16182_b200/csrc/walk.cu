@@ -379,29 +379,6 @@ __global__ void __launch_bounds__(kBlock) k_init_states(WalkParams P, InitParams
   add_counters(stats, cn);
 }
 
-struct AliveFn {
-  const u32* ids;
-  const u8* flags;
-  __device__ __forceinline__ u32 operator()(u64 i) const { return flags[ids[i]] & 1u; }
-};
-
-__global__ void k_compact_alive(const u32* ids, u64 n, const u8* flags, const u32* cur, const u32* pos, u32* keys,
-                                u32* vals) {
-  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<u64>(gridDim.x) * blockDim.x) {
-    const u32 w = ids[i];
-    if (flags[w] & 1u) {
-      keys[pos[i]] = cur[w];
-      vals[pos[i]] = w;
-    }
-  }
-}
-
-struct RunFlagFn {
-  const u32* keys;
-  __device__ __forceinline__ u32 operator()(u64 i) const { return (i == 0 || keys[i] != keys[i - 1]) ? 1u : 0u; }
-};
-
 // DispatchTask (walk_engine.hpp:87-94)
 struct Task {
   u32 node;
@@ -416,10 +393,6 @@ struct TaskLists {
   // count[0..4] tasks per list; count[5] / count[6] split pieces in the
   // block-cached / block-direct lists (booked as multi_block, :157-161)
   u32* count;
-};
-
-struct OneFn {
-  __device__ __forceinline__ u32 operator()(u64) const { return 1u; }
 };
 
 // Classify runs on the dispatch plane (walk_engine.cpp:314-343).
@@ -492,20 +465,6 @@ __device__ __forceinline__ void hop_member(const WalkParams& P, const StateArray
   store_state(S, w, r, alive, P.stride);
 }
 
-// solo tier: one thread per task (W < w_warp), global marks
-__global__ void __launch_bounds__(kBlock) k_tier_solo(WalkParams P, StateArrays S, const u32* ids, const Task* tasks,
-                                                      const u32* count, u64* stats) {
-  const u32 n = *count;
-  Ctr amb{0, 0};
-  for (u32 k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-    const Task task = tasks[k];
-    const NodeMeta a = P.s.nm[task.node];
-    for (u32 i = task.begin; i < task.end; ++i)
-      hop_member(P, S, ids[i], P.s.mk_time, P.s.mk_start, mark_ring(a), a.gb, a.ge, entry_ring(a), a.eb, a.ee, &amb);
-  }
-  add_counters(stats, amb);
-}
-
 // warp tiers: one warp per task; cached => the node's marks staged in this
 // warp's shared-memory slice (G <= cap)
 template <bool kCached>
@@ -573,6 +532,68 @@ __global__ void __launch_bounds__(kBlock) k_tier_block(WalkParams P, StateArrays
     }
   }
   add_counters(stats, amb);
+}
+
+// ---- Coop step, front half (Alg. 1 step 1-3 without the global sort) ----
+// The run length W of a node is its number of alive walks, so the solo tier
+// (W < w_warp: one thread per walk, global marks) needs no grouping at all:
+// a histogram of the current nodes decides it per walk. Only walks on nodes
+// with W >= w_warp (the warp / block tiers) are compacted and sorted by node.
+// Outputs are identical (every draw is keyed by (walk, hop)); tier counts are
+// the reference's (one solo task per distinct solo node).
+__global__ void k_coop_count(StateArrays S, u64 count, u32* ncnt, u8* first, u64* alive) {
+  u64 a = 0;
+  for (u64 w = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; w < count;
+       w += static_cast<u64>(gridDim.x) * blockDim.x) {
+    if (S.flags[w] & 1u) {
+      first[w] = atomicAdd(ncnt + S.cur[w], 1u) == 0 ? 1 : 0;
+      ++a;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  if ((threadIdx.x & 31) == 0 && a) atomicAdd(reinterpret_cast<unsigned long long*>(alive), a);
+}
+
+// solo walks hop now; the others are compacted into (node, walk) pairs.
+// scal: [0] hub walks, [1] solo tasks (distinct solo nodes)
+__global__ void __launch_bounds__(kBlock) k_coop_solo(WalkParams P, StateArrays S, u64 count, const u32* ncnt,
+                                                     const u8* first, u32 w_warp, u32* hub_keys, u32* hub_vals,
+                                                     u64* scal, u64* stats) {
+  Ctr cn{0, 0};
+  const u32 lane = threadIdx.x & 31;
+  for (u64 b = blockIdx.x * static_cast<u64>(blockDim.x); b < count; b += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const u64 w = b + threadIdx.x;
+    bool hub = false, solo_task = false;
+    u32 node = 0;
+    if (w < count && (S.flags[w] & 1u)) {
+      node = S.cur[w];
+      if (ncnt[node] < w_warp) {
+        solo_task = first[w] != 0;
+        const NodeMeta a = P.s.nm[node];
+        WalkReg r;
+        load_state(S, static_cast<u32>(w), r);
+        const bool ok = hop(P, w, r, P.s.mk_time, P.s.mk_start, mark_ring(a), a.gb, a.ge, entry_ring(a), a.eb, a.ee,
+                            &cn);
+        store_state(S, static_cast<u32>(w), r, ok, P.stride);
+      } else {
+        hub = true;
+      }
+    }
+    const u32 hb = __ballot_sync(0xffffffffu, hub), sb = __ballot_sync(0xffffffffu, solo_task);
+    u32 base = 0;
+    if (lane == 0) {
+      if (hb) base = static_cast<u32>(atomicAdd(reinterpret_cast<unsigned long long*>(&scal[0]),
+                                                static_cast<unsigned long long>(__popc(hb))));
+      if (sb) atomicAdd(reinterpret_cast<unsigned long long*>(&scal[1]), static_cast<unsigned long long>(__popc(sb)));
+    }
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (hub) {
+      const u32 k = base + __popc(hb & ((1u << lane) - 1u));
+      hub_keys[k] = node;
+      hub_vals[k] = static_cast<u32>(w);
+    }
+  }
+  add_counters(stats, cn);
 }
 
 __global__ void k_finalize(const StateArrays S, u64 count, u32* lengths, u64* stats) {
@@ -933,13 +954,10 @@ WalkSetDev* generate_walks(Ctx& ctx, Store& s_in, const twg_walk_config& cfg, co
     StateArrays S{cur.p, prev.p, tt.p, len.p, flags.p};
     k_init_states<<<grid_for(count, kBlock, 0xffffffffu), kBlock, 0, st>>>(P, I, count, S, stats.p);
     TWG_LAUNCHED(ctx);
-    DevBuf<u32> ids(count, st), pos(count + 1, st), k0(count, st), k1(count, st), v0(count, st), v1(count, st);
+    DevBuf<u32> k0(count, st), k1(count, st), v0(count, st), v1(count, st);
     DevBuf<Task> tasks(5 * count, st);
     DevBuf<u32> subcount(5 * count, st);
     DevBuf<u32> counters(8, st);
-    // candidates = iota (walk_engine.cpp:395-398), as the scan of all-ones
-    exclusive_scan<u32>(ctx, OneFn{}, count, ids.p);
-    u64 n_cand = count;
     const int vb = s.V > 1 ? bit_width_u64(s.V - 1) : 0;
     TaskLists T;
     for (int k = 0; k < 5; ++k) {
@@ -959,25 +977,32 @@ WalkSetDev* generate_walks(Ctx& ctx, Store& s_in, const twg_walk_config& cfg, co
     if (cache)
       TWG_CUDA(cudaFuncSetAttribute(k_tier_block<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(block_smem)));
+    DevBuf<u32> ncnt(s.V ? s.V : 1, st);
+    DevBuf<u8> first(count, st);
+    u64* sc2 = ctx.d_scalars + 48;  // [48] alive, [49] hub walks, [50] solo tasks
     while (true) {
-      // 1. flag + compact alive (partition_flagged, primitives.cpp:140-148)
-      exclusive_scan<u32>(ctx, AliveFn{ids.p, flags.p}, n_cand, pos.p);
-      u64 sc[1];
-      TWG_CUDA(cudaMemsetAsync(ctx.d_scalars, 0, 8, st));
-      TWG_CUDA(cudaMemcpyAsync(ctx.d_scalars, pos.p + n_cand, 4, cudaMemcpyDeviceToDevice, st));
-      read_scalars(ctx, ctx.d_scalars, sc, 1);
-      const u64 n = sc[0];
-      if (n == 0) break;
-      ++coop_steps;
-      k_compact_alive<<<grid(ctx, n_cand), kBlock, 0, st>>>(ids.p, n_cand, flags.p, cur.p, pos.p, k0.p, v0.p);
+      // 1. alive walks per current node (the run lengths W)
+      TWG_CUDA(cudaMemsetAsync(ncnt.p, 0, ncnt.bytes(), st));
+      TWG_CUDA(cudaMemsetAsync(sc2, 0, 3 * sizeof(u64), st));
+      k_coop_count<<<grid(ctx, count), kBlock, 0, st>>>(S, count, ncnt.p, first.p, sc2);
       TWG_LAUNCHED(ctx);
-      // 2. stable sort (node, walk) by node
+      // 2. solo tier (W < w_warp): hop per walk; the rest compacted as (node, walk)
+      k_coop_solo<<<grid(ctx, count), kBlock, 0, st>>>(P, S, count, ncnt.p, first.p, th.w_warp, k0.p, v0.p, sc2 + 1,
+                                                        stats.p);
+      TWG_LAUNCHED(ctx);
+      u64 sc[3];
+      read_scalars(ctx, sc2, sc, 3);
+      if (sc[0] == 0) break;
+      ++coop_steps;
+      tiers[0] += sc[2];
+      const u64 n = sc[1];
+      if (n == 0) continue;
+      // 3. stable sort of the hub walks by node, runs, dispatch plane, mega-hub split
       u32* kp = k0.p;
       u32* ka = k1.p;
       u32* vp = v0.p;
       u32* va = v1.p;
       radix_sort_pairs<u32>(ctx, &kp, &ka, &vp, &va, n, vb);
-      // 3-5. RLE + dispatch plane + mega-hub split
       TWG_CUDA(cudaMemsetAsync(counters.p, 0, counters.bytes(), st));
       k_classify<<<grid(ctx, n), kBlock, 0, st>>>(kp, n, s.view(), th, T);
       TWG_LAUNCHED(ctx);
@@ -986,15 +1011,11 @@ WalkSetDev* generate_walks(Ctx& ctx, Store& s_in, const twg_walk_config& cfg, co
       read_scalars(ctx, reinterpret_cast<const u64*>(counters.p), words, 4);
       std::memcpy(cnt, words, sizeof cnt);
       // tier counts (count_tier, walk_engine.cpp:157-169): split pieces count as multi_block
-      for (int k = 0; k < 3; ++k) tiers[k] += cnt[k];
+      for (int k = 1; k < 3; ++k) tiers[k] += cnt[k];
       tiers[3] += cnt[3] - cnt[5];
       tiers[4] += cnt[4] - cnt[6];
       tiers[5] += cnt[5] + cnt[6];
-      // 6. terminal tiers
-      if (cnt[0]) {
-        k_tier_solo<<<grid(ctx, cnt[0]), kBlock, 0, st>>>(P, S, vp, T.list[0], counters.p + 0, stats.p);
-        TWG_LAUNCHED(ctx);
-      }
+      // 4. terminal tiers (runs here all have W >= w_warp)
       if (cnt[1]) {
         if (warp_stage) {
           k_tier_warp<true><<<static_cast<unsigned>(std::min<u64>((cnt[1] + 7) / 8, 1u << 20)), kBlock, warp_smem, st>>>(
@@ -1025,9 +1046,6 @@ WalkSetDev* generate_walks(Ctx& ctx, Store& s_in, const twg_walk_config& cfg, co
             P, S, vp, T.list[4], counters.p + 4, 0, stats.p);
         TWG_LAUNCHED(ctx);
       }
-      // next candidates = this step's grouped order (walk_engine.cpp:416)
-      TWG_CUDA(cudaMemcpyAsync(ids.p, vp, n * sizeof(u32), cudaMemcpyDeviceToDevice, st));
-      n_cand = n;
     }
     k_finalize<<<grid_for(count, kBlock, 0xffffffffu), kBlock, 0, st>>>(S, count, out->lengths.p, stats.p);
     TWG_LAUNCHED(ctx);
