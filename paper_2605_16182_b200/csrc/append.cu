@@ -38,11 +38,6 @@ constexpr int kChunk = 1024;       // bucket entries staged per placement round
 constexpr int kChunkItems = kChunk / kPB;
 static_assert(kPB == 1 << kBucketShift, "one thread per bucket node");
 
-__device__ __forceinline__ u32 owner_of(int mode, const u32* s, const u32* d, u64 j) {
-  if (mode == TWG_UNDIRECTED) return (j & 1) ? d[j >> 1] : s[j >> 1];
-  return mode == TWG_BACKWARD ? d[j] : s[j];
-}
-
 unsigned grid(Ctx& ctx, u64 n) { return grid_for(n, kBlock, static_cast<unsigned>(ctx.sm_count) * 16); }
 
 // first k in [0, n) with t[zr(k)] >= x (one thread)
@@ -131,12 +126,9 @@ __device__ __forceinline__ u32 gallop_lb(TimeAt at, u32 lo, u32 hi, i64 c) {
   return a;
 }
 
-__device__ __forceinline__ u32 entry_edge(int mode, u32 j) { return mode == TWG_UNDIRECTED ? (j >> 1) : j; }
-
 using Rec = BatchRec16;
 
-// the sorted batch into the log, plus a 16-byte record per edge for the
-// owner-ordered gathers
+// the admitted batch into the log ring
 __global__ void k_append_batch(const EdgeRec* b, Ring br, u64 n, EdgeRec* log, Ring wr) {
   for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<u64>(gridDim.x) * blockDim.x)

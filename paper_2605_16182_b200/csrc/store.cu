@@ -189,17 +189,6 @@ struct TimeChangeFn {
   __device__ __forceinline__ u32 operator()(u64 i) const { return (i == 0 || t[i] != t[i - 1]) ? 1u : 0u; }
 };
 
-__global__ void k_ts_fill(const i64* t, const u32* gscan, u64 m, u32* ts_off, i64* ts_time) {
-  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < m;
-       i += static_cast<u64>(gridDim.x) * blockDim.x) {
-    if (i == 0 || t[i] != t[i - 1]) {
-      const u32 g = gscan[i];
-      ts_off[g] = static_cast<u32>(i);
-      ts_time[g] = t[i];
-    }
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) ts_off[gscan[m]] = static_cast<u32>(m);
-}
 
 // ts_w[g] = sum_{h<=g} exp(t_h - t_last) (edge_store.cpp:100-110). Zero
 // prefix by memset; this one-warp kernel does the <=746-group serial tail.
@@ -248,18 +237,6 @@ __global__ void k_entries(const u32* owners, const u32* jidx, u64 P, int mode, c
   }
 }
 
-// Region bounds from the sorted owner keys: every v in (owner[pos-1], owner[pos]]
-// starts at pos; the tail (owner[P-1], V] starts at P. Writes each v once.
-__global__ void k_region_bounds(const u32* owners, u64 P, u64 V, uint2* nmeta) {
-  for (u64 pos = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; pos <= P;
-       pos += static_cast<u64>(gridDim.x) * blockDim.x) {
-    const u64 lo = pos == 0 ? 0 : static_cast<u64>(owners[pos - 1]) + 1;
-    const u64 hi = pos == P ? V : static_cast<u64>(owners[pos]);
-    if (pos == 0 || pos == P || owners[pos] != owners[pos - 1]) {
-      for (u64 v = lo; v <= hi && v <= V; ++v) nmeta[v].x = static_cast<u32>(pos);
-    }
-  }
-}
 
 struct GroupStartFn {
   const u32* owners;
@@ -269,23 +246,7 @@ struct GroupStartFn {
   }
 };
 
-__global__ void k_marks(const u32* owners, const Entry* ent, const u32* gscan, u64 P, i64* mk_time, u32* mk_start) {
-  for (u64 p = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; p < P;
-       p += static_cast<u64>(gridDim.x) * blockDim.x) {
-    if (p == 0 || owners[p] != owners[p - 1] || ent[p].t != ent[p - 1].t) {
-      const u32 g = gscan[p];
-      mk_time[g] = ent[p].t;
-      mk_start[g] = static_cast<u32>(p);
-    }
-  }
-}
 
-__global__ void k_group_offsets(const u32* gscan, u64 P, u64 V, uint2* nmeta) {
-  for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v <= V;
-       v += static_cast<u64>(gridDim.x) * blockDim.x) {
-    nmeta[v].y = gscan[nmeta[v].x];  // gscan[P] == Q
-  }
-}
 
 // node_weight_prefix_ (edge_store.cpp:159, :208-209): per node, serial sum of
 // exp(t - anchor_v) over the entries within 745 time units of the anchor.

@@ -192,29 +192,6 @@ __global__ void k_compact_batch(const i64* bs, const i64* bd, const i64* bt, u64
 
 // ---- streaming route ---------------------------------------------------------------
 
-// old nodes referenced by a surviving edge (check-before-write: hub slots are
-// hammered by many edges; a plain store from each would serialise in L2)
-// 4 survivors per thread per iteration: the id loads are independent, so a
-// thread keeps 8 alive-flag probes in flight instead of 2
-__global__ void k_flag_survivor_nodes(const u32* e_src, const u32* e_dst, u64 from, u64 m, u8* alive) {
-  const u64 n = m - from;
-  const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
-  for (u64 k = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; k < (n + 3) / 4; k += stride) {
-    u32 ids[8];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const u64 i = from + 4 * k + j;
-      ids[2 * j] = i < m ? e_src[i] : 0xffffffffu;
-      ids[2 * j + 1] = i < m ? e_dst[i] : 0xffffffffu;
-    }
-    u8 seen[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) seen[j] = ids[j] != 0xffffffffu ? alive[ids[j]] : 1;
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (!seen[j]) alive[ids[j]] = 1;
-  }
-}
 
 // old node v is an endpoint of a surviving edge iff its newest incident
 // edge is not evicted (all of v's edges are in the old window)
@@ -443,9 +420,7 @@ struct XScatter {
 // passes), one scan gives the new regions, survivors are written straight to
 // their final slots (no compaction scan, no merge), batch entries are placed
 // with per-node cursors and each node's (short) batch segment is re-sorted by
-// position. Falls back to the sort + merge route when a node receives more
-// than kYSegMax batch entries.
-constexpr u32 kYSegMax = 32;
+// position (a stable radix sort of the batch's entries by owner).
 
 __device__ __forceinline__ u32 owner_of_side(int mode, u32 s, u32 d, int side) {
   if (mode == TWG_UNDIRECTED) return side ? d : s;
@@ -493,11 +468,6 @@ __global__ void k_region_sizes(const uint2* old_meta, const u32* evicted, const 
   }
 }
 
-__global__ void k_cursor_init(const u32* new_off, const u32* xcnt, u64 V, u32* cursor) {
-  for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < V;
-       v += static_cast<u64>(gridDim.x) * blockDim.x)
-    cursor[v] = new_off[v] + xcnt[v];
-}
 
 struct SizeFn {
   const u32* x;
@@ -505,14 +475,6 @@ struct SizeFn {
   __device__ __forceinline__ u32 operator()(u64 v) const { return x[v] + y[v]; }
 };
 
-__global__ void k_max_u32(const u32* a, u64 n, u64* out) {
-  u32 m = 0;
-  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<u64>(gridDim.x) * blockDim.x)
-    m = max(m, a[i]);
-  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0 && m) atomicMax(reinterpret_cast<unsigned long long*>(out), static_cast<u64>(m));
-}
 
 // survivors straight to their final slots: slot = new_off[v'] + (p - first surviving entry of v)
 __global__ void k_place_x(const Entry* ent, const u32* owner, u64 Po, u32 from, const uint2* old_meta,
@@ -533,52 +495,7 @@ __global__ void k_place_x(const Entry* ent, const u32* owner, u64 Po, u32 from, 
   }
 }
 
-// batch entries via per-node cursors (order fixed up by k_sort_y_segments)
-__global__ void k_place_y(const u32* s, const u32* d, const i64* t, u64 A, u64 S, int mode, u32* cursor, Entry* out_ent,
-                          u32* out_owner) {
-  const int sides = mode == TWG_UNDIRECTED ? 2 : 1;
-  const u64 n = A * sides;
-  for (u64 j = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; j < n;
-       j += static_cast<u64>(gridDim.x) * blockDim.x) {
-    const u64 k = sides == 2 ? (j >> 1) : j;
-    const int side = sides == 2 ? static_cast<int>(j & 1) : 0;
-    const u32 o = owner_of_side(mode, s[k], d[k], side);
-    u32 nbr;
-    if (mode == TWG_FORWARD) nbr = d[k];
-    else if (mode == TWG_BACKWARD) nbr = s[k];
-    else nbr = side ? s[k] : d[k];
-    const u32 slot = atomicAdd(cursor + o, 1u);
-    Entry x;
-    x.nbr = nbr;
-    x.edge = static_cast<u32>(S + k);
-    x.t = t[k];
-    out_ent[slot] = x;
-    out_owner[slot] = o;
-  }
-}
 
-// each node's batch segment [new_off + xcnt, new_off + xcnt + ycnt) sorted by
-// (position, side) — the reference's entry order (edge_store.cpp:196-210)
-__global__ void k_sort_y_segments(const u32* new_off, const u32* xcnt, const u32* ycnt, u64 V, Entry* ent) {
-  for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < V;
-       v += static_cast<u64>(gridDim.x) * blockDim.x) {
-    const u32 len = ycnt[v];
-    if (len < 2) continue;
-    Entry* seg = ent + new_off[v] + xcnt[v];
-    Entry buf[kYSegMax];
-    for (u32 i = 0; i < len; ++i) {
-      Entry x = seg[i];
-      u32 j = i;
-      // undirected self-loops give two identical entries: any order is equal content
-      while (j > 0 && buf[j - 1].edge > x.edge) {
-        buf[j] = buf[j - 1];
-        --j;
-      }
-      buf[j] = x;
-    }
-    for (u32 i = 0; i < len; ++i) seg[i] = buf[i];
-  }
-}
 
 struct BatchRec;
 __global__ void k_place_y_sorted(const u32* owners, const u32* jidx, u64 Yn, int mode, const BatchRec* rec,
@@ -662,22 +579,6 @@ __global__ void k_make_y_rec(const u32* owners, const u32* jidx, u64 P, int mode
   }
 }
 
-__global__ void k_make_x(const Entry* ent, const u32* owner, u64 P, u32 from, const u32* xpos, const u32* o2n,
-                         const u32* spos, const u32* bpos, u64 A, u64 S, u64* xkey, u32* xnbr, i64* xt) {
-  const u64 i0 = A ? bpos[0] : S;
-  for (u64 p = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; p < P;
-       p += static_cast<u64>(gridDim.x) * blockDim.x) {
-    const Entry e = ent[p];
-    if (e.edge >= from) {
-      const u32 k = xpos[p];
-      const u32 i = e.edge - from;
-      const u32 np = i < i0 ? i : spos[i];
-      xkey[k] = (static_cast<u64>(o2n[owner[p]]) << 32) | np;
-      xnbr[k] = o2n[e.nbr];
-      xt[k] = e.t;
-    }
-  }
-}
 
 // batch entries in canonical order: j -> owner (edge_store.cpp:120-124)
 __global__ void k_batch_owner_keys(const u32* s, const u32* d, u64 A, int mode, u32* keys, u32* vals) {
@@ -693,22 +594,6 @@ __global__ void k_batch_owner_keys(const u32* s, const u32* d, u64 A, int mode, 
   }
 }
 
-__global__ void k_make_y(const u32* owners, const u32* jidx, u64 P, int mode, const u32* s, const u32* d,
-                         const i64* t, const u32* bpos, u64* ykey, u32* ynbr, i64* yt) {
-  for (u64 q = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; q < P;
-       q += static_cast<u64>(gridDim.x) * blockDim.x) {
-    const u32 j = jidx[q];
-    const u32 k = mode == TWG_UNDIRECTED ? (j >> 1) : j;
-    const u32 o = owners[q];
-    u32 nbr;
-    if (mode == TWG_FORWARD) nbr = d[k];
-    else if (mode == TWG_BACKWARD) nbr = s[k];
-    else nbr = (j & 1) ? s[k] : d[k];
-    ykey[q] = (static_cast<u64>(o) << 32) | bpos[k];
-    ynbr[q] = nbr;
-    yt[q] = t[k];
-  }
-}
 
 struct U64Key {
   const u64* k;
@@ -732,13 +617,6 @@ struct EntryEmit {
   }
 };
 
-u64 read_u32_total(Ctx& ctx, const u32* p) {
-  u64 v[1];
-  TWG_CUDA(cudaMemsetAsync(ctx.d_scalars + 8, 0, 8, ctx.stream));
-  TWG_CUDA(cudaMemcpyAsync(ctx.d_scalars + 8, p, 4, cudaMemcpyDeviceToDevice, ctx.stream));
-  read_scalars(ctx, ctx.d_scalars + 8, v, 1);
-  return v[0];
-}
 
 // The streaming rebuild (file header, steps 1-4). `pos` = admitted-batch
 // compaction offsets. Returns the new snapshot.
