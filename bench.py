@@ -316,6 +316,12 @@ def run_ours(args, rank, world, local_rank):
     # kernel alone on the GPU); --pipelined adds an overlapped headline pass
     seq = timed_pass(False, b)
     b += args.steps
+    # causality audit (GPU, validity.cpp:108-120 semantics) of one full walk
+    # generation on the current snapshot, outside the timed region
+    snap = window.snapshot()
+    ws = tw.generate_walks(snap, walk_cfg(), variant=variant)
+    audit, _ = ws.audit(snap)
+    del ws, snap
     head = timed_pass(True, b) if args.pipelined else seq
     total_ms, launches, clk = head["total_ms"], head["launches"], head["clocks"]
     hops, alg_bytes, ingest_alg = head["hops"], seq["alg_bytes"], seq["ingest_alg"]
@@ -349,7 +355,8 @@ def run_ours(args, rank, world, local_rank):
     result = dict(total_ms=total_ms, ingest_ms=ingest_ms, walk_ms=walk_ms, hops=hops_all, edges=edges_all,
                   launches=launches, clocks=clk, alg_bytes=allsum(alg_bytes), ingest_alg=ingest_alg,
                   append_alg=append_alg,
-                  seq_total_ms=allmax(seq_total_ms), seq_hops=allsum(seq_hops), pipelined=bool(args.pipelined))
+                  seq_total_ms=allmax(seq_total_ms), seq_hops=allsum(seq_hops), pipelined=bool(args.pipelined),
+                  audit=audit)
 
     # ---- e2e pass through the C ABI with host buffers -----------------------------------
     e2e = None
@@ -737,6 +744,8 @@ def main():
             "config": {**wl.describe(args.scale), "variant": args.variant, "parallelism": f"replicas{world}+walk-shards",
                        "global_walks_per_batch": wl.walks * world},
             "pipelined": res["pipelined"],
+            "causality_audit": {**res["audit"], "scope": "one full walk generation on the steady-state window, "
+                                                         "GPU auditor (twg_walkset_audit, EdgeOracle semantics)"},
             "phases": {"source": "sequential pass (ingest then walks per batch, one stream, device events)",
                        "ms_per_step": res["seq_total_ms"] / args.steps,
                        "ingest_ms_per_step": res["ingest_ms"] / args.steps,

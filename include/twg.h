@@ -253,6 +253,18 @@ int twg_walkset_wait(twg_walkset* w);
 int twg_walkset_device(twg_walkset* w, int64_t** d_nodes, int64_t** d_times,
                        uint32_t** d_lengths);
 
+/* Causality audit on the device: timewalk::check_walkset (validity.cpp:108-120,
+ * check_timed_walk :32-66) of every emitted walk (length >= 2) of w against
+ * the edges of s, independent of the node view (a (source, target, time)-
+ * sorted copy of the edge list, as EdgeOracle, :14-30). direction: 0 forward,
+ * 1 backward; strict: strict time order. first_violation (optional, host,
+ * walk_count entries): each walk's first invalid hop, or -1. */
+typedef struct twg_audit_report {
+  uint64_t walks, valid_walks, hops, valid_hops;
+} twg_audit_report;
+int twg_walkset_audit(twg_walkset* w, twg_store* s, int direction, int strict, int64_t* first_violation,
+                      twg_audit_report* out);
+
 /* sample_start_edge over the store for n (u1, u2) pairs -> time-sorted edge index */
 int twg_sample_start_edges(twg_store* s, int bias, const double* u1, const double* u2, uint64_t n,
                            uint64_t* out);

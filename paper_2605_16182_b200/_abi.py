@@ -32,6 +32,11 @@ class twg_store_info(C.Structure):
     ]
 
 
+class twg_audit_report(C.Structure):
+    _fields_ = [("walks", C.c_uint64), ("valid_walks", C.c_uint64), ("hops", C.c_uint64),
+                ("valid_hops", C.c_uint64)]
+
+
 class twg_batch_stats(C.Structure):
     _fields_ = [
         ("ingested", C.c_uint64), ("dropped_late", C.c_uint64), ("evicted", C.c_uint64),
@@ -106,6 +111,7 @@ SIGNATURES = {
     "twg_walkset_info": (I, [VP, C.POINTER(C.c_uint32), C.POINTER(U64), C.POINTER(U64), C.POINTER(U64)]),
     "twg_walkset_download": (I, [VP, VP, VP, VP]),
     "twg_walkset_download_compact": (I, [VP, VP, VP, VP]),
+    "twg_walkset_audit": (I, [VP, VP, I, I, VP, VP]),
     "twg_walkset_device": (I, [VP, PP, PP, PP]),
     "twg_sample_start_edges": (I, [VP, I, VP, VP, U64, VP]),
     "twg_schedule_step": (I, [VP, VP, VP, U64, VP, VP, VP, U64, VP]),

@@ -568,6 +568,22 @@ int twg_walkset_download(twg_walkset* w, int64_t* nodes, int64_t* times, uint32_
   });
 }
 
+int twg_walkset_audit(twg_walkset* w, twg_store* s, int direction, int strict, int64_t* first_violation,
+                      twg_audit_report* out) {
+  return guarded([&] {
+    WalkSetDev& x = *w->w;
+    Ctx& c = *x.ctx;
+    require(direction == 0 || direction == 1, "twg_walkset_audit: direction");
+    DevBuf<i64> first;
+    if (first_violation) first.alloc(x.count ? x.count : 1, c.stream);
+    u64 r[4];
+    audit_walks(c, x, *s->s, direction, strict != 0, first_violation ? first.p : nullptr, r);
+    if (first_violation && x.count) d2h(c, first_violation, first.p, x.count);
+    sync(c);
+    if (out) *out = twg_audit_report{r[0], r[1], r[2], r[3]};
+  });
+}
+
 int twg_walkset_download_compact(twg_walkset* w, uint64_t* offsets, int64_t* nodes, int64_t* times) {
   return guarded([&] {
     WalkSetDev& x = *w->w;

@@ -76,6 +76,12 @@ void exclusive_scan_dev(Ctx& ctx, const u64* in, u64* out, u64 n);
 u64 run_length_encode_dev(Ctx& ctx, const u64* keys, u64 n, u64* rows);
 u64 partition_flagged_dev(Ctx& ctx, const u32* items, u64 n, const u8* flags, u32* out);
 
+// check_walkset (validity.cpp:108-120) on the device: report = {walks,
+// valid walks, hops, valid hops}; d_first (optional, count entries) gets each
+// walk's first invalid hop or -1
+void audit_walks(Ctx& ctx, const WalkSetDev& w, const Store& s, int direction, bool strict, i64* d_first,
+                 u64 report[4]);
+
 // batched queries on a store
 void neighborhood_batch(Ctx& ctx, Store& s, const i64* d_v, const i64* d_t, u64 n, int dir, u64* d_out3);
 void find_nodes_batch(Ctx& ctx, Store& s, const i64* d_v, u64 n, u32* d_internal, u8* d_found);

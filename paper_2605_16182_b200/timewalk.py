@@ -580,6 +580,17 @@ class WalkSet:
         except Exception:
             pass
 
+    def audit(self, store: "EdgeStore", direction: WalkDirection = WalkDirection.Forward, strict: bool = True,
+              first_violation: bool = False):
+        """Causality audit on the GPU (validity.cpp:108-120 check_walkset):
+        returns (report dict, per-walk first invalid hop or -1 | None)."""
+        rep = _abi.twg_audit_report()
+        fv = np.zeros(max(self.walk_count, 1), np.int64) if first_violation else None
+        _call("twg_walkset_audit", self.handle, store.handle, int(direction), int(strict),
+              _ptr(fv) if fv is not None else None, C.byref(rep))
+        out = {"walks": rep.walks, "valid_walks": rep.valid_walks, "hops": rep.hops, "valid_hops": rep.valid_hops}
+        return out, (fv[: self.walk_count] if fv is not None else None)
+
     def _download(self):
         if self._nodes is None:
             cells = self.walk_count * self.stride
