@@ -34,7 +34,7 @@ namespace {
 constexpr int kBlock = 256;
 constexpr int kPB = 256;           // nodes per bucket = threads per placement CTA
 constexpr u32 kBucketShift = 8;
-constexpr int kChunk = 1024;       // bucket entries staged per placement round
+constexpr int kChunk = 2048;       // bucket entries staged per placement round
 constexpr int kChunkItems = kChunk / kPB;
 static_assert(kPB == 1 << kBucketShift, "one thread per bucket node");
 
@@ -476,10 +476,17 @@ __global__ void __launch_bounds__(kPB) k_bucket_place(PlaceArgs a) {
     }
     __syncthreads();
     if (warp == 0) {  // exclusive scan of the kChunkItems x 8 counts in item order
-      const u32 c = lane < kChunkItems * (kPB / 32) ? (&sm.rwcnt[0][0])[lane] : 0u;
-      const u32 incl = warp_incl_scan(c);
-      if (lane < kChunkItems * (kPB / 32)) (&sm.rwcnt[0][0])[lane] = incl - c;
-      if (lane == 31) sm.mtotal = incl;
+      constexpr int kCounts = kChunkItems * (kPB / 32);
+      u32 carry = 0;
+#pragma unroll
+      for (int base = 0; base < kCounts; base += 32) {
+        const int i = base + lane;
+        const u32 c = i < kCounts ? (&sm.rwcnt[0][0])[i] : 0u;
+        const u32 incl = warp_incl_scan(c);
+        if (i < kCounts) (&sm.rwcnt[0][0])[i] = carry + incl - c;
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      if (lane == 0) sm.mtotal = carry;
     }
     __syncthreads();
 #pragma unroll
