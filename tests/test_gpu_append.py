@@ -154,3 +154,35 @@ def test_append_node_leaves_window(tw, co, mode):
         counts.append(w.snapshot().node_count())
         assert_store(w.snapshot(), ed)
     assert counts[0] == 100 and counts[-1] == 99
+
+
+def test_c5_law_stream_small_scale(tw, co):
+    """The bench's own pipeline at 1/1000 scale: the C5 stream law generated
+    on the device (twg_synth_stream_device), ingested batch by batch through
+    the device-resident fast route, every snapshot compared with the oracle's
+    window over the same (host-generated) stream, and exp-index walks on the
+    last one compared with the oracle's."""
+    import torch
+    from bench import Workload
+    from oracle.py import Cfg
+    wl = Workload(0.001)
+    B, lib = wl.batch_edges, tw._abi.load()
+    ctx = tw.Context(0)
+    w = tw.WindowManager(wl.window, weights=False, adjacency=False, ctx=ctx)
+    dev = [torch.empty(B, dtype=torch.int64, device="cuda") for _ in range(3)]
+    batches = [co.gen_stream(wl.nodes, b * B, B, wl.seed) for b in range(wl.prefill + 5)]
+    exp_stats, exp_dumps = co.window_run(batches, wl.window, 0, every=True)
+    streaming = 0
+    for b, ed in enumerate(exp_dumps):
+        assert lib.twg_synth_stream_device(ctx.handle, wl.nodes, b * B, B, wl.seed, dev[0].data_ptr(),
+                                           dev[1].data_ptr(), dev[2].data_ptr()) == 0
+        w.ingest_batch_device(dev[0].data_ptr(), dev[1].data_ptr(), dev[2].data_ptr(), B, stats=False)
+        snap = w.snapshot()
+        streaming += snap.is_streaming()
+        assert_store(snap, ed, keys=["src_ext", "dst_ext", "t", "ts_off", "ts_time", "n_off", "n_tsidx", "mk_time",
+                                     "mk_start", "ref_edge", "ref_nbr", "ext"])
+    assert streaming >= 3
+    edges = np.stack([exp_dumps[-1]["src_ext"], exp_dumps[-1]["dst_ext"], exp_dumps[-1]["t"]], 1)
+    c = Cfg(walk_length=wl.walk_length, start_mode=1, total_walks=5000, bias=2, start_bias=0, seed=wl.seed)
+    exp, _ = co.generate(edges, 0, c)
+    assert_walks(tw.generate_walks(w.snapshot(), to_cfg(tw, c), variant=tw.Variant.FullWalk), exp)
