@@ -325,9 +325,43 @@ void read_scalars(Ctx& ctx, const u64* d_src, u64* host_dst, int n) {
   for (int i = 0; i < n; ++i) host_dst[i] = reinterpret_cast<volatile u64*>(ctx.h_pinned)[i];
 }
 
+// streaming stores: ts_w[g] = sum_{h<=g} exp(t_h - t_last) is +0 before the
+// first group within 745 time units of t_last; only that tail (<= 746 values)
+// is materialised. The per-node prefixes are evaluated by the walk kernels
+// from the node's tail entries (walk.cu draw_weighted_ring), exactly.
+__global__ void k_ts_wtail(StoreView s, const double* exp_neg, double* tail, u64* t0) {
+  if (threadIdx.x != 0 || s.Z == 0) return;
+  const i64 anchor = s.ts_time[s.zrg(static_cast<u32>(s.Z - 1))];
+  u64 lo = 0, hi = s.Z;  // first group with time >= anchor - 745
+  while (lo < hi) {
+    const u64 mid = (lo + hi) >> 1;
+    if (s.ts_time[s.zrg(static_cast<u32>(mid))] < anchor - (kExpTableSize - 1)) lo = mid + 1;
+    else hi = mid;
+  }
+  *t0 = lo;
+  double acc = 0.0;
+  for (u64 g = lo; g < s.Z; ++g) {
+    acc = __dadd_rn(acc, exp_neg[anchor - s.ts_time[s.zrg(static_cast<u32>(g))]]);
+    tail[g - lo] = acc;
+  }
+}
+
 void ensure_weights(Ctx& ctx, Store& s) {
   if (s.has_weights) return;
-  if (s.gapped) fail(TWG_ELOGIC, "ensure_weights: streaming store (use ensure_compact)");
+  if (s.gapped) {
+    cudaStream_t st = ctx.stream;
+    s.ts_wtail.alloc(kExpTableSize + 1, st);
+    TWG_CUDA(cudaMemsetAsync(ctx.d_scalars + 20, 0, sizeof(u64), st));
+    if (s.Z) {
+      k_ts_wtail<<<1, 32, 0, st>>>(s.view(), ctx.d_exp_neg, s.ts_wtail.p, ctx.d_scalars + 20);
+      TWG_LAUNCHED(ctx);
+    }
+    u64 t0[1];
+    read_scalars(ctx, ctx.d_scalars + 20, t0, 1);
+    s.ts_wt0 = t0[0];
+    s.has_weights = true;
+    return;
+  }
   cudaStream_t st = ctx.stream;
   s.ts_w.alloc(s.Z ? s.Z : 1, st);
   TWG_CUDA(cudaMemsetAsync(s.ts_w.p, 0, s.ts_w.bytes(), st));

@@ -93,6 +93,10 @@ struct StoreView {
   u32 seq0;
   Ring erg;  // snapshot edge i -> slot erg(i) of e_src/e_dst/e_t (identity in contiguous stores)
   Ring zrg;  // snapshot ts group g -> slot zrg(g) of ts_off/ts_time
+  // streaming stores (no ts_w): the nonzero tail of the ts weight prefix,
+  // ts_wtail[g - ts_wt0] for groups g >= ts_wt0 (every earlier value is +0)
+  const double* ts_wtail;
+  u64 ts_wt0;
 };
 
 // snapshot edge i
@@ -189,6 +193,8 @@ struct Store {
   u64 log_first = 0;  // logical log position of edge 0
   u64 ts_first = 0;   // logical log group position of group 0
   u32 e_cap = kIdentityCap, e_org = 0, z_cap = kIdentityCap, z_org = 0;  // StoreView::erg / zrg
+  DevBuf<double> ts_wtail;  // streaming stores: the nonzero tail of the ts weight prefix
+  u64 ts_wt0 = 0;
   // contiguous materialisation of a gapped store (reference layout), built on
   // first use by the accessors / downloads / weighted views (ensure_compact)
   mutable std::unique_ptr<Store> compact;
@@ -199,7 +205,7 @@ struct Store {
                      e_src.p,  e_dst.p,   e_t.p,     e_rec.p,    ext.p,     ts_off.p,  ts_time.p,
                      ts_w.p,   nmeta.p,   nm.p,      mk_time.p,  mk_start.p, ent.p,   wp.p,
                      adj_off.p, adj.p,  ext_identity ? 1 : 0, seq0,
-                     Ring{0u, e_cap, e_org}, Ring{0u, z_cap, z_org}};
+                     Ring{0u, e_cap, e_org}, Ring{0u, z_cap, z_org}, ts_wtail.p, ts_wt0};
   }
   u64 device_bytes() const {
     return e_src.bytes() + e_dst.bytes() + e_t.bytes() + e_rec.bytes() + ext.bytes() + ts_off.bytes() +

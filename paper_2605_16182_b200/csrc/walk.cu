@@ -135,14 +135,60 @@ __device__ u64 draw_weighted_local(const WalkParams& P, double u, u32 c, u32 e) 
   return e - 1 - c;
 }
 
+// walk_engine.cpp:49-63 through the node's ring (streaming stores)
+__device__ u64 draw_weighted_local_ring(const WalkParams& P, double u, Ring er, u32 c, u32 e) {
+  const i64 anchor = load_entry(P.s.ent + er(e - 1)).t;
+  double total = 0.0;
+  for (u32 x = c; x < e; ++x) total = __dadd_rn(total, exp_nonpos(P.s.ent[er(x)].t - anchor, P.exp_neg));
+  const double r = __dmul_rn(u, total);
+  double cum = 0.0;
+  for (u32 x = c; x < e; ++x) {
+    cum = __dadd_rn(cum, exp_nonpos(P.s.ent[er(x)].t - anchor, P.exp_neg));
+    if (r < cum) return x - c;
+  }
+  return e - 1 - c;
+}
+
+// ExponentialWeight draw on a streaming store, without a materialised
+// node_weight_prefix_: the prefix of region [lo, hi) is anchored at its
+// newest time (edge_store.cpp:159, :208-209), so every value before the first
+// entry within 745 time units of the anchor is exactly +0 and the rest is a
+// serial sum over that tail — evaluated here in the reference's order, then
+// the reference's base / mass / lower_bound logic (walk_engine.cpp:73-80,
+// samplers.cpp:82-90). Bit-identical to the contiguous path.
+__device__ u64 draw_weighted_ring(const WalkParams& P, double u, Ring er, u32 lo, u32 hi, u32 c, u32 e) {
+  const i64 anchor = load_entry(P.s.ent + er(hi - 1)).t;
+  const i64 floor_t = anchor - (kExpTableSize - 1);
+  u32 ts = hi;  // tail [ts, hi)
+  while (ts > lo && P.s.ent[er(ts - 1)].t >= floor_t) --ts;
+  double acc = 0.0, base = 0.0;
+  for (u32 x = ts; x < e; ++x) {
+    acc = __dadd_rn(acc, exp_nonpos(P.s.ent[er(x)].t - anchor, P.exp_neg));
+    if (x + 1 == c) base = acc;
+  }
+  const double total = e > ts ? acc : 0.0;
+  const double mass = __dsub_rn(total, base);
+  if (!(mass > 0.0) || !isfinite(mass)) return draw_weighted_local_ring(P, u, er, c, e);
+  const double r = __dadd_rn(base, __dmul_rn(u, mass));
+  if (c < ts && 0.0 >= r) return 0;  // prefix[c] == +0 already reaches r
+  acc = 0.0;
+  for (u32 x = ts; x < e; ++x) {
+    acc = __dadd_rn(acc, exp_nonpos(P.s.ent[er(x)].t - anchor, P.exp_neg));
+    if (x >= c && acc >= r) return x - c;
+  }
+  return e - 1 - c;
+}
+
 // walk_engine.cpp:65-84
-__device__ __forceinline__ u64 draw_index(const WalkParams& P, double u, u32 lo, u32 c, u32 e, u32* amb) {
+__device__ __forceinline__ u64 draw_index(const WalkParams& P, double u, u32 lo, u32 c, u32 e, u32* amb, Ring er,
+                                          u32 hi) {
   const u64 n = e - c;
   switch (P.bias) {
     case TWG_UNIFORM: return pick_uniform(u, n);
     case TWG_LINEAR: return pick_linear(u, n);
     case TWG_EXPINDEX: return pick_exponential(u, n, P.expm1_tab, amb);
     default: {
+      if (!P.s.wp) return draw_weighted_ring(P, u, er, lo, hi, c, e);  // streaming store
       const double base = c > lo ? P.s.wp[c - 1] : 0.0;
       const double mass = __dsub_rn(P.s.wp[e - 1], base);
       if (!(mass > 0.0) || !isfinite(mass)) return draw_weighted_local(P, u, c, e);
@@ -212,7 +258,7 @@ __device__ __forceinline__ bool hop(const WalkParams& P, u64 wl, WalkReg& r, con
     idx = 0;
     for (u32 k = 0; k < kNode2VecMaxRetries; ++k) {
       const double u = P.rng.uniform(w, hop_index, 2ull * k);
-      idx = draw_index(P, u, lo, c, e, amb);
+      idx = draw_index(P, u, lo, c, e, amb, er, hi);
       const u32 cand = load_entry(P.s.ent + er(c + static_cast<u32>(idx))).nbr;
       const double ua = P.rng.uniform(w, hop_index, 2ull * k + 1);
       double beta;  // samplers.hpp:74-86
@@ -224,7 +270,7 @@ __device__ __forceinline__ bool hop(const WalkParams& P, u64 wl, WalkReg& r, con
     }
   } else {
     const double u = P.rng.uniform(w, hop_index, 0);
-    idx = draw_index(P, u, lo, c, e, amb);
+    idx = draw_index(P, u, lo, c, e, amb, er, hi);
   }
   const Entry x = load_entry(P.s.ent + er(c + static_cast<u32>(idx)));
   const u64 slot = out_index(P, wl, r.len);
@@ -249,7 +295,25 @@ __device__ __forceinline__ u64 sample_start_edge_dev(const StoreView& s, int bia
     case TWG_UNIFORM: g = pick_uniform(u1, Z); break;
     case TWG_LINEAR: g = pick_linear(u1, Z); break;
     case TWG_EXPINDEX: g = pick_exponential(u1, Z, expm1_tab, amb); break;
-    default: g = pick_weighted(u1, s.ts_w, Z); break;
+    default:
+      if (s.ts_w) {
+        g = pick_weighted(u1, s.ts_w, Z);
+      } else {  // streaming store: zeros then the materialised tail (samplers.cpp:74-80)
+        const u64 nt = Z - s.ts_wt0;
+        const double r = __dmul_rn(u1, s.ts_wtail[nt - 1]);
+        if (s.ts_wt0 > 0 && 0.0 >= r) {
+          g = 0;
+        } else {
+          u64 a = 0, b = nt;
+          while (a < b) {
+            const u64 mid = (a + b) >> 1;
+            if (s.ts_wtail[mid] < r) a = mid + 1;
+            else b = mid;
+          }
+          g = s.ts_wt0 + (a == nt ? nt - 1 : a);
+        }
+      }
+      break;
   }
   u64 lo, hi;
   ts_group_range(s, g, lo, hi);
@@ -653,13 +717,12 @@ __global__ void k_compact_walks(const i64* nodes, const i64* times, const u32* l
 
 unsigned grid(Ctx& ctx, u64 n) { return grid_for(n, kBlock, static_cast<unsigned>(ctx.sm_count) * 32); }
 
-// The store a walk runs on: streaming (gapped) stores serve the index and
-// exponential-index pickers directly; the weight prefixes and the node2vec
-// adjacency are defined over the contiguous layout, so those configurations
-// run on the store's contiguous form.
+// The store a walk runs on: streaming (gapped) stores serve every picker
+// directly (exp-weight prefixes evaluated on the fly, draw_weighted_ring);
+// the static node2vec adjacency is built over the contiguous layout, so that
+// configuration runs on the store's contiguous form.
 Store& walk_store(Ctx& ctx, Store& s, const twg_walk_config& cfg) {
-  const bool needs = cfg.bias == TWG_EXPWEIGHT || cfg.start_bias == TWG_EXPWEIGHT ||
-                     (cfg.node2vec && !cfg.temporal_adjacency);
+  const bool needs = cfg.node2vec && !cfg.temporal_adjacency;
   return s.gapped && needs ? ensure_compact(ctx, s) : s;
 }
 

@@ -183,6 +183,10 @@ def test_c5_law_stream_small_scale(tw, co):
                                      "mk_start", "ref_edge", "ref_nbr", "ext"])
     assert streaming >= 3
     edges = np.stack([exp_dumps[-1]["src_ext"], exp_dumps[-1]["dst_ext"], exp_dumps[-1]["t"]], 1)
-    c = Cfg(walk_length=wl.walk_length, start_mode=1, total_walks=5000, bias=2, start_bias=0, seed=wl.seed)
-    exp, _ = co.generate(edges, 0, c)
-    assert_walks(tw.generate_walks(w.snapshot(), to_cfg(tw, c), variant=tw.Variant.FullWalk), exp)
+    for bias, start_bias in ((2, 0), (3, 3), (3, 0)):  # exp-index; exp-weight (the reference default) both ways
+        c = Cfg(walk_length=wl.walk_length, start_mode=1, total_walks=5000, bias=bias, start_bias=start_bias,
+                seed=wl.seed)
+        exp, _ = co.generate(edges, 0, c)
+        snap = w.snapshot()
+        assert snap.is_streaming()
+        assert_walks(tw.generate_walks(snap, to_cfg(tw, c), variant=tw.Variant.FullWalk), exp)
