@@ -564,7 +564,7 @@ Store& ensure_compact(Ctx& ctx, const Store& g) {
 
 void ensure_adjacency(Ctx& ctx, Store& s) {
   if (s.has_adjacency) return;
-  if (s.gapped) fail(TWG_ELOGIC, "ensure_adjacency: streaming store (use ensure_compact)");
+  if (s.gapped) return;  // streaming stores answer adjacency from the node view (walk.cu adjacent)
   DevBuf<u32> owners(s.P ? s.P : 1, ctx.stream);
   if (s.P) {
     k_entry_owners<<<grid(ctx, s.V), kBlock, 0, ctx.stream>>>(s.nmeta.p, s.V, owners.p);

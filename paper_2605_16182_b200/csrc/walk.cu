@@ -199,6 +199,13 @@ __device__ __forceinline__ u64 draw_index(const WalkParams& P, double u, u32 lo,
 
 // edge_store.cpp:310-314
 __device__ __forceinline__ bool adjacent(const StoreView& s, u32 a, u32 b) {
+  if (!s.adj_off) {  // streaming store: b among the neighbours of a's live region (any time)
+    const NodeMeta na = s.nm[a];
+    const Ring er = entry_ring(na);
+    for (u32 x = na.eb; x < na.ee; ++x)
+      if (s.ent[er(x)].nbr == b) return true;
+    return false;
+  }
   u32 lo = s.adj_off[a], hi = s.adj_off[a + 1];
   const u32 end = hi;
   while (lo < hi) {
@@ -718,13 +725,9 @@ __global__ void k_compact_walks(const i64* nodes, const i64* times, const u32* l
 unsigned grid(Ctx& ctx, u64 n) { return grid_for(n, kBlock, static_cast<unsigned>(ctx.sm_count) * 32); }
 
 // The store a walk runs on: streaming (gapped) stores serve every picker
-// directly (exp-weight prefixes evaluated on the fly, draw_weighted_ring);
-// the static node2vec adjacency is built over the contiguous layout, so that
-// configuration runs on the store's contiguous form.
-Store& walk_store(Ctx& ctx, Store& s, const twg_walk_config& cfg) {
-  const bool needs = cfg.node2vec && !cfg.temporal_adjacency;
-  return s.gapped && needs ? ensure_compact(ctx, s) : s;
-}
+// directly (exp-weight prefixes evaluated on the fly, draw_weighted_ring;
+// the static node2vec adjacency by a scan of the previous node's region).
+Store& walk_store(Ctx&, Store& s, const twg_walk_config&) { return s; }
 
 WalkParams make_params(Ctx& ctx, Store& s, const twg_walk_config& cfg, u32 stride, u64 walk_begin, WalkSetDev& out,
                        bool slot_major = false, u64 count = 0) {
