@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(kBlock) k_plan(PlanArgs a) {
       fits = !a.relocate_all && static_cast<u64>(o.ee - low) + y <= o.cap;
       if (!fits) {
         const u32 need = (o.ee - eb) + y;
-        req = need + (a.relocate_all ? need / 2 : need) + 4;
+        req = 2 * need + 4;  // 2x slack: a typical ring absorbs ~10 batches before it moves
       }
       if (a.need_last && o.ee > eb) a.last_t[v] = a.oent[oer(o.ee - 1)].t;
     }
@@ -712,7 +712,7 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
   if (nrel == 0) {
     auto na = std::make_shared<NodeArena>();
     na->V = V;
-    na->cap = std::min<u64>(2 * s->P + 12 * V + 1024, 0xffffff00ull);  // >= 1.5 P + 4 V: the repack always fits
+    na->cap = std::min<u64>((5 * s->P) / 2 + 12 * V + 1024, 0xffffff00ull);  // >= 2 P + 4 V: the repack fits
     na->ent.alloc(na->cap, st);
     na->mk_time.alloc(na->cap, st);
     na->mk_start.alloc(na->cap, st);
@@ -731,6 +731,8 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
   }
   reloc.release();
   pt.mark(fresh ? "plan+repack" : "plan");
+  if (pt.on) std::fprintf(stderr, "[twg phases] relocated rings: %llu of %llu\n", static_cast<unsigned long long>(nrel),
+                          static_cast<unsigned long long>(V));
   static bool attr_set = false;
   if (!attr_set) {
     TWG_CUDA(cudaFuncSetAttribute(k_bucket_place, cudaFuncAttributeMaxDynamicSharedMemorySize,
