@@ -80,7 +80,7 @@ __device__ __forceinline__ Entry load_entry(const Entry* p) {
 // Binary search down to a window of kScan marks, then the window's times in
 // one round of independent loads (the window spans 2-3 sectors): a typical
 // node (G ~ 33) costs 3 dependent round trips instead of 6.
-constexpr u32 kScan = 8;
+constexpr u32 kScan = 4;
 __device__ __forceinline__ u32 ub_ring(const i64* a, Ring r, u32 lo, u32 hi, i64 x) {
   while (hi - lo > kScan) {
     const u32 mid = lo + ((hi - lo) >> 1);
