@@ -49,8 +49,21 @@ __global__ void k_init_scalars(u64* s) {
 // scal[7]: bit0 = batch not time-ordered, bit1 = some equal-time run > kSegMax
 constexpr int kSegMax = 32;
 
-// scal[8]: batch min t, scal[9]: some id negative
-__global__ void k_batch_stats(const i64* bs, const i64* bd, const i64* bt, u64 n, u64* scal) {
+// the fast append route's speculative work, prepared before the statistics pass
+struct FastSpec {
+  bool on = false, in_log = false;
+  Ring wring{0u, kIdentityCap, 0u};
+  DevBuf<EdgeRec> tmp;
+  EdgeRec* rec = nullptr;
+  u64 from = 0;
+};
+
+// scal[8]: batch min t, scal[9]: some id negative.
+// rec != null: speculatively also emit the canonical records of a
+// time-ordered batch (each edge ranked by (src, dst) inside its equal-time
+// run, runs scanned up to kSegMax each way) through the ring wr — used only
+// when the statistics admit the fast append route, ignored otherwise.
+__global__ void k_batch_stats(const i64* bs, const i64* bd, const i64* bt, u64 n, u64* scal, EdgeRec* rec, Ring wr) {
   i64 mt = kTimeUnset, lt = kTimeInfinite;
   u64 mid = 0;
   u32 shape = 0, neg = 0;
@@ -64,6 +77,18 @@ __global__ void k_batch_stats(const i64* bs, const i64* bd, const i64* bt, u64 n
     if (a < 0 || b < 0) neg = 1;
     if (i + 1 < n && t > bt[i + 1]) shape |= 1u;
     if (i + kSegMax < n && t == bt[i + kSegMax]) shape |= 2u;
+    if (rec) {
+      u64 lo = i, hi = i + 1;
+      while (lo > 0 && i - lo < kSegMax && bt[lo - 1] == t) --lo;
+      while (hi < n && hi - i < kSegMax && bt[hi] == t) ++hi;
+      const u64 key = (static_cast<u64>(a) << 32) | static_cast<u64>(b);
+      u32 rank = 0;
+      for (u64 q = lo; q < hi; ++q) {
+        const u64 kq = (static_cast<u64>(bs[q]) << 32) | static_cast<u64>(bd[q]);
+        rank += (kq < key || (kq == key && q < i)) ? 1u : 0u;
+      }
+      rec[wr(static_cast<u32>(lo + rank))] = EdgeRec{static_cast<u32>(a), static_cast<u32>(b), t};
+    }
   }
   for (int o = 16; o > 0; o >>= 1) {
     mt = max(mt, __shfl_xor_sync(0xffffffffu, mt, o));
@@ -79,6 +104,20 @@ __global__ void k_batch_stats(const i64* bs, const i64* bd, const i64* bt, u64 n
     if (shape) atomicOr(reinterpret_cast<unsigned long long*>(&scal[7]), static_cast<u64>(shape));
     if (neg) atomicOr(reinterpret_cast<unsigned long long*>(&scal[9]), 1ull);
   }
+}
+
+// lower_bound of the cutoff implied by the batch maximum (scal[0]) over a snapshot's edges
+__global__ void k_lower_bound_cut(StoreView s, i64 t_high, i64 duration, const u64* scal, u64* out) {
+  const i64 bh = static_cast<i64>(scal[0]);
+  const i64 high = t_high > bh ? t_high : bh;
+  const i64 cutoff = high > duration ? high - duration : 0;
+  u64 lo = 0, hi = s.m;
+  while (lo < hi) {
+    const u64 mid = (lo + hi) >> 1;
+    if (edge_time(s, mid) < cutoff) lo = mid + 1;
+    else hi = mid;
+  }
+  *out = lo;
 }
 
 // Canonical order of a time-ordered batch whose equal-time runs are short
@@ -108,32 +147,7 @@ __global__ void k_segment_sort(const u32* s, const u32* d, const i64* t, u64 A, 
   }
 }
 
-// Fast append route, batch side in one pass: a time-ordered batch over the
-// existing population 0..V-1 (internal id == external id): canonical order
-// by sorting each short equal-time run by (src, dst) in registers (one
-// thread per run), written as log records through the ring.
-template <bool kTimeOrdered>
-__device__ __forceinline__ void agg_max(i64* last, u32 key, i64 t, bool valid);
 
-__global__ void k_batch_fast(const i64* bs, const i64* bd, const i64* bt, u64 n, EdgeRec* rec, Ring orr) {
-  // one thread per edge: its rank by (src, dst) inside its equal-time run
-  // (runs are <= kSegMax long: the batch shape check), neighbours from L1
-  for (u64 k = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; k < n;
-       k += static_cast<u64>(gridDim.x) * blockDim.x) {
-    const i64 tk = bt[k];
-    u64 lo = k, hi = k + 1;
-    while (lo > 0 && bt[lo - 1] == tk) --lo;
-    while (hi < n && bt[hi] == tk) ++hi;
-    const u64 sk = static_cast<u64>(bs[k]), dk = static_cast<u64>(bd[k]);
-    const u64 key = (sk << 32) | dk;
-    u32 rank = 0;
-    for (u64 q = lo; q < hi; ++q) {
-      const u64 kq = (static_cast<u64>(bs[q]) << 32) | static_cast<u64>(bd[q]);
-      rank += (kq < key || (kq == key && q < k)) ? 1u : 0u;  // equal keys: content-equal, any stable order
-    }
-    rec[orr(static_cast<u32>(lo + rank))] = EdgeRec{static_cast<u32>(sk), static_cast<u32>(dk), tk};
-  }
-}
 
 __global__ void k_pack_rec(const u32* s, const u32* d, const i64* t, u64 n, EdgeRec* out) {
   for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
@@ -891,17 +905,13 @@ Store* ingest_streaming(Window& w, const i64* bs, const i64* bd, const i64* bt, 
 // population 0..V-1 (internal == external), and no old node leaving the
 // window (checked on the device after the newest-time update; otherwise the
 // general route runs from scratch and the speculative work is discarded).
-Store* ingest_fast(Window& w, const i64* bs, const i64* bd, const i64* bt, u64 n, const u64* sc, i64 cutoff,
-                   twg_batch_stats* stats) {
+Store* ingest_fast(Window& w, FastSpec& spec, u64 n, const u64* sc, i64 cutoff, twg_batch_stats* stats) {
   Ctx& ctx = *w.ctx;
   cudaStream_t st = ctx.stream;
   const Store& O = *w.store;
   const i64 batch_min = static_cast<i64>(sc[8]);
   const u32 shape = static_cast<u32>(sc[7]);
-  if (!append_ingest_enabled() || O.m == 0 || O.V == 0 || !O.ext_identity || shape != 0 || sc[9] ||
-      batch_min < cutoff || batch_min <= w.t_high || sc[1] >= O.V || n >= 0xffffffffull / 2)
-    return nullptr;
-  PhaseTimer pt(ctx, "ingest_fast");
+  if (!spec.on || shape != 0 || sc[9] || batch_min < cutoff || batch_min <= w.t_high || sc[1] >= O.V) return nullptr;
   const u64 V = O.V;
   auto s = std::make_unique<Store>();
   s->ctx = &ctx;
@@ -918,31 +928,12 @@ Store* ingest_fast(Window& w, const i64* bs, const i64* bd, const i64* bt, u64 n
   s->last_t.alloc(V, st);
   TWG_CUDA(cudaMemcpyAsync(s->last_t.p, O.last_t.p, V * sizeof(i64), cudaMemcpyDeviceToDevice, st));
   s->last_t_exact = w.mode == TWG_UNDIRECTED && O.last_t_exact;
-  // the canonical batch goes straight into the shared log when it has room
-  Ring wring{0u, kIdentityCap, 0u};
-  const bool in_log = append_log_slot(O, w.previous, n, &wring);
-  DevBuf<EdgeRec> tmp;
-  EdgeRec* rec;
-  if (in_log) {
-    rec = O.log->rec.p;
-  } else {
-    tmp.alloc(n, st);
-    rec = tmp.p;
-  }
-  TWG_CUDA(cudaMemsetAsync(ctx.d_scalars + 12, 0, 16, st));
-  k_lower_bound<<<1, 1, 0, st>>>(O.view(), cutoff, ctx.d_scalars + 12);
-  TWG_LAUNCHED(ctx);
-  k_batch_fast<<<grid(ctx, n), kBlock, 0, st>>>(bs, bd, bt, n, rec, wring);
-  TWG_LAUNCHED(ctx);
-  u64 r[1];
-  read_scalars(ctx, ctx.d_scalars + 12, r, 1);
-  pt.mark("batch_fast");
-  const u64 from = r[0];
+  const u64 from = spec.from;
   s->m = O.m - from + n;
   stats->evicted = from;
   stats->dropped_late = 0;
   w.max_ext = static_cast<i64>(V - 1);
-  Store* out = ingest_append(w, O, std::move(s), rec, wring, n, from, cutoff, true, in_log, true);
+  Store* out = ingest_append(w, O, std::move(s), spec.rec, spec.wring, n, from, cutoff, true, spec.in_log, true);
   if (!out) {  // an old node leaves the window: the general route recomputes everything
     stats->evicted = stats->dropped_late = 0;
     return nullptr;
@@ -999,16 +990,37 @@ void window_ingest(Window& w, const i64* d_src, const i64* d_dst, const i64* d_t
   // batch_high, new_high, cutoff (window_manager.cpp:30-33)
   k_init_scalars<<<1, 1, 0, st>>>(ctx.d_scalars);
   TWG_LAUNCHED(ctx);
-  k_batch_stats<<<grid(ctx, n), kBlock, 0, st>>>(d_src, d_dst, d_t, n, ctx.d_scalars);
+  // Fast-route speculation: over a dense population 0..V-1 the statistics
+  // pass also writes the canonical records (into the log ring when it has
+  // room) and the survivor bound is found on the device — one read-back
+  // decides, nothing is published if the route does not apply.
+  FastSpec spec;
+  spec.on = append_ingest_enabled() && old.m > 0 && old.V > 0 && old.ext_identity && n < 0xffffffffull / 2;
+  if (spec.on) {
+    spec.in_log = append_log_slot(old, w.previous, n, &spec.wring);
+    if (!spec.in_log) {
+      spec.tmp.alloc(n, st);
+      spec.rec = spec.tmp.p;
+    } else {
+      spec.rec = old.log->rec.p;
+    }
+    TWG_CUDA(cudaMemsetAsync(ctx.d_scalars + 12, 0, 8, st));
+  }
+  k_batch_stats<<<grid(ctx, n), kBlock, 0, st>>>(d_src, d_dst, d_t, n, ctx.d_scalars, spec.rec, spec.wring);
   TWG_LAUNCHED(ctx);
-  u64 sc[10];
-  read_scalars(ctx, ctx.d_scalars, sc, 10);
+  if (spec.on) {
+    k_lower_bound_cut<<<1, 1, 0, st>>>(old.view(), w.t_high, w.duration, ctx.d_scalars, ctx.d_scalars + 12);
+    TWG_LAUNCHED(ctx);
+  }
+  u64 sc[13];
+  read_scalars(ctx, ctx.d_scalars, sc, 13);
+  spec.from = sc[12];
   const i64 batch_high = static_cast<i64>(sc[0]);
   const u64 batch_max_id = sc[1];
   w.batch_shape = static_cast<u32>(sc[7]);
   const i64 new_high = w.t_high > batch_high ? w.t_high : batch_high;
   const i64 cutoff = w.cutoff_for(new_high);
-  if (Store* fast = ingest_fast(w, d_src, d_dst, d_t, n, sc, cutoff, &stats)) {
+  if (Store* fast = ingest_fast(w, spec, n, sc, cutoff, &stats)) {
     stats.retained = fast->m;
     stats.peak_bytes = old.device_bytes() + fast->device_bytes();
     TWG_CUDA(cudaStreamSynchronize(st));
