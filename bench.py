@@ -171,6 +171,22 @@ def run_ours(args, rank, world, local_rank):
             with torch.cuda.stream(stream):
                 broadcast_batch(buf, src=0)
 
+    side = torch.cuda.Stream(device=f"cuda:{local_rank}") if world > 1 else None
+
+    def bcast_async(buf):
+        # the next batch's NCCL broadcast is issued from an idle side stream, so
+        # it runs over NVLink while the current batch is ingested and walked
+        if world == 1:
+            return None
+        with torch.cuda.stream(side):
+            return [dist.broadcast(x, src=0, async_op=True) for x in buf]
+
+    def bcast_wait(works):
+        if works:
+            with torch.cuda.stream(stream):  # the compute stream waits for the replica's data
+                for wk in works:
+                    wk.wait()
+
     def new_buf():
         return [torch.empty(B, dtype=torch.int64, device=f"cuda:{local_rank}") for _ in range(3)]
 
@@ -222,8 +238,10 @@ def run_ours(args, rank, world, local_rank):
         if not pipelined:
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(3 * args.steps + 2)]
             ev[0].record(stream)
+            pending = bcast_async(bufs[0])
             for k in range(args.steps):
-                bcast(bufs[k])
+                bcast_wait(pending)
+                pending = bcast_async(bufs[k + 1]) if k + 1 < args.steps else None
                 ev[1 + 3 * k].record(stream)
                 bst = window.ingest_batch_device(bufs[k][0].data_ptr(), bufs[k][1].data_ptr(),
                                                  bufs[k][2].data_ptr(), B, stats=True)
