@@ -384,7 +384,7 @@ static_assert(kChunk < 65536, "16-bit chunk counters");
 // and staged in node order in shared memory, mark flags + block scan, then
 // written in node order (a node's new entries / marks are contiguous in its
 // ring, so the stores coalesce); finally publish {eb, ee, gb, ge, ring}.
-__global__ void __launch_bounds__(kPB) k_bucket_place(PlaceArgs a) {
+__global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PlaceSmem& sm = *reinterpret_cast<PlaceSmem*>(smem_raw);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -410,12 +410,10 @@ __global__ void __launch_bounds__(kPB) k_bucket_place(PlaceArgs a) {
     __syncthreads();
     // item i = warp*R*32 + r*32 + lane of the chunk belongs to this lane in round r
     u32 dk[kChunkItems];
-    Entry pe[kChunkItems];
 #pragma unroll
     for (int r = 0; r < kChunkItems; ++r) {
       const u32 i = warp * (32 * kChunkItems) + r * 32 + lane;
       dk[r] = i < n ? (a.keys[c0 + i] & (kPB - 1)) : 0u;
-      if (i < n) pe[r] = a.vals[c0 + i];
     }
     for (int i = t; i < (kPB / 32) * kPB; i += kPB) (&sm.wcnt[0][0])[i] = 0;
     __syncthreads();
@@ -448,12 +446,12 @@ __global__ void __launch_bounds__(kPB) k_bucket_place(PlaceArgs a) {
     }
     __syncthreads();
 #pragma unroll
-    for (int r = 0; r < kChunkItems; ++r) {
+    for (int r = 0; r < kChunkItems; ++r) {  // payloads loaded only now: not live across the ranking
       const u32 i = warp * (32 * kChunkItems) + r * 32 + lane;
       if (i < n) {
         const u32 nd = dk[r];
         const u32 sp = sm.off[nd] + sm.wcnt[warp][nd] + rank[r];
-        sm.sent[sp] = pe[r];
+        sm.sent[sp] = a.vals[c0 + i];
         sm.snode[sp] = static_cast<u8>(nd);
       }
     }
