@@ -82,6 +82,16 @@ __device__ __forceinline__ Entry load_entry(const Entry* p) {
 // node (G ~ 33) costs 3 dependent round trips instead of 6.
 constexpr u32 kScan = 4;
 __device__ __forceinline__ u32 ub_ring(const i64* a, Ring r, u32 lo, u32 hi, i64 x) {
+  if (hi - lo > kScan) {
+    // forward walks move to ever later times: the answer is usually among
+    // the run's last keys (or past them: the walk ends), so those go first
+    const u32 s0 = hi - kScan;
+    u32 n = 0;
+#pragma unroll
+    for (u32 i = 0; i < kScan; ++i) n += a[r(s0 + i)] <= x ? 1u : 0u;
+    if (n) return s0 + n;
+    hi = s0;
+  }
   while (hi - lo > kScan) {
     const u32 mid = lo + ((hi - lo) >> 1);
     if (x < a[r(mid)]) hi = mid;
@@ -94,6 +104,13 @@ __device__ __forceinline__ u32 ub_ring(const i64* a, Ring r, u32 lo, u32 hi, i64
   return lo + n;
 }
 __device__ __forceinline__ u32 lb_ring(const i64* a, Ring r, u32 lo, u32 hi, i64 x) {
+  if (hi - lo > kScan) {  // mirror of ub_ring: backward walks move to ever earlier times
+    u32 n = 0;
+#pragma unroll
+    for (u32 i = 0; i < kScan; ++i) n += a[r(lo + i)] < x ? 1u : 0u;
+    if (n < kScan) return lo + n;
+    lo += kScan;
+  }
   while (hi - lo > kScan) {
     const u32 mid = lo + ((hi - lo) >> 1);
     if (a[r(mid)] < x) lo = mid + 1;
@@ -128,6 +145,18 @@ __device__ __forceinline__ void causal_slice_entries(const Entry* ent, Ring er, 
                                                      u32& c, u32& e) {
   u32 a = lo, b = hi;
   if (dir == 0) {
+    if (b - a > kScan) {  // the run's end first, as in ub_ring
+      const u32 s0 = b - kScan;
+      u32 n = 0;
+#pragma unroll
+      for (u32 i = 0; i < kScan; ++i) n += ent[er(s0 + i)].t <= t ? 1u : 0u;
+      if (n) {
+        c = s0 + n;
+        e = hi;
+        return;
+      }
+      b = s0;
+    }
     while (b - a > kScan) {
       const u32 mid = a + ((b - a) >> 1);
       if (t < ent[er(mid)].t) b = mid;
@@ -140,6 +169,17 @@ __device__ __forceinline__ void causal_slice_entries(const Entry* ent, Ring er, 
     c = a + n;
     e = hi;
   } else {
+    if (b - a > kScan) {
+      u32 n = 0;
+#pragma unroll
+      for (u32 i = 0; i < kScan; ++i) n += ent[er(a + i)].t < t ? 1u : 0u;
+      if (n < kScan) {
+        c = lo;
+        e = a + n;
+        return;
+      }
+      a += kScan;
+    }
     while (b - a > kScan) {
       const u32 mid = a + ((b - a) >> 1);
       if (ent[er(mid)].t < t) a = mid + 1;
