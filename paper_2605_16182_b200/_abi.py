@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libtimewalk_b200.so")
+LIB_PATH = os.environ.get("TWG_LIB_PATH") or os.path.join(_HERE, "lib", "libtimewalk_b200.so")  # override: A/B builds
 
 TWG_OK, TWG_EINVAL, TWG_ERANGE, TWG_ELOGIC, TWG_ECUDA, TWG_ENOMEM = range(6)
 

@@ -85,12 +85,17 @@ __device__ __forceinline__ u32 ub_ring(const i64* a, Ring r, u32 lo, u32 hi, i64
   if (hi - lo > kScan) {
     // forward walks move to ever later times: the answer is usually among
     // the run's last keys (or past them: the walk ends), so those go first
-    const u32 s0 = hi - kScan;
+    // (the 32-B sector holding the last key: up to kScan keys, one sector)
+    const u32 last = hi - 1;
+    const u32 d0 = last - r.org, d = d0 >= r.cap ? d0 - r.cap : d0;
+    const u32 k = min((r.base + d) & (kScan - 1), d);  // keys of the sector before `last` (no ring wrap)
+    const i64* g = a + (r.base + d - k);
     u32 n = 0;
 #pragma unroll
-    for (u32 i = 0; i < kScan; ++i) n += a[r(s0 + i)] <= x ? 1u : 0u;
-    if (n) return s0 + n;
-    hi = s0;
+    for (u32 i = 0; i < kScan; ++i)
+      if (i <= k) n += g[i] <= x ? 1u : 0u;
+    if (n) return last - k + n;
+    hi = last - k;
   }
   while (hi - lo > kScan) {
     const u32 mid = lo + ((hi - lo) >> 1);
@@ -145,17 +150,35 @@ __device__ __forceinline__ void causal_slice_entries(const Entry* ent, Ring er, 
                                                      u32& c, u32& e) {
   u32 a = lo, b = hi;
   if (dir == 0) {
-    if (b - a > kScan) {  // the run's end first, as in ub_ring
-      const u32 s0 = b - kScan;
+    if (b - a > kScan) {  // the run's end first, as in ub_ring: the 64-B atom holding the last entry
+      const u32 last = b - 1;
+      const u32 d0 = last - er.org, d = d0 >= er.cap ? d0 - er.cap : d0;
+      const u32 k = min((er.base + d) & 3u, d);  // entries of the atom before `last` (no ring wrap)
+      const u32 s0 = last - k;
+      const Entry* g = ent + (er.base + d - k);
       u32 n = 0;
 #pragma unroll
-      for (u32 i = 0; i < kScan; ++i) n += ent[er(s0 + i)].t <= t ? 1u : 0u;
+      for (u32 i = 0; i < kScan; ++i)
+        if (i <= k) n += g[i].t <= t ? 1u : 0u;
       if (n) {
         c = s0 + n;
         e = hi;
         return;
       }
       b = s0;
+      const u32 ds = d - k;  // ring offset of s0
+      if (b - a > kScan && ds >= 4u) {  // then the whole atom before it
+        const Entry* h = ent + (er.base + ds - 4u);
+        u32 m = 0;
+#pragma unroll
+        for (u32 i = 0; i < 4u; ++i) m += h[i].t <= t ? 1u : 0u;
+        if (m) {
+          c = s0 - 4u + m;
+          e = hi;
+          return;
+        }
+        b = s0 - 4u;
+      }
     }
     while (b - a > kScan) {
       const u32 mid = a + ((b - a) >> 1);
