@@ -24,8 +24,6 @@ constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanBlock * kScanItems;
 
 constexpr int kSortBlock = 256;
-constexpr int kSortItems = 8;
-constexpr int kSortTile = kSortBlock * kSortItems;
 constexpr int kRadixBits = 8;
 constexpr int kRadix = 1 << kRadixBits;
 
@@ -157,120 +155,6 @@ struct ArrayIn {
   __device__ __forceinline__ V val(u64 i) const { return v[i]; }
   __device__ __forceinline__ bool has_val() const { return v != nullptr; }
 };
-
-template <class K, int kItems = kSortItems, class In = ArrayIn<K, u32>>
-__global__ void __launch_bounds__(kSortBlock) k_radix_hist(In in, u64 n, int shift, u32* __restrict__ counts,
-                                                           u64 tiles) {
-  constexpr int kTile = kSortBlock * kItems;
-  __shared__ u32 hist[kRadix];
-  for (int b = threadIdx.x; b < kRadix; b += kSortBlock) hist[b] = 0;
-  __syncthreads();
-  const u64 base = static_cast<u64>(blockIdx.x) * kTile;
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    const u64 i = base + static_cast<u64>(j) * kSortBlock + threadIdx.x;
-    if (i < n) atomicAdd(&hist[static_cast<u32>(in.key(i) >> shift) & (kRadix - 1)], 1u);
-  }
-  __syncthreads();
-  for (int b = threadIdx.x; b < kRadix; b += kSortBlock) counts[static_cast<u64>(b) * tiles + blockIdx.x] = hist[b];
-}
-
-// Stable tile rank + coalesced scatter. Item order inside a tile is
-// (round j, warp, lane) == input order, which keeps the sort stable. V is
-// the value type (u32 indices, or a 16-byte payload carried through the
-// passes so the consumer reads it in order instead of gathering it).
-template <class K, class V, int kItems, class In = ArrayIn<K, V>>
-__global__ void __launch_bounds__(kSortBlock) k_radix_scatter(In in, K* __restrict__ keys_out,
-                                                              V* __restrict__ vals_out, u64 n,
-                                                              int shift, const u32* __restrict__ offsets,
-                                                              u64 tiles) {
-  const bool has_val = in.has_val();
-  constexpr int kWarps = kSortBlock / 32;
-  constexpr int kTile = kSortBlock * kItems;
-  __shared__ u32 wcount[kWarps][kRadix];
-  __shared__ u32 running[kRadix];
-  __shared__ u32 tile_start[kRadix];
-  __shared__ K skeys[kTile];
-  __shared__ V svals[kTile];
-
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const u64 base = static_cast<u64>(blockIdx.x) * kTile;
-  const u32 lanemask_lt = (1u << lane) - 1u;
-  for (int b = threadIdx.x; b < kRadix; b += kSortBlock) running[b] = 0;
-
-  // Warp-private ranking: warp w owns the tile's items [w*32*kItems, ...) in
-  // kItems rounds of 32 lanes, so its digit counters need no block barrier
-  // between rounds; one cross-warp scan per digit at the end.
-  K key[kItems];
-  V val[kItems];
-  u32 rank[kItems];
-  for (int b = threadIdx.x; b < kWarps * kRadix; b += kSortBlock) (&wcount[0][0])[b] = 0;
-  __syncthreads();
-  const u64 wbase = base + static_cast<u64>(warp) * (32 * kItems);
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    const u64 i = wbase + static_cast<u64>(j) * 32 + lane;
-    const bool valid = i < n;
-    key[j] = valid ? in.key(i) : K(0);
-    if (has_val && valid) val[j] = in.val(i);
-  }
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    const u64 i = wbase + static_cast<u64>(j) * 32 + lane;
-    const bool valid = i < n;
-    const u32 d = valid ? (static_cast<u32>(key[j] >> shift) & (kRadix - 1)) : 0u;
-    const u32 peers = digit_peers<kRadixBits>(d, valid);
-    const u32 r_in_round = __popc(peers & lanemask_lt);
-    const u32 before = valid ? wcount[warp][d] : 0u;
-    __syncwarp();
-    if (valid && r_in_round == 0) wcount[warp][d] = before + __popc(peers);
-    __syncwarp();
-    rank[j] = before + r_in_round;
-  }
-  __syncthreads();
-  for (int b = threadIdx.x; b < kRadix; b += kSortBlock) {  // per digit: exclusive scan across warps
-    u32 acc = 0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-      const u32 c = wcount[w][b];
-      wcount[w][b] = acc;
-      acc += c;
-    }
-    running[b] = acc;
-  }
-  __syncthreads();
-  // digit starts inside the tile
-  {
-    u32 total;
-    const u32 c = threadIdx.x < kRadix ? running[threadIdx.x] : 0u;
-    const u32 ex = block_excl_scan<u32>(c, &total);
-    if (threadIdx.x < kRadix) tile_start[threadIdx.x] = ex;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    const u64 i = wbase + static_cast<u64>(j) * 32 + lane;
-    if (i < n) {
-      const u32 d = static_cast<u32>(key[j] >> shift) & (kRadix - 1);
-      const u32 pos = tile_start[d] + wcount[warp][d] + rank[j];
-      skeys[pos] = key[j];
-      if (has_val) svals[pos] = val[j];
-    }
-  }
-  __syncthreads();
-  const u64 tile_n = n - base < static_cast<u64>(kTile) ? n - base : static_cast<u64>(kTile);
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    const u32 pos = static_cast<u32>(j) * kSortBlock + threadIdx.x;
-    if (pos < tile_n) {
-      const K k = skeys[pos];
-      const u32 d = static_cast<u32>(k >> shift) & (kRadix - 1);
-      const u64 dst = static_cast<u64>(offsets[static_cast<u64>(d) * tiles + blockIdx.x]) + (pos - tile_start[d]);
-      keys_out[dst] = k;
-      if (has_val) vals_out[dst] = svals[pos];
-    }
-  }
-}
 
 // ---------------------------------------------------- single-pass scan ----
 //
@@ -499,36 +383,214 @@ void merge_path(Ctx& ctx, KA ka, u64 na, KB kb, u64 nb, Emit emit) {
   TWG_LAUNCHED(ctx);
 }
 
-// Stable LSD sort of (keys, vals) by key bits [lo_bit, bits). Sorted
-// output lands in (*keys, *vals); the alt buffers are scratch of the same
-// size. Pointers are swapped as passes ping-pong. n < 2^32. Keys-only when
-// *vals == nullptr.
-// One LSD pass over digit `shift`: (in) -> (keys_out, vals_out).
-template <class K, class V, class In>
-void radix_pass(Ctx& ctx, In in, K* keys_out, V* vals_out, u64 n, int shift) {
-  constexpr int kItems = sizeof(V) > 4 ? kSortItems / 2 : kSortItems;  // 16-B payloads: staging < 48 KB
-  constexpr int kTile = kSortBlock * kItems;
-  cudaStream_t st = ctx.stream;
-  const u64 tiles = (n + kTile - 1) / kTile;
-  if (tiles * kRadix >= (1ull << 32)) fail(TWG_EINVAL, "radix_sort_pairs: input too large");
-  DevBuf<u32> counts(tiles * kRadix + 1, st);
-  DevBuf<u32> offsets(tiles * kRadix + 1, st);
-  k_radix_hist<K, kItems, In><<<static_cast<unsigned>(tiles), kSortBlock, 0, st>>>(in, n, shift, counts.p, tiles);
-  TWG_LAUNCHED(ctx);
-  exclusive_scan<u32>(ctx, LoadFn<u32>{counts.p}, tiles * kRadix, offsets.p);
-  k_radix_scatter<K, V, kItems, In><<<static_cast<unsigned>(tiles), kSortBlock, 0, st>>>(in, keys_out, vals_out, n,
-                                                                                          shift, offsets.p, tiles);
-  TWG_LAUNCHED(ctx);
+// ---------------------------------------------------------- radix sort ----
+//
+// Stable LSD radix sort, one kernel per 8-bit digit pass ("onesweep"): the
+// digit histograms of ALL passes come from one read of the keys up front;
+// each pass then takes its tiles by ticket, ranks the tile stably (warp-
+// private match/ballot counters + a cross-warp scan), resolves every digit's
+// global offset by a decoupled look-back over the preceding tiles' posted
+// counts (one thread per digit), stages the tile in digit order in shared
+// memory and writes digit-contiguous, coalesced runs. Each pass reads and
+// writes the data once; no per-pass histogram kernel, no count-matrix scan.
+constexpr int kMaxPasses = 8;
+
+template <class K>
+__device__ __forceinline__ u32 digit_of(K k, int shift) {
+  return static_cast<u32>(k >> shift) & (kRadix - 1);
 }
 
+// hist[p * 256 + d] = items whose digit p (bits lo_bit + 8p ...) is d
+template <class K, class In>
+__global__ void __launch_bounds__(kSortBlock) k_radix_global_hist(In in, u64 n, int lo_bit, int passes, u32* hist) {
+  __shared__ u32 h[kMaxPasses][kRadix];
+  for (int i = threadIdx.x; i < kMaxPasses * kRadix; i += kSortBlock) (&h[0][0])[i] = 0;
+  __syncthreads();
+  for (u64 i = blockIdx.x * static_cast<u64>(kSortBlock) + threadIdx.x; i < n;
+       i += static_cast<u64>(gridDim.x) * kSortBlock) {
+    const K k = in.key(i);
+    for (int p = 0; p < passes; ++p) atomicAdd(&h[p][digit_of(k, lo_bit + p * kRadixBits)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < passes * kRadix; i += kSortBlock) {
+    const u32 c = (&h[0][0])[i];
+    if (c) atomicAdd(&hist[i], c);
+  }
+}
+
+// per pass: exclusive scan of the 256 digit counts -> digit starts (in place)
+static __global__ void __launch_bounds__(kRadix) k_radix_digit_starts(u32* hist, int passes) {
+  for (int p = 0; p < passes; ++p) {
+    u32 total;
+    const u32 c = hist[p * kRadix + threadIdx.x];
+    const u32 ex = block_excl_scan<u32>(c, &total);
+    __syncthreads();
+    hist[p * kRadix + threadIdx.x] = ex;
+    __syncthreads();
+  }
+}
+
+template <class K, class V>
+struct OnesweepSmem {
+  static constexpr int kItems = sizeof(K) + sizeof(V) > 8 ? 8 : 16;
+  static constexpr int kTile = kSortBlock * kItems;
+  u32 wcount[kSortBlock / 32][kRadix];
+  u32 tile_start[kRadix + 1];
+  u64 gstart[kRadix];
+  u32 tile;
+  K keys[kTile];
+  V vals[kTile];
+};
+
+template <class K, class V, class In>
+__global__ void __launch_bounds__(kSortBlock) k_radix_onesweep(In in, K* __restrict__ keys_out,
+                                                               V* __restrict__ vals_out, u64 n, int shift,
+                                                               const u32* __restrict__ digit_start, u64* state,
+                                                               u32* ticket) {
+  using S = OnesweepSmem<K, V>;
+  constexpr int kItems = S::kItems, kTile = S::kTile, kWarps = kSortBlock / 32;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  S& sm = *reinterpret_cast<S*>(smem_raw);
+  const bool has_val = in.has_val();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const u32 lt = (1u << lane) - 1u;
+  if (threadIdx.x == 0) sm.tile = atomicAdd(ticket, 1u);
+  for (int b = threadIdx.x; b < kWarps * kRadix; b += kSortBlock) (&sm.wcount[0][0])[b] = 0;
+  __syncthreads();
+  const u64 tile = sm.tile;
+  const u64 base = tile * kTile;
+  const u32 tile_n = static_cast<u32>(n - base < static_cast<u64>(kTile) ? n - base : kTile);
+  // warp w owns the tile's items [w*32*kItems, ...) in kItems rounds of 32:
+  // item order (warp, round, lane) == input order keeps the sort stable
+  const u32 wbase = static_cast<u32>(warp) * (32 * kItems);
+  K key[kItems];
+  u32 rank[kItems];
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const u32 i = wbase + j * 32 + lane;
+    key[j] = i < tile_n ? in.key(base + i) : K(0);
+  }
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const u32 i = wbase + j * 32 + lane;
+    const bool valid = i < tile_n;
+    const u32 d = valid ? digit_of(key[j], shift) : 0u;
+    const u32 peers = digit_peers<kRadixBits>(d, valid);
+    const u32 before = valid ? sm.wcount[warp][d] : 0u;
+    __syncwarp();
+    if (valid && (__ffs(peers) - 1) == lane) sm.wcount[warp][d] = before + __popc(peers);
+    __syncwarp();
+    rank[j] = before + __popc(peers & lt);
+  }
+  __syncthreads();
+  {  // thread d: digit d's count in this tile, its look-back, its tile start
+    const int d = threadIdx.x;
+    u32 acc = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const u32 c = sm.wcount[w][d];
+      sm.wcount[w][d] = acc;
+      acc += c;
+    }
+    volatile u64* st = state;
+    u64 excl = 0;
+    if (tile == 0) {
+      st[d] = kLbInclusive | acc;
+    } else {
+      st[tile * kRadix + d] = kLbAggregate | acc;
+      for (u64 j = tile - 1;; --j) {
+        u64 s;
+        do {
+          s = st[j * kRadix + d];
+        } while ((s >> 62) == 0);
+        excl += s & kLbValueMask;
+        if ((s >> 62) == 2) break;
+      }
+      st[tile * kRadix + d] = kLbInclusive | (excl + acc);
+    }
+    sm.gstart[d] = digit_start[d] + excl;
+    u32 total;
+    sm.tile_start[d] = block_excl_scan<u32>(acc, &total);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {  // stage in digit order; payloads loaded only now
+    const u32 i = wbase + j * 32 + lane;
+    if (i < tile_n) {
+      const u32 d = digit_of(key[j], shift);
+      const u32 pos = sm.tile_start[d] + sm.wcount[warp][d] + rank[j];
+      sm.keys[pos] = key[j];
+      if (has_val) sm.vals[pos] = in.val(base + i);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const u32 pos = static_cast<u32>(j) * kSortBlock + threadIdx.x;
+    if (pos < tile_n) {
+      const K k = sm.keys[pos];
+      const u32 d = digit_of(k, shift);
+      const u64 dst = sm.gstart[d] + (pos - sm.tile_start[d]);
+      keys_out[dst] = k;
+      if (has_val) vals_out[dst] = sm.vals[pos];
+    }
+  }
+}
+
+// Passes over key bits [lo_bit, bits): the first reads through `in0`, the
+// rest ping-pong between (*keys, *vals) and the alt buffers; the sorted
+// result ends in (*keys, *vals). Keys-only when the values are null.
+template <class K, class V, class In>
+void radix_sort_impl(Ctx& ctx, In in0, bool from_in, K** keys, K** keys_alt, V** vals, V** vals_alt, u64 n,
+                     int bits, int lo_bit) {
+  using S = OnesweepSmem<K, V>;
+  cudaStream_t st = ctx.stream;
+  const int passes = (bits - lo_bit + kRadixBits - 1) / kRadixBits;
+  if (passes > kMaxPasses) fail(TWG_EINVAL, "radix_sort_pairs: key too wide");
+  const u64 tiles = (n + S::kTile - 1) / S::kTile;
+  if (tiles >= (1ull << 31)) fail(TWG_EINVAL, "radix_sort_pairs: input too large");
+  static const bool attr = [] {
+    TWG_CUDA(cudaFuncSetAttribute(k_radix_onesweep<K, V, In>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sizeof(S))));
+    TWG_CUDA(cudaFuncSetAttribute(k_radix_onesweep<K, V, ArrayIn<K, V>>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(S))));
+    return true;
+  }();
+  (void)attr;
+  DevBuf<u32> hist(static_cast<u64>(passes) * kRadix, st);
+  DevBuf<u64> state(tiles * kRadix + 1, st);  // + the ticket word
+  TWG_CUDA(cudaMemsetAsync(hist.p, 0, hist.bytes(), st));
+  const unsigned hgrid = grid_for(n, kSortBlock, static_cast<unsigned>(ctx.sm_count) * 8);
+  if (from_in) k_radix_global_hist<K, In><<<hgrid, kSortBlock, 0, st>>>(in0, n, lo_bit, passes, hist.p);
+  else k_radix_global_hist<K, ArrayIn<K, V>><<<hgrid, kSortBlock, 0, st>>>(ArrayIn<K, V>{*keys, *vals}, n, lo_bit,
+                                                                            passes, hist.p);
+  TWG_LAUNCHED(ctx);
+  k_radix_digit_starts<<<1, kRadix, 0, st>>>(hist.p, passes);
+  TWG_LAUNCHED(ctx);
+  u32* ticket = reinterpret_cast<u32*>(state.p + tiles * kRadix);
+  for (int p = 0; p < passes; ++p) {
+    const int shift = lo_bit + p * kRadixBits;
+    TWG_CUDA(cudaMemsetAsync(state.p, 0, state.bytes(), st));
+    if (p == 0 && from_in) {
+      k_radix_onesweep<K, V, In><<<static_cast<unsigned>(tiles), kSortBlock, sizeof(S), st>>>(
+          in0, *keys, *vals, n, shift, hist.p + p * kRadix, state.p, ticket);
+    } else {
+      k_radix_onesweep<K, V, ArrayIn<K, V>><<<static_cast<unsigned>(tiles), kSortBlock, sizeof(S), st>>>(
+          ArrayIn<K, V>{*keys, *vals}, *keys_alt, *vals_alt, n, shift, hist.p + p * kRadix, state.p, ticket);
+      std::swap(*keys, *keys_alt);
+      std::swap(*vals, *vals_alt);
+    }
+    TWG_LAUNCHED(ctx);
+  }
+}
+
+// Stable LSD sort of (keys, vals) by key bits [lo_bit, bits). Sorted output
+// lands in (*keys, *vals); the alt buffers are scratch of the same size.
+// n < 2^32. Keys-only when *vals == nullptr.
 template <class K, class V = u32>
 void radix_sort_pairs(Ctx& ctx, K** keys, K** keys_alt, V** vals, V** vals_alt, u64 n, int bits, int lo_bit = 0) {
   if (n < 2 || bits <= lo_bit) return;
-  for (int shift = lo_bit; shift < bits; shift += kRadixBits) {
-    radix_pass<K, V>(ctx, ArrayIn<K, V>{*keys, *vals}, *keys_alt, *vals_alt, n, shift);
-    std::swap(*keys, *keys_alt);
-    std::swap(*vals, *vals_alt);
-  }
+  radix_sort_impl<K, V>(ctx, ArrayIn<K, V>{*keys, *vals}, false, keys, keys_alt, vals, vals_alt, n, bits, lo_bit);
 }
 
 // Same, the first pass reading its items through `in` (sorted result in
@@ -536,8 +598,7 @@ void radix_sort_pairs(Ctx& ctx, K** keys, K** keys_alt, V** vals, V** vals_alt, 
 template <class K, class V, class In>
 void radix_sort_pairs_from(Ctx& ctx, In in, K** keys, K** keys_alt, V** vals, V** vals_alt, u64 n, int bits,
                            int lo_bit) {
-  radix_pass<K, V>(ctx, in, *keys, *vals, n, lo_bit);
-  radix_sort_pairs<K, V>(ctx, keys, keys_alt, vals, vals_alt, n, bits, lo_bit + kRadixBits);
+  radix_sort_impl<K, V>(ctx, in, true, keys, keys_alt, vals, vals_alt, n, bits > lo_bit ? bits : lo_bit + 1, lo_bit);
 }
 
 }  // namespace twg
