@@ -424,6 +424,7 @@ def run_e2e_pipelined(args, tw, ctx, wl, variant, walk_cfg):
     timed_hops = 0
     t_start = None
     assert lib.twg_stage_batch(ctx.handle, 0, C.c_void_p(hosts[0].data_ptr()), B) == 0
+    t_prev = time.perf_counter()
     for k in range(n_steps):
         if k == args.warmup:
             ctx.sync()
@@ -450,6 +451,10 @@ def run_e2e_pipelined(args, tw, ctx, wl, variant, walk_cfg):
                                                     C.c_void_p(times.data_ptr()), nodes.numel(), C.byref(total))
         assert rc == 0, lib.twg_last_error()
         pending[slot] = (ws, total.value)
+        if os.environ.get("TWG_BENCH_VERBOSE") == "1":
+            now = time.perf_counter()
+            print(f"e2e step {k}: {(now - t_prev) * 1e3:7.2f} ms (host loop)", file=sys.stderr)
+            t_prev = now
         timed_hops += wst.hops
         d2h += 8 * (ws.walk_count + 1) + 16 * total.value
         del snap
