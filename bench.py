@@ -337,11 +337,12 @@ def run_ours(args, rank, world, local_rank):
     b += args.steps
     # causality audit (GPU, validity.cpp:108-120 semantics) of one full walk
     # generation on the current snapshot, outside the timed region
-    audit = None
+    audit = walk_output = None
     if not args.no_audit:
         snap = window.snapshot()
         ws = tw.generate_walks(snap, walk_cfg(), variant=variant)
         audit, _ = ws.audit(snap)
+        walk_output = measure_walk_output(tw, ws, lib)
         del ws, snap
     head = timed_pass(True, b) if args.pipelined else seq
     total_ms, launches, clk = head["total_ms"], head["launches"], head["clocks"]
@@ -377,13 +378,40 @@ def run_ours(args, rank, world, local_rank):
                   launches=launches, clocks=clk, alg_bytes=allsum(alg_bytes), ingest_alg=ingest_alg,
                   append_alg=append_alg,
                   seq_total_ms=allmax(seq_total_ms), seq_hops=allsum(seq_hops), pipelined=bool(args.pipelined),
-                  audit=audit)
+                  audit=audit, walk_output=walk_output)
 
     # ---- e2e pass through the C ABI with host buffers -----------------------------------
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, tw, ctx, wl, rank, world, local_rank, variant, walk_cfg)
     return result, e2e, wl
+
+
+def measure_walk_output(tw, ws, lib):
+    """The walk writers (io.cpp:119-135 text, :173-183 binary) on one full
+    C5 walk generation: device formatting alone, and formatting + D2H into
+    pinned host memory (outside the timed region; wall clock around
+    synchronous C-ABI calls)."""
+    import ctypes as C
+
+    import torch
+
+    n = C.c_uint64()
+    t0 = time.perf_counter()
+    assert lib.twg_walkset_text(ws.handle, None, 0, C.byref(n)) == 0
+    fmt_s = time.perf_counter() - t0
+    text_bytes = n.value
+    buf = torch.empty(max(text_bytes, 1), dtype=torch.uint8, pin_memory=True)
+    t0 = time.perf_counter()
+    assert lib.twg_walkset_text(ws.handle, C.c_void_p(buf.data_ptr()), buf.numel(), C.byref(n)) == 0
+    text_s = time.perf_counter() - t0
+    assert lib.twg_walkset_binary(ws.handle, None, 0, C.byref(n)) == 0
+    bin_bytes = n.value
+    del buf
+    return {"walks": ws.walk_count, "hops": ws.total_hops, "text_bytes": text_bytes,
+            "text_format_ms": fmt_s * 1e3, "text_format_plus_d2h_ms": text_s * 1e3,
+            "text_GBps": text_bytes / text_s / 1e9, "binary_bytes": bin_bytes,
+            "path": "twg_walkset_text (device formatting, pinned D2H); byte-identical to write_walks_text"}
 
 
 def run_e2e_pipelined(args, tw, ctx, wl, variant, walk_cfg):
@@ -773,6 +801,7 @@ def main():
             "causality_audit": {**res["audit"], "scope": "one full walk generation on the steady-state window, "
                                                          "GPU auditor (twg_walkset_audit, EdgeOracle semantics)"}
                                if res["audit"] else None,
+            "walk_output": res.get("walk_output"),
             "phases": {"source": "sequential pass (ingest then walks per batch, one stream, device events)",
                        "ms_per_step": res["seq_total_ms"] / args.steps,
                        "ingest_ms_per_step": res["ingest_ms"] / args.steps,

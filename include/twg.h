@@ -265,6 +265,22 @@ typedef struct twg_audit_report {
 int twg_walkset_audit(twg_walkset* w, twg_store* s, int direction, int strict, int64_t* first_violation,
                       twg_audit_report* out);
 
+/* Walk writers (io.cpp:119-135 write_walks_text, io.cpp:173-183
+ * write_walks_binary), serialised on the device so only the finished bytes
+ * cross PCIe. Each call sets *len to the image size; with dst != NULL the
+ * image is copied there (cap >= *len, else TWG_EINVAL). Text: one line per
+ * walk of length >= 2, `node@time` entries separated by ' ', a start
+ * sentinel as `node@-`, '\n' per line. Binary: "TMPW0002", u32 stride,
+ * u64 walk_count, walk-major i64 nodes and times (zero past each length),
+ * u32 lengths — byte-identical to the reference's writers. */
+int twg_walkset_text(twg_walkset* w, void* dst, uint64_t cap, uint64_t* len);
+int twg_walkset_binary(twg_walkset* w, void* dst, uint64_t cap, uint64_t* len);
+/* A device walk set from a host WalkSet image (walk_engine.hpp:55-70:
+ * walk-major nodes/times [walk_count * stride], lengths [walk_count]) — the
+ * façade's io over host WalkSets. */
+int twg_walkset_from_host(twg_ctx* ctx, uint32_t stride, uint64_t walk_count, const int64_t* nodes,
+                          const int64_t* times, const uint32_t* lengths, twg_walkset** out);
+
 /* sample_start_edge over the store for n (u1, u2) pairs -> time-sorted edge index */
 int twg_sample_start_edges(twg_store* s, int bias, const double* u1, const double* u2, uint64_t n,
                            uint64_t* out);

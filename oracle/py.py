@@ -424,6 +424,8 @@ class RefOracle:
         L.twref_walks_count.argtypes = [VP]
         L.twref_walks_copy.argtypes = [VP, VP, VP, VP]
         L.twref_walks_free.argtypes = [VP]
+        if hasattr(L, "twref_walks_serialize"):
+            L.twref_walks_serialize.argtypes = [C.c_uint32, U64, VP, VP, VP, I, VP, U64, C.POINTER(U64)]
         L.twref_schedule_step.argtypes = [VP, VP, VP, U64, C.POINTER(ThresholdsC), VP, VP, U64]
         L.twref_replay.argtypes = [VP, U64, C.POINTER(ReplayCfgRef), C.POINTER(U64), C.POINTER(I)]
         L.twref_replay_record.argtypes = [VP, U64, C.POINTER(BatchStatsC), C.POINTER(WalkStatsC)]
@@ -584,6 +586,21 @@ class RefOracle:
         finally:
             self.L.twref_replay_free(h)
         return out
+
+    def serialize_walks(self, walks: dict, binary: bool) -> bytes:
+        """The reference's write_walks_text / write_walks_binary (io.cpp:119-135, :173-183)."""
+        args = (walks["stride"], walks["walk_count"], _p(np.ascontiguousarray(walks["nodes"], np.int64)),
+                _p(np.ascontiguousarray(walks["times"], np.int64)),
+                _p(np.ascontiguousarray(walks["lengths"], np.uint32)), int(binary))
+        n = U64()
+        rc = self.L.twref_walks_serialize(*args, None, 0, C.byref(n))
+        if rc:
+            self._err(rc)
+        buf = np.empty(max(n.value, 1), np.uint8)
+        rc = self.L.twref_walks_serialize(*args, _p(buf), buf.size, C.byref(n))
+        if rc:
+            self._err(rc)
+        return buf[: n.value].tobytes()
 
     def check_walkset(self, edges, undirected, walks: dict, direction=0):
         e = edges_array(edges)

@@ -20,7 +20,10 @@
 #include <string>
 #include <vector>
 
+#include <sstream>
+
 #include "timewalk/edge_store.hpp"
+#include "timewalk/io.hpp"
 #include "timewalk/replay.hpp"
 #include "timewalk/rng.hpp"
 #include "timewalk/samplers.hpp"
@@ -412,6 +415,27 @@ void twref_walks_copy(void* h, int64_t* nodes, int64_t* times, uint32_t* lengths
   if (lengths) std::memcpy(lengths, w.lengths.data(), w.lengths.size() * sizeof(uint32_t));
 }
 void twref_walks_free(void* h) { delete static_cast<WalkSet*>(h); }
+
+// The reference's walk writers (io.cpp:119-135 write_walks_text, :173-183
+// write_walks_binary) over a WalkSet image: *len = bytes; copied to dst when
+// dst != NULL and cap >= *len.
+int twref_walks_serialize(uint32_t stride, uint64_t count, const int64_t* nodes, const int64_t* times,
+                          const uint32_t* lengths, int binary, char* dst, uint64_t cap, uint64_t* len) {
+  return guarded([&] {
+    WalkSet w;
+    w.stride = stride;
+    w.walk_count = count;
+    w.nodes.assign(nodes, nodes + count * stride);
+    w.times.assign(times, times + count * stride);
+    w.lengths.assign(lengths, lengths + count);
+    std::ostringstream out;
+    if (binary) write_walks_binary(out, w);
+    else write_walks_text(out, w);
+    const std::string b = out.str();
+    *len = b.size();
+    if (dst && cap >= b.size()) std::memcpy(dst, b.data(), b.size());
+  });
+}
 
 // Tier counts of one schedule_step over given walk populations at internal
 // nodes (test_walk_engine.cpp:16-29 style fixtures). out: 5 task-list sizes +

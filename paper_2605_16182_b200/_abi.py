@@ -112,6 +112,9 @@ SIGNATURES = {
     "twg_walkset_download": (I, [VP, VP, VP, VP]),
     "twg_walkset_download_compact": (I, [VP, VP, VP, VP]),
     "twg_walkset_audit": (I, [VP, VP, I, I, VP, VP]),
+    "twg_walkset_text": (I, [VP, VP, U64, C.POINTER(U64)]),
+    "twg_walkset_binary": (I, [VP, VP, U64, C.POINTER(U64)]),
+    "twg_walkset_from_host": (I, [VP, C.c_uint32, U64, VP, VP, VP, PP]),
     "twg_walkset_device": (I, [VP, PP, PP, PP]),
     "twg_sample_start_edges": (I, [VP, I, VP, VP, U64, VP]),
     "twg_schedule_step": (I, [VP, VP, VP, U64, VP, VP, VP, U64, VP]),

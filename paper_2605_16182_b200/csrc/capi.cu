@@ -568,6 +568,65 @@ int twg_walkset_download(twg_walkset* w, int64_t* nodes, int64_t* times, uint32_
   });
 }
 
+int twg_walkset_text(twg_walkset* w, void* dst, uint64_t cap, uint64_t* len) {
+  return guarded([&] {
+    require(len != nullptr, "twg_walkset_text: len");
+    WalkSetDev& x = *w->w;
+    Ctx& c = *x.ctx;
+    DevBuf<char> text;
+    u64 bytes = 0;
+    walks_text(c, x, text, &bytes);
+    *len = bytes;
+    if (dst) {
+      require(cap >= bytes, "twg_walkset_text: buffer too small");
+      if (bytes) d2h(c, static_cast<char*>(dst), text.p, bytes);
+    }
+    sync(c);
+  });
+}
+
+int twg_walkset_binary(twg_walkset* w, void* dst, uint64_t cap, uint64_t* len) {
+  return guarded([&] {
+    require(len != nullptr, "twg_walkset_binary: len");
+    WalkSetDev& x = *w->w;
+    Ctx& c = *x.ctx;
+    const u64 bytes = walks_binary_size(x);
+    *len = bytes;
+    if (!dst) return;
+    require(cap >= bytes, "twg_walkset_binary: buffer too small");
+    char* p = static_cast<char*>(dst);
+    std::memcpy(p, "TMPW0002", 8);  // kWalkBinaryMagic (io.hpp:29), then write_raw fields (io.cpp:175-176)
+    const u32 stride = x.stride;
+    const u64 count = x.count;
+    std::memcpy(p + 8, &stride, 4);
+    std::memcpy(p + 12, &count, 8);
+    const u64 cells = count * stride;
+    char* pn = p + kWalkBinaryHeader;
+    char* pt = pn + 8 * cells;
+    char* pl = pt + 8 * cells;
+    DevBuf<i64> wn, wt;
+    if (cells) {
+      walk_major_image(c, x, wn, wt);
+      TWG_CUDA(cudaMemcpyAsync(pn, wn.p, 8 * cells, cudaMemcpyDeviceToHost, c.stream));
+      TWG_CUDA(cudaMemcpyAsync(pt, wt.p, 8 * cells, cudaMemcpyDeviceToHost, c.stream));
+    }
+    if (count) TWG_CUDA(cudaMemcpyAsync(pl, x.lengths.p, 4 * count, cudaMemcpyDeviceToHost, c.stream));
+    sync(c);
+  });
+}
+
+int twg_walkset_from_host(twg_ctx* ctx, uint32_t stride, uint64_t walk_count, const int64_t* nodes,
+                          const int64_t* times, const uint32_t* lengths, twg_walkset** out) {
+  return guarded([&] {
+    require(out != nullptr, "twg_walkset_from_host: out");
+    require(walk_count == 0 || (lengths && (stride == 0 || (nodes && times))), "twg_walkset_from_host: arrays");
+    for (u64 i = 0; i < walk_count; ++i) require(lengths[i] <= stride, "twg_walkset_from_host: length > stride");
+    auto w = std::make_unique<WalkSetDev>();
+    walks_from_host(ctx->c, stride, walk_count, nodes, times, lengths, *w);
+    *out = new twg_walkset{w.release()};
+  });
+}
+
 int twg_walkset_audit(twg_walkset* w, twg_store* s, int direction, int strict, int64_t* first_violation,
                       twg_audit_report* out) {
   return guarded([&] {

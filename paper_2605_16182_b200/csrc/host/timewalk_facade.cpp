@@ -6,6 +6,13 @@
 // Status codes become the reference's exception types.
 #include <algorithm>
 #include <chrono>
+#include <charconv>
+#include <cstring>
+#include <fstream>
+#include <istream>
+#include <ostream>
+#include <sstream>
+#include <vector>
 #include <cmath>
 #include <map>
 #include <mutex>
@@ -14,6 +21,7 @@
 #include <string>
 
 #include "timewalk/edge_store.hpp"
+#include "timewalk/io.hpp"
 #include "timewalk/primitives.hpp"
 #include "timewalk/replay.hpp"
 #include "timewalk/samplers.hpp"
@@ -627,6 +635,140 @@ std::uint64_t replay_stream(std::span<const TemporalEdge> edges, const ReplayCon
   }
   flush(edges.size());
   return batch_index;
+}
+
+// ---- walk writers (io.cpp:119-135, :173-183) on the device ----------------------
+
+namespace {
+
+// uploads the host image, has the device serialise it, streams the bytes out
+void write_walks_device(std::ostream& out, const WalkSet& walks, bool binary) {
+  std::lock_guard<std::recursive_mutex> lk(api_mutex());
+  twg_walkset* w = nullptr;
+  check(twg_walkset_from_host(ctx(), walks.stride, walks.walk_count, walks.nodes.data(), walks.times.data(),
+                              walks.lengths.data(), &w));
+  std::uint64_t len = 0;
+  int rc = binary ? twg_walkset_binary(w, nullptr, 0, &len) : twg_walkset_text(w, nullptr, 0, &len);
+  std::vector<char> bytes;
+  if (rc == TWG_OK) {
+    bytes.resize(len);
+    rc = binary ? twg_walkset_binary(w, bytes.data(), len, &len) : twg_walkset_text(w, bytes.data(), len, &len);
+  }
+  twg_walkset_destroy(w);
+  check(rc);
+  out.write(bytes.data(), static_cast<std::streamsize>(bytes.size()));
+}
+
+}  // namespace
+
+void write_walks_text(std::ostream& out, const WalkSet& walks) { write_walks_device(out, walks, false); }
+
+void write_walks_binary(std::ostream& out, const WalkSet& walks) { write_walks_device(out, walks, true); }
+
+void write_walks(const std::string& path, const WalkSet& walks, bool binary) {
+  std::ofstream out(path, std::ios::binary);
+  if (!out) throw std::runtime_error("cannot open " + path + " for writing");
+  write_walks_device(out, walks, binary);
+}
+
+// ---- walk readers (host deserialisers, io.cpp:137-216) ----------------------------
+
+namespace {
+
+// a non-negative decimal token (std::from_chars semantics, io.cpp:14-22)
+std::int64_t parse_token(std::string_view tok, std::size_t line, const char* what) {
+  std::int64_t v = 0;
+  const auto r = std::from_chars(tok.data(), tok.data() + tok.size(), v);
+  if (r.ec != std::errc{} || r.ptr != tok.data() + tok.size())
+    throw ParseError(std::string("invalid ") + what + " '" + std::string(tok) + "'", line);
+  if (v < 0) throw ParseError(std::string("negative ") + what, line);
+  return v;
+}
+
+template <class T>
+T read_pod(std::istream& in) {
+  T v{};
+  in.read(reinterpret_cast<char*>(&v), sizeof(T));
+  if (!in) throw std::runtime_error("binary input truncated");
+  return v;
+}
+
+}  // namespace
+
+std::vector<WalkRecord> read_walks_text(std::istream& in) {
+  std::vector<WalkRecord> out;
+  std::string line;
+  std::size_t no = 0;
+  while (std::getline(in, line)) {
+    ++no;
+    if (line.empty() || line[0] == '#') continue;
+    WalkRecord rec;
+    bool timed = false, untimed = false;
+    std::istringstream toks(line);
+    std::string tok;
+    while (toks >> tok) {
+      const std::string_view v(tok);
+      const std::size_t at = v.find('@');
+      if (at == std::string_view::npos) {
+        untimed = true;
+        rec.nodes.push_back(parse_token(v, no, "node"));
+        rec.times.push_back(kTimeUnset);
+      } else {
+        timed = true;
+        rec.nodes.push_back(parse_token(v.substr(0, at), no, "node"));
+        const std::string_view tp = v.substr(at + 1);
+        rec.times.push_back(tp == "-" ? kTimeUnset : parse_token(tp, no, "timestamp"));
+      }
+    }
+    if (rec.nodes.empty()) continue;
+    if (timed && untimed) throw ParseError("walk mixes timed and untimed entries", no);
+    if (untimed) rec.times.clear();
+    out.push_back(std::move(rec));
+  }
+  return out;
+}
+
+WalkSet read_walks_binary(std::istream& in) {
+  char magic[8];
+  in.read(magic, sizeof(magic));
+  if (!in || std::memcmp(magic, kWalkBinaryMagic, 8) != 0) throw std::runtime_error("walk binary: bad magic header");
+  WalkSet w;
+  w.stride = read_pod<std::uint32_t>(in);
+  w.walk_count = read_pod<std::uint64_t>(in);
+  const std::size_t cells = w.walk_count * w.stride;
+  w.nodes.resize(cells);
+  w.times.resize(cells);
+  w.lengths.resize(w.walk_count);
+  in.read(reinterpret_cast<char*>(w.nodes.data()), static_cast<std::streamsize>(cells * sizeof(NodeId)));
+  in.read(reinterpret_cast<char*>(w.times.data()), static_cast<std::streamsize>(cells * sizeof(Timestamp)));
+  in.read(reinterpret_cast<char*>(w.lengths.data()),
+          static_cast<std::streamsize>(w.walk_count * sizeof(std::uint32_t)));
+  if (!in) throw std::runtime_error("walk binary: truncated payload");
+  return w;
+}
+
+std::vector<WalkRecord> read_walks(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw std::runtime_error("cannot open " + path);
+  char magic[8] = {};
+  in.read(magic, sizeof(magic));
+  const bool binary = in.gcount() == 8 && std::memcmp(magic, kWalkBinaryMagic, 8) == 0;
+  in.clear();
+  in.seekg(0);
+  if (!binary) return read_walks_text(in);
+  const WalkSet w = read_walks_binary(in);
+  std::vector<WalkRecord> out;
+  for (std::uint64_t i = 0; i < w.walk_count; ++i) {
+    const std::uint32_t len = w.lengths[i];
+    if (len < 2) continue;  // as the text writer: walks that never left the start node
+    WalkRecord rec;
+    for (std::uint32_t j = 0; j < len; ++j) {
+      rec.nodes.push_back(w.node_at(i, j));
+      rec.times.push_back(w.time_at(i, j));
+    }
+    out.push_back(std::move(rec));
+  }
+  return out;
 }
 
 }  // namespace timewalk

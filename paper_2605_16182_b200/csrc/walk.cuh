@@ -53,6 +53,15 @@ void hop_walks_dev(Ctx& ctx, Store& s, const twg_walk_config& cfg, const u32* id
 // zero-initialised WalkSet (walk_engine.cpp:237-239)
 void walk_major_image(Ctx& ctx, const WalkSetDev& w, DevBuf<i64>& nodes, DevBuf<i64>& times);
 
+// walk writers (walkio.cu, io.cpp:119-135 / :173-183): the text image on the
+// device (bytes = its length), the binary image size, and a device walk set
+// from a host walk-major image (the façade's io over host WalkSets)
+constexpr u64 kWalkBinaryHeader = 20;  // "TMPW0002" + u32 stride + u64 walk_count
+void walks_text(Ctx& ctx, const WalkSetDev& w, DevBuf<char>& text, u64* bytes);
+u64 walks_binary_size(const WalkSetDev& w);
+void walks_from_host(Ctx& ctx, u32 stride, u64 count, const i64* nodes, const i64* times, const u32* lengths,
+                     WalkSetDev& out);
+
 // compact (CSR) image on the device: offsets[count+1], nodes/times[total]
 void compact_walks(Ctx& ctx, const WalkSetDev& w, DevBuf<u64>& offsets, DevBuf<i64>& nodes,
                    DevBuf<i64>& times, u64* total);

@@ -591,6 +591,44 @@ class WalkSet:
         out = {"walks": rep.walks, "valid_walks": rep.valid_walks, "hops": rep.hops, "valid_hops": rep.valid_hops}
         return out, (fv[: self.walk_count] if fv is not None else None)
 
+    @classmethod
+    def from_arrays(cls, stride: int, nodes, times, lengths, ctx: Optional[Context] = None) -> "WalkSet":
+        """A device walk set from a host WalkSet image (walk-major nodes /
+        times of walk_count x stride, lengths) — e.g. walks of another engine
+        to be written with the writers below."""
+        ctx = ctx or default_context()
+        lengths = np.ascontiguousarray(lengths, np.uint32)
+        nodes = np.ascontiguousarray(nodes, np.int64).reshape(-1)
+        times = np.ascontiguousarray(times, np.int64).reshape(-1)
+        count = len(lengths)
+        if nodes.size != count * stride or times.size != count * stride:
+            raise ValueError("WalkSet.from_arrays: nodes/times must hold walk_count * stride entries")
+        h = C.c_void_p()
+        _call("twg_walkset_from_host", ctx.handle, int(stride), count, _ptr(nodes), _ptr(times), _ptr(lengths),
+              C.byref(h))
+        return cls(h, ctx)
+
+    def to_text(self) -> bytes:
+        """write_walks_text (io.cpp:119-135), formatted on the device."""
+        n = C.c_uint64()
+        _call("twg_walkset_text", self.handle, None, 0, C.byref(n))
+        buf = np.empty(max(n.value, 1), np.uint8)
+        _call("twg_walkset_text", self.handle, _ptr(buf), buf.size, C.byref(n))
+        return buf[: n.value].tobytes()
+
+    def to_binary(self) -> bytes:
+        """write_walks_binary (io.cpp:173-183): the TMPW0002 image."""
+        n = C.c_uint64()
+        _call("twg_walkset_binary", self.handle, None, 0, C.byref(n))
+        buf = np.empty(max(n.value, 1), np.uint8)
+        _call("twg_walkset_binary", self.handle, _ptr(buf), buf.size, C.byref(n))
+        return buf[: n.value].tobytes()
+
+    def write(self, path: str, binary: bool = False) -> None:
+        """write_walks (io.hpp:61): the text or binary image to a file."""
+        with open(path, "wb") as f:
+            f.write(self.to_binary() if binary else self.to_text())
+
     def _download(self):
         if self._nodes is None:
             cells = self.walk_count * self.stride

@@ -11,6 +11,9 @@
 #include <stdexcept>
 #include <vector>
 
+#include <sstream>
+
+#include "timewalk/io.hpp"
 #include "timewalk/primitives.hpp"
 #include "timewalk/replay.hpp"
 #include "timewalk/rng.hpp"
@@ -369,6 +372,73 @@ static void primitive_cases() {
   CHECK((ex == std::vector<std::uint64_t>{0, 3, 4, 8, 9}));
 }
 
+// test_io.cpp:62-108 — walk writers (device) and readers
+void io_cases() {
+  {
+    WalkSet walks;
+    walks.stride = 3;
+    walks.walk_count = 2;
+    walks.nodes = {1, 2, 3, 9, 0, 0};
+    walks.times = {kTimeUnset, 5, 8, kTimeUnset, 0, 0};
+    walks.lengths = {3, 1};  // the second walk never left its start
+    std::ostringstream out;
+    write_walks_text(out, walks);
+    CHECK(out.str() == "1@- 2@5 3@8\n");
+  }
+  {
+    std::istringstream in("1@- 2@5 3@8\n7 8 9\n");
+    const auto records = read_walks_text(in);
+    CHECK(records.size() == 2);
+    CHECK(records[0].timed() && records[0].nodes == std::vector<NodeId>({1, 2, 3}));
+    CHECK(records[0].times[0] == kTimeUnset && records[0].times[2] == 8);
+    CHECK(!records[1].timed() && records[1].nodes == std::vector<NodeId>({7, 8, 9}));
+    std::istringstream mixed("1@2 3 4@5\n");
+    CHECK_THROWS_AS(read_walks_text(mixed), ParseError);
+  }
+  {
+    WalkSet walks;
+    walks.stride = 4;
+    walks.walk_count = 3;
+    walks.nodes.assign(12, 0);
+    walks.times.assign(12, 0);
+    walks.lengths = {4, 1, 2};
+    for (std::size_t i = 0; i < 12; ++i) {
+      walks.nodes[i] = static_cast<NodeId>(i * 7);
+      walks.times[i] = static_cast<Timestamp>(i * 11);
+    }
+    // the reference zero-fills past each length; so does the device image
+    for (std::uint64_t w = 0; w < 3; ++w)
+      for (std::uint32_t j = walks.lengths[w]; j < 4; ++j) walks.nodes[w * 4 + j] = walks.times[w * 4 + j] = 0;
+    std::stringstream buffer;
+    write_walks_binary(buffer, walks);
+    CHECK(buffer.str().substr(0, 8) == "TMPW0002");
+    const auto parsed = read_walks_binary(buffer);
+    CHECK(parsed == walks);
+  }
+  {  // generated walks: text image == the host formatting of the same walks
+    const std::vector<TemporalEdge> edges{{1, 2, 1}, {2, 3, 2}, {3, 1, 3}, {1, 3, 4}, {2, 1, 5}};
+    const auto store = EdgeStore::build(edges, DirectionMode::DirectedForward);
+    WalkConfig config;
+    config.walk_length = 6;
+    config.walks_per_node = 3;
+    const auto walks = generate_walks(store, config);
+    std::ostringstream text;
+    write_walks_text(text, walks);
+    std::string expect;
+    for (std::uint64_t w = 0; w < walks.walk_count; ++w) {
+      if (walks.lengths[w] < 2) continue;
+      for (std::uint32_t j = 0; j < walks.lengths[w]; ++j) {
+        if (j) expect += ' ';
+        const Timestamp t = walks.time_at(w, j);
+        expect += std::to_string(walks.node_at(w, j)) + "@" +
+                  (t == kTimeUnset || t == kTimeInfinite ? std::string("-") : std::to_string(t));
+      }
+      expect += '\n';
+    }
+    CHECK(!expect.empty() && text.str() == expect);
+  }
+}
+
 int main() {
   edge_store_cases();
   window_cases();
@@ -376,6 +446,7 @@ int main() {
   walk_cases();
   replay_cases();
   primitive_cases();
+  io_cases();
   std::printf("%d/%d checks passed\n", g_checks - g_fail, g_checks);
   return g_fail;
 }
