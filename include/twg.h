@@ -49,7 +49,8 @@ enum {
   TWG_ERANGE = 2,
   TWG_ELOGIC = 3,
   TWG_ECUDA = 4,
-  TWG_ENOMEM = 5
+  TWG_ENOMEM = 5,
+  TWG_EPARSE = 6  /* timewalk::ParseError (io.hpp:15-23): see *error_line */
 };
 
 /* types.hpp:28-34 — AoS, 24 bytes, layout-identical to timewalk::TemporalEdge */
@@ -275,6 +276,25 @@ int twg_walkset_audit(twg_walkset* w, twg_store* s, int direction, int strict, i
  * u32 lengths — byte-identical to the reference's writers. */
 int twg_walkset_text(twg_walkset* w, void* dst, uint64_t cap, uint64_t* len);
 int twg_walkset_binary(twg_walkset* w, void* dst, uint64_t cap, uint64_t* len);
+/* Edge lists on the device and the edge-file formats (io.cpp:40-69).
+ * twg_parse_edges_tsv: read_edges_tsv on the device — `source<TAB>target<TAB>
+ * timestamp` lines, '#' and blank lines skipped, a trailing '\r' dropped,
+ * non-negative int64 fields; text = host bytes (one H2D). A malformed line
+ * returns TWG_EPARSE with *error_line = its 1-based number and
+ * twg_last_error() = the reference's ParseError text without the
+ * " (line N)" suffix. The result stays on the device: count, AoS download,
+ * SoA device views (ready for twg_window_ingest_device; valid until
+ * destroy). twg_edges_format_tsv: write_edges_tsv on the device (*len =
+ * size; copied to dst when non-NULL, cap >= *len). */
+typedef struct twg_edges twg_edges;
+int twg_parse_edges_tsv(twg_ctx* ctx, const char* text, uint64_t bytes, twg_edges** out,
+                        uint64_t* error_line);
+int twg_edges_from_host(twg_ctx* ctx, const twg_edge* edges, uint64_t n, twg_edges** out);
+int twg_edges_info(twg_edges* e, uint64_t* count);
+int twg_edges_download(twg_edges* e, twg_edge* out);
+int twg_edges_device(twg_edges* e, int64_t** d_src, int64_t** d_dst, int64_t** d_t);
+int twg_edges_format_tsv(twg_edges* e, char* dst, uint64_t cap, uint64_t* len);
+int twg_edges_destroy(twg_edges* e);
 /* A device walk set from a host WalkSet image (walk_engine.hpp:55-70:
  * walk-major nodes/times [walk_count * stride], lengths [walk_count]) — the
  * façade's io over host WalkSets. */

@@ -424,6 +424,9 @@ class RefOracle:
         L.twref_walks_count.argtypes = [VP]
         L.twref_walks_copy.argtypes = [VP, VP, VP, VP]
         L.twref_walks_free.argtypes = [VP]
+        if hasattr(L, "twref_read_edges_tsv"):
+            L.twref_read_edges_tsv.argtypes = [VP, U64, VP, U64, C.POINTER(U64), C.POINTER(U64)]
+            L.twref_write_edges_tsv.argtypes = [VP, U64, VP, U64, C.POINTER(U64)]
         if hasattr(L, "twref_walks_serialize"):
             L.twref_walks_serialize.argtypes = [C.c_uint32, U64, VP, VP, VP, I, VP, U64, C.POINTER(U64)]
         L.twref_schedule_step.argtypes = [VP, VP, VP, U64, C.POINTER(ThresholdsC), VP, VP, U64]
@@ -586,6 +589,34 @@ class RefOracle:
         finally:
             self.L.twref_replay_free(h)
         return out
+
+    def read_edges_tsv(self, text: bytes):
+        """read_edges_tsv (io.cpp:40-63): (edges (n, 3) int64, None) or
+        (None, (line, what())) on a ParseError."""
+        buf = np.frombuffer(text, np.uint8) if text else np.zeros(1, np.uint8)
+        n, line = U64(), U64()
+        rc = self.L.twref_read_edges_tsv(_p(buf), len(text), None, 0, C.byref(n), C.byref(line))
+        if rc == 5:
+            return None, (line.value, self.L.twref_last_error().decode())
+        if rc:
+            self._err(rc)
+        out = np.zeros((max(n.value, 1), 3), np.int64)
+        rc = self.L.twref_read_edges_tsv(_p(buf), len(text), _p(out), n.value, C.byref(n), C.byref(line))
+        if rc:
+            self._err(rc)
+        return out[: n.value], None
+
+    def write_edges_tsv(self, edges) -> bytes:
+        e = edges_array(edges)
+        n = U64()
+        rc = self.L.twref_write_edges_tsv(_p(e), e.shape[0], None, 0, C.byref(n))
+        if rc:
+            self._err(rc)
+        buf = np.empty(max(n.value, 1), np.uint8)
+        rc = self.L.twref_write_edges_tsv(_p(e), e.shape[0], _p(buf), buf.size, C.byref(n))
+        if rc:
+            self._err(rc)
+        return buf[: n.value].tobytes()
 
     def serialize_walks(self, walks: dict, binary: bool) -> bytes:
         """The reference's write_walks_text / write_walks_binary (io.cpp:119-135, :173-183)."""

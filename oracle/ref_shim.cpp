@@ -416,6 +416,37 @@ void twref_walks_copy(void* h, int64_t* nodes, int64_t* times, uint32_t* lengths
 }
 void twref_walks_free(void* h) { delete static_cast<WalkSet*>(h); }
 
+// The reference's edge TSV reader / writer (io.cpp:40-69). read: *count
+// edges copied to out when cap allows; a ParseError returns 5 with its line
+// in *error_line and the full what() in twref_last_error().
+int twref_read_edges_tsv(const char* text, uint64_t bytes, twref_edge* out, uint64_t cap, uint64_t* count,
+                         uint64_t* error_line) {
+  *error_line = 0;
+  try {
+    std::istringstream in(std::string(text, bytes));
+    const auto edges = read_edges_tsv(in);
+    *count = edges.size();
+    if (out && cap >= edges.size()) std::memcpy(out, edges.data(), edges.size() * sizeof(TemporalEdge));
+    return 0;
+  } catch (const ParseError& e) {
+    g_error = e.what();
+    *error_line = e.line();
+    return 5;
+  } catch (const std::exception& e) {
+    return classify(e);
+  }
+}
+
+int twref_write_edges_tsv(const twref_edge* edges, uint64_t n, char* dst, uint64_t cap, uint64_t* len) {
+  return guarded([&] {
+    std::ostringstream out;
+    write_edges_tsv(out, std::span<const TemporalEdge>(reinterpret_cast<const TemporalEdge*>(edges), n));
+    const std::string b = out.str();
+    *len = b.size();
+    if (dst && cap >= b.size()) std::memcpy(dst, b.data(), b.size());
+  });
+}
+
 // The reference's walk writers (io.cpp:119-135 write_walks_text, :173-183
 // write_walks_binary) over a WalkSet image: *len = bytes; copied to dst when
 // dst != NULL and cap >= *len.

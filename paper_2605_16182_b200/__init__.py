@@ -11,6 +11,7 @@ from .timewalk import *  # noqa: F401,F403
 from .timewalk import (BatchRecord, BatchStats, BiasKind, Context, DirectionMode, EdgeStore,  # noqa: F401
                        LogicError, Node2VecParams, ReplayConfig, RngKind, StartMode, TierCounts,
                        TierThresholds, Variant, WalkConfig, WalkDirection, WalkSet, WalkStats, WindowManager,
-                       default_context, generate_walks, generate_walks_fullwalk, replay_stream, sample_start_edge)
+                       DeviceEdges, default_context, format_edges_tsv, generate_walks, generate_walks_fullwalk, ParseError,
+                       read_edges_tsv, replay_stream, sample_start_edge)
 
 _abi.load()

@@ -12,7 +12,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TWG_LIB_PATH") or os.path.join(_HERE, "lib", "libtimewalk_b200.so")  # override: A/B builds
 
-TWG_OK, TWG_EINVAL, TWG_ERANGE, TWG_ELOGIC, TWG_ECUDA, TWG_ENOMEM = range(6)
+TWG_OK, TWG_EINVAL, TWG_ERANGE, TWG_ELOGIC, TWG_ECUDA, TWG_ENOMEM, TWG_EPARSE = range(7)
 
 
 class twg_edge(C.Structure):
@@ -115,6 +115,13 @@ SIGNATURES = {
     "twg_walkset_text": (I, [VP, VP, U64, C.POINTER(U64)]),
     "twg_walkset_binary": (I, [VP, VP, U64, C.POINTER(U64)]),
     "twg_walkset_from_host": (I, [VP, C.c_uint32, U64, VP, VP, VP, PP]),
+    "twg_parse_edges_tsv": (I, [VP, VP, U64, PP, C.POINTER(U64)]),
+    "twg_edges_from_host": (I, [VP, VP, U64, PP]),
+    "twg_edges_info": (I, [VP, C.POINTER(U64)]),
+    "twg_edges_download": (I, [VP, VP]),
+    "twg_edges_device": (I, [VP, PP, PP, PP]),
+    "twg_edges_format_tsv": (I, [VP, VP, U64, C.POINTER(U64)]),
+    "twg_edges_destroy": (I, [VP]),
     "twg_walkset_device": (I, [VP, PP, PP, PP]),
     "twg_sample_start_edges": (I, [VP, I, VP, VP, U64, VP]),
     "twg_schedule_step": (I, [VP, VP, VP, U64, VP, VP, VP, U64, VP]),

@@ -25,6 +25,11 @@ struct twg_window {
 struct twg_walkset {
   WalkSetDev* w;
 };
+struct twg_edges {  // a device edge list (SoA columns)
+  twg::Ctx* c = nullptr;
+  twg::u64 n = 0;
+  twg::DevBuf<twg::i64> src, dst, t;
+};
 
 namespace {
 
@@ -613,6 +618,140 @@ int twg_walkset_binary(twg_walkset* w, void* dst, uint64_t cap, uint64_t* len) {
     if (count) TWG_CUDA(cudaMemcpyAsync(pl, x.lengths.p, 4 * count, cudaMemcpyDeviceToHost, c.stream));
     sync(c);
   });
+}
+
+}  // extern "C"
+
+namespace {
+
+// The reference's ParseError text for a bad line (io.cpp:14-22, :52-59):
+// re-derived on the host from the line's bytes and the device's verdict.
+std::string edge_line_message(const char* text, u64 bytes, u64 line, u8 kind) {
+  u64 b = 0;
+  for (u64 n = 1; n < line && b < bytes; ++b)
+    if (text[b] == '\n') ++n;
+  u64 e = b;
+  while (e < bytes && text[e] != '\n') ++e;
+  if (e > b && text[e - 1] == '\r') --e;
+  if (kind == kLineErrTabs) return "expected source<TAB>target<TAB>timestamp";
+  const std::string l(text + b, e - b);
+  const size_t t1 = l.find('\t'), t2 = l.find('\t', t1 + 1);
+  static const char* names[3] = {"source", "target", "timestamp"};
+  const int f = kind >= kLineErrNegative ? kind - kLineErrNegative : kind - kLineErrInvalid;
+  if (kind >= kLineErrNegative) return std::string("negative ") + names[f];
+  const std::string tok = f == 0 ? l.substr(0, t1) : f == 1 ? l.substr(t1 + 1, t2 - t1 - 1) : l.substr(t2 + 1);
+  return std::string("invalid ") + names[f] + " '" + tok + "'";
+}
+
+void parse_tsv(Ctx& c, const char* text, u64 bytes, DevBuf<i64>& s, DevBuf<i64>& d, DevBuf<i64>& t, u64* count,
+               uint64_t* error_line) {
+  u64 line = 0;
+  u8 kind = 0;
+  parse_edges_tsv(c, text, bytes, s, d, t, count, &line, &kind);
+  if (error_line) *error_line = line;
+  if (line) throw Error(TWG_EPARSE, edge_line_message(text, bytes, line, kind));
+}
+
+__global__ void k_unpack_edges(const twg_edge* in, u64 n, i64* s, i64* d, i64* t) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const twg_edge x = in[i];
+    s[i] = x.src;
+    d[i] = x.dst;
+    t[i] = x.t;
+  }
+}
+
+__global__ void k_pack_edges(const i64* s, const i64* d, const i64* t, u64 n, twg_edge* out) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<u64>(gridDim.x) * blockDim.x)
+    out[i] = twg_edge{s[i], d[i], t[i]};
+}
+
+}  // namespace
+
+extern "C" {
+
+int twg_parse_edges_tsv(twg_ctx* ctx, const char* text, uint64_t bytes, twg_edges** out, uint64_t* error_line) {
+  return guarded([&] {
+    require(out != nullptr && (bytes == 0 || text), "twg_parse_edges_tsv: arguments");
+    auto e = std::make_unique<twg_edges>();
+    e->c = &ctx->c;
+    parse_tsv(ctx->c, text, bytes, e->src, e->dst, e->t, &e->n, error_line);
+    *out = e.release();
+  });
+}
+
+int twg_edges_from_host(twg_ctx* ctx, const twg_edge* edges, uint64_t n, twg_edges** out) {
+  return guarded([&] {
+    require(out != nullptr && (n == 0 || edges), "twg_edges_from_host: arguments");
+    Ctx& c = ctx->c;
+    auto e = std::make_unique<twg_edges>();
+    e->c = &c;
+    e->n = n;
+    e->src.alloc(n ? n : 1, c.stream);
+    e->dst.alloc(n ? n : 1, c.stream);
+    e->t.alloc(n ? n : 1, c.stream);
+    if (n) {
+      DevBuf<twg_edge> aos(n, c.stream);
+      TWG_CUDA(cudaMemcpyAsync(aos.p, edges, n * sizeof(twg_edge), cudaMemcpyHostToDevice, c.stream));
+      k_unpack_edges<<<grid_for(n, 256, static_cast<unsigned>(c.sm_count) * 16), 256, 0, c.stream>>>(
+          aos.p, n, e->src.p, e->dst.p, e->t.p);
+      TWG_LAUNCHED(c);
+      sync(c);
+    }
+    *out = e.release();
+  });
+}
+
+int twg_edges_info(twg_edges* e, uint64_t* count) {
+  return guarded([&] {
+    require(count != nullptr, "twg_edges_info: count");
+    *count = e->n;
+  });
+}
+
+int twg_edges_download(twg_edges* e, twg_edge* out) {
+  return guarded([&] {
+    Ctx& c = *e->c;
+    if (!e->n) return;
+    require(out != nullptr, "twg_edges_download: out");
+    DevBuf<twg_edge> aos(e->n, c.stream);
+    k_pack_edges<<<grid_for(e->n, 256, static_cast<unsigned>(c.sm_count) * 16), 256, 0, c.stream>>>(
+        e->src.p, e->dst.p, e->t.p, e->n, aos.p);
+    TWG_LAUNCHED(c);
+    d2h(c, out, aos.p, e->n);
+    sync(c);
+  });
+}
+
+int twg_edges_device(twg_edges* e, int64_t** d_src, int64_t** d_dst, int64_t** d_t) {
+  return guarded([&] {
+    if (d_src) *d_src = e->src.p;
+    if (d_dst) *d_dst = e->dst.p;
+    if (d_t) *d_t = e->t.p;
+  });
+}
+
+int twg_edges_format_tsv(twg_edges* e, char* dst, uint64_t cap, uint64_t* len) {
+  return guarded([&] {
+    require(len != nullptr, "twg_edges_format_tsv: len");
+    Ctx& c = *e->c;
+    DevBuf<char> text;
+    u64 bytes = 0;
+    format_edges_tsv(c, e->src.p, e->dst.p, e->t.p, e->n, text, &bytes);
+    *len = bytes;
+    if (dst) {
+      require(cap >= bytes, "twg_edges_format_tsv: buffer too small");
+      if (bytes) d2h(c, dst, text.p, bytes);
+    }
+    sync(c);
+  });
+}
+
+int twg_edges_destroy(twg_edges* e) {
+  delete e;
+  return TWG_OK;
 }
 
 int twg_walkset_from_host(twg_ctx* ctx, uint32_t stride, uint64_t walk_count, const int64_t* nodes,

@@ -10,6 +10,7 @@
 #include <cstring>
 #include <fstream>
 #include <istream>
+#include <iterator>
 #include <ostream>
 #include <sstream>
 #include <vector>
@@ -769,6 +770,86 @@ std::vector<WalkRecord> read_walks(const std::string& path) {
     out.push_back(std::move(rec));
   }
   return out;
+}
+
+// ---- edge files (io.cpp:40-107): TSV on the device, binary as raw triples -----------
+
+std::vector<TemporalEdge> read_edges_tsv(std::istream& in) {
+  const std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  std::lock_guard<std::recursive_mutex> lk(api_mutex());
+  twg_edges* e = nullptr;
+  std::uint64_t line = 0;
+  const int rc = twg_parse_edges_tsv(ctx(), text.data(), text.size(), &e, &line);
+  if (rc == TWG_EPARSE) throw ParseError(twg_last_error(), line);
+  check(rc);
+  std::uint64_t n = 0;
+  std::vector<TemporalEdge> edges;
+  static_assert(sizeof(TemporalEdge) == sizeof(twg_edge));
+  int rc2 = twg_edges_info(e, &n);
+  if (rc2 == TWG_OK && n) {
+    edges.resize(n);
+    rc2 = twg_edges_download(e, reinterpret_cast<twg_edge*>(edges.data()));
+  }
+  twg_edges_destroy(e);
+  check(rc2);
+  return edges;
+}
+
+void write_edges_tsv(std::ostream& out, std::span<const TemporalEdge> edges) {
+  std::lock_guard<std::recursive_mutex> lk(api_mutex());
+  twg_edges* e = nullptr;
+  check(twg_edges_from_host(ctx(), reinterpret_cast<const twg_edge*>(edges.data()), edges.size(), &e));
+  std::uint64_t len = 0;
+  int rc = twg_edges_format_tsv(e, nullptr, 0, &len);
+  std::vector<char> bytes;
+  if (rc == TWG_OK) {
+    bytes.resize(len);
+    rc = twg_edges_format_tsv(e, bytes.data(), len, &len);
+  }
+  twg_edges_destroy(e);
+  check(rc);
+  out.write(bytes.data(), static_cast<std::streamsize>(bytes.size()));
+}
+
+std::vector<TemporalEdge> read_edges_binary(std::istream& in) {
+  char magic[8];
+  in.read(magic, sizeof(magic));
+  if (!in || std::memcmp(magic, kEdgeBinaryMagic, 8) != 0) throw std::runtime_error("edge binary: bad magic header");
+  const auto count = read_pod<std::uint64_t>(in);
+  std::vector<TemporalEdge> edges;
+  edges.reserve(count);
+  for (std::uint64_t i = 0; i < count; ++i) {
+    const auto s = read_pod<std::int64_t>(in);
+    const auto d = read_pod<std::int64_t>(in);
+    const auto t = read_pod<std::int64_t>(in);
+    edges.push_back({s, d, t});
+  }
+  return edges;
+}
+
+void write_edges_binary(std::ostream& out, std::span<const TemporalEdge> edges) {
+  out.write(kEdgeBinaryMagic, 8);
+  const std::uint64_t n = edges.size();
+  out.write(reinterpret_cast<const char*>(&n), sizeof(n));
+  out.write(reinterpret_cast<const char*>(edges.data()), static_cast<std::streamsize>(n * sizeof(TemporalEdge)));
+}
+
+std::vector<TemporalEdge> read_edges(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw std::runtime_error("cannot open " + path);
+  char magic[8] = {};
+  in.read(magic, sizeof(magic));
+  const bool binary = in.gcount() == 8 && std::memcmp(magic, kEdgeBinaryMagic, 8) == 0;
+  in.clear();
+  in.seekg(0);
+  return binary ? read_edges_binary(in) : read_edges_tsv(in);
+}
+
+void write_edges(const std::string& path, std::span<const TemporalEdge> edges, bool binary) {
+  std::ofstream out(path, std::ios::binary);
+  if (!out) throw std::runtime_error("cannot open " + path + " for writing");
+  if (binary) write_edges_binary(out, edges);
+  else write_edges_tsv(out, edges);
 }
 
 }  // namespace timewalk

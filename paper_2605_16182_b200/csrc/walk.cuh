@@ -62,6 +62,21 @@ u64 walks_binary_size(const WalkSetDev& w);
 void walks_from_host(Ctx& ctx, u32 stride, u64 count, const i64* nodes, const i64* times, const u32* lengths,
                      WalkSetDev& out);
 
+// edge files (edgeio.cu, io.cpp:40-69): TSV parse into device SoA columns
+// (count data lines; on a bad line: error_line 1-based + its kind, no
+// output) and TSV formatting of device edges
+enum : u8 {
+  kLineSkip = 0,
+  kLineEdge = 1,
+  kLineErrTabs = 2,
+  kLineErrInvalid = 3,   // + field (0 source, 1 target, 2 timestamp)
+  kLineErrNegative = 6,  // + field
+};
+void parse_edges_tsv(Ctx& ctx, const char* text, u64 bytes, DevBuf<i64>& src, DevBuf<i64>& dst, DevBuf<i64>& t,
+                     u64* count, u64* error_line, u8* error_kind);
+void format_edges_tsv(Ctx& ctx, const i64* src, const i64* dst, const i64* t, u64 n, DevBuf<char>& text,
+                      u64* bytes);
+
 // compact (CSR) image on the device: offsets[count+1], nodes/times[total]
 void compact_walks(Ctx& ctx, const WalkSetDev& w, DevBuf<u64>& offsets, DevBuf<i64>& nodes,
                    DevBuf<i64>& times, u64* total);

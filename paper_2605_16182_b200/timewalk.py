@@ -27,6 +27,14 @@ kExponentialExactLimit = 700
 kNode2VecMaxRetries = 64
 
 
+class ParseError(RuntimeError):
+    """timewalk::ParseError (io.hpp:15-23): message + 1-based line."""
+
+    def __init__(self, what: str, line: int):
+        super().__init__(f"{what} (line {line})")
+        self.line = line
+
+
 class LogicError(RuntimeError):
     """std::logic_error."""
 
@@ -93,6 +101,78 @@ def _call(name: str, *args) -> None:
 
 def _ptr(a: np.ndarray) -> C.c_void_p:
     return C.c_void_p(a.ctypes.data) if a.size else C.c_void_p(0)
+
+
+# --------------------------------------------------------------------------- edge files
+
+class DeviceEdges:
+    """A device edge list (twg_edges): the result of the device TSV parser or
+    an upload; SoA columns in HBM (``device()`` views feed
+    WindowManager.ingest_batch_device directly)."""
+
+    def __init__(self, handle: C.c_void_p):
+        self.handle = handle
+        n = C.c_uint64()
+        _call("twg_edges_info", handle, C.byref(n))
+        self.count = n.value
+
+    def __del__(self):
+        try:
+            if self.handle:
+                _abi.load().twg_edges_destroy(self.handle)
+        except Exception:
+            pass
+
+    @classmethod
+    def parse_tsv(cls, text: bytes, ctx: Optional["Context"] = None) -> "DeviceEdges":
+        """read_edges_tsv (io.cpp:40-63) on the device. Raises ParseError like the reference."""
+        ctx = ctx or default_context()
+        buf = np.frombuffer(text, np.uint8) if text else np.zeros(1, np.uint8)
+        h, line = C.c_void_p(), C.c_uint64()
+        lib = _abi.load()
+        rc = lib.twg_parse_edges_tsv(ctx.handle, _ptr(buf), len(text), C.byref(h), C.byref(line))
+        if rc == _abi.TWG_EPARSE:
+            raise ParseError((lib.twg_last_error() or b"").decode(), line.value)
+        if rc:
+            _raise(rc)
+        return cls(h)
+
+    @classmethod
+    def from_array(cls, edges, ctx: Optional["Context"] = None) -> "DeviceEdges":
+        ctx = ctx or default_context()
+        e = np.ascontiguousarray(np.asarray(edges, np.int64)).reshape(-1, 3)
+        h = C.c_void_p()
+        _call("twg_edges_from_host", ctx.handle, _ptr(e), e.shape[0], C.byref(h))
+        return cls(h)
+
+    def to_array(self) -> np.ndarray:
+        out = np.zeros((max(self.count, 1), 3), np.int64)
+        _call("twg_edges_download", self.handle, _ptr(out))
+        return out[: self.count]
+
+    def device(self):
+        """(d_src, d_dst, d_t) device pointers (ints), valid while this object lives."""
+        s, d, t = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        _call("twg_edges_device", self.handle, C.byref(s), C.byref(d), C.byref(t))
+        return s.value, d.value, t.value
+
+    def to_tsv(self) -> bytes:
+        """write_edges_tsv (io.cpp:65-69), formatted on the device."""
+        n = C.c_uint64()
+        _call("twg_edges_format_tsv", self.handle, None, 0, C.byref(n))
+        buf = np.empty(max(n.value, 1), np.uint8)
+        _call("twg_edges_format_tsv", self.handle, _ptr(buf), buf.size, C.byref(n))
+        return buf[: n.value].tobytes()
+
+
+def read_edges_tsv(text: bytes, ctx: Optional["Context"] = None) -> np.ndarray:
+    """read_edges_tsv (io.cpp:40-63), parsed on the device: (n, 3) int64."""
+    return DeviceEdges.parse_tsv(text, ctx).to_array()
+
+
+def format_edges_tsv(edges, ctx: Optional["Context"] = None) -> bytes:
+    """write_edges_tsv (io.cpp:65-69), formatted on the device."""
+    return DeviceEdges.from_array(edges, ctx).to_tsv()
 
 
 # --------------------------------------------------------------------------- context

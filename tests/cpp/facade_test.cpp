@@ -372,6 +372,51 @@ static void primitive_cases() {
   CHECK((ex == std::vector<std::uint64_t>{0, 3, 4, 8, 9}));
 }
 
+// test_io.cpp:12-60 — edge files (TSV on the device)
+void edge_io_cases() {
+  {
+    std::istringstream in("# temporal edges\n1\t2\t10\n\n3\t4\t20\n");
+    const auto edges = read_edges_tsv(in);
+    CHECK(edges.size() == 2);
+    CHECK(edges.size() == 2 && edges[0] == (TemporalEdge{1, 2, 10}) && edges[1] == (TemporalEdge{3, 4, 20}));
+    std::ostringstream out;
+    write_edges_tsv(out, edges);
+    CHECK(out.str() == "1\t2\t10\n3\t4\t20\n");
+  }
+  {
+    std::istringstream missing("1\t2\t3\n4\t5\n");
+    bool ok = false;
+    try {
+      read_edges_tsv(missing);
+    } catch (const ParseError& e) {
+      ok = std::string(e.what()) == "expected source<TAB>target<TAB>timestamp (line 2)" && e.line() == 2;
+    }
+    CHECK(ok);
+    std::istringstream garbage("1\t2\tbogus\n");
+    CHECK_THROWS_AS(read_edges_tsv(garbage), ParseError);
+    std::istringstream negative("1\t2\t-5\n");
+    CHECK_THROWS_AS(read_edges_tsv(negative), ParseError);
+    std::size_t line = 0;
+    try {
+      std::istringstream bad("# ok\n1\t2\t3\nx\ty\tz\n");
+      read_edges_tsv(bad);
+    } catch (const ParseError& e) {
+      line = e.line();
+    }
+    CHECK(line == 3);
+  }
+  {
+    std::vector<TemporalEdge> edges;
+    for (std::int64_t i = 0; i < 500; ++i) edges.push_back({(i * 7) % 50, (i * 13) % 50, i * 3});
+    std::stringstream buffer;
+    write_edges_binary(buffer, edges);
+    CHECK(buffer.str().substr(0, 8) == "TMPW0001");
+    CHECK(read_edges_binary(buffer) == edges);
+    std::istringstream corrupt("XXXX0001payload");
+    CHECK_THROWS_AS(read_edges_binary(corrupt), std::runtime_error);
+  }
+}
+
 // test_io.cpp:62-108 — walk writers (device) and readers
 void io_cases() {
   {
@@ -446,6 +491,7 @@ int main() {
   walk_cases();
   replay_cases();
   primitive_cases();
+  edge_io_cases();
   io_cases();
   std::printf("%d/%d checks passed\n", g_checks - g_fail, g_checks);
   return g_fail;
