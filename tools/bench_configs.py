@@ -72,7 +72,7 @@ if "C2" in only:
     g = co.gen_uniform(100000, 1000000, 1000000, 1)
     g = g[np.argsort(g[:, 2], kind="stable")]
     bounds = tw.split_batches(g[:, 2], 100000)
-    for name in ("exp_weight", "exp_index"):
+    for name in ("exp_weight", "exp_index", "exp_weight"):  # the first pass also warms the pools
         w = tw.WindowManager(333333, ctx=ctx)
         ing = wk = hops = 0.0
         for k, (a, b) in enumerate(bounds):
