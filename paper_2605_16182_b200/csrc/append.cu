@@ -178,6 +178,7 @@ struct OwnerIn {
     return e;
   }
   __device__ __forceinline__ bool has_val() const { return true; }
+  __device__ __forceinline__ void prefetch_val(u64) const {}  // the key's record load brings it
 };
 
 // bucket b = owner >> 8 of the bucket-sorted entries starts at bstart[b]
@@ -410,6 +411,11 @@ __global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs a) {
     __syncthreads();
     // item i = warp*R*32 + r*32 + lane of the chunk belongs to this lane in round r
     u32 dk[kChunkItems];
+#pragma unroll
+    for (int r = 0; r < kChunkItems; ++r) {  // the payloads' DRAM fetch starts now, into L2
+      const u32 i = warp * (32 * kChunkItems) + r * 32 + lane;
+      if (i < n) prefetch_l2(a.vals + c0 + i);
+    }
 #pragma unroll
     for (int r = 0; r < kChunkItems; ++r) {
       const u32 i = warp * (32 * kChunkItems) + r * 32 + lane;

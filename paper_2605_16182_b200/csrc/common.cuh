@@ -48,6 +48,9 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
     (ctx).launches++;     \
   } while (0)
 
+// start the DRAM fetch of the line holding p into L2 (no register, no wait)
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 struct Ctx {
   int device = 0;
   int sm_count = 148;

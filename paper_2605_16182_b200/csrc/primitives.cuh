@@ -154,6 +154,9 @@ struct ArrayIn {
   __device__ __forceinline__ K key(u64 i) const { return k[i]; }
   __device__ __forceinline__ V val(u64 i) const { return v[i]; }
   __device__ __forceinline__ bool has_val() const { return v != nullptr; }
+  __device__ __forceinline__ void prefetch_val(u64 i) const {
+    if (v) prefetch_l2(v + i);
+  }
 };
 
 // ---------------------------------------------------- single-pass scan ----
@@ -465,6 +468,11 @@ __global__ void __launch_bounds__(kSortBlock) k_radix_onesweep(In in, K* __restr
   const u32 wbase = static_cast<u32>(warp) * (32 * kItems);
   K key[kItems];
   u32 rank[kItems];
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {  // the payloads' DRAM fetch starts now, into L2
+    const u32 i = wbase + j * 32 + lane;
+    if (i < tile_n) in.prefetch_val(base + i);
+  }
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
     const u32 i = wbase + j * 32 + lane;
