@@ -167,6 +167,18 @@ struct ArrayIn {
 // and hands every item (index, exclusive prefix, flag) to the scatter
 // functor. Replaces the three-kernel chains (tile sums, rescan, scatter)
 // that read the input twice. The grand total lands in *total.
+// look-back status words: relaxed GPU-scope atomics (the word carries flag and
+// value together, nothing else is published through it), not volatile
+// accesses, which compile to system-scope strong loads
+__device__ __forceinline__ u64 lb_load(const u64* p) {
+  u64 v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void lb_store(u64* p, u64 v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 constexpr u64 kLbAggregate = 1ull << 62;
 constexpr u64 kLbInclusive = 2ull << 62;
 constexpr u64 kLbValueMask = (1ull << 62) - 1;
@@ -215,19 +227,19 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_scatter(FlagFn flag, u64 n,
   const u32 agg = s_warp[kScanBlock / 32];
   if (warp == 0) {
     // warp-parallel decoupled look-back: 32 predecessors per round
-    volatile u64* st = tile_state;
+    u64* st = tile_state;
     u64 prefix = 0;
     if (tile == 0) {
-      if (lane == 0) st[0] = kLbInclusive | agg;
+      if (lane == 0) lb_store(st, kLbInclusive | agg);
     } else {
-      if (lane == 0) st[tile] = kLbAggregate | agg;
+      if (lane == 0) lb_store(st + tile, kLbAggregate | agg);
       long long p = static_cast<long long>(tile) - 1;
       while (true) {
         const long long idx = p - lane;
         u64 s = kLbInclusive;  // before tile 0: inclusive zero
         if (idx >= 0) {
           do {
-            s = st[idx];
+            s = lb_load(st + idx);
           } while ((s >> 62) == 0);
         }
         const u32 incl = __ballot_sync(0xffffffffu, (s >> 62) == 2);
@@ -238,7 +250,7 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_scatter(FlagFn flag, u64 n,
         if (incl) break;
         p -= 32;
       }
-      if (lane == 0) st[tile] = kLbInclusive | (prefix + agg);
+      if (lane == 0) lb_store(st + tile, kLbInclusive | (prefix + agg));
     }
     if (lane == 0) {
       s_prefix = prefix;
@@ -491,32 +503,19 @@ __global__ void __launch_bounds__(kSortBlock) k_radix_onesweep(In in, K* __restr
     rank[j] = before + __popc(peers & lt);
   }
   __syncthreads();
-  {  // thread d: digit d's count in this tile, its look-back, its tile start
-    const int d = threadIdx.x;
-    u32 acc = 0;
+  // thread d: digit d's count in this tile, posted at once (successors wait
+  // on it); the tile is staged in shared memory BEFORE this tile's own look-
+  // back, so the predecessors get that long to post theirs
+  const int d = threadIdx.x;
+  u32 acc = 0;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-      const u32 c = sm.wcount[w][d];
-      sm.wcount[w][d] = acc;
-      acc += c;
-    }
-    volatile u64* st = state;
-    u64 excl = 0;
-    if (tile == 0) {
-      st[d] = kLbInclusive | acc;
-    } else {
-      st[tile * kRadix + d] = kLbAggregate | acc;
-      for (u64 j = tile - 1;; --j) {
-        u64 s;
-        do {
-          s = st[j * kRadix + d];
-        } while ((s >> 62) == 0);
-        excl += s & kLbValueMask;
-        if ((s >> 62) == 2) break;
-      }
-      st[tile * kRadix + d] = kLbInclusive | (excl + acc);
-    }
-    sm.gstart[d] = digit_start[d] + excl;
+  for (int w = 0; w < kWarps; ++w) {
+    const u32 c = sm.wcount[w][d];
+    sm.wcount[w][d] = acc;
+    acc += c;
+  }
+  lb_store(state + tile * kRadix + d, (tile == 0 ? kLbInclusive : kLbAggregate) | acc);
+  {
     u32 total;
     sm.tile_start[d] = block_excl_scan<u32>(acc, &total);
   }
@@ -525,11 +524,34 @@ __global__ void __launch_bounds__(kSortBlock) k_radix_onesweep(In in, K* __restr
   for (int j = 0; j < kItems; ++j) {  // stage in digit order; payloads loaded only now
     const u32 i = wbase + j * 32 + lane;
     if (i < tile_n) {
-      const u32 d = digit_of(key[j], shift);
-      const u32 pos = sm.tile_start[d] + sm.wcount[warp][d] + rank[j];
+      const u32 dg = digit_of(key[j], shift);
+      const u32 pos = sm.tile_start[dg] + sm.wcount[warp][dg] + rank[j];
       sm.keys[pos] = key[j];
       if (has_val) sm.vals[pos] = in.val(base + i);
     }
+  }
+  {
+    u64 excl = 0;
+    if (tile > 0) {
+      // four predecessors per round: their words are requested together
+      long long j = static_cast<long long>(tile) - 1;
+      bool done = false;
+      while (!done) {
+        u64 st4[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) st4[q] = j - q >= 0 ? lb_load(state + (j - q) * kRadix + d) : kLbInclusive;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (done) break;
+          while ((st4[q] >> 62) == 0) st4[q] = lb_load(state + (j - q) * kRadix + d);
+          excl += st4[q] & kLbValueMask;
+          done = (st4[q] >> 62) == 2;
+        }
+        j -= 4;
+      }
+      lb_store(state + tile * kRadix + d, kLbInclusive | (excl + acc));
+    }
+    sm.gstart[d] = digit_start[d] + excl;
   }
   __syncthreads();
 #pragma unroll
