@@ -394,7 +394,11 @@ __global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs a) {
   const bool valid = v < a.V;
   const u32 bs = a.bstart[bkt], be = a.bstart[bkt + 1];
   NodeMeta p{};
-  if (valid) p = a.plan[v];
+  i64 lt_v = 0;
+  if (valid) {  // independent loads, in flight together
+    p = a.plan[v];
+    if (a.last_t) lt_v = a.last_t[v];
+  }
   sm.cur[t] = p.ee;
   sm.gcur[t] = p.ge;
   sm.base[t] = p.base;
@@ -403,7 +407,7 @@ __global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs a) {
   sm.gorg[t] = p.gorg;
   const bool has = valid && a.last_t && p.ee > p.eb && be > bs;
   sm.has_last[t] = has ? 1u : 0u;
-  sm.last_t[t] = has ? a.last_t[v] : 0;
+  sm.last_t[t] = has ? lt_v : 0;
 
   const u32 lt = (1u << lane) - 1u;
   for (u32 c0 = bs; c0 < be; c0 += kChunk) {
