@@ -1,0 +1,1 @@
+for l in "$@"; do echo $l; TWG_LIB_PATH=$PWD/$l timeout 300 python tools/bench_configs.py C3 2>/dev/null | grep walks; done

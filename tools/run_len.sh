@@ -1,0 +1,1 @@
+for l in "$@"; do echo $l; TWG_LIB_PATH=$PWD/$l timeout 300 python tools/diag_walk_len.py 2>&1 | grep "L="; done
