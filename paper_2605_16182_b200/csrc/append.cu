@@ -538,8 +538,7 @@ __global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs a) {
     a.nm_new[v] = r;
     q = r.ge - r.gb;
   }
-  for (int o2 = 16; o2 > 0; o2 >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o2);
-  if (lane == 0 && q) atomicAdd(reinterpret_cast<unsigned long long*>(a.q_total), q);
+  block_atomic_add(reinterpret_cast<unsigned long long*>(a.q_total), q);
 }
 
 bool append_enabled() {

@@ -43,6 +43,23 @@ __device__ __forceinline__ u32 digit_peers(u32 d, bool valid) {
   return m;
 }
 
+// One atomicAdd per block of the block's sum (every thread of the block must
+// call it): per-warp atomics on one word serialise at L2 when a large grid
+// finishes at once.
+__device__ __forceinline__ void block_atomic_add(unsigned long long* dst, u64 v) {
+  __shared__ u64 s_part[32];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  if (lane == 0) s_part[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    u64 x = lane < nw ? s_part[lane] : 0ull;
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0 && x) atomicAdd(dst, static_cast<unsigned long long>(x));
+  }
+  __syncthreads();  // s_part may be reused by a second call
+}
+
 // ---------------------------------------------------------------- scan ----
 
 template <class T>

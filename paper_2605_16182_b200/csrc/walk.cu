@@ -478,18 +478,6 @@ __device__ __forceinline__ void init_walk(const WalkParams& P, const InitParams&
 }
 
 // stats[0] walks, [1] hops, [2] max hops (fullwalk steps), [3] ambiguous, [4] algorithmic bytes
-__device__ __forceinline__ void add_counters(u64* stats, const Ctr& cn) {
-  u64 a = cn.amb, b = cn.bytes;
-  for (int o = 16; o > 0; o >>= 1) {
-    a += __shfl_xor_sync(0xffffffffu, a, o);
-    b += __shfl_xor_sync(0xffffffffu, b, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    if (a) atomicAdd(reinterpret_cast<unsigned long long*>(&stats[3]), a);
-    if (b) atomicAdd(reinterpret_cast<unsigned long long*>(&stats[4]), b);
-  }
-}
-
 
 // add_stats with one atomic per counter per BLOCK (every thread of the block
 // calls it): per-warp atomics on the same five words serialise at L2 and
@@ -759,8 +747,7 @@ __global__ void k_coop_count(StateArrays S, u64 count, u32* ncnt, u8* first, u64
       ++a;
     }
   }
-  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-  if ((threadIdx.x & 31) == 0 && a) atomicAdd(reinterpret_cast<unsigned long long*>(alive), a);
+  block_atomic_add(reinterpret_cast<unsigned long long*>(alive), a);
 }
 
 // solo walks hop now; the others are compacted into (node, walk) pairs.
