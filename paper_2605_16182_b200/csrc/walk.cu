@@ -665,36 +665,62 @@ struct TaskLists {
 
 // Classify runs on the dispatch plane (walk_engine.cpp:314-343).
 __global__ void k_classify(const u32* keys, u64 n, StoreView s, twg_thresholds th, TaskLists T) {
-  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<u64>(gridDim.x) * blockDim.x) {
-    if (!(i == 0 || keys[i] != keys[i - 1])) continue;
-    // run [i, end): galloping search for the first j > i with keys[j] != keys[i]
-    const u32 v = keys[i];
-    u64 lo = i + 1, step = 1, hi = i + 1;
-    while (hi < n && keys[hi] == v) {
-      lo = hi + 1;
-      hi = i + 1 + step;
-      step <<= 1;
+  const u32 lane = threadIdx.x & 31;
+  const u64 stride = static_cast<u64>(gridDim.x) * blockDim.x;
+  // warp-uniform loop: the list slots are allocated per warp and tier (one
+  // atomic per tier present in the warp, not one per task)
+  for (u64 i0 = blockIdx.x * static_cast<u64>(blockDim.x) + (threadIdx.x & ~31u); i0 < n; i0 += stride) {
+    const u64 i = i0 + lane;
+    const bool act = i < n && (i == 0 || keys[i] != keys[i - 1]);
+    u32 v = 0, W = 0, pieces = 1;
+    u64 end = i;
+    int tier = -1;
+    if (act) {
+      // run [i, end): galloping search for the first j > i with keys[j] != keys[i]
+      v = keys[i];
+      u64 lo = i + 1, step = 1, hi = i + 1;
+      while (hi < n && keys[hi] == v) {
+        lo = hi + 1;
+        hi = i + 1 + step;
+        step <<= 1;
+      }
+      if (hi > n) hi = n;
+      while (lo < hi) {  // first j in [lo, hi) with keys[j] != v
+        const u64 mid = (lo + hi) >> 1;
+        if (keys[mid] == v) lo = mid + 1;
+        else hi = mid;
+      }
+      end = lo;
+      W = static_cast<u32>(end - i);
+      const NodeMeta nv = s.nm[v];
+      const u32 G = nv.ge - nv.gb;
+      if (W < th.w_warp) tier = 0;
+      else if (W <= th.block_dim) tier = G <= th.g_warp_cap ? 1 : 2;
+      else {
+        tier = G <= th.g_block_cap ? 3 : 4;
+        if (W > th.w_max) pieces = (W + th.w_max - 1) / th.w_max;
+      }
     }
-    if (hi > n) hi = n;
-    while (lo < hi) {  // first j in [lo, hi) with keys[j] != v
-      const u64 mid = (lo + hi) >> 1;
-      if (keys[mid] == v) lo = mid + 1;
-      else hi = mid;
+    u32 slot = 0;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const bool mine = tier == k;
+      const u32 m = __ballot_sync(0xffffffffu, mine);
+      if (!m) continue;
+      u32 incl = mine ? pieces : 0u;  // inclusive scan of the pieces over the lanes
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 x = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= static_cast<u32>(o)) incl += x;
+      }
+      const u32 total = __shfl_sync(0xffffffffu, incl, 31);
+      const int leader = __ffs(m) - 1;
+      u32 base = 0;
+      if (static_cast<int>(lane) == leader) base = atomicAdd(&T.count[k], total);
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (mine) slot = base + incl - pieces;
     }
-    const u64 end = lo;
-    const u32 W = static_cast<u32>(end - i);
-    const NodeMeta nv = s.nm[v];
-    const u32 G = nv.ge - nv.gb;
-    int tier;
-    u32 pieces = 1;
-    if (W < th.w_warp) tier = 0;
-    else if (W <= th.block_dim) tier = G <= th.g_warp_cap ? 1 : 2;
-    else {
-      tier = G <= th.g_block_cap ? 3 : 4;
-      if (W > th.w_max) pieces = (W + th.w_max - 1) / th.w_max;
-    }
-    const u32 slot = atomicAdd(&T.count[tier], pieces);
+    if (!act) continue;
     if (pieces > 1) atomicAdd(&T.count[tier == 3 ? 5 : 6], pieces);
     for (u32 p = 0; p < pieces; ++p) {
       Task task;
@@ -826,6 +852,7 @@ __global__ void k_coop_count(StateArrays S, u64 count, u32* ncnt, u8* first, u64
 __global__ void __launch_bounds__(kBlock) k_coop_solo(WalkParams P, StateArrays S, u64 count, const u32* ncnt,
                                                      const u8* first, u32 w_warp, u32* hub_keys, u32* hub_vals,
                                                      u64* scal, u64* stats) {
+  __shared__ u32 s_hub[kBlock / 32], s_solo[kBlock / 32], s_base;
   Ctr cn{0, 0};
   const u32 lane = threadIdx.x & 31;
   for (u64 b = blockIdx.x * static_cast<u64>(blockDim.x); b < count; b += static_cast<u64>(gridDim.x) * blockDim.x) {
@@ -846,14 +873,31 @@ __global__ void __launch_bounds__(kBlock) k_coop_solo(WalkParams P, StateArrays 
         hub = true;
       }
     }
+    // hub-list slots: one atomic per block (per-warp atomics on one word
+    // serialise at L2), warps ordered inside the block
     const u32 hb = __ballot_sync(0xffffffffu, hub), sb = __ballot_sync(0xffffffffu, solo_task);
-    u32 base = 0;
+    const u32 warp = threadIdx.x >> 5;
     if (lane == 0) {
-      if (hb) base = static_cast<u32>(atomicAdd(reinterpret_cast<unsigned long long*>(&scal[0]),
-                                                static_cast<unsigned long long>(__popc(hb))));
-      if (sb) atomicAdd(reinterpret_cast<unsigned long long*>(&scal[1]), static_cast<unsigned long long>(__popc(sb)));
+      s_hub[warp] = __popc(hb);
+      s_solo[warp] = __popc(sb);
     }
-    base = __shfl_sync(0xffffffffu, base, 0);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      u32 h = 0, so = 0;
+      for (int q = 0; q < kBlock / 32; ++q) {
+        const u32 c = s_hub[q];
+        s_hub[q] = h;
+        h += c;
+        so += s_solo[q];
+      }
+      s_base = h ? static_cast<u32>(atomicAdd(reinterpret_cast<unsigned long long*>(&scal[0]),
+                                              static_cast<unsigned long long>(h)))
+                 : 0u;
+      if (so) atomicAdd(reinterpret_cast<unsigned long long*>(&scal[1]), static_cast<unsigned long long>(so));
+    }
+    __syncthreads();
+    const u32 base = s_base + s_hub[warp];
+    __syncthreads();  // s_hub / s_base are rewritten next round
     if (hub) {
       const u32 k = base + __popc(hb & ((1u << lane) - 1u));
       hub_keys[k] = node;
