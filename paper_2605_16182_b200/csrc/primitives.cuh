@@ -60,6 +60,24 @@ __device__ __forceinline__ void block_atomic_add(unsigned long long* dst, u64 v)
   __syncthreads();  // s_part may be reused by a second call
 }
 
+// Block-wide reduction of one u64 (op: 0 add, 1 max, 2 min, 3 or); the
+// result is valid in thread 0. Every thread of the block must call it.
+template <int kOp>
+__device__ __forceinline__ u64 block_reduce_u64(u64 v) {
+  __shared__ u64 s_red[32];
+  auto f = [](u64 a, u64 b) { return kOp == 0 ? a + b : kOp == 1 ? (a > b ? a : b) : kOp == 2 ? (a < b ? a : b) : (a | b); };
+  for (int o = 16; o > 0; o >>= 1) v = f(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  if (lane == 0) s_red[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    v = lane < nw ? s_red[lane] : s_red[0];
+    for (int o = 16; o > 0; o >>= 1) v = f(v, __shfl_xor_sync(0xffffffffu, v, o));
+  }
+  __syncthreads();
+  return v;
+}
+
 // ---------------------------------------------------------------- scan ----
 
 template <class T>

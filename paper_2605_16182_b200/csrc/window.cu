@@ -90,19 +90,20 @@ __global__ void k_batch_stats(const i64* bs, const i64* bd, const i64* bt, u64 n
       rec[wr(static_cast<u32>(lo + rank))] = EdgeRec{static_cast<u32>(a), static_cast<u32>(b), t};
     }
   }
-  for (int o = 16; o > 0; o >>= 1) {
-    mt = max(mt, __shfl_xor_sync(0xffffffffu, mt, o));
-    lt = min(lt, __shfl_xor_sync(0xffffffffu, lt, o));
-    mid = max(mid, __shfl_xor_sync(0xffffffffu, mid, o));
-    shape |= __shfl_xor_sync(0xffffffffu, shape, o);
-    neg |= __shfl_xor_sync(0xffffffffu, neg, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    atomicMax(reinterpret_cast<long long*>(&scal[0]), static_cast<long long>(mt));
-    atomicMin(reinterpret_cast<long long*>(&scal[8]), static_cast<long long>(lt));
-    atomicMax(reinterpret_cast<unsigned long long*>(&scal[1]), mid);
-    if (shape) atomicOr(reinterpret_cast<unsigned long long*>(&scal[7]), static_cast<u64>(shape));
-    if (neg) atomicOr(reinterpret_cast<unsigned long long*>(&scal[9]), 1ull);
+  // one set of atomics per block (the whole grid finishes at once: per-warp
+  // atomics on these words would serialise at L2); signed times through the
+  // order-preserving flip of the sign bit
+  const u64 kSign = 1ull << 63;
+  const u64 bmt = block_reduce_u64<1>(static_cast<u64>(mt) ^ kSign);
+  const u64 blt = block_reduce_u64<2>(static_cast<u64>(lt) ^ kSign);
+  const u64 bmid = block_reduce_u64<1>(mid);
+  const u64 bflags = block_reduce_u64<3>(static_cast<u64>(shape) | (static_cast<u64>(neg) << 32));
+  if (threadIdx.x == 0) {
+    atomicMax(reinterpret_cast<long long*>(&scal[0]), static_cast<long long>(bmt ^ kSign));
+    atomicMin(reinterpret_cast<long long*>(&scal[8]), static_cast<long long>(blt ^ kSign));
+    atomicMax(reinterpret_cast<unsigned long long*>(&scal[1]), bmid);
+    if (bflags & 0xffffffffull) atomicOr(reinterpret_cast<unsigned long long*>(&scal[7]), bflags & 0xffffffffull);
+    if (bflags >> 32) atomicOr(reinterpret_cast<unsigned long long*>(&scal[9]), 1ull);
   }
 }
 
