@@ -835,31 +835,66 @@ __global__ void __launch_bounds__(kBlock) k_tier_block(WalkParams P, StateArrays
 // with W >= w_warp (the warp / block tiers) are compacted and sorted by node.
 // Outputs are identical (every draw is keyed by (walk, hop)); tier counts are
 // the reference's (one solo task per distinct solo node).
-__global__ void k_coop_count(StateArrays S, u64 count, u32* ncnt, u8* first, u64* alive) {
-  u64 a = 0;
-  for (u64 w = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; w < count;
-       w += static_cast<u64>(gridDim.x) * blockDim.x) {
-    if (S.flags[w] & 1u) {
-      first[w] = atomicAdd(ncnt + S.cur[w], 1u) == 0 ? 1 : 0;
-      ++a;
+// Alg. 1 step start over the alive list: alive walks per node (the run
+// lengths W), and the alive walks appended to the next list (one atomic per
+// block; list order is free: the hub list is sorted by node, solo-task
+// counting only needs one `first` per node)
+__global__ void k_coop_count(StateArrays S, const u32* ids, const u64* n_ids, u32* ncnt, u8* first, u64* alive,
+                             u32* next) {
+  __shared__ u32 s_cnt[kBlock / 32], s_base;
+  const u64 n = *n_ids;
+  const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (u64 b = blockIdx.x * static_cast<u64>(blockDim.x); b < n; b += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const u64 k = b + threadIdx.x;
+    u32 w = 0;
+    bool al = false;
+    if (k < n) {
+      w = ids[k];
+      al = (S.flags[w] & 1u) != 0;
+      if (al) first[w] = atomicAdd(ncnt + S.cur[w], 1u) == 0 ? 1 : 0;
     }
+    const u32 m = __ballot_sync(0xffffffffu, al);
+    if (lane == 0) s_cnt[warp] = __popc(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      u32 acc = 0;
+      for (int q = 0; q < kBlock / 32; ++q) {
+        const u32 c = s_cnt[q];
+        s_cnt[q] = acc;
+        acc += c;
+      }
+      s_base = acc ? static_cast<u32>(atomicAdd(reinterpret_cast<unsigned long long*>(alive),
+                                                static_cast<unsigned long long>(acc)))
+                   : 0u;
+    }
+    __syncthreads();
+    if (al) next[s_base + s_cnt[warp] + __popc(m & ((1u << lane) - 1u))] = w;
+    __syncthreads();
   }
-  block_atomic_add(reinterpret_cast<unsigned long long*>(alive), a);
+}
+
+__global__ void k_iota(u32* ids, u64 n, u64* n_out) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<u64>(gridDim.x) * blockDim.x)
+    ids[i] = static_cast<u32>(i);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *n_out = n;
 }
 
 // solo walks hop now; the others are compacted into (node, walk) pairs.
 // scal: [0] hub walks, [1] solo tasks (distinct solo nodes)
-__global__ void __launch_bounds__(kBlock) k_coop_solo(WalkParams P, StateArrays S, u64 count, const u32* ncnt,
-                                                     const u8* first, u32 w_warp, u32* hub_keys, u32* hub_vals,
-                                                     u64* scal, u64* stats) {
+__global__ void __launch_bounds__(kBlock) k_coop_solo(WalkParams P, StateArrays S, const u32* ids, const u64* n_ids,
+                                                     const u32* ncnt, const u8* first, u32 w_warp, u32* hub_keys,
+                                                     u32* hub_vals, u64* scal, u64* stats) {
   __shared__ u32 s_hub[kBlock / 32], s_solo[kBlock / 32], s_base;
   Ctr cn{0, 0};
   const u32 lane = threadIdx.x & 31;
+  const u64 count = *n_ids;  // the alive list of this step
   for (u64 b = blockIdx.x * static_cast<u64>(blockDim.x); b < count; b += static_cast<u64>(gridDim.x) * blockDim.x) {
-    const u64 w = b + threadIdx.x;
+    const u64 kk = b + threadIdx.x;
+    const u32 w = kk < count ? ids[kk] : 0u;
     bool hub = false, solo_task = false;
     u32 node = 0;
-    if (w < count && (S.flags[w] & 1u)) {
+    if (kk < count) {
       node = S.cur[w];
       if (ncnt[node] < w_warp) {
         solo_task = first[w] != 0;
@@ -1285,20 +1320,31 @@ WalkSetDev* generate_walks(Ctx& ctx, Store& s_in, const twg_walk_config& cfg, co
                                     static_cast<int>(block_smem)));
     DevBuf<u32> ncnt(s.V ? s.V : 1, st);
     DevBuf<u8> first(count, st);
-    u64* sc2 = ctx.d_scalars + 48;  // [48] alive, [49] hub walks, [50] solo tasks
+    // the alive list, compacted every step so a step costs O(alive walks)
+    DevBuf<u32> ids0(count ? count : 1, st), ids1(count ? count : 1, st);
+    u32* ids_cur = ids0.p;
+    u32* ids_next = ids1.p;
+    u64* sc2 = ctx.d_scalars + 48;  // [48] alive (next list size), [49] hub walks, [50] solo tasks, [51] list size
+    u64* n_cur = sc2 + 3;
+    k_iota<<<grid(ctx, count), kBlock, 0, st>>>(ids_cur, count, n_cur);
+    TWG_LAUNCHED(ctx);
+    u64 n_alive = count;
     while (true) {
-      // 1. alive walks per current node (the run lengths W)
+      // 1. alive walks per current node (the run lengths W), alive list compacted
       TWG_CUDA(cudaMemsetAsync(ncnt.p, 0, ncnt.bytes(), st));
       TWG_CUDA(cudaMemsetAsync(sc2, 0, 3 * sizeof(u64), st));
-      k_coop_count<<<grid(ctx, count), kBlock, 0, st>>>(S, count, ncnt.p, first.p, sc2);
+      k_coop_count<<<grid(ctx, n_alive), kBlock, 0, st>>>(S, ids_cur, n_cur, ncnt.p, first.p, sc2, ids_next);
       TWG_LAUNCHED(ctx);
       // 2. solo tier (W < w_warp): hop per walk; the rest compacted as (node, walk)
-      k_coop_solo<<<grid(ctx, count), kBlock, 0, st>>>(P, S, count, ncnt.p, first.p, th.w_warp, k0.p, v0.p, sc2 + 1,
-                                                        stats.p);
+      k_coop_solo<<<grid(ctx, n_alive), kBlock, 0, st>>>(P, S, ids_next, sc2, ncnt.p, first.p, th.w_warp, k0.p, v0.p,
+                                                          sc2 + 1, stats.p);
       TWG_LAUNCHED(ctx);
       u64 sc[3];
       read_scalars(ctx, sc2, sc, 3);
       if (sc[0] == 0) break;
+      n_alive = sc[0];
+      std::swap(ids_cur, ids_next);
+      TWG_CUDA(cudaMemcpyAsync(n_cur, sc2, sizeof(u64), cudaMemcpyDeviceToDevice, st));
       ++coop_steps;
       tiers[0] += sc[2];
       const u64 n = sc[1];
