@@ -75,10 +75,12 @@ struct BatchGroupFn {
   const EdgeRec* b;
   Ring br;                     // batch index -> slot of b
   const i64* last_survivor_t;  // null when there are no survivors
+  const i64* bt;               // the batch's time column in batch order, when at hand (8 B/edge, not 16)
+  __device__ __forceinline__ i64 time(u64 k) const { return bt ? bt[k] : b[br(static_cast<u32>(k))].t; }
   __device__ __forceinline__ u32 operator()(u64 k) const {
-    const i64 tk = b[br(static_cast<u32>(k))].t;
+    const i64 tk = time(k);
     if (k == 0) return last_survivor_t ? (tk != *last_survivor_t ? 1u : 0u) : 1u;
-    return tk != b[br(static_cast<u32>(k - 1))].t ? 1u : 0u;
+    return tk != time(k - 1) ? 1u : 0u;
   }
 };
 
@@ -91,11 +93,12 @@ struct BatchGroupScatter {
   u64 cap;                // ring slots
   u32* ts_off;
   i64* ts_time;
+  const i64* bt;
   __device__ __forceinline__ void operator()(u64 k, u64 g, u32 f) const {
     if (!f) return;
     const u64 z = ((zbase_dev ? *zbase_dev : zbase) + g) % cap;
     ts_off[z] = seq_b + static_cast<u32>(k);
-    ts_time[z] = b[br(static_cast<u32>(k))].t;
+    ts_time[z] = bt ? bt[k] : b[br(static_cast<u32>(k))].t;
   }
 };
 
@@ -574,7 +577,7 @@ bool append_log_slot(const Store& O, const Store* R, u64 A, Ring* wr) {
 }
 
 Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const EdgeRec* batch, Ring bring, u64 A,
-                     u64 from, i64 cutoff, bool no_ties, bool in_log, bool check_dead) {
+                     u64 from, i64 cutoff, bool no_ties, bool in_log, bool check_dead, const i64* bt) {
   Ctx& ctx = *w.ctx;
   cudaStream_t st = ctx.stream;
   PhaseTimer pt(ctx, "ingest_append");
@@ -635,8 +638,8 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
   const Rec* brec = log->rec.p;  // batch edge k at log slot wr(k) from here on
   const i64* last_surv = nullptr;  // the last survivor's time: the first batch group merges with it on a tie
   if (S) last_surv = O.gapped ? &O.e_rec.p[(O.log_first + O.m - 1) % O.log->cap].t : O.e_t.p + (O.m - 1);
-  scan_scatter(ctx, BatchGroupFn{brec, wr, last_surv}, A, sc + 5,
-               BatchGroupScatter{brec, wr, seq_b, zbase, zbase_dev, log->cap, log->ts_off.p, log->ts_time.p});
+  scan_scatter(ctx, BatchGroupFn{brec, wr, last_surv, bt}, A, sc + 5,
+               BatchGroupScatter{brec, wr, seq_b, zbase, zbase_dev, log->cap, log->ts_off.p, log->ts_time.p, bt});
   pt.mark("log+ts");
 
   // 2. batch entries grouped into 256-node buckets: stable radix sort of

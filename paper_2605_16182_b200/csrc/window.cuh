@@ -40,7 +40,8 @@ bool append_log_slot(const Store& O, const Store* R, u64 A, Ring* wr);
 // side is merged here and the ingest returns null (nothing published) when an
 // old node would leave the window.
 Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const EdgeRec* batch, Ring bring, u64 A,
-                     u64 from, i64 cutoff, bool no_ties, bool in_log = false, bool check_dead = false);
+                     u64 from, i64 cutoff, bool no_ties, bool in_log = false, bool check_dead = false,
+                     const i64* bt = nullptr);
 
 Window* window_create(Ctx& ctx, i64 duration, int mode, BuildOpts opts);
 void window_destroy(Window* w);
