@@ -182,6 +182,15 @@ struct OwnerIn {
   }
   __device__ __forceinline__ bool has_val() const { return true; }
   __device__ __forceinline__ void prefetch_val(u64) const {}  // the key's record load brings it
+  // the same multiset of keys from the batch's own id columns (input order,
+  // 8 B per item instead of a 16-B record) when they are at hand
+  const i64* bs = nullptr;
+  const i64* bd = nullptr;
+  __device__ __forceinline__ u32 hist_key(u64 j) const {
+    if (!bs) return key(j);
+    if (mode == TWG_UNDIRECTED) return static_cast<u32>((j & 1) ? bd[j >> 1] : bs[j >> 1]);
+    return static_cast<u32>(mode == TWG_BACKWARD ? bd[j] : bs[j]);
+  }
 };
 
 // bucket b = owner >> 8 of the bucket-sorted entries starts at bstart[b]
@@ -577,7 +586,8 @@ bool append_log_slot(const Store& O, const Store* R, u64 A, Ring* wr) {
 }
 
 Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const EdgeRec* batch, Ring bring, u64 A,
-                     u64 from, i64 cutoff, bool no_ties, bool in_log, bool check_dead, const i64* bt) {
+                     u64 from, i64 cutoff, bool no_ties, bool in_log, bool check_dead, const i64* bt,
+                     const i64* const* bcols) {
   Ctx& ctx = *w.ctx;
   cudaStream_t st = ctx.stream;
   PhaseTimer pt(ctx, "ingest_append");
@@ -654,7 +664,10 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
   Entry* vp = v0.p;
   Entry* va = v1.p;
   if (vb > static_cast<int>(kBucketShift)) {  // the first pass builds (owner, entry) from the log records
-    radix_sort_pairs_from<u32, Entry>(ctx, OwnerIn{brec, wr, mode, seq_b}, &kp, &ka, &vp, &va, Yn, vb,
+    OwnerIn oin{brec, wr, mode, seq_b};
+    oin.bs = bcols ? bcols[0] : nullptr;
+    oin.bd = bcols ? bcols[1] : nullptr;
+    radix_sort_pairs_from<u32, Entry>(ctx, oin, &kp, &ka, &vp, &va, Yn, vb,
                                       kBucketShift);
   } else {
     k_owner_keys<<<grid(ctx, Yn), kBlock, 0, st>>>(brec, wr, A, mode, seq_b, kp, vp);

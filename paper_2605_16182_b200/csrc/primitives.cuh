@@ -192,6 +192,7 @@ struct ArrayIn {
   __device__ __forceinline__ void prefetch_val(u64 i) const {
     if (v) prefetch_l2(v + i);
   }
+  __device__ __forceinline__ K hist_key(u64 i) const { return k[i]; }
 };
 
 // ---------------------------------------------------- single-pass scan ----
@@ -458,7 +459,7 @@ __global__ void __launch_bounds__(kSortBlock) k_radix_global_hist(In in, u64 n, 
   __syncthreads();
   for (u64 i = blockIdx.x * static_cast<u64>(kSortBlock) + threadIdx.x; i < n;
        i += static_cast<u64>(gridDim.x) * kSortBlock) {
-    const K k = in.key(i);
+    const K k = in.hist_key(i);  // any item order will do for counts
     for (int p = 0; p < passes; ++p) atomicAdd(&h[p][digit_of(k, lo_bit + p * kRadixBits)], 1u);
   }
   __syncthreads();

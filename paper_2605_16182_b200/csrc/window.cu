@@ -57,6 +57,7 @@ struct FastSpec {
   EdgeRec* rec = nullptr;
   u64 from = 0;
   const i64* bt = nullptr;  // the batch's time column (device): equals the canonical order's times
+  const i64* cols[2] = {nullptr, nullptr};  // its source / target columns (input order)
 };
 
 // scal[8]: batch min t, scal[9]: some id negative.
@@ -936,7 +937,8 @@ Store* ingest_fast(Window& w, FastSpec& spec, u64 n, const u64* sc, i64 cutoff, 
   stats->dropped_late = 0;
   w.max_ext = static_cast<i64>(V - 1);
   Store* out =
-      ingest_append(w, O, std::move(s), spec.rec, spec.wring, n, from, cutoff, true, spec.in_log, true, spec.bt);
+      ingest_append(w, O, std::move(s), spec.rec, spec.wring, n, from, cutoff, true, spec.in_log, true, spec.bt,
+                    spec.cols);
   if (!out) {  // an old node leaves the window: the general route recomputes everything
     stats->evicted = stats->dropped_late = 0;
     return nullptr;
@@ -1000,6 +1002,8 @@ void window_ingest(Window& w, const i64* d_src, const i64* d_dst, const i64* d_t
   FastSpec spec;
   spec.on = append_ingest_enabled() && old.m > 0 && old.V > 0 && old.ext_identity && n < 0xffffffffull / 2;
   spec.bt = d_t;
+  spec.cols[0] = d_src;
+  spec.cols[1] = d_dst;
   if (spec.on) {
     spec.in_log = append_log_slot(old, w.previous, n, &spec.wring);
     if (!spec.in_log) {

@@ -41,7 +41,7 @@ bool append_log_slot(const Store& O, const Store* R, u64 A, Ring* wr);
 // old node would leave the window.
 Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const EdgeRec* batch, Ring bring, u64 A,
                      u64 from, i64 cutoff, bool no_ties, bool in_log = false, bool check_dead = false,
-                     const i64* bt = nullptr);
+                     const i64* bt = nullptr, const i64* const* bcols = nullptr);
 
 Window* window_create(Ctx& ctx, i64 duration, int mode, BuildOpts opts);
 void window_destroy(Window* w);
