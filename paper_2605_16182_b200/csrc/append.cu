@@ -307,7 +307,10 @@ __global__ void __launch_bounds__(kBlock) k_plan(PlanArgs a) {
       // evicted whole: eviction is by time), so one search over the marks
       // gives both bounds
       gb = evict_lb([&](u32 x) { return a.omt[omr(x)]; }, o.gb, o.ge, a.cutoff);
-      eb = gb == o.ge ? o.ee : a.oms[omr(gb)];
+      // a ring whose groups are single entries (distinct times: the common
+      // case) maps mark k to entry k, so the mark's start needs no load
+      if (o.ge - o.gb == o.ee - o.eb) eb = o.eb + (gb - o.gb);
+      else eb = gb == o.ge ? o.ee : a.oms[omr(gb)];
       u32 low = o.eb;
       if (a.rnm) {
         const NodeMeta r = a.rnm[v];
