@@ -151,8 +151,9 @@ __device__ __forceinline__ void causal_slice(const i64* mt, const u32* ms, Ring 
 // after 2 estimates it bisects. A first hop from a sampled start (t
 // anywhere in the window) costs about two atoms instead of a bisection's
 // five or six; later hops (t near the newest times) land on the run's end.
-template <u32 kPer, class Key>
+template <u32 kPer, bool kLower = false, class Key>
 __device__ __forceinline__ u32 interp_ub(Key key, Ring er, u32 lo, u32 hi, i64 t, i64 tl, i64 th) {
+  // kLower: lower_bound (first key >= t, backward walks) instead of upper_bound
   u32 a = lo, b = hi;
   i64 ta = tl, tb = th;  // times just before a / at b (anchors of the estimate)
   for (int round = 0; b - a > kScan; ++round) {
@@ -171,7 +172,7 @@ __device__ __forceinline__ u32 interp_ub(Key key, Ring er, u32 lo, u32 hi, i64 t
       const u32 pos = x - k + j;
       if (pos >= a && pos < b) {  // in-run keys only (memory-safe: the run is allocated)
         const i64 v = key(er(pos));
-        if (v <= t) {
+        if (kLower ? v < t : v <= t) {
           a = pos + 1;
           ta = v;
         } else {
@@ -184,7 +185,7 @@ __device__ __forceinline__ u32 interp_ub(Key key, Ring er, u32 lo, u32 hi, i64 t
   u32 n = 0;
 #pragma unroll
   for (u32 i = 0; i < kScan; ++i)
-    if (a + i < b) n += key(er(a + i)) <= t ? 1u : 0u;
+    if (a + i < b) n += (kLower ? key(er(a + i)) < t : key(er(a + i)) <= t) ? 1u : 0u;
   return a + n;
 }
 
@@ -399,28 +400,45 @@ __device__ __forceinline__ bool hop(const WalkParams& P, u64 wl, WalkReg& r, con
     // mostly distinct times: search the entries themselves — the first entry
     // later than t IS the first entry of the first later group, so the mark
     // start lookup disappears (one fewer random sector per hop)
+    // interpolate when the answer is far from where the walk direction
+    // usually finds it (forward: the run's end, backward: its start)
     bool interp = false;
-    if (P.dir == 0 && th > tl && r.t >= tl && hi - lo > 16u) {  // t far from the run's end: interpolate
+    if (th > tl && r.t >= tl && r.t <= th && hi - lo > 16u) {
       const double f = static_cast<double>(r.t - tl) / static_cast<double>(th - tl);
-      interp = f * static_cast<double>(hi - lo) + 12.0 < static_cast<double>(hi - lo);
+      const double n = static_cast<double>(hi - lo);
+      interp = P.dir == 0 ? f * n + 12.0 < n : f * n > 12.0;
     }
     if (interp) {
       const Entry* ent = P.s.ent;
-      c = interp_ub<4>([ent](u32 p) { return ent[p].t; }, er, lo, hi, r.t, tl, th);
-      e = hi;
+      const auto key = [ent](u32 p) { return ent[p].t; };
+      if (P.dir == 0) {
+        c = interp_ub<4>(key, er, lo, hi, r.t, tl, th);
+        e = hi;
+      } else {
+        c = lo;
+        e = interp_ub<4, true>(key, er, lo, hi, r.t, tl, th);
+      }
     } else {
       causal_slice_entries(P.s.ent, er, lo, hi, r.t, P.dir, c, e);
     }
   } else {
     bool interp = false;  // the same choice over the marks (8 per atom)
-    if (P.dir == 0 && th > tl && r.t >= tl && ghi - glo > 16u) {
+    if (th > tl && r.t >= tl && r.t <= th && ghi - glo > 16u) {
       const double f = static_cast<double>(r.t - tl) / static_cast<double>(th - tl);
-      interp = f * static_cast<double>(ghi - glo) + 12.0 < static_cast<double>(ghi - glo);
+      const double n = static_cast<double>(ghi - glo);
+      interp = P.dir == 0 ? f * n + 12.0 < n : f * n > 12.0;
     }
     if (interp) {
-      const u32 g = interp_ub<8>([mt](u32 p) { return mt[p]; }, mr, glo, ghi, r.t, tl, th);
-      c = g == ghi ? hi : ms[mr(g)];
-      e = hi;
+      const auto key = [mt](u32 p) { return mt[p]; };
+      if (P.dir == 0) {
+        const u32 g = interp_ub<8>(key, mr, glo, ghi, r.t, tl, th);
+        c = g == ghi ? hi : ms[mr(g)];
+        e = hi;
+      } else {
+        const u32 g = interp_ub<8, true>(key, mr, glo, ghi, r.t, tl, th);
+        c = lo;
+        e = g == ghi ? hi : ms[mr(g)];
+      }
     } else {
       causal_slice(mt, ms, mr, glo, ghi, lo, hi, r.t, P.dir, c, e);
     }

@@ -453,3 +453,22 @@ def test_replay_parity(tw, co):
                 ei["ingested"], ei["dropped_late"], ei["evicted"], ei["retained"])
             assert r.walk.hops == ew["hops"]
             assert_walks(w, ex)
+
+
+@pytest.mark.parametrize("mode,direction", [(0, 0), (1, 1), (2, 0), (2, 1)])
+@pytest.mark.parametrize("t_max", [1000000, 400])
+def test_walks_long_runs_bit_exact(tw, co, mode, direction, t_max):
+    """Runs of ~200 entries per node (the interpolation search over the
+    entries, t_max large: distinct times) and heavily tied runs (the marks,
+    t_max small), both walk directions, sampled and per-node starts."""
+    g = co.gen_uniform(200, 40000, t_max, 5)
+    store = tw.EdgeStore.build(g, tw.DirectionMode(mode))
+    for bias in (0, 2):
+        for start_mode in (0, 1):
+            cfg = Cfg(walk_length=20, start_mode=start_mode, walks_per_node=5, total_walks=4000, bias=bias,
+                      seed=13, direction=direction)
+            exp, es = co.generate(g, mode, cfg, variant=0)
+            st = tw.WalkStats()
+            ws = tw.generate_walks(store, to_cfg(tw, cfg), variant=tw.Variant.FullWalk, stats=st)
+            assert_walks(ws, exp)
+            assert (st.walks, st.hops) == (es["walks"], es["hops"])
