@@ -23,6 +23,7 @@
 
 #include "timewalk/edge_store.hpp"
 #include "timewalk/io.hpp"
+#include "timewalk/validity.hpp"
 #include "timewalk/primitives.hpp"
 #include "timewalk/replay.hpp"
 #include "timewalk/samplers.hpp"
@@ -850,6 +851,133 @@ void write_edges(const std::string& path, std::span<const TemporalEdge> edges, b
   if (!out) throw std::runtime_error("cannot open " + path + " for writing");
   if (binary) write_edges_binary(out, edges);
   else write_edges_tsv(out, edges);
+}
+
+// ---- walk validity (validity.cpp) ---------------------------------------------------
+
+EdgeOracle::EdgeOracle(std::span<const TemporalEdge> edges, bool undirected)
+    : store_(std::make_shared<EdgeStore>(
+          EdgeStore::build(edges, undirected ? DirectionMode::Undirected : DirectionMode::DirectedForward,
+                           BuildOptions{false, false}))) {}
+
+const std::vector<Timestamp>* EdgeOracle::find(NodeId a, NodeId b) const {
+  if (!store_) return nullptr;
+  std::lock_guard<std::mutex> lk(cache_->mu);
+  const auto key = std::make_pair(a, b);
+  if (auto it = cache_->hit.find(key); it != cache_->hit.end()) return &it->second;
+  if (cache_->miss.count(key)) return nullptr;
+  // a's node-view region holds its out-edges (forward) or both orientations
+  // (undirected: a self-loop twice, as the reference's map gets it), time-sorted
+  const auto ia = store_->find_node(a), ib = store_->find_node(b);
+  std::vector<Timestamp> times;
+  if (ia && ib) {
+    const auto [lo, hi] = store_->node_region(*ia);
+    for (std::size_t p = lo; p < hi; ++p)
+      if (store_->ref_neighbor(p, *ia) == *ib) times.push_back(store_->ref_time(p));
+  }
+  if (times.empty()) {
+    cache_->miss.insert(key);
+    return nullptr;
+  }
+  return &cache_->hit.emplace(key, std::move(times)).first->second;
+}
+
+bool EdgeOracle::contains(NodeId a, NodeId b, Timestamp t) const {
+  const auto* times = find(a, b);
+  return times && std::binary_search(times->begin(), times->end(), t);
+}
+
+WalkCheckResult check_timed_walk(std::span<const NodeId> nodes, std::span<const Timestamp> times,
+                                 const EdgeOracle& oracle, WalkDirection direction, bool strict) {
+  WalkCheckResult r;
+  if (nodes.size() < 2) return r;  // no hop: vacuously valid
+  const bool fwd = direction == WalkDirection::Forward;
+  r.hops = nodes.size() - 1;
+  r.hop_valid.assign(r.hops, false);
+  for (std::size_t j = 0; j < r.hops; ++j) {
+    const Timestamp tp = times[j], th = times[j + 1];
+    // backward hops traverse the stored edge target -> source
+    const bool edge = fwd ? oracle.contains(nodes[j], nodes[j + 1], th) : oracle.contains(nodes[j + 1], nodes[j], th);
+    const bool order = (j == 0 && (tp == kTimeUnset || tp == kTimeInfinite)) ||
+                       (fwd ? (strict ? th > tp : th >= tp) : (strict ? th < tp : th <= tp));
+    if (edge && order) {
+      r.hop_valid[j] = true;
+      ++r.valid_hops;
+    } else if (!r.first_violation) {
+      r.first_violation = j;
+    }
+  }
+  r.valid = r.valid_hops == r.hops;
+  return r;
+}
+
+WalkCheckResult check_untimed_walk_greedy(std::span<const NodeId> nodes, const EdgeOracle& oracle, bool strict) {
+  WalkCheckResult r;
+  if (nodes.size() < 2) return r;
+  r.hops = nodes.size() - 1;
+  r.hop_valid.assign(r.hops, false);
+  Timestamp at = kTimeUnset;  // earliest feasible assignment so far
+  for (std::size_t j = 0; j < r.hops; ++j) {
+    const auto* c = oracle.find(nodes[j], nodes[j + 1]);
+    auto it = c ? (strict ? std::upper_bound(c->begin(), c->end(), at) : std::lower_bound(c->begin(), c->end(), at))
+                : std::vector<Timestamp>::const_iterator{};
+    if (!c || it == c->end()) {
+      r.first_violation = j;  // greedy-earliest failing proves infeasibility: later hops unreachable
+      break;
+    }
+    at = *it;
+    r.hop_valid[j] = true;
+    ++r.valid_hops;
+  }
+  r.valid = r.valid_hops == r.hops;
+  return r;
+}
+
+ValidityReport summarize(std::span<const WalkCheckResult> results) {
+  ValidityReport rep;
+  rep.total_walks = results.size();
+  rep.first_violation_per_walk.reserve(results.size());
+  for (const WalkCheckResult& r : results) {
+    rep.total_hops += r.hops;
+    rep.valid_hops += r.valid_hops;
+    rep.valid_walks += r.valid ? 1 : 0;
+    rep.first_violation_per_walk.push_back(r.first_violation);
+  }
+  return rep;
+}
+
+ValidityReport check_walkset(const WalkSet& walks, const EdgeOracle& oracle, WalkDirection direction, bool strict) {
+  ValidityReport rep;
+  std::vector<std::int64_t> first(walks.walk_count ? walks.walk_count : 1, -1);
+  twg_audit_report r{};
+  if (oracle.store()) {
+    std::lock_guard<std::recursive_mutex> lk(api_mutex());
+    twg_walkset* w = nullptr;
+    check(twg_walkset_from_host(ctx(), walks.stride, walks.walk_count, walks.nodes.data(), walks.times.data(),
+                                walks.lengths.data(), &w));
+    const int rc = twg_walkset_audit(w, oracle.store()->device_handle(), static_cast<int>(direction), strict ? 1 : 0,
+                                     first.data(), &r);
+    twg_walkset_destroy(w);
+    check(rc);
+  } else {  // an empty oracle holds no edge: every emitted walk fails at hop 0
+    for (std::uint64_t i = 0; i < walks.walk_count; ++i) {
+      if (walks.lengths[i] < 2) continue;
+      ++r.walks;
+      r.hops += walks.lengths[i] - 1;
+      first[i] = 0;
+    }
+  }
+  rep.total_walks = r.walks;
+  rep.valid_walks = r.valid_walks;
+  rep.total_hops = r.hops;
+  rep.valid_hops = r.valid_hops;
+  rep.first_violation_per_walk.reserve(r.walks);
+  for (std::uint64_t i = 0; i < walks.walk_count; ++i) {
+    if (walks.lengths[i] < 2) continue;  // skipped, as the writers do
+    rep.first_violation_per_walk.push_back(first[i] < 0 ? std::nullopt
+                                                        : std::optional<std::size_t>(static_cast<std::size_t>(first[i])));
+  }
+  return rep;
 }
 
 }  // namespace timewalk

@@ -5,7 +5,10 @@
 // test_walk_engine.cpp, test_replay.cpp, test_primitives.cpp); each block
 // cites the test it follows. Exit code = number of failed checks.
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
+#include <optional>
+#include <span>
 #include <numeric>
 #include <set>
 #include <stdexcept>
@@ -18,6 +21,7 @@
 #include "timewalk/replay.hpp"
 #include "timewalk/rng.hpp"
 #include "timewalk/samplers.hpp"
+#include "timewalk/validity.hpp"
 #include "timewalk/walk_engine.hpp"
 #include "timewalk/window_manager.hpp"
 
@@ -484,6 +488,111 @@ void io_cases() {
   }
 }
 
+// test_validity.cpp:34-190 — the auditor (check_walkset on the GPU)
+void validity_cases() {
+  const std::vector<TemporalEdge> edges{{1, 2, 1}, {2, 3, 2}};
+  const EdgeOracle oracle(edges, false);
+  {
+    const std::vector<NodeId> n{1};
+    const std::vector<Timestamp> t{0};
+    const auto r = check_timed_walk(n, t, oracle);
+    CHECK(r.valid && r.hops == 0);
+  }
+  {
+    const std::vector<NodeId> n{1, 2, 3};
+    const std::vector<Timestamp> t{0, 1, 2};
+    const auto r = check_timed_walk(n, t, oracle);
+    CHECK(r.valid && r.valid_hops == 2);
+  }
+  {
+    const std::vector<TemporalEdge> tied{{1, 2, 1}, {2, 3, 1}};
+    const EdgeOracle tied_oracle(tied, false);
+    const std::vector<NodeId> n{1, 2, 3};
+    const std::vector<Timestamp> t{0, 1, 1};
+    const auto r = check_timed_walk(n, t, tied_oracle);
+    CHECK(!r.valid && r.valid_hops == 1 && r.first_violation == std::optional<std::size_t>(1));
+    CHECK(check_timed_walk(n, t, tied_oracle, WalkDirection::Forward, false).valid);
+  }
+  {
+    const std::vector<NodeId> n{1, 3};
+    const std::vector<Timestamp> t{0, 2};
+    CHECK(!check_timed_walk(n, t, oracle).valid);
+    const std::vector<NodeId> m{1, 2};
+    const std::vector<Timestamp> u{kTimeUnset, 1};
+    CHECK(check_timed_walk(m, u, oracle).valid);
+  }
+  {  // backward walks traverse stored edges in reverse
+    const std::vector<TemporalEdge> chain{{1, 2, 5}, {3, 1, 2}};
+    const EdgeOracle o(chain, false);
+    const std::vector<NodeId> n{2, 1, 3};
+    const std::vector<Timestamp> t{kTimeInfinite, 5, 2}, rising{kTimeInfinite, 2, 5};
+    CHECK(check_timed_walk(n, t, o, WalkDirection::Backward).valid);
+    CHECK(!check_timed_walk(n, rising, o, WalkDirection::Backward).valid);
+  }
+  {  // greedy untimed
+    const std::vector<TemporalEdge> e1{{1, 2, 1}, {1, 2, 5}, {2, 3, 3}, {2, 3, 7}};
+    const std::vector<NodeId> n{1, 2, 3};
+    CHECK(check_untimed_walk_greedy(n, EdgeOracle(e1, false)).valid);
+    const std::vector<TemporalEdge> e2{{1, 2, 5}, {2, 3, 3}};
+    const auto r = check_untimed_walk_greedy(n, EdgeOracle(e2, false));
+    CHECK(!r.valid && r.first_violation == std::optional<std::size_t>(1));
+    const std::vector<NodeId> single{4};
+    CHECK(check_untimed_walk_greedy(single, EdgeOracle({}, false)).valid);
+  }
+  {  // summarize
+    std::vector<WalkCheckResult> res(10);
+    for (auto& r : res) {
+      r.hops = 80;
+      r.valid_hops = 1;
+      r.valid = false;
+      r.first_violation = 0;
+    }
+    const auto rep = summarize(res);
+    CHECK(rep.walk_percent() == 0.0 && std::abs(rep.hop_percent() - 1.25) < 1e-12);
+    CHECK(rep.first_violation_per_walk.size() == 10 && summarize({}).walk_percent() == 100.0);
+  }
+  {  // undirected oracles accept either orientation
+    const std::vector<TemporalEdge> e{{1, 2, 3}};
+    CHECK(!EdgeOracle(e, false).contains(2, 1, 3));
+    CHECK(EdgeOracle(e, true).contains(2, 1, 3) && EdgeOracle(e, true).contains(1, 2, 3));
+    const EdgeOracle u(e, true);
+    const auto* times = u.find(1, 2);
+    CHECK(times && times->size() == 1 && (*times)[0] == 3);
+  }
+  {  // engine output audits clean end to end (the GPU check_walkset)
+    std::vector<TemporalEdge> graph;
+    for (std::int64_t i = 0; i < 4000; ++i) graph.push_back({(i * 37) % 60, (i * 101 + 7) % 60, (i * 13) % 500});
+    const auto store = EdgeStore::build(graph, DirectionMode::DirectedForward);
+    WalkConfig config;
+    config.walk_length = 16;
+    config.walks_per_node = 4;
+    const auto walks = generate_walks(store, config);
+    const EdgeOracle o(graph, false);
+    const auto rep = check_walkset(walks, o);
+    CHECK(rep.total_walks > 0 && rep.hop_percent() == 100.0 && rep.walk_percent() == 100.0);
+    // the same walks against an oracle missing every edge of node 0: the GPU
+    // audit agrees hop for hop with the single-walk rules
+    std::vector<TemporalEdge> fewer;
+    for (const auto& e : graph)
+      if (e.source != 0) fewer.push_back(e);
+    const EdgeOracle of(fewer, false);
+    const auto bad = check_walkset(walks, of);
+    std::vector<WalkCheckResult> host;
+    for (std::uint64_t w = 0; w < walks.walk_count; ++w) {
+      if (walks.lengths[w] < 2) continue;
+      host.push_back(check_timed_walk(std::span<const NodeId>(walks.nodes.data() + w * walks.stride, walks.lengths[w]),
+                                      std::span<const Timestamp>(walks.times.data() + w * walks.stride,
+                                                                 walks.lengths[w]),
+                                      of));
+    }
+    const auto ref = summarize(host);
+    CHECK(bad.valid_hops < bad.total_hops);
+    CHECK(bad.total_walks == ref.total_walks && bad.valid_walks == ref.valid_walks &&
+          bad.total_hops == ref.total_hops && bad.valid_hops == ref.valid_hops &&
+          bad.first_violation_per_walk == ref.first_violation_per_walk);
+  }
+}
+
 int main() {
   edge_store_cases();
   window_cases();
@@ -493,6 +602,7 @@ int main() {
   primitive_cases();
   edge_io_cases();
   io_cases();
+  validity_cases();
   std::printf("%d/%d checks passed\n", g_checks - g_fail, g_checks);
   return g_fail;
 }
