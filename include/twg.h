@@ -362,6 +362,13 @@ int twg_synth_stream_host(uint64_t nodes, uint64_t first, uint64_t count, uint64
 /* Same law generated directly into device SoA arrays on the ctx stream. */
 int twg_synth_stream_device(twg_ctx* ctx, uint64_t nodes, uint64_t first, uint64_t count,
                             uint64_t seed, int64_t* d_src, int64_t* d_dst, int64_t* d_t);
+/* The reference's synthetic graphs (synthetic.hpp:10-35) into host AoS
+ * edges, bit-identical: kind 0 make_uniform_graph(a nodes, b edges, t_max),
+ * 1 make_hub_skewed_graph(a background nodes, b background edges),
+ * 2 make_mega_hub_graph(a feeders), 3 make_time_ladder_graph(a edges, b
+ * rungs). *count = the edge count; out (cap >= *count) may be NULL. */
+int twg_synth_graph(twg_ctx* ctx, int kind, uint64_t a, uint64_t b, int64_t t_max, uint64_t seed,
+                    twg_edge* out, uint64_t cap, uint64_t* count);
 /* make_uniform_graph (synthetic.cpp:24-36) into device SoA arrays */
 int twg_synth_uniform_device(twg_ctx* ctx, uint64_t nodes, uint64_t count, int64_t t_max,
                              uint64_t seed, int64_t* d_src, int64_t* d_dst, int64_t* d_t);

@@ -12,6 +12,6 @@ from .timewalk import (BatchRecord, BatchStats, BiasKind, Context, DirectionMode
                        LogicError, Node2VecParams, ReplayConfig, RngKind, StartMode, TierCounts,
                        TierThresholds, Variant, WalkConfig, WalkDirection, WalkSet, WalkStats, WindowManager,
                        DeviceEdges, default_context, format_edges_tsv, generate_walks, generate_walks_fullwalk, ParseError,
-                       read_edges_tsv, replay_stream, sample_start_edge)
+                       read_edges_tsv, replay_stream, sample_start_edge, synth_graph)
 
 _abi.load()

@@ -116,6 +116,7 @@ SIGNATURES = {
     "twg_walkset_binary": (I, [VP, VP, U64, C.POINTER(U64)]),
     "twg_walkset_from_host": (I, [VP, C.c_uint32, U64, VP, VP, VP, PP]),
     "twg_parse_edges_tsv": (I, [VP, VP, U64, PP, C.POINTER(U64)]),
+    "twg_synth_graph": (I, [VP, I, U64, U64, I64, U64, VP, U64, C.POINTER(U64)]),
     "twg_edges_from_host": (I, [VP, VP, U64, PP]),
     "twg_edges_info": (I, [VP, C.POINTER(U64)]),
     "twg_edges_download": (I, [VP, VP]),

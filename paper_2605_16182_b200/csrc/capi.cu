@@ -1023,6 +1023,21 @@ int twg_synth_stream_device(twg_ctx* ctx, uint64_t nodes, uint64_t first, uint64
   });
 }
 
+int twg_synth_graph(twg_ctx* ctx, int kind, uint64_t a, uint64_t b, int64_t t_max, uint64_t seed, twg_edge* out,
+                    uint64_t cap, uint64_t* count) {
+  return guarded([&] {
+    require(count != nullptr && kind >= 0 && kind <= 3, "twg_synth_graph: kind");
+    require(kind != 0 || (a > 0 && t_max >= 0), "twg_synth_graph: uniform needs nodes > 0 and t_max >= 0");
+    require(kind != 1 || a > 0, "twg_synth_graph: hub-skewed needs background nodes > 0");
+    require(kind != 3 || b > 0, "twg_synth_graph: time ladder needs rungs > 0");
+    const u64 n = synth_graph_size(kind, a, b);
+    *count = n;
+    if (!out) return;
+    require(cap >= n, "twg_synth_graph: buffer too small");
+    synth_graph(ctx->c, kind, a, b, t_max, mix64_host(seed), out);
+  });
+}
+
 int twg_synth_uniform_device(twg_ctx* ctx, uint64_t nodes, uint64_t count, int64_t t_max, uint64_t seed,
                              int64_t* d_src, int64_t* d_dst, int64_t* d_t) {
   return guarded([&] {

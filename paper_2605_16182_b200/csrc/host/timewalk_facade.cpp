@@ -23,6 +23,7 @@
 
 #include "timewalk/edge_store.hpp"
 #include "timewalk/io.hpp"
+#include "timewalk/synthetic.hpp"
 #include "timewalk/validity.hpp"
 #include "timewalk/primitives.hpp"
 #include "timewalk/replay.hpp"
@@ -978,6 +979,39 @@ ValidityReport check_walkset(const WalkSet& walks, const EdgeOracle& oracle, Wal
                                                         : std::optional<std::size_t>(static_cast<std::size_t>(first[i])));
   }
   return rep;
+}
+
+// ---- synthetic graphs (synthetic.cpp) on the device ------------------------------------
+
+namespace {
+
+std::vector<TemporalEdge> synth(int kind, std::uint64_t a, std::uint64_t b, Timestamp t_max, std::uint64_t seed) {
+  std::lock_guard<std::recursive_mutex> lk(api_mutex());
+  std::uint64_t n = 0;
+  check(twg_synth_graph(ctx(), kind, a, b, t_max, seed, nullptr, 0, &n));
+  std::vector<TemporalEdge> edges(n);
+  check(twg_synth_graph(ctx(), kind, a, b, t_max, seed, reinterpret_cast<twg_edge*>(edges.data()), n, &n));
+  return edges;
+}
+
+}  // namespace
+
+std::vector<TemporalEdge> make_uniform_graph(std::uint64_t node_count, std::uint64_t edge_count, Timestamp t_max,
+                                             std::uint64_t seed) {
+  return synth(0, node_count, edge_count, t_max, seed);
+}
+
+std::vector<TemporalEdge> make_hub_skewed_graph(std::uint64_t background_nodes, std::uint64_t background_edges,
+                                                std::uint64_t seed) {
+  return synth(1, background_nodes, background_edges, 0, seed);
+}
+
+std::vector<TemporalEdge> make_mega_hub_graph(std::uint32_t feeder_count, std::uint64_t seed) {
+  return synth(2, feeder_count, 0, 0, seed);
+}
+
+std::vector<TemporalEdge> make_time_ladder_graph(std::uint64_t edge_count, std::uint32_t rungs, std::uint64_t seed) {
+  return synth(3, edge_count, rungs, 0, seed);
 }
 
 }  // namespace timewalk

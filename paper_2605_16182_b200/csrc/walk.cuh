@@ -77,6 +77,10 @@ void parse_edges_tsv(Ctx& ctx, const char* text, u64 bytes, DevBuf<i64>& src, De
 void format_edges_tsv(Ctx& ctx, const i64* src, const i64* dst, const i64* t, u64 n, DevBuf<char>& text,
                       u64* bytes);
 
+// the reference's synthetic graphs (synth.cu, synthetic.cpp:24-140)
+u64 synth_graph_size(int kind, u64 a, u64 b);
+void synth_graph(Ctx& ctx, int kind, u64 a, u64 b, i64 t_max, u64 key, twg_edge* out);
+
 // compact (CSR) image on the device: offsets[count+1], nodes/times[total]
 void compact_walks(Ctx& ctx, const WalkSetDev& w, DevBuf<u64>& offsets, DevBuf<i64>& nodes,
                    DevBuf<i64>& times, u64* total);

@@ -165,6 +165,21 @@ class DeviceEdges:
         return buf[: n.value].tobytes()
 
 
+def synth_graph(kind: str, a: int, b: int = 0, t_max: int = 0, seed: int = 0,
+                ctx: Optional["Context"] = None) -> np.ndarray:
+    """The reference's synthetic graphs (synthetic.hpp) generated on the GPU,
+    bit-identical: kind "uniform" (a nodes, b edges, t_max), "hub_skewed" (a
+    background nodes, b background edges), "mega_hub" (a feeders),
+    "time_ladder" (a edges, b rungs). Returns (n, 3) int64."""
+    k = {"uniform": 0, "hub_skewed": 1, "mega_hub": 2, "time_ladder": 3}[kind]
+    ctx = ctx or default_context()
+    n = C.c_uint64()
+    _call("twg_synth_graph", ctx.handle, k, a, b, t_max, seed, None, 0, C.byref(n))
+    out = np.zeros((max(n.value, 1), 3), np.int64)
+    _call("twg_synth_graph", ctx.handle, k, a, b, t_max, seed, _ptr(out), n.value, C.byref(n))
+    return out[: n.value]
+
+
 def read_edges_tsv(text: bytes, ctx: Optional["Context"] = None) -> np.ndarray:
     """read_edges_tsv (io.cpp:40-63), parsed on the device: (n, 3) int64."""
     return DeviceEdges.parse_tsv(text, ctx).to_array()

@@ -21,6 +21,7 @@
 #include "timewalk/replay.hpp"
 #include "timewalk/rng.hpp"
 #include "timewalk/samplers.hpp"
+#include "timewalk/synthetic.hpp"
 #include "timewalk/validity.hpp"
 #include "timewalk/walk_engine.hpp"
 #include "timewalk/window_manager.hpp"
@@ -593,6 +594,26 @@ void validity_cases() {
   }
 }
 
+// acceptance.cpp:276-294 / test_output.txt:38 — the tier-coverage input built
+// by the device generator, default config, per-node starts: the reference's
+// exact tier counts
+void synthetic_cases() {
+  const auto graph = make_hub_skewed_graph(2000, 20000, 0);
+  CHECK(graph.size() == 13136 + 20000);
+  const auto store = EdgeStore::build(graph, DirectionMode::DirectedForward);
+  WalkStats st;
+  const auto walks = generate_walks(store, WalkConfig{}, TierThresholds{}, Variant::Coop, &st);
+  CHECK(st.tiers.solo == 19 && st.tiers.warp_cached == 6230 && st.tiers.warp_direct == 4 &&
+        st.tiers.block_cached == 11 && st.tiers.block_direct == 1 && st.tiers.multi_block == 7);
+  CHECK(make_mega_hub_graph(100, 3).size() == 100 + 64 + 1000);
+  const auto ladder = make_time_ladder_graph(1000, 10, 4);
+  CHECK(ladder.size() == 1000 && ladder[11].source == 1 && ladder[11].time == 1);
+  const auto uni = make_uniform_graph(50, 300, 9, 2);
+  CHECK(uni.size() == 300 && std::all_of(uni.begin(), uni.end(), [](const TemporalEdge& e) {
+          return e.source >= 0 && e.source < 50 && e.target < 50 && e.time >= 0 && e.time <= 9;
+        }));
+}
+
 int main() {
   edge_store_cases();
   window_cases();
@@ -603,6 +624,7 @@ int main() {
   edge_io_cases();
   io_cases();
   validity_cases();
+  synthetic_cases();
   std::printf("%d/%d checks passed\n", g_checks - g_fail, g_checks);
   return g_fail;
 }
