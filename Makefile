@@ -43,3 +43,27 @@ facade_test: $(FACADE_TEST)
 $(FACADE_TEST): tests/cpp/facade_test.cpp $(CXXHDRS) $(LIB)
 	@mkdir -p build
 	g++ -std=c++20 -O2 -Wall -Wextra -Iinclude $< -o $@ -L$(dir $(LIB)) -ltimewalk_b200 -Wl,-rpath,'$$ORIGIN/../$(dir $(LIB))'
+
+# The reference's OWN test suites (proj/tests/test_*.cpp + acceptance.cpp),
+# compiled UNCHANGED from where they lie under /root/reference (needs it at
+# build time; the binaries travel to the GPU box):
+#   build/ref_suites/gpu/<t>  against include/timewalk + libtimewalk_b200.so (the drop-in)
+#   build/ref_suites/cpu/<t>  against the reference core itself (oracle/_ref objects):
+#                             pins the doctest shim (every suite must pass there)
+REF        ?= /root/reference
+REF_TESTS  := $(REF)/proj/tests
+SUITES     := test_primitives test_rng test_samplers test_edge_store test_window test_walk_engine \
+              test_validity test_io test_replay test_synthetic acceptance
+HAVE_REF_TESTS := $(shell test -d $(REF_TESTS) && echo 1)
+SHIM       := tests/cpp/doctest_shim
+.PHONY: ref_suites
+ref_suites: $(if $(HAVE_REF_TESTS),$(addprefix build/ref_suites/gpu/,$(SUITES)) $(addprefix build/ref_suites/cpu/,$(SUITES)))
+
+build/ref_suites/gpu/%: $(REF_TESTS)/%.cpp $(SHIM)/doctest.h $(CXXHDRS) $(LIB)
+	@mkdir -p $(dir $@)
+	g++ -std=c++20 -O2 -I$(SHIM) -Iinclude $< -o $@ -L$(dir $(LIB)) -ltimewalk_b200 \
+	    -Wl,-rpath,'$$ORIGIN/../../../$(dir $(LIB))'
+
+build/ref_suites/cpu/%: $(REF_TESTS)/%.cpp $(SHIM)/doctest.h oracle/_ref/libtimewalk_ref.so
+	@mkdir -p $(dir $@)
+	g++ -std=c++20 -O2 -fopenmp -I$(SHIM) -I$(REF)/proj/core/include $< -o $@ oracle/_ref/obj/*.o

@@ -444,8 +444,7 @@ def run_e2e_pipelined(args, tw, ctx, wl, variant, walk_cfg):
     hosts = [torch.empty((B, 3), dtype=torch.int64, pin_memory=True) for _ in range(n_host)]
     for i, h in enumerate(hosts):  # pre-generated input stream (untimed)
         assert lib.twg_synth_stream_host(wl.nodes, (b + i) * B, B, wl.seed, C.c_void_p(h.data_ptr())) == 0
-    if n_host < n_steps:  # not enough host RAM for the whole run: reuse batches cyclically, times advance anyway
-        pass
+    regenerated = 0  # host buffers refilled inside the loop (host RAM below the whole run's input)
     cap = wl.walks * 8  # entries; grown if needed
     outs = [[torch.empty(wl.walks + 1, dtype=torch.int64, pin_memory=True),
              torch.empty(cap, dtype=torch.int64, pin_memory=True),
@@ -465,6 +464,11 @@ def run_e2e_pipelined(args, tw, ctx, wl, variant, walk_cfg):
             t_start = time.perf_counter()
             timed_hops, d2h = 0, 0
         if k + 1 < n_steps:  # H2D of the next batch overlaps this step
+            if k + 1 >= n_host:  # buffer reused: refill it with batch k+1 of the stream (its last H2D has landed:
+                # the ingest of step k+1-n_host <= k-1 consumed it), so times keep advancing; counted in the timing
+                assert lib.twg_synth_stream_host(wl.nodes, (b + k + 1) * B, B, wl.seed,
+                                                 C.c_void_p(hosts[(k + 1) % n_host].data_ptr())) == 0
+                regenerated += 1
             assert lib.twg_stage_batch(ctx.handle, (k + 1) % 2, C.c_void_p(hosts[(k + 1) % n_host].data_ptr()), B) == 0
         st = tw._abi.twg_batch_stats()
         rc = lib.twg_window_ingest_staged(window.handle, k % 2, None)
@@ -495,7 +499,7 @@ def run_e2e_pipelined(args, tw, ctx, wl, variant, walk_cfg):
     ctx.sync()
     total_s = time.perf_counter() - t_start
     return dict(total_s=total_s, hops=timed_hops, edges=B * args.steps, h2d=B * 24, d2h=d2h / args.steps,
-                pipelined=True, host_batches=n_host)
+                pipelined=True, host_batches=n_host, host_batches_regenerated_in_loop=regenerated)
 
 
 def run_e2e(args, tw, ctx, wl, rank, world, local_rank, variant, walk_cfg):

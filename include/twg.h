@@ -123,6 +123,20 @@ typedef struct twg_store_info {
 } twg_store_info;
 int twg_store_get_info(twg_store* s, twg_store_info* out);
 
+/* Streaming-representation layout of a snapshot (diagnostics and tests: the
+ * regime a parity run reached). Zero for contiguous stores. */
+typedef struct twg_store_layout {
+  uint64_t log_cap;         /* edge-log ring slots */
+  uint64_t log_first;       /* logical position of edge 0 (wrapped iff log_first + edges > log_cap) */
+  uint64_t ts_first;        /* logical position of ts group 0 */
+  uint64_t arena_cap;       /* node-arena slots */
+  uint64_t arena_used;      /* bump pointer after the ingest that made this snapshot */
+  uint64_t arena_serial;    /* changes when the arena is replaced (repack) */
+  uint64_t relocated_rings; /* rings moved by the ingest that made this snapshot */
+  uint64_t max_ring_end;    /* largest logical entry end (ee) over the snapshot's nodes */
+} twg_store_layout;
+int twg_store_get_layout(twg_store* s, twg_store_layout* out);
+
 /* Field ids for twg_store_download (host destination, exact element types):
  *  0 edge src external i64[m]      1 edge dst external i64[m]    2 edge time i64[m]
  *  3 edge src internal u32[m]      4 edge dst internal u32[m]
@@ -161,8 +175,11 @@ int twg_window_create(twg_ctx* ctx, int64_t duration, int mode, const twg_build_
                       twg_window** out);
 int twg_window_destroy(twg_window* w);
 int twg_window_ingest(twg_window* w, const twg_edge* batch, uint64_t n, twg_batch_stats* out);
-/* Device-resident batch (SoA). stats may be NULL to skip the host read-back
- * (then the call is fully asynchronous on the ctx stream). */
+/* Device-resident batch (SoA). stats may be NULL to skip the statistics
+ * read-back. The call is NOT asynchronous: the route decision (append vs
+ * rebuild), the ring plan and the new snapshot's counts are read back to the
+ * host (a few scalar read-backs per batch), so it returns with the snapshot
+ * published and the stream drained up to that point. */
 int twg_window_ingest_device(twg_window* w, const int64_t* d_src, const int64_t* d_dst,
                              const int64_t* d_t, uint64_t n, twg_batch_stats* out);
 /* Streaming pipeline (double-buffered host ingest). twg_stage_batch enqueues

@@ -481,7 +481,7 @@ class RefOracle:
             self._err(st.value)
         return h
 
-    def dump_handle(self, h) -> dict:
+    def dump_handle(self, h, keys=None) -> dict:
         cnt = np.zeros(8, np.uint64)
         self.L.twref_store_counts(h, _p(cnt))
         m, V, Z, P, Q = (int(x) for x in cnt[:5])
@@ -493,6 +493,8 @@ class RefOracle:
                 ("ref_edge", 12, np.uint32, P), ("wprefix", 13, np.float64, P), ("ext", 14, np.int64, V),
                 ("ref_nbr", 15, np.uint32, P)]
         for name, fid, dt, n in spec:
+            if keys is not None and name not in keys:
+                continue
             out = np.zeros(max(n, 1), dt)
             rc = self.L.twref_store_dump(h, fid, _p(out))
             if rc:
@@ -558,6 +560,32 @@ class RefOracle:
                 return stats, self.dump_handle(h)
             finally:
                 self.L.twref_store_free(h)
+        finally:
+            self.L.twref_window_free(w)
+
+    def window_iter(self, batches, duration, mode, keys=None):
+        """WindowManager::ingest_batch batch by batch (window_manager.cpp:14-62):
+        yields (BatchStats, window_bounds, snapshot dump) after EVERY batch,
+        one snapshot at a time (large windows: nothing accumulates)."""
+        st = I()
+        w = self.L.twref_window_create(duration, mode, C.byref(st))
+        if not w:
+            self._err(st.value)
+        try:
+            for b in batches:
+                e = edges_array(b)
+                bs = BatchStatsC()
+                rc = self.L.twref_window_ingest(w, _p(e), e.shape[0], C.byref(bs))
+                if rc:
+                    self._err(rc)
+                lo, hi = I64(), I64()
+                rcb = self.L.twref_window_bounds(w, C.byref(lo), C.byref(hi))
+                h = self.L.twref_window_snapshot(w)
+                try:
+                    d = self.dump_handle(h, keys)
+                finally:
+                    self.L.twref_store_free(h)
+                yield stats_dict(bs), ((lo.value, hi.value) if rcb == 0 else None), d
         finally:
             self.L.twref_window_free(w)
 

@@ -32,6 +32,11 @@ class twg_store_info(C.Structure):
     ]
 
 
+class twg_store_layout(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in ("log_cap", "log_first", "ts_first", "arena_cap", "arena_used",
+                                            "arena_serial", "relocated_rings", "max_ring_end")]
+
+
 class twg_audit_report(C.Structure):
     _fields_ = [("walks", C.c_uint64), ("valid_walks", C.c_uint64), ("hops", C.c_uint64),
                 ("valid_hops", C.c_uint64)]
@@ -91,6 +96,7 @@ SIGNATURES = {
     "twg_store_retain": (I, [VP]),
     "twg_store_release": (I, [VP]),
     "twg_store_get_info": (I, [VP, C.POINTER(twg_store_info)]),
+    "twg_store_get_layout": (I, [VP, C.POINTER(twg_store_layout)]),
     "twg_store_download": (I, [VP, I, VP]),
     "twg_store_neighborhood": (I, [VP, VP, VP, U64, I, VP]),
     "twg_store_find_nodes": (I, [VP, VP, U64, VP, VP]),

@@ -279,6 +279,7 @@ struct PlanArgs {
   i64 cutoff;
   int need_last;        // a batch time may equal a node's newest live time (mark merge)
   int relocate_all;     // repack every ring into a fresh arena
+  u32 rebase_at;        // a ring whose logical end would pass this is relocated (positions rebased to 0)
   u64 arena_cap;
   NodeMeta* plan;       // new bounds / ring; ee, ge = where the batch's entries / marks start
   i64* last_t;          // time of the last live entry (valid iff need_last and plan.ee > plan.eb)
@@ -303,20 +304,28 @@ __global__ void __launch_bounds__(kBlock) k_plan(PlanArgs a) {
       o = a.onm[v];
       y = a.y[v];
       const Ring oer = entry_ring(o), omr = mark_ring(o);
-      // the first surviving mark starts the first surviving entry (a group is
-      // evicted whole: eviction is by time), so one search over the marks
-      // gives both bounds
-      gb = evict_lb([&](u32 x) { return a.omt[omr(x)]; }, o.gb, o.ge, a.cutoff);
-      // a ring whose groups are single entries (distinct times: the common
-      // case) maps mark k to entry k, so the mark's start needs no load
-      if (o.ge - o.gb == o.ee - o.eb) eb = o.eb + (gb - o.gb);
-      else eb = gb == o.ge ? o.ee : a.oms[omr(gb)];
+      if (implicit_marks(o)) {
+        // single-entry groups (distinct times: the common case): marks are
+        // not stored, mark k is entry k — search the entry times
+        eb = evict_lb([&](u32 x) { return a.oent[oer(x)].t; }, o.eb, o.ee, a.cutoff);
+        gb = o.gb + (eb - o.eb);
+      } else {
+        // the first surviving mark starts the first surviving entry (a group
+        // is evicted whole: eviction is by time), so one search over the
+        // marks gives both bounds
+        gb = evict_lb([&](u32 x) { return a.omt[omr(x)]; }, o.gb, o.ge, a.cutoff);
+        eb = gb == o.ge ? o.ee : a.oms[omr(gb)];
+      }
       u32 low = o.eb;
       if (a.rnm) {
         const NodeMeta r = a.rnm[v];
         if (r.base == o.base && r.cap == o.cap) low = r.eb;  // same ring: the retired snapshot reads [r.eb, ..)
       }
-      fits = !a.relocate_all && static_cast<u64>(o.ee - low) + y <= o.cap;
+      // Logical positions are u32 and only rebased when a ring moves: a ring
+      // that keeps fitting would otherwise count past 2^32 over a long
+      // stream and break every [eb, ee) comparison, so it moves first.
+      fits = !a.relocate_all && static_cast<u64>(o.ee - low) + y <= o.cap &&
+             static_cast<u64>(o.ee) + y <= a.rebase_at;
       if (!fits) {
         const u32 need = (o.ee - eb) + y;
         req = 2 * need + 4;  // 2x slack: a typical ring absorbs ~10 batches before it moves
@@ -358,6 +367,7 @@ __global__ void k_reloc_copy(const Reloc* list, const u64* scal, const NodeMeta*
     const NodeMeta on = onm[r.v], p = plan[r.v];
     const Ring er = entry_ring(on), mr = mark_ring(on);
     for (u32 j = lane; j < p.ee; j += 32) ent[p.base + j] = oent[er(r.src_e + j)];
+    if (p.ge == p.ee) continue;  // implicit marks (single-entry groups): nothing stored to copy
     for (u32 j = lane; j < p.ge; j += 32) {
       mt[p.base + j] = omt[mr(r.src_g + j)];
       ms[p.base + j] = oms[mr(r.src_g + j)] - r.src_e;
@@ -385,6 +395,8 @@ struct PlaceSmem {  // ~34 KB: 6 CTAs per SM
   u32 cur[kPB], gcur[kPB], base[kPB], cap[kPB], eorg[kPB], gorg[kPB];
   i64 last_t[kPB];
   u32 has_last[kPB];
+  u8 expl[kPB];  // node stores its marks (a repeated time in its region)
+  u8 tie[kPB];   // this chunk holds an entry of the node that continues a group
   u32 mtotal;
   u32 rwcnt[kChunkItems][kPB / 32];
   u8 snode[kChunk];
@@ -423,6 +435,7 @@ __global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs a) {
   const bool has = valid && a.last_t && p.ee > p.eb && be > bs;
   sm.has_last[t] = has ? 1u : 0u;
   sm.last_t[t] = has ? lt_v : 0;
+  sm.expl[t] = implicit_marks(p) ? 0 : 1;
 
   const u32 lt = (1u << lane) - 1u;
   for (u32 c0 = bs; c0 < be; c0 += kChunk) {
@@ -441,6 +454,7 @@ __global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs a) {
       dk[r] = i < n ? (a.keys[c0 + i] & (kPB - 1)) : 0u;
     }
     for (int i = t; i < (kPB / 32) * kPB; i += kPB) (&sm.wcnt[0][0])[i] = 0;
+    sm.tie[t] = 0;
     __syncthreads();
     // stable rank: warp w owns items [w*R*32, (w+1)*R*32) in R rounds of 32
     u32 rank[kChunkItems];
@@ -493,6 +507,7 @@ __global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs a) {
         const i64 ti = sm.sent[i].t;
         if (i == sm.off[nd]) f = (!sm.has_last[nd] || ti != sm.last_t[nd]) ? 1u : 0u;
         else f = ti != sm.sent[i - 1].t ? 1u : 0u;
+        if (!f) sm.tie[nd] = 1;
       }
       fl[r] = __ballot_sync(0xffffffffu, f != 0);
       if (lane == 0) sm.rwcnt[r][warp] = __popc(fl[r]);
@@ -518,6 +533,18 @@ __global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs a) {
       sm.mscan[i] = static_cast<u16>(sm.rwcnt[r][warp] + __popc(fl[r] & lt));
       sm.flag[i] = static_cast<u8>((fl[r] >> lane) & 1u);
     }
+    if (sm.tie[t] && !sm.expl[t]) {
+      // the node's region gets a repeated time: its marks become explicit —
+      // store the implicit ones of everything placed so far (mark k = entry
+      // k over [eb, cur)); rare (ties inside a node's region)
+      const Ring er{sm.base[t], sm.cap[t], sm.eorg[t]}, mr{sm.base[t], sm.cap[t], sm.gorg[t]};
+      for (u32 x = p.eb; x < sm.cur[t]; ++x) {
+        const u32 g = p.gb + (x - p.eb);
+        a.mt[mr(g)] = a.ent[er(x)].t;
+        a.ms[mr(g)] = x;
+      }
+      sm.expl[t] = 1;
+    }
     __syncthreads();
     // write out in staged (node) order
     for (u32 i = t; i < n; i += kPB) {
@@ -526,7 +553,7 @@ __global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs a) {
       const Ring er{sm.base[nd], sm.cap[nd], sm.eorg[nd]};
       const Entry e = sm.sent[i];
       a.ent[er(pos)] = e;
-      if (sm.flag[i]) {
+      if (sm.flag[i] && sm.expl[nd]) {
         const Ring mr{sm.base[nd], sm.cap[nd], sm.gorg[nd]};
         const u32 g = sm.gcur[nd] + (sm.mscan[i] - sm.mscan[sm.off[nd]]);
         a.mt[mr(g)] = e.t;
@@ -554,6 +581,14 @@ __global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs a) {
     q = r.ge - r.gb;
   }
   block_atomic_add(reinterpret_cast<unsigned long long*>(a.q_total), q);
+}
+
+// logical ring end beyond which a ring is rebased (TWG_RING_REBASE lowers it
+// for tests; the default keeps every position below 2^31 + one batch)
+u32 ring_rebase_at() {  // read per batch (one getenv), so a test can lower it mid-process
+  const char* e = std::getenv("TWG_RING_REBASE");
+  const unsigned long long x = e ? std::strtoull(e, nullptr, 10) : 0ull;
+  return x ? static_cast<u32>(std::min<unsigned long long>(x, 0x80000000ull)) : 0x80000000u;
 }
 
 bool append_enabled() {
@@ -721,6 +756,7 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
     pa.need_last = no_ties ? 0 : 1;
     pa.cutoff = cutoff;
     pa.relocate_all = all ? 1 : 0;
+    pa.rebase_at = ring_rebase_at();
     pa.arena_cap = dst.cap;
     pa.plan = plan.p;
     pa.last_t = last_t.p;
@@ -737,6 +773,8 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
   u64 nrel = arena ? run_plan(*arena, false) : 0;
   if (nrel == 0) {
     auto na = std::make_shared<NodeArena>();
+    static std::atomic<u64> serials{0};
+    na->serial = ++serials;
     na->V = V;
     na->cap = std::min<u64>((5 * s->P) / 2 + 12 * V + 1024, 0xffffff00ull);  // >= 2 P + 4 V: the repack fits
     na->ent.alloc(na->cap, st);
@@ -749,6 +787,7 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
     fresh = true;
   }
   --nrel;
+  s->relocated = nrel;
   if (nrel) {
     k_reloc_copy<<<grid(ctx, 32 * nrel), kBlock, 0, st>>>(reloc.p, sc, O.nm.p, plan.p, O.ent.p, O.mk_time.p,
                                                           O.mk_start.p, arena->ent.p, arena->mk_time.p,

@@ -294,6 +294,43 @@ int twg_store_get_info(twg_store* h, twg_store_info* out) {
 }
 
 namespace {
+__global__ void k_max_ring_end(const NodeMeta* nm, u64 V, u64* out) {
+  u32 mx = 0;
+  for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < V;
+       v += static_cast<u64>(gridDim.x) * blockDim.x)
+    mx = max(mx, nm[v].ee);
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(reinterpret_cast<unsigned long long*>(out), static_cast<u64>(mx));
+}
+}  // namespace
+
+int twg_store_get_layout(twg_store* h, twg_store_layout* out) {
+  return guarded([&] {
+    const Store& s = *h->s;
+    twg_store_layout l{};
+    if (s.gapped) {
+      Ctx& c = *s.ctx;
+      l.log_cap = s.log->cap;
+      l.log_first = s.log_first;
+      l.ts_first = s.ts_first;
+      l.arena_cap = s.arena->cap;
+      l.arena_used = s.arena->used;
+      l.arena_serial = s.arena->serial;
+      l.relocated_rings = s.relocated;
+      if (s.V) {
+        TWG_CUDA(cudaMemsetAsync(c.d_scalars, 0, 8, c.stream));
+        k_max_ring_end<<<grid_for(s.V, 256, c.sm_count * 8), 256, 0, c.stream>>>(s.nm.p, s.V, c.d_scalars);
+        TWG_LAUNCHED(c);
+        u64 r[1];
+        read_scalars(c, c.d_scalars, r, 1);
+        l.max_ring_end = r[0];
+      }
+    }
+    *out = l;
+  });
+}
+
+namespace {
 __global__ void k_widen_u32(const u32* in, u64 n, u64* out) {
   for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<u64>(gridDim.x) * blockDim.x)
@@ -953,6 +990,10 @@ int twg_pick_index(twg_ctx* ctx, int kind, const double* u, const uint64_t* n, u
       if (!(u[i] >= 0.0) || u[i] >= 1.0) fail(TWG_EINVAL, "picker: u outside [0,1)");
     }
     Ctx& c = ctx->c;
+    if (count <= PickSmall::kMax) {  // scalar façade calls: no device buffers, no copies
+      pick_index_small(c, kind, u, n, static_cast<u32>(count), out);
+      return;
+    }
     DevBuf<double> du;
     DevBuf<u64> dn;
     h2d(c, du, u, count);

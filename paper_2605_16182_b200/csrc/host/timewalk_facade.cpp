@@ -666,12 +666,29 @@ void write_walks_device(std::ostream& out, const WalkSet& walks, bool binary) {
 
 void write_walks_text(std::ostream& out, const WalkSet& walks) { write_walks_device(out, walks, false); }
 
-void write_walks_binary(std::ostream& out, const WalkSet& walks) { write_walks_device(out, walks, true); }
+// TMPW0002 of a HOST walk set is its raw image (io.cpp:176-186): the host
+// vectors are written as they are (tails past lengths[w] included), with no
+// device round trip. Device-resident walk sets serialise on the GPU
+// (twg_walkset_binary).
+void write_walks_binary(std::ostream& out, const WalkSet& walks) {
+  const std::uint32_t stride = walks.stride;
+  const std::uint64_t count = walks.walk_count;
+  out.write(kWalkBinaryMagic, 8);
+  out.write(reinterpret_cast<const char*>(&stride), sizeof(stride));
+  out.write(reinterpret_cast<const char*>(&count), sizeof(count));
+  out.write(reinterpret_cast<const char*>(walks.nodes.data()),
+            static_cast<std::streamsize>(walks.nodes.size() * sizeof(NodeId)));
+  out.write(reinterpret_cast<const char*>(walks.times.data()),
+            static_cast<std::streamsize>(walks.times.size() * sizeof(Timestamp)));
+  out.write(reinterpret_cast<const char*>(walks.lengths.data()),
+            static_cast<std::streamsize>(walks.lengths.size() * sizeof(std::uint32_t)));
+}
 
 void write_walks(const std::string& path, const WalkSet& walks, bool binary) {
   std::ofstream out(path, std::ios::binary);
   if (!out) throw std::runtime_error("cannot open " + path + " for writing");
-  write_walks_device(out, walks, binary);
+  if (binary) write_walks_binary(out, walks);
+  else write_walks_device(out, walks, false);
 }
 
 // ---- walk readers (host deserialisers, io.cpp:137-216) ----------------------------

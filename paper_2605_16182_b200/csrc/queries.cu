@@ -60,6 +60,17 @@ __global__ void k_neighborhood(StoreView s, const i64* v, const i64* t, u64 n, i
   }
 }
 
+// any query node present in the store (the unsupported-direction error is
+// raised only for known nodes: the reference returns {} for an unknown one
+// before it checks the direction, edge_store.cpp:270-282)
+__global__ void k_any_known(StoreView s, const i64* v, u64 n, u64* any) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<u64>(gridDim.x) * blockDim.x) {
+    u32 iv;
+    if (find_ext(s, v[i], &iv)) *any = 1;
+  }
+}
+
 __global__ void k_find_nodes(StoreView s, const i64* v, u64 n, u32* internal, u8* found) {
   for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<u64>(gridDim.x) * blockDim.x) {
@@ -133,6 +144,17 @@ __global__ void k_pick_index(int kind, const double* u, const u64* n, u64 count,
     else r = pick_exponential(u[i], n[i], expm1_tab, &amb);
     out[i] = r;
   }
+}
+
+// a handful of picks (the scalar façade calls): inputs by value, results
+// straight into mapped pinned host memory — one launch + one sync per call
+__global__ void k_pick_index_small(int kind, PickSmall in, const double* expm1_tab, u64* out_mapped) {
+  const u32 i = threadIdx.x;
+  if (i >= in.count) return;
+  u32 amb = 0;
+  out_mapped[i] = kind == 0 ? pick_uniform(in.u[i], in.n[i])
+                  : kind == 1 ? pick_linear(in.u[i], in.n[i])
+                              : pick_exponential(in.u[i], in.n[i], expm1_tab, &amb);
 }
 
 __global__ void k_pick_weighted_range(const double* u, const double* prefix, const u64* begin, const u64* end,
@@ -252,10 +274,18 @@ u64 partition_flagged_dev(Ctx& ctx, const u32* items, u64 n, const u8* flags, u3
 
 void neighborhood_batch(Ctx& ctx, Store& s, const i64* d_v, const i64* d_t, u64 n, int dir, u64* d_out3) {
   const bool supports = s.mode == TWG_UNDIRECTED || ((s.mode == TWG_FORWARD) == (dir == 0));
-  if (!supports)
-    fail(TWG_EINVAL,
-         "temporal_neighborhood: walk direction not served by this store's direction mode");
   if (!n) return;
+  if (!supports) {
+    TWG_CUDA(cudaMemsetAsync(ctx.d_scalars, 0, 8, ctx.stream));
+    k_any_known<<<grid(ctx, n), kBlock, 0, ctx.stream>>>(s.view(), d_v, n, ctx.d_scalars);
+    TWG_LAUNCHED(ctx);
+    u64 any[1];
+    read_scalars(ctx, ctx.d_scalars, any, 1);
+    if (any[0])
+      fail(TWG_EINVAL, "temporal_neighborhood: walk direction not served by this store's direction mode");
+    TWG_CUDA(cudaMemsetAsync(d_out3, 0, 3 * n * sizeof(u64), ctx.stream));
+    return;
+  }
   k_neighborhood<<<grid(ctx, n), kBlock, 0, ctx.stream>>>(s.view(), d_v, d_t, n, dir, d_out3);
   TWG_LAUNCHED(ctx);
 }
@@ -287,6 +317,19 @@ void pick_index_batch(Ctx& ctx, int kind, const double* d_u, const u64* d_n, u64
   if (!count) return;
   k_pick_index<<<grid(ctx, count), kBlock, 0, ctx.stream>>>(kind, d_u, d_n, count, ctx.d_expm1, d_out);
   TWG_LAUNCHED(ctx);
+}
+
+void pick_index_small(Ctx& ctx, int kind, const double* u, const u64* n, u32 count, u64* out) {
+  PickSmall in{};
+  in.count = count;
+  for (u32 i = 0; i < count; ++i) {
+    in.u[i] = u[i];
+    in.n[i] = n[i];
+  }
+  k_pick_index_small<<<1, 32, 0, ctx.stream>>>(kind, in, ctx.d_expm1, ctx.d_mapped);
+  TWG_LAUNCHED(ctx);
+  TWG_CUDA(cudaStreamSynchronize(ctx.stream));
+  for (u32 i = 0; i < count; ++i) out[i] = reinterpret_cast<volatile u64*>(ctx.h_pinned)[i];
 }
 
 void pick_weighted_range_batch(Ctx& ctx, const double* d_u, const double* d_prefix, const u64* d_begin,

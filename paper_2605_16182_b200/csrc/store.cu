@@ -480,9 +480,16 @@ __global__ void k_compact_regions(const NodeMeta* nm, u64 V, const Entry* ent, c
       ent_c[o.x + i] = e;
       owner_c[o.x + i] = static_cast<u32>(v);
     }
-    for (u32 i = lane; i < r.ge - r.gb; i += 32) {
-      mk_time_c[o.y + i] = mk_time[mr(r.gb + i)];
-      mk_start_c[o.y + i] = mk_start[mr(r.gb + i)] - r.eb + o.x;
+    if (implicit_marks(r)) {  // single-entry groups: mark k is entry k (marks not stored)
+      for (u32 i = lane; i < r.ge - r.gb; i += 32) {
+        mk_time_c[o.y + i] = ent[er(r.eb + i)].t;
+        mk_start_c[o.y + i] = o.x + i;
+      }
+    } else {
+      for (u32 i = lane; i < r.ge - r.gb; i += 32) {
+        mk_time_c[o.y + i] = mk_time[mr(r.gb + i)];
+        mk_start_c[o.y + i] = mk_start[mr(r.gb + i)] - r.eb + o.x;
+      }
     }
   }
 }

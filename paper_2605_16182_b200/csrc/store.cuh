@@ -59,6 +59,13 @@ struct Ring {
     return base + (d >= cap ? d - cap : d);
   }
 };
+// Implicit marks: a region whose timestamp groups are all single entries
+// (as many groups as entries — distinct times, the common case of a
+// streaming window) has mark k == {time of entry k, position of entry k}.
+// The streaming ingest then does not store its marks (append.cu), and every
+// reader derives them from the entries; explicit marks are stored whenever
+// a region holds a repeated time.
+__device__ __forceinline__ bool implicit_marks(const NodeMeta& m) { return m.ge - m.gb == m.ee - m.eb; }
 __device__ __forceinline__ Ring entry_ring(const NodeMeta& m) { return Ring{m.base, m.cap, m.eorg}; }
 __device__ __forceinline__ Ring mark_ring(const NodeMeta& m) { return Ring{m.base, m.cap, m.gorg}; }
 constexpr u32 kIdentityCap = 0xffffffffu;
@@ -154,6 +161,7 @@ struct EdgeLog {  // two rings of `cap` slots; positions are logical (slot = pos
 };
 
 struct NodeArena {
+  u64 serial = 0;    // distinct per arena (diagnostics: twg_store_get_layout)
   DevBuf<Entry> ent;
   DevBuf<i64> mk_time;
   DevBuf<u32> mk_start;
@@ -192,6 +200,7 @@ struct Store {
   std::shared_ptr<NodeArena> arena;
   u64 log_first = 0;  // logical log position of edge 0
   u64 ts_first = 0;   // logical log group position of group 0
+  u64 relocated = 0;  // rings moved by the ingest that made this snapshot (diagnostics)
   u32 e_cap = kIdentityCap, e_org = 0, z_cap = kIdentityCap, z_org = 0;  // StoreView::erg / zrg
   DevBuf<double> ts_wtail;  // streaming stores: the nonzero tail of the ts weight prefix
   u64 ts_wt0 = 0;

@@ -363,7 +363,8 @@ __device__ bool adjacent_after(const StoreView& s, u32 a, u32 b, i64 t, int dir)
   const NodeMeta na = s.nm[a];
   const Ring er = entry_ring(na);
   u32 c, e;
-  causal_slice(s.mk_time, s.mk_start, mark_ring(na), na.gb, na.ge, na.eb, na.ee, t, dir, c, e);
+  if (implicit_marks(na)) causal_slice_entries(s.ent, er, na.eb, na.ee, t, dir, c, e);
+  else causal_slice(s.mk_time, s.mk_start, mark_ring(na), na.gb, na.ge, na.eb, na.ee, t, dir, c, e);
   for (u32 pos = c; pos < e; ++pos)
     if (s.ent[er(pos)].nbr == b) return true;
   return false;
@@ -795,9 +796,10 @@ __global__ void __launch_bounds__(kBlock) k_tier_warp(WalkParams P, StateArrays 
     const Ring mr = mark_ring(a), er = entry_ring(a);
     const u32 G = a.ge - a.gb;
     if (kCached && G <= cap) {
+      const bool imp = implicit_marks(a);
       for (u32 g = lane; g < G; g += 32) {
-        smt[g] = P.s.mk_time[mr(a.gb + g)];
-        sms[g] = P.s.mk_start[mr(a.gb + g)];
+        smt[g] = imp ? P.s.ent[er(a.eb + g)].t : P.s.mk_time[mr(a.gb + g)];
+        sms[g] = imp ? a.eb + g : P.s.mk_start[mr(a.gb + g)];
       }
       __syncwarp();
       const Ring staged{0u, kIdentityCap, a.gb};
@@ -830,9 +832,10 @@ __global__ void __launch_bounds__(kBlock) k_tier_block(WalkParams P, StateArrays
     const u32 G = a.ge - a.gb;
     if (kCached && G <= cap) {
       __syncthreads();
+      const bool imp = implicit_marks(a);
       for (u32 g = threadIdx.x; g < G; g += blockDim.x) {
-        smt[g] = P.s.mk_time[mr(a.gb + g)];
-        sms[g] = P.s.mk_start[mr(a.gb + g)];
+        smt[g] = imp ? P.s.ent[er(a.eb + g)].t : P.s.mk_time[mr(a.gb + g)];
+        sms[g] = imp ? a.eb + g : P.s.mk_start[mr(a.gb + g)];
       }
       __syncthreads();
       const Ring staged{0u, kIdentityCap, a.gb};

@@ -93,6 +93,14 @@ void schedule_step_explicit(Ctx& ctx, Store& s, const u32* d_nodes, const u8* d_
                             const twg_thresholds& th, u64* sizes5, u32* rows, u64 cap, u32* walk_ids);
 
 void pick_index_batch(Ctx& ctx, int kind, const double* d_u, const u64* d_n, u64 count, u64* d_out);
+struct PickSmall {
+  static constexpr u32 kMax = 16;
+  u32 count;
+  double u[kMax];
+  u64 n[kMax];
+};
+// count <= PickSmall::kMax host values -> host results (one launch, one sync)
+void pick_index_small(Ctx& ctx, int kind, const double* u, const u64* n, u32 count, u64* out);
 void pick_weighted_range_batch(Ctx& ctx, const double* d_u, const double* d_prefix, const u64* d_begin,
                                const u64* d_end, const double* d_base, u64 count, u64* d_out);
 void rng_bits_batch(Ctx& ctx, int rng, u64 seed, const u64* d_walk, const u64* d_hop, const u64* d_ord,

@@ -65,31 +65,65 @@ struct FastSpec {
 // time-ordered batch (each edge ranked by (src, dst) inside its equal-time
 // run, runs scanned up to kSegMax each way) through the ring wr — used only
 // when the statistics admit the fast append route, ignored otherwise.
-__global__ void k_batch_stats(const i64* bs, const i64* bd, const i64* bt, u64 n, u64* scal, EdgeRec* rec, Ring wr) {
+//
+// Tiled: a CTA stages kStatTile edges plus a kSegMax halo on each side in
+// shared memory with coalesced column loads (24 B per edge read once from
+// HBM), then every edge finds its run and its rank from shared memory.
+constexpr int kStatItems = 8;
+constexpr int kStatTile = kBlock * kStatItems;
+constexpr int kStatSpan = kStatTile + 2 * kSegMax;
+__global__ void __launch_bounds__(kBlock) k_batch_stats(const i64* bs, const i64* bd, const i64* bt, u64 n, u64* scal,
+                                                        EdgeRec* rec, Ring wr) {
+  __shared__ i64 st_t[kStatSpan];
+  __shared__ u32 st_a[kStatSpan], st_b[kStatSpan];
   i64 mt = kTimeUnset, lt = kTimeInfinite;
   u64 mid = 0;
   u32 shape = 0, neg = 0;
-  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<u64>(gridDim.x) * blockDim.x) {
-    const i64 t = bt[i], a = bs[i], b = bd[i];
-    mt = max(mt, t);
-    lt = min(lt, t);
-    if (a > 0) mid = max(mid, static_cast<u64>(a));
-    if (b > 0) mid = max(mid, static_cast<u64>(b));
-    if (a < 0 || b < 0) neg = 1;
-    if (i + 1 < n && t > bt[i + 1]) shape |= 1u;
-    if (i + kSegMax < n && t == bt[i + kSegMax]) shape |= 2u;
-    if (rec) {
-      u64 lo = i, hi = i + 1;
-      while (lo > 0 && i - lo < kSegMax && bt[lo - 1] == t) --lo;
-      while (hi < n && hi - i < kSegMax && bt[hi] == t) ++hi;
-      const u64 key = (static_cast<u64>(a) << 32) | static_cast<u64>(b);
-      u32 rank = 0;
-      for (u64 q = lo; q < hi; ++q) {
-        const u64 kq = (static_cast<u64>(bs[q]) << 32) | static_cast<u64>(bd[q]);
-        rank += (kq < key || (kq == key && q < i)) ? 1u : 0u;
+  const u64 tiles = (n + kStatTile - 1) / kStatTile;
+  for (u64 tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const u64 base = tile * kStatTile;
+    const i64 lo_g = static_cast<i64>(base) - kSegMax;  // global index of st_*[0]
+    __syncthreads();
+    for (int j = threadIdx.x; j < kStatSpan; j += kBlock) {
+      const i64 g = lo_g + j;
+      if (g >= 0 && static_cast<u64>(g) < n) {
+        const i64 t = bt[g], a = bs[g], b = bd[g];
+        st_t[j] = t;
+        st_a[j] = static_cast<u32>(a);
+        st_b[j] = static_cast<u32>(b);
+        if (j >= kSegMax && j < kSegMax + kStatTile) {  // this tile's own edges: statistics
+          mt = max(mt, t);
+          lt = min(lt, t);
+          if (a > 0) mid = max(mid, static_cast<u64>(a));
+          if (b > 0) mid = max(mid, static_cast<u64>(b));
+          if (a < 0 || b < 0) neg = 1;
+        }
       }
-      rec[wr(static_cast<u32>(lo + rank))] = EdgeRec{static_cast<u32>(a), static_cast<u32>(b), t};
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int k = 0; k < kStatItems; ++k) {
+      const int j = kSegMax + k * kBlock + threadIdx.x;  // smem index of edge i
+      const u64 i = base + k * kBlock + threadIdx.x;
+      if (i >= n) break;
+      const i64 t = st_t[j];
+      if (i + 1 < n && t > st_t[j + 1]) shape |= 1u;
+      if (i + kSegMax < n && t == st_t[j + kSegMax]) shape |= 2u;
+      if (rec) {
+        int lo = j, hi = j + 1;
+        const i64 jn = static_cast<i64>(n) - lo_g;
+        const int jmin = lo_g < 0 ? static_cast<int>(-lo_g) : 0;                 // smem index of edge 0
+        const int jend = jn < kStatSpan ? static_cast<int>(jn) : kStatSpan;       // of edge n (clamped)
+        while (lo > jmin && j - lo < kSegMax && st_t[lo - 1] == t) --lo;
+        while (hi < jend && hi - j < kSegMax && st_t[hi] == t) ++hi;
+        const u64 key = (static_cast<u64>(st_a[j]) << 32) | st_b[j];
+        u32 rank = 0;
+        for (int q = lo; q < hi; ++q) {
+          const u64 kq = (static_cast<u64>(st_a[q]) << 32) | st_b[q];
+          rank += (kq < key || (kq == key && q < j)) ? 1u : 0u;
+        }
+        rec[wr(static_cast<u32>(lo_g + lo + rank))] = EdgeRec{st_a[j], st_b[j], t};
+      }
     }
   }
   // one set of atomics per block (the whole grid finishes at once: per-warp
@@ -1014,7 +1048,8 @@ void window_ingest(Window& w, const i64* d_src, const i64* d_dst, const i64* d_t
     }
     TWG_CUDA(cudaMemsetAsync(ctx.d_scalars + 12, 0, 8, st));
   }
-  k_batch_stats<<<grid(ctx, n), kBlock, 0, st>>>(d_src, d_dst, d_t, n, ctx.d_scalars, spec.rec, spec.wring);
+  k_batch_stats<<<grid_for((n + kStatTile - 1) / kStatTile, 1, static_cast<unsigned>(ctx.sm_count) * 8), kBlock, 0, st>>>(
+      d_src, d_dst, d_t, n, ctx.d_scalars, spec.rec, spec.wring);
   TWG_LAUNCHED(ctx);
   if (spec.on) {
     k_lower_bound_cut<<<1, 1, 0, st>>>(old.view(), w.t_high, w.duration, ctx.d_scalars, ctx.d_scalars + 12);

@@ -345,6 +345,13 @@ class EdgeStore:
         arena (the time-ordered streaming fast path, csrc/append.cu)."""
         return bool(self.info.streaming)
 
+    def layout(self) -> dict:
+        """Streaming-representation layout (twg_store_get_layout): log ring,
+        arena, rings relocated by the producing ingest, largest ring end."""
+        lo = _abi.twg_store_layout()
+        _call("twg_store_get_layout", self.handle, C.byref(lo))
+        return {n: int(getattr(lo, n)) for n, _ in lo._fields_}
+
     def ts_group_count(self) -> int:
         return int(self.info.ts_groups)
 

@@ -190,3 +190,16 @@ def test_c5_law_stream_small_scale(tw, co):
         snap = w.snapshot()
         assert snap.is_streaming()
         assert_walks(tw.generate_walks(snap, to_cfg(tw, c), variant=tw.Variant.FullWalk), exp)
+
+
+@pytest.mark.parametrize("mode", [0, 2])
+def test_append_ring_rebase(tw, co, mode, monkeypatch):
+    """Ring positions are u32 and rebased only when a ring moves; a ring whose
+    logical end would pass the rebase bound (2^31 by default, lowered to 64
+    here through TWG_RING_REBASE) is relocated to logical 0 although it
+    still fits. With the bound this low nearly every ring is rebased every
+    batch; the whole index must stay bit-exact after every batch."""
+    monkeypatch.setenv("TWG_RING_REBASE", "64")
+    batches = _ordered_stream(57 + mode, 10, 3000, 60, 100)
+    n = _run(tw, co, batches, 350, mode, check_walks=True)
+    assert n == len(batches) - 1

@@ -133,6 +133,9 @@ def test_neighborhood_queries(tw, co, graphs):
     s = tw.EdgeStore.build([(1, 2, 2), (3, 2, 5), (4, 2, 9)], tw.DirectionMode.DirectedBackward)
     with pytest.raises(ValueError):
         s.temporal_neighborhood(2, 6, tw.WalkDirection.Forward)
+    # an unknown node answers {} before the direction check (edge_store.cpp:270-282)
+    r = s.temporal_neighborhood(99, 6, tw.WalkDirection.Forward)
+    assert (r.start, r.end, r.group_count) == (0, 0, 0)
 
 
 def test_adjacency_predicate(tw):
@@ -423,7 +426,7 @@ def test_pickers_vs_oracle(tw, co):
     gl = tw.pick_index_linear(u, n)
     ge = tw.pick_index_exponential(u, ne)
     gb = tw.pick_index_exponential(u, big)
-    for i in range(0, 100000, 97):
+    for i in range(100000):
         assert gu[i] == co.pick(0, u[i], int(n[i]))
         assert gl[i] == co.pick(1, u[i], int(n[i]))
         assert ge[i] == co.pick(2, u[i], int(ne[i]))
@@ -434,6 +437,27 @@ def test_pickers_vs_oracle(tw, co):
     assert tw.pick_index_linear(0.3, 3) == 1 and tw.pick_index_linear(0.95, 3) == 2
     with pytest.raises(ValueError):
         tw.pick_index_uniform(0.5, 0)
+
+
+def test_pickers_million_vs_reference(tw, ref):
+    """acceptance.cpp:95-150 at its own size: 10^6 random (u, n) per closed
+    form against the unmodified reference's pick_index_* (glibc libm on the
+    host), 0 mismatches; n spans both exponential regimes (n <= 700 exact
+    expm1/log1p form, n > 700 asymptotic form) plus tiny n."""
+    rs = np.random.default_rng(1234)
+    N = 1_000_000
+    u = rs.random(N)
+    u[:1000] = np.ldexp(1.0, -rs.integers(1, 1074, 1000).astype(np.int32))  # tiny u (deep tail)
+    u[1000:2000] = 1.0 - np.ldexp(1.0, -rs.integers(1, 53, 1000).astype(np.int32))  # u next to 1
+    n_all = np.concatenate([rs.integers(1, 16, N // 4), rs.integers(1, 701, N // 4),
+                            rs.integers(701, 1 << 20, N // 4), rs.integers(1, 1 << 31, N - 3 * (N // 4))])
+    n_all = rs.permutation(n_all).astype(np.uint64)
+    got = {0: tw.pick_index_uniform(u, n_all), 1: tw.pick_index_linear(u, n_all),
+           2: tw.pick_index_exponential(u, n_all)}
+    for kind in (0, 1, 2):
+        exp = ref.pick_many(kind, u, n_all)
+        bad = np.flatnonzero(np.asarray(got[kind], np.uint64) != exp)
+        assert bad.size == 0, (kind, bad[:5], u[bad[:5]], n_all[bad[:5]])
 
 
 # ------------------------------------------------------------------ replay
