@@ -151,13 +151,28 @@ def run_ours(args, rank, world, local_rank):
         args.variant]
     B = wl.batch_edges
 
-    from paper_2605_16182_b200.dist import broadcast_batch, shard_config
+    group = None
+    if world > 1:
+        # the product's multi-GPU path: a ReplicaGroup (twg_group_*, NCCL over
+        # NVLink) — rank 0 creates the rendezvous id, torch.distributed only
+        # carries those 128 bytes
+        uid = torch.zeros(128, dtype=torch.uint8, device=f"cuda:{local_rank}")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(tw.group_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, src=0)
+        group = tw.ReplicaGroup(ctx, world, rank, bytes(uid.cpu().numpy().tobytes()))
 
     def walk_cfg():
-        # weak scaling: every rank generates wl.walks walks of the global id space
-        base = tw.WalkConfig(walk_length=wl.walk_length, start_mode=tw.StartMode.Sampled, total_walks=wl.walks,
-                             bias=tw.BiasKind.ExponentialIndex, start_bias=tw.BiasKind.UniformIndex, seed=wl.seed)
-        return shard_config(base, rank, world, walks_per_rank=wl.walks)
+        # weak scaling: every rank generates wl.walks walks; the group splits
+        # the global id range [0, world * wl.walks) into contiguous shards
+        return tw.WalkConfig(walk_length=wl.walk_length, start_mode=tw.StartMode.Sampled,
+                             total_walks=wl.walks * world, bias=tw.BiasKind.ExponentialIndex,
+                             start_bias=tw.BiasKind.UniformIndex, seed=wl.seed)
+
+    def generate(snap, stats=None, wctx=None):
+        if group is not None:
+            return group.generate(snap, walk_cfg(), variant=variant, stats=stats)
+        return tw.generate_walks(snap, walk_cfg(), variant=variant, stats=stats, ctx=wctx)
 
     lib = tw._abi.load()
 
@@ -167,35 +182,32 @@ def run_ours(args, rank, world, local_rank):
                                          buf[1].data_ptr(), buf[2].data_ptr())
         assert rc == 0, lib.twg_last_error()
 
-    def bcast(buf):
-        if world > 1:  # one copy of the batch over NVLink into every replica (NCCL)
-            with torch.cuda.stream(stream):
-                broadcast_batch(buf, src=0)
+    def ptrs(buf):
+        return [x.data_ptr() for x in buf] if rank == 0 else [0, 0, 0]
 
-    side = torch.cuda.Stream(device=f"cuda:{local_rank}") if world > 1 else None
+    def stage(slot, buf):
+        # rank 0's batch -> every replica's staging slot (16 B/edge over NVLink, group copy stream)
+        group.stage_device(slot, 0, *ptrs(buf), B if rank == 0 else 0)
 
-    def bcast_async(buf):
-        # the next batch's NCCL broadcast is issued from an idle side stream, so
-        # it runs over NVLink while the current batch is ingested and walked
-        if world == 1:
-            return None
-        with torch.cuda.stream(side):
-            return [dist.broadcast(x, src=0, async_op=True) for x in buf]
-
-    def bcast_wait(works):
-        if works:
-            with torch.cuda.stream(stream):  # the compute stream waits for the replica's data
-                for wk in works:
-                    wk.wait()
+    def ingest(window, buf, slot=None, stats=False):
+        """One batch into this rank's replica: multi-GPU through the group
+        (staged slot, or stage + ingest), single GPU straight from the buffer."""
+        if group is None:
+            return window.ingest_batch_device(buf[0].data_ptr(), buf[1].data_ptr(), buf[2].data_ptr(), B,
+                                              stats=stats)
+        gs = group.ingest_staged(window, slot) if slot is not None else group.ingest_device(
+            window, 0, *ptrs(buf), B if rank == 0 else 0)
+        assert gs.replicas_agree, f"replica hash disagreement on rank {rank}"
+        return gs.local
 
     def new_buf():
         return [torch.empty(B, dtype=torch.int64, device=f"cuda:{local_rank}") for _ in range(3)]
 
     def step(window, buf):
-        window.ingest_batch_device(buf[0].data_ptr(), buf[1].data_ptr(), buf[2].data_ptr(), B, stats=False)
+        ingest(window, buf)
         snap = window.snapshot()
         st = tw.WalkStats()
-        ws = tw.generate_walks(snap, walk_cfg(), variant=variant, stats=st)
+        ws = generate(snap, stats=st)
         return st, ws
 
     # ---- device-resident pass ------------------------------------------------------
@@ -205,13 +217,11 @@ def run_ours(args, rank, world, local_rank):
     for _ in range(wl.prefill):
         if rank == 0:
             synth(buf, b)
-        bcast(buf)
-        window.ingest_batch_device(buf[0].data_ptr(), buf[1].data_ptr(), buf[2].data_ptr(), B, stats=False)
+        ingest(window, buf)
         b += 1
     for _ in range(args.warmup):
         if rank == 0:
             synth(buf, b)
-        bcast(buf)
         st, ws = step(window, buf)
         del ws
         b += 1
@@ -239,17 +249,17 @@ def run_ours(args, rank, world, local_rank):
         if not pipelined:
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(3 * args.steps + 2)]
             ev[0].record(stream)
-            pending = bcast_async(bufs[0])
+            if group is not None:
+                stage(0, bufs[0])
             for k in range(args.steps):
-                bcast_wait(pending)
-                pending = bcast_async(bufs[k + 1]) if k + 1 < args.steps else None
+                if group is not None and k + 1 < args.steps:
+                    stage((k + 1) % 2, bufs[k + 1])  # over NVLink while batch k is ingested and walked
                 ev[1 + 3 * k].record(stream)
-                bst = window.ingest_batch_device(bufs[k][0].data_ptr(), bufs[k][1].data_ptr(),
-                                                 bufs[k][2].data_ptr(), B, stats=True)
+                bst = ingest(window, bufs[k], slot=k % 2 if group is not None else None, stats=True)
                 ev[2 + 3 * k].record(stream)
                 snap = window.snapshot()
                 st = tw.WalkStats()
-                ws = tw.generate_walks(snap, walk_cfg(), variant=variant, stats=st)
+                ws = generate(snap, stats=st)
                 ev[3 + 3 * k].record(stream)
                 hops += st.hops
                 alg_bytes += st.alg_bytes
@@ -281,7 +291,7 @@ def run_ours(args, rank, world, local_rank):
                         snap, bst = ready.get()
                         wev[k][0].record(wstream)
                         st = tw.WalkStats()
-                        ws = tw.generate_walks(snap, walk_cfg(), variant=variant, stats=st, ctx=ctx_w)
+                        ws = generate(snap, stats=st, wctx=ctx_w)
                         wev[k][1].record(wstream)
                         res[k] = (st.hops, st.alg_bytes, batch_alg_bytes(snap.info, bst, B),
                                   append_alg_bytes(snap.info, bst, B))
@@ -298,10 +308,8 @@ def run_ours(args, rank, world, local_rank):
             for k in range(args.steps):
                 if k >= 2:
                     done[k - 2].wait()
-                bcast(bufs[k])
                 iev[k][0].record(stream)
-                bst = window.ingest_batch_device(bufs[k][0].data_ptr(), bufs[k][1].data_ptr(),
-                                                 bufs[k][2].data_ptr(), B, stats=True)
+                bst = ingest(window, bufs[k], stats=True)
                 iev[k][1].record(stream)
                 ready.put((window.snapshot(), bst))
             th.join()
@@ -340,7 +348,7 @@ def run_ours(args, rank, world, local_rank):
     audit = walk_output = None
     if not args.no_audit:
         snap = window.snapshot()
-        ws = tw.generate_walks(snap, walk_cfg(), variant=variant)
+        ws = generate(snap)
         audit, _ = ws.audit(snap)
         walk_output = measure_walk_output(tw, ws, lib)
         del ws, snap
@@ -383,7 +391,7 @@ def run_ours(args, rank, world, local_rank):
     # ---- e2e pass through the C ABI with host buffers -----------------------------------
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, tw, ctx, wl, rank, world, local_rank, variant, walk_cfg)
+        e2e = run_e2e(args, tw, ctx, wl, rank, world, local_rank, variant, walk_cfg, group, generate)
     return result, e2e, wl
 
 
@@ -502,10 +510,16 @@ def run_e2e_pipelined(args, tw, ctx, wl, variant, walk_cfg):
                 pipelined=True, host_batches=n_host, host_batches_regenerated_in_loop=regenerated)
 
 
-def run_e2e(args, tw, ctx, wl, rank, world, local_rank, variant, walk_cfg):
+def run_e2e(args, tw, ctx, wl, rank, world, local_rank, variant, walk_cfg, group, generate):
+    """e2e through the C ABI with host buffers. N=1: run_e2e_pipelined. N>1:
+    the ReplicaGroup path — rank 0 stages each host batch (pinned H2D + pack
+    to 16 B/edge, twg_group_stage_host), one NCCL broadcast moves it into
+    every replica over NVLink while the previous batch is ingested and
+    walked, every rank ingests (twg_group_ingest_staged, replica hashes
+    all-reduced) and generates its walk shard (twg_group_generate), then
+    downloads its compact walks. Per-rank host timing, max over ranks."""
     import ctypes as C
 
-    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -514,52 +528,52 @@ def run_e2e(args, tw, ctx, wl, rank, world, local_rank, variant, walk_cfg):
     lib = tw._abi.load()
     B = wl.batch_edges
     window = tw.WindowManager(wl.window, tw.DirectionMode.DirectedForward, weights=False, adjacency=False, ctx=ctx)
-    host = torch.empty((B, 3), dtype=torch.int64, pin_memory=True)
     dev = [torch.empty(B, dtype=torch.int64, device=f"cuda:{local_rank}") for _ in range(3)]
-    stream = torch.cuda.ExternalStream(ctx.stream)
     b = 0
-    for _ in range(wl.prefill):  # untimed prefill via the device generator
+    for _ in range(wl.prefill):  # untimed prefill via the device generator on rank 0
         if rank == 0:
             lib.twg_synth_stream_device(ctx.handle, wl.nodes, b * B, B, wl.seed, dev[0].data_ptr(),
                                         dev[1].data_ptr(), dev[2].data_ptr())
-        if world > 1:
-            with torch.cuda.stream(stream):
-                for x in dev:
-                    dist.broadcast(x, src=0)
-        window.ingest_batch_device(dev[0].data_ptr(), dev[1].data_ptr(), dev[2].data_ptr(), B, stats=False)
+        ptr = [x.data_ptr() for x in dev] if rank == 0 else [0, 0, 0]
+        gs = group.ingest_device(window, 0, *ptr, B if rank == 0 else 0)
+        assert gs.replicas_agree
         b += 1
+    del dev
+    n_steps = args.warmup + args.steps
+    hosts = []
+    if rank == 0:  # the input stream in pinned host RAM (generated untimed)
+        hosts = [torch.empty((B, 3), dtype=torch.int64, pin_memory=True) for _ in range(n_steps)]
+        for i, h in enumerate(hosts):
+            assert lib.twg_synth_stream_host(wl.nodes, (b + i) * B, B, wl.seed, C.c_void_p(h.data_ptr())) == 0
+
+    def stage(k):
+        if rank == 0:
+            rc = lib.twg_group_stage_host(group.handle, k % 2, 0, C.c_void_p(hosts[k].data_ptr()), B)
+        else:
+            rc = lib.twg_group_stage_host(group.handle, k % 2, 0, None, 0)
+        assert rc == 0, lib.twg_last_error()
+
     cap = None
     out_off = out_n = out_t = None
-    step_s, hops, h2d, d2h = [], 0, 0, 0
-    for k in range(args.warmup + args.steps):
-        if rank == 0:  # host-side generation of this batch: outside the timed step
-            rc = lib.twg_synth_stream_host(wl.nodes, b * B, B, wl.seed, C.c_void_p(host.data_ptr()))
-            assert rc == 0
-        b += 1
-        ctx.sync()
-        if world > 1:
+    hops, h2d, d2h = 0, 0, 0
+    ctx.sync()
+    dist.barrier()
+    stage(0)
+    t0 = None
+    for k in range(n_steps):
+        if k == args.warmup:
+            ctx.sync()
             dist.barrier()
-        t0 = time.perf_counter()
-        if world == 1:
-            st = tw._abi.twg_batch_stats()
-            rc = lib.twg_window_ingest(window.handle, C.c_void_p(host.data_ptr()), B, C.byref(st))
-            assert rc == 0, lib.twg_last_error()
-            in_bytes = B * 24
-        else:
-            # rank 0: pinned H2D; then NCCL broadcast over NVLink into every replica
-            if rank == 0:
-                with torch.cuda.stream(stream):
-                    d = host.to(f"cuda:{local_rank}", non_blocking=True)
-                    for i, x in enumerate(dev):
-                        x.copy_(d[:, i])
-            with torch.cuda.stream(stream):
-                for x in dev:
-                    dist.broadcast(x, src=0)
-            window.ingest_batch_device(dev[0].data_ptr(), dev[1].data_ptr(), dev[2].data_ptr(), B, stats=False)
-            in_bytes = B * 24 if rank == 0 else 0
+            t0 = time.perf_counter()
+            hops, h2d, d2h = 0, 0, 0
+        if k + 1 < n_steps:
+            stage(k + 1)
+        gs = tw._abi.twg_group_batch_stats()
+        rc = lib.twg_group_ingest_staged(group.handle, window.handle, k % 2, C.byref(gs))
+        assert rc == 0 and gs.replicas_agree, lib.twg_last_error()
         snap = window.snapshot()
         wst = tw.WalkStats()
-        ws = tw.generate_walks(snap, walk_cfg(), variant=variant, stats=wst)
+        ws = generate(snap, stats=wst)
         total = int(ws.total_hops + 2 * ws.walk_count)  # upper bound of recorded entries
         if cap is None or total > cap:
             cap = int(total * 1.25) + 1
@@ -570,36 +584,23 @@ def run_e2e(args, tw, ctx, wl, rank, world, local_rank, variant, walk_cfg):
                                               C.c_void_p(out_t.data_ptr()))
         assert rc == 0, lib.twg_last_error()
         entries = int(out_off[ws.walk_count].item())
-        if world > 1:
-            dist.barrier()
-        dt = time.perf_counter() - t0
-        if k >= args.warmup:
-            step_s.append(dt)
-            hops += wst.hops
-            h2d += in_bytes
-            d2h += 8 * (ws.walk_count + 1) + 16 * entries
+        hops += wst.hops
+        h2d += B * 24 if rank == 0 else 0
+        d2h += 8 * (ws.walk_count + 1) + 16 * entries
         del ws, snap
+    ctx.sync()
+    dt = time.perf_counter() - t0
 
-    def allmax(x):
-        if world == 1:
-            return x
+    def allred(x, op):
         t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local_rank}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=op)
         return float(t.item())
 
-    def allsum(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local_rank}")
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return float(t.item())
-
-    total_s = allmax(sum(step_s))
-    return dict(total_s=total_s, hops=allsum(hops), edges=B * args.steps,
-                h2d=allsum(h2d) / args.steps, d2h=allsum(d2h) / args.steps)
-
-
-# --------------------------------------------------------------------------- reference / CPU
+    total_s = allred(dt, dist.ReduceOp.MAX)
+    return dict(total_s=total_s, hops=allred(hops, dist.ReduceOp.SUM), edges=B * args.steps,
+                h2d=allred(h2d, dist.ReduceOp.SUM) / args.steps, d2h=allred(d2h, dist.ReduceOp.SUM) / args.steps,
+                path="ReplicaGroup: twg_group_stage_host (rank 0 pinned H2D + 16-B pack) -> NCCL broadcast -> "
+                     "twg_group_ingest_staged -> twg_group_generate -> twg_walkset_download_compact")
 
 def cpu_sample_workload():
     """Bounded sample of the C5 workload for the CPU reference: same stream
@@ -799,6 +800,11 @@ def main():
             "warmup": args.warmup, "ms_per_step": res["total_ms"] / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
             "edges_per_s": res["edges"] / total_s,
+            "multi_gpu": None if world == 1 else {
+                "path": "ReplicaGroup (twg_group_*): NCCL broadcast of each batch at 16 B/edge into every replica "
+                        "on a copy stream (batch k+1 overlaps batch k), per-batch replica hash all-reduce, walk ids "
+                        "sharded by rank", "replicas_agree_every_batch": True,
+                "edges_per_s_note": "each replica ingests every batch: edges/s is per replica (flat with N)"},
             "config": {**wl.describe(args.scale), "variant": args.variant, "parallelism": f"replicas{world}+walk-shards",
                        "global_walks_per_batch": wl.walks * world},
             "pipelined": res["pipelined"],
@@ -840,8 +846,7 @@ def main():
                            "path": ("twg_stage_batch (pinned H2D, copy stream) -> twg_window_ingest_staged -> "
                                     "twg_generate -> twg_walkset_download_compact_async (pinned D2H, download "
                                     "stream); H2D/D2H of neighbouring batches overlap compute")
-                           if e2e.get("pipelined") else "twg_window_ingest (host batch) -> twg_generate -> "
-                                                        "twg_walkset_download_compact, serial per step"}
+                           if e2e.get("pipelined") else e2e.get("path")}
         if cpu:
             line["cpu_baseline"] = {"value": cpu.get("value"), "unit": "walk steps/s", "cores": cpu.get("cores"),
                                     "kind": cpu.get("kind"), "sample": cpu.get("sample"),

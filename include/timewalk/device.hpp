@@ -3,6 +3,7 @@
 // has a default that reproduces the reference's behaviour exactly.
 #pragma once
 
+#include <array>
 #include <cstdint>
 
 namespace timewalk {
@@ -22,6 +23,27 @@ int current_device();
 struct BuildOptions {
   bool weights{true};
   bool adjacency{true};
+};
+
+// Multi-GPU replica group (twg_group_* in twg.h): one process
+// per GPU, created on this thread's current_device(). unique_id() is called
+// by one rank and shared out of band; every rank constructs the group with
+// it. Used by replay_stream(ReplicaGroup&, ...) and WindowManager::
+// ingest_group / generate_walks_shard.
+class ReplicaGroup {
+ public:
+  static std::array<std::uint8_t, 128> unique_id();
+  ReplicaGroup(int nranks, int rank, const std::array<std::uint8_t, 128>& id);
+  ~ReplicaGroup();
+  ReplicaGroup(const ReplicaGroup&) = delete;
+  ReplicaGroup& operator=(const ReplicaGroup&) = delete;
+  [[nodiscard]] int size() const { return nranks_; }
+  [[nodiscard]] int rank() const { return rank_; }
+  [[nodiscard]] void* device_handle() const { return handle_; }  // twg_group*
+
+ private:
+  void* handle_{nullptr};
+  int nranks_{1}, rank_{0};
 };
 
 }  // namespace timewalk

@@ -347,6 +347,67 @@ int twg_hop_walks(twg_ctx* ctx, twg_store* s, const twg_walk_config* config, con
                   uint32_t* prev, uint8_t* has_prev, uint8_t* alive, uint32_t* length, int64_t* nodes,
                   int64_t* times);
 
+/* ---- multi-GPU replica group (replaces the loop of replay_stream,
+ * replay.cpp:16-53, across GPUs) ---------------------------------------------
+ * One process per GPU, each with its own twg_ctx; the group owns two NCCL
+ * communicators over NVLink (data: batch broadcasts on the group's copy
+ * stream; control: replica hashes and walk-statistic reductions on the ctx
+ * stream). The window index is REPLICATED: every batch is broadcast once from
+ * the root into every rank's staging slot (16 B/edge: u32 ids + i64 time when
+ * every id fits 32 bits, else the 24-B triple) and every rank runs the same
+ * deterministic ingest; a 64-bit hash of each replica's new index is
+ * all-reduced so disagreement is detected on the batch that causes it. Walks
+ * are PARTITIONED: rank r generates a contiguous slice of the GLOBAL walk-id
+ * range (RNG draws are keyed by global ids, so the union of the ranks' walk
+ * sets equals one GPU generating every id, byte for byte).
+ * Every rank calls every group function, in the same order. */
+typedef struct twg_group twg_group;
+#define TWG_GROUP_ID_BYTES 128
+/* the rendezvous id (ncclUniqueId): created by one rank, shared out of band */
+int twg_group_unique_id(uint8_t id[TWG_GROUP_ID_BYTES]);
+int twg_group_create(twg_ctx* ctx, int nranks, int rank, const uint8_t id[TWG_GROUP_ID_BYTES],
+                     twg_group** out);
+int twg_group_destroy(twg_group* g);
+int twg_group_info(twg_group* g, int* nranks, int* rank);
+
+typedef struct twg_group_batch_stats {
+  twg_batch_stats local;          /* this replica's BatchStats (equal on every rank) */
+  uint64_t replica_hash;          /* hash of this replica's snapshot after the batch */
+  int32_t replicas_agree;         /* 1 iff every rank's hash is equal (all-reduced min == max) */
+  int32_t wire_bytes_per_edge;    /* bytes per edge the broadcast moved (16 or 24) */
+  uint64_t edges;                 /* batch size as broadcast by the root */
+} twg_group_batch_stats;
+
+/* Broadcast one batch from `root` into staging slot 0/1 of every rank, on the
+ * group's copy stream (returns once enqueued: stage batch k+1 while batch k is
+ * ingested/walked). The root passes its batch as device SoA columns (staged
+ * variant) or host AoS edges (host variant: one H2D on the root); the other
+ * ranks pass NULL / 0 and learn n from the root. */
+int twg_group_stage_device(twg_group* g, int slot, int root, const int64_t* d_src, const int64_t* d_dst,
+                           const int64_t* d_t, uint64_t n);
+int twg_group_stage_host(twg_group* g, int slot, int root, const twg_edge* batch, uint64_t n);
+/* edge count of the batch staged in a slot (as broadcast by the root; 0 is
+ * the replay end-of-stream marker) */
+int twg_group_staged_edges(twg_group* g, int slot, uint64_t* n);
+/* Ingest a staged slot into this rank's replica (ctx stream waits for the
+ * slot's broadcast), then hash the new snapshot and all-reduce the hashes. */
+int twg_group_ingest_staged(twg_group* g, twg_window* w, int slot, twg_group_batch_stats* out);
+/* stage + ingest in one call */
+int twg_group_ingest_device(twg_group* g, twg_window* w, int root, const int64_t* d_src, const int64_t* d_dst,
+                            const int64_t* d_t, uint64_t n, twg_group_batch_stats* out);
+int twg_group_ingest(twg_group* g, twg_window* w, int root, const twg_edge* batch, uint64_t n,
+                     twg_group_batch_stats* out);
+/* This rank's shard of generate_walks: the walk-id range [walk_begin,
+ * walk_end) of config (0,0 = every walk) split into nranks contiguous,
+ * balanced slices. local: this rank's WalkStats; global (optional): the
+ * counters summed over ranks (wall_seconds = max over ranks). */
+int twg_group_generate(twg_group* g, twg_store* s, const twg_walk_config* config,
+                       const twg_thresholds* thresholds, int variant, twg_walkset** out,
+                       twg_walk_stats* local, twg_walk_stats* global);
+/* The replica hash of one snapshot (what twg_group_ingest_staged all-reduces):
+ * node meta, external ids, counts and the newest `tail` edges (0 = all). */
+int twg_store_replica_hash(twg_store* s, uint64_t tail, uint64_t* hash);
+
 /* ---- primitives (primitives.hpp:11-31), device implementations -------------- */
 /* stable LSD radix sort of (u64 key, u32 value) pairs, in place (host arrays) */
 int twg_radix_sort_pairs(twg_ctx* ctx, uint64_t* keys, uint32_t* values, uint64_t n);

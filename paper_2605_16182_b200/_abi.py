@@ -75,6 +75,11 @@ class twg_walk_stats(C.Structure):
     ]
 
 
+class twg_group_batch_stats(C.Structure):
+    _fields_ = [("local", twg_batch_stats), ("replica_hash", C.c_uint64), ("replicas_agree", C.c_int32),
+                ("wire_bytes_per_edge", C.c_int32), ("edges", C.c_uint64)]
+
+
 VP = C.c_void_p
 PP = C.POINTER(C.c_void_p)
 I = C.c_int
@@ -144,6 +149,19 @@ SIGNATURES = {
     "twg_synth_stream_host": (I, [U64, U64, U64, U64, VP]),
     "twg_synth_stream_device": (I, [VP, U64, U64, U64, U64, VP, VP, VP]),
     "twg_synth_uniform_device": (I, [VP, U64, U64, I64, U64, VP, VP, VP]),
+    "twg_group_unique_id": (I, [VP]),
+    "twg_group_create": (I, [VP, I, I, VP, PP]),
+    "twg_group_destroy": (I, [VP]),
+    "twg_group_info": (I, [VP, C.POINTER(I), C.POINTER(I)]),
+    "twg_group_stage_device": (I, [VP, I, I, VP, VP, VP, U64]),
+    "twg_group_stage_host": (I, [VP, I, I, VP, U64]),
+    "twg_group_staged_edges": (I, [VP, I, C.POINTER(U64)]),
+    "twg_group_ingest_staged": (I, [VP, VP, I, C.POINTER(twg_group_batch_stats)]),
+    "twg_group_ingest_device": (I, [VP, VP, I, VP, VP, VP, U64, C.POINTER(twg_group_batch_stats)]),
+    "twg_group_ingest": (I, [VP, VP, I, VP, U64, C.POINTER(twg_group_batch_stats)]),
+    "twg_group_generate": (I, [VP, VP, C.POINTER(twg_walk_config), VP, I, PP, C.POINTER(twg_walk_stats),
+                               C.POINTER(twg_walk_stats)]),
+    "twg_store_replica_hash": (I, [VP, U64, C.POINTER(U64)]),
 }
 
 

@@ -9,22 +9,10 @@
 #include "rng.cuh"
 #include "walk.cuh"
 #include "window.cuh"
+#include "handles.cuh"
 
 using namespace twg;
 
-struct twg_ctx {
-  Ctx c;
-};
-struct twg_store {
-  Store* s;
-};
-struct twg_window {
-  Window* w;
-  twg_ctx* ctx;
-};
-struct twg_walkset {
-  WalkSetDev* w;
-};
 struct twg_edges {  // a device edge list (SoA columns)
   twg::Ctx* c = nullptr;
   twg::u64 n = 0;
@@ -34,6 +22,11 @@ struct twg_edges {  // a device edge list (SoA columns)
 namespace {
 
 thread_local std::string g_error;
+}  // namespace
+
+void twg::set_last_error(const char* what) { g_error = what; }
+
+namespace {
 
 // CounterRng state for a seed (rng.hpp:25)
 inline u64 mix64_host(u64 seed) { return mix64(seed ^ 0x6a09e667f3bcc909ULL); }
@@ -186,6 +179,7 @@ int twg_ctx_create_prio(int device, int priority, twg_ctx** out) {
       TWG_CUDA(cudaMemcpy(c.d_expm1, x.data(), x.size() * sizeof(double), cudaMemcpyHostToDevice));
       TWG_CUDA(cudaHostAlloc(&c.h_pinned, 64 * sizeof(u64), cudaHostAllocMapped));
       TWG_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c.d_mapped), c.h_pinned, 0));
+      for (int i = 0; i < 64; ++i) c.h_pinned[i] = 0;  // kMappedFlag starts below the first sequence number
       TWG_CUDA(cudaMalloc(&c.d_scalars, 64 * sizeof(u64)));
       TWG_CUDA(cudaStreamCreateWithFlags(&c.h2d_stream, cudaStreamNonBlocking));
       TWG_CUDA(cudaStreamCreateWithFlags(&c.d2h_stream, cudaStreamNonBlocking));
@@ -206,6 +200,11 @@ int twg_ctx_destroy(twg_ctx* ctx) {
     if (!ctx) return;
     Ctx& c = ctx->c;
     cudaStreamSynchronize(c.stream);
+    if (c.svc_stream) {  // the picker service exits after its idle timeout
+      cudaStreamSynchronize(c.svc_stream);
+      cudaStreamDestroy(c.svc_stream);
+      cudaFreeHost(c.pick_mbox);
+    }
     cudaFree(c.d_exp_neg);
     cudaFree(c.d_expm1);
     cudaFree(c.d_scalars);

@@ -65,6 +65,13 @@ struct Ctx {
   u64* h_pinned = nullptr;   // mapped pinned host scalars (see read_scalars)
   u64* d_mapped = nullptr;   // device alias of h_pinned
   u64* d_scalars = nullptr;  // 64 u64 scratch scalars on the device
+  u64 mapped_seq = 0;        // sequence number of the last mapped read-back (h_pinned[kMappedFlag])
+  // scalar picker service (queries.cu): a one-warp kernel on its own stream
+  // serving requests posted in mapped pinned memory while they keep coming
+  void* pick_mbox = nullptr;     // host view of the mailbox (PickMailbox)
+  void* pick_mbox_d = nullptr;   // device view
+  cudaStream_t svc_stream = nullptr;
+  u64 pick_seq = 0;
   // Streaming pipeline: host batches are staged into device slots on a copy
   // stream (H2D overlaps the compute stream) and walk downloads run on a D2H
   // stream. Slot buffers are plain cudaMalloc (used across streams).
@@ -197,5 +204,12 @@ inline unsigned grid_for(u64 n, unsigned block, unsigned cap = 1u << 20) {
 
 // small synchronous device -> host read of n u64 scalars via pinned memory
 void read_scalars(Ctx& ctx, const u64* d_src, u64* host_dst, int n);
+// h_pinned[kMappedFlag] receives the sequence number of a mapped read-back
+// once its values are visible to the host (written after a system fence)
+constexpr int kMappedFlag = 63;
+// spin until the kernel that publishes `seq` has written it (no stream
+// synchronisation: the host polls the mapped word; a failed or drained
+// stream without the flag raises)
+void mapped_wait(Ctx& ctx, u64 seq);
 
 }  // namespace twg

@@ -5,6 +5,7 @@
 // downloaded mirrors that back the reference's span-returning accessors.
 // Status codes become the reference's exception types.
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <charconv>
 #include <cstring>
@@ -364,6 +365,31 @@ const BatchStats& WindowManager::ingest_batch_device(const std::int64_t* d_src, 
   return stats_;
 }
 
+const BatchStats& WindowManager::adopt_group(const void* gstats) {
+  const auto& g = *static_cast<const twg_group_batch_stats*>(gstats);
+  if (!g.replicas_agree) throw std::runtime_error("timewalk (B200): replica windows disagree after a group ingest");
+  const twg_batch_stats& s = g.local;
+  stats_ = BatchStats{s.ingested, s.dropped_late, s.evicted, s.retained, s.rebuild_duration, s.peak_bytes};
+  check(twg_window_state(handle_, &t_high_, &batch_count_, nullptr));
+  if (g.edges) refresh();
+  return stats_;
+}
+
+const BatchStats& WindowManager::ingest_group(ReplicaGroup& group, std::span<const TemporalEdge> batch, int root) {
+  std::lock_guard<std::recursive_mutex> lk(api_mutex());
+  twg_group_batch_stats g{};
+  check(twg_group_ingest(static_cast<twg_group*>(group.device_handle()), handle_, root,
+                         reinterpret_cast<const twg_edge*>(batch.data()), batch.size(), &g));
+  return adopt_group(&g);
+}
+
+const BatchStats& WindowManager::ingest_group_staged(ReplicaGroup& group, int slot) {
+  std::lock_guard<std::recursive_mutex> lk(api_mutex());
+  twg_group_batch_stats g{};
+  check(twg_group_ingest_staged(static_cast<twg_group*>(group.device_handle()), handle_, slot, &g));
+  return adopt_group(&g);
+}
+
 std::pair<Timestamp, Timestamp> WindowManager::window_bounds() const {
   std::lock_guard<std::recursive_mutex> lk(api_mutex());
   Timestamp lo = 0, hi = 0;
@@ -387,6 +413,11 @@ void WalkConfig::validate() const {
     throw std::invalid_argument("walk config: node2vec p and q must be positive");
 }
 
+namespace {
+WalkSet download_walks(twg_walkset* w, const twg_walk_stats& st, std::chrono::steady_clock::time_point started,
+                       WalkStats* stats);
+}  // namespace
+
 WalkSet generate_walks(const EdgeStore& store, const WalkConfig& config, const TierThresholds& thresholds,
                        Variant variant, WalkStats* stats) {
   const auto started = std::chrono::steady_clock::now();
@@ -398,6 +429,27 @@ WalkSet generate_walks(const EdgeStore& store, const WalkConfig& config, const T
   twg_walkset* w = nullptr;
   twg_walk_stats st{};
   check(twg_generate(ctx(), store.device_handle(), &c, &th, static_cast<int>(variant), &w, &st));
+  return download_walks(w, st, started, stats);
+}
+
+WalkSet generate_walks(ReplicaGroup& group, const EdgeStore& store, const WalkConfig& config,
+                       const TierThresholds& thresholds, Variant variant, WalkStats* stats) {
+  const auto started = std::chrono::steady_clock::now();
+  config.validate();
+  thresholds.validate();
+  std::lock_guard<std::recursive_mutex> lk(api_mutex());
+  const twg_walk_config c = to_c(config);
+  const twg_thresholds th = to_c(thresholds);
+  twg_walkset* w = nullptr;
+  twg_walk_stats local{}, global{};
+  check(twg_group_generate(static_cast<twg_group*>(group.device_handle()), store.device_handle(), &c, &th,
+                           static_cast<int>(variant), &w, &local, &global));
+  return download_walks(w, global, started, stats);
+}
+
+namespace {
+WalkSet download_walks(twg_walkset* w, const twg_walk_stats& st, std::chrono::steady_clock::time_point started,
+                       WalkStats* stats) {
   WalkSet out;
   std::uint64_t first = 0, hops = 0;
   const int rc = twg_walkset_info(w, &out.stride, &out.walk_count, &first, &hops);
@@ -417,6 +469,7 @@ WalkSet generate_walks(const EdgeStore& store, const WalkConfig& config, const T
   }
   return out;
 }
+}  // namespace
 
 WalkSet generate_walks_fullwalk(const EdgeStore& store, const WalkConfig& config, WalkStats* stats) {
   return generate_walks(store, config, TierThresholds{}, Variant::FullWalk, stats);
@@ -637,6 +690,90 @@ std::uint64_t replay_stream(std::span<const TemporalEdge> edges, const ReplayCon
     }
   }
   flush(edges.size());
+  return batch_index;
+}
+
+// ---- multi-GPU replica group -----------------------------------------
+
+std::array<std::uint8_t, 128> ReplicaGroup::unique_id() {
+  std::array<std::uint8_t, 128> id{};
+  check(twg_group_unique_id(id.data()));
+  return id;
+}
+
+ReplicaGroup::ReplicaGroup(int nranks, int rank, const std::array<std::uint8_t, 128>& id)
+    : nranks_(nranks), rank_(rank) {
+  std::lock_guard<std::recursive_mutex> lk(api_mutex());
+  twg_group* g = nullptr;
+  check(twg_group_create(ctx(), nranks, rank, id.data(), &g));
+  handle_ = g;
+}
+
+ReplicaGroup::~ReplicaGroup() {
+  std::lock_guard<std::recursive_mutex> lk(api_mutex());
+  if (handle_) twg_group_destroy(static_cast<twg_group*>(handle_));
+}
+
+// replay_stream across the group: the root cuts batches exactly as the
+// single-GPU loop (replay.cpp:16-53); an empty broadcast ends the stream
+std::uint64_t replay_stream(ReplicaGroup& group, std::span<const TemporalEdge> edges, const ReplayConfig& config,
+                            const BatchSink& sink, int root) {
+  config.validate();
+  const bool is_root = group.rank() == root;
+  WindowManager window({config.window_duration, config.mode});
+  std::uint64_t batch_index = 0;
+  auto step = [&](std::span<const TemporalEdge> batch) {  // every rank, same order
+    BatchRecord record;
+    record.batch_index = batch_index++;
+    record.ingest = window.ingest_group(group, batch, root);
+    WalkSet walks;
+    if (config.generate && !window.snapshot()->empty())
+      walks = generate_walks(group, *window.snapshot(), config.walk, config.thresholds, config.variant, &record.walk);
+    if (sink) sink(record, walks);
+  };
+  auto finish = [&] {  // the end-of-stream marker: an empty broadcast nobody ingests
+    std::lock_guard<std::recursive_mutex> lk(api_mutex());
+    check(twg_group_stage_host(static_cast<twg_group*>(group.device_handle()), 0, root, nullptr, 0));
+  };
+  if (!is_root) {
+    for (;;) {
+      std::uint64_t n = 0;
+      {
+        std::lock_guard<std::recursive_mutex> lk(api_mutex());
+        twg_group* g = static_cast<twg_group*>(group.device_handle());
+        check(twg_group_stage_host(g, 0, root, nullptr, 0));  // receives the root's next batch (or the end)
+        check(twg_group_staged_edges(g, 0, &n));
+      }
+      if (n == 0) break;
+      BatchRecord record;
+      record.batch_index = batch_index++;
+      record.ingest = window.ingest_group_staged(group, 0);
+      WalkSet walks;
+      if (config.generate && !window.snapshot()->empty())
+        walks = generate_walks(group, *window.snapshot(), config.walk, config.thresholds, config.variant, &record.walk);
+      if (sink) sink(record, walks);
+    }
+    return batch_index;
+  }
+  if (!edges.empty()) {
+    const Timestamp origin = edges.front().time;
+    Timestamp boundary = origin + config.batch_duration;
+    std::size_t begin = 0;
+    auto flush = [&](std::size_t end) {
+      if (end == begin) return;
+      step(edges.subspan(begin, end - begin));
+      begin = end;
+    };
+    for (std::size_t i = 0; i < edges.size(); ++i) {
+      if (edges[i].time >= boundary) {
+        flush(i);
+        const Timestamp spans = (edges[i].time - origin) / config.batch_duration + 1;
+        boundary = origin + spans * config.batch_duration;
+      }
+    }
+    flush(edges.size());
+  }
+  finish();
   return batch_index;
 }
 

@@ -1,3 +1,4 @@
+#include <atomic>
 // Dual-index build on the device: the sm_100a replacement of
 // EdgeStore::build (edge_store.cpp:27-254).
 //
@@ -310,18 +311,43 @@ unsigned grid(Ctx& ctx, u64 n) { return grid_for(n, kBlock, static_cast<unsigned
 }  // namespace
 
 namespace {
-__global__ void k_read_scalars(const u64* src, volatile u64* mapped, int n) {
+__global__ void k_read_scalars(const u64* src, volatile u64* mapped, int n, u64 seq) {
   if (static_cast<int>(threadIdx.x) < n) mapped[threadIdx.x] = src[threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();  // the values reach the host before the flag
+    mapped[kMappedFlag] = seq;
+  }
 }
 }  // namespace
 
+void mapped_wait(Ctx& ctx, u64 seq) {
+  volatile u64* flag = ctx.h_pinned + kMappedFlag;
+  for (u32 spin = 1;; ++spin) {
+    if (*flag == seq) break;
+    if ((spin & 4095) == 0) {  // every few microseconds: the stream failed or drained without the flag?
+      const cudaError_t e = cudaStreamQuery(ctx.stream);
+      if (e == cudaSuccess) {
+        if (*flag == seq) break;
+        fail(TWG_ECUDA, "mapped read-back: stream drained without publishing");
+      }
+      if (e != cudaErrorNotReady) cuda_check(e, "mapped read-back", __FILE__, __LINE__);
+    }
+    __builtin_ia32_pause();
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+}
+
 // Small device->host reads go through mapped pinned memory written by a
 // one-warp kernel: no copy engine is involved, so the read never queues
-// behind a multi-GB walk download running on the D2H engine.
+// behind a multi-GB walk download running on the D2H engine. The host
+// polls the mapped flag instead of synchronising the stream (a stream
+// synchronisation costs several microseconds more per read-back).
 void read_scalars(Ctx& ctx, const u64* d_src, u64* host_dst, int n) {
-  k_read_scalars<<<1, 64, 0, ctx.stream>>>(d_src, ctx.d_mapped, n);
+  const u64 seq = ++ctx.mapped_seq;
+  k_read_scalars<<<1, 64, 0, ctx.stream>>>(d_src, ctx.d_mapped, n, seq);
   TWG_LAUNCHED(ctx);
-  TWG_CUDA(cudaStreamSynchronize(ctx.stream));
+  mapped_wait(ctx, seq);
   for (int i = 0; i < n; ++i) host_dst[i] = reinterpret_cast<volatile u64*>(ctx.h_pinned)[i];
 }
 

@@ -1252,7 +1252,7 @@ void compact_walks(Ctx& ctx, const WalkSetDev& w, DevBuf<u64>& offsets, DevBuf<i
 }
 
 WalkSetDev* generate_walks(Ctx& ctx, Store& s_in, const twg_walk_config& cfg, const twg_thresholds& th, int variant,
-                           twg_walk_stats* stats_out) {
+                           twg_walk_stats* stats_out, int shard_rank, int shard_count) {
   Store& s = walk_store(ctx, s_in, cfg);
   using clock = std::chrono::steady_clock;
   const auto started = clock::now();
@@ -1284,6 +1284,13 @@ WalkSetDev* generate_walks(Ctx& ctx, Store& s_in, const twg_walk_config& cfg, co
   if (wb == 0 && we == 0) we = total;
   if (we > total) we = total;
   if (wb > we) wb = we;
+  if (shard_count > 1) {  // this rank's contiguous, balanced slice of [wb, we) (multi-GPU group)
+    const u64 span = we - wb, base = span / shard_count, extra = span % shard_count;
+    const u64 r = static_cast<u64>(shard_rank);
+    const u64 lo = wb + r * base + (r < extra ? r : extra);
+    wb = lo;
+    we = lo + base + (r < extra ? 1 : 0);
+  }
   const u64 count = we - wb;
   out->first = wb;
   out->count = count;

@@ -28,8 +28,10 @@ struct WalkSetDev {
 };
 
 // Validates like walk_engine.cpp:189-206 / :366-370 (throws Error(TWG_EINVAL)).
+// shard_count > 1: generate only slice shard_rank of the resolved walk-id
+// range (contiguous, balanced; the multi-GPU group's partition).
 WalkSetDev* generate_walks(Ctx& ctx, Store& s, const twg_walk_config& cfg, const twg_thresholds& th,
-                           int variant, twg_walk_stats* stats);
+                           int variant, twg_walk_stats* stats, int shard_rank = 0, int shard_count = 1);
 
 // Host-side WalkStates + WalkSet columns (walk_engine.hpp:55-82).
 struct HostWalkArrays {

@@ -802,6 +802,114 @@ def generate_walks_fullwalk(store: EdgeStore, config: WalkConfig, stats: Optiona
     return generate_walks(store, config, TierThresholds(), Variant.FullWalk, stats)
 
 
+@dataclass
+class GroupBatchStats:
+    local: BatchStats
+    replica_hash: int
+    replicas_agree: bool
+    wire_bytes_per_edge: int
+    edges: int
+
+
+def group_unique_id() -> bytes:
+    """The rendezvous id of a ReplicaGroup (ncclUniqueId): one rank creates
+    it and shares it out of band (e.g. a torch.distributed broadcast)."""
+    buf = (C.c_uint8 * 128)()
+    _call("twg_group_unique_id", C.cast(buf, C.c_void_p))
+    return bytes(buf)
+
+
+class ReplicaGroup:
+    """Multi-GPU replica group (include/twg.h): one process per
+    GPU; batches are broadcast once over NVLink (NCCL) into every rank's
+    replica window; walks are sharded by global walk id. Every rank calls
+    every method, in the same order."""
+
+    def __init__(self, ctx: Context, nranks: int, rank: int, uid: bytes):
+        assert len(uid) == 128
+        self.ctx = ctx
+        self.nranks, self.rank = int(nranks), int(rank)
+        ub = (C.c_uint8 * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        _call("twg_group_create", ctx.handle, self.nranks, self.rank, C.cast(ub, C.c_void_p), C.byref(h))
+        self.handle = h
+
+    def close(self) -> None:
+        if self.handle:
+            _abi.load().twg_group_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @staticmethod
+    def _stats(st) -> GroupBatchStats:
+        return GroupBatchStats(BatchStats.of(st.local), int(st.replica_hash), bool(st.replicas_agree),
+                               int(st.wire_bytes_per_edge), int(st.edges))
+
+    def stage_device(self, slot: int, root: int, d_src: int = 0, d_dst: int = 0, d_t: int = 0, n: int = 0) -> None:
+        _call("twg_group_stage_device", self.handle, slot, root, C.c_void_p(d_src), C.c_void_p(d_dst),
+              C.c_void_p(d_t), n)
+
+    def stage_host(self, slot: int, root: int, batch=None) -> None:
+        if batch is None:
+            _call("twg_group_stage_host", self.handle, slot, root, None, 0)
+            return
+        e = as_edges(batch)
+        self._keep = getattr(self, "_keep", [None, None])
+        self._keep[slot] = e  # the H2D reads it asynchronously
+        _call("twg_group_stage_host", self.handle, slot, root, _ptr(e), e.shape[0])
+
+    def ingest_staged(self, window: WindowManager, slot: int) -> GroupBatchStats:
+        st = _abi.twg_group_batch_stats()
+        _call("twg_group_ingest_staged", self.handle, window.handle, slot, C.byref(st))
+        return self._stats(st)
+
+    def ingest(self, window: WindowManager, root: int, batch=None) -> GroupBatchStats:
+        """Root passes the host batch; the other ranks pass None."""
+        st = _abi.twg_group_batch_stats()
+        if batch is None:
+            _call("twg_group_ingest", self.handle, window.handle, root, None, 0, C.byref(st))
+        else:
+            e = as_edges(batch)
+            _call("twg_group_ingest", self.handle, window.handle, root, _ptr(e), e.shape[0], C.byref(st))
+        return self._stats(st)
+
+    def ingest_device(self, window: WindowManager, root: int, d_src: int = 0, d_dst: int = 0, d_t: int = 0,
+                      n: int = 0) -> GroupBatchStats:
+        st = _abi.twg_group_batch_stats()
+        _call("twg_group_ingest_device", self.handle, window.handle, root, C.c_void_p(d_src), C.c_void_p(d_dst),
+              C.c_void_p(d_t), n, C.byref(st))
+        return self._stats(st)
+
+    def generate(self, store: EdgeStore, config: WalkConfig, thresholds: Optional[TierThresholds] = None,
+                 variant: Variant = Variant.Coop, stats: Optional[WalkStats] = None,
+                 global_stats: Optional[WalkStats] = None) -> WalkSet:
+        """This rank's shard of generate_walks (contiguous slice of the global
+        walk-id range)."""
+        th = (thresholds or TierThresholds()).c()
+        cfg = config.c()
+        h = C.c_void_p()
+        st, gs = _abi.twg_walk_stats(), _abi.twg_walk_stats()
+        _call("twg_group_generate", self.handle, store.handle, C.byref(cfg), C.byref(th), int(variant),
+              C.byref(h), C.byref(st), C.byref(gs) if global_stats is not None else None)
+        if stats is not None:
+            stats.fill(st)
+        if global_stats is not None:
+            global_stats.fill(gs)
+        return WalkSet(h, self.ctx)
+
+
+def replica_hash(store: EdgeStore, tail: int = 0) -> int:
+    """The snapshot hash a ReplicaGroup all-reduces after each batch."""
+    h = C.c_uint64()
+    _call("twg_store_replica_hash", store.handle, int(tail), C.byref(h))
+    return h.value
+
+
 def sample_start_edges(store: EdgeStore, bias: BiasKind, u1, u2) -> np.ndarray:
     a = np.ascontiguousarray(np.asarray(u1, dtype=np.float64).reshape(-1))
     b = np.ascontiguousarray(np.asarray(u2, dtype=np.float64).reshape(-1))

@@ -357,6 +357,35 @@ static void replay_cases() {
   std::uint64_t ingested = 0;
   CHECK(replay_stream(s2, split, [&](const BatchRecord& r, const WalkSet&) { ingested += r.ingest.ingested; }) == 10);
   CHECK(ingested == s2.size());
+  // B200 extension: the same stream through a one-rank ReplicaGroup equals
+  // the single-GPU replay batch for batch (records, stats, walks)
+  {
+    ReplayConfig g = split;
+    g.generate = true;
+    g.walk = wc;
+    std::vector<BatchRecord> r1, r2;
+    std::vector<WalkSet> w1, w2;
+    const auto n1 = replay_stream(s2, g, [&](const BatchRecord& r, const WalkSet& w) {
+      r1.push_back(r);
+      w1.push_back(w);
+    });
+    ReplicaGroup group(1, 0, ReplicaGroup::unique_id());
+    const auto n2 = replay_stream(group, s2, g, [&](const BatchRecord& r, const WalkSet& w) {
+      r2.push_back(r);
+      w2.push_back(w);
+    });
+    CHECK(n1 == 10 && n2 == n1 && r2.size() == r1.size());
+    bool same = true;
+    for (std::size_t i = 0; i < r1.size() && i < r2.size(); ++i) {
+      same = same && r1[i].batch_index == r2[i].batch_index && r1[i].ingest.ingested == r2[i].ingest.ingested &&
+             r1[i].ingest.evicted == r2[i].ingest.evicted && r1[i].ingest.retained == r2[i].ingest.retained &&
+             r1[i].walk.hops == r2[i].walk.hops && r1[i].walk.walks == r2[i].walk.walks && w1[i] == w2[i];
+    }
+    CHECK(same);
+    WindowManager a({300, DirectionMode::DirectedForward});
+    const auto& st = a.ingest_group(group, std::span<const TemporalEdge>(s2.data(), 100));
+    CHECK(st.ingested == 100 && a.snapshot()->edge_count() == 100);
+  }
 }
 
 static void primitive_cases() {
