@@ -29,7 +29,7 @@ $(OBJDIR)/host_timewalk_facade.o: $(CSRC)/host/timewalk_facade.cpp $(CXXHDRS)
 
 $(LIB): $(OBJS)
 	@mkdir -p $(dir $@)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -Xcompiler -fopenmp -lgomp -lnccl
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -Xcompiler -fopenmp -lgomp -ldl
 
 oracle:
 	$(MAKE) -C oracle

@@ -18,6 +18,7 @@
 //
 // Two communicators: `data` (broadcasts, copy stream) and `ctl` (reductions,
 // the ctx stream), so a broadcast in flight never orders the control path.
+#include <dlfcn.h>
 #include <nccl.h>
 
 #include <atomic>
@@ -30,9 +31,50 @@ using namespace twg;
 namespace twg {
 namespace {
 
+// NCCL is resolved at run time (dlopen), not linked: a process that imports
+// PyTorch already holds PyTorch's own libnccl.so.2, and a second NCCL linked
+// into this library would claim the same soname first and break it. The
+// copy already loaded in the process wins (RTLD_NOLOAD); otherwise
+// TWG_NCCL_LIB, else the system libnccl.so.2.
+struct Nccl {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+  ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*);
+  ncclResult_t (*CommDestroy)(ncclComm_t);
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+  const char* (*GetErrorString)(ncclResult_t);
+};
+
+const Nccl& nccl() {
+  static Nccl api = [] {
+    Nccl a{};
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) {
+      const char* e = std::getenv("TWG_NCCL_LIB");
+      h = dlopen(e && *e ? e : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    }
+    if (!h) fail(TWG_ECUDA, std::string("multi-GPU group: cannot load NCCL (libnccl.so.2): ") + dlerror());
+    auto sym = [h](const char* n) {
+      void* f = dlsym(h, n);
+      if (!f) fail(TWG_ECUDA, std::string("multi-GPU group: NCCL lacks ") + n);
+      return f;
+    };
+    a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(sym("ncclGetUniqueId"));
+    a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(sym("ncclCommInitRank"));
+    a.CommSplit = reinterpret_cast<decltype(a.CommSplit)>(sym("ncclCommSplit"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(sym("ncclCommDestroy"));
+    a.Broadcast = reinterpret_cast<decltype(a.Broadcast)>(sym("ncclBroadcast"));
+    a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(sym("ncclAllReduce"));
+    a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(sym("ncclGetErrorString"));
+    return a;
+  }();
+  return api;
+}
+
 void nccl_check(ncclResult_t r, const char* what) {
   if (r != ncclSuccess) {
-    std::string m = std::string("NCCL: ") + what + ": " + ncclGetErrorString(r);
+    std::string m = std::string("NCCL: ") + what + ": " + nccl().GetErrorString(r);
     fail(TWG_ECUDA, m);
   }
 }
@@ -250,7 +292,7 @@ void stage(twg_group& g, int slot, int root, u64 n_root, RootPrep root_prep) {
     TWG_CUDA(cudaMemcpyAsync(g.d_small, hdr, sizeof(hdr), cudaMemcpyHostToDevice, g.copy));
   }
   if (g.nranks > 1) {
-    TWG_NCCL(ncclBroadcast(g.d_small, g.d_small, 2, ncclUint64, root, g.data, g.copy));
+    TWG_NCCL(nccl().Broadcast(g.d_small, g.d_small, 2, ncclUint64, root, g.data, g.copy));
     if (g.rank != root) g.read_copy_stream(g.d_small, hdr, 2);
   }
   const u64 n = hdr[0];
@@ -258,7 +300,7 @@ void stage(twg_group& g, int slot, int root, u64 n_root, RootPrep root_prep) {
   const u64 bytes = n * (narrow ? 16 : 24);
   if (g.rank != root) g.ensure_wire(sl, bytes ? bytes : 16);
   if (g.nranks > 1 && bytes)
-    TWG_NCCL(ncclBroadcast(sl.wire, sl.wire, bytes, ncclUint8, root, g.data, g.copy));
+    TWG_NCCL(nccl().Broadcast(sl.wire, sl.wire, bytes, ncclUint8, root, g.data, g.copy));
   TWG_CUDA(cudaEventRecord(sl.ready, g.copy));
   sl.n = n;
   sl.narrow = narrow;
@@ -301,7 +343,7 @@ void ingest_staged(twg_group& g, twg_window* w, int slot, twg_group_batch_stats*
   replica_hash_dev(c, *w->w->store, n, g.d_small + 4);
   k_hash_pair<<<1, 1, 0, c.stream>>>(g.d_small + 4, counts_mix(*w->w->store), g.d_small + 6);
   TWG_LAUNCHED(c);
-  if (g.nranks > 1) TWG_NCCL(ncclAllReduce(g.d_small + 6, g.d_small + 8, 2, ncclUint64, ncclMax, g.ctl, c.stream));
+  if (g.nranks > 1) TWG_NCCL(nccl().AllReduce(g.d_small + 6, g.d_small + 8, 2, ncclUint64, ncclMax, g.ctl, c.stream));
   else TWG_CUDA(cudaMemcpyAsync(g.d_small + 8, g.d_small + 6, 16, cudaMemcpyDeviceToDevice, c.stream));
   TWG_CUDA(cudaMemcpyAsync(g.d_small + 10, g.d_small + 6, 8, cudaMemcpyDeviceToDevice, c.stream));
   u64 r[3];
@@ -324,7 +366,7 @@ int twg_group_unique_id(uint8_t id[TWG_GROUP_ID_BYTES]) {
   return gguarded([&] {
     static_assert(sizeof(ncclUniqueId) == TWG_GROUP_ID_BYTES, "ncclUniqueId size");
     ncclUniqueId u;
-    TWG_NCCL(ncclGetUniqueId(&u));
+    TWG_NCCL(nccl().GetUniqueId(&u));
     std::memcpy(id, &u, sizeof(u));
   });
 }
@@ -341,8 +383,8 @@ int twg_group_create(twg_ctx* ctx, int nranks, int rank, const uint8_t id[TWG_GR
       TWG_CUDA(cudaSetDevice(c.device));
       ncclUniqueId u;
       std::memcpy(&u, id, sizeof(u));
-      TWG_NCCL(ncclCommInitRank(&g->data, nranks, u, rank));
-      TWG_NCCL(ncclCommSplit(g->data, 0, rank, &g->ctl, nullptr));
+      TWG_NCCL(nccl().CommInitRank(&g->data, nranks, u, rank));
+      TWG_NCCL(nccl().CommSplit(g->data, 0, rank, &g->ctl, nullptr));
       TWG_CUDA(cudaStreamCreateWithFlags(&g->copy, cudaStreamNonBlocking));
       TWG_CUDA(cudaHostAlloc(&g->h_map, 32 * sizeof(u64), cudaHostAllocMapped));
       std::memset(g->h_map, 0, 32 * sizeof(u64));
@@ -374,8 +416,8 @@ int twg_group_destroy(twg_group* g) {
     if (g->d_small) cudaFree(g->d_small);
     if (g->h_map) cudaFreeHost(g->h_map);
     if (g->copy) cudaStreamDestroy(g->copy);
-    if (g->ctl) ncclCommDestroy(g->ctl);
-    if (g->data) ncclCommDestroy(g->data);
+    if (g->ctl) nccl().CommDestroy(g->ctl);
+    if (g->data) nccl().CommDestroy(g->data);
     delete g;
   });
 }
@@ -501,8 +543,8 @@ int twg_group_generate(twg_group* g, twg_store* s, const twg_walk_config* config
       TWG_CUDA(cudaMemcpyAsync(d, words, sizeof(words), cudaMemcpyHostToDevice, c.stream));
       TWG_CUDA(cudaMemcpyAsync(d + 11, &tw, 8, cudaMemcpyHostToDevice, c.stream));
       if (g->nranks > 1) {
-        TWG_NCCL(ncclAllReduce(d, d, kWords + 2, ncclUint64, ncclSum, g->ctl, c.stream));
-        TWG_NCCL(ncclAllReduce(d + 11, d + 11, 1, ncclUint64, ncclMax, g->ctl, c.stream));
+        TWG_NCCL(nccl().AllReduce(d, d, kWords + 2, ncclUint64, ncclSum, g->ctl, c.stream));
+        TWG_NCCL(nccl().AllReduce(d + 11, d + 11, 1, ncclUint64, ncclMax, g->ctl, c.stream));
       }
       u64 r[12];
       read_scalars(c, d, r, 12);

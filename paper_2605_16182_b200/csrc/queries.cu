@@ -315,20 +315,29 @@ void pick_index_batch(Ctx& ctx, int kind, const double* d_u, const u64* d_n, u64
 // one (u, n) pair: a kernel launch + completion wait per call costs ~15 us,
 // which dominates the reference's closed-form acceptance criterion (3x10^6
 // calls). Instead one warp, launched on the ctx's service stream on first
-// use, polls a mailbox in mapped pinned memory and answers each request in a
-// few microseconds (one PCIe round trip); it exits after kIdleNs without a
-// request (so it never outlives a burst of calls, never blocks a device
-// synchronisation for long, and never spins under a profiler's replay), and
-// the next request relaunches it.
-struct PickMailbox {
-  u64 req;             // host: sequence number of the posted request
-  u64 resp;            // device: sequence number of the last answered request
-  u32 running;         // host sets 1 at launch; the kernel clears it when it exits
-  u32 kind, count, _pad;
-  double u[PickSmall::kMax];
-  u64 n[PickSmall::kMax];
-  u64 out[PickSmall::kMax];
+// use, polls a mailbox in mapped pinned memory and answers each request in
+// about one PCIe round trip; it exits after kIdleNs without a request (so it
+// never outlives a burst of calls, never holds a device synchronisation for
+// long, and never spins under a profiler's replay), and the next request
+// relaunches it.
+//
+// The request is two 16-B words read with two independent loads in one
+// round trip: a = {u, n}, b = {tag, check} with tag = seq << 2 | kind and
+// check a hash of (u, n, tag); a torn read (the host mid-way through
+// posting) fails the check and is simply read again.
+struct alignas(64) PickMailbox {
+  u64 a[2];        // u (bits), n
+  u64 b[2];        // tag, check  (tag written last)
+  u64 resp[2];     // device: {answered tag, result}
+  u32 running;     // host sets 1 at launch; the kernel clears it when it exits
+  u32 _pad;
 };
+
+__host__ __device__ __forceinline__ u64 pick_check(u64 ubits, u64 n, u64 tag) {
+  u64 x = ubits ^ (n * 0x9e3779b97f4a7c15ull) ^ (tag * 0xbf58476d1ce4e5b9ull);
+  x = (x ^ (x >> 31)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 29);
+}
 
 __device__ __forceinline__ u64 global_ns() {
   u64 t;
@@ -336,46 +345,35 @@ __device__ __forceinline__ u64 global_ns() {
   return t;
 }
 
-__global__ void k_pick_service(volatile PickMailbox* mb, const double* expm1_tab) {
+__device__ __forceinline__ void ld_sys_v2(const u64* p, u64& x, u64& y) {
+  asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "l"(p) : "memory");
+}
+
+__global__ void k_pick_service(PickMailbox* mb, const double* expm1_tab) {
   constexpr u64 kIdleNs = 2000000;  // 2 ms without a request: exit
-  const u32 lane = threadIdx.x;
-  u64 served = mb->resp;
+  if (threadIdx.x != 0) return;
+  u64 served = reinterpret_cast<volatile u64*>(mb->resp)[0];
   u64 idle_from = global_ns();
   for (;;) {
-    u64 req = 0;
-    if (lane == 0) {
-      req = mb->req;
-      while (req == served) {
-        if (global_ns() - idle_from > kIdleNs) {
-          req = mb->req;  // a final look before leaving
-          if (req == served) break;
-        }
-        __nanosleep(100);
-        req = mb->req;
-      }
-    }
-    req = __shfl_sync(0xffffffffu, req, 0);
-    if (req == served) break;
-    __threadfence_system();  // the request's fields were written before req
-    const u32 kind = mb->kind, count = mb->count;
-    if (lane < count) {
+    u64 a0, a1, b0, b1;
+    ld_sys_v2(mb->a, a0, a1);
+    ld_sys_v2(mb->b, b0, b1);
+    if (b0 != served && b1 == pick_check(a0, a1, b0)) {
+      const int kind = static_cast<int>(b0 & 3u);
+      const double u = __longlong_as_double(static_cast<long long>(a0));
       u32 amb = 0;
-      const double u = mb->u[lane];
-      const u64 n = mb->n[lane];
-      mb->out[lane] = kind == 0 ? pick_uniform(u, n) : kind == 1 ? pick_linear(u, n) : pick_exponential(u, n, expm1_tab, &amb);
-    }
-    __syncwarp();
-    if (lane == 0) {
+      const u64 r = kind == 0 ? pick_uniform(u, a1) : kind == 1 ? pick_linear(u, a1) : pick_exponential(u, a1, expm1_tab, &amb);
+      reinterpret_cast<volatile u64*>(mb->resp)[1] = r;  // posted writes arrive in order: result, then tag
       __threadfence_system();
-      mb->resp = req;
+      reinterpret_cast<volatile u64*>(mb->resp)[0] = b0;
+      served = b0;
+      idle_from = global_ns();
+    } else if (global_ns() - idle_from > kIdleNs) {
+      break;
     }
-    served = req;
-    idle_from = global_ns();
   }
-  if (lane == 0) {
-    __threadfence_system();
-    mb->running = 0;
-  }
+  __threadfence_system();
+  reinterpret_cast<volatile u32*>(&mb->running)[0] = 0;
 }
 
 void pick_index_small(Ctx& ctx, int kind, const double* u, const u64* n, u32 count, u64* out) {
@@ -385,30 +383,36 @@ void pick_index_small(Ctx& ctx, int kind, const double* u, const u64* n, u32 cou
     TWG_CUDA(cudaHostGetDevicePointer(&ctx.pick_mbox_d, ctx.pick_mbox, 0));
     TWG_CUDA(cudaStreamCreateWithFlags(&ctx.svc_stream, cudaStreamNonBlocking));
   }
-  volatile PickMailbox* mb = static_cast<volatile PickMailbox*>(ctx.pick_mbox);
-  mb->kind = static_cast<u32>(kind);
-  mb->count = count;
+  PickMailbox* mb = static_cast<PickMailbox*>(ctx.pick_mbox);
+  volatile u64* va = mb->a;
+  volatile u64* vb = mb->b;
+  volatile u64* vr = mb->resp;
+  volatile u32* vrun = &mb->running;
   for (u32 i = 0; i < count; ++i) {
-    mb->u[i] = u[i];
-    mb->n[i] = n[i];
-  }
-  std::atomic_thread_fence(std::memory_order_release);
-  const u64 seq = ++ctx.pick_seq;
-  mb->req = seq;
-  for (u32 spin = 0; mb->resp != seq; ++spin) {
-    if (mb->running == 0) {  // no service (first call, or it idled out): start one
-      mb->running = 1;
-      k_pick_service<<<1, 32, 0, ctx.svc_stream>>>(static_cast<PickMailbox*>(ctx.pick_mbox_d), ctx.d_expm1);
-      TWG_LAUNCHED(ctx);
+    u64 ubits;
+    std::memcpy(&ubits, &u[i], 8);
+    const u64 tag = (++ctx.pick_seq << 2) | static_cast<u64>(kind);
+    va[0] = ubits;
+    va[1] = n[i];
+    vb[1] = pick_check(ubits, n[i], tag);
+    std::atomic_thread_fence(std::memory_order_release);
+    vb[0] = tag;  // posted last
+    for (u32 spin = 0;; ++spin) {
+      if (vr[0] == tag) break;
+      if (*vrun == 0) {  // no service (first call, or it idled out): start one
+        *vrun = 1;
+        k_pick_service<<<1, 32, 0, ctx.svc_stream>>>(static_cast<PickMailbox*>(ctx.pick_mbox_d), ctx.d_expm1);
+        TWG_LAUNCHED(ctx);
+      }
+      if ((spin & 65535) == 65535) {  // a failed service stream surfaces here
+        const cudaError_t e = cudaStreamQuery(ctx.svc_stream);
+        if (e != cudaSuccess && e != cudaErrorNotReady) cuda_check(e, "picker service", __FILE__, __LINE__);
+      }
+      __builtin_ia32_pause();
     }
-    if ((spin & 65535) == 65535) {  // a failed service stream surfaces here
-      const cudaError_t e = cudaStreamQuery(ctx.svc_stream);
-      if (e != cudaSuccess && e != cudaErrorNotReady) cuda_check(e, "picker service", __FILE__, __LINE__);
-    }
-    __builtin_ia32_pause();
+    std::atomic_thread_fence(std::memory_order_acquire);
+    out[i] = vr[1];
   }
-  std::atomic_thread_fence(std::memory_order_acquire);
-  for (u32 i = 0; i < count; ++i) out[i] = mb->out[i];
 }
 
 void pick_weighted_range_batch(Ctx& ctx, const double* d_u, const double* d_prefix, const u64* d_begin,

@@ -811,9 +811,20 @@ class GroupBatchStats:
     edges: int
 
 
+def _load_process_nccl() -> None:
+    """The group resolves NCCL at run time and uses the copy already loaded
+    in the process; when PyTorch is importable it is imported first, so that
+    copy is PyTorch's own (two NCCLs cannot share the libnccl.so.2 soname)."""
+    try:
+        import torch  # noqa: F401
+    except ImportError:
+        pass
+
+
 def group_unique_id() -> bytes:
     """The rendezvous id of a ReplicaGroup (ncclUniqueId): one rank creates
     it and shares it out of band (e.g. a torch.distributed broadcast)."""
+    _load_process_nccl()
     buf = (C.c_uint8 * 128)()
     _call("twg_group_unique_id", C.cast(buf, C.c_void_p))
     return bytes(buf)
@@ -827,6 +838,7 @@ class ReplicaGroup:
 
     def __init__(self, ctx: Context, nranks: int, rank: int, uid: bytes):
         assert len(uid) == 128
+        _load_process_nccl()
         self.ctx = ctx
         self.nranks, self.rank = int(nranks), int(rank)
         ub = (C.c_uint8 * 128).from_buffer_copy(uid)
