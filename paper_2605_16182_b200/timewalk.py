@@ -871,7 +871,7 @@ class ReplicaGroup:
             _call("twg_group_stage_host", self.handle, slot, root, None, 0)
             return
         e = as_edges(batch)
-        self._keep = getattr(self, "_keep", [None, None])
+        self._keep = getattr(self, "_keep", {})
         self._keep[slot] = e  # the H2D reads it asynchronously
         _call("twg_group_stage_host", self.handle, slot, root, _ptr(e), e.shape[0])
 
