@@ -526,44 +526,8 @@ struct InitParams {
   i64 sentinel;
 };
 
-// ts group g of a sampled start (walk_engine.cpp:284-293) for the index
-// biases: draws and closed forms only, no loads (kNoGroup for exp-weight)
-constexpr u64 kNoGroup = ~0ull;
-__device__ __forceinline__ u64 start_group_closed_form(const WalkParams& P, const InitParams& I, u64 wl) {
-  const u64 w = P.walk_begin + wl;
-  const double u1 = P.rng.uniform(w, 0, 0);
-  u32 amb = 0;
-  switch (I.start_bias) {
-    case TWG_UNIFORM: return pick_uniform(u1, P.s.Z);
-    case TWG_LINEAR: return pick_linear(u1, P.s.Z);
-    case TWG_EXPINDEX: return pick_exponential(u1, P.s.Z, P.expm1_tab, &amb);
-    default: return kNoGroup;
-  }
-}
-
-// start the DRAM fetch of group g's bounds (ts_off[g], ts_off[g + 1])
-__device__ __forceinline__ void prefetch_group(const StoreView& s, u64 g) {
-  prefetch_l2(s.ts_off + s.zrg(static_cast<u32>(g)));
-  if (g + 1 < s.Z) prefetch_l2(s.ts_off + s.zrg(static_cast<u32>(g + 1)));
-}
-
-// start the DRAM fetch of snapshot edge i's record
-__device__ __forceinline__ void prefetch_edge(const StoreView& s, u64 i) {
-  const u32 p = s.erg(static_cast<u32>(i));
-  if (s.erec) {
-    prefetch_l2(s.erec + p);
-  } else {
-    prefetch_l2(s.e_src + p);
-    prefetch_l2(s.e_dst + p);
-    prefetch_l2(s.e_t + p);
-  }
-}
-
-// seed_walk + init_walks (walk_engine.cpp:147-155, :247-279). eidx_known:
-// the sampled start edge when the caller already resolved it (pipelined
-// FullWalk), else kNoGroup.
-__device__ __forceinline__ void init_walk(const WalkParams& P, const InitParams& I, u64 wl, WalkReg& r, Ctr* cn,
-                                          u64 eidx_known = kNoGroup) {
+// seed_walk + init_walks (walk_engine.cpp:147-155, :247-279)
+__device__ __forceinline__ void init_walk(const WalkParams& P, const InitParams& I, u64 wl, WalkReg& r, Ctr* cn) {
   const u64 w = P.walk_begin + wl;
   const u64 base = out_index(P, wl, 0), base1 = out_index(P, wl, 1);
   r.prev = 0;
@@ -576,16 +540,9 @@ __device__ __forceinline__ void init_walk(const WalkParams& P, const InitParams&
     r.t = I.sentinel;
     r.len = 1;
   } else {
-    u64 eidx = eidx_known;
-    if (eidx == kNoGroup) {
-      const double u1 = P.rng.uniform(w, 0, 0);
-      const double u2 = P.rng.uniform(w, 0, 1);
-      eidx = sample_start_edge_dev(P.s, I.start_bias, u1, u2, P.expm1_tab, &cn->amb);
-    } else if (I.start_bias == TWG_EXPINDEX) {  // the pipelined pick's ambiguity count belongs to this walk
-      u32 amb = 0;
-      (void)pick_exponential(P.rng.uniform(w, 0, 0), P.s.Z, P.expm1_tab, &amb);
-      cn->amb += amb;
-    }
+    const double u1 = P.rng.uniform(w, 0, 0);
+    const double u2 = P.rng.uniform(w, 0, 1);
+    const u64 eidx = sample_start_edge_dev(P.s, I.start_bias, u1, u2, P.expm1_tab, &cn->amb);
     cn->bytes += 24u + (I.start_bias == TWG_EXPWEIGHT ? 8u * (64u - __clzll(P.s.Z)) : 0u);
     const EdgeRec er = edge_at(P.s, eidx);  // one 128-bit load on streaming stores
     const u32 sv = er.src, dv = er.dst;
@@ -604,16 +561,6 @@ __device__ __forceinline__ void init_walk(const WalkParams& P, const InitParams&
       r.has_prev = 1;
     }
   }
-}
-
-// start edge of walk wl from its (prefetched) group bounds
-__device__ __forceinline__ u64 start_edge_of_group(const WalkParams& P, u64 wl, u64 g) {
-  u64 lo, hi;
-  ts_group_range(P.s, g, lo, hi);
-  const double u2 = P.rng.uniform(P.walk_begin + wl, 0, 1);
-  u64 off = __double2ull_rz(__dmul_rn(u2, __ull2double_rn(hi - lo)));
-  if (off >= hi - lo) off = hi - lo - 1;
-  return lo + off;
 }
 
 // stats[0] walks, [1] hops, [2] max hops (fullwalk steps), [3] ambiguous, [4] algorithmic bytes
@@ -650,35 +597,6 @@ __device__ __forceinline__ void add_stats_block(u64* stats, u32 len, u32 init_le
   }
 }
 
-// the same five totals from per-thread sums (persistent kernels)
-__device__ __forceinline__ void add_totals_block(u64* stats, u64 walks, u64 hops, u64 max_steps, const Ctr& cn) {
-  __shared__ u64 part3[kBlock / 32][5];
-  u64 v[5] = {walks, hops, max_steps, cn.amb, cn.bytes};
-  for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-    for (int q = 0; q < 5; ++q) {
-      const u64 x = __shfl_xor_sync(0xffffffffu, v[q], o);
-      v[q] = q == 2 ? max(v[q], x) : v[q] + x;
-    }
-  }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (lane == 0) {
-#pragma unroll
-    for (int q = 0; q < 5; ++q) part3[warp][q] = v[q];
-  }
-  __syncthreads();
-  if (threadIdx.x < 5) {
-    const int q = threadIdx.x;
-    u64 acc = 0;
-    for (int w = 0; w < kBlock / 32; ++w) acc = q == 2 ? max(acc, part3[w][q]) : acc + part3[w][q];
-    if (acc) {
-      unsigned long long* dst = reinterpret_cast<unsigned long long*>(&stats[q]);
-      if (q == 2) atomicMax(dst, acc);
-      else atomicAdd(dst, acc);
-    }
-  }
-}
-
 __device__ __forceinline__ void add_counters_block(u64* stats, const Ctr& cn) {
   __shared__ u64 part2[kBlock / 32][2];
   u64 a = cn.amb, b = cn.bytes;
@@ -700,38 +618,17 @@ __device__ __forceinline__ void add_counters_block(u64* stats, const Ctr& cn) {
 
 // ---- FullWalk -----------------------------------------------------------------
 
-// Persistent: thread t walks wl = t, t + T, t + 2T, ... (a warp always holds
-// 32 consecutive walks: the slot-major writes stay coalesced). Sampled starts
-// are software-pipelined across a thread's walks: while walk wl runs, the
-// ts-group bounds of walk wl + 2T and the start record of walk wl + T are
-// already on their way into L2 (prefetch.global.L2: no registers held), so
-// a walk's two dependent start gathers are L2 hits instead of two DRAM
-// round trips.
 __global__ void __launch_bounds__(kBlock, 4) k_fullwalk(WalkParams P, InitParams I, u64 count, u32* lengths, u64* stats) {
-  const u64 T = static_cast<u64>(gridDim.x) * blockDim.x;
-  u64 wl = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x;
+  const u64 wl = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x;
+  const bool active = wl < count;
   Ctr cn{0, 0};
-  u64 n_walks = 0, n_hops = 0, max_steps = 0;
-  // the snapshot's time span: anchors of the interpolation search
-  const i64 tl = P.s.m ? edge_time(P.s, 0) - 1 : 0, th = P.s.m ? edge_time(P.s, P.s.m - 1) + 1 : -1;
-  const bool pipe = I.start_mode == 1 && I.start_bias != TWG_EXPWEIGHT;
-  u64 e_cur = kNoGroup;  // start edge of walk wl, resolved one iteration ahead
-  if (pipe) {
-    if (wl < count) prefetch_group(P.s, start_group_closed_form(P, I, wl));
-    if (wl + T < count) prefetch_group(P.s, start_group_closed_form(P, I, wl + T));
-  }
-  for (; wl < count; wl += T) {
-    u64 e_next = kNoGroup;
-    if (pipe) {
-      if (wl + 2 * T < count) prefetch_group(P.s, start_group_closed_form(P, I, wl + 2 * T));
-      if (wl + T < count) {  // its group bounds were prefetched an iteration ago
-        e_next = start_edge_of_group(P, wl + T, start_group_closed_form(P, I, wl + T));
-        prefetch_edge(P.s, e_next);
-      }
-    }
-    WalkReg r{};
-    init_walk(P, I, wl, r, &cn, e_cur);
-    const u32 init_len = r.len;
+  u32 init_len = 0;
+  WalkReg r{};
+  if (active) {
+    init_walk(P, I, wl, r, &cn);
+    init_len = r.len;
+    // the snapshot's time span: anchors of the interpolation search
+    const i64 tl = P.s.m ? edge_time(P.s, 0) - 1 : 0, th = P.s.m ? edge_time(P.s, P.s.m - 1) + 1 : -1;
     while (r.len < P.stride) {
       const NodeMeta a = P.s.nm[r.cur];
       if (!hop(P, wl, r, P.s.mk_time, P.s.mk_start, mark_ring(a), a.gb, a.ge, entry_ring(a), a.eb, a.ee, &cn, tl,
@@ -739,14 +636,8 @@ __global__ void __launch_bounds__(kBlock, 4) k_fullwalk(WalkParams P, InitParams
         break;
     }
     lengths[wl] = r.len;
-    if (r.len >= 2) {
-      ++n_walks;
-      n_hops += r.len - 1;
-    }
-    max_steps = max(max_steps, static_cast<u64>(r.len - init_len));
-    e_cur = e_next;
   }
-  add_totals_block(stats, n_walks, n_hops, max_steps, cn);
+  add_stats_block(stats, r.len, init_len, cn, active);
 }
 
 // ---- Coop scheduler -------------------------------------------------------------
@@ -1134,15 +1025,6 @@ unsigned grid(Ctx& ctx, u64 n) { return grid_for(n, kBlock, static_cast<unsigned
 // the static node2vec adjacency by a scan of the previous node's region).
 Store& walk_store(Ctx&, Store& s, const twg_walk_config&) { return s; }
 
-unsigned fullwalk_ctas_per_sm() {  // TWG_FULLWALK_CTAS overrides (tuning)
-  static const unsigned n = [] {
-    const char* e = std::getenv("TWG_FULLWALK_CTAS");
-    const int v = e ? std::atoi(e) : 0;
-    return v > 0 ? static_cast<unsigned>(v) : 4u;
-  }();
-  return n;
-}
-
 WalkParams make_params(Ctx& ctx, Store& s, const twg_walk_config& cfg, u32 stride, u64 walk_begin, WalkSetDev& out,
                        bool slot_major = false, u64 count = 0) {
   WalkParams P;
@@ -1431,9 +1313,7 @@ WalkSetDev* generate_walks(Ctx& ctx, Store& s_in, const twg_walk_config& cfg, co
   if (count == 0) {
     // nothing to do
   } else if (variant == TWG_FULLWALK) {
-    // persistent: 4 CTAs per SM (the register-limited residency), each thread a strided walk sequence
-    k_fullwalk<<<grid_for(count, kBlock, static_cast<unsigned>(ctx.sm_count) * fullwalk_ctas_per_sm()), kBlock, 0,
-                 st>>>(P, I, count, out->lengths.p, stats.p);
+    k_fullwalk<<<grid_for(count, kBlock, 0xffffffffu), kBlock, 0, st>>>(P, I, count, out->lengths.p, stats.p);
     TWG_LAUNCHED(ctx);
   } else {
     const bool cache = variant == TWG_COOP;
