@@ -134,7 +134,6 @@ typedef struct twg_store_layout {
   uint64_t arena_serial;    /* changes when the arena is replaced (repack) */
   uint64_t relocated_rings; /* rings moved by the ingest that made this snapshot */
   uint64_t max_ring_end;    /* largest logical entry end (ee) over the snapshot's nodes */
-  uint64_t bucket_route;    /* how the producing ingest grouped the batch by node: 1 sorted (radix), 2 segmented scatter */
 } twg_store_layout;
 int twg_store_get_layout(twg_store* s, twg_store_layout* out);
 

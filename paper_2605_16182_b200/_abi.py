@@ -34,7 +34,7 @@ class twg_store_info(C.Structure):
 
 class twg_store_layout(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in ("log_cap", "log_first", "ts_first", "arena_cap", "arena_used",
-                                            "arena_serial", "relocated_rings", "max_ring_end", "bucket_route")]
+                                            "arena_serial", "relocated_rings", "max_ring_end")]
 
 
 class twg_audit_report(C.Structure):

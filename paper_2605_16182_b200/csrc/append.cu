@@ -583,294 +583,12 @@ __global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs a) {
   block_atomic_add(reinterpret_cast<unsigned long long*>(a.q_total), q);
 }
 
-// ---- segmented bucketing (the common streaming shape) ----------------------
-//
-// When the batch's entries spread thinly over the nodes (at most kChunk per
-// 256-node bucket, e.g. the C5 stream: ~1,280), the two stable radix passes
-// that group them by bucket are replaced by ONE scatter into fixed
-// kChunk-slot bucket segments (an atomic cursor per bucket; arrival order is
-// arbitrary), and the placement kernel restores the canonical order inside
-// each bucket in shared memory (group by node, then order each node's
-// entries by edge sequence number — canonical order within a node, ties
-// between the two sides of an undirected self-loop being content-equal).
-// A bucket that would overflow its segment sends the whole batch down the
-// sorted route (nothing has been published; the sorted route recomputes
-// every count).
-
-// batch entry j -> (owner, node-view entry) from the log record
-struct EntryOf {
-  const Rec* rec;
-  Ring br;
-  int mode;
-  u32 seq_b;
-  __device__ __forceinline__ void operator()(u64 j, u32& owner, Entry& e) const {
-    const u32 k = mode == TWG_UNDIRECTED ? static_cast<u32>(j >> 1) : static_cast<u32>(j);
-    const Rec r = rec[br(k)];
-    owner = mode == TWG_UNDIRECTED ? ((j & 1) ? r.dst : r.src) : (mode == TWG_BACKWARD ? r.dst : r.src);
-    e.nbr = nbr_of(mode, r, static_cast<u32>(j));
-    e.edge = seq_b + k;
-    e.t = r.t;
-  }
-};
-
-__global__ void __launch_bounds__(kBlock) k_bucketize(EntryOf in, u64 Yn, u32* cursor, Entry* sval, u8* snode) {
-  for (u64 j = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; j < Yn;
-       j += static_cast<u64>(gridDim.x) * blockDim.x) {
-    u32 owner;
-    Entry e;
-    in(j, owner, e);
-    const u64 b = owner >> kBucketShift;
-    const u32 pos = atomicAdd(&cursor[b], 1u);
-    if (pos < static_cast<u32>(kChunk)) {
-      sval[b * kChunk + pos] = e;
-      snode[b * kChunk + pos] = static_cast<u8>(owner & (kPB - 1));
-    }
-  }
-}
-
-// Per bucket: per-node counts y (owner side), overflow detection, and the
-// population check — a node with batch entries is alive (its batch times
-// are admitted, >= cutoff); any other node must still have its newest
-// incident time (old, merged with the batch's non-owner side) >= cutoff.
-__global__ void __launch_bounds__(kPB) k_seg_count(const u32* cursor, const u8* snode, u64 V, u32* y,
-                                                   const i64* last_t, i64 cutoff, u64* dead, u64* overflow) {
-  __shared__ u32 cnt[kPB];
-  const u64 bkt = blockIdx.x;
-  const u32 n_raw = cursor[bkt];
-  cnt[threadIdx.x] = 0;
-  __syncthreads();
-  if (n_raw > static_cast<u32>(kChunk)) {
-    if (threadIdx.x == 0) atomicAdd(reinterpret_cast<unsigned long long*>(overflow), 1ull);
-    return;
-  }
-  for (u32 i = threadIdx.x; i < n_raw; i += kPB) atomicAdd(&cnt[snode[bkt * kChunk + i]], 1u);
-  __syncthreads();
-  const u64 v = (bkt << kBucketShift) + threadIdx.x;
-  u64 d = 0;
-  if (v < V) {
-    const u32 c = cnt[threadIdx.x];
-    y[v] = c;
-    if (last_t && c == 0 && last_t[v] < cutoff) d = 1;
-  }
-  if (last_t) block_atomic_add(reinterpret_cast<unsigned long long*>(dead), d);
-}
-
-struct SegPlaceArgs {
-  u64 V;
-  u32 seq_b;
-  const NodeMeta* plan;
-  const i64* last_t;    // the live region's newest time (need_last), or null
-  const u32* cursor;
-  const Entry* sval;
-  const u8* snode;
-  Entry* ent;
-  i64* mt;
-  u32* ms;
-  NodeMeta* nm_new;
-  i64* node_last;       // snapshot last_t: the owner side merged here (max of the node's batch times)
-  u64* q_total;
-};
-
-struct SegSmem {  // ~60 KB: 3 CTAs per SM
-  Entry raw[kChunk];        // the bucket's entries in arrival order
-  u8 rnode[kChunk];
-  u16 gidx[kChunk];         // staged (node, canonical) order -> raw index
-  u16 gtmp[kChunk];
-  u8 flag[kChunk];
-  u16 mscan[kChunk];
-  u32 cnt[kPB];
-  u32 off[kPB + 1];
-  u32 cur[kPB], gcur[kPB], base[kPB], cap[kPB], eorg[kPB], gorg[kPB];
-  i64 last_t[kPB];
-  u32 has_last[kPB];
-  u8 expl[kPB];
-  u8 tie[kPB];
-  u32 rwcnt[kChunkItems][kPB / 32];
-  u32 mtotal;
-  u32 nbig;
-  u16 big[kPB];
-};
-
-// One CTA per bucket (thread t <-> node (bucket << 8) + t): the bucket's
-// entries (arrival order) grouped by node with shared-memory counters, each
-// node's run ordered by edge sequence (insertion sort by its thread; a CTA-
-// wide rank sort for runs longer than 32), then mark flags + block scan and
-// node-ordered writes exactly as k_bucket_place does for one chunk.
-__global__ void __launch_bounds__(kPB, 3) k_seg_place(SegPlaceArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  SegSmem& sm = *reinterpret_cast<SegSmem*>(smem_raw);
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const u64 bkt = blockIdx.x;
-  const u64 v = (bkt << kBucketShift) + t;
-  const bool valid = v < a.V;
-  const u32 n = a.cursor[bkt];  // <= kChunk (an overflow sent the batch down the sorted route)
-  NodeMeta p{};
-  i64 lt_v = 0;
-  if (valid) {
-    p = a.plan[v];
-    if (a.last_t) lt_v = a.last_t[v];
-  }
-  sm.cur[t] = p.ee;
-  sm.gcur[t] = p.ge;
-  sm.base[t] = p.base;
-  sm.cap[t] = p.cap;
-  sm.eorg[t] = p.eorg;
-  sm.gorg[t] = p.gorg;
-  const bool has = valid && a.last_t && p.ee > p.eb && n > 0;
-  sm.has_last[t] = has ? 1u : 0u;
-  sm.last_t[t] = has ? lt_v : 0;
-  sm.expl[t] = implicit_marks(p) ? 0 : 1;
-  sm.tie[t] = 0;
-  sm.cnt[t] = 0;
-  if (t == 0) sm.nbig = 0;
-  __syncthreads();
-  const u64 seg = bkt * kChunk;
-  for (u32 i = t; i < n; i += kPB) {
-    sm.raw[i] = a.sval[seg + i];
-    const u8 nd = a.snode[seg + i];
-    sm.rnode[i] = nd;
-    sm.gtmp[i] = static_cast<u16>(atomicAdd(&sm.cnt[nd], 1u));  // slot inside the node's group (any order)
-  }
-  __syncthreads();
-  {
-    u32 total;
-    sm.off[t] = block_excl_scan<u32>(sm.cnt[t], &total);
-    if (t == 0) sm.off[kPB] = total;
-  }
-  __syncthreads();
-  for (u32 i = t; i < n; i += kPB) sm.gidx[sm.off[sm.rnode[i]] + sm.gtmp[i]] = static_cast<u16>(i);
-  __syncthreads();
-  const u32 seq_b = a.seq_b;
-  auto rel = [&](u16 i) { return sm.raw[i].edge - seq_b; };  // batch-relative edge order (u32 wrap-safe)
-  {  // this node's run by edge sequence: insertion sort (runs are short: ~5 entries per node per batch)
-    const u32 o = sm.off[t], c = sm.cnt[t];
-    if (c > 32) {
-      sm.big[atomicAdd(&sm.nbig, 1u)] = static_cast<u16>(t);
-    } else {
-      for (u32 i = 1; i < c; ++i) {
-        const u16 x = sm.gidx[o + i];
-        const u32 kx = rel(x);
-        u32 j = i;
-        while (j > 0 && rel(sm.gidx[o + j - 1]) > kx) {
-          sm.gidx[o + j] = sm.gidx[o + j - 1];
-          --j;
-        }
-        sm.gidx[o + j] = x;
-      }
-    }
-  }
-  __syncthreads();
-  for (u32 q = 0; q < sm.nbig; ++q) {  // long runs (hubs): CTA-wide rank sort, stable on ties
-    const u32 nd = sm.big[q], o = sm.off[nd], c = sm.cnt[nd];
-    for (u32 k = t; k < c; k += kPB) {
-      const u16 x = sm.gidx[o + k];
-      const u32 kx = rel(x);
-      u32 r = 0;
-      for (u32 j = 0; j < c; ++j) {
-        const u32 kj = rel(sm.gidx[o + j]);
-        r += (kj < kx || (kj == kx && j < k)) ? 1u : 0u;
-      }
-      sm.gtmp[r] = x;
-    }
-    __syncthreads();
-    for (u32 k = t; k < c; k += kPB) sm.gidx[o + k] = sm.gtmp[k];
-    __syncthreads();
-  }
-  const u32 lt = (1u << lane) - 1u;
-  // mark flags over the staged order; item i = r*256 + t
-  u32 fl[kChunkItems];
-#pragma unroll
-  for (int r = 0; r < kChunkItems; ++r) {
-    const u32 i = r * kPB + t;
-    u32 f = 0;
-    if (i < n) {
-      const u16 x = sm.gidx[i];
-      const u32 nd = sm.rnode[x];
-      const i64 ti = sm.raw[x].t;
-      if (i == sm.off[nd]) f = (!sm.has_last[nd] || ti != sm.last_t[nd]) ? 1u : 0u;
-      else f = ti != sm.raw[sm.gidx[i - 1]].t ? 1u : 0u;
-      if (!f) sm.tie[nd] = 1;
-    }
-    fl[r] = __ballot_sync(0xffffffffu, f != 0);
-    if (lane == 0) sm.rwcnt[r][warp] = __popc(fl[r]);
-  }
-  __syncthreads();
-  if (warp == 0) {  // exclusive scan of the kChunkItems x 8 counts in item order
-    constexpr int kCounts = kChunkItems * (kPB / 32);
-    u32 carry = 0;
-#pragma unroll
-    for (int base = 0; base < kCounts; base += 32) {
-      const int i = base + lane;
-      const u32 c = i < kCounts ? (&sm.rwcnt[0][0])[i] : 0u;
-      const u32 incl = warp_incl_scan(c);
-      if (i < kCounts) (&sm.rwcnt[0][0])[i] = carry + incl - c;
-      carry += __shfl_sync(0xffffffffu, incl, 31);
-    }
-    if (lane == 0) sm.mtotal = carry;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int r = 0; r < kChunkItems; ++r) {
-    const u32 i = r * kPB + t;
-    sm.mscan[i] = static_cast<u16>(sm.rwcnt[r][warp] + __popc(fl[r] & lt));
-    sm.flag[i] = static_cast<u8>((fl[r] >> lane) & 1u);
-  }
-  if (sm.tie[t] && !sm.expl[t]) {
-    // the region gets a repeated time: its marks become explicit (mark k =
-    // entry k over the live region [eb, cur)); rare
-    const Ring er{sm.base[t], sm.cap[t], sm.eorg[t]}, mr{sm.base[t], sm.cap[t], sm.gorg[t]};
-    for (u32 x = p.eb; x < sm.cur[t]; ++x) {
-      const u32 g = p.gb + (x - p.eb);
-      a.mt[mr(g)] = a.ent[er(x)].t;
-      a.ms[mr(g)] = x;
-    }
-    sm.expl[t] = 1;
-  }
-  __syncthreads();
-  // write out in staged (node) order: a node's new entries are contiguous in its ring
-  for (u32 i = t; i < n; i += kPB) {
-    const u16 x = sm.gidx[i];
-    const u32 nd = sm.rnode[x];
-    const u32 pos = sm.cur[nd] + (i - sm.off[nd]);
-    const Ring er{sm.base[nd], sm.cap[nd], sm.eorg[nd]};
-    const Entry e = sm.raw[x];
-    a.ent[er(pos)] = e;
-    if (sm.flag[i] && sm.expl[nd]) {
-      const Ring mr{sm.base[nd], sm.cap[nd], sm.gorg[nd]};
-      const u32 g = sm.gcur[nd] + (sm.mscan[i] - sm.mscan[sm.off[nd]]);
-      a.mt[mr(g)] = e.t;
-      a.ms[mr(g)] = pos;
-    }
-  }
-  u64 q = 0;
-  if (valid) {
-    const u32 o1 = sm.off[t], c = sm.cnt[t];
-    u32 ee = p.ee, ge = p.ge;
-    if (c) {
-      const u32 mend = o1 + c < n ? sm.mscan[o1 + c] : sm.mtotal;
-      ee += c;
-      ge += mend - sm.mscan[o1];
-      const i64 tl = sm.raw[sm.gidx[o1 + c - 1]].t;  // the node's newest batch time (owner side)
-      if (a.node_last && a.node_last[v] < tl) a.node_last[v] = tl;
-    }
-    const NodeMeta r{p.eb, ee, p.gb, ge, p.base, p.cap, p.eorg, p.gorg};
-    a.nm_new[v] = r;
-    q = r.ge - r.gb;
-  }
-  block_atomic_add(reinterpret_cast<unsigned long long*>(a.q_total), q);
-}
-
 // logical ring end beyond which a ring is rebased (TWG_RING_REBASE lowers it
 // for tests; the default keeps every position below 2^31 + one batch)
 u32 ring_rebase_at() {  // read per batch (one getenv), so a test can lower it mid-process
   const char* e = std::getenv("TWG_RING_REBASE");
   const unsigned long long x = e ? std::strtoull(e, nullptr, 10) : 0ull;
   return x ? static_cast<u32>(std::min<unsigned long long>(x, 0x80000000ull)) : 0x80000000u;
-}
-
-bool segmented_enabled() {  // TWG_SEGMENTED=0 forces the sorted bucket route (A/B and tests)
-  const char* e = std::getenv("TWG_SEGMENTED");
-  return !(e && e[0] == '0');
 }
 
 bool append_enabled() {
@@ -972,87 +690,47 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
                BatchGroupScatter{brec, wr, seq_b, zbase, zbase_dev, log->cap, log->ts_off.p, log->ts_time.p, bt});
   pt.mark("log+ts");
 
-  // 2. batch entries grouped into 256-node buckets: one scatter into
-  //    fixed bucket segments when every bucket fits one (ordered inside the
-  //    bucket at placement), else a stable radix sort of (owner, entry) pairs
-  //    on the owner bits above the bucket (canonical order inside a bucket)
+  // 2. batch entries grouped into 256-node buckets: stable radix sort of
+  //    (owner, entry) pairs on the owner bits above the bucket (canonical
+  //    order inside a bucket), bucket bounds
   const int vb = V > 1 ? bit_width_u64(V - 1) : 0;
   const u64 nb = (V + kPB - 1) / kPB;
-  s->nm.alloc(V, st);
-  DevBuf<u32> ycnt(V, st);
-  // mean bucket load <= 0.8 of a segment (C5: 1,280 of 2,048; a uniform
-  // owner spread then never overflows); a window whose batches overflowed
-  // twice stays on the sorted route
-  bool seg = segmented_enabled() && 5 * Yn <= 4 * nb * kChunk && w.seg_overflows < 2;
-  DevBuf<u32> cursor;
-  DevBuf<Entry> sval;
-  DevBuf<u8> snd;
-  if (seg) {
-    cursor.alloc(nb, st);
-    TWG_CUDA(cudaMemsetAsync(cursor.p, 0, nb * sizeof(u32), st));
-    sval.alloc(nb * kChunk, st);
-    snd.alloc(nb * kChunk, st);
-    k_bucketize<<<grid(ctx, Yn), kBlock, 0, st>>>(EntryOf{brec, wr, mode, seq_b}, Yn, cursor.p, sval.p, snd.p);
+  DevBuf<u32> k0(Yn, st), k1(Yn, st);
+  DevBuf<Entry> v0(Yn, st), v1(Yn, st);
+  u32* kp = k0.p;
+  u32* ka = k1.p;
+  Entry* vp = v0.p;
+  Entry* va = v1.p;
+  if (vb > static_cast<int>(kBucketShift)) {  // the first pass builds (owner, entry) from the log records
+    OwnerIn oin{brec, wr, mode, seq_b};
+    oin.bs = bcols ? bcols[0] : nullptr;
+    oin.bd = bcols ? bcols[1] : nullptr;
+    radix_sort_pairs_from<u32, Entry>(ctx, oin, &kp, &ka, &vp, &va, Yn, vb,
+                                      kBucketShift);
+  } else {
+    k_owner_keys<<<grid(ctx, Yn), kBlock, 0, st>>>(brec, wr, A, mode, seq_b, kp, vp);
     TWG_LAUNCHED(ctx);
-    TWG_CUDA(cudaMemsetAsync(sc + 13, 0, 2 * sizeof(u64), st));
-    k_seg_count<<<static_cast<unsigned>(nb), kPB, 0, st>>>(cursor.p, snd.p, V, ycnt.p,
-                                                          check_dead ? s->last_t.p : nullptr, cutoff, sc + 13,
-                                                          sc + 14);
-    TWG_LAUNCHED(ctx);
-    u64 r2[2];
-    read_scalars(ctx, sc + 13, r2, 2);  // [0] nodes that would leave, [1] overflowing buckets
-    if (check_dead && r2[0]) return nullptr;
-    if (r2[1]) {  // a bucket exceeds its segment: the sorted route for this batch
-      ++w.seg_overflows;
-      seg = false;
-      cursor.release();
-      sval.release();
-      snd.release();
-    }
   }
-  DevBuf<u32> k0, k1, bstart;
-  DevBuf<Entry> v0, v1;
-  u32* kp = nullptr;
-  Entry* vp = nullptr;
-  if (!seg) {
-    k0.alloc(Yn, st);
-    k1.alloc(Yn, st);
-    v0.alloc(Yn, st);
-    v1.alloc(Yn, st);
-    kp = k0.p;
-    u32* ka = k1.p;
-    vp = v0.p;
-    Entry* va = v1.p;
-    if (vb > static_cast<int>(kBucketShift)) {  // the first pass builds (owner, entry) from the log records
-      OwnerIn oin{brec, wr, mode, seq_b};
-      oin.bs = bcols ? bcols[0] : nullptr;
-      oin.bd = bcols ? bcols[1] : nullptr;
-      radix_sort_pairs_from<u32, Entry>(ctx, oin, &kp, &ka, &vp, &va, Yn, vb, kBucketShift);
-    } else {
-      k_owner_keys<<<grid(ctx, Yn), kBlock, 0, st>>>(brec, wr, A, mode, seq_b, kp, vp);
-      TWG_LAUNCHED(ctx);
-    }
-    bstart.alloc(nb + 1, st);
-    k_bucket_bounds<<<grid(ctx, Yn + 1), kBlock, 0, st>>>(kp, Yn, nb, bstart.p);
-    TWG_LAUNCHED(ctx);
-    (kp == k0.p ? k1 : k0).release();  // the pass count decides which buffer holds the result
-    (vp == v0.p ? v1 : v0).release();
-  }
-  pt.mark(seg ? "bucket_scatter" : "bucket_sort");
+  DevBuf<u32> bstart(nb + 1, st);
+  k_bucket_bounds<<<grid(ctx, Yn + 1), kBlock, 0, st>>>(kp, Yn, nb, bstart.p);
+  TWG_LAUNCHED(ctx);
+  (kp == k0.p ? k1 : k0).release();  // the pass count decides which buffer holds the result
+  (vp == v0.p ? v1 : v0).release();
+  pt.mark("bucket_sort");
 
   // 3. per node: eviction, ring room / relocation; then per bucket:
   //    placement, marks, publish
-  if (!seg) {
-    k_bucket_count<<<static_cast<unsigned>(nb), kPB, 0, st>>>(kp, vp, bstart.p, V, ycnt.p, s->last_t.p);
+  s->nm.alloc(V, st);
+  DevBuf<u32> ycnt(V, st);
+  k_bucket_count<<<static_cast<unsigned>(nb), kPB, 0, st>>>(kp, vp, bstart.p, V, ycnt.p, s->last_t.p);
+  TWG_LAUNCHED(ctx);
+  if (check_dead) {  // fast route: the population must not shrink (nothing is published yet)
+    TWG_CUDA(cudaMemsetAsync(sc + 13, 0, sizeof(u64), st));
+    k_count_dead<<<grid(ctx, V), kBlock, 0, st>>>(s->last_t.p, V, cutoff, sc + 13);
     TWG_LAUNCHED(ctx);
-    if (check_dead) {  // fast route: the population must not shrink (nothing is published yet)
-      TWG_CUDA(cudaMemsetAsync(sc + 13, 0, sizeof(u64), st));
-      k_count_dead<<<grid(ctx, V), kBlock, 0, st>>>(s->last_t.p, V, cutoff, sc + 13);
-      TWG_LAUNCHED(ctx);
-      u64 dead[1];
-      read_scalars(ctx, sc + 13, dead, 1);
-      if (dead[0]) return nullptr;
-    }
+    u64 dead[1];
+    read_scalars(ctx, sc + 13, dead, 1);
+    if (dead[0]) return nullptr;
   }
   std::shared_ptr<NodeArena> arena = O.gapped ? O.arena : nullptr;
   // a snapshot older than the retired one still holding this arena may read
@@ -1110,7 +788,6 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
   }
   --nrel;
   s->relocated = nrel;
-  s->bucket_route = seg ? 2 : 1;
   if (nrel) {
     k_reloc_copy<<<grid(ctx, 32 * nrel), kBlock, 0, st>>>(reloc.p, sc, O.nm.p, plan.p, O.ent.p, O.mk_time.p,
                                                           O.mk_start.p, arena->ent.p, arena->mk_time.p,
@@ -1125,29 +802,8 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
   if (!attr_set) {
     TWG_CUDA(cudaFuncSetAttribute(k_bucket_place, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(sizeof(PlaceSmem))));
-    TWG_CUDA(cudaFuncSetAttribute(k_seg_place, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(sizeof(SegSmem))));
     attr_set = true;
   }
-  TWG_CUDA(cudaMemsetAsync(sc + 7, 0, sizeof(u64), st));
-  if (seg) {
-    SegPlaceArgs sp;
-    sp.V = V;
-    sp.seq_b = seq_b;
-    sp.plan = plan.p;
-    sp.last_t = no_ties ? nullptr : last_t.p;
-    sp.cursor = cursor.p;
-    sp.sval = sval.p;
-    sp.snode = snd.p;
-    sp.ent = arena->ent.p;
-    sp.mt = arena->mk_time.p;
-    sp.ms = arena->mk_start.p;
-    sp.nm_new = s->nm.p;
-    sp.node_last = s->last_t.p;
-    sp.q_total = sc + 7;
-    k_seg_place<<<static_cast<unsigned>(nb), kPB, sizeof(SegSmem), st>>>(sp);
-    TWG_LAUNCHED(ctx);
-  } else {
   PlaceArgs pl;
   pl.V = V;
   pl.plan = plan.p;
@@ -1160,9 +816,9 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
   pl.ms = arena->mk_start.p;
   pl.nm_new = s->nm.p;
   pl.q_total = sc + 7;
+  TWG_CUDA(cudaMemsetAsync(sc + 7, 0, sizeof(u64), st));
   k_bucket_place<<<static_cast<unsigned>(nb), kPB, sizeof(PlaceSmem), st>>>(pl);
   TWG_LAUNCHED(ctx);
-  }
   pt.mark("place");
 
   // the one closing read-back: g_cut, batch groups, Q

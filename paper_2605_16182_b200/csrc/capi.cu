@@ -316,7 +316,6 @@ int twg_store_get_layout(twg_store* h, twg_store_layout* out) {
       l.arena_used = s.arena->used;
       l.arena_serial = s.arena->serial;
       l.relocated_rings = s.relocated;
-      l.bucket_route = s.bucket_route;
       if (s.V) {
         TWG_CUDA(cudaMemsetAsync(c.d_scalars, 0, 8, c.stream));
         k_max_ring_end<<<grid_for(s.V, 256, c.sm_count * 8), 256, 0, c.stream>>>(s.nm.p, s.V, c.d_scalars);

@@ -201,7 +201,6 @@ struct Store {
   u64 log_first = 0;  // logical log position of edge 0
   u64 ts_first = 0;   // logical log group position of group 0
   u64 relocated = 0;  // rings moved by the ingest that made this snapshot (diagnostics)
-  u64 bucket_route = 0;  // 1 sorted, 2 segmented (append.cu; diagnostics)
   u32 e_cap = kIdentityCap, e_org = 0, z_cap = kIdentityCap, z_org = 0;  // StoreView::erg / zrg
   DevBuf<double> ts_wtail;  // streaming stores: the nonzero tail of the ts weight prefix
   u64 ts_wt0 = 0;

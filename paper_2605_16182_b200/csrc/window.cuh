@@ -18,7 +18,6 @@ struct Window {
   i64 max_ext = -1;            // largest external id in the current snapshot (dense-id fast path)
   i64 t_high_pending = 0;      // new_high of the batch being ingested
   u32 batch_shape = 0;         // bit0 not time-ordered, bit1 long equal-time runs
-  u32 seg_overflows = 0;       // batches whose bucket segments overflowed (append.cu)
 
   i64 cutoff_for(i64 high) const { return high > duration ? high - duration : 0; }  // window_manager.hpp:51-53
 };

@@ -203,64 +203,3 @@ def test_append_ring_rebase(tw, co, mode, monkeypatch):
     batches = _ordered_stream(57 + mode, 10, 3000, 60, 100)
     n = _run(tw, co, batches, 350, mode, check_walks=True)
     assert n == len(batches) - 1
-
-
-def _thin_stream(seed, nb, n, nodes, step, hub=None, hub_n=0, ties=False):
-    """Time-ordered batches over many nodes (a few entries per node per batch:
-    the segmented bucket route). hub: a node owning hub_n extra entries per
-    batch (a run longer than 32 inside one bucket: the CTA rank sort).
-    ties: times drawn from a narrow range, so nodes get equal-time entries
-    (explicit marks, merged marks across the batch boundary)."""
-    rs = np.random.default_rng(seed)
-    out = []
-    for b in range(nb):
-        span = step // 8 if ties else step
-        t = b * step + rs.integers(0, span, n)
-        s = rs.integers(0, nodes, n)
-        d = rs.integers(0, nodes, n)
-        if hub is not None:
-            s[:hub_n] = hub
-            d[hub_n:2 * hub_n] = hub
-        d[n // 50: n // 25] = s[n // 50: n // 25]  # self-loops
-        e = np.stack([s, d, np.sort(t)], 1)
-        out.append(e[np.lexsort((e[:, 1], e[:, 0], e[:, 2]))])
-    return out
-
-
-@pytest.mark.parametrize("mode", [0, 1, 2])
-@pytest.mark.parametrize("kind", ["plain", "hub", "ties"])
-def test_segmented_route_bit_exact(tw, co, mode, kind):
-    """The segmented bucket route (one scatter into per-bucket segments,
-    canonical order restored in shared memory) against the oracle's full
-    rebuild after every batch: a thin stream over 30K nodes, with a planted
-    hub (runs of 600 entries inside one bucket) or with equal-time entries
-    inside nodes (explicit marks, the batch-boundary mark merge)."""
-    hub = 12345 if kind == "hub" else None
-    batches = _thin_stream(100 + mode, 10, 40000, 30000, 1000, hub=hub, hub_n=600, ties=kind == "ties")
-    exp_stats, exp_dumps = co.window_run(batches, 3500, mode, every=True)
-    w = tw.WindowManager(3500, tw.DirectionMode(mode))
-    routes = []
-    for b, (es, eb), ed in zip(batches, exp_stats, exp_dumps):
-        st = w.ingest_batch(b)
-        assert (st.evicted, st.retained) == (es["evicted"], es["retained"])
-        snap = w.snapshot()
-        routes.append(snap.layout()["bucket_route"] if snap.is_streaming() else 0)
-        assert_store(snap, ed)
-    assert routes.count(2) >= len(batches) - 2, routes
-    _check_walks(tw, co, w.snapshot(), exp_dumps[-1], mode)
-
-
-def test_segmented_equals_sorted_route(tw, co, monkeypatch):
-    """The same stream through both bucket routes gives identical snapshots."""
-    batches = _thin_stream(77, 8, 30000, 20000, 1000)
-    dumps = []
-    for flag in ("1", "0"):
-        monkeypatch.setenv("TWG_SEGMENTED", flag)
-        w = tw.WindowManager(2500)
-        for b in batches:
-            w.ingest_batch(b)
-        snap = w.snapshot()
-        assert snap.layout()["bucket_route"] == (2 if flag == "1" else 1)
-        dumps.append(snap.dump())
-    for k in dumps[0]:
-        assert np.array_equal(dumps[0][k], dumps[1][k]), k
