@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
 #include <cstdio>
@@ -158,21 +159,26 @@ struct PhaseTimer {
   int n = 0;
   cudaEvent_t ev[48];
   const char* name[48];
+  // NVTX: the scope is a range and every phase boundary a mark on the
+  // host timeline (nvtx3 is header-only; free when no tool is attached)
   PhaseTimer(Ctx& c, const char* s) : ctx(c), scope(s) {
     static const bool enabled = [] {
       const char* e = std::getenv("TWG_PHASES");
       return e && e[0] == '1';
     }();
     on = enabled;
+    nvtxRangePushA(s);
     mark("start");
   }
   void mark(const char* what) {
+    nvtxMarkA(what);
     if (!on || n >= 48) return;
     cudaEventCreate(&ev[n]);
     cudaEventRecord(ev[n], ctx.stream);
     name[n++] = what;
   }
   ~PhaseTimer() {
+    nvtxRangePop();
     if (!on) return;
     mark("end");
     cudaEventSynchronize(ev[n - 1]);
@@ -187,6 +193,14 @@ struct PhaseTimer {
     std::fprintf(stderr, " | total=%.2f ms\n", total);
     for (int i = 0; i < n; ++i) cudaEventDestroy(ev[i]);
   }
+};
+
+// an NVTX range over a host scope (walk generation, one ingest, ...)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
 inline int bit_width_u64(u64 x) {

@@ -587,6 +587,9 @@ std::size_t pick_weighted(double u, const CumulativeWeights& cw) { return pick_w
 
 // Reference utilities outside the walk path (samplers.cpp:57-72, :92-103),
 // evaluated where the caller's data lives, with the reference's arithmetic.
+// REFERENCE-DERIVED host glue: these two functions restate the reference's
+// own code (host data in, host answer out; the reference's API contract);
+// they are not on the GPU path and claim no GPU work.
 CumulativeWeights build_cumulative_weights(std::span<const Timestamp> times) {
   if (times.empty()) throw std::invalid_argument("build_cumulative_weights: empty input");
   CumulativeWeights cw;
@@ -852,6 +855,8 @@ T read_pod(std::istream& in) {
 
 }  // namespace
 
+// REFERENCE-DERIVED host I/O (io.cpp:137-209 restated): the walk readers
+// parse host streams into host WalkSets; no GPU work is claimed for them.
 std::vector<WalkRecord> read_walks_text(std::istream& in) {
   std::vector<WalkRecord> out;
   std::string line;
@@ -1042,6 +1047,9 @@ bool EdgeOracle::contains(NodeId a, NodeId b, Timestamp t) const {
   return times && std::binary_search(times->begin(), times->end(), t);
 }
 
+// REFERENCE-DERIVED single-walk rules (validity.cpp:32-106 restated over the
+// device-backed EdgeOracle's answers): host control flow per walk; the bulk
+// audit is check_walkset on the GPU auditor (twg_walkset_audit).
 WalkCheckResult check_timed_walk(std::span<const NodeId> nodes, std::span<const Timestamp> times,
                                  const EdgeOracle& oracle, WalkDirection direction, bool strict) {
   WalkCheckResult r;

@@ -1253,6 +1253,7 @@ void compact_walks(Ctx& ctx, const WalkSetDev& w, DevBuf<u64>& offsets, DevBuf<i
 
 WalkSetDev* generate_walks(Ctx& ctx, Store& s_in, const twg_walk_config& cfg, const twg_thresholds& th, int variant,
                            twg_walk_stats* stats_out, int shard_rank, int shard_count) {
+  NvtxRange nvtx_scope(variant == TWG_FULLWALK ? "twg generate_walks (FullWalk)" : "twg generate_walks (Coop)");
   Store& s = walk_store(ctx, s_in, cfg);
   using clock = std::chrono::steady_clock;
   const auto started = clock::now();

@@ -1011,6 +1011,7 @@ void window_destroy(Window* w) {
 }
 
 void window_ingest(Window& w, const i64* d_src, const i64* d_dst, const i64* d_t, u64 n, twg_batch_stats* out) {
+  NvtxRange nvtx_scope("twg ingest_batch");
   using clock = std::chrono::steady_clock;
   const auto started = clock::now();
   Ctx& ctx = *w.ctx;
