@@ -602,11 +602,17 @@ def run_e2e(args, tw, ctx, wl, rank, world, local_rank, variant, walk_cfg, group
                 path="ReplicaGroup: twg_group_stage_host (rank 0 pinned H2D + 16-B pack) -> NCCL broadcast -> "
                      "twg_group_ingest_staged -> twg_group_generate -> twg_walkset_download_compact")
 
+CPU_SCALE = 0.1
+
+
 def cpu_sample_workload():
-    """Bounded sample of the C5 workload for the CPU reference: same stream
-    law and window/batch ratios at 1/100 scale (N=100K nodes, 500K-edge
-    batches, Δ=span/3 -> ~3.3M-edge window, 100K walks per batch, L=80)."""
-    return Workload(0.01)
+    """The C5 workload for the CPU reference at the SURVEY §8(d) fallback
+    shape, 1/10 scale: same stream law and window/batch ratios (N=1M nodes,
+    5M-edge batches, Δ=span/3 -> ~33M-edge window, 1M walks per batch,
+    L=80). The window is filled by one window-sized batch (the reference's
+    rebuild is O(window) per batch either way, so the steady state is the
+    same); every timed step is one 5M-edge batch + its walks."""
+    return Workload(CPU_SCALE)
 
 
 def run_cpu(steps: int, warmup: int, which: str = "reference"):
@@ -635,13 +641,15 @@ def run_cpu(steps: int, warmup: int, which: str = "reference"):
         L = R.L
         st = C.c_int()
         w = L.twref_window_create(wl.window, 0, C.byref(st))
-        for b in range(wl.prefill + warmup + steps):
+        e = co.gen_stream(wl.nodes, 0, wl.prefill * B, wl.seed)  # the window in one batch
+        bs = BatchStatsC()
+        assert L.twref_window_ingest(w, _p(e), wl.prefill * B, C.byref(bs)) == 0
+        del e
+        for b in range(wl.prefill, wl.prefill + warmup + steps):
             e = co.gen_stream(wl.nodes, b * B, B, wl.seed)
             bs = BatchStatsC()
             rc = L.twref_window_ingest(w, _p(e), B, C.byref(bs))
             assert rc == 0
-            if b < wl.prefill:
-                continue
             snap = L.twref_window_snapshot(w)
             ws = WalkStatsC()
             status = C.c_int()
@@ -660,12 +668,13 @@ def run_cpu(steps: int, warmup: int, which: str = "reference"):
         st = C.c_int()
         Lc = co.L
         w = Lc.two_window_create(wl.window, 0, C.byref(st))
-        for b in range(wl.prefill + warmup + steps):
+        e = co.gen_stream(wl.nodes, 0, wl.prefill * B, wl.seed)
+        bs = BatchStatsC()
+        Lc.two_window_ingest(w, _p(e), wl.prefill * B, C.byref(bs))
+        for b in range(wl.prefill, wl.prefill + warmup + steps):
             e = co.gen_stream(wl.nodes, b * B, B, wl.seed)
             bs = BatchStatsC()
             Lc.two_window_ingest(w, _p(e), B, C.byref(bs))
-            if b < wl.prefill:
-                continue
             from oracle.py import two_window, two_walkset
             store = C.cast(w, C.POINTER(two_window)).contents.store
             out = two_walkset()
@@ -693,9 +702,10 @@ def run_cpu(steps: int, warmup: int, which: str = "reference"):
                 ingest_edges_per_s=edges / ingest_s if ingest_s else 0.0,
                 walk_steps_per_s=hops / walk_s if walk_s else 0.0, total_s=total, hops=hops, edges=edges,
                 kind=kind, cores=cores, cpu_model=cpu_model,
-                sample=f"C5 law at 1/100 scale: N={wl.nodes} nodes, {B}-edge batches, window {wl.window} "
-                       f"time units (~{4 * wl.window} edges), {wl.walks} exp-index walks/batch, L=80; "
-                       f"{steps} timed batches after {wl.prefill} prefill + {warmup} warm-up")
+                sample=f"C5 law at 1/{round(1 / CPU_SCALE)} scale (SURVEY 8d fallback shape): N={wl.nodes} nodes, "
+                       f"{B}-edge batches, window {wl.window} time units (~{4 * wl.window} edges, filled by one "
+                       f"window-sized batch), {wl.walks} exp-index walks/batch, L=80; {steps} timed batches after "
+                       f"{warmup} warm-up; reference timers (BatchStats::rebuild_duration + WalkStats::wall_seconds)")
 
 
 # --------------------------------------------------------------------------- main
@@ -763,7 +773,7 @@ def main():
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
                 "impl": "reference", "edges_per_s": r["edges_per_s"],
-                "config": {**cpu_sample_workload().describe(0.01), "parallelism": "CPU OpenMP"},
+                "config": {**cpu_sample_workload().describe(CPU_SCALE), "parallelism": "CPU OpenMP"},
                 "cpu_baseline": {"value": r["value"], "unit": "walk steps/s", "cores": r["cores"], "kind": r["kind"],
                                  "sample": r["sample"], "cpu_model": r["cpu_model"]},
                 "e2e": {"value": r["value"], "unit": "walk steps/s", "h2d_bytes_per_step": 0,
@@ -784,7 +794,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = run_cpu(2, 0, "reference")
+            cpu = run_cpu(1, 0, "reference")  # one 1/10-scale batch + walks: ~10-30 s of host work
         except Exception as ex:  # the baseline is reported, never the product path
             cpu = {"value": None, "kind": "unavailable", "cores": 0, "sample": str(ex)}
 
