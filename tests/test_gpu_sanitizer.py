@@ -31,5 +31,5 @@ def test_sanitizer_clean(tool):
     cmd += [sys.executable, os.path.join(ROOT, "tools", "sanitize_workload.py")]
     p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=1500)
     out = p.stdout + p.stderr
-    m = re.search(r"ERROR SUMMARY: (\d+) error", out)
+    m = re.search(r"ERROR SUMMARY: (\d+) error", out) or re.search(r"SUMMARY: \d+ hazards displayed \((\d+) error", out)
     assert p.returncode == 0 and "sanitize workload ok" in out and m and int(m.group(1)) == 0, out[-4000:]
