@@ -1358,6 +1358,11 @@ WalkSetDev* generate_walks(Ctx& ctx, Store& s_in, const twg_walk_config& cfg, co
     k_iota<<<grid(ctx, count), kBlock, 0, st>>>(ids_cur, count, n_cur);
     TWG_LAUNCHED(ctx);
     u64 n_alive = count;
+    static const bool trace = [] {
+      const char* e = std::getenv("TWG_COOP_TRACE");
+      return e && e[0] == '1';
+    }();
+    auto t_prev = std::chrono::steady_clock::now();
     while (true) {
       // 1. alive walks per current node (the run lengths W), alive list compacted
       TWG_CUDA(cudaMemsetAsync(ncnt.p, 0, ncnt.bytes(), st));
@@ -1370,6 +1375,14 @@ WalkSetDev* generate_walks(Ctx& ctx, Store& s_in, const twg_walk_config& cfg, co
       TWG_LAUNCHED(ctx);
       u64 sc[3];
       read_scalars(ctx, sc2, sc, 3);
+      if (trace) {
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[twg coop] step %llu alive %llu hub-walks %llu solo-tasks %llu  %.1f us\n",
+                     static_cast<unsigned long long>(coop_steps), static_cast<unsigned long long>(n_alive),
+                     static_cast<unsigned long long>(sc[1]), static_cast<unsigned long long>(sc[2]),
+                     std::chrono::duration<double, std::micro>(now - t_prev).count());
+        t_prev = now;
+      }
       if (sc[0] == 0) break;
       n_alive = sc[0];
       std::swap(ids_cur, ids_next);
