@@ -412,39 +412,20 @@ static_assert(kChunk < 65536, "16-bit chunk counters");
 // and staged in node order in shared memory, mark flags + block scan, then
 // written in node order (a node's new entries / marks are contiguous in its
 // ring, so the stores coalesce); finally publish {eb, ee, gb, ge, ring}.
-__global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs a, u64 nb) {
+__global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PlaceSmem& sm = *reinterpret_cast<PlaceSmem*>(smem_raw);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  u64 q = 0;
-  u64 bkt = blockIdx.x;
-  u32 bs = 0, be = 0;
-  if (bkt < nb) {
-    bs = a.bstart[bkt];
-    be = a.bstart[bkt + 1];
-  }
-  // Persistent: a CTA places buckets bkt, bkt + grid, ...; while it works on
-  // one, the next one's bounds, plan rows, keys and payloads are already on
-  // their way into L2 (prefetch: no registers held), so its dependent
-  // loads hit L2 instead of each paying a DRAM round trip.
-  for (; bkt < nb; bkt += gridDim.x) {
-  const u64 nxt = bkt + gridDim.x;
-  u32 nbs = 0, nbe = 0;
-  if (nxt < nb) {
-    nbs = a.bstart[nxt];
-    nbe = a.bstart[nxt + 1];
-    if ((nxt << kBucketShift) + t < a.V) prefetch_l2(a.plan + (nxt << kBucketShift) + t);
-  }
-  bool next_fetched = nxt >= nb;
+  const u64 bkt = blockIdx.x;
   const u64 v = (bkt << kBucketShift) + t;
   const bool valid = v < a.V;
+  const u32 bs = a.bstart[bkt], be = a.bstart[bkt + 1];
   NodeMeta p{};
   i64 lt_v = 0;
   if (valid) {  // independent loads, in flight together
     p = a.plan[v];
     if (a.last_t) lt_v = a.last_t[v];
   }
-  __syncthreads();  // the previous bucket is done with the shared arrays
   sm.cur[t] = p.ee;
   sm.gcur[t] = p.ge;
   sm.base[t] = p.base;
@@ -474,14 +455,6 @@ __global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs a, u64 nb) {
     }
     for (int i = t; i < (kPB / 32) * kPB; i += kPB) (&sm.wcnt[0][0])[i] = 0;
     sm.tie[t] = 0;
-    if (!next_fetched) {  // the next bucket's keys (4 B) and payloads (16 B), 128-B lines
-      next_fetched = true;
-      const u32 m = nbe - nbs, kl = (m + 31) / 32, vl = (m + 7) / 8;
-      for (u32 j = t; j < kl + vl; j += kPB) {
-        if (j < kl) prefetch_l2(a.keys + nbs + 32 * j);
-        else prefetch_l2(a.vals + nbs + 8 * (j - kl));
-      }
-    }
     __syncthreads();
     // stable rank: warp w owns items [w*R*32, (w+1)*R*32) in R rounds of 32
     u32 rank[kChunkItems];
@@ -600,13 +573,12 @@ __global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs a, u64 nb) {
     }
   }
   __syncthreads();
+
+  u64 q = 0;
   if (valid) {
     const NodeMeta r{p.eb, sm.cur[t], p.gb, sm.gcur[t], p.base, p.cap, p.eorg, p.gorg};
     a.nm_new[v] = r;
-    q += r.ge - r.gb;
-  }
-  bs = nbs;
-  be = nbe;
+    q = r.ge - r.gb;
   }
   block_atomic_add(reinterpret_cast<unsigned long long*>(a.q_total), q);
 }
@@ -617,15 +589,6 @@ u32 ring_rebase_at() {  // read per batch (one getenv), so a test can lower it m
   const char* e = std::getenv("TWG_RING_REBASE");
   const unsigned long long x = e ? std::strtoull(e, nullptr, 10) : 0ull;
   return x ? static_cast<u32>(std::min<unsigned long long>(x, 0x80000000ull)) : 0x80000000u;
-}
-
-u64 place_ctas_per_sm() {  // persistent placement CTAs per SM (TWG_PLACE_CTAS overrides; tuning)
-  static const u64 n = [] {
-    const char* e = std::getenv("TWG_PLACE_CTAS");
-    const int v = e ? std::atoi(e) : 0;
-    return v > 0 ? static_cast<u64>(v) : 4ull;
-  }();
-  return n;
 }
 
 bool append_enabled() {
@@ -854,8 +817,7 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
   pl.nm_new = s->nm.p;
   pl.q_total = sc + 7;
   TWG_CUDA(cudaMemsetAsync(sc + 7, 0, sizeof(u64), st));
-  k_bucket_place<<<static_cast<unsigned>(std::min<u64>(nb, static_cast<u64>(ctx.sm_count) * place_ctas_per_sm())), kPB,
-                   sizeof(PlaceSmem), st>>>(pl, nb);
+  k_bucket_place<<<static_cast<unsigned>(nb), kPB, sizeof(PlaceSmem), st>>>(pl);
   TWG_LAUNCHED(ctx);
   pt.mark("place");
 
