@@ -96,7 +96,10 @@ struct BatchGroupScatter {
   const i64* bt;
   __device__ __forceinline__ void operator()(u64 k, u64 g, u32 f) const {
     if (!f) return;
-    const u64 z = ((zbase_dev ? *zbase_dev : zbase) + g) % cap;
+    // zbase < cap (reduced on the host; the device-resident one is a fresh
+    // log's count, below its capacity) and g < cap: one compare, no division
+    const u64 x = (zbase_dev ? *zbase_dev : zbase) + g;
+    const u64 z = x >= cap ? x - cap : x;
     ts_off[z] = seq_b + static_cast<u32>(k);
     ts_time[z] = bt ? bt[k] : b[br(static_cast<u32>(k))].t;
   }
@@ -687,7 +690,8 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
   const i64* last_surv = nullptr;  // the last survivor's time: the first batch group merges with it on a tie
   if (S) last_surv = O.gapped ? &O.e_rec.p[(O.log_first + O.m - 1) % O.log->cap].t : O.e_t.p + (O.m - 1);
   scan_scatter(ctx, BatchGroupFn{brec, wr, last_surv, bt}, A, sc + 5,
-               BatchGroupScatter{brec, wr, seq_b, zbase, zbase_dev, log->cap, log->ts_off.p, log->ts_time.p, bt});
+               BatchGroupScatter{brec, wr, seq_b, zbase % log->cap, zbase_dev, log->cap, log->ts_off.p,
+                                 log->ts_time.p, bt});
   pt.mark("log+ts");
 
   // 2. batch entries grouped into 256-node buckets: stable radix sort of

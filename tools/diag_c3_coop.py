@@ -15,7 +15,8 @@ store = tw.EdgeStore.build(g, weights=False, adjacency=False, ctx=ctx)
 del g
 cfg = tw.WalkConfig(start_mode=tw.StartMode.Sampled, total_walks=10000000, walk_length=80,
                     bias=tw.BiasKind.LinearIndex, seed=7)
-for v in (tw.Variant.Coop, tw.Variant.FullWalk):
+variants = [tw.Variant(int(x)) for x in sys.argv[1].split(",")] if len(sys.argv) > 1 else [tw.Variant.Coop, tw.Variant.CoopDirect, tw.Variant.FullWalk]
+for v in variants:
     for r in range(2):
         ctx.sync()
         t0 = time.perf_counter()
