@@ -83,16 +83,6 @@ __global__ void __launch_bounds__(kBlock) k_batch_stats(const i64* bs, const i64
   for (u64 tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const u64 base = tile * kStatTile;
     const i64 lo_g = static_cast<i64>(base) - kSegMax;  // global index of st_*[0]
-    {  // the CTA's next tile starts its DRAM fetch into L2 now (consumed one tile later)
-      const u64 nb0 = base + static_cast<u64>(gridDim.x) * kStatTile;
-      if (nb0 < n) {
-        const u64 nlines = (min(static_cast<u64>(kStatTile), n - nb0) * 8 + 127) / 128;  // 128-B lines per column
-        for (u64 q = threadIdx.x; q < 3 * nlines; q += kBlock) {
-          const u64 col = q / nlines, off = (q % nlines) * 16;  // 16 i64 per line
-          prefetch_l2((col == 0 ? bt : col == 1 ? bs : bd) + nb0 + off);
-        }
-      }
-    }
     __syncthreads();
     for (int j = threadIdx.x; j < kStatSpan; j += kBlock) {
       const i64 g = lo_g + j;
@@ -120,29 +110,12 @@ __global__ void __launch_bounds__(kBlock) k_batch_stats(const i64* bs, const i64
       if (i + 1 < n && t > st_t[j + 1]) shape |= 1u;
       if (i + kSegMax < n && t == st_t[j + kSegMax]) shape |= 2u;
       if (rec) {
-        // the equal-time run around edge j: from the warp's ballot of run
-        // starts over its 32 consecutive edges, scanning only for a run that
-        // crosses the warp's window (the lanes of a round hold consecutive edges)
+        int lo = j, hi = j + 1;
         const i64 jn = static_cast<i64>(n) - lo_g;
         const int jmin = lo_g < 0 ? static_cast<int>(-lo_g) : 0;                 // smem index of edge 0
         const int jend = jn < kStatSpan ? static_cast<int>(jn) : kStatSpan;       // of edge n (clamped)
-        const u32 lane = threadIdx.x & 31;
-        const u32 act = __activemask();
-        const bool start = j <= jmin || st_t[j - 1] != t;
-        const u32 starts = __ballot_sync(act, start);
-        const u32 upto = starts & (0xffffffffu >> (31 - lane));                  // run starts at lanes <= lane
-        const u32 after = starts & ~(0xffffffffu >> (31 - lane));                // run starts at lanes > lane
-        int lo, hi;
-        if (upto && ((act >> (31 - __clz(upto))) & 1u)) lo = j - static_cast<int>(lane - (31 - __clz(upto)));
-        else {
-          lo = j;
-          while (lo > jmin && j - lo < kSegMax && st_t[lo - 1] == t) --lo;
-        }
-        if (after) hi = j + static_cast<int>((__ffs(after) - 1) - lane);
-        else {
-          hi = j + 1;
-          while (hi < jend && hi - j < kSegMax && st_t[hi] == t) ++hi;
-        }
+        while (lo > jmin && j - lo < kSegMax && st_t[lo - 1] == t) --lo;
+        while (hi < jend && hi - j < kSegMax && st_t[hi] == t) ++hi;
         const u64 key = (static_cast<u64>(st_a[j]) << 32) | st_b[j];
         u32 rank = 0;
         for (int q = lo; q < hi; ++q) {
