@@ -147,41 +147,62 @@ __device__ __forceinline__ u32 nbr_of(int mode, const Rec& r, u32 j) {
   return (j & 1) ? r.src : r.dst;  // side 1 (owner dst) -> src; self-loops give the owner
 }
 
+// Bucket-sort payloads: the finished node-view entry (16 B), or — when the
+// batch's times span less than 2^32 — the same entry with its time as a u32
+// offset from the batch minimum (12 B: every radix pass and the placement
+// move 16 B per item with the key instead of 20).
+struct alignas(4) PEnt {
+  u32 nbr, edge, dt;
+};
+template <class V>
+struct Payload;
+template <>
+struct Payload<Entry> {
+  __device__ __forceinline__ static Entry make(u32 nbr, u32 edge, i64 t, i64) { return Entry{nbr, edge, t}; }
+  __device__ __forceinline__ static Entry entry(const Entry& e, i64) { return e; }
+  __device__ __forceinline__ static i64 time(const Entry& e, i64) { return e.t; }
+};
+template <>
+struct Payload<PEnt> {
+  __device__ __forceinline__ static PEnt make(u32 nbr, u32 edge, i64 t, i64 tb) {
+    return PEnt{nbr, edge, static_cast<u32>(t - tb)};
+  }
+  __device__ __forceinline__ static Entry entry(const PEnt& e, i64 tb) {
+    return Entry{e.nbr, e.edge, tb + static_cast<i64>(e.dt)};
+  }
+  __device__ __forceinline__ static i64 time(const PEnt& e, i64 tb) { return tb + static_cast<i64>(e.dt); }
+};
+
 // batch entry j: key = owner, payload = the finished node-view entry (carried
 // through the bucket sort, so the placement reads it in order)
-__global__ void k_owner_keys(const Rec* rec, Ring br, u64 A, int mode, u32 seq_b, u32* keys, Entry* vals) {
+template <class V>
+__global__ void k_owner_keys(const Rec* rec, Ring br, u64 A, int mode, u32 seq_b, i64 tb, u32* keys, V* vals) {
   const u64 Yn = mode == TWG_UNDIRECTED ? 2 * A : A;
   for (u64 j = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; j < Yn;
        j += static_cast<u64>(gridDim.x) * blockDim.x) {
     const u32 k = mode == TWG_UNDIRECTED ? static_cast<u32>(j >> 1) : static_cast<u32>(j);
     const Rec r = rec[br(k)];
     keys[j] = mode == TWG_UNDIRECTED ? ((j & 1) ? r.dst : r.src) : (mode == TWG_BACKWARD ? r.dst : r.src);
-    Entry e;
-    e.nbr = nbr_of(mode, r, static_cast<u32>(j));
-    e.edge = seq_b + k;
-    e.t = r.t;
-    vals[j] = e;
+    vals[j] = Payload<V>::make(nbr_of(mode, r, static_cast<u32>(j)), seq_b + k, r.t, tb);
   }
 }
 
 // (owner, node-view entry) of batch entry j, computed from the log records
+template <class V>
 struct OwnerIn {
   const Rec* rec;
   Ring br;
   int mode;
   u32 seq_b;
+  i64 tb;  // time base of a PEnt payload
   __device__ __forceinline__ u32 key(u64 j) const {
     const Rec r = rec[br(mode == TWG_UNDIRECTED ? static_cast<u32>(j >> 1) : static_cast<u32>(j))];
     return mode == TWG_UNDIRECTED ? ((j & 1) ? r.dst : r.src) : (mode == TWG_BACKWARD ? r.dst : r.src);
   }
-  __device__ __forceinline__ Entry val(u64 j) const {
+  __device__ __forceinline__ V val(u64 j) const {
     const u32 k = mode == TWG_UNDIRECTED ? static_cast<u32>(j >> 1) : static_cast<u32>(j);
     const Rec r = rec[br(k)];
-    Entry e;
-    e.nbr = nbr_of(mode, r, static_cast<u32>(j));
-    e.edge = seq_b + k;
-    e.t = r.t;
-    return e;
+    return Payload<V>::make(nbr_of(mode, r, static_cast<u32>(j)), seq_b + k, r.t, tb);
   }
   __device__ __forceinline__ bool has_val() const { return true; }
   __device__ __forceinline__ void prefetch_val(u64) const {}  // the key's record load brings it
@@ -210,8 +231,9 @@ __global__ void k_bucket_bounds(const u32* keys, u64 Yn, u64 nb, u32* bstart) {
 // Per-node batch counts from the bucket-sorted keys (one CTA per bucket),
 // and the owner side of the newest-incident-time update: a node's last entry
 // in the (canonical) bucket order carries its newest batch time.
-__global__ void __launch_bounds__(kPB) k_bucket_count(const u32* keys, const Entry* vals, const u32* bstart, u64 V,
-                                                      u32* y, i64* last_t) {
+template <class PV>
+__global__ void __launch_bounds__(kPB) k_bucket_count(const u32* keys, const PV* vals, const u32* bstart, u64 V,
+                                                      i64 tb, u32* y, i64* last_t) {
   __shared__ u32 cnt[kPB];
   __shared__ u32 lastq[kPB];
   const u64 bkt = blockIdx.x;
@@ -229,7 +251,7 @@ __global__ void __launch_bounds__(kPB) k_bucket_count(const u32* keys, const Ent
   if (v < V) {
     y[v] = cnt[threadIdx.x];
     if (last_t && cnt[threadIdx.x]) {
-      const i64 t = vals[lastq[threadIdx.x] - 1].t;
+      const i64 t = Payload<PV>::time(vals[lastq[threadIdx.x] - 1], tb);
       if (last_t[v] < t) last_t[v] = t;
     }
   }
@@ -378,12 +400,14 @@ __global__ void k_reloc_copy(const Reloc* list, const u64* scal, const NodeMeta*
   }
 }
 
+template <class PV>
 struct PlaceArgs {
   u64 V;
+  i64 tb;  // time base of PEnt payloads
   const NodeMeta* plan;
   const i64* last_t;
   const u32* keys;      // batch entries bucket-sorted (owner >> 8), canonical order inside a bucket
-  const Entry* vals;    // their node-view entries
+  const PV* vals;       // their node-view entries
   const u32* bstart;
   Entry* ent;
   i64* mt;
@@ -415,7 +439,8 @@ static_assert(kChunk < 65536, "16-bit chunk counters");
 // and staged in node order in shared memory, mark flags + block scan, then
 // written in node order (a node's new entries / marks are contiguous in its
 // ring, so the stores coalesce); finally publish {eb, ee, gb, ge, ring}.
-__global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs a) {
+template <class PV>
+__global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs<PV> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PlaceSmem& sm = *reinterpret_cast<PlaceSmem*>(smem_raw);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -493,7 +518,7 @@ __global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs a) {
       if (i < n) {
         const u32 nd = dk[r];
         const u32 sp = sm.off[nd] + sm.wcnt[warp][nd] + rank[r];
-        sm.sent[sp] = a.vals[c0 + i];
+        sm.sent[sp] = Payload<PV>::entry(a.vals[c0 + i], a.tb);
         sm.snode[sp] = static_cast<u8>(nd);
       }
     }
@@ -628,7 +653,7 @@ bool append_log_slot(const Store& O, const Store* R, u64 A, Ring* wr) {
 
 Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const EdgeRec* batch, Ring bring, u64 A,
                      u64 from, i64 cutoff, bool no_ties, bool in_log, bool check_dead, const i64* bt,
-                     const i64* const* bcols) {
+                     const i64* const* bcols, const u64* groups_done, i64 tbase, bool compact) {
   Ctx& ctx = *w.ctx;
   cudaStream_t st = ctx.stream;
   PhaseTimer pt(ctx, "ingest_append");
@@ -689,141 +714,155 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
   const Rec* brec = log->rec.p;  // batch edge k at log slot wr(k) from here on
   const i64* last_surv = nullptr;  // the last survivor's time: the first batch group merges with it on a tie
   if (S) last_surv = O.gapped ? &O.e_rec.p[(O.log_first + O.m - 1) % O.log->cap].t : O.e_t.p + (O.m - 1);
-  scan_scatter(ctx, BatchGroupFn{brec, wr, last_surv, bt}, A, sc + 5,
-               BatchGroupScatter{brec, wr, seq_b, zbase % log->cap, zbase_dev, log->cap, log->ts_off.p,
-                                 log->ts_time.p, bt});
+  if (groups_done) {  // the statistics pass numbered and wrote them (fast route, batch in the log)
+    if (!in_place || !in_log) fail(TWG_ECUDA, "ingest_append: ts groups staged without the log");
+    TWG_CUDA(cudaMemcpyAsync(sc + 5, groups_done, sizeof(u64), cudaMemcpyDeviceToDevice, st));
+  } else {
+    scan_scatter(ctx, BatchGroupFn{brec, wr, last_surv, bt}, A, sc + 5,
+                 BatchGroupScatter{brec, wr, seq_b, zbase % log->cap, zbase_dev, log->cap, log->ts_off.p,
+                                   log->ts_time.p, bt});
+  }
   pt.mark("log+ts");
 
-  // 2. batch entries grouped into 256-node buckets: stable radix sort of
-  //    (owner, entry) pairs on the owner bits above the bucket (canonical
-  //    order inside a bucket), bucket bounds
-  const int vb = V > 1 ? bit_width_u64(V - 1) : 0;
-  const u64 nb = (V + kPB - 1) / kPB;
-  DevBuf<u32> k0(Yn, st), k1(Yn, st);
-  DevBuf<Entry> v0(Yn, st), v1(Yn, st);
-  u32* kp = k0.p;
-  u32* ka = k1.p;
-  Entry* vp = v0.p;
-  Entry* va = v1.p;
-  if (vb > static_cast<int>(kBucketShift)) {  // the first pass builds (owner, entry) from the log records
-    OwnerIn oin{brec, wr, mode, seq_b};
-    oin.bs = bcols ? bcols[0] : nullptr;
-    oin.bd = bcols ? bcols[1] : nullptr;
-    radix_sort_pairs_from<u32, Entry>(ctx, oin, &kp, &ka, &vp, &va, Yn, vb,
-                                      kBucketShift);
-  } else {
-    k_owner_keys<<<grid(ctx, Yn), kBlock, 0, st>>>(brec, wr, A, mode, seq_b, kp, vp);
+  // 2.-3. with the compact 12-B payload when the batch's times span < 2^32
+  std::shared_ptr<NodeArena> arena;
+  auto sort_and_place = [&](auto tag) -> bool {
+    using PV = decltype(tag);
+    // 2. batch entries grouped into 256-node buckets: stable radix sort of
+    //    (owner, entry) pairs on the owner bits above the bucket (canonical
+    //    order inside a bucket), bucket bounds
+    const int vb = V > 1 ? bit_width_u64(V - 1) : 0;
+    const u64 nb = (V + kPB - 1) / kPB;
+    DevBuf<u32> k0(Yn, st), k1(Yn, st);
+    DevBuf<PV> v0(Yn, st), v1(Yn, st);
+    u32* kp = k0.p;
+    u32* ka = k1.p;
+    PV* vp = v0.p;
+    PV* va = v1.p;
+    if (vb > static_cast<int>(kBucketShift)) {  // the first pass builds (owner, entry) from the log records
+      OwnerIn<PV> oin{brec, wr, mode, seq_b, tbase};
+      oin.bs = bcols ? bcols[0] : nullptr;
+      oin.bd = bcols ? bcols[1] : nullptr;
+      radix_sort_pairs_from<u32, PV>(ctx, oin, &kp, &ka, &vp, &va, Yn, vb, kBucketShift);
+    } else {
+      k_owner_keys<PV><<<grid(ctx, Yn), kBlock, 0, st>>>(brec, wr, A, mode, seq_b, tbase, kp, vp);
+      TWG_LAUNCHED(ctx);
+    }
+    DevBuf<u32> bstart(nb + 1, st);
+    k_bucket_bounds<<<grid(ctx, Yn + 1), kBlock, 0, st>>>(kp, Yn, nb, bstart.p);
     TWG_LAUNCHED(ctx);
-  }
-  DevBuf<u32> bstart(nb + 1, st);
-  k_bucket_bounds<<<grid(ctx, Yn + 1), kBlock, 0, st>>>(kp, Yn, nb, bstart.p);
-  TWG_LAUNCHED(ctx);
-  (kp == k0.p ? k1 : k0).release();  // the pass count decides which buffer holds the result
-  (vp == v0.p ? v1 : v0).release();
-  pt.mark("bucket_sort");
+    (kp == k0.p ? k1 : k0).release();  // the pass count decides which buffer holds the result
+    (vp == v0.p ? v1 : v0).release();
+    pt.mark("bucket_sort");
 
-  // 3. per node: eviction, ring room / relocation; then per bucket:
-  //    placement, marks, publish
-  s->nm.alloc(V, st);
-  DevBuf<u32> ycnt(V, st);
-  k_bucket_count<<<static_cast<unsigned>(nb), kPB, 0, st>>>(kp, vp, bstart.p, V, ycnt.p, s->last_t.p);
-  TWG_LAUNCHED(ctx);
-  if (check_dead) {  // fast route: the population must not shrink (nothing is published yet)
-    TWG_CUDA(cudaMemsetAsync(sc + 13, 0, sizeof(u64), st));
-    k_count_dead<<<grid(ctx, V), kBlock, 0, st>>>(s->last_t.p, V, cutoff, sc + 13);
+    // 3. per node: eviction, ring room / relocation; then per bucket:
+    //    placement, marks, publish
+    s->nm.alloc(V, st);
+    DevBuf<u32> ycnt(V, st);
+    k_bucket_count<PV><<<static_cast<unsigned>(nb), kPB, 0, st>>>(kp, vp, bstart.p, V, tbase, ycnt.p, s->last_t.p);
     TWG_LAUNCHED(ctx);
-    u64 dead[1];
-    read_scalars(ctx, sc + 13, dead, 1);
-    if (dead[0]) return nullptr;
-  }
-  std::shared_ptr<NodeArena> arena = O.gapped ? O.arena : nullptr;
-  // a snapshot older than the retired one still holding this arena may read
-  // any slot: then nothing of it is reused (fresh arena)
-  if (arena) {
-    const long expected = 2 + ((R && R->gapped && R->arena == arena) ? 1 : 0);  // O, R, this local copy
-    if (arena.use_count() > expected) arena.reset();
-  }
-  DevBuf<NodeMeta> plan(V, st);
-  DevBuf<i64> last_t(V, st);
-  DevBuf<Reloc> reloc(V, st);
-  auto run_plan = [&](NodeArena& dst, bool all) {
-    TWG_CUDA(cudaMemsetAsync(sc, 0, 3 * sizeof(u64), st));
-    TWG_CUDA(cudaMemcpyAsync(sc, &dst.used, sizeof(u64), cudaMemcpyHostToDevice, st));
-    PlanArgs pa;
-    pa.onm = O.nm.p;
-    pa.rnm = (!all && R && R->gapped && R->arena.get() == &dst) ? R->nm.p : nullptr;
-    pa.V = V;
-    pa.oent = O.ent.p;
-    pa.omt = O.mk_time.p;
-    pa.oms = O.mk_start.p;
-    pa.y = ycnt.p;
-    pa.need_last = no_ties ? 0 : 1;
-    pa.cutoff = cutoff;
-    pa.relocate_all = all ? 1 : 0;
-    pa.rebase_at = ring_rebase_at();
-    pa.arena_cap = dst.cap;
-    pa.plan = plan.p;
-    pa.last_t = last_t.p;
-    pa.reloc = reloc.p;
-    pa.scal = sc;
-    k_plan<<<grid(ctx, V), kBlock, 0, st>>>(pa);
+    if (check_dead) {  // fast route: the population must not shrink (nothing is published yet)
+      TWG_CUDA(cudaMemsetAsync(sc + 13, 0, sizeof(u64), st));
+      k_count_dead<<<grid(ctx, V), kBlock, 0, st>>>(s->last_t.p, V, cutoff, sc + 13);
+      TWG_LAUNCHED(ctx);
+      u64 dead[1];
+      read_scalars(ctx, sc + 13, dead, 1);
+      if (dead[0]) return false;
+    }
+    arena = O.gapped ? O.arena : nullptr;
+    // a snapshot older than the retired one still holding this arena may read
+    // any slot: then nothing of it is reused (fresh arena)
+    if (arena) {
+      const long expected = 2 + ((R && R->gapped && R->arena == arena) ? 1 : 0);  // O, R, this local copy
+      if (arena.use_count() > expected) arena.reset();
+    }
+    DevBuf<NodeMeta> plan(V, st);
+    DevBuf<i64> last_t(V, st);
+    DevBuf<Reloc> reloc(V, st);
+    auto run_plan = [&](NodeArena& dst, bool all) {
+      TWG_CUDA(cudaMemsetAsync(sc, 0, 3 * sizeof(u64), st));
+      TWG_CUDA(cudaMemcpyAsync(sc, &dst.used, sizeof(u64), cudaMemcpyHostToDevice, st));
+      PlanArgs pa;
+      pa.onm = O.nm.p;
+      pa.rnm = (!all && R && R->gapped && R->arena.get() == &dst) ? R->nm.p : nullptr;
+      pa.V = V;
+      pa.oent = O.ent.p;
+      pa.omt = O.mk_time.p;
+      pa.oms = O.mk_start.p;
+      pa.y = ycnt.p;
+      pa.need_last = no_ties ? 0 : 1;
+      pa.cutoff = cutoff;
+      pa.relocate_all = all ? 1 : 0;
+      pa.rebase_at = ring_rebase_at();
+      pa.arena_cap = dst.cap;
+      pa.plan = plan.p;
+      pa.last_t = last_t.p;
+      pa.reloc = reloc.p;
+      pa.scal = sc;
+      k_plan<<<grid(ctx, V), kBlock, 0, st>>>(pa);
+      TWG_LAUNCHED(ctx);
+      u64 r3[3];
+      read_scalars(ctx, sc, r3, 3);
+      dst.used = r3[0];
+      return r3[1] == 0 ? static_cast<u64>(r3[2] & 0xffffffffull) + 1 : 0;  // relocations + 1, 0 = exhausted
+    };
+    bool fresh = false;
+    u64 nrel = arena ? run_plan(*arena, false) : 0;
+    if (nrel == 0) {
+      auto na = std::make_shared<NodeArena>();
+      static std::atomic<u64> serials{0};
+      na->serial = ++serials;
+      na->V = V;
+      na->cap = std::min<u64>((5 * s->P) / 2 + 12 * V + 1024, 0xffffff00ull);  // >= 2 P + 4 V: the repack fits
+      na->ent.alloc(na->cap, st);
+      na->mk_time.alloc(na->cap, st);
+      na->mk_start.alloc(na->cap, st);
+      na->used = 0;
+      arena = std::move(na);
+      nrel = run_plan(*arena, true);
+      if (nrel == 0) fail(TWG_ENOMEM, "ingest: node arena sized below the live regions");
+      fresh = true;
+    }
+    --nrel;
+    s->relocated = nrel;
+    if (nrel) {
+      k_reloc_copy<<<grid(ctx, 32 * nrel), kBlock, 0, st>>>(reloc.p, sc, O.nm.p, plan.p, O.ent.p, O.mk_time.p,
+                                                            O.mk_start.p, arena->ent.p, arena->mk_time.p,
+                                                            arena->mk_start.p);
+      TWG_LAUNCHED(ctx);
+    }
+    reloc.release();
+    pt.mark(fresh ? "plan+repack" : "plan");
+    if (pt.on) std::fprintf(stderr, "[twg phases] relocated rings: %llu of %llu\n", static_cast<unsigned long long>(nrel),
+                            static_cast<unsigned long long>(V));
+    static bool attr_set = false;
+    if (!attr_set) {
+      TWG_CUDA(cudaFuncSetAttribute(k_bucket_place<Entry>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(sizeof(PlaceSmem))));
+      TWG_CUDA(cudaFuncSetAttribute(k_bucket_place<PEnt>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(sizeof(PlaceSmem))));
+      attr_set = true;
+    }
+    PlaceArgs<PV> pl;
+    pl.V = V;
+    pl.tb = tbase;
+    pl.plan = plan.p;
+    pl.last_t = no_ties ? nullptr : last_t.p;
+    pl.keys = kp;
+    pl.vals = vp;
+    pl.bstart = bstart.p;
+    pl.ent = arena->ent.p;
+    pl.mt = arena->mk_time.p;
+    pl.ms = arena->mk_start.p;
+    pl.nm_new = s->nm.p;
+    pl.q_total = sc + 7;
+    TWG_CUDA(cudaMemsetAsync(sc + 7, 0, sizeof(u64), st));
+    k_bucket_place<PV><<<static_cast<unsigned>(nb), kPB, sizeof(PlaceSmem), st>>>(pl);
     TWG_LAUNCHED(ctx);
-    u64 r3[3];
-    read_scalars(ctx, sc, r3, 3);
-    dst.used = r3[0];
-    return r3[1] == 0 ? static_cast<u64>(r3[2] & 0xffffffffull) + 1 : 0;  // relocations + 1, 0 = exhausted
+    pt.mark("place");
+    return true;
   };
-  bool fresh = false;
-  u64 nrel = arena ? run_plan(*arena, false) : 0;
-  if (nrel == 0) {
-    auto na = std::make_shared<NodeArena>();
-    static std::atomic<u64> serials{0};
-    na->serial = ++serials;
-    na->V = V;
-    na->cap = std::min<u64>((5 * s->P) / 2 + 12 * V + 1024, 0xffffff00ull);  // >= 2 P + 4 V: the repack fits
-    na->ent.alloc(na->cap, st);
-    na->mk_time.alloc(na->cap, st);
-    na->mk_start.alloc(na->cap, st);
-    na->used = 0;
-    arena = std::move(na);
-    nrel = run_plan(*arena, true);
-    if (nrel == 0) fail(TWG_ENOMEM, "ingest: node arena sized below the live regions");
-    fresh = true;
-  }
-  --nrel;
-  s->relocated = nrel;
-  if (nrel) {
-    k_reloc_copy<<<grid(ctx, 32 * nrel), kBlock, 0, st>>>(reloc.p, sc, O.nm.p, plan.p, O.ent.p, O.mk_time.p,
-                                                          O.mk_start.p, arena->ent.p, arena->mk_time.p,
-                                                          arena->mk_start.p);
-    TWG_LAUNCHED(ctx);
-  }
-  reloc.release();
-  pt.mark(fresh ? "plan+repack" : "plan");
-  if (pt.on) std::fprintf(stderr, "[twg phases] relocated rings: %llu of %llu\n", static_cast<unsigned long long>(nrel),
-                          static_cast<unsigned long long>(V));
-  static bool attr_set = false;
-  if (!attr_set) {
-    TWG_CUDA(cudaFuncSetAttribute(k_bucket_place, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(sizeof(PlaceSmem))));
-    attr_set = true;
-  }
-  PlaceArgs pl;
-  pl.V = V;
-  pl.plan = plan.p;
-  pl.last_t = no_ties ? nullptr : last_t.p;
-  pl.keys = kp;
-  pl.vals = vp;
-  pl.bstart = bstart.p;
-  pl.ent = arena->ent.p;
-  pl.mt = arena->mk_time.p;
-  pl.ms = arena->mk_start.p;
-  pl.nm_new = s->nm.p;
-  pl.q_total = sc + 7;
-  TWG_CUDA(cudaMemsetAsync(sc + 7, 0, sizeof(u64), st));
-  k_bucket_place<<<static_cast<unsigned>(nb), kPB, sizeof(PlaceSmem), st>>>(pl);
-  TWG_LAUNCHED(ctx);
-  pt.mark("place");
+  if (!(compact ? sort_and_place(PEnt{}) : sort_and_place(Entry{}))) return nullptr;
 
   // the one closing read-back: g_cut, batch groups, Q
   u64 r[4];

@@ -48,6 +48,13 @@ struct WalkParams {
   i64* times;
   const double* exp_neg;
   const double* expm1_tab;
+  // newest time in each node's view (>= every entry time of v's region; the
+  // store's last_t), or null: a forward walk at time t ends at v without
+  // touching v's NodeMeta or ring when last_t[v] <= t (its causal slice is
+  // empty) — every walk's terminal hop costs one small, mostly L2-resident
+  // load instead of a NodeMeta sector plus the ring's end atom
+  const i64* last_t;
+  u64 l2_keep;  // createpolicy evict_last (0: no hint)
 };
 
 // Output cell of (local walk, slot). The device-resident WalkSet is
@@ -618,18 +625,75 @@ __device__ __forceinline__ void add_counters_block(u64* stats, const Ctr& cn) {
 
 // ---- FullWalk -----------------------------------------------------------------
 
-__global__ void __launch_bounds__(kBlock, 4) k_fullwalk(WalkParams P, InitParams I, u64 count, u32* lengths, u64* stats) {
-  const u64 wl = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x;
+// Walk statistics of one warp into one of kStatSlots partial rows (spread
+// over many L2 words: no hot spot when every warp finishes at once, and no
+// block barrier, so a warp whose walks are done never waits for the block's
+// longest walk); k_fold_stats folds the rows into stats[0..4].
+constexpr u32 kStatSlots = 1024;
+__device__ __forceinline__ void add_stats_warp(u64* part, u32 len, u32 init_len, const Ctr& cn, bool active) {
+  u64 v[5] = {active && len >= 2 ? 1ull : 0ull, active && len >= 2 ? len - 1ull : 0ull,
+              active ? static_cast<u64>(len - init_len) : 0ull, cn.amb, cn.bytes};
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      const u64 x = __shfl_xor_sync(0xffffffffu, v[q], o);
+      v[q] = q == 2 ? max(v[q], x) : v[q] + x;
+    }
+  }
+  const u32 lane = threadIdx.x & 31;
+  if (lane < 5) {
+    u64 mine = v[0];
+#pragma unroll
+    for (int q = 1; q < 5; ++q)
+      if (lane == static_cast<u32>(q)) mine = v[q];
+    if (mine) {
+      const u64 warp = (blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x) >> 5;
+      unsigned long long* dst = reinterpret_cast<unsigned long long*>(&part[(warp % kStatSlots) * 8 + lane]);
+      if (lane == 2) atomicMax(dst, mine);
+      else atomicAdd(dst, mine);
+    }
+  }
+}
+
+__global__ void k_fold_stats(const u64* part, u64* stats) {
+  const u32 q = threadIdx.x >> 5, lane = threadIdx.x & 31;  // warp q folds column q
+  if (q >= 5) return;
+  u64 acc = 0;
+  for (u32 r = lane; r < kStatSlots; r += 32) acc = q == 2 ? max(acc, part[r * 8 + q]) : acc + part[r * 8 + q];
+  for (int o = 16; o > 0; o >>= 1) {
+    const u64 x = __shfl_xor_sync(0xffffffffu, acc, o);
+    acc = q == 2 ? max(acc, x) : acc + x;
+  }
+  if (lane == 0) stats[q] = q == 2 ? max(stats[q], acc) : stats[q] + acc;
+}
+
+__device__ __forceinline__ i64 load_last_t(const i64* p, u64 pol) {
+  i64 v;
+  if (pol) asm volatile("ld.global.nc.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+  else v = __ldg(p);
+  return v;
+}
+
+// One thread per walk, init fused, the whole walk in registers
+// (walk_engine.cpp:380-392). kWB-thread blocks (32 by default): a block
+// retires — and its slots take new walks — as soon as its own walks end.
+template <int kWB>
+__global__ void __launch_bounds__(kWB, 1024 / kWB) k_fullwalk(WalkParams P, InitParams I, u64 count, u32* lengths,
+                                                               u64* part) {
+  const u64 wl = blockIdx.x * static_cast<u64>(kWB) + threadIdx.x;
   const bool active = wl < count;
   Ctr cn{0, 0};
   u32 init_len = 0;
   WalkReg r{};
   if (active) {
+    u64 pol = 0;
+    if (P.l2_keep) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     init_walk(P, I, wl, r, &cn);
     init_len = r.len;
     // the snapshot's time span: anchors of the interpolation search
     const i64 tl = P.s.m ? edge_time(P.s, 0) - 1 : 0, th = P.s.m ? edge_time(P.s, P.s.m - 1) + 1 : -1;
     while (r.len < P.stride) {
+      if (P.last_t && load_last_t(P.last_t + r.cur, pol) <= r.t) break;  // nothing later than t at r.cur
       const NodeMeta a = P.s.nm[r.cur];
       if (!hop(P, wl, r, P.s.mk_time, P.s.mk_start, mark_ring(a), a.gb, a.ge, entry_ring(a), a.eb, a.ee, &cn, tl,
                th))
@@ -637,7 +701,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_fullwalk(WalkParams P, InitParams
     }
     lengths[wl] = r.len;
   }
-  add_stats_block(stats, r.len, init_len, cn, active);
+  add_stats_warp(part, r.len, init_len, cn, active);
 }
 
 // ---- Coop scheduler -------------------------------------------------------------
@@ -1025,6 +1089,24 @@ unsigned grid(Ctx& ctx, u64 n) { return grid_for(n, kBlock, static_cast<unsigned
 // the static node2vec adjacency by a scan of the previous node's region).
 Store& walk_store(Ctx&, Store& s, const twg_walk_config&) { return s; }
 
+// FullWalk launch knobs (A/B experiments; defaults are the measured best)
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e && e[0] ? std::atoi(e) : dflt;
+}
+int walk_block() {
+  static const int b = env_int("TWG_WALK_BLOCK", 32);
+  return b;
+}
+bool walk_last_t_filter() {
+  static const bool on = env_int("TWG_WALK_LASTT", 0) != 0;
+  return on;
+}
+u64 walk_l2_keep() {
+  static const u64 k = static_cast<u64>(env_int("TWG_WALK_L2KEEP", 0));
+  return k;
+}
+
 WalkParams make_params(Ctx& ctx, Store& s, const twg_walk_config& cfg, u32 stride, u64 walk_begin, WalkSetDev& out,
                        bool slot_major = false, u64 count = 0) {
   WalkParams P;
@@ -1051,6 +1133,8 @@ WalkParams make_params(Ctx& ctx, Store& s, const twg_walk_config& cfg, u32 strid
   P.times = out.times.p;
   P.exp_neg = ctx.d_exp_neg;
   P.expm1_tab = ctx.d_expm1;
+  P.last_t = nullptr;
+  P.l2_keep = 0;
   return P;
 }
 
@@ -1314,7 +1398,20 @@ WalkSetDev* generate_walks(Ctx& ctx, Store& s_in, const twg_walk_config& cfg, co
   if (count == 0) {
     // nothing to do
   } else if (variant == TWG_FULLWALK) {
-    k_fullwalk<<<grid_for(count, kBlock, 0xffffffffu), kBlock, 0, st>>>(P, I, count, out->lengths.p, stats.p);
+    if (P.dir == 0 && walk_last_t_filter() && s.last_t.p && s.last_t.n >= s.V) P.last_t = s.last_t.p;
+    P.l2_keep = walk_l2_keep();
+    DevBuf<u64> part(kStatSlots * 8, st);
+    TWG_CUDA(cudaMemsetAsync(part.p, 0, part.bytes(), st));
+    const int wb = walk_block();
+    const unsigned g = static_cast<unsigned>((count + wb - 1) / wb);
+    switch (wb) {
+      case 32: k_fullwalk<32><<<g, 32, 0, st>>>(P, I, count, out->lengths.p, part.p); break;
+      case 64: k_fullwalk<64><<<g, 64, 0, st>>>(P, I, count, out->lengths.p, part.p); break;
+      case 128: k_fullwalk<128><<<g, 128, 0, st>>>(P, I, count, out->lengths.p, part.p); break;
+      default: k_fullwalk<256><<<g, 256, 0, st>>>(P, I, count, out->lengths.p, part.p); break;
+    }
+    TWG_LAUNCHED(ctx);
+    k_fold_stats<<<1, 160, 0, st>>>(part.p, stats.p);
     TWG_LAUNCHED(ctx);
   } else {
     const bool cache = variant == TWG_COOP;

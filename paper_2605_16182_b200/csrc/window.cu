@@ -58,6 +58,8 @@ struct FastSpec {
   u64 from = 0;
   const i64* bt = nullptr;  // the batch's time column (device): equals the canonical order's times
   const i64* cols[2] = {nullptr, nullptr};  // its source / target columns (input order)
+  DevBuf<u64> ts_state;  // look-back words of the statistics pass's ts-group numbering
+  bool groups = false;   // the statistics pass wrote the batch's ts groups into the log (total: d_scalars[14])
 };
 
 // scal[8]: batch min t, scal[9]: some id negative.
@@ -68,26 +70,82 @@ struct FastSpec {
 //
 // Tiled: a CTA stages kStatTile edges plus a kSegMax halo on each side in
 // shared memory with coalesced column loads (24 B per edge read once from
-// HBM), then every edge finds its run and its rank from shared memory.
+// HBM; every load of the tile issued before the first shared store), then
+// every edge finds its run and its rank from shared memory.
+//
+// kGroups: the same pass also writes the batch's timestamp groups (the
+// append route's step 1, otherwise a second read of the time column): a
+// group starts at every edge whose time differs from its predecessor's —
+// and at edge 0, since the fast route admits only batches strictly newer
+// than the window — numbered by a decoupled look-back over tiles taken by
+// ticket, written as {start sequence, time} through the log's ts ring.
 constexpr int kStatItems = 8;
 constexpr int kStatTile = kBlock * kStatItems;
 constexpr int kStatSpan = kStatTile + 2 * kSegMax;
+constexpr int kStatRounds = (kStatSpan + kBlock - 1) / kBlock;
+
+bool compact_payload_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TWG_COMPACT_PAYLOAD");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+bool stats_groups_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TWG_STATS_GROUPS");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+struct TsSpec {
+  u64* tile_state;  // tiles + 1 words, zeroed (the last one is the ticket)
+  u32* ts_off;
+  i64* ts_time;
+  u64 zbase;        // ring slot of the batch's first group (< cap)
+  u64 cap;
+  u32 seq_b;        // sequence number of batch edge 0
+  u64* total;       // groups of the batch
+};
+
+template <bool kGroups>
 __global__ void __launch_bounds__(kBlock) k_batch_stats(const i64* bs, const i64* bd, const i64* bt, u64 n, u64* scal,
-                                                        EdgeRec* rec, Ring wr) {
+                                                        EdgeRec* rec, Ring wr, TsSpec ts) {
   __shared__ i64 st_t[kStatSpan];
   __shared__ u32 st_a[kStatSpan], st_b[kStatSpan];
+  __shared__ u32 s_tile;
+  __shared__ u32 s_cnt[kStatItems][kBlock / 32];
+  __shared__ u64 s_prefix;
   i64 mt = kTimeUnset, lt = kTimeInfinite;
   u64 mid = 0;
   u32 shape = 0, neg = 0;
-  const u64 tiles = (n + kStatTile - 1) / kStatTile;
-  for (u64 tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-    const u64 base = tile * kStatTile;
-    const i64 lo_g = static_cast<i64>(base) - kSegMax;  // global index of st_*[0]
+  if (kGroups) {
+    if (threadIdx.x == 0) s_tile = atomicAdd(reinterpret_cast<u32*>(ts.tile_state + gridDim.x), 1u);
     __syncthreads();
-    for (int j = threadIdx.x; j < kStatSpan; j += kBlock) {
+  }
+  const u64 tile = kGroups ? s_tile : blockIdx.x;
+  const u64 base = tile * kStatTile;
+  const i64 lo_g = static_cast<i64>(base) - kSegMax;  // global index of st_*[0]
+  {
+    i64 tv[kStatRounds], av[kStatRounds], bv[kStatRounds];
+#pragma unroll
+    for (int r = 0; r < kStatRounds; ++r) {
+      const int j = threadIdx.x + r * kBlock;
       const i64 g = lo_g + j;
-      if (g >= 0 && static_cast<u64>(g) < n) {
-        const i64 t = bt[g], a = bs[g], b = bd[g];
+      if (j < kStatSpan && g >= 0 && static_cast<u64>(g) < n) {
+        tv[r] = bt[g];
+        av[r] = bs[g];
+        bv[r] = bd[g];
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kStatRounds; ++r) {
+      const int j = threadIdx.x + r * kBlock;
+      const i64 g = lo_g + j;
+      if (j < kStatSpan && g >= 0 && static_cast<u64>(g) < n) {
+        const i64 t = tv[r], a = av[r], b = bv[r];
         st_t[j] = t;
         st_a[j] = static_cast<u32>(a);
         st_b[j] = static_cast<u32>(b);
@@ -100,30 +158,101 @@ __global__ void __launch_bounds__(kBlock) k_batch_stats(const i64* bs, const i64
         }
       }
     }
-    __syncthreads();
-#pragma unroll 2
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  u32 gbal[kStatItems];
+  if (kGroups) {
+    // group starts first, and the tile's count posted at once: the
+    // successors' look-backs wait on it while this tile ranks its runs
+#pragma unroll
     for (int k = 0; k < kStatItems; ++k) {
-      const int j = kSegMax + k * kBlock + threadIdx.x;  // smem index of edge i
+      const int j = kSegMax + k * kBlock + threadIdx.x;
       const u64 i = base + k * kBlock + threadIdx.x;
-      if (i >= n) break;
-      const i64 t = st_t[j];
-      if (i + 1 < n && t > st_t[j + 1]) shape |= 1u;
-      if (i + kSegMax < n && t == st_t[j + kSegMax]) shape |= 2u;
-      if (rec) {
-        int lo = j, hi = j + 1;
-        const i64 jn = static_cast<i64>(n) - lo_g;
-        const int jmin = lo_g < 0 ? static_cast<int>(-lo_g) : 0;                 // smem index of edge 0
-        const int jend = jn < kStatSpan ? static_cast<int>(jn) : kStatSpan;       // of edge n (clamped)
-        while (lo > jmin && j - lo < kSegMax && st_t[lo - 1] == t) --lo;
-        while (hi < jend && hi - j < kSegMax && st_t[hi] == t) ++hi;
-        const u64 key = (static_cast<u64>(st_a[j]) << 32) | st_b[j];
-        u32 rank = 0;
-        for (int q = lo; q < hi; ++q) {
-          const u64 kq = (static_cast<u64>(st_a[q]) << 32) | st_b[q];
-          rank += (kq < key || (kq == key && q < j)) ? 1u : 0u;
+      gbal[k] = __ballot_sync(0xffffffffu, i < n && (i == 0 || st_t[j] != st_t[j - 1]));
+      if (lane == 0) s_cnt[k][warp] = __popc(gbal[k]);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // exclusive offsets of (round, warp) in position order
+      u32 acc = 0;
+      for (int k = 0; k < kStatItems; ++k)
+        for (int w = 0; w < kBlock / 32; ++w) {
+          const u32 c = s_cnt[k][w];
+          s_cnt[k][w] = acc;
+          acc += c;
         }
-        rec[wr(static_cast<u32>(lo_g + lo + rank))] = EdgeRec{st_a[j], st_b[j], t};
+      s_prefix = acc;
+      lb_store(ts.tile_state + tile, (tile == 0 ? kLbInclusive : kLbAggregate) | acc);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int k = 0; k < kStatItems; ++k) {
+    const int j = kSegMax + k * kBlock + threadIdx.x;  // smem index of edge i
+    const u64 i = base + k * kBlock + threadIdx.x;
+    if (i >= n) continue;
+    const i64 t = st_t[j];
+    if (i + 1 < n && t > st_t[j + 1]) shape |= 1u;
+    if (i + kSegMax < n && t == st_t[j + kSegMax]) shape |= 2u;
+    if (rec) {
+      int lo = j, hi = j + 1;
+      const i64 jn = static_cast<i64>(n) - lo_g;
+      const int jmin = lo_g < 0 ? static_cast<int>(-lo_g) : 0;                 // smem index of edge 0
+      const int jend = jn < kStatSpan ? static_cast<int>(jn) : kStatSpan;       // of edge n (clamped)
+      while (lo > jmin && j - lo < kSegMax && st_t[lo - 1] == t) --lo;
+      while (hi < jend && hi - j < kSegMax && st_t[hi] == t) ++hi;
+      const u64 key = (static_cast<u64>(st_a[j]) << 32) | st_b[j];
+      u32 rank = 0;
+      for (int q = lo; q < hi; ++q) {
+        const u64 kq = (static_cast<u64>(st_a[q]) << 32) | st_b[q];
+        rank += (kq < key || (kq == key && q < j)) ? 1u : 0u;
       }
+      rec[wr(static_cast<u32>(lo_g + lo + rank))] = EdgeRec{st_a[j], st_b[j], t};
+    }
+  }
+  if (kGroups) {
+    if (warp == 0) {  // warp-parallel decoupled look-back (as k_scan_scatter)
+      const u64 agg = s_prefix;
+      u64* st = ts.tile_state;
+      u64 prefix = 0;
+      if (tile > 0) {
+        long long p = static_cast<long long>(tile) - 1;
+        while (true) {
+          const long long idx = p - lane;
+          u64 sv = kLbInclusive;
+          if (idx >= 0) {
+            do {
+              sv = lb_load(st + idx);
+            } while ((sv >> 62) == 0);
+          }
+          const u32 incl = __ballot_sync(0xffffffffu, (sv >> 62) == 2);
+          const int stop = incl ? __ffs(incl) - 1 : 31;
+          u64 v = lane <= stop ? (sv & kLbValueMask) : 0;
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          prefix += v;
+          if (incl) break;
+          p -= 32;
+        }
+        if (lane == 0) lb_store(st + tile, kLbInclusive | (prefix + agg));
+      }
+      __syncwarp();
+      if (lane == 0) {
+        if (base + kStatTile >= n) *ts.total = prefix + agg;
+        s_prefix = prefix;
+      }
+    }
+    __syncthreads();
+    const u64 pre = s_prefix;
+    const u32 lt32 = (1u << lane) - 1u;
+#pragma unroll
+    for (int k = 0; k < kStatItems; ++k) {
+      if (!(gbal[k] >> lane & 1u)) continue;
+      const int j = kSegMax + k * kBlock + threadIdx.x;
+      const u64 i = base + k * kBlock + threadIdx.x;
+      const u64 x = ts.zbase + pre + s_cnt[k][warp] + __popc(gbal[k] & lt32);
+      const u64 z = x >= ts.cap ? x - ts.cap : x;
+      ts.ts_off[z] = ts.seq_b + static_cast<u32>(i);
+      ts.ts_time[z] = st_t[j];
     }
   }
   // one set of atomics per block (the whole grid finishes at once: per-warp
@@ -972,7 +1101,8 @@ Store* ingest_fast(Window& w, FastSpec& spec, u64 n, const u64* sc, i64 cutoff, 
   w.max_ext = static_cast<i64>(V - 1);
   Store* out =
       ingest_append(w, O, std::move(s), spec.rec, spec.wring, n, from, cutoff, true, spec.in_log, true, spec.bt,
-                    spec.cols);
+                    spec.cols, spec.groups ? ctx.d_scalars + 14 : nullptr, batch_min,
+                    compact_payload_enabled() && static_cast<u64>(static_cast<i64>(sc[0]) - batch_min) < (1ull << 32));
   if (!out) {  // an old node leaves the window: the general route recomputes everything
     stats->evicted = stats->dropped_late = 0;
     return nullptr;
@@ -1049,8 +1179,21 @@ void window_ingest(Window& w, const i64* d_src, const i64* d_dst, const i64* d_t
     }
     TWG_CUDA(cudaMemsetAsync(ctx.d_scalars + 12, 0, 8, st));
   }
-  k_batch_stats<<<grid_for((n + kStatTile - 1) / kStatTile, 1, static_cast<unsigned>(ctx.sm_count) * 8), kBlock, 0, st>>>(
-      d_src, d_dst, d_t, n, ctx.d_scalars, spec.rec, spec.wring);
+  const u64 stat_tiles = (n + kStatTile - 1) / kStatTile;
+  TsSpec ts{};
+  spec.groups = spec.on && spec.in_log && stats_groups_enabled();
+  if (spec.groups) {
+    const EdgeLog& L = *old.log;
+    spec.ts_state.alloc(stat_tiles + 1, st);
+    TWG_CUDA(cudaMemsetAsync(spec.ts_state.p, 0, spec.ts_state.bytes(), st));
+    ts = TsSpec{spec.ts_state.p, L.ts_off.p, L.ts_time.p, L.zlen % L.cap, L.cap,
+                old.seq0 + static_cast<u32>(old.m), ctx.d_scalars + 14};
+    k_batch_stats<true><<<static_cast<unsigned>(stat_tiles), kBlock, 0, st>>>(d_src, d_dst, d_t, n, ctx.d_scalars,
+                                                                              spec.rec, spec.wring, ts);
+  } else {
+    k_batch_stats<false><<<static_cast<unsigned>(stat_tiles), kBlock, 0, st>>>(d_src, d_dst, d_t, n, ctx.d_scalars,
+                                                                               spec.rec, spec.wring, ts);
+  }
   TWG_LAUNCHED(ctx);
   if (spec.on) {
     k_lower_bound_cut<<<1, 1, 0, st>>>(old.view(), w.t_high, w.duration, ctx.d_scalars, ctx.d_scalars + 12);
