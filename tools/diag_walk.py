@@ -12,6 +12,7 @@ from bench import Workload
 scale = float(sys.argv[1]) if len(sys.argv) > 1 else 1.0
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 variants = sys.argv[3].split(",") if len(sys.argv) > 3 else ["fullwalk"]
+walk_length = int(sys.argv[4]) if len(sys.argv) > 4 else 80
 wl = Workload(scale)
 ctx = tw.Context(0)
 lib = tw._abi.load()
@@ -25,7 +26,7 @@ for b in range(wl.prefill + 1):
 snap = w.snapshot()
 print("window edges", snap.edge_count(), "nodes", snap.node_count(), flush=True)
 stream = torch.cuda.ExternalStream(ctx.stream)
-cfg = tw.WalkConfig(walk_length=80, start_mode=tw.StartMode.Sampled, total_walks=wl.walks,
+cfg = tw.WalkConfig(walk_length=walk_length, start_mode=tw.StartMode.Sampled, total_walks=wl.walks,
                     bias=tw.BiasKind.ExponentialIndex, seed=5)
 for v in variants:
     var = {"fullwalk": tw.Variant.FullWalk, "coop": tw.Variant.Coop, "coopdirect": tw.Variant.CoopDirect}[v]
