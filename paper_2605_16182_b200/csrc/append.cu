@@ -413,6 +413,8 @@ struct PlaceArgs {
   i64* mt;
   u32* ms;
   NodeMeta* nm_new;
+  WalkRec* wrec_new;
+  const WalkRec* owrec;  // the previous snapshot's walk records (null: read its tail from the ring)
   u64* q_total;
 };
 
@@ -426,6 +428,9 @@ struct PlaceSmem {  // ~34 KB: 6 CTAs per SM
   u8 tie[kPB];   // this chunk holds an entry of the node that continues a group
   u32 mtotal;
   u32 rwcnt[kChunkItems][kPB / 32];
+  u32 tcnt[kPB];              // node's new entries so far
+  u32 tn[kWalkTail][kPB];     // its newest ones (newest first): neighbour
+  i64 tt[kWalkTail][kPB];     // and time
   u8 snode[kChunk];
   u8 flag[kChunk];
   u16 mscan[kChunk];
@@ -466,6 +471,10 @@ __global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs<PV> a) {
   sm.expl[t] = implicit_marks(p) ? 0 : 1;
 
   const u32 lt = (1u << lane) - 1u;
+  // node t's newest new entries so far (newest first), for its walk record
+  sm.tcnt[t] = 0;
+#pragma unroll
+  for (u32 i = 0; i < kWalkTail; ++i) sm.tn[i][t] = 0, sm.tt[i][t] = 0;
   for (u32 c0 = bs; c0 < be; c0 += kChunk) {
     const u32 n = min(static_cast<u32>(kChunk), be - c0);
     __syncthreads();
@@ -597,6 +606,18 @@ __global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs<PV> a) {
         sm.gcur[t] += mend - sm.mscan[o1];
         sm.last_t[t] = sm.sent[o1 + c - 1].t;
         sm.has_last[t] = 1u;
+        // shift the tail by min(c, kWalkTail) and take this chunk's newest entries
+        for (int i = kWalkTail - 1; i >= 0; --i) {
+          if (static_cast<u32>(i) < c) {
+            const Entry e = sm.sent[o1 + c - 1 - i];
+            sm.tn[i][t] = e.nbr;
+            sm.tt[i][t] = e.t;
+          } else {
+            sm.tn[i][t] = sm.tn[i - c][t];
+            sm.tt[i][t] = sm.tt[i - c][t];
+          }
+        }
+        sm.tcnt[t] += c;
       }
     }
   }
@@ -607,6 +628,49 @@ __global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs<PV> a) {
     const NodeMeta r{p.eb, sm.cur[t], p.gb, sm.gcur[t], p.base, p.cap, p.eorg, p.gorg};
     a.nm_new[v] = r;
     q = r.ge - r.gb;
+    // the walk record: the newest entries read back from the ring (this
+    // CTA's writes are visible after the barrier; the older ones share the
+    // lines the appends just touched)
+    WalkRec w;
+    w.eb = r.eb;
+    w.ee = r.ee;
+    w.base = r.base;
+    w.cap = r.cap;
+    w.eorg = r.eorg;
+    w.g = r.ge - r.gb;
+    w.pad = 0;
+    // the tail: this batch's newest entries, then (when fewer than the
+    // tail) the previous snapshot's newest ones — from its walk record, or
+    // from the ring when it has none
+#pragma unroll
+    for (u32 i = 0; i < kWalkTail; ++i) w.nbr[i] = sm.tn[i][t], w.t[i] = sm.tt[i][t];
+    const u32 tcnt = sm.tcnt[t];
+    const u32 k = min(r.ee - r.eb, kWalkTail);
+    if (tcnt < k) {
+      const Ring er = entry_ring(r);
+      WalkRec o;
+      if (a.owrec) o = a.owrec[v];
+#pragma unroll
+      for (u32 i = 0; i < kWalkTail; ++i) {
+        if (i >= tcnt && i < k) {
+          const u32 j = i - tcnt;  // j-th newest entry before this batch's
+          u32 nb;
+          i64 tj;
+          if (a.owrec) {
+            nb = j == 0 ? o.nbr[0] : j == 1 ? o.nbr[1] : o.nbr[2];
+            tj = j == 0 ? o.t[0] : j == 1 ? o.t[1] : o.t[2];
+          } else {
+            const Entry e = a.ent[er(p.ee - 1 - j)];
+            nb = e.nbr;
+            tj = e.t;
+          }
+          if (i == 0) w.nbr[0] = nb, w.t[0] = tj;
+          else if (i == 1) w.nbr[1] = nb, w.t[1] = tj;
+          else w.nbr[2] = nb, w.t[2] = tj;
+        }
+      }
+    }
+    a.wrec_new[v] = w;
   }
   block_atomic_add(reinterpret_cast<unsigned long long*>(a.q_total), q);
 }
@@ -758,6 +822,7 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
     // 3. per node: eviction, ring room / relocation; then per bucket:
     //    placement, marks, publish
     s->nm.alloc(V, st);
+    s->wrec.alloc(V, st);
     DevBuf<u32> ycnt(V, st);
     k_bucket_count<PV><<<static_cast<unsigned>(nb), kPB, 0, st>>>(kp, vp, bstart.p, V, tbase, ycnt.p, s->last_t.p);
     TWG_LAUNCHED(ctx);
@@ -855,6 +920,8 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
     pl.mt = arena->mk_time.p;
     pl.ms = arena->mk_start.p;
     pl.nm_new = s->nm.p;
+    pl.wrec_new = s->wrec.p;
+    pl.owrec = O.wrec.n >= V ? O.wrec.p : nullptr;
     pl.q_total = sc + 7;
     TWG_CUDA(cudaMemsetAsync(sc + 7, 0, sizeof(u64), st));
     k_bucket_place<PV><<<static_cast<unsigned>(nb), kPB, sizeof(PlaceSmem), st>>>(pl);

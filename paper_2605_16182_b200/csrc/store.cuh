@@ -52,6 +52,24 @@ struct alignas(32) NodeMeta {
 };
 static_assert(sizeof(NodeMeta) == 32, "NodeMeta must be one 32-byte sector");
 
+// Walk record of a streaming snapshot's node (64 B, one DRAM line access
+// per hop — a random access moves a whole line, so the line carries what a
+// forward hop usually needs beyond the bounds): the entry ring, the mark
+// count, and the node's kWalkTail newest entries (newest first). A forward
+// walk at time t whose causal slice starts inside the tail (t at or after the
+// tail's oldest time — later hops, which move to the newest times, and every
+// terminal hop) and whose pick lands in it never touches the ring.
+constexpr u32 kWalkTail = 3;
+struct alignas(64) WalkRec {
+  u32 eb, ee;           // logical entry bounds
+  u32 base, cap, eorg;  // entry ring
+  u32 g;                // marks (ge - gb)
+  u32 nbr[kWalkTail];   // nbr[i]: neighbour of entry ee - 1 - i (i < min(kWalkTail, ee - eb))
+  u32 pad;
+  i64 t[kWalkTail];     // its time
+};
+static_assert(sizeof(WalkRec) == 64, "WalkRec must be 64 bytes");
+
 struct Ring {
   u32 base, cap, org;
   __device__ __forceinline__ u32 operator()(u32 x) const {
@@ -104,6 +122,7 @@ struct StoreView {
   // ts_wtail[g - ts_wt0] for groups g >= ts_wt0 (every earlier value is +0)
   const double* ts_wtail;
   u64 ts_wt0;
+  const WalkRec* wrec;  // streaming stores built by the append route: per-node walk records (else null)
 };
 
 // snapshot edge i
@@ -193,6 +212,7 @@ struct Store {
   DevBuf<i64> last_t; // newest incident edge time per node: v survives a cutoff c iff last_t[v] >= c
   bool last_t_exact = true;  // false: a lower bound (the streaming route tracks only the owner side)
   DevBuf<NodeMeta> nm;  // per-node bounds + ring: the walk kernels' node meta (every store)
+  DevBuf<WalkRec> wrec; // append-route snapshots: nm + the newest entries per node (forward walks)
   u32 seq0 = 0;       // sequence number of edge 0 (StoreView)
   // streaming representation (gapped == true): slices of a shared log/arena
   bool gapped = false;
@@ -214,13 +234,13 @@ struct Store {
                      e_src.p,  e_dst.p,   e_t.p,     e_rec.p,    ext.p,     ts_off.p,  ts_time.p,
                      ts_w.p,   nmeta.p,   nm.p,      mk_time.p,  mk_start.p, ent.p,   wp.p,
                      adj_off.p, adj.p,  ext_identity ? 1 : 0, seq0,
-                     Ring{0u, e_cap, e_org}, Ring{0u, z_cap, z_org}, ts_wtail.p, ts_wt0};
+                     Ring{0u, e_cap, e_org}, Ring{0u, z_cap, z_org}, ts_wtail.p, ts_wt0, wrec.p};
   }
   u64 device_bytes() const {
     return e_src.bytes() + e_dst.bytes() + e_t.bytes() + e_rec.bytes() + ext.bytes() + ts_off.bytes() +
            ts_time.bytes() + ts_w.bytes() + nmeta.bytes() + mk_time.bytes() + mk_start.bytes() +
            ent.bytes() + wp.bytes() + adj_off.bytes() + adj.bytes() + owner.bytes() + nm.bytes() +
-           last_t.bytes();
+           last_t.bytes() + wrec.bytes();
   }
 };
 

@@ -55,6 +55,7 @@ struct WalkParams {
   // load instead of a NodeMeta sector plus the ring's end atom
   const i64* last_t;
   u64 l2_keep;  // createpolicy evict_last (0: no hint)
+  int rec;      // hop through the store's walk records (hop_rec)
 };
 
 // Output cell of (local walk, slot). The device-resident WalkSet is
@@ -489,6 +490,89 @@ __device__ __forceinline__ bool hop(const WalkParams& P, u64 wl, WalkReg& r, con
   return true;
 }
 
+// One forward hop through the node's walk record (walk_engine.cpp:88-145 for
+// the index pickers): the causal slice starts inside the record's tail when t
+// is at or after the tail's oldest time (or the tail is the whole region);
+// otherwise the ring is searched over [eb, tail) — the entry at the tail's
+// start is later than t, so the slice starts at or before it. The pick
+// reads the ring only when it lands before the tail. Same c, e, draw and
+// entry as hop(): byte-identical walks.
+__device__ __forceinline__ WalkRec load_wrec(const WalkRec* p) {
+  const int4* q = reinterpret_cast<const int4*>(p);
+  const int4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2), d = __ldg(q + 3);
+  WalkRec w;
+  w.eb = static_cast<u32>(a.x);
+  w.ee = static_cast<u32>(a.y);
+  w.base = static_cast<u32>(a.z);
+  w.cap = static_cast<u32>(a.w);
+  w.eorg = static_cast<u32>(b.x);
+  w.g = static_cast<u32>(b.y);
+  w.nbr[0] = static_cast<u32>(b.z);
+  w.nbr[1] = static_cast<u32>(b.w);
+  w.nbr[2] = static_cast<u32>(c.x);
+  w.pad = static_cast<u32>(c.y);
+  w.t[0] = static_cast<i64>((static_cast<u64>(static_cast<u32>(c.w)) << 32) | static_cast<u32>(c.z));
+  w.t[1] = static_cast<i64>((static_cast<u64>(static_cast<u32>(d.y)) << 32) | static_cast<u32>(d.x));
+  w.t[2] = static_cast<i64>((static_cast<u64>(static_cast<u32>(d.w)) << 32) | static_cast<u32>(d.z));
+  return w;
+}
+static_assert(kWalkTail == 3, "load_wrec / tail selects assume three tail entries");
+__device__ __forceinline__ i64 tail_time(const WalkRec& R, u32 i) { return i == 0 ? R.t[0] : i == 1 ? R.t[1] : R.t[2]; }
+__device__ __forceinline__ u32 tail_nbr(const WalkRec& R, u32 i) {
+  return i == 0 ? R.nbr[0] : i == 1 ? R.nbr[1] : R.nbr[2];
+}
+
+__device__ __forceinline__ bool hop_rec(const WalkParams& P, u64 wl, WalkReg& r, const WalkRec& R, Ctr* cn, i64 tl) {
+  const u32 lo = R.eb, hi = R.ee;
+  if (lo == hi || r.t >= R.t[0]) return false;  // nothing later than t (R.t[0] is the newest time)
+  const u32 k = min(hi - lo, kWalkTail), tail = hi - k;
+  const Ring er{R.base, R.cap, R.eorg};
+  u32 c;
+  const i64 t_tail = tail_time(R, k - 1);  // time of entry `tail`
+  if (tail == lo || r.t >= t_tail) {
+    u32 n = 0;  // tail entries not later than t (the oldest of the tail)
+#pragma unroll
+    for (u32 i = 0; i < kWalkTail; ++i)
+      if (i < k) n += R.t[i] <= r.t ? 1u : 0u;
+    c = tail + n;
+  } else {
+    bool interp = false;
+    if (t_tail > tl && r.t >= tl && tail - lo > 16u) {
+      const double f = static_cast<double>(r.t - tl) / static_cast<double>(t_tail - tl);
+      const double n = static_cast<double>(tail - lo);
+      interp = f * n + 12.0 < n;
+    }
+    if (interp) {
+      const Entry* ent = P.s.ent;
+      c = interp_ub<4>([ent](u32 q) { return ent[q].t; }, er, lo, tail, r.t, tl, t_tail);
+    } else {
+      u32 e_unused;
+      causal_slice_entries(P.s.ent, er, lo, tail, r.t, 0, c, e_unused);
+    }
+  }
+  cn->bytes += 80u + 8u * ceil_log2p1(R.g);
+  const u64 w = P.walk_begin + wl;
+  const double u = P.rng.uniform(w, r.len, 0);
+  const u32 pos = c + static_cast<u32>(draw_index(P, u, lo, c, hi, &cn->amb, er, hi));
+  u32 nbr;
+  i64 nt;
+  if (pos >= tail) {
+    nbr = tail_nbr(R, hi - 1 - pos);
+    nt = tail_time(R, hi - 1 - pos);
+  } else {
+    const Entry x = load_entry(P.s.ent + er(pos));
+    nbr = x.nbr;
+    nt = x.t;
+  }
+  const u64 slot = out_index(P, wl, r.len);
+  P.nodes[slot] = ext_of(P.s, nbr);
+  P.times[slot] = nt;
+  r.len += 1;
+  r.cur = nbr;
+  r.t = nt;
+  return true;
+}
+
 // walk_engine.cpp:284-299
 __device__ __forceinline__ u64 sample_start_edge_dev(const StoreView& s, int bias, double u1, double u2,
                                                      const double* expm1_tab, u32* amb) {
@@ -677,7 +761,7 @@ __device__ __forceinline__ i64 load_last_t(const i64* p, u64 pol) {
 // One thread per walk, init fused, the whole walk in registers
 // (walk_engine.cpp:380-392). kWB-thread blocks (32 by default): a block
 // retires — and its slots take new walks — as soon as its own walks end.
-template <int kWB>
+template <int kWB, bool kRec>
 __global__ void __launch_bounds__(kWB, 1024 / kWB) k_fullwalk(WalkParams P, InitParams I, u64 count, u32* lengths,
                                                                u64* part) {
   const u64 wl = blockIdx.x * static_cast<u64>(kWB) + threadIdx.x;
@@ -692,7 +776,11 @@ __global__ void __launch_bounds__(kWB, 1024 / kWB) k_fullwalk(WalkParams P, Init
     init_len = r.len;
     // the snapshot's time span: anchors of the interpolation search
     const i64 tl = P.s.m ? edge_time(P.s, 0) - 1 : 0, th = P.s.m ? edge_time(P.s, P.s.m - 1) + 1 : -1;
-    while (r.len < P.stride) {
+    if (kRec) {  // forward index-biased walks over an append-route snapshot: walk records
+      while (r.len < P.stride)
+        if (!hop_rec(P, wl, r, load_wrec(P.s.wrec + r.cur), &cn, tl)) break;
+    }
+    while (!kRec && r.len < P.stride) {
       if (P.last_t && load_last_t(P.last_t + r.cur, pol) <= r.t) break;  // nothing later than t at r.cur
       const NodeMeta a = P.s.nm[r.cur];
       if (!hop(P, wl, r, P.s.mk_time, P.s.mk_start, mark_ring(a), a.gb, a.ge, entry_ring(a), a.eb, a.ee, &cn, tl,
@@ -1102,6 +1190,10 @@ bool walk_last_t_filter() {
   static const bool on = env_int("TWG_WALK_LASTT", 0) != 0;
   return on;
 }
+bool walk_rec_enabled() {
+  static const bool on = env_int("TWG_WALK_REC", 1) != 0;
+  return on;
+}
 u64 walk_l2_keep() {
   static const u64 k = static_cast<u64>(env_int("TWG_WALK_L2KEEP", 0));
   return k;
@@ -1135,6 +1227,7 @@ WalkParams make_params(Ctx& ctx, Store& s, const twg_walk_config& cfg, u32 strid
   P.expm1_tab = ctx.d_expm1;
   P.last_t = nullptr;
   P.l2_keep = 0;
+  P.rec = 0;
   return P;
 }
 
@@ -1400,15 +1493,22 @@ WalkSetDev* generate_walks(Ctx& ctx, Store& s_in, const twg_walk_config& cfg, co
   } else if (variant == TWG_FULLWALK) {
     if (P.dir == 0 && walk_last_t_filter() && s.last_t.p && s.last_t.n >= s.V) P.last_t = s.last_t.p;
     P.l2_keep = walk_l2_keep();
+    P.rec = walk_rec_enabled() && s.wrec.p && s.wrec.n >= s.V && P.dir == 0 && !P.node2vec &&
+            (P.bias == TWG_UNIFORM || P.bias == TWG_LINEAR || P.bias == TWG_EXPINDEX);
     DevBuf<u64> part(kStatSlots * 8, st);
     TWG_CUDA(cudaMemsetAsync(part.p, 0, part.bytes(), st));
     const int wb = walk_block();
     const unsigned g = static_cast<unsigned>((count + wb - 1) / wb);
-    switch (wb) {
-      case 32: k_fullwalk<32><<<g, 32, 0, st>>>(P, I, count, out->lengths.p, part.p); break;
-      case 64: k_fullwalk<64><<<g, 64, 0, st>>>(P, I, count, out->lengths.p, part.p); break;
-      case 128: k_fullwalk<128><<<g, 128, 0, st>>>(P, I, count, out->lengths.p, part.p); break;
-      default: k_fullwalk<256><<<g, 256, 0, st>>>(P, I, count, out->lengths.p, part.p); break;
+    if (P.rec) {
+      k_fullwalk<32, true><<<static_cast<unsigned>((count + 31) / 32), 32, 0, st>>>(P, I, count, out->lengths.p,
+                                                                                   part.p);
+    } else {
+      switch (wb) {
+        case 32: k_fullwalk<32, false><<<g, 32, 0, st>>>(P, I, count, out->lengths.p, part.p); break;
+        case 64: k_fullwalk<64, false><<<g, 64, 0, st>>>(P, I, count, out->lengths.p, part.p); break;
+        case 128: k_fullwalk<128, false><<<g, 128, 0, st>>>(P, I, count, out->lengths.p, part.p); break;
+        default: k_fullwalk<256, false><<<g, 256, 0, st>>>(P, I, count, out->lengths.p, part.p); break;
+      }
     }
     TWG_LAUNCHED(ctx);
     k_fold_stats<<<1, 160, 0, st>>>(part.p, stats.p);
