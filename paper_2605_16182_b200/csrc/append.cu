@@ -40,15 +40,10 @@ static_assert(kPB == 1 << kBucketShift, "one thread per bucket node");
 
 unsigned grid(Ctx& ctx, u64 n) { return grid_for(n, kBlock, static_cast<unsigned>(ctx.sm_count) * 16); }
 
-// first k in [0, n) with t[zr(k)] >= x (one thread)
+// first k in [0, n) with t[zr(k)] >= x (one warp)
 __global__ void k_lb_time(const i64* t, Ring zr, u64 n, i64 x, u64* out) {
-  u64 lo = 0, hi = n;
-  while (lo < hi) {
-    const u64 mid = (lo + hi) >> 1;
-    if (t[zr(static_cast<u32>(mid))] < x) lo = mid + 1;
-    else hi = mid;
-  }
-  *out = lo;
+  const u64 r = warp_lower_bound([&](u64 k) { return t[zr(static_cast<u32>(k))]; }, n, x);
+  if (threadIdx.x == 0) *out = r;
 }
 
 // survivors [from, from + n) of a snapshot -> the start of a new log
@@ -218,13 +213,31 @@ struct OwnerIn {
 };
 
 // bucket b = owner >> 8 of the bucket-sorted entries starts at bstart[b]
-// (empty buckets included); bstart[nb] = Yn
+// (empty buckets included); bstart[nb] = Yn. Four keys per thread (one
+// 128-bit load; the key before them from the neighbouring lane).
 __global__ void k_bucket_bounds(const u32* keys, u64 Yn, u64 nb, u32* bstart) {
-  for (u64 q = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; q <= Yn;
-       q += static_cast<u64>(gridDim.x) * blockDim.x) {
-    const i64 prev = q == 0 ? -1 : static_cast<i64>(keys[q - 1] >> kBucketShift);
-    const i64 cur = q == Yn ? static_cast<i64>(nb) : static_cast<i64>(keys[q] >> kBucketShift);
-    for (i64 b = prev + 1; b <= cur; ++b) bstart[b] = static_cast<u32>(q);
+  const u64 quads = (Yn + 4) / 4;  // positions 0..Yn (Yn itself closes the last bucket)
+  for (u64 g = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; g < quads;
+       g += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const u64 q0 = 4 * g;
+    i64 cur[4];
+    if (q0 + 4 <= Yn && (reinterpret_cast<uintptr_t>(keys) & 15) == 0) {
+      const uint4 k4 = __ldg(reinterpret_cast<const uint4*>(keys) + g);
+      cur[0] = k4.x >> kBucketShift, cur[1] = k4.y >> kBucketShift, cur[2] = k4.z >> kBucketShift,
+      cur[3] = k4.w >> kBucketShift;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        cur[j] = q0 + j < Yn ? static_cast<i64>(keys[q0 + j] >> kBucketShift) : static_cast<i64>(nb);
+    }
+    i64 prev = q0 == 0 ? -1 : static_cast<i64>(keys[q0 - 1] >> kBucketShift);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const u64 q = q0 + j;
+      if (q > Yn) break;
+      for (i64 b = prev + 1; b <= cur[j]; ++b) bstart[b] = static_cast<u32>(q);
+      prev = cur[j];
+    }
   }
 }
 
@@ -233,7 +246,12 @@ __global__ void k_bucket_bounds(const u32* keys, u64 Yn, u64 nb, u32* bstart) {
 // in the (canonical) bucket order carries its newest batch time.
 template <class PV>
 __global__ void __launch_bounds__(kPB) k_bucket_count(const u32* keys, const PV* vals, const u32* bstart, u64 V,
-                                                      i64 tb, u32* y, i64* last_t) {
+                                                      i64 tb, u32* y, const i64* old_last, i64* last_t, i64 cutoff,
+                                                      u64* dead) {
+  // old_last != null: last_t[v] = max(old_last[v], the batch's owner-side
+  // newest) for every node of the bucket (the new snapshot's copy, no
+  // separate device copy); else updated in place. dead != null: the nodes
+  // whose newest time falls before the cutoff (they would leave) are counted.
   __shared__ u32 cnt[kPB];
   __shared__ u32 lastq[kPB];
   const u64 bkt = blockIdx.x;
@@ -248,24 +266,23 @@ __global__ void __launch_bounds__(kPB) k_bucket_count(const u32* keys, const PV*
   }
   __syncthreads();
   const u64 v = (bkt << kBucketShift) + threadIdx.x;
+  u64 d = 0;
   if (v < V) {
     y[v] = cnt[threadIdx.x];
-    if (last_t && cnt[threadIdx.x]) {
-      const i64 t = Payload<PV>::time(vals[lastq[threadIdx.x] - 1], tb);
-      if (last_t[v] < t) last_t[v] = t;
+    if (last_t) {
+      i64 lt = old_last ? old_last[v] : last_t[v];
+      const bool upd = cnt[threadIdx.x] != 0;
+      if (upd) {
+        const i64 t = Payload<PV>::time(vals[lastq[threadIdx.x] - 1], tb);
+        if (lt < t) lt = t;
+      }
+      if (old_last || upd) last_t[v] = lt;
+      d = lt < cutoff ? 1u : 0u;
     }
   }
+  if (dead) block_atomic_add(reinterpret_cast<unsigned long long*>(dead), d);
 }
 
-// nodes whose newest incident edge falls before the cutoff (they would leave the snapshot)
-__global__ void k_count_dead(const i64* last, u64 V, i64 cutoff, u64* dead) {
-  u64 c = 0;
-  for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < V;
-       v += static_cast<u64>(gridDim.x) * blockDim.x)
-    c += last[v] < cutoff ? 1u : 0u;
-  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd(reinterpret_cast<unsigned long long*>(dead), c);
-}
 
 // Eviction bound: first logical x in [lo, hi) with time >= c. The eight
 // times after lo are loaded at once (independent loads, one round trip):
@@ -717,7 +734,8 @@ bool append_log_slot(const Store& O, const Store* R, u64 A, Ring* wr) {
 
 Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const EdgeRec* batch, Ring bring, u64 A,
                      u64 from, i64 cutoff, bool no_ties, bool in_log, bool check_dead, const i64* bt,
-                     const i64* const* bcols, const u64* groups_done, i64 tbase, bool compact) {
+                     const i64* const* bcols, const u64* groups_done, i64 tbase, bool compact,
+                     const i64* old_last) {
   Ctx& ctx = *w.ctx;
   cudaStream_t st = ctx.stream;
   PhaseTimer pt(ctx, "ingest_append");
@@ -731,7 +749,7 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
   u64* sc = ctx.d_scalars + 32;  // 32..47 private to this path
   TWG_CUDA(cudaMemsetAsync(sc, 0, 16 * sizeof(u64), st));
   const u64* d_gcut = sc + 9;  // first surviving ts group of O
-  k_lb_time<<<1, 1, 0, st>>>(O.ts_time.p, O.view().zrg, O.Z, cutoff, sc + 9);
+  k_lb_time<<<1, 32, 0, st>>>(O.ts_time.p, O.view().zrg, O.Z, cutoff, sc + 9);
   TWG_LAUNCHED(ctx);
 
   // 1. edge log + ts groups
@@ -813,7 +831,7 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
       TWG_LAUNCHED(ctx);
     }
     DevBuf<u32> bstart(nb + 1, st);
-    k_bucket_bounds<<<grid(ctx, Yn + 1), kBlock, 0, st>>>(kp, Yn, nb, bstart.p);
+    k_bucket_bounds<<<grid(ctx, (Yn + 4) / 4), kBlock, 0, st>>>(kp, Yn, nb, bstart.p);
     TWG_LAUNCHED(ctx);
     (kp == k0.p ? k1 : k0).release();  // the pass count decides which buffer holds the result
     (vp == v0.p ? v1 : v0).release();
@@ -824,16 +842,13 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
     s->nm.alloc(V, st);
     s->wrec.alloc(V, st);
     DevBuf<u32> ycnt(V, st);
-    k_bucket_count<PV><<<static_cast<unsigned>(nb), kPB, 0, st>>>(kp, vp, bstart.p, V, tbase, ycnt.p, s->last_t.p);
+    if (check_dead) TWG_CUDA(cudaMemsetAsync(sc + 13, 0, sizeof(u64), st));
+    k_bucket_count<PV><<<static_cast<unsigned>(nb), kPB, 0, st>>>(kp, vp, bstart.p, V, tbase, ycnt.p, old_last,
+                                                                 s->last_t.p, cutoff, check_dead ? sc + 13 : nullptr);
     TWG_LAUNCHED(ctx);
-    if (check_dead) {  // fast route: the population must not shrink (nothing is published yet)
-      TWG_CUDA(cudaMemsetAsync(sc + 13, 0, sizeof(u64), st));
-      k_count_dead<<<grid(ctx, V), kBlock, 0, st>>>(s->last_t.p, V, cutoff, sc + 13);
-      TWG_LAUNCHED(ctx);
-      u64 dead[1];
-      read_scalars(ctx, sc + 13, dead, 1);
-      if (dead[0]) return false;
-    }
+    // fast route: the population must not shrink — the dead count (sc[13]) is
+    // read back with the plan's scalars; nothing is published before
+    bool dead = false;
     arena = O.gapped ? O.arena : nullptr;
     // a snapshot older than the retired one still holding this arena may read
     // any slot: then nothing of it is reused (fresh arena)
@@ -866,13 +881,18 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
       pa.scal = sc;
       k_plan<<<grid(ctx, V), kBlock, 0, st>>>(pa);
       TWG_LAUNCHED(ctx);
-      u64 r3[3];
-      read_scalars(ctx, sc, r3, 3);
+      u64 r3[14];
+      read_scalars(ctx, sc, r3, check_dead ? 14 : 3);
+      if (check_dead && r3[13]) {
+        dead = true;
+        return u64{1};
+      }
       dst.used = r3[0];
       return r3[1] == 0 ? static_cast<u64>(r3[2] & 0xffffffffull) + 1 : 0;  // relocations + 1, 0 = exhausted
     };
     bool fresh = false;
     u64 nrel = arena ? run_plan(*arena, false) : 0;
+    if (dead) return false;
     if (nrel == 0) {
       auto na = std::make_shared<NodeArena>();
       static std::atomic<u64> serials{0};
@@ -887,6 +907,7 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
       nrel = run_plan(*arena, true);
       if (nrel == 0) fail(TWG_ENOMEM, "ingest: node arena sized below the live regions");
       fresh = true;
+      if (dead) return false;
     }
     --nrel;
     s->relocated = nrel;

@@ -60,6 +60,31 @@ __device__ __forceinline__ void block_atomic_add(unsigned long long* dst, u64 v)
   __syncthreads();  // s_part may be reused by a second call
 }
 
+// First k in [0, n) with key(k) >= x over a sorted key, by one warp: each
+// round the 32 lanes probe 32 evenly spaced positions and keep the piece
+// holding the boundary (log33 n dependent rounds instead of log2 n). Every
+// lane of the warp calls it; every lane gets the answer.
+template <class Key>
+__device__ __forceinline__ u64 warp_lower_bound(Key key, u64 n, i64 x) {
+  const u32 lane = threadIdx.x & 31;
+  u64 lo = 0, hi = n;  // answer in [lo, hi]
+  while (hi > lo) {
+    const u64 span = hi - lo;
+    const bool small = span <= 32;
+    const u64 p = small ? lo + lane : lo + (static_cast<u64>(lane) + 1) * span / 33;
+    const bool in = small ? lane < span : true;
+    const u32 c = __popc(__ballot_sync(0xffffffffu, in && key(p) < x));
+    if (small) return lo + c;
+    const u64 plo = lo, pspan = span;
+    auto probe = [&](u32 i) { return plo + (static_cast<u64>(i) + 1) * pspan / 33; };
+    const u64 nlo = c > 0 ? probe(c - 1) + 1 : lo;
+    const u64 nhi = c < 32 ? probe(c) : hi;
+    lo = nlo;
+    hi = nhi;
+  }
+  return lo;
+}
+
 // Block-wide reduction of one u64 (op: 0 add, 1 max, 2 min, 3 or); the
 // result is valid in thread 0. Every thread of the block must call it.
 template <int kOp>

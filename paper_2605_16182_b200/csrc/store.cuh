@@ -198,6 +198,7 @@ struct Store {
   bool ext_identity = false;
   DevBuf<u32> e_src, e_dst;
   DevBuf<i64> e_t, ext;
+  std::shared_ptr<DevBuf<i64>> ext_keep;  // owner of ext when it is shared between snapshots (ext aliases it)
   DevBuf<EdgeRec> e_rec;  // streaming stores: alias of the log's records
   DevBuf<u32> ts_off;
   DevBuf<i64> ts_time;

@@ -277,13 +277,8 @@ __global__ void k_lower_bound_cut(StoreView s, i64 t_high, i64 duration, const u
   const i64 bh = static_cast<i64>(scal[0]);
   const i64 high = t_high > bh ? t_high : bh;
   const i64 cutoff = high > duration ? high - duration : 0;
-  u64 lo = 0, hi = s.m;
-  while (lo < hi) {
-    const u64 mid = (lo + hi) >> 1;
-    if (edge_time(s, mid) < cutoff) lo = mid + 1;
-    else hi = mid;
-  }
-  *out = lo;
+  const u64 r = warp_lower_bound([&](u64 k) { return edge_time(s, k); }, s.m, cutoff);
+  if (threadIdx.x == 0) *out = r;
 }
 
 // Canonical order of a time-ordered batch whose equal-time runs are short
@@ -323,13 +318,8 @@ __global__ void k_pack_rec(const u32* s, const u32* d, const i64* t, u64 n, Edge
 
 // lower_bound(time_, cutoff) (edge_store.cpp:326) over the snapshot's edges
 __global__ void k_lower_bound(StoreView s, i64 cutoff, u64* out) {
-  u64 lo = 0, hi = s.m;
-  while (lo < hi) {
-    const u64 mid = (lo + hi) >> 1;
-    if (edge_time(s, mid) < cutoff) lo = mid + 1;
-    else hi = mid;
-  }
-  *out = lo;
+  const u64 r = warp_lower_bound([&](u64 k) { return edge_time(s, k); }, s.m, cutoff);
+  if (threadIdx.x == 0) *out = r;
 }
 
 struct AdmitFn {
@@ -1084,15 +1074,20 @@ Store* ingest_fast(Window& w, FastSpec& spec, u64 n, const u64* sc, i64 cutoff, 
   s->mode = w.mode;
   s->V = V;
   s->ext_identity = true;
-  s->ext.alloc(V, st);
-  TWG_CUDA(cudaMemcpyAsync(s->ext.p, O.ext.p, V * sizeof(i64), cudaMemcpyDeviceToDevice, st));
+  // the id map is the identity 0..V-1 on this route: one immutable copy shared by the snapshots
+  if (O.ext_keep) {
+    s->ext_keep = O.ext_keep;
+  } else {
+    s->ext_keep = std::make_shared<DevBuf<i64>>(V, st);
+    TWG_CUDA(cudaMemcpyAsync(s->ext_keep->p, O.ext.p, V * sizeof(i64), cudaMemcpyDeviceToDevice, st));
+  }
+  s->ext.alias(s->ext_keep->p, V);
   // newest incident time: only the owner side is tracked here (merged by the
   // placement's bucket counts); in directed modes the non-owner side would
   // cost one random atomic per edge, so last_t becomes a lower bound — the
   // population check stays sound (a node it cannot prove alive sends the
   // batch to the general route, which recomputes exact times)
-  s->last_t.alloc(V, st);
-  TWG_CUDA(cudaMemcpyAsync(s->last_t.p, O.last_t.p, V * sizeof(i64), cudaMemcpyDeviceToDevice, st));
+  s->last_t.alloc(V, st);  // filled from O.last_t by the bucket counts (ingest_append old_last)
   s->last_t_exact = w.mode == TWG_UNDIRECTED && O.last_t_exact;
   const u64 from = spec.from;
   s->m = O.m - from + n;
@@ -1102,7 +1097,8 @@ Store* ingest_fast(Window& w, FastSpec& spec, u64 n, const u64* sc, i64 cutoff, 
   Store* out =
       ingest_append(w, O, std::move(s), spec.rec, spec.wring, n, from, cutoff, true, spec.in_log, true, spec.bt,
                     spec.cols, spec.groups ? ctx.d_scalars + 14 : nullptr, batch_min,
-                    compact_payload_enabled() && static_cast<u64>(static_cast<i64>(sc[0]) - batch_min) < (1ull << 32));
+                    compact_payload_enabled() && static_cast<u64>(static_cast<i64>(sc[0]) - batch_min) < (1ull << 32),
+                    O.last_t.p);
   if (!out) {  // an old node leaves the window: the general route recomputes everything
     stats->evicted = stats->dropped_late = 0;
     return nullptr;
@@ -1196,7 +1192,7 @@ void window_ingest(Window& w, const i64* d_src, const i64* d_dst, const i64* d_t
   }
   TWG_LAUNCHED(ctx);
   if (spec.on) {
-    k_lower_bound_cut<<<1, 1, 0, st>>>(old.view(), w.t_high, w.duration, ctx.d_scalars, ctx.d_scalars + 12);
+    k_lower_bound_cut<<<1, 32, 0, st>>>(old.view(), w.t_high, w.duration, ctx.d_scalars, ctx.d_scalars + 12);
     TWG_LAUNCHED(ctx);
   }
   u64 sc[13];
@@ -1223,7 +1219,7 @@ void window_ingest(Window& w, const i64* d_src, const i64* d_dst, const i64* d_t
   }
 
   // survivors (export_suffix) and admitted batch edges
-  k_lower_bound<<<1, 1, 0, st>>>(old.view(), cutoff, ctx.d_scalars + 2);
+  k_lower_bound<<<1, 32, 0, st>>>(old.view(), cutoff, ctx.d_scalars + 2);
   TWG_LAUNCHED(ctx);
   DevBuf<u32> pos(n + 1, st);
   exclusive_scan<u32>(ctx, AdmitFn{d_t, cutoff}, n, pos.p);
