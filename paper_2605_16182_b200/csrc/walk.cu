@@ -761,9 +761,9 @@ __device__ __forceinline__ i64 load_last_t(const i64* p, u64 pol) {
 // One thread per walk, init fused, the whole walk in registers
 // (walk_engine.cpp:380-392). kWB-thread blocks (32 by default): a block
 // retires — and its slots take new walks — as soon as its own walks end.
-template <int kWB, bool kRec>
-__global__ void __launch_bounds__(kWB, 1024 / kWB) k_fullwalk(WalkParams P, InitParams I, u64 count, u32* lengths,
-                                                               u64* part) {
+template <int kWB, bool kRec, int kMinB = 1024 / kWB>
+__global__ void __launch_bounds__(kWB, kMinB) k_fullwalk(WalkParams P, InitParams I, u64 count, u32* lengths,
+                                                          u64* part) {
   const u64 wl = blockIdx.x * static_cast<u64>(kWB) + threadIdx.x;
   const bool active = wl < count;
   Ctr cn{0, 0};
@@ -1190,6 +1190,10 @@ bool walk_last_t_filter() {
   static const bool on = env_int("TWG_WALK_LASTT", 0) != 0;
   return on;
 }
+int walk_min_blocks() {
+  static const int b = env_int("TWG_WALK_MINB", 32);
+  return b;
+}
 bool walk_rec_enabled() {
   static const bool on = env_int("TWG_WALK_REC", 1) != 0;
   return on;
@@ -1500,8 +1504,13 @@ WalkSetDev* generate_walks(Ctx& ctx, Store& s_in, const twg_walk_config& cfg, co
     const int wb = walk_block();
     const unsigned g = static_cast<unsigned>((count + wb - 1) / wb);
     if (P.rec) {
-      k_fullwalk<32, true><<<static_cast<unsigned>((count + 31) / 32), 32, 0, st>>>(P, I, count, out->lengths.p,
-                                                                                   part.p);
+      const unsigned g32 = static_cast<unsigned>((count + 31) / 32), g64 = static_cast<unsigned>((count + 63) / 64);
+      // 64 registers (1024 resident threads per SM: the 32-block limit with 32-thread blocks, the
+      // register file with 64-thread ones); 40-register builds spill (measured)
+      switch (walk_min_blocks()) {
+        case 16: k_fullwalk<64, true, 16><<<g64, 64, 0, st>>>(P, I, count, out->lengths.p, part.p); break;
+        default: k_fullwalk<32, true><<<g32, 32, 0, st>>>(P, I, count, out->lengths.p, part.p); break;
+      }
     } else {
       switch (wb) {
         case 32: k_fullwalk<32, false><<<g, 32, 0, st>>>(P, I, count, out->lengths.p, part.p); break;

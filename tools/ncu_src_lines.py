@@ -30,4 +30,4 @@ for r in csv.reader(open(path)):
 tot = [sum(x[i] for x in rows) for i in range(5)]
 print(f"totals: samples {tot[1]:.0f}  L2 sectors {tot[2]:.4g}  L1 tag req {tot[3]:.4g}  warp inst {tot[4]:.4g}")
 for x in sorted(rows, key=lambda x: -x[0])[:top]:
-    print(f"{x[1]:7.0f} {100*x[1]/max(tot[1],1):5.1f}%  L2sec {x[2]:11.4g}  L1req {x[3]:10.4g}  {x[5]:18s} {x[6]}")
+    print(f"{x[1]:7.0f} {100*x[1]/max(tot[1],1):5.1f}%  inst {x[4]:10.4g}  L2sec {x[2]:11.4g}  L1req {x[3]:10.4g}  {x[5]:18s} {x[6]}")
