@@ -284,22 +284,22 @@ __global__ void __launch_bounds__(kPB) k_bucket_count(const u32* keys, const PV*
 }
 
 
-// Eviction bound: first logical x in [lo, hi) with time >= c. The eight
-// times after lo are loaded at once (independent loads, one round trip):
-// a batch evicts only a few entries of a typical node; longer prefixes
-// continue by galloping.
-template <class TimeAt>
-__device__ __forceinline__ u32 evict_lb(TimeAt at, u32 lo, u32 hi, i64 c) {
-  constexpr u32 kAhead = 8;
-  const u32 k = min(hi - lo, kAhead);
-  i64 tt[kAhead];
+// Eviction bound: first logical x in [lo, hi) with time >= c. The times
+// from lo to the end of lo's 128-B line (kLine keys of the array) are loaded
+// at once (independent loads, one round trip, one DRAM line — the whole line
+// comes in anyway): a batch evicts only a few entries of a typical node;
+// longer prefixes continue by galloping.
+template <u32 kLine, class TimeAt>
+__device__ __forceinline__ u32 evict_lb(TimeAt at, u32 slot_lo, u32 lo, u32 hi, i64 c) {
+  const u32 k = min(hi - lo, kLine - (slot_lo & (kLine - 1)));
+  i64 tt[kLine];
 #pragma unroll
-  for (u32 i = 0; i < kAhead; ++i) tt[i] = i < k ? at(lo + i) : c;
+  for (u32 i = 0; i < kLine; ++i) tt[i] = i < k ? at(lo + i) : c;
   u32 n = 0;
 #pragma unroll
-  for (u32 i = 0; i < kAhead; ++i) n += tt[i] < c ? 1u : 0u;
+  for (u32 i = 0; i < kLine; ++i) n += tt[i] < c ? 1u : 0u;
   if (n < k || k == hi - lo) return lo + n;
-  return gallop_lb(at, lo + kAhead, hi, c);
+  return gallop_lb(at, lo + k, hi, c);
 }
 
 __device__ __forceinline__ u32 adjust_org(u32 org, u32 x, u32 cap) {  // org' = org (mod cap), 0 <= x - org' < cap
@@ -349,13 +349,13 @@ __global__ void __launch_bounds__(kBlock) k_plan(PlanArgs a) {
       if (implicit_marks(o)) {
         // single-entry groups (distinct times: the common case): marks are
         // not stored, mark k is entry k — search the entry times
-        eb = evict_lb([&](u32 x) { return a.oent[oer(x)].t; }, o.eb, o.ee, a.cutoff);
+        eb = evict_lb<8>([&](u32 x) { return a.oent[oer(x)].t; }, oer(o.eb), o.eb, o.ee, a.cutoff);
         gb = o.gb + (eb - o.eb);
       } else {
         // the first surviving mark starts the first surviving entry (a group
         // is evicted whole: eviction is by time), so one search over the
         // marks gives both bounds
-        gb = evict_lb([&](u32 x) { return a.omt[omr(x)]; }, o.gb, o.ge, a.cutoff);
+        gb = evict_lb<8>([&](u32 x) { return a.omt[omr(x)]; }, omr(o.gb), o.gb, o.ge, a.cutoff);
         eb = gb == o.ge ? o.ee : a.oms[omr(gb)];
       }
       u32 low = o.eb;
@@ -435,7 +435,7 @@ struct PlaceArgs {
   u64* q_total;
 };
 
-struct PlaceSmem {  // ~34 KB: 6 CTAs per SM
+struct PlaceSmem {  // ~55 KB: 4 CTAs per SM (the register budget allows 4 as well)
   u16 wcnt[kPB / 32][kPB];  // chunk counts fit 16 bits (kChunk <= 65535)
   u32 off[kPB + 1];
   u32 cur[kPB], gcur[kPB], base[kPB], cap[kPB], eorg[kPB], gorg[kPB];
@@ -445,15 +445,13 @@ struct PlaceSmem {  // ~34 KB: 6 CTAs per SM
   u8 tie[kPB];   // this chunk holds an entry of the node that continues a group
   u32 mtotal;
   u32 rwcnt[kChunkItems][kPB / 32];
-  u32 tcnt[kPB];              // node's new entries so far
-  u32 tn[kWalkTail][kPB];     // its newest ones (newest first): neighbour
-  i64 tt[kWalkTail][kPB];     // and time
   u8 snode[kChunk];
   u8 flag[kChunk];
   u16 mscan[kChunk];
   Entry sent[kChunk];
 };
 static_assert(kChunk < 65536, "16-bit chunk counters");
+static_assert(sizeof(PlaceSmem) <= 56 * 1024, "placement: 4 CTAs per SM (228 KB of shared memory)");
 
 // One CTA per bucket of 256 nodes (thread t <-> node (bucket << 8) + t):
 // the bucket's entries in rounds of kChunk: stable rank per node
@@ -488,10 +486,6 @@ __global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs<PV> a) {
   sm.expl[t] = implicit_marks(p) ? 0 : 1;
 
   const u32 lt = (1u << lane) - 1u;
-  // node t's newest new entries so far (newest first), for its walk record
-  sm.tcnt[t] = 0;
-#pragma unroll
-  for (u32 i = 0; i < kWalkTail; ++i) sm.tn[i][t] = 0, sm.tt[i][t] = 0;
   for (u32 c0 = bs; c0 < be; c0 += kChunk) {
     const u32 n = min(static_cast<u32>(kChunk), be - c0);
     __syncthreads();
@@ -623,18 +617,6 @@ __global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs<PV> a) {
         sm.gcur[t] += mend - sm.mscan[o1];
         sm.last_t[t] = sm.sent[o1 + c - 1].t;
         sm.has_last[t] = 1u;
-        // shift the tail by min(c, kWalkTail) and take this chunk's newest entries
-        for (int i = kWalkTail - 1; i >= 0; --i) {
-          if (static_cast<u32>(i) < c) {
-            const Entry e = sm.sent[o1 + c - 1 - i];
-            sm.tn[i][t] = e.nbr;
-            sm.tt[i][t] = e.t;
-          } else {
-            sm.tn[i][t] = sm.tn[i - c][t];
-            sm.tt[i][t] = sm.tt[i - c][t];
-          }
-        }
-        sm.tcnt[t] += c;
       }
     }
   }
@@ -645,9 +627,10 @@ __global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs<PV> a) {
     const NodeMeta r{p.eb, sm.cur[t], p.gb, sm.gcur[t], p.base, p.cap, p.eorg, p.gorg};
     a.nm_new[v] = r;
     q = r.ge - r.gb;
-    // the walk record: the newest entries read back from the ring (this
-    // CTA's writes are visible after the barrier; the older ones share the
-    // lines the appends just touched)
+    // the walk record; its tail (the newest entries, newest first) comes
+    // from the last chunk still staged in shared memory, then from this
+    // batch's earlier chunks (ring slots this CTA wrote, visible after the
+    // barrier), then from the previous snapshot's record (or its ring)
     WalkRec w;
     w.eb = r.eb;
     w.ee = r.ee;
@@ -656,36 +639,34 @@ __global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs<PV> a) {
     w.eorg = r.eorg;
     w.g = r.ge - r.gb;
     w.pad = 0;
-    // the tail: this batch's newest entries, then (when fewer than the
-    // tail) the previous snapshot's newest ones — from its walk record, or
-    // from the ring when it has none
-#pragma unroll
-    for (u32 i = 0; i < kWalkTail; ++i) w.nbr[i] = sm.tn[i][t], w.t[i] = sm.tt[i][t];
-    const u32 tcnt = sm.tcnt[t];
+    const Ring er = entry_ring(r);
+    const u32 total = r.ee - p.ee;  // this batch's entries of the node
+    const u32 o1 = be > bs ? sm.off[t] : 0u, cl = be > bs ? sm.off[t + 1] - o1 : 0u;  // in the last chunk
     const u32 k = min(r.ee - r.eb, kWalkTail);
-    if (tcnt < k) {
-      const Ring er = entry_ring(r);
-      WalkRec o;
-      if (a.owrec) o = a.owrec[v];
+    WalkRec o;
+    if (a.owrec && total < k) o = a.owrec[v];
 #pragma unroll
-      for (u32 i = 0; i < kWalkTail; ++i) {
-        if (i >= tcnt && i < k) {
-          const u32 j = i - tcnt;  // j-th newest entry before this batch's
-          u32 nb;
-          i64 tj;
-          if (a.owrec) {
-            nb = j == 0 ? o.nbr[0] : j == 1 ? o.nbr[1] : o.nbr[2];
-            tj = j == 0 ? o.t[0] : j == 1 ? o.t[1] : o.t[2];
-          } else {
-            const Entry e = a.ent[er(p.ee - 1 - j)];
-            nb = e.nbr;
-            tj = e.t;
-          }
-          if (i == 0) w.nbr[0] = nb, w.t[0] = tj;
-          else if (i == 1) w.nbr[1] = nb, w.t[1] = tj;
-          else w.nbr[2] = nb, w.t[2] = tj;
+    for (u32 i = 0; i < kWalkTail; ++i) {
+      u32 nb = 0;
+      i64 tj = 0;
+      if (i < k) {
+        if (i < cl || i < total) {
+          const Entry e = i < cl ? sm.sent[o1 + cl - 1 - i] : a.ent[er(r.ee - 1 - i)];
+          nb = e.nbr;
+          tj = e.t;
+        } else if (a.owrec) {
+          const u32 j = i - total;
+          nb = j == 0 ? o.nbr[0] : j == 1 ? o.nbr[1] : o.nbr[2];
+          tj = j == 0 ? o.t[0] : j == 1 ? o.t[1] : o.t[2];
+        } else {
+          const Entry e = a.ent[entry_ring(p)(p.ee - 1 - (i - total))];
+          nb = e.nbr;
+          tj = e.t;
         }
       }
+      if (i == 0) w.nbr[0] = nb, w.t[0] = tj;
+      else if (i == 1) w.nbr[1] = nb, w.t[1] = tj;
+      else w.nbr[2] = nb, w.t[2] = tj;
     }
     a.wrec_new[v] = w;
   }
