@@ -60,6 +60,34 @@ __device__ __forceinline__ void block_atomic_add(unsigned long long* dst, u64 v)
   __syncthreads();  // s_part may be reused by a second call
 }
 
+// ---- 1-D TMA bulk copies (cp.async.bulk) into shared memory --------------
+//
+// One thread arms an mbarrier with the byte count and issues the copies; the
+// copy engine writes shared memory directly (no registers, no per-thread
+// loads) and completes the transaction on the barrier; every thread waits on
+// the barrier's phase. Addresses and sizes must be 16-B aligned.
+__device__ __forceinline__ u32 smem_u32(const void* p) { return static_cast<u32>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(u64* bar, u32 count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(u64* bar, u32 bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 bytes, u64* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 // First k in [0, n) with key(k) >= x over a sorted key, by one warp: each
 // round the 32 lanes probe 32 evenly spaced positions and keep the piece
 // holding the boundary (log33 n dependent rounds instead of log2 n). Every

@@ -110,14 +110,24 @@ struct TsSpec {
   u64* total;       // groups of the batch
 };
 
+// shared memory of one statistics tile: the span's three columns as they
+// lie in HBM (i64), staged by TMA bulk copies
+struct StatSmem {
+  i64 t[kStatSpan], a[kStatSpan], b[kStatSpan];
+};
+
 template <bool kGroups>
 __global__ void __launch_bounds__(kBlock) k_batch_stats(const i64* bs, const i64* bd, const i64* bt, u64 n, u64* scal,
                                                         EdgeRec* rec, Ring wr, TsSpec ts) {
-  __shared__ i64 st_t[kStatSpan];
-  __shared__ u32 st_a[kStatSpan], st_b[kStatSpan];
+  extern __shared__ __align__(128) unsigned char stat_smem[];
+  StatSmem& S = *reinterpret_cast<StatSmem*>(stat_smem);
+  i64* st_t = S.t;
+  i64* st_a = S.a;
+  i64* st_b = S.b;
   __shared__ u32 s_tile;
   __shared__ u32 s_cnt[kStatItems][kBlock / 32];
   __shared__ u64 s_prefix;
+  __shared__ alignas(8) u64 s_bar;
   i64 mt = kTimeUnset, lt = kTimeInfinite;
   u64 mid = 0;
   u32 shape = 0, neg = 0;
@@ -128,34 +138,30 @@ __global__ void __launch_bounds__(kBlock) k_batch_stats(const i64* bs, const i64
   const u64 tile = kGroups ? s_tile : blockIdx.x;
   const u64 base = tile * kStatTile;
   const i64 lo_g = static_cast<i64>(base) - kSegMax;  // global index of st_*[0]
-  {
-    i64 tv[kStatRounds], av[kStatRounds], bv[kStatRounds];
-#pragma unroll
-    for (int r = 0; r < kStatRounds; ++r) {
-      const int j = threadIdx.x + r * kBlock;
-      const i64 g = lo_g + j;
-      if (j < kStatSpan && g >= 0 && static_cast<u64>(g) < n) {
-        tv[r] = bt[g];
-        av[r] = bs[g];
-        bv[r] = bd[g];
-      }
+  // interior tiles (the whole span inside the batch, 16-B aligned columns):
+  // three 1-D TMA bulk copies; the first and last tiles: per-thread loads
+  const bool bulk = lo_g >= 0 && static_cast<u64>(lo_g) + kStatSpan <= n &&
+                    ((reinterpret_cast<uintptr_t>(bt) | reinterpret_cast<uintptr_t>(bs) |
+                      reinterpret_cast<uintptr_t>(bd)) & 15) == 0;
+  if (bulk) {
+    constexpr u32 kBytes = kStatSpan * sizeof(i64);
+    static_assert(kBytes % 16 == 0, "bulk copy size");
+    if (threadIdx.x == 0) {
+      mbar_init(&s_bar, 1);
+      mbar_arrive_expect_tx(&s_bar, 3 * kBytes);
+      bulk_g2s(st_t, bt + lo_g, kBytes, &s_bar);
+      bulk_g2s(st_a, bs + lo_g, kBytes, &s_bar);
+      bulk_g2s(st_b, bd + lo_g, kBytes, &s_bar);
     }
-#pragma unroll
-    for (int r = 0; r < kStatRounds; ++r) {
-      const int j = threadIdx.x + r * kBlock;
+    __syncthreads();  // the barrier is initialised before anyone waits on it
+    mbar_wait(&s_bar, 0);
+  } else {
+    for (int j = threadIdx.x; j < kStatSpan; j += kBlock) {
       const i64 g = lo_g + j;
-      if (j < kStatSpan && g >= 0 && static_cast<u64>(g) < n) {
-        const i64 t = tv[r], a = av[r], b = bv[r];
-        st_t[j] = t;
-        st_a[j] = static_cast<u32>(a);
-        st_b[j] = static_cast<u32>(b);
-        if (j >= kSegMax && j < kSegMax + kStatTile) {  // this tile's own edges: statistics
-          mt = max(mt, t);
-          lt = min(lt, t);
-          if (a > 0) mid = max(mid, static_cast<u64>(a));
-          if (b > 0) mid = max(mid, static_cast<u64>(b));
-          if (a < 0 || b < 0) neg = 1;
-        }
+      if (g >= 0 && static_cast<u64>(g) < n) {
+        st_t[j] = bt[g];
+        st_a[j] = bs[g];
+        st_b[j] = bd[g];
       }
     }
   }
@@ -192,6 +198,14 @@ __global__ void __launch_bounds__(kBlock) k_batch_stats(const i64* bs, const i64
     const u64 i = base + k * kBlock + threadIdx.x;
     if (i >= n) continue;
     const i64 t = st_t[j];
+    {  // this tile's own edges: statistics
+      const i64 a = st_a[j], b = st_b[j];
+      mt = max(mt, t);
+      lt = min(lt, t);
+      if (a > 0) mid = max(mid, static_cast<u64>(a));
+      if (b > 0) mid = max(mid, static_cast<u64>(b));
+      if (a < 0 || b < 0) neg = 1;
+    }
     if (i + 1 < n && t > st_t[j + 1]) shape |= 1u;
     if (i + kSegMax < n && t == st_t[j + kSegMax]) shape |= 2u;
     if (rec) {
@@ -201,13 +215,14 @@ __global__ void __launch_bounds__(kBlock) k_batch_stats(const i64* bs, const i64
       const int jend = jn < kStatSpan ? static_cast<int>(jn) : kStatSpan;       // of edge n (clamped)
       while (lo > jmin && j - lo < kSegMax && st_t[lo - 1] == t) --lo;
       while (hi < jend && hi - j < kSegMax && st_t[hi] == t) ++hi;
-      const u64 key = (static_cast<u64>(st_a[j]) << 32) | st_b[j];
+      const u32 aj = static_cast<u32>(st_a[j]), bj = static_cast<u32>(st_b[j]);
+      const u64 key = (static_cast<u64>(aj) << 32) | bj;
       u32 rank = 0;
       for (int q = lo; q < hi; ++q) {
-        const u64 kq = (static_cast<u64>(st_a[q]) << 32) | st_b[q];
+        const u64 kq = (static_cast<u64>(static_cast<u32>(st_a[q])) << 32) | static_cast<u32>(st_b[q]);
         rank += (kq < key || (kq == key && q < j)) ? 1u : 0u;
       }
-      rec[wr(static_cast<u32>(lo_g + lo + rank))] = EdgeRec{st_a[j], st_b[j], t};
+      rec[wr(static_cast<u32>(lo_g + lo + rank))] = EdgeRec{aj, bj, t};
     }
   }
   if (kGroups) {
@@ -1176,6 +1191,14 @@ void window_ingest(Window& w, const i64* d_src, const i64* d_dst, const i64* d_t
     TWG_CUDA(cudaMemsetAsync(ctx.d_scalars + 12, 0, 8, st));
   }
   const u64 stat_tiles = (n + kStatTile - 1) / kStatTile;
+  static const bool stat_attr = [] {
+    TWG_CUDA(cudaFuncSetAttribute(k_batch_stats<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sizeof(StatSmem))));
+    TWG_CUDA(cudaFuncSetAttribute(k_batch_stats<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sizeof(StatSmem))));
+    return true;
+  }();
+  (void)stat_attr;
   TsSpec ts{};
   spec.groups = spec.on && spec.in_log && stats_groups_enabled();
   if (spec.groups) {
@@ -1184,11 +1207,11 @@ void window_ingest(Window& w, const i64* d_src, const i64* d_dst, const i64* d_t
     TWG_CUDA(cudaMemsetAsync(spec.ts_state.p, 0, spec.ts_state.bytes(), st));
     ts = TsSpec{spec.ts_state.p, L.ts_off.p, L.ts_time.p, L.zlen % L.cap, L.cap,
                 old.seq0 + static_cast<u32>(old.m), ctx.d_scalars + 14};
-    k_batch_stats<true><<<static_cast<unsigned>(stat_tiles), kBlock, 0, st>>>(d_src, d_dst, d_t, n, ctx.d_scalars,
-                                                                              spec.rec, spec.wring, ts);
+    k_batch_stats<true><<<static_cast<unsigned>(stat_tiles), kBlock, sizeof(StatSmem), st>>>(
+        d_src, d_dst, d_t, n, ctx.d_scalars, spec.rec, spec.wring, ts);
   } else {
-    k_batch_stats<false><<<static_cast<unsigned>(stat_tiles), kBlock, 0, st>>>(d_src, d_dst, d_t, n, ctx.d_scalars,
-                                                                               spec.rec, spec.wring, ts);
+    k_batch_stats<false><<<static_cast<unsigned>(stat_tiles), kBlock, sizeof(StatSmem), st>>>(
+        d_src, d_dst, d_t, n, ctx.d_scalars, spec.rec, spec.wring, ts);
   }
   TWG_LAUNCHED(ctx);
   if (spec.on) {
