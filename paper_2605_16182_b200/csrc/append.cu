@@ -241,49 +241,6 @@ __global__ void k_bucket_bounds(const u32* keys, u64 Yn, u64 nb, u32* bstart) {
   }
 }
 
-// Per-node batch counts from the bucket-sorted keys (one CTA per bucket),
-// and the owner side of the newest-incident-time update: a node's last entry
-// in the (canonical) bucket order carries its newest batch time.
-template <class PV>
-__global__ void __launch_bounds__(kPB) k_bucket_count(const u32* keys, const PV* vals, const u32* bstart, u64 V,
-                                                      i64 tb, u32* y, const i64* old_last, i64* last_t, i64 cutoff,
-                                                      u64* dead) {
-  // old_last != null: last_t[v] = max(old_last[v], the batch's owner-side
-  // newest) for every node of the bucket (the new snapshot's copy, no
-  // separate device copy); else updated in place. dead != null: the nodes
-  // whose newest time falls before the cutoff (they would leave) are counted.
-  __shared__ u32 cnt[kPB];
-  __shared__ u32 lastq[kPB];
-  const u64 bkt = blockIdx.x;
-  cnt[threadIdx.x] = 0;
-  lastq[threadIdx.x] = 0;
-  __syncthreads();
-  const u32 bs = bstart[bkt], be = bstart[bkt + 1];
-  for (u32 q = bs + threadIdx.x; q < be; q += kPB) {
-    const u32 nd = keys[q] & (kPB - 1);
-    atomicAdd(&cnt[nd], 1u);
-    atomicMax(&lastq[nd], q + 1);
-  }
-  __syncthreads();
-  const u64 v = (bkt << kBucketShift) + threadIdx.x;
-  u64 d = 0;
-  if (v < V) {
-    y[v] = cnt[threadIdx.x];
-    if (last_t) {
-      i64 lt = old_last ? old_last[v] : last_t[v];
-      const bool upd = cnt[threadIdx.x] != 0;
-      if (upd) {
-        const i64 t = Payload<PV>::time(vals[lastq[threadIdx.x] - 1], tb);
-        if (lt < t) lt = t;
-      }
-      if (old_last || upd) last_t[v] = lt;
-      d = lt < cutoff ? 1u : 0u;
-    }
-  }
-  if (dead) block_atomic_add(reinterpret_cast<unsigned long long*>(dead), d);
-}
-
-
 // Eviction bound: first logical x in [lo, hi) with time >= c. The times
 // from lo to the end of lo's 128-B line (kLine keys of the array) are loaded
 // at once (independent loads, one round trip, one DRAM line — the whole line
@@ -310,6 +267,7 @@ struct Reloc {
   u32 v, src_e, src_g;
 };
 
+template <class PV>
 struct PlanArgs {
   const NodeMeta* onm;  // the current snapshot
   const NodeMeta* rnm;  // the retired one when it shares the arena (its rings stay readable), else null
@@ -317,7 +275,6 @@ struct PlanArgs {
   const Entry* oent;
   const i64* omt;
   const u32* oms;
-  const u32* y;
   i64 cutoff;
   int need_last;        // a batch time may equal a node's newest live time (mark merge)
   int relocate_all;     // repack every ring into a fresh arena
@@ -327,24 +284,66 @@ struct PlanArgs {
   i64* last_t;          // time of the last live entry (valid iff need_last and plan.ee > plan.eb)
   Reloc* reloc;
   u64* scal;            // [0] bump, [1] overflow, [2] relocations
+  // the batch's per-node counts, from the bucket-sorted keys (one bucket per
+  // CTA iteration), and the newest-time update (see the note at k_plan)
+  const u32* keys;
+  const PV* vals;
+  const u32* bstart;
+  i64 tb;               // time base of PEnt payloads
+  const i64* old_last;  // null: node_last is updated in place
+  i64* node_last;       // the new snapshot's newest incident time per node (null: none)
+  u64* dead;            // null, or: count the nodes whose newest time falls before the cutoff
 };
 
 // Per node: eviction (cutoff lower bound on the ring's entry and mark
 // times), room check against the oldest live begin in the ring (the retired
 // snapshot's, while it shares the ring), otherwise a new ring from the bump
 // allocator (CTA-aggregated) with logical positions rebased to 0.
-__global__ void __launch_bounds__(kBlock) k_plan(PlanArgs a) {
+//
+// One CTA iteration = one bucket of kPB nodes: the bucket's batch entries are
+// counted per node first (shared-memory atomics over the bucket-sorted keys;
+// a node's last entry in canonical order carries its newest batch time), which
+// also updates the newest-incident-time array (owner side; max with the old
+// snapshot's) and counts nodes about to leave the window — the former
+// k_bucket_count pass, without its per-node count array round trip.
+template <class PV>
+__global__ void __launch_bounds__(kBlock) k_plan(PlanArgs<PV> a) {
+  static_assert(kBlock == kPB, "one bucket per CTA iteration");
   __shared__ u64 s_base;
   __shared__ u32 s_rbase;
+  __shared__ u32 cnt[kPB], lastq[kPB];
   for (u64 b0 = static_cast<u64>(blockIdx.x) * kBlock; b0 < a.V; b0 += static_cast<u64>(gridDim.x) * kBlock) {
     const u64 v = b0 + threadIdx.x;
     const bool valid = v < a.V;
+    cnt[threadIdx.x] = 0;
+    lastq[threadIdx.x] = 0;
+    __syncthreads();
+    {
+      const u64 bkt = b0 >> kBucketShift;
+      const u32 bs = a.bstart[bkt], be = a.bstart[bkt + 1];
+      for (u32 q = bs + threadIdx.x; q < be; q += kPB) {
+        const u32 nd = a.keys[q] & (kPB - 1);
+        atomicAdd(&cnt[nd], 1u);
+        atomicMax(&lastq[nd], q + 1);
+      }
+    }
+    __syncthreads();
     NodeMeta o{};
     u32 eb = 0, gb = 0, req = 0, y = 0;
     bool fits = true;
+    u64 d = 0;
     if (valid) {
       o = a.onm[v];
-      y = a.y[v];
+      y = cnt[threadIdx.x];
+      if (a.node_last) {
+        i64 lt = a.old_last ? a.old_last[v] : a.node_last[v];
+        if (y) {
+          const i64 t = Payload<PV>::time(a.vals[lastq[threadIdx.x] - 1], a.tb);
+          if (lt < t) lt = t;
+        }
+        if (a.old_last || y) a.node_last[v] = lt;
+        d = lt < a.cutoff ? 1u : 0u;
+      }
       const Ring oer = entry_ring(o), omr = mark_ring(o);
       if (implicit_marks(o)) {
         // single-entry groups (distinct times: the common case): marks are
@@ -394,6 +393,7 @@ __global__ void __launch_bounds__(kBlock) k_plan(PlanArgs a) {
         a.reloc[s_rbase + midx] = Reloc{static_cast<u32>(v), eb, gb};
       }
     }
+    if (a.dead) block_atomic_add(reinterpret_cast<unsigned long long*>(a.dead), d);
     __syncthreads();
   }
 }
@@ -822,11 +822,6 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
     //    placement, marks, publish
     s->nm.alloc(V, st);
     s->wrec.alloc(V, st);
-    DevBuf<u32> ycnt(V, st);
-    if (check_dead) TWG_CUDA(cudaMemsetAsync(sc + 13, 0, sizeof(u64), st));
-    k_bucket_count<PV><<<static_cast<unsigned>(nb), kPB, 0, st>>>(kp, vp, bstart.p, V, tbase, ycnt.p, old_last,
-                                                                 s->last_t.p, cutoff, check_dead ? sc + 13 : nullptr);
-    TWG_LAUNCHED(ctx);
     // fast route: the population must not shrink — the dead count (sc[13]) is
     // read back with the plan's scalars; nothing is published before
     bool dead = false;
@@ -842,15 +837,22 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
     DevBuf<Reloc> reloc(V, st);
     auto run_plan = [&](NodeArena& dst, bool all) {
       TWG_CUDA(cudaMemsetAsync(sc, 0, 3 * sizeof(u64), st));
+      if (check_dead) TWG_CUDA(cudaMemsetAsync(sc + 13, 0, sizeof(u64), st));
       TWG_CUDA(cudaMemcpyAsync(sc, &dst.used, sizeof(u64), cudaMemcpyHostToDevice, st));
-      PlanArgs pa;
+      PlanArgs<PV> pa;
       pa.onm = O.nm.p;
       pa.rnm = (!all && R && R->gapped && R->arena.get() == &dst) ? R->nm.p : nullptr;
       pa.V = V;
       pa.oent = O.ent.p;
       pa.omt = O.mk_time.p;
       pa.oms = O.mk_start.p;
-      pa.y = ycnt.p;
+      pa.keys = kp;
+      pa.vals = vp;
+      pa.bstart = bstart.p;
+      pa.tb = tbase;
+      pa.old_last = old_last;
+      pa.node_last = s->last_t.p;
+      pa.dead = check_dead ? sc + 13 : nullptr;
       pa.need_last = no_ties ? 0 : 1;
       pa.cutoff = cutoff;
       pa.relocate_all = all ? 1 : 0;
@@ -860,7 +862,7 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
       pa.last_t = last_t.p;
       pa.reloc = reloc.p;
       pa.scal = sc;
-      k_plan<<<grid(ctx, V), kBlock, 0, st>>>(pa);
+      k_plan<PV><<<grid(ctx, V), kBlock, 0, st>>>(pa);
       TWG_LAUNCHED(ctx);
       u64 r3[14];
       read_scalars(ctx, sc, r3, check_dead ? 14 : 3);
