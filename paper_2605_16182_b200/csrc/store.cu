@@ -528,10 +528,39 @@ __global__ void k_entry_owners(const uint2* nmeta, u64 V, u32* owners) {
 }
 }  // namespace
 
+// walk records of a contiguous store (identity ring): bounds + the newest
+// kWalkTail entries of each region, newest first (store.cuh WalkRec)
+__global__ void k_wrec_from_nm(const NodeMeta* nm, const Entry* ent, u64 V, WalkRec* wrec) {
+  for (u64 v = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; v < V;
+       v += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const NodeMeta m = nm[v];
+    WalkRec w;
+    w.eb = m.eb;
+    w.ee = m.ee;
+    w.base = m.base;
+    w.cap = m.cap;
+    w.eorg = m.eorg;
+    w.g = m.ge - m.gb;
+    w.pad = 0;
+    const Ring er = entry_ring(m);
+#pragma unroll
+    for (u32 i = 0; i < kWalkTail; ++i) {
+      const bool in = i < m.ee - m.eb;
+      const Entry e = in ? ent[er(m.ee - 1 - i)] : Entry{0u, 0u, 0};
+      w.nbr[i] = e.nbr;
+      w.t[i] = e.t;
+    }
+    wrec[v] = w;
+  }
+}
+
 void build_nm(Ctx& ctx, Store& s) {
   s.nm.alloc(s.V ? s.V : 1, ctx.stream);
   if (s.V) {
     k_nm_from_nmeta<<<grid(ctx, s.V), kBlock, 0, ctx.stream>>>(s.nmeta.p, s.V, s.nm.p);
+    TWG_LAUNCHED(ctx);
+    s.wrec.alloc(s.V, ctx.stream);
+    k_wrec_from_nm<<<grid(ctx, s.V), kBlock, 0, ctx.stream>>>(s.nm.p, s.ent.p, s.V, s.wrec.p);
     TWG_LAUNCHED(ctx);
   }
 }

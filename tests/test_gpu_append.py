@@ -66,9 +66,12 @@ def _check_walks(tw, co, snap, ed, mode):
                         start_bias=bias, direction=direction, seed=5)
                 exp, _ = co.generate(edges, mode, c)
                 # fresh handle each time: the weighted configurations run on
-                # the snapshot's contiguous form, the others on the slices
-                ws = tw.generate_walks(snap, to_cfg(tw, c))
-                assert_walks(ws, exp)
+                # the snapshot's contiguous form, the others on the slices;
+                # FullWalk takes the walk-record path (hop_rec) for the
+                # forward index biases, Coop the ring path
+                for variant in (tw.Variant.Coop, tw.Variant.FullWalk):
+                    ws = tw.generate_walks(snap, to_cfg(tw, c), variant=variant)
+                    assert_walks(ws, exp)
         c = Cfg(walk_length=10, start_mode=1, total_walks=500, bias=3, start_bias=0, node2vec=1, p=0.5, q=2.0,
                 direction=direction, seed=9)
         exp, _ = co.generate(edges, mode, c)
