@@ -5,7 +5,7 @@ out=gpurun_out/ab_ingest.txt; : > $out
 timeout 900 python -m pytest tests -m gpu -x -q -k "append or parity or golden or group" 2>&1 | tail -3 >> $out
 for envs in "$@"; do
   echo "== $envs" >> $out
-  env $envs timeout 600 python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --no-audit 2>/dev/null | python -c "
+  env $envs timeout 600 python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu-baseline --no-audit 2>/dev/null | python -c "
 import json,sys
 for l in sys.stdin:
   l=l.strip()
