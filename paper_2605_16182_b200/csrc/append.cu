@@ -716,7 +716,7 @@ bool append_log_slot(const Store& O, const Store* R, u64 A, Ring* wr) {
 Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const EdgeRec* batch, Ring bring, u64 A,
                      u64 from, i64 cutoff, bool no_ties, bool in_log, bool check_dead, const i64* bt,
                      const i64* const* bcols, const u64* groups_done, i64 tbase, bool compact,
-                     const i64* old_last) {
+                     const i64* old_last, u32* pre_hist) {
   Ctx& ctx = *w.ctx;
   cudaStream_t st = ctx.stream;
   PhaseTimer pt(ctx, "ingest_append");
@@ -806,7 +806,7 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
       OwnerIn<PV> oin{brec, wr, mode, seq_b, tbase};
       oin.bs = bcols ? bcols[0] : nullptr;
       oin.bd = bcols ? bcols[1] : nullptr;
-      radix_sort_pairs_from<u32, PV>(ctx, oin, &kp, &ka, &vp, &va, Yn, vb, kBucketShift);
+      radix_sort_pairs_from<u32, PV>(ctx, oin, &kp, &ka, &vp, &va, Yn, vb, kBucketShift, pre_hist);
     } else {
       k_owner_keys<PV><<<grid(ctx, Yn), kBlock, 0, st>>>(brec, wr, A, mode, seq_b, tbase, kp, vp);
       TWG_LAUNCHED(ctx);

@@ -659,9 +659,12 @@ __global__ void __launch_bounds__(kSortBlock) k_radix_onesweep(In in, K* __restr
 // Passes over key bits [lo_bit, bits): the first reads through `in0`, the
 // rest ping-pong between (*keys, *vals) and the alt buffers; the sorted
 // result ends in (*keys, *vals). Keys-only when the values are null.
+// pre_hist (device, passes x 256 digit counts of the items): computed by the
+// caller (the statistics pass fuses the owner-digit histogram), so the
+// histogram kernel is skipped; it is consumed (turned into digit starts).
 template <class K, class V, class In>
 void radix_sort_impl(Ctx& ctx, In in0, bool from_in, K** keys, K** keys_alt, V** vals, V** vals_alt, u64 n,
-                     int bits, int lo_bit) {
+                     int bits, int lo_bit, u32* pre_hist = nullptr) {
   using S = OnesweepSmem<K, V>;
   cudaStream_t st = ctx.stream;
   const int passes = (bits - lo_bit + kRadixBits - 1) / kRadixBits;
@@ -676,15 +679,20 @@ void radix_sort_impl(Ctx& ctx, In in0, bool from_in, K** keys, K** keys_alt, V**
     return true;
   }();
   (void)attr;
-  DevBuf<u32> hist(static_cast<u64>(passes) * kRadix, st);
+  DevBuf<u32> own_hist;
   DevBuf<u64> state(tiles * kRadix + 1, st);  // + the ticket word
-  TWG_CUDA(cudaMemsetAsync(hist.p, 0, hist.bytes(), st));
-  const unsigned hgrid = grid_for(n, kSortBlock, static_cast<unsigned>(ctx.sm_count) * 8);
-  if (from_in) k_radix_global_hist<K, In><<<hgrid, kSortBlock, 0, st>>>(in0, n, lo_bit, passes, hist.p);
-  else k_radix_global_hist<K, ArrayIn<K, V>><<<hgrid, kSortBlock, 0, st>>>(ArrayIn<K, V>{*keys, *vals}, n, lo_bit,
-                                                                            passes, hist.p);
-  TWG_LAUNCHED(ctx);
-  k_radix_digit_starts<<<1, kRadix, 0, st>>>(hist.p, passes);
+  u32* hist = pre_hist;
+  if (!hist) {
+    own_hist.alloc(static_cast<u64>(passes) * kRadix, st);
+    hist = own_hist.p;
+    TWG_CUDA(cudaMemsetAsync(hist, 0, own_hist.bytes(), st));
+    const unsigned hgrid = grid_for(n, kSortBlock, static_cast<unsigned>(ctx.sm_count) * 8);
+    if (from_in) k_radix_global_hist<K, In><<<hgrid, kSortBlock, 0, st>>>(in0, n, lo_bit, passes, hist);
+    else k_radix_global_hist<K, ArrayIn<K, V>><<<hgrid, kSortBlock, 0, st>>>(ArrayIn<K, V>{*keys, *vals}, n, lo_bit,
+                                                                              passes, hist);
+    TWG_LAUNCHED(ctx);
+  }
+  k_radix_digit_starts<<<1, kRadix, 0, st>>>(hist, passes);
   TWG_LAUNCHED(ctx);
   u32* ticket = reinterpret_cast<u32*>(state.p + tiles * kRadix);
   for (int p = 0; p < passes; ++p) {
@@ -692,10 +700,10 @@ void radix_sort_impl(Ctx& ctx, In in0, bool from_in, K** keys, K** keys_alt, V**
     TWG_CUDA(cudaMemsetAsync(state.p, 0, state.bytes(), st));
     if (p == 0 && from_in) {
       k_radix_onesweep<K, V, In><<<static_cast<unsigned>(tiles), kSortBlock, sizeof(S), st>>>(
-          in0, *keys, *vals, n, shift, hist.p + p * kRadix, state.p, ticket);
+          in0, *keys, *vals, n, shift, hist + p * kRadix, state.p, ticket);
     } else {
       k_radix_onesweep<K, V, ArrayIn<K, V>><<<static_cast<unsigned>(tiles), kSortBlock, sizeof(S), st>>>(
-          ArrayIn<K, V>{*keys, *vals}, *keys_alt, *vals_alt, n, shift, hist.p + p * kRadix, state.p, ticket);
+          ArrayIn<K, V>{*keys, *vals}, *keys_alt, *vals_alt, n, shift, hist + p * kRadix, state.p, ticket);
       std::swap(*keys, *keys_alt);
       std::swap(*vals, *vals_alt);
     }
@@ -716,8 +724,18 @@ void radix_sort_pairs(Ctx& ctx, K** keys, K** keys_alt, V** vals, V** vals_alt, 
 // (*keys, *vals); n >= 1).
 template <class K, class V, class In>
 void radix_sort_pairs_from(Ctx& ctx, In in, K** keys, K** keys_alt, V** vals, V** vals_alt, u64 n, int bits,
-                           int lo_bit) {
-  radix_sort_impl<K, V>(ctx, in, true, keys, keys_alt, vals, vals_alt, n, bits > lo_bit ? bits : lo_bit + 1, lo_bit);
+                           int lo_bit, u32* pre_hist = nullptr) {
+  radix_sort_impl<K, V>(ctx, in, true, keys, keys_alt, vals, vals_alt, n, bits > lo_bit ? bits : lo_bit + 1, lo_bit,
+                        pre_hist);
+}
+
+// Per-tile digit-count rows (rows x 2*256, the statistics pass's output)
+// summed into hist (zeroed) — the fused owner-digit histogram's reduction.
+static __global__ void __launch_bounds__(512) k_hist_rows(const u32* rows, u64 nrows, u64 rows_per_block, u32* hist) {
+  const u64 r0 = blockIdx.x * rows_per_block, r1 = min(nrows, r0 + rows_per_block);
+  u32 acc = 0;
+  for (u64 r = r0; r < r1; ++r) acc += rows[r * 512 + threadIdx.x];
+  if (acc) atomicAdd(&hist[threadIdx.x], acc);
 }
 
 }  // namespace twg

@@ -60,6 +60,7 @@ struct FastSpec {
   const i64* cols[2] = {nullptr, nullptr};  // its source / target columns (input order)
   DevBuf<u64> ts_state;  // look-back words of the statistics pass's ts-group numbering
   bool groups = false;   // the statistics pass wrote the batch's ts groups into the log (total: d_scalars[14])
+  DevBuf<u32> hist_rows, hist;  // the fused owner-digit histogram (rows per tile, their sum)
 };
 
 // scal[8]: batch min t, scal[9]: some id negative.
@@ -82,11 +83,18 @@ struct FastSpec {
 constexpr int kStatItems = 8;
 constexpr int kStatTile = kBlock * kStatItems;
 constexpr int kStatSpan = kStatTile + 2 * kSegMax;
-constexpr int kStatRounds = (kStatSpan + kBlock - 1) / kBlock;
 
 bool compact_payload_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("TWG_COMPACT_PAYLOAD");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+bool stats_hist_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TWG_STATS_HIST");
     return !(e && e[0] == '0');
   }();
   return on;
@@ -116,9 +124,18 @@ struct StatSmem {
   i64 t[kStatSpan], a[kStatSpan], b[kStatSpan];
 };
 
+// the owner-digit histogram of the bucket sort, fused (fast route): per tile
+// one row of 2 x 256 counts (digits of bits 8-15 and 16-23 of each entry's
+// owner), summed by k_hist_rows
+struct HistSpec {
+  u32* rows;   // null: not fused
+  int passes;  // 1 or 2
+  int mode;    // direction mode: which endpoint(s) own the entries
+};
+
 template <bool kGroups>
 __global__ void __launch_bounds__(kBlock) k_batch_stats(const i64* bs, const i64* bd, const i64* bt, u64 n, u64* scal,
-                                                        EdgeRec* rec, Ring wr, TsSpec ts) {
+                                                        EdgeRec* rec, Ring wr, TsSpec ts, HistSpec hs) {
   extern __shared__ __align__(128) unsigned char stat_smem[];
   StatSmem& S = *reinterpret_cast<StatSmem*>(stat_smem);
   i64* st_t = S.t;
@@ -128,6 +145,10 @@ __global__ void __launch_bounds__(kBlock) k_batch_stats(const i64* bs, const i64
   __shared__ u32 s_cnt[kStatItems][kBlock / 32];
   __shared__ u64 s_prefix;
   __shared__ alignas(8) u64 s_bar;
+  __shared__ u32 s_hist[2][kRadix];
+  static_assert(kBlock == kRadix, "one histogram bin per thread");
+  const bool fuse_hist = kGroups && hs.rows != nullptr;
+  if (fuse_hist) s_hist[0][threadIdx.x] = 0, s_hist[1][threadIdx.x] = 0;  // kBlock == kRadix
   i64 mt = kTimeUnset, lt = kTimeInfinite;
   u64 mid = 0;
   u32 shape = 0, neg = 0;
@@ -205,6 +226,16 @@ __global__ void __launch_bounds__(kBlock) k_batch_stats(const i64* bs, const i64
       if (a > 0) mid = max(mid, static_cast<u64>(a));
       if (b > 0) mid = max(mid, static_cast<u64>(b));
       if (a < 0 || b < 0) neg = 1;
+      if (fuse_hist) {
+        const u32 o1 = static_cast<u32>(hs.mode == TWG_BACKWARD ? b : a);
+        atomicAdd(&s_hist[0][(o1 >> 8) & (kRadix - 1)], 1u);
+        if (hs.passes > 1) atomicAdd(&s_hist[1][(o1 >> 16) & (kRadix - 1)], 1u);
+        if (hs.mode == TWG_UNDIRECTED) {
+          const u32 o2 = static_cast<u32>(b);
+          atomicAdd(&s_hist[0][(o2 >> 8) & (kRadix - 1)], 1u);
+          if (hs.passes > 1) atomicAdd(&s_hist[1][(o2 >> 16) & (kRadix - 1)], 1u);
+        }
+      }
     }
     if (i + 1 < n && t > st_t[j + 1]) shape |= 1u;
     if (i + kSegMax < n && t == st_t[j + kSegMax]) shape |= 2u;
@@ -269,6 +300,11 @@ __global__ void __launch_bounds__(kBlock) k_batch_stats(const i64* bs, const i64
       ts.ts_off[z] = ts.seq_b + static_cast<u32>(i);
       ts.ts_time[z] = st_t[j];
     }
+  }
+  if (fuse_hist) {
+    __syncthreads();
+    hs.rows[tile * 512 + threadIdx.x] = s_hist[0][threadIdx.x];
+    hs.rows[tile * 512 + kRadix + threadIdx.x] = s_hist[1][threadIdx.x];
   }
   // one set of atomics per block (the whole grid finishes at once: per-warp
   // atomics on these words would serialise at L2); signed times through the
@@ -1113,7 +1149,7 @@ Store* ingest_fast(Window& w, FastSpec& spec, u64 n, const u64* sc, i64 cutoff, 
       ingest_append(w, O, std::move(s), spec.rec, spec.wring, n, from, cutoff, true, spec.in_log, true, spec.bt,
                     spec.cols, spec.groups ? ctx.d_scalars + 14 : nullptr, batch_min,
                     compact_payload_enabled() && static_cast<u64>(static_cast<i64>(sc[0]) - batch_min) < (1ull << 32),
-                    O.last_t.p);
+                    O.last_t.p, spec.hist.n ? spec.hist.p : nullptr);
   if (!out) {  // an old node leaves the window: the general route recomputes everything
     stats->evicted = stats->dropped_late = 0;
     return nullptr;
@@ -1207,11 +1243,27 @@ void window_ingest(Window& w, const i64* d_src, const i64* d_dst, const i64* d_t
     TWG_CUDA(cudaMemsetAsync(spec.ts_state.p, 0, spec.ts_state.bytes(), st));
     ts = TsSpec{spec.ts_state.p, L.ts_off.p, L.ts_time.p, L.zlen % L.cap, L.cap,
                 old.seq0 + static_cast<u32>(old.m), ctx.d_scalars + 14};
+    // the bucket sort's owner-digit histogram, fused (<= 2 digit passes above the 256-node bucket)
+    HistSpec hs{nullptr, 0, w.mode};
+    const int vb = old.V > 1 ? bit_width_u64(old.V - 1) : 0;
+    const int passes = vb > 8 ? (vb - 8 + 7) / 8 : 0;
+    if (passes >= 1 && passes <= 2 && stats_hist_enabled()) {
+      spec.hist_rows.alloc(stat_tiles * 512, st);
+      spec.hist.alloc(512, st);
+      TWG_CUDA(cudaMemsetAsync(spec.hist.p, 0, spec.hist.bytes(), st));
+      hs = HistSpec{spec.hist_rows.p, passes, w.mode};
+    }
     k_batch_stats<true><<<static_cast<unsigned>(stat_tiles), kBlock, sizeof(StatSmem), st>>>(
-        d_src, d_dst, d_t, n, ctx.d_scalars, spec.rec, spec.wring, ts);
+        d_src, d_dst, d_t, n, ctx.d_scalars, spec.rec, spec.wring, ts, hs);
+    if (hs.rows) {
+      TWG_LAUNCHED(ctx);
+      constexpr u64 kRowsPerBlock = 256;
+      k_hist_rows<<<static_cast<unsigned>((stat_tiles + kRowsPerBlock - 1) / kRowsPerBlock), 512, 0, st>>>(
+          spec.hist_rows.p, stat_tiles, kRowsPerBlock, spec.hist.p);
+    }
   } else {
     k_batch_stats<false><<<static_cast<unsigned>(stat_tiles), kBlock, sizeof(StatSmem), st>>>(
-        d_src, d_dst, d_t, n, ctx.d_scalars, spec.rec, spec.wring, ts);
+        d_src, d_dst, d_t, n, ctx.d_scalars, spec.rec, spec.wring, ts, HistSpec{nullptr, 0, 0});
   }
   TWG_LAUNCHED(ctx);
   if (spec.on) {
