@@ -315,6 +315,14 @@ __global__ void __launch_bounds__(kBlock) k_plan(PlanArgs<PV> a) {
   for (u64 b0 = static_cast<u64>(blockIdx.x) * kBlock; b0 < a.V; b0 += static_cast<u64>(gridDim.x) * kBlock) {
     const u64 v = b0 + threadIdx.x;
     const bool valid = v < a.V;
+    // the node's own rows go out before the bucket's key counting
+    NodeMeta o{}, rm{};
+    i64 lt_old = 0;
+    if (valid) {
+      o = a.onm[v];
+      if (a.rnm) rm = a.rnm[v];
+      if (a.node_last) lt_old = a.old_last ? a.old_last[v] : a.node_last[v];
+    }
     cnt[threadIdx.x] = 0;
     lastq[threadIdx.x] = 0;
     __syncthreads();
@@ -328,15 +336,13 @@ __global__ void __launch_bounds__(kBlock) k_plan(PlanArgs<PV> a) {
       }
     }
     __syncthreads();
-    NodeMeta o{};
     u32 eb = 0, gb = 0, req = 0, y = 0;
     bool fits = true;
     u64 d = 0;
     if (valid) {
-      o = a.onm[v];
       y = cnt[threadIdx.x];
       if (a.node_last) {
-        i64 lt = a.old_last ? a.old_last[v] : a.node_last[v];
+        i64 lt = lt_old;
         if (y) {
           const i64 t = Payload<PV>::time(a.vals[lastq[threadIdx.x] - 1], a.tb);
           if (lt < t) lt = t;
@@ -358,10 +364,7 @@ __global__ void __launch_bounds__(kBlock) k_plan(PlanArgs<PV> a) {
         eb = gb == o.ge ? o.ee : a.oms[omr(gb)];
       }
       u32 low = o.eb;
-      if (a.rnm) {
-        const NodeMeta r = a.rnm[v];
-        if (r.base == o.base && r.cap == o.cap) low = r.eb;  // same ring: the retired snapshot reads [r.eb, ..)
-      }
+      if (a.rnm && rm.base == o.base && rm.cap == o.cap) low = rm.eb;  // same ring: the retired snapshot reads [rm.eb, ..)
       // Logical positions are u32 and only rebased when a ring moves: a ring
       // that keeps fitting would otherwise count past 2^32 over a long
       // stream and break every [eb, ee) comparison, so it moves first.
@@ -468,6 +471,23 @@ __global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs<PV> a) {
   const u64 v = (bkt << kBucketShift) + t;
   const bool valid = v < a.V;
   const u32 bs = a.bstart[bkt], be = a.bstart[bkt + 1];
+  // the first chunk's keys and payload prefetch go out before the plan row,
+  // so the CTA's first DRAM round trips overlap
+  // (item i = warp*R*32 + r*32 + lane of a chunk belongs to this lane in round r)
+  u32 dk[kChunkItems];
+  auto load_chunk = [&](u32 c0, u32 n) {
+#pragma unroll
+    for (int r = 0; r < kChunkItems; ++r) {  // the payloads' DRAM fetch starts now, into L2
+      const u32 i = warp * (32 * kChunkItems) + r * 32 + lane;
+      if (i < n) prefetch_l2(a.vals + c0 + i);
+    }
+#pragma unroll
+    for (int r = 0; r < kChunkItems; ++r) {
+      const u32 i = warp * (32 * kChunkItems) + r * 32 + lane;
+      dk[r] = i < n ? (a.keys[c0 + i] & (kPB - 1)) : 0u;
+    }
+  };
+  if (be > bs) load_chunk(bs, min(static_cast<u32>(kChunk), be - bs));
   NodeMeta p{};
   i64 lt_v = 0;
   if (valid) {  // independent loads, in flight together
@@ -489,18 +509,7 @@ __global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs<PV> a) {
   for (u32 c0 = bs; c0 < be; c0 += kChunk) {
     const u32 n = min(static_cast<u32>(kChunk), be - c0);
     __syncthreads();
-    // item i = warp*R*32 + r*32 + lane of the chunk belongs to this lane in round r
-    u32 dk[kChunkItems];
-#pragma unroll
-    for (int r = 0; r < kChunkItems; ++r) {  // the payloads' DRAM fetch starts now, into L2
-      const u32 i = warp * (32 * kChunkItems) + r * 32 + lane;
-      if (i < n) prefetch_l2(a.vals + c0 + i);
-    }
-#pragma unroll
-    for (int r = 0; r < kChunkItems; ++r) {
-      const u32 i = warp * (32 * kChunkItems) + r * 32 + lane;
-      dk[r] = i < n ? (a.keys[c0 + i] & (kPB - 1)) : 0u;
-    }
+    if (c0 != bs) load_chunk(c0, n);  // later chunks (the first one is in flight since the start)
     for (int i = t; i < (kPB / 32) * kPB; i += kPB) (&sm.wcnt[0][0])[i] = 0;
     sm.tie[t] = 0;
     __syncthreads();

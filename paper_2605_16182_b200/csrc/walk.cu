@@ -48,13 +48,6 @@ struct WalkParams {
   i64* times;
   const double* exp_neg;
   const double* expm1_tab;
-  // newest time in each node's view (>= every entry time of v's region; the
-  // store's last_t), or null: a forward walk at time t ends at v without
-  // touching v's NodeMeta or ring when last_t[v] <= t (its causal slice is
-  // empty) — every walk's terminal hop costs one small, mostly L2-resident
-  // load instead of a NodeMeta sector plus the ring's end atom
-  const i64* last_t;
-  u64 l2_keep;  // createpolicy evict_last (0: no hint)
   int rec;      // hop through the store's walk records (hop_rec)
 };
 
@@ -749,18 +742,11 @@ __global__ void k_fold_stats(const u64* part, u64* stats) {
   if (lane == 0) stats[q] = q == 2 ? max(stats[q], acc) : stats[q] + acc;
 }
 
-__device__ __forceinline__ i64 load_last_t(const i64* p, u64 pol) {
-  i64 v;
-  if (pol) asm volatile("ld.global.nc.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
-  else v = __ldg(p);
-  return v;
-}
-
 // One thread per walk, init fused, the whole walk in registers
 // (walk_engine.cpp:380-392). kWB-thread blocks (32 by default): a block
 // retires — and its slots take new walks — as soon as its own walks end.
-template <int kWB, bool kRec, int kMinB = 1024 / kWB>
-__global__ void __launch_bounds__(kWB, kMinB) k_fullwalk(WalkParams P, InitParams I, u64 count, u32* lengths,
+template <int kWB, bool kRec>
+__global__ void __launch_bounds__(kWB, 1024 / kWB) k_fullwalk(WalkParams P, InitParams I, u64 count, u32* lengths,
                                                           u64* part) {
   const u64 wl = blockIdx.x * static_cast<u64>(kWB) + threadIdx.x;
   const bool active = wl < count;
@@ -768,8 +754,6 @@ __global__ void __launch_bounds__(kWB, kMinB) k_fullwalk(WalkParams P, InitParam
   u32 init_len = 0;
   WalkReg r{};
   if (active) {
-    u64 pol = 0;
-    if (P.l2_keep) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     init_walk(P, I, wl, r, &cn);
     init_len = r.len;
     // the snapshot's time span: anchors of the interpolation search
@@ -779,7 +763,6 @@ __global__ void __launch_bounds__(kWB, kMinB) k_fullwalk(WalkParams P, InitParam
         if (!hop_rec(P, wl, r, load_wrec(P.s.wrec + r.cur), &cn, tl)) break;
     }
     while (!kRec && r.len < P.stride) {
-      if (P.last_t && load_last_t(P.last_t + r.cur, pol) <= r.t) break;  // nothing later than t at r.cur
       const NodeMeta a = P.s.nm[r.cur];
       if (!hop(P, wl, r, P.s.mk_time, P.s.mk_start, mark_ring(a), a.gb, a.ge, entry_ring(a), a.eb, a.ee, &cn, tl,
                th))
@@ -1184,21 +1167,9 @@ int walk_block() {
   static const int b = env_int("TWG_WALK_BLOCK", 32);
   return b;
 }
-bool walk_last_t_filter() {
-  static const bool on = env_int("TWG_WALK_LASTT", 0) != 0;
-  return on;
-}
-int walk_min_blocks() {
-  static const int b = env_int("TWG_WALK_MINB", 32);
-  return b;
-}
 bool walk_rec_enabled() {
   static const bool on = env_int("TWG_WALK_REC", 1) != 0;
   return on;
-}
-u64 walk_l2_keep() {
-  static const u64 k = static_cast<u64>(env_int("TWG_WALK_L2KEEP", 0));
-  return k;
 }
 
 WalkParams make_params(Ctx& ctx, Store& s, const twg_walk_config& cfg, u32 stride, u64 walk_begin, WalkSetDev& out,
@@ -1227,8 +1198,6 @@ WalkParams make_params(Ctx& ctx, Store& s, const twg_walk_config& cfg, u32 strid
   P.times = out.times.p;
   P.exp_neg = ctx.d_exp_neg;
   P.expm1_tab = ctx.d_expm1;
-  P.last_t = nullptr;
-  P.l2_keep = 0;
   P.rec = 0;
   return P;
 }
@@ -1493,8 +1462,6 @@ WalkSetDev* generate_walks(Ctx& ctx, Store& s_in, const twg_walk_config& cfg, co
   if (count == 0) {
     // nothing to do
   } else if (variant == TWG_FULLWALK) {
-    if (P.dir == 0 && walk_last_t_filter() && s.last_t.p && s.last_t.n >= s.V) P.last_t = s.last_t.p;
-    P.l2_keep = walk_l2_keep();
     P.rec = walk_rec_enabled() && s.wrec.p && s.wrec.n >= s.V && P.dir == 0 && !P.node2vec &&
             (P.bias == TWG_UNIFORM || P.bias == TWG_LINEAR || P.bias == TWG_EXPINDEX);
     DevBuf<u64> part(kStatSlots * 8, st);
@@ -1502,13 +1469,11 @@ WalkSetDev* generate_walks(Ctx& ctx, Store& s_in, const twg_walk_config& cfg, co
     const int wb = walk_block();
     const unsigned g = static_cast<unsigned>((count + wb - 1) / wb);
     if (P.rec) {
-      const unsigned g32 = static_cast<unsigned>((count + 31) / 32), g64 = static_cast<unsigned>((count + 63) / 64);
-      // 64 registers (1024 resident threads per SM: the 32-block limit with 32-thread blocks, the
-      // register file with 64-thread ones); 40-register builds spill (measured)
-      switch (walk_min_blocks()) {
-        case 16: k_fullwalk<64, true, 16><<<g64, 64, 0, st>>>(P, I, count, out->lengths.p, part.p); break;
-        default: k_fullwalk<32, true><<<g32, 32, 0, st>>>(P, I, count, out->lengths.p, part.p); break;
-      }
+      // 32-thread blocks at 64 registers: 1024 resident threads per SM (the
+      // 32-block limit); 40-register builds spill, 64-thread blocks measured
+      // slower
+      k_fullwalk<32, true><<<static_cast<unsigned>((count + 31) / 32), 32, 0, st>>>(P, I, count, out->lengths.p,
+                                                                                   part.p);
     } else {
       switch (wb) {
         case 32: k_fullwalk<32, false><<<g, 32, 0, st>>>(P, I, count, out->lengths.p, part.p); break;
