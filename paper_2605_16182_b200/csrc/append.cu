@@ -539,6 +539,9 @@ __global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs<PV> a) {
       u32 total;
       sm.off[t] = block_excl_scan<u32>(acc, &total);
       if (t == 0) sm.off[kPB] = total;
+      // a node this batch gives fewer entries than the walk-record tail takes
+      // the rest from the previous record: fetch its line into L2 now
+      if (c0 == bs && valid && a.owrec && c0 + n >= be && acc < kWalkTail) prefetch_l2(a.owrec + v);
     }
     __syncthreads();
 #pragma unroll
