@@ -83,6 +83,7 @@ struct FastSpec {
 constexpr int kStatItems = 8;
 constexpr int kStatTile = kBlock * kStatItems;
 constexpr int kStatSpan = kStatTile + 2 * kSegMax;
+static_assert(kStatSpan % 32 == 0 && kSegMax == 32, "span words and the one-word run-bound search");
 
 bool compact_payload_enabled() {
   static const bool on = [] {
@@ -146,6 +147,7 @@ __global__ void __launch_bounds__(kBlock) k_batch_stats(const i64* bs, const i64
   __shared__ u64 s_prefix;
   __shared__ alignas(8) u64 s_bar;
   __shared__ u32 s_hist[2][kRadix];
+  __shared__ u32 s_start[kStatSpan / 32];  // bit j: an equal-time run starts at span position j
   static_assert(kBlock == kRadix, "one histogram bin per thread");
   const bool fuse_hist = kGroups && hs.rows != nullptr;
   if (fuse_hist) s_hist[0][threadIdx.x] = 0, s_hist[1][threadIdx.x] = 0;  // kBlock == kRadix
@@ -188,15 +190,29 @@ __global__ void __launch_bounds__(kBlock) k_batch_stats(const i64* bs, const i64
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const i64 jn = static_cast<i64>(n) - lo_g;
+  const int jmin = lo_g < 0 ? static_cast<int>(-lo_g) : 0;            // span index of edge 0
+  const int jend = jn < kStatSpan ? static_cast<int>(jn) : kStatSpan;  // of edge n (clamped)
+  // run starts as a bitmask over the span (one ballot per 32 positions);
+  // edge 0 and everything outside [jmin, jend) count as starts, so a run's
+  // bounds never leave the staged edges
+  for (int w0 = warp * 32; w0 < kStatSpan; w0 += kBlock) {
+    const int j = w0 + lane;
+    const bool f = j <= jmin || j >= jend || st_t[j] != st_t[j - 1];
+    const u32 word = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) s_start[w0 >> 5] = word;
+  }
+  __syncthreads();
   u32 gbal[kStatItems];
   if (kGroups) {
-    // group starts first, and the tile's count posted at once: the
-    // successors' look-backs wait on it while this tile ranks its runs
+    // group starts = run starts of the tile's own edges; the tile's count is
+    // posted at once: the successors' look-backs wait on it while this tile
+    // ranks its runs
 #pragma unroll
     for (int k = 0; k < kStatItems; ++k) {
-      const int j = kSegMax + k * kBlock + threadIdx.x;
-      const u64 i = base + k * kBlock + threadIdx.x;
-      gbal[k] = __ballot_sync(0xffffffffu, i < n && (i == 0 || st_t[j] != st_t[j - 1]));
+      const u64 i0 = base + k * kBlock + warp * 32;  // edge of lane 0
+      const u32 valid = i0 >= n ? 0u : (n - i0 >= 32 ? 0xffffffffu : (1u << (n - i0)) - 1u);
+      gbal[k] = s_start[(kSegMax + k * kBlock) / 32 + warp] & valid;
       if (lane == 0) s_cnt[k][warp] = __popc(gbal[k]);
     }
     __syncthreads();
@@ -240,12 +256,26 @@ __global__ void __launch_bounds__(kBlock) k_batch_stats(const i64* bs, const i64
     if (i + 1 < n && t > st_t[j + 1]) shape |= 1u;
     if (i + kSegMax < n && t == st_t[j + kSegMax]) shape |= 2u;
     if (rec) {
-      int lo = j, hi = j + 1;
-      const i64 jn = static_cast<i64>(n) - lo_g;
-      const int jmin = lo_g < 0 ? static_cast<int>(-lo_g) : 0;                 // smem index of edge 0
-      const int jend = jn < kStatSpan ? static_cast<int>(jn) : kStatSpan;       // of edge n (clamped)
-      while (lo > jmin && j - lo < kSegMax && st_t[lo - 1] == t) --lo;
-      while (hi < jend && hi - j < kSegMax && st_t[hi] == t) ++hi;
+      // the run [lo, hi) around j from the start bitmask: the last start at
+      // or before j, the first after it, each within one word either side (a
+      // run longer than kSegMax sets shape bit 1; its records are not used)
+      const int w = j >> 5, b = j & 31;
+      const u32 upto = 0xffffffffu >> (31 - b);  // bits 0..b
+      u32 m = s_start[w] & upto;
+      int lo, hi;
+      if (m) {
+        lo = (w << 5) + 31 - __clz(m);
+      } else {
+        m = s_start[w - 1];
+        lo = m ? ((w - 1) << 5) + 31 - __clz(m) : j - (kSegMax - 1);
+      }
+      m = s_start[w] & ~upto;
+      if (m) {
+        hi = (w << 5) + __ffs(m) - 1;
+      } else {
+        m = w + 1 < kStatSpan / 32 ? s_start[w + 1] : 1u;
+        hi = m ? ((w + 1) << 5) + __ffs(m) - 1 : j + kSegMax;
+      }
       const u32 aj = static_cast<u32>(st_a[j]), bj = static_cast<u32>(st_b[j]);
       const u64 key = (static_cast<u64>(aj) << 32) | bj;
       u32 rank = 0;
