@@ -87,6 +87,20 @@ def test_append_every_batch_bit_exact(tw, co, mode):
     assert n == len(batches) - 1
 
 
+@pytest.mark.parametrize("mode,step", [(2, 200000), (0, 1 << 33)])
+def test_append_two_pass_sort_and_time_span(tw, co, mode, step):
+    """70K nodes (bucket sort over two 8-bit digit passes, the owner-digit
+    histogram fused into the statistics pass), 600K-edge batches (every node
+    present: the fast route; interior statistics tiles staged by TMA bulk
+    copies), and either a batch time span
+    below 2^32 (12-B sort payloads) or of 2^33 (16-B payloads: the time does
+    not fit a u32 offset): the index after every batch and the walks on the
+    last snapshot equal the oracle's."""
+    batches = _ordered_stream(90 + mode, 4, 600000, 70000, step)
+    n = _run(tw, co, batches, 2 * step, mode, check_walks=step < (1 << 32))
+    assert n == len(batches) - 1
+
+
 @pytest.mark.parametrize("mode", [0, 2])
 def test_append_tie_boundary(tw, co, mode):
     """Batch boundaries sharing a timestamp: the first batch group and the
