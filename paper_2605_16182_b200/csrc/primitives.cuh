@@ -24,6 +24,9 @@ constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanBlock * kScanItems;
 
 constexpr int kSortBlock = 256;
+#ifndef TWG_SORT_ITEMS_WIDE
+#define TWG_SORT_ITEMS_WIDE 8  // items per thread of a onesweep tile for pairs wider than 8 B
+#endif
 constexpr int kRadixBits = 8;
 constexpr int kRadix = 1 << kRadixBits;
 
@@ -536,7 +539,7 @@ static __global__ void __launch_bounds__(kRadix) k_radix_digit_starts(u32* hist,
 
 template <class K, class V>
 struct OnesweepSmem {
-  static constexpr int kItems = sizeof(K) + sizeof(V) > 8 ? 8 : 16;
+  static constexpr int kItems = sizeof(K) + sizeof(V) > 8 ? TWG_SORT_ITEMS_WIDE : 16;
   static constexpr int kTile = kSortBlock * kItems;
   u32 wcount[kSortBlock / 32][kRadix];
   u32 tile_start[kRadix + 1];

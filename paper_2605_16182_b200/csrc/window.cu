@@ -196,9 +196,16 @@ __global__ void __launch_bounds__(kBlock) k_batch_stats(const i64* bs, const i64
   // run starts as a bitmask over the span (one ballot per 32 positions);
   // edge 0 and everything outside [jmin, jend) count as starts, so a run's
   // bounds never leave the staged edges
+  // (the same pass flags a descending pair (j-1, j) of this tile's own edges:
+  // the batch is not time-ordered)
   for (int w0 = warp * 32; w0 < kStatSpan; w0 += kBlock) {
     const int j = w0 + lane;
-    const bool f = j <= jmin || j >= jend || st_t[j] != st_t[j - 1];
+    bool f = true;
+    if (j > jmin && j < jend) {
+      const i64 tj = st_t[j], tp = st_t[j - 1];
+      f = tj != tp;
+      if (tj < tp && j > kSegMax && j <= kSegMax + kStatTile) shape |= 1u;
+    }
     const u32 word = __ballot_sync(0xffffffffu, f);
     if (lane == 0) s_start[w0 >> 5] = word;
   }
@@ -253,7 +260,6 @@ __global__ void __launch_bounds__(kBlock) k_batch_stats(const i64* bs, const i64
         }
       }
     }
-    if (i + 1 < n && t > st_t[j + 1]) shape |= 1u;
     if (i + kSegMax < n && t == st_t[j + kSegMax]) shape |= 2u;
     if (rec) {
       // the run [lo, hi) around j from the start bitmask: the last start at
@@ -276,11 +282,15 @@ __global__ void __launch_bounds__(kBlock) k_batch_stats(const i64* bs, const i64
         m = w + 1 < kStatSpan / 32 ? s_start[w + 1] : 1u;
         hi = m ? ((w + 1) << 5) + __ffs(m) - 1 : j + kSegMax;
       }
-      const u32 aj = static_cast<u32>(st_a[j]), bj = static_cast<u32>(st_b[j]);
+      // ids below 2^32 (the fast route's dense population): the low words of
+      // the staged i64 columns (32-bit shared loads, little-endian)
+      const u32* a32 = reinterpret_cast<const u32*>(st_a);
+      const u32* b32 = reinterpret_cast<const u32*>(st_b);
+      const u32 aj = a32[2 * j], bj = b32[2 * j];
       const u64 key = (static_cast<u64>(aj) << 32) | bj;
       u32 rank = 0;
       for (int q = lo; q < hi; ++q) {
-        const u64 kq = (static_cast<u64>(static_cast<u32>(st_a[q])) << 32) | static_cast<u32>(st_b[q]);
+        const u64 kq = (static_cast<u64>(a32[2 * q]) << 32) | b32[2 * q];
         rank += (kq < key || (kq == key && q < j)) ? 1u : 0u;
       }
       rec[wr(static_cast<u32>(lo_g + lo + rank))] = EdgeRec{aj, bj, t};
