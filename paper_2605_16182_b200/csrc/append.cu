@@ -31,11 +31,18 @@ namespace twg {
 
 namespace {
 
+#ifndef TWG_PLACE_CHUNK
+#define TWG_PLACE_CHUNK 2048
+#endif
+#ifndef TWG_PLACE_MINB
+#define TWG_PLACE_MINB 4
+#endif
 constexpr int kBlock = 256;
 constexpr int kPB = 256;           // nodes per bucket = threads per placement CTA
 constexpr u32 kBucketShift = 8;
-constexpr int kChunk = 2048;       // bucket entries staged per placement round
+constexpr int kChunk = TWG_PLACE_CHUNK;  // bucket entries staged per placement round
 constexpr int kChunkItems = kChunk / kPB;
+static_assert(kChunk % kPB == 0, "whole rounds per chunk");
 static_assert(kPB == 1 << kBucketShift, "one thread per bucket node");
 
 unsigned grid(Ctx& ctx, u64 n) { return grid_for(n, kBlock, static_cast<unsigned>(ctx.sm_count) * 16); }
@@ -438,7 +445,8 @@ struct PlaceArgs {
   u64* q_total;
 };
 
-struct PlaceSmem {  // ~55 KB: 4 CTAs per SM (the register budget allows 4 as well)
+template <class PV>
+struct PlaceSmem {  // ~47 KB with 12-B staged payloads, ~55 KB with 16-B ones (kChunk 2048)
   u16 wcnt[kPB / 32][kPB];  // chunk counts fit 16 bits (kChunk <= 65535)
   u32 off[kPB + 1];
   u32 cur[kPB], gcur[kPB], base[kPB], cap[kPB], eorg[kPB], gorg[kPB];
@@ -451,10 +459,10 @@ struct PlaceSmem {  // ~55 KB: 4 CTAs per SM (the register budget allows 4 as we
   u8 snode[kChunk];
   u8 flag[kChunk];
   u16 mscan[kChunk];
-  Entry sent[kChunk];
+  PV sent[kChunk];  // the chunk's payloads in node order, as sorted (expanded to entries on the way out)
 };
 static_assert(kChunk < 65536, "16-bit chunk counters");
-static_assert(sizeof(PlaceSmem) <= 56 * 1024, "placement: 4 CTAs per SM (228 KB of shared memory)");
+static_assert(sizeof(PlaceSmem<Entry>) <= 56 * 1024, "placement: 4 CTAs per SM (228 KB of shared memory)");
 
 // One CTA per bucket of 256 nodes (thread t <-> node (bucket << 8) + t):
 // the bucket's entries in rounds of kChunk: stable rank per node
@@ -463,9 +471,9 @@ static_assert(sizeof(PlaceSmem) <= 56 * 1024, "placement: 4 CTAs per SM (228 KB 
 // written in node order (a node's new entries / marks are contiguous in its
 // ring, so the stores coalesce); finally publish {eb, ee, gb, ge, ring}.
 template <class PV>
-__global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs<PV> a) {
+__global__ void __launch_bounds__(kPB, TWG_PLACE_MINB) k_bucket_place(PlaceArgs<PV> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  PlaceSmem& sm = *reinterpret_cast<PlaceSmem*>(smem_raw);
+  PlaceSmem<PV>& sm = *reinterpret_cast<PlaceSmem<PV>*>(smem_raw);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const u64 bkt = blockIdx.x;
   const u64 v = (bkt << kBucketShift) + t;
@@ -550,7 +558,7 @@ __global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs<PV> a) {
       if (i < n) {
         const u32 nd = dk[r];
         const u32 sp = sm.off[nd] + sm.wcnt[warp][nd] + rank[r];
-        sm.sent[sp] = Payload<PV>::entry(a.vals[c0 + i], a.tb);
+        sm.sent[sp] = a.vals[c0 + i];
         sm.snode[sp] = static_cast<u8>(nd);
       }
     }
@@ -564,9 +572,9 @@ __global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs<PV> a) {
       u32 f = 0;
       if (i < n) {
         const u32 nd = sm.snode[i];
-        const i64 ti = sm.sent[i].t;
+        const i64 ti = Payload<PV>::time(sm.sent[i], a.tb);
         if (i == sm.off[nd]) f = (!sm.has_last[nd] || ti != sm.last_t[nd]) ? 1u : 0u;
-        else f = ti != sm.sent[i - 1].t ? 1u : 0u;
+        else f = ti != Payload<PV>::time(sm.sent[i - 1], a.tb) ? 1u : 0u;
         if (!f) sm.tie[nd] = 1;
       }
       fl[r] = __ballot_sync(0xffffffffu, f != 0);
@@ -611,7 +619,7 @@ __global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs<PV> a) {
       const u32 nd = sm.snode[i];
       const u32 pos = sm.cur[nd] + (i - sm.off[nd]);
       const Ring er{sm.base[nd], sm.cap[nd], sm.eorg[nd]};
-      const Entry e = sm.sent[i];
+      const Entry e = Payload<PV>::entry(sm.sent[i], a.tb);
       a.ent[er(pos)] = e;
       if (sm.flag[i] && sm.expl[nd]) {
         const Ring mr{sm.base[nd], sm.cap[nd], sm.gorg[nd]};
@@ -627,7 +635,7 @@ __global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs<PV> a) {
         const u32 mend = o1 + c < n ? sm.mscan[o1 + c] : sm.mtotal;
         sm.cur[t] += c;
         sm.gcur[t] += mend - sm.mscan[o1];
-        sm.last_t[t] = sm.sent[o1 + c - 1].t;
+        sm.last_t[t] = Payload<PV>::time(sm.sent[o1 + c - 1], a.tb);
         sm.has_last[t] = 1u;
       }
     }
@@ -663,7 +671,7 @@ __global__ void __launch_bounds__(kPB, 4) k_bucket_place(PlaceArgs<PV> a) {
       i64 tj = 0;
       if (i < k) {
         if (i < cl || i < total) {
-          const Entry e = i < cl ? sm.sent[o1 + cl - 1 - i] : a.ent[er(r.ee - 1 - i)];
+          const Entry e = i < cl ? Payload<PV>::entry(sm.sent[o1 + cl - 1 - i], a.tb) : a.ent[er(r.ee - 1 - i)];
           nb = e.nbr;
           tj = e.t;
         } else if (a.owrec) {
@@ -919,9 +927,9 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
     static bool attr_set = false;
     if (!attr_set) {
       TWG_CUDA(cudaFuncSetAttribute(k_bucket_place<Entry>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(sizeof(PlaceSmem))));
+                                    static_cast<int>(sizeof(PlaceSmem<Entry>))));
       TWG_CUDA(cudaFuncSetAttribute(k_bucket_place<PEnt>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(sizeof(PlaceSmem))));
+                                    static_cast<int>(sizeof(PlaceSmem<PEnt>))));
       attr_set = true;
     }
     PlaceArgs<PV> pl;
@@ -940,7 +948,7 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
     pl.owrec = O.wrec.n >= V ? O.wrec.p : nullptr;
     pl.q_total = sc + 7;
     TWG_CUDA(cudaMemsetAsync(sc + 7, 0, sizeof(u64), st));
-    k_bucket_place<PV><<<static_cast<unsigned>(nb), kPB, sizeof(PlaceSmem), st>>>(pl);
+    k_bucket_place<PV><<<static_cast<unsigned>(nb), kPB, sizeof(PlaceSmem<PV>), st>>>(pl);
     TWG_LAUNCHED(ctx);
     pt.mark("place");
     return true;

@@ -80,7 +80,10 @@ struct FastSpec {
 // and at edge 0, since the fast route admits only batches strictly newer
 // than the window — numbered by a decoupled look-back over tiles taken by
 // ticket, written as {start sequence, time} through the log's ts ring.
-constexpr int kStatItems = 8;
+#ifndef TWG_STAT_ITEMS
+#define TWG_STAT_ITEMS 8
+#endif
+constexpr int kStatItems = TWG_STAT_ITEMS;
 constexpr int kStatTile = kBlock * kStatItems;
 constexpr int kStatSpan = kStatTile + 2 * kSegMax;
 static_assert(kStatSpan % 32 == 0 && kSegMax == 32, "span words and the one-word run-bound search");
