@@ -81,7 +81,7 @@ struct FastSpec {
 // than the window — numbered by a decoupled look-back over tiles taken by
 // ticket, written as {start sequence, time} through the log's ts ring.
 #ifndef TWG_STAT_ITEMS
-#define TWG_STAT_ITEMS 8
+#define TWG_STAT_ITEMS 6
 #endif
 constexpr int kStatItems = TWG_STAT_ITEMS;
 constexpr int kStatTile = kBlock * kStatItems;
