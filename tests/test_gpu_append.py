@@ -106,7 +106,8 @@ def test_append_tie_boundary(tw, co, mode):
     """Batch boundaries sharing a timestamp: the first batch group and the
     first batch mark of a node merge with the survivors' last ones."""
     batches = _ordered_stream(7, 10, 2000, 150, 60, tie_boundary=True)
-    n = _run(tw, co, batches, 150, mode)
+    # walks too: a merged boundary group's record (the sampled-start line) is rebuilt
+    n = _run(tw, co, batches, 150, mode, check_walks=True)
     assert n == len(batches) - 1
 
 
