@@ -42,7 +42,7 @@ FACADE_TEST := build/facade_test
 facade_test: $(FACADE_TEST)
 $(FACADE_TEST): tests/cpp/facade_test.cpp $(CXXHDRS) $(LIB)
 	@mkdir -p build
-	g++ -std=c++20 -O2 -Wall -Wextra -Iinclude $< -o $@ -L$(dir $(LIB)) -ltimewalk_b200 -Wl,-rpath,'$$ORIGIN/../$(dir $(LIB))'
+	g++ -std=c++20 -O2 -Wall -Wextra -pthread -Iinclude $< -o $@ -L$(dir $(LIB)) -ltimewalk_b200 -Wl,-rpath,'$$ORIGIN/../$(dir $(LIB))'
 
 # The reference's OWN test suites (proj/tests/test_*.cpp + acceptance.cpp),
 # compiled UNCHANGED from where they lie under /root/reference (needs it at

@@ -72,6 +72,27 @@ twg_ctx* ctx() {
   return c;
 }
 
+// Walk generation runs on the calling thread's own context (stream and
+// scratch): the reference's contract — one ingest in flight while any number
+// of walk generations run over published snapshots (window_manager.hpp:
+// 27-30) — holds without the API lock. Snapshots are immutable once
+// published (the ingest synchronises before publishing; the lazily completed
+// views are built under a per-store lock and published complete), and a
+// snapshot older than the window's retired one that a caller still holds
+// makes the next ingest repack instead of reusing its slots.
+twg_ctx* walk_ctx() {
+  thread_local std::map<int, twg_ctx*> mine;
+  auto it = mine.find(t_device);
+  if (it != mine.end()) return it->second;
+  twg_ctx* c = nullptr;
+  {
+    std::lock_guard<std::recursive_mutex> lk(api_mutex());  // context creation touches device-global state
+    check(twg_ctx_create(t_device, &c));
+  }
+  mine[t_device] = c;  // lives for the process, like the shared context
+  return c;
+}
+
 twg_walk_config to_c(const WalkConfig& c) {
   twg_walk_config w{};
   w.walk_length = c.walk_length;
@@ -423,12 +444,11 @@ WalkSet generate_walks(const EdgeStore& store, const WalkConfig& config, const T
   const auto started = std::chrono::steady_clock::now();
   config.validate();
   thresholds.validate();
-  std::lock_guard<std::recursive_mutex> lk(api_mutex());
   const twg_walk_config c = to_c(config);
   const twg_thresholds th = to_c(thresholds);
   twg_walkset* w = nullptr;
   twg_walk_stats st{};
-  check(twg_generate(ctx(), store.device_handle(), &c, &th, static_cast<int>(variant), &w, &st));
+  check(twg_generate(walk_ctx(), store.device_handle(), &c, &th, static_cast<int>(variant), &w, &st));
   return download_walks(w, st, started, stats);
 }
 

@@ -373,6 +373,7 @@ __global__ void k_ts_wtail(StoreView s, const double* exp_neg, double* tail, u64
 }
 
 void ensure_weights(Ctx& ctx, Store& s) {
+  std::lock_guard<std::mutex> lk(s.lazy_mu);
   if (s.has_weights) return;
   if (s.gapped) {
     cudaStream_t st = ctx.stream;
@@ -401,6 +402,7 @@ void ensure_weights(Ctx& ctx, Store& s) {
     k_node_weights<<<grid(ctx, s.V), kBlock, 0, st>>>(s.view(), ctx.d_exp_neg, s.wp.p);
     TWG_LAUNCHED(ctx);
   }
+  TWG_CUDA(cudaStreamSynchronize(st));  // complete before any other stream may see the flag
   s.has_weights = true;
 }
 
@@ -441,6 +443,7 @@ static void build_adjacency(Ctx& ctx, Store& s, const u32* owners) {
   k_region_bounds_u32<<<grid(ctx, A + 1), kBlock, 0, st>>>(adj_owner.p, A, V, s.adj_off.p);
   TWG_LAUNCHED(ctx);
   s.A = A;
+  TWG_CUDA(cudaStreamSynchronize(st));  // complete before any other stream may see the flag
   s.has_adjacency = true;
 }
 
@@ -620,13 +623,15 @@ Store& ensure_compact(Ctx& ctx, const Store& g) {
   build_nm(ctx, *c);
   c->has_weights = false;
   c->has_adjacency = false;
+  TWG_CUDA(cudaStreamSynchronize(st));  // complete before another context's stream may read it
   g.compact = std::move(c);
   return *g.compact;
 }
 
 void ensure_adjacency(Ctx& ctx, Store& s) {
-  if (s.has_adjacency) return;
   if (s.gapped) return;  // streaming stores answer adjacency from the node view (walk.cu adjacent)
+  std::lock_guard<std::mutex> lk(s.lazy_mu);
+  if (s.has_adjacency) return;
   DevBuf<u32> owners(s.P ? s.P : 1, ctx.stream);
   if (s.P) {
     k_entry_owners<<<grid(ctx, s.V), kBlock, 0, ctx.stream>>>(s.nmeta.p, s.V, owners.p);

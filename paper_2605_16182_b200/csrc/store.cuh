@@ -229,6 +229,10 @@ struct Store {
   // first use by the accessors / downloads / weighted views (ensure_compact)
   mutable std::unique_ptr<Store> compact;
   mutable std::mutex compact_mu;
+  // the lazily completed views (weights, adjacency): built under this lock and
+  // published (flag set) only after their kernels finished, so a walk on
+  // another context's stream never reads a half-built view
+  std::mutex lazy_mu;
 
   StoreView view() const {
     return StoreView{mode,     m,         V,         Z,          P,         Q,        A,

@@ -12,6 +12,7 @@
 #include <numeric>
 #include <set>
 #include <stdexcept>
+#include <thread>
 #include <vector>
 
 #include <sstream>
@@ -643,6 +644,64 @@ void synthetic_cases() {
         }));
 }
 
+// The reference's concurrency contract (window_manager.hpp:27-30): one ingest
+// in flight while walk generations run over published snapshots. Thread A
+// streams batches into the window while thread B repeatedly walks a snapshot
+// it holds; B's walks must equal the single-threaded result, and A's final
+// window must equal a sequential run's.
+static void concurrency_cases() {
+  const CounterRng rng(404);
+  std::vector<std::vector<TemporalEdge>> batches;
+  for (std::uint64_t b = 0; b < 10; ++b) {
+    std::vector<TemporalEdge> e;
+    for (std::uint64_t i = 0; i < 20000; ++i) {
+      e.push_back({static_cast<NodeId>(rng.bits(b, i, 0) % 800), static_cast<NodeId>(rng.bits(b, i, 1) % 800),
+                   static_cast<Timestamp>(b * 1000 + (i * 1000) / 20000)});
+    }
+    batches.push_back(std::move(e));
+  }
+  WindowManager seq({3000, DirectionMode::DirectedForward});
+  for (const auto& b : batches) seq.ingest_batch(b);
+  WalkConfig cfg;
+  cfg.start_mode = StartMode::Sampled;
+  cfg.total_walks = 20000;
+  cfg.walk_length = 20;
+  cfg.bias = BiasKind::ExponentialIndex;
+  cfg.start_bias = BiasKind::UniformIndex;
+  cfg.seed = 11;
+  WindowManager w({3000, DirectionMode::DirectedForward});
+  for (int b = 0; b < 3; ++b) w.ingest_batch(batches[b]);
+  const auto held = w.snapshot();
+  const WalkSet expect_full = generate_walks_fullwalk(*held, cfg);
+  const WalkSet expect_coop = generate_walks(*held, cfg);
+  bool walks_equal = true;
+  std::thread walker([&] {
+    for (int k = 0; k < 6; ++k) {
+      const WalkSet a = generate_walks_fullwalk(*held, cfg);
+      const WalkSet c = generate_walks(*held, cfg);
+      walks_equal = walks_equal && a.nodes == expect_full.nodes && a.times == expect_full.times &&
+                    c.nodes == expect_coop.nodes && c.times == expect_coop.times;
+    }
+  });
+  std::thread ingester([&] {
+    for (std::size_t b = 3; b < batches.size(); ++b) w.ingest_batch(batches[b]);
+  });
+  walker.join();
+  ingester.join();
+  CHECK(walks_equal);
+  CHECK(expect_full.nodes == expect_coop.nodes && expect_full.times == expect_coop.times);
+  const auto a = w.snapshot(), b = seq.snapshot();
+  CHECK(a->edge_count() == b->edge_count() && a->node_count() == b->node_count());
+  bool same = a->edge_count() == b->edge_count();
+  for (std::size_t i = 0; same && i < a->edge_count(); i += 97) {
+    const auto ea = a->edge_at(i), eb = b->edge_at(i);
+    same = ea.source == eb.source && ea.target == eb.target && ea.time == eb.time;
+  }
+  CHECK(same);
+  const WalkSet after_a = generate_walks_fullwalk(*a, cfg), after_b = generate_walks_fullwalk(*b, cfg);
+  CHECK(after_a.nodes == after_b.nodes && after_a.times == after_b.times);
+}
+
 int main() {
   edge_store_cases();
   window_cases();
@@ -654,6 +713,7 @@ int main() {
   io_cases();
   validity_cases();
   synthetic_cases();
+  concurrency_cases();
   std::printf("%d/%d checks passed\n", g_checks - g_fail, g_checks);
   return g_fail;
 }
