@@ -4,6 +4,15 @@
 // stream — stream order makes the reuse safe without events. On an
 // allocation failure every cached block of every class is released and the
 // request retried once.
+//
+// TWG_GUARD=1 (a debug mode for the guard test, tests/test_gpu_sanitizer.py):
+// every block is poisoned (0xA5) when handed out, so a read of memory no
+// kernel wrote changes results, and carries a 4 KiB guard past the requested
+// bytes that is checked when the block is freed (a synchronous read-back), so
+// a write past the end of an allocation is reported on stderr.
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <map>
 #include <mutex>
 #include <unordered_map>
@@ -20,7 +29,18 @@ struct Arena {
   std::unordered_map<void*, size_t> owned;  // live block -> its class
   size_t in_use = 0;
   size_t reserved = 0;
+  std::unordered_map<void*, size_t> asked;  // TWG_GUARD: live block -> requested bytes
 };
+
+constexpr size_t kGuardBytes = 4096;
+constexpr unsigned char kPoison = 0xA5;
+size_t guard_bytes() {
+  static const size_t g = [] {
+    const char* e = std::getenv("TWG_GUARD");
+    return (e && *e && *e != '0') ? kGuardBytes : size_t(0);
+  }();
+  return g;
+}
 
 std::mutex g_mu;
 std::unordered_map<cudaStream_t, Arena*>& arenas() {
@@ -63,10 +83,20 @@ void arena_unregister(cudaStream_t s) {
   delete a;
 }
 
+namespace {
+void* guarded(Arena* a, cudaStream_t s, void* p, size_t bytes) {
+  if (a && guard_bytes()) {
+    a->asked[p] = bytes;
+    cuda_check(cudaMemsetAsync(p, kPoison, bytes + guard_bytes(), s), "TWG_GUARD poison", __FILE__, __LINE__);
+  }
+  return p;
+}
+}  // namespace
+
 void* arena_alloc(cudaStream_t s, size_t bytes) {
   std::lock_guard<std::mutex> lk(g_mu);
   Arena* a = find(s);
-  const size_t c = size_class(bytes);
+  const size_t c = size_class(bytes + guard_bytes());
   if (a) {
     // smallest cached block of class in [c, 2c): batch-to-batch size jitter
     // (a few more nodes or groups) must not trigger a fresh cudaMalloc,
@@ -77,7 +107,7 @@ void* arena_alloc(cudaStream_t s, size_t bytes) {
         it->second.pop_back();
         a->in_use += it->first;
         a->owned[p] = it->first;
-        return p;
+        return guarded(a, s, p, bytes);
       }
     }
   }
@@ -101,7 +131,7 @@ void* arena_alloc(cudaStream_t s, size_t bytes) {
     a->reserved += c;
     a->owned[p] = c;
   }
-  return p;
+  return guarded(a, s, p, bytes);
 }
 
 void arena_free(cudaStream_t s, void* p, size_t bytes) {
@@ -110,6 +140,19 @@ void arena_free(cudaStream_t s, void* p, size_t bytes) {
   if (!a) {  // ctx already gone: release for real
     cudaFree(p);
     return;
+  }
+  if (auto g = a->asked.find(p); g != a->asked.end()) {  // TWG_GUARD: the block's tail guard intact?
+    std::vector<unsigned char> tail(guard_bytes());
+    cudaMemcpyAsync(tail.data(), static_cast<char*>(p) + g->second, tail.size(), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    for (size_t i = 0; i < tail.size(); ++i) {
+      if (tail[i] != kPoison) {
+        std::fprintf(stderr, "TWG_GUARD: write past the end of a %zu-byte block (byte +%zu of its guard)\n",
+                     g->second, i);
+        break;
+      }
+    }
+    a->asked.erase(g);
   }
   auto it = a->owned.find(p);
   const size_t c = it != a->owned.end() ? it->second : size_class(bytes);

@@ -6,7 +6,13 @@ node2vec) plus the auditor and the walk writers. No torch: only the C ABI
 through the package's ctypes mirror, so the sanitizer sees our kernels alone.
 
 usage: compute-sanitizer --tool memcheck python tools/sanitize_workload.py
+       TWG_GUARD=1 python tools/sanitize_workload.py   (poisoned blocks + tail guards)
+
+Prints a digest of every walk set it downloads, so a poisoned run (TWG_GUARD=1:
+fresh device blocks filled with 0xA5) can be compared with a plain one.
 """
+import gc
+import hashlib
 import os
 import sys
 
@@ -33,6 +39,12 @@ def stream(seed, nb, n, nodes, step, tie_boundary=False):
 
 
 def main():
+    h = hashlib.sha256()
+
+    def take(ws):
+        for a in (ws.nodes, ws.times, ws.lengths):
+            h.update(memoryview(a).cast("B"))
+
     for mode in (0, 1, 2):
         w = tw.WindowManager(250, tw.DirectionMode(mode))
         for b in stream(40 + mode, 10, 1500, 120, 100, tie_boundary=mode == 2):
@@ -46,19 +58,24 @@ def main():
                     cfg = tw.WalkConfig(walk_length=12, start_mode=tw.StartMode.Sampled, total_walks=600, bias=bias,
                                         start_bias=bias, direction=tw.WalkDirection(d), seed=3)
                     ws = tw.generate_walks(snap, cfg, variant=variant)
-                    ws.nodes  # download
+                    take(ws)
             cfg = tw.WalkConfig(walk_length=10, start_mode=tw.StartMode.PerNode, walks_per_node=2,
                                 bias=tw.BiasKind.ExponentialWeight, direction=tw.WalkDirection(d), seed=5,
                                 node2vec=tw.Node2VecParams(0.5, 2.0))
             ws = tw.generate_walks(snap, cfg)
-            ws.audit(snap, direction=tw.WalkDirection(d))
+            take(ws)
+            h.update(repr(ws.audit(snap, direction=tw.WalkDirection(d))).encode())
     # general route (unordered batch) + EdgeStore::build + hub tiers
     g = tw.synth_graph("hub_skewed", 2000, 20000, seed=0)
     st = tw.EdgeStore.build(g)
     ws = tw.generate_walks(st, tw.WalkConfig())
-    ws.nodes
+    take(ws)
     w = tw.WindowManager(10 ** 9)
     w.ingest_batch(g[::-1].copy())
+    take(tw.generate_walks(w.snapshot(), tw.WalkConfig(seed=9)))
+    del w, ws, st, snap
+    gc.collect()  # device blocks freed (and, under TWG_GUARD, their guards checked) before the digest
+    print("digest", h.hexdigest())
     print("sanitize workload ok")
 
 
