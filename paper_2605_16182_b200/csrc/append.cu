@@ -217,6 +217,25 @@ struct OwnerIn {
     if (mode == TWG_UNDIRECTED) return static_cast<u32>((j & 1) ? bd[j >> 1] : bs[j >> 1]);
     return static_cast<u32>(mode == TWG_BACKWARD ? bd[j] : bs[j]);
   }
+  // (directed modes, one entry per edge; one warp) the first pass's tile
+  // offsets come from the statistics pass's per-tile counts in INPUT order;
+  // the log holds the CANONICAL order, which permutes edges only inside
+  // equal-time runs of <= kSegMax edges (the fast route's admission). Below
+  // `base` the two orders differ only in the run straddling it, [rs, base):
+  // corr[d] += its canonical entries' digits - its input entries' digits.
+  __device__ __forceinline__ void run_fix(u64 base, int shift, int* corr) const {
+    if (base == 0) return;
+    const int lane = threadIdx.x & 31;
+    const i64 tb = rec[br(static_cast<u32>(base))].t;
+    const i64 q = static_cast<i64>(base) - 32 + lane;
+    if (q < 0) return;
+    const Rec r = rec[br(static_cast<u32>(q))];
+    if (r.t != tb) return;  // times ascend: the lanes left are the run's part below base
+    const u32 oc = mode == TWG_BACKWARD ? r.dst : r.src;
+    const u32 oi = static_cast<u32>(mode == TWG_BACKWARD ? bd[q] : bs[q]);
+    atomicAdd(&corr[(oc >> shift) & (kRadix - 1)], 1);
+    atomicAdd(&corr[(oi >> shift) & (kRadix - 1)], -1);
+  }
 };
 
 // bucket b = owner >> 8 of the bucket-sorted entries starts at bstart[b]
@@ -736,7 +755,7 @@ bool append_log_slot(const Store& O, const Store* R, u64 A, Ring* wr) {
 Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const EdgeRec* batch, Ring bring, u64 A,
                      u64 from, i64 cutoff, bool no_ties, bool in_log, bool check_dead, const i64* bt,
                      const i64* const* bcols, const u64* groups_done, i64 tbase, bool compact,
-                     const i64* old_last, u32* pre_hist) {
+                     const i64* old_last, u32* pre_hist, const u32* pre_rows) {
   Ctx& ctx = *w.ctx;
   cudaStream_t st = ctx.stream;
   PhaseTimer pt(ctx, "ingest_append");
@@ -826,7 +845,8 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
       OwnerIn<PV> oin{brec, wr, mode, seq_b, tbase};
       oin.bs = bcols ? bcols[0] : nullptr;
       oin.bd = bcols ? bcols[1] : nullptr;
-      radix_sort_pairs_from<u32, PV>(ctx, oin, &kp, &ka, &vp, &va, Yn, vb, kBucketShift, pre_hist);
+      radix_sort_pairs_from<u32, PV>(ctx, oin, &kp, &ka, &vp, &va, Yn, vb, kBucketShift, pre_hist,
+                                     (mode != TWG_UNDIRECTED && oin.bs) ? pre_rows : nullptr);
     } else {
       k_owner_keys<PV><<<grid(ctx, Yn), kBlock, 0, st>>>(brec, wr, A, mode, seq_b, tbase, kp, vp);
       TWG_LAUNCHED(ctx);

@@ -249,6 +249,7 @@ struct ArrayIn {
     if (v) prefetch_l2(v + i);
   }
   __device__ __forceinline__ K hist_key(u64 i) const { return k[i]; }
+  __device__ __forceinline__ void run_fix(u64, int, int*) const {}  // input order is the sort's order
 };
 
 // ---------------------------------------------------- single-pass scan ----
@@ -537,9 +538,9 @@ static __global__ void __launch_bounds__(kRadix) k_radix_digit_starts(u32* hist,
   }
 }
 
-template <class K, class V>
+template <class K, class V, int Items = 0>
 struct OnesweepSmem {
-  static constexpr int kItems = sizeof(K) + sizeof(V) > 8 ? TWG_SORT_ITEMS_WIDE : 16;
+  static constexpr int kItems = Items ? Items : (sizeof(K) + sizeof(V) > 8 ? TWG_SORT_ITEMS_WIDE : 16);
   static constexpr int kTile = kSortBlock * kItems;
   u32 wcount[kSortBlock / 32][kRadix];
   u32 tile_start[kRadix + 1];
@@ -549,21 +550,35 @@ struct OnesweepSmem {
   V vals[kTile];
 };
 
-template <class K, class V, class In>
+// kPre (the first pass of the streaming bucket sort): the tile's digit
+// offsets are known up front — pre_rows[tile * 512 + d] is the exclusive
+// prefix over the preceding tiles of the statistics pass's per-tile digit
+// counts (input order, tiles of the same size), corrected by the input's
+// run_fix for the one equal-time run the canonical order may permute across
+// the tile's start — so the pass has no look-back and no ticket.
+template <class K, class V, class In, int Items = 0, bool kPre = false>
 __global__ void __launch_bounds__(kSortBlock) k_radix_onesweep(In in, K* __restrict__ keys_out,
                                                                V* __restrict__ vals_out, u64 n, int shift,
                                                                const u32* __restrict__ digit_start, u64* state,
-                                                               u32* ticket) {
-  using S = OnesweepSmem<K, V>;
+                                                               u32* ticket, const u32* __restrict__ pre_rows = nullptr) {
+  using S = OnesweepSmem<K, V, Items>;
   constexpr int kItems = S::kItems, kTile = S::kTile, kWarps = kSortBlock / 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   S& sm = *reinterpret_cast<S*>(smem_raw);
   const bool has_val = in.has_val();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const u32 lt = (1u << lane) - 1u;
-  if (threadIdx.x == 0) sm.tile = atomicAdd(ticket, 1u);
+  if (kPre) {
+    if (threadIdx.x == 0) sm.tile = blockIdx.x;
+    reinterpret_cast<int*>(sm.gstart)[threadIdx.x] = 0;  // run_fix's per-digit corrections
+  } else if (threadIdx.x == 0) {
+    sm.tile = atomicAdd(ticket, 1u);
+  }
   for (int b = threadIdx.x; b < kWarps * kRadix; b += kSortBlock) (&sm.wcount[0][0])[b] = 0;
   __syncthreads();
+  if constexpr (kPre) {
+    if (warp == 0) in.run_fix(static_cast<u64>(blockIdx.x) * kTile, shift, reinterpret_cast<int*>(sm.gstart));
+  }
   const u64 tile = sm.tile;
   const u64 base = tile * kTile;
   const u32 tile_n = static_cast<u32>(n - base < static_cast<u64>(kTile) ? n - base : kTile);
@@ -606,7 +621,7 @@ __global__ void __launch_bounds__(kSortBlock) k_radix_onesweep(In in, K* __restr
     sm.wcount[w][d] = acc;
     acc += c;
   }
-  lb_store(state + tile * kRadix + d, (tile == 0 ? kLbInclusive : kLbAggregate) | acc);
+  if (!kPre) lb_store(state + tile * kRadix + d, (tile == 0 ? kLbInclusive : kLbAggregate) | acc);
   {
     u32 total;
     sm.tile_start[d] = block_excl_scan<u32>(acc, &total);
@@ -622,7 +637,11 @@ __global__ void __launch_bounds__(kSortBlock) k_radix_onesweep(In in, K* __restr
       if (has_val) sm.vals[pos] = in.val(base + i);
     }
   }
-  {
+  if (kPre) {
+    const int fix = reinterpret_cast<const int*>(sm.gstart)[d];  // read before gstart is overwritten
+    __syncthreads();
+    sm.gstart[d] = digit_start[d] + static_cast<u64>(static_cast<i64>(pre_rows[tile * 512 + d]) + fix);
+  } else {
     u64 excl = 0;
     if (tile > 0) {
       // four predecessors per round: their words are requested together
@@ -665,9 +684,14 @@ __global__ void __launch_bounds__(kSortBlock) k_radix_onesweep(In in, K* __restr
 // pre_hist (device, passes x 256 digit counts of the items): computed by the
 // caller (the statistics pass fuses the owner-digit histogram), so the
 // histogram kernel is skipped; it is consumed (turned into digit starts).
+// pre_rows (with pre_hist; the first pass reading through `in0`): per
+// statistics tile of kPreItems * kSortBlock items, the exclusive prefix of the
+// first digit's counts (k_rows_prefix) — that pass runs without look-back.
+constexpr int kPreItems = 6;  // = the statistics pass's edges per thread (window.cu kStatItems)
+
 template <class K, class V, class In>
 void radix_sort_impl(Ctx& ctx, In in0, bool from_in, K** keys, K** keys_alt, V** vals, V** vals_alt, u64 n,
-                     int bits, int lo_bit, u32* pre_hist = nullptr) {
+                     int bits, int lo_bit, u32* pre_hist = nullptr, const u32* pre_rows = nullptr) {
   using S = OnesweepSmem<K, V>;
   cudaStream_t st = ctx.stream;
   const int passes = (bits - lo_bit + kRadixBits - 1) / kRadixBits;
@@ -682,6 +706,15 @@ void radix_sort_impl(Ctx& ctx, In in0, bool from_in, K** keys, K** keys_alt, V**
     return true;
   }();
   (void)attr;
+  using SP = OnesweepSmem<K, V, kPreItems>;
+  if (pre_rows) {
+    static const bool attr_pre = [] {
+      TWG_CUDA(cudaFuncSetAttribute(k_radix_onesweep<K, V, In, kPreItems, true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(SP))));
+      return true;
+    }();
+    (void)attr_pre;
+  }
   DevBuf<u32> own_hist;
   DevBuf<u64> state(tiles * kRadix + 1, st);  // + the ticket word
   u32* hist = pre_hist;
@@ -701,7 +734,11 @@ void radix_sort_impl(Ctx& ctx, In in0, bool from_in, K** keys, K** keys_alt, V**
   for (int p = 0; p < passes; ++p) {
     const int shift = lo_bit + p * kRadixBits;
     TWG_CUDA(cudaMemsetAsync(state.p, 0, state.bytes(), st));
-    if (p == 0 && from_in) {
+    if (p == 0 && from_in && pre_rows) {
+      k_radix_onesweep<K, V, In, kPreItems, true>
+          <<<static_cast<unsigned>((n + SP::kTile - 1) / SP::kTile), kSortBlock, sizeof(SP), st>>>(
+              in0, *keys, *vals, n, shift, hist + p * kRadix, state.p, ticket, pre_rows);
+    } else if (p == 0 && from_in) {
       k_radix_onesweep<K, V, In><<<static_cast<unsigned>(tiles), kSortBlock, sizeof(S), st>>>(
           in0, *keys, *vals, n, shift, hist + p * kRadix, state.p, ticket);
     } else {
@@ -727,18 +764,36 @@ void radix_sort_pairs(Ctx& ctx, K** keys, K** keys_alt, V** vals, V** vals_alt, 
 // (*keys, *vals); n >= 1).
 template <class K, class V, class In>
 void radix_sort_pairs_from(Ctx& ctx, In in, K** keys, K** keys_alt, V** vals, V** vals_alt, u64 n, int bits,
-                           int lo_bit, u32* pre_hist = nullptr) {
+                           int lo_bit, u32* pre_hist = nullptr, const u32* pre_rows = nullptr) {
   radix_sort_impl<K, V>(ctx, in, true, keys, keys_alt, vals, vals_alt, n, bits > lo_bit ? bits : lo_bit + 1, lo_bit,
-                        pre_hist);
+                        pre_hist, pre_hist ? pre_rows : nullptr);
 }
 
 // Per-tile digit-count rows (rows x 2*256, the statistics pass's output)
 // summed into hist (zeroed) — the fused owner-digit histogram's reduction.
-static __global__ void __launch_bounds__(512) k_hist_rows(const u32* rows, u64 nrows, u64 rows_per_block, u32* hist) {
+// csum (optional): each block's column sums, for k_rows_prefix.
+static __global__ void __launch_bounds__(512) k_hist_rows(const u32* rows, u64 nrows, u64 rows_per_block, u32* hist,
+                                                          u32* csum = nullptr) {
   const u64 r0 = blockIdx.x * rows_per_block, r1 = min(nrows, r0 + rows_per_block);
   u32 acc = 0;
   for (u64 r = r0; r < r1; ++r) acc += rows[r * 512 + threadIdx.x];
   if (acc) atomicAdd(&hist[threadIdx.x], acc);
+  if (csum) csum[blockIdx.x * 512ull + threadIdx.x] = acc;
+}
+
+// The first digit's half of every row (columns 0-255) replaced in place by its
+// exclusive prefix over the preceding rows: block c adds the column sums of
+// blocks < c (k_hist_rows' csum, same rows_per_block), then walks its rows.
+static __global__ void __launch_bounds__(256) k_rows_prefix(u32* rows, u64 nrows, u64 rows_per_block,
+                                                            const u32* csum) {
+  u32 pre = 0;
+  for (u64 c = 0; c < blockIdx.x; ++c) pre += csum[c * 512 + threadIdx.x];
+  const u64 r0 = blockIdx.x * rows_per_block, r1 = min(nrows, r0 + rows_per_block);
+  for (u64 r = r0; r < r1; ++r) {
+    const u32 v = rows[r * 512 + threadIdx.x];
+    rows[r * 512 + threadIdx.x] = pre;
+    pre += v;
+  }
 }
 
 }  // namespace twg

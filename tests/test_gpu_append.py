@@ -101,6 +101,30 @@ def test_append_two_pass_sort_and_time_span(tw, co, mode, step):
     assert n == len(batches) - 1
 
 
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_append_shuffled_ties_across_sort_tiles(tw, co, mode):
+    """Time-ordered batches whose equal-time runs (about 6 edges, up to ~25)
+    arrive in random order: the statistics pass writes them to the log in
+    canonical (src, dst) order, so around every 1536-edge tile boundary a run
+    straddles, the input order (the statistics pass's per-tile owner-digit
+    counts) and the canonical order (the first bucket-sort pass's items)
+    disagree — the first pass's precomputed tile offsets must be corrected for
+    exactly that run (OwnerIn::run_fix). 70K nodes (two digit passes),
+    600K-edge batches on the fast route; the index after every batch and the
+    walks on the last snapshot equal the oracle's."""
+    rs = np.random.default_rng(77 + mode)
+    batches = []
+    for b in range(4):
+        n, nodes, step = 600000, 70000, 100000
+        t = np.sort(b * step + rs.integers(0, step, n))
+        s = rs.integers(0, nodes, n)
+        d = np.minimum((nodes * rs.random(n) ** 2).astype(np.int64), nodes - 1)
+        e = np.stack([s, d, t], 1)
+        batches.append(e[np.lexsort((rs.random(n), e[:, 2]))])  # time order, runs shuffled
+    n = _run(tw, co, batches, 2 * 100000, mode, check_walks=mode != 2)
+    assert n == len(batches) - 1
+
+
 @pytest.mark.parametrize("mode", [0, 2])
 def test_append_tie_boundary(tw, co, mode):
     """Batch boundaries sharing a timestamp: the first batch group and the
