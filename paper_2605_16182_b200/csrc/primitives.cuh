@@ -687,7 +687,10 @@ __global__ void __launch_bounds__(kSortBlock) k_radix_onesweep(In in, K* __restr
 // pre_rows (with pre_hist; the first pass reading through `in0`): per
 // statistics tile of kPreItems * kSortBlock items, the exclusive prefix of the
 // first digit's counts (k_rows_prefix) — that pass runs without look-back.
-constexpr int kPreItems = 6;  // = the statistics pass's edges per thread (window.cu kStatItems)
+#ifndef TWG_STAT_ITEMS
+#define TWG_STAT_ITEMS 6  // the statistics pass's edges per thread (window.cu kStatItems)
+#endif
+constexpr int kPreItems = TWG_STAT_ITEMS;
 
 template <class K, class V, class In>
 void radix_sort_impl(Ctx& ctx, In in0, bool from_in, K** keys, K** keys_alt, V** vals, V** vals_alt, u64 n,
