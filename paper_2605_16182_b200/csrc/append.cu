@@ -208,6 +208,18 @@ struct OwnerIn {
   }
   __device__ __forceinline__ bool has_val() const { return true; }
   __device__ __forceinline__ void prefetch_val(u64) const {}  // the key's record load brings it
+  // the record itself held from the key load to the payload (kPre pass)
+  using Item = Rec;
+  __device__ __forceinline__ Rec item(u64 j) const {
+    return rec[br(mode == TWG_UNDIRECTED ? static_cast<u32>(j >> 1) : static_cast<u32>(j))];
+  }
+  __device__ __forceinline__ u32 key_of(const Rec& r, u64 j) const {
+    return mode == TWG_UNDIRECTED ? ((j & 1) ? r.dst : r.src) : (mode == TWG_BACKWARD ? r.dst : r.src);
+  }
+  __device__ __forceinline__ V val_of(const Rec& r, u64 j) const {
+    const u32 k = mode == TWG_UNDIRECTED ? static_cast<u32>(j >> 1) : static_cast<u32>(j);
+    return Payload<V>::make(nbr_of(mode, r, static_cast<u32>(j)), seq_b + k, r.t, tb);
+  }
   // the same multiset of keys from the batch's own id columns (input order,
   // 8 B per item instead of a 16-B record) when they are at hand
   const i64* bs = nullptr;
@@ -755,7 +767,7 @@ bool append_log_slot(const Store& O, const Store* R, u64 A, Ring* wr) {
 Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const EdgeRec* batch, Ring bring, u64 A,
                      u64 from, i64 cutoff, bool no_ties, bool in_log, bool check_dead, const i64* bt,
                      const i64* const* bcols, const u64* groups_done, i64 tbase, bool compact,
-                     const i64* old_last, u32* pre_hist, const u32* pre_rows) {
+                     const i64* old_last, u32* pre_hist, const u32* pre_rows, const u32* stat_rows) {
   Ctx& ctx = *w.ctx;
   cudaStream_t st = ctx.stream;
   PhaseTimer pt(ctx, "ingest_append");
@@ -846,7 +858,7 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
       oin.bs = bcols ? bcols[0] : nullptr;
       oin.bd = bcols ? bcols[1] : nullptr;
       radix_sort_pairs_from<u32, PV>(ctx, oin, &kp, &ka, &vp, &va, Yn, vb, kBucketShift, pre_hist,
-                                     (mode != TWG_UNDIRECTED && oin.bs) ? pre_rows : nullptr);
+                                     pre_rows, (mode != TWG_UNDIRECTED && oin.bs) ? stat_rows : nullptr);
     } else {
       k_owner_keys<PV><<<grid(ctx, Yn), kBlock, 0, st>>>(brec, wr, A, mode, seq_b, tbase, kp, vp);
       TWG_LAUNCHED(ctx);

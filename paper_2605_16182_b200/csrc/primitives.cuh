@@ -250,6 +250,10 @@ struct ArrayIn {
   }
   __device__ __forceinline__ K hist_key(u64 i) const { return k[i]; }
   __device__ __forceinline__ void run_fix(u64, int, int*) const {}  // input order is the sort's order
+  using Item = K;  // (the kPre pass's register-held items; not used with ArrayIn)
+  __device__ __forceinline__ K item(u64 i) const { return k[i]; }
+  __device__ __forceinline__ K key_of(K x, u64) const { return x; }
+  __device__ __forceinline__ V val_of(K, u64 i) const { return v[i]; }
 };
 
 // ---------------------------------------------------- single-pass scan ----
@@ -538,6 +542,16 @@ static __global__ void __launch_bounds__(kRadix) k_radix_digit_starts(u32* hist,
   }
 }
 
+#ifndef TWG_SORT_HOLD
+#define TWG_SORT_HOLD 1
+#endif
+constexpr bool kSortHold = TWG_SORT_HOLD != 0;
+#ifndef TWG_STAT_ITEMS
+#define TWG_STAT_ITEMS 6  // the statistics pass's edges per thread (window.cu kStatItems)
+#endif
+constexpr int kPreItems = TWG_STAT_ITEMS;
+constexpr u32 kPreRowsPerBlock = 8;  // statistics rows per k_hist_rows block when the prefixes are wanted
+
 template <class K, class V, int Items = 0>
 struct OnesweepSmem {
   static constexpr int kItems = Items ? Items : (sizeof(K) + sizeof(V) > 8 ? TWG_SORT_ITEMS_WIDE : 16);
@@ -551,16 +565,18 @@ struct OnesweepSmem {
 };
 
 // kPre (the first pass of the streaming bucket sort): the tile's digit
-// offsets are known up front — pre_rows[tile * 512 + d] is the exclusive
-// prefix over the preceding tiles of the statistics pass's per-tile digit
-// counts (input order, tiles of the same size), corrected by the input's
-// run_fix for the one equal-time run the canonical order may permute across
-// the tile's start — so the pass has no look-back and no ticket.
+// offsets are known up front — the exclusive prefix over the preceding tiles
+// of the statistics pass's per-tile digit counts (input order, tiles of the
+// same size: pre_rows[tile's k_hist_rows block] + stat_rows of the block's
+// earlier tiles), corrected by the input's run_fix for the one equal-time run
+// the canonical order may permute across the tile's start — so the pass has
+// no look-back and no ticket.
 template <class K, class V, class In, int Items = 0, bool kPre = false>
 __global__ void __launch_bounds__(kSortBlock) k_radix_onesweep(In in, K* __restrict__ keys_out,
                                                                V* __restrict__ vals_out, u64 n, int shift,
                                                                const u32* __restrict__ digit_start, u64* state,
-                                                               u32* ticket, const u32* __restrict__ pre_rows = nullptr) {
+                                                               u32* ticket, const u32* __restrict__ pre_rows = nullptr,
+                                                               const u32* __restrict__ stat_rows = nullptr) {
   using S = OnesweepSmem<K, V, Items>;
   constexpr int kItems = S::kItems, kTile = S::kTile, kWarps = kSortBlock / 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -587,15 +603,44 @@ __global__ void __launch_bounds__(kSortBlock) k_radix_onesweep(In in, K* __restr
   const u32 wbase = static_cast<u32>(warp) * (32 * kItems);
   K key[kItems];
   u32 rank[kItems];
+  // kPre && TWG_SORT_HOLD: the input's whole item (OwnerIn: the 16-B log
+  // record) stays in registers from the key load to the staging store
+  [[maybe_unused]] typename In::Item held[(kPre && kSortHold) ? kItems : 1];
+  if constexpr (kPre && kSortHold) {
 #pragma unroll
-  for (int j = 0; j < kItems; ++j) {  // the payloads' DRAM fetch starts now, into L2
-    const u32 i = wbase + j * 32 + lane;
-    if (i < tile_n) in.prefetch_val(base + i);
+    for (int j = 0; j < kItems; ++j) {
+      const u32 i = wbase + j * 32 + lane;
+      if (i < tile_n) {
+        held[j] = in.item(base + i);
+        key[j] = in.key_of(held[j], base + i);
+      } else {
+        key[j] = K(0);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {  // the payloads' DRAM fetch starts now, into L2
+      const u32 i = wbase + j * 32 + lane;
+      if (i < tile_n) in.prefetch_val(base + i);
+    }
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+      const u32 i = wbase + j * 32 + lane;
+      key[j] = i < tile_n ? in.key(base + i) : K(0);
+    }
   }
+  // kPre: this tile's digit-d offset = the prefix of its k_hist_rows block
+  // (pre_rows = csum after k_csum_scan) + the statistics rows of the block's
+  // tiles before it (< kPreRowsPerBlock loads in flight with the key loads)
+  [[maybe_unused]] u32 pre_base = 0, pre_sum = 0;
+  if constexpr (kPre) {
+    const u64 blk = tile / kPreRowsPerBlock;
+    pre_base = pre_rows[blk * 512 + threadIdx.x];
 #pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    const u32 i = wbase + j * 32 + lane;
-    key[j] = i < tile_n ? in.key(base + i) : K(0);
+    for (u32 k = 0; k < kPreRowsPerBlock - 1; ++k) {
+      const u64 r = blk * kPreRowsPerBlock + k;
+      if (r < tile) pre_sum += stat_rows[r * 512 + threadIdx.x];
+    }
   }
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
@@ -634,13 +679,14 @@ __global__ void __launch_bounds__(kSortBlock) k_radix_onesweep(In in, K* __restr
       const u32 dg = digit_of(key[j], shift);
       const u32 pos = sm.tile_start[dg] + sm.wcount[warp][dg] + rank[j];
       sm.keys[pos] = key[j];
-      if (has_val) sm.vals[pos] = in.val(base + i);
+      if constexpr (kPre && kSortHold) sm.vals[pos] = in.val_of(held[j], base + i);
+      else if (has_val) sm.vals[pos] = in.val(base + i);
     }
   }
   if (kPre) {
     const int fix = reinterpret_cast<const int*>(sm.gstart)[d];  // read before gstart is overwritten
     __syncthreads();
-    sm.gstart[d] = digit_start[d] + static_cast<u64>(static_cast<i64>(pre_rows[tile * 512 + d]) + fix);
+    sm.gstart[d] = digit_start[d] + static_cast<u64>(static_cast<i64>(pre_base + pre_sum) + fix);
   } else {
     u64 excl = 0;
     if (tile > 0) {
@@ -684,17 +730,15 @@ __global__ void __launch_bounds__(kSortBlock) k_radix_onesweep(In in, K* __restr
 // pre_hist (device, passes x 256 digit counts of the items): computed by the
 // caller (the statistics pass fuses the owner-digit histogram), so the
 // histogram kernel is skipped; it is consumed (turned into digit starts).
-// pre_rows (with pre_hist; the first pass reading through `in0`): per
-// statistics tile of kPreItems * kSortBlock items, the exclusive prefix of the
-// first digit's counts (k_rows_prefix) — that pass runs without look-back.
-#ifndef TWG_STAT_ITEMS
-#define TWG_STAT_ITEMS 6  // the statistics pass's edges per thread (window.cu kStatItems)
-#endif
-constexpr int kPreItems = TWG_STAT_ITEMS;
+// pre_rows + stat_rows (with pre_hist; the first pass reading through `in0`):
+// the statistics pass's per-tile digit rows (tiles of kPreItems * kSortBlock
+// items) and the exclusive prefixes of their k_hist_rows block sums
+// (k_csum_scan) — that pass runs without look-back.
 
 template <class K, class V, class In>
 void radix_sort_impl(Ctx& ctx, In in0, bool from_in, K** keys, K** keys_alt, V** vals, V** vals_alt, u64 n,
-                     int bits, int lo_bit, u32* pre_hist = nullptr, const u32* pre_rows = nullptr) {
+                     int bits, int lo_bit, u32* pre_hist = nullptr, const u32* pre_rows = nullptr,
+                     const u32* stat_rows = nullptr) {
   using S = OnesweepSmem<K, V>;
   cudaStream_t st = ctx.stream;
   const int passes = (bits - lo_bit + kRadixBits - 1) / kRadixBits;
@@ -740,7 +784,7 @@ void radix_sort_impl(Ctx& ctx, In in0, bool from_in, K** keys, K** keys_alt, V**
     if (p == 0 && from_in && pre_rows) {
       k_radix_onesweep<K, V, In, kPreItems, true>
           <<<static_cast<unsigned>((n + SP::kTile - 1) / SP::kTile), kSortBlock, sizeof(SP), st>>>(
-              in0, *keys, *vals, n, shift, hist + p * kRadix, state.p, ticket, pre_rows);
+              in0, *keys, *vals, n, shift, hist + p * kRadix, state.p, ticket, pre_rows, stat_rows);
     } else if (p == 0 && from_in) {
       k_radix_onesweep<K, V, In><<<static_cast<unsigned>(tiles), kSortBlock, sizeof(S), st>>>(
           in0, *keys, *vals, n, shift, hist + p * kRadix, state.p, ticket);
@@ -767,36 +811,67 @@ void radix_sort_pairs(Ctx& ctx, K** keys, K** keys_alt, V** vals, V** vals_alt, 
 // (*keys, *vals); n >= 1).
 template <class K, class V, class In>
 void radix_sort_pairs_from(Ctx& ctx, In in, K** keys, K** keys_alt, V** vals, V** vals_alt, u64 n, int bits,
-                           int lo_bit, u32* pre_hist = nullptr, const u32* pre_rows = nullptr) {
+                           int lo_bit, u32* pre_hist = nullptr, const u32* pre_rows = nullptr,
+                           const u32* stat_rows = nullptr) {
   radix_sort_impl<K, V>(ctx, in, true, keys, keys_alt, vals, vals_alt, n, bits > lo_bit ? bits : lo_bit + 1, lo_bit,
-                        pre_hist, pre_hist ? pre_rows : nullptr);
+                        pre_hist, pre_hist && stat_rows ? pre_rows : nullptr, stat_rows);
 }
 
 // Per-tile digit-count rows (rows x 2*256, the statistics pass's output)
 // summed into hist (zeroed) — the fused owner-digit histogram's reduction.
-// csum (optional): each block's column sums, for k_rows_prefix.
+// csum (optional): each block's column sums, for k_csum_scan (which then writes hist).
 static __global__ void __launch_bounds__(512) k_hist_rows(const u32* rows, u64 nrows, u64 rows_per_block, u32* hist,
                                                           u32* csum = nullptr) {
   const u64 r0 = blockIdx.x * rows_per_block, r1 = min(nrows, r0 + rows_per_block);
   u32 acc = 0;
   for (u64 r = r0; r < r1; ++r) acc += rows[r * 512 + threadIdx.x];
-  if (acc) atomicAdd(&hist[threadIdx.x], acc);
-  if (csum) csum[blockIdx.x * 512ull + threadIdx.x] = acc;
+  if (csum) csum[blockIdx.x * 512ull + threadIdx.x] = acc;  // k_csum_scan writes hist
+  else if (acc) atomicAdd(&hist[threadIdx.x], acc);
 }
 
-// The first digit's half of every row (columns 0-255) replaced in place by its
-// exclusive prefix over the preceding rows: block c adds the column sums of
-// blocks < c (k_hist_rows' csum, same rows_per_block), then walks its rows.
-static __global__ void __launch_bounds__(256) k_rows_prefix(u32* rows, u64 nrows, u64 rows_per_block,
-                                                            const u32* csum) {
-  u32 pre = 0;
-  for (u64 c = 0; c < blockIdx.x; ++c) pre += csum[c * 512 + threadIdx.x];
-  const u64 r0 = blockIdx.x * rows_per_block, r1 = min(nrows, r0 + rows_per_block);
-  for (u64 r = r0; r < r1; ++r) {
-    const u32 v = rows[r * 512 + threadIdx.x];
-    rows[r * 512 + threadIdx.x] = pre;
-    pre += v;
+// k_csum_scan: column d of csum (k_hist_rows' block sums, nblocks rows of 512,
+// <= kCsumPer * 1024 rows) turned in place into its exclusive prefix over the
+// blocks, and its total written to hist[d] (the digit histogram). Block d,
+// thread t owns kCsumPer consecutive block rows.
+constexpr u32 kCsumPer = 8;
+static __global__ void __launch_bounds__(1024) k_csum_scan(u32* csum, u32 nblocks, u32* hist) {
+  __shared__ u32 ws[32];
+  const u32 t = threadIdx.x, lane = t & 31, warp = t >> 5, d = blockIdx.x;
+  u32 v[kCsumPer];
+  u32 mine = 0;
+#pragma unroll
+  for (u32 k = 0; k < kCsumPer; ++k) {
+    const u32 c = t * kCsumPer + k;
+    v[k] = c < nblocks ? csum[c * 512ull + d] : 0u;
   }
+#pragma unroll
+  for (u32 k = 0; k < kCsumPer; ++k) mine += v[k];
+  u32 incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const u32 y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= static_cast<u32>(o)) incl += y;
+  }
+  if (lane == 31) ws[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    u32 w = ws[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= static_cast<u32>(o)) w += y;
+    }
+    ws[lane] = w;
+  }
+  __syncthreads();
+  u32 run = (warp ? ws[warp - 1] : 0u) + incl - mine;
+#pragma unroll
+  for (u32 k = 0; k < kCsumPer; ++k) {
+    const u32 c = t * kCsumPer + k;
+    if (c < nblocks) csum[c * 512ull + d] = run;
+    run += v[k];
+  }
+  if (t == 0) hist[d] = ws[31];
 }
 
 }  // namespace twg

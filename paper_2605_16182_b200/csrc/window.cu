@@ -61,8 +61,8 @@ struct FastSpec {
   DevBuf<u64> ts_state;  // look-back words of the statistics pass's ts-group numbering
   bool groups = false;   // the statistics pass wrote the batch's ts groups into the log (total: d_scalars[14])
   DevBuf<u32> hist_rows, hist;  // the fused owner-digit histogram (rows per tile, their sum)
-  DevBuf<u32> hist_csum;        // k_hist_rows' per-block sums (rows_pre)
-  bool rows_pre = false;        // hist_rows' first-digit half holds per-tile exclusive prefixes
+  DevBuf<u32> hist_csum;        // k_hist_rows' per-block sums, then their exclusive prefixes (rows_pre)
+  bool rows_pre = false;        // the first bucket-sort pass takes its offsets from hist_csum + hist_rows
 };
 
 // scal[8]: batch min t, scal[9]: some id negative.
@@ -1202,7 +1202,8 @@ Store* ingest_fast(Window& w, FastSpec& spec, u64 n, const u64* sc, i64 cutoff, 
       ingest_append(w, O, std::move(s), spec.rec, spec.wring, n, from, cutoff, true, spec.in_log, true, spec.bt,
                     spec.cols, spec.groups ? ctx.d_scalars + 14 : nullptr, batch_min,
                     compact_payload_enabled() && static_cast<u64>(static_cast<i64>(sc[0]) - batch_min) < (1ull << 32),
-                    O.last_t.p, spec.hist.n ? spec.hist.p : nullptr, spec.rows_pre ? spec.hist_rows.p : nullptr);
+                    O.last_t.p, spec.hist.n ? spec.hist.p : nullptr, spec.rows_pre ? spec.hist_csum.p : nullptr,
+                    spec.rows_pre ? spec.hist_rows.p : nullptr);
   if (!out) {  // an old node leaves the window: the general route recomputes everything
     stats->evicted = stats->dropped_late = 0;
     return nullptr;
@@ -1310,17 +1311,18 @@ void window_ingest(Window& w, const i64* d_src, const i64* d_dst, const i64* d_t
         d_src, d_dst, d_t, n, ctx.d_scalars, spec.rec, spec.wring, ts, hs);
     if (hs.rows) {
       TWG_LAUNCHED(ctx);
-      constexpr u64 kRowsPerBlock = 256;
-      const u64 hblocks = (stat_tiles + kRowsPerBlock - 1) / kRowsPerBlock;
       static_assert(kStatTile == kPreItems * kSortBlock, "the first sort pass's tiles are the statistics tiles");
-      spec.rows_pre = w.mode != TWG_UNDIRECTED && sort_pre_enabled();  // one entry per edge
+      // one entry per edge; k_csum_scan covers <= kCsumPer * 1024 blocks of kPreRowsPerBlock rows
+      spec.rows_pre = w.mode != TWG_UNDIRECTED && sort_pre_enabled() &&
+                      stat_tiles <= static_cast<u64>(kCsumPer) * 1024 * kPreRowsPerBlock;
+      const u64 rpb = spec.rows_pre ? kPreRowsPerBlock : 256;
+      const u64 hblocks = (stat_tiles + rpb - 1) / rpb;
       if (spec.rows_pre) spec.hist_csum.alloc(hblocks * 512, st);
-      k_hist_rows<<<static_cast<unsigned>(hblocks), 512, 0, st>>>(spec.hist_rows.p, stat_tiles, kRowsPerBlock,
-                                                                   spec.hist.p, spec.rows_pre ? spec.hist_csum.p : nullptr);
+      k_hist_rows<<<static_cast<unsigned>(hblocks), 512, 0, st>>>(spec.hist_rows.p, stat_tiles, rpb, spec.hist.p,
+                                                                   spec.rows_pre ? spec.hist_csum.p : nullptr);
       if (spec.rows_pre) {
         TWG_LAUNCHED(ctx);
-        k_rows_prefix<<<static_cast<unsigned>(hblocks), 256, 0, st>>>(spec.hist_rows.p, stat_tiles, kRowsPerBlock,
-                                                                       spec.hist_csum.p);
+        k_csum_scan<<<512, 1024, 0, st>>>(spec.hist_csum.p, static_cast<u32>(hblocks), spec.hist.p);
       }
     }
   } else {

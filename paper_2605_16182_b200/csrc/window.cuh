@@ -46,13 +46,15 @@ bool append_log_slot(const Store& O, const Store* R, u64 A, Ring* wr);
 // old_last: s->last_t is unfilled; it becomes max(old_last, the batch's
 // owner-side newest) per node (else s->last_t is updated in place).
 // pre_hist: the bucket sort's digit histogram, already computed (fused into
-// the statistics pass); pre_rows: per statistics tile, the exclusive prefix of
-// the first digit's counts (k_rows_prefix) — the first pass skips its look-back.
+// the statistics pass); stat_rows / pre_rows: its per-tile digit rows and the
+// exclusive prefixes of their block sums (k_csum_scan) — the first pass skips
+// its look-back.
 Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const EdgeRec* batch, Ring bring, u64 A,
                      u64 from, i64 cutoff, bool no_ties, bool in_log = false, bool check_dead = false,
                      const i64* bt = nullptr, const i64* const* bcols = nullptr,
                      const u64* groups_done = nullptr, i64 tbase = 0, bool compact = false,
-                     const i64* old_last = nullptr, u32* pre_hist = nullptr, const u32* pre_rows = nullptr);
+                     const i64* old_last = nullptr, u32* pre_hist = nullptr, const u32* pre_rows = nullptr,
+                     const u32* stat_rows = nullptr);
 
 Window* window_create(Ctx& ctx, i64 duration, int mode, BuildOpts opts);
 void window_destroy(Window* w);
