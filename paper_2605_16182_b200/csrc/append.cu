@@ -442,6 +442,7 @@ __global__ void __launch_bounds__(kBlock) k_plan(PlanArgs<PV> a) {
 // live entries and marks into the new rings (rebased to logical 0), one warp per ring
 __global__ void k_reloc_copy(const Reloc* list, const u64* scal, const NodeMeta* onm, const NodeMeta* plan,
                              const Entry* oent, const i64* omt, const u32* oms, Entry* ent, i64* mt, u32* ms) {
+  if (scal[1] | scal[13]) return;  // the plan failed (arena exhausted / a node leaves): queued speculatively
   const u64 n = scal[2] & 0xffffffffull;
   const u64 warps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
   const u32 lane = threadIdx.x & 31;
@@ -474,6 +475,7 @@ struct PlaceArgs {
   WalkRec* wrec_new;
   const WalkRec* owrec;  // the previous snapshot's walk records (null: read its tail from the ring)
   u64* q_total;
+  const u64* abort;  // the plan's scalars: [1] arena exhausted, [13] a node leaves the window -> do nothing
 };
 
 template <class PV>
@@ -507,6 +509,7 @@ __global__ void __launch_bounds__(kPB, TWG_PLACE_MINB) k_bucket_place(PlaceArgs<
   PlaceSmem<PV>& sm = *reinterpret_cast<PlaceSmem<PV>*>(smem_raw);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const u64 bkt = blockIdx.x;
+  if (a.abort[1] | a.abort[13]) return;  // queued before the host saw the plan fail
   const u64 v = (bkt << kBucketShift) + t;
   const bool valid = v < a.V;
   const u32 bs = a.bstart[bkt], be = a.bstart[bkt + 1];
@@ -840,6 +843,7 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
 
   // 2.-3. with the compact 12-B payload when the batch's times span < 2^32
   std::shared_ptr<NodeArena> arena;
+  u64 r[14];  // the closing read-back (sc[0..13])
   auto sort_and_place = [&](auto tag) -> bool {
     using PV = decltype(tag);
     // 2. batch entries grouped into 256-node buckets: stable radix sort of
@@ -887,7 +891,10 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
     DevBuf<NodeMeta> plan(V, st);
     DevBuf<i64> last_t(V, st);
     DevBuf<Reloc> reloc(V, st);
-    auto run_plan = [&](NodeArena& dst, bool all) {
+    // run_plan: k_plan into dst; with readback, its scalars come back at once
+    // (relocations + 1, 0 = exhausted; `dead` set when the population would
+    // shrink), else the closing read-back below collects them
+    auto run_plan = [&](NodeArena& dst, bool all, bool readback) -> u64 {
       TWG_CUDA(cudaMemsetAsync(sc, 0, 3 * sizeof(u64), st));
       if (check_dead) TWG_CUDA(cudaMemsetAsync(sc + 13, 0, sizeof(u64), st));
       TWG_CUDA(cudaMemcpyAsync(sc, &dst.used, sizeof(u64), cudaMemcpyHostToDevice, st));
@@ -916,6 +923,7 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
       pa.scal = sc;
       k_plan<PV><<<grid(ctx, V), kBlock, 0, st>>>(pa);
       TWG_LAUNCHED(ctx);
+      if (!readback) return 0;
       u64 r3[14];
       read_scalars(ctx, sc, r3, check_dead ? 14 : 3);
       if (check_dead && r3[13]) {
@@ -925,10 +933,49 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
       dst.used = r3[0];
       return r3[1] == 0 ? static_cast<u64>(r3[2] & 0xffffffffull) + 1 : 0;  // relocations + 1, 0 = exhausted
     };
-    bool fresh = false;
-    u64 nrel = arena ? run_plan(*arena, false) : 0;
-    if (dead) return false;
-    if (nrel == 0) {
+    static bool attr_set = false;
+    if (!attr_set) {
+      TWG_CUDA(cudaFuncSetAttribute(k_bucket_place<Entry>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(sizeof(PlaceSmem<Entry>))));
+      TWG_CUDA(cudaFuncSetAttribute(k_bucket_place<PEnt>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(sizeof(PlaceSmem<PEnt>))));
+      attr_set = true;
+    }
+    // relocation copies (count read on the device: sc[2]) and the placement;
+    // both return at once when the plan failed (sc[1]: arena exhausted,
+    // sc[13]: a node leaves the window), so they can be queued before the
+    // plan's scalars are known
+    auto copy_and_place = [&](NodeArena& ar, u64 rel_bound) {
+      k_reloc_copy<<<grid(ctx, 32 * std::max<u64>(rel_bound, 1)), kBlock, 0, st>>>(
+          reloc.p, sc, O.nm.p, plan.p, O.ent.p, O.mk_time.p, O.mk_start.p, ar.ent.p, ar.mk_time.p, ar.mk_start.p);
+      TWG_LAUNCHED(ctx);
+      PlaceArgs<PV> pl;
+      pl.V = V;
+      pl.tb = tbase;
+      pl.plan = plan.p;
+      pl.last_t = no_ties ? nullptr : last_t.p;
+      pl.keys = kp;
+      pl.vals = vp;
+      pl.bstart = bstart.p;
+      pl.ent = ar.ent.p;
+      pl.mt = ar.mk_time.p;
+      pl.ms = ar.mk_start.p;
+      pl.nm_new = s->nm.p;
+      pl.wrec_new = s->wrec.p;
+      pl.owrec = O.wrec.n >= V ? O.wrec.p : nullptr;
+      pl.q_total = sc + 7;
+      pl.abort = sc;
+      TWG_CUDA(cudaMemsetAsync(sc + 7, 0, sizeof(u64), st));
+      k_bucket_place<PV><<<static_cast<unsigned>(nb), kPB, sizeof(PlaceSmem<PV>), st>>>(pl);
+      TWG_LAUNCHED(ctx);
+    };
+    // the closing read-back: the plan's scalars [0..2], [13] with g_cut,
+    // batch groups, marks, Q [5..8]
+    auto closing = [&]() {
+      TWG_CUDA(cudaMemcpyAsync(sc + 8, d_gcut, sizeof(u64), cudaMemcpyDeviceToDevice, st));
+      read_scalars(ctx, sc, r, 14);
+    };
+    auto fresh_arena = [&]() -> bool {  // every ring relocated into a new arena (synchronous plan)
       auto na = std::make_shared<NodeArena>();
       static std::atomic<u64> serials{0};
       na->serial = ++serials;
@@ -939,59 +986,44 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
       na->mk_start.alloc(na->cap, st);
       na->used = 0;
       arena = std::move(na);
-      nrel = run_plan(*arena, true);
-      if (nrel == 0) fail(TWG_ENOMEM, "ingest: node arena sized below the live regions");
-      fresh = true;
+      const u64 n1 = run_plan(*arena, true, true);
       if (dead) return false;
+      if (n1 == 0) fail(TWG_ENOMEM, "ingest: node arena sized below the live regions");
+      copy_and_place(*arena, n1 - 1);
+      closing();
+      return true;
+    };
+    bool fresh = false;
+    u64 nrel = 0;
+    if (arena) {  // speculative: plan, copies and placement queued back to back, one read-back
+      run_plan(*arena, false, false);
+      copy_and_place(*arena, 4096);  // grid-stride over the device's relocation count
+      closing();
+      if (check_dead && r[13]) return false;
+      if (r[1] == 0) {
+        arena->used = r[0];
+        nrel = r[2] & 0xffffffffull;
+      } else {  // the arena is exhausted: the queued copies and placement did nothing
+        if (!fresh_arena()) return false;
+        fresh = true;
+        nrel = r[2] & 0xffffffffull;
+        arena->used = r[0];
+      }
+    } else {
+      if (!fresh_arena()) return false;
+      fresh = true;
+      nrel = r[2] & 0xffffffffull;
+      arena->used = r[0];
     }
-    --nrel;
     s->relocated = nrel;
-    if (nrel) {
-      k_reloc_copy<<<grid(ctx, 32 * nrel), kBlock, 0, st>>>(reloc.p, sc, O.nm.p, plan.p, O.ent.p, O.mk_time.p,
-                                                            O.mk_start.p, arena->ent.p, arena->mk_time.p,
-                                                            arena->mk_start.p);
-      TWG_LAUNCHED(ctx);
-    }
     reloc.release();
-    pt.mark(fresh ? "plan+repack" : "plan");
+    pt.mark(fresh ? "plan+place+repack" : "plan+place");
     if (pt.on) std::fprintf(stderr, "[twg phases] relocated rings: %llu of %llu\n", static_cast<unsigned long long>(nrel),
                             static_cast<unsigned long long>(V));
-    static bool attr_set = false;
-    if (!attr_set) {
-      TWG_CUDA(cudaFuncSetAttribute(k_bucket_place<Entry>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(sizeof(PlaceSmem<Entry>))));
-      TWG_CUDA(cudaFuncSetAttribute(k_bucket_place<PEnt>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(sizeof(PlaceSmem<PEnt>))));
-      attr_set = true;
-    }
-    PlaceArgs<PV> pl;
-    pl.V = V;
-    pl.tb = tbase;
-    pl.plan = plan.p;
-    pl.last_t = no_ties ? nullptr : last_t.p;
-    pl.keys = kp;
-    pl.vals = vp;
-    pl.bstart = bstart.p;
-    pl.ent = arena->ent.p;
-    pl.mt = arena->mk_time.p;
-    pl.ms = arena->mk_start.p;
-    pl.nm_new = s->nm.p;
-    pl.wrec_new = s->wrec.p;
-    pl.owrec = O.wrec.n >= V ? O.wrec.p : nullptr;
-    pl.q_total = sc + 7;
-    TWG_CUDA(cudaMemsetAsync(sc + 7, 0, sizeof(u64), st));
-    k_bucket_place<PV><<<static_cast<unsigned>(nb), kPB, sizeof(PlaceSmem<PV>), st>>>(pl);
-    TWG_LAUNCHED(ctx);
-    pt.mark("place");
     return true;
   };
   if (!(compact ? sort_and_place(PEnt{}) : sort_and_place(Entry{}))) return nullptr;
-
-  // the one closing read-back: g_cut, batch groups, Q
-  u64 r[4];
-  TWG_CUDA(cudaMemcpyAsync(sc + 8, d_gcut, sizeof(u64), cudaMemcpyDeviceToDevice, st));
-  read_scalars(ctx, sc + 5, r, 4);  // [5] Zb, [6] marks, [7] Q, [8] g_cut
-  const u64 Zb = r[0], Q = r[2], g_cut = r[3];
+  const u64 Zb = r[5], Q = r[7], g_cut = r[8];
   const u64 Z = (O.Z - g_cut) + Zb;
   s->ts_first = in_place ? O.ts_first + g_cut : 0;
   log->len = lpos + A;
