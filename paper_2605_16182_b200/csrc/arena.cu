@@ -141,7 +141,7 @@ void arena_free(cudaStream_t s, void* p, size_t bytes) {
     cudaFree(p);
     return;
   }
-  if (auto g = a->asked.find(p); g != a->asked.end()) {  // TWG_GUARD: the block's tail guard intact?
+  if (auto g = guard_bytes() ? a->asked.find(p) : a->asked.end(); g != a->asked.end()) {  // TWG_GUARD: tail intact?
     std::vector<unsigned char> tail(guard_bytes());
     cudaMemcpyAsync(tail.data(), static_cast<char*>(p) + g->second, tail.size(), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
