@@ -780,8 +780,9 @@ void radix_sort_impl(Ctx& ctx, In in0, bool from_in, K** keys, K** keys_alt, V**
   u32* ticket = reinterpret_cast<u32*>(state.p + tiles * kRadix);
   for (int p = 0; p < passes; ++p) {
     const int shift = lo_bit + p * kRadixBits;
-    TWG_CUDA(cudaMemsetAsync(state.p, 0, state.bytes(), st));
-    if (p == 0 && from_in && pre_rows) {
+    const bool pre = p == 0 && from_in && pre_rows;  // no look-back: its state words are not read
+    if (!pre) TWG_CUDA(cudaMemsetAsync(state.p, 0, state.bytes(), st));
+    if (pre) {
       k_radix_onesweep<K, V, In, kPreItems, true>
           <<<static_cast<unsigned>((n + SP::kTile - 1) / SP::kTile), kSortBlock, sizeof(SP), st>>>(
               in0, *keys, *vals, n, shift, hist + p * kRadix, state.p, ticket, pre_rows, stat_rows);
