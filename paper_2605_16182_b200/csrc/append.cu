@@ -980,7 +980,11 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
       static std::atomic<u64> serials{0};
       na->serial = ++serials;
       na->V = V;
-      na->cap = std::min<u64>((5 * s->P) / 2 + 12 * V + 1024, 0xffffff00ull);  // >= 2 P + 4 V: the repack fits
+      // >= 2 P + 4 V: the repack fits (TWG_ARENA_TIGHT=1, for tests: exactly that, so later
+      // batches exhaust it and take the speculative plan's exhausted path)
+      const char* tight = std::getenv("TWG_ARENA_TIGHT");
+      na->cap = std::min<u64>((tight && tight[0] == '1') ? 2 * s->P + 4 * V + 1024 : (5 * s->P) / 2 + 12 * V + 1024,
+                              0xffffff00ull);
       na->ent.alloc(na->cap, st);
       na->mk_time.alloc(na->cap, st);
       na->mk_start.alloc(na->cap, st);

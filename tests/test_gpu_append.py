@@ -126,6 +126,32 @@ def test_append_shuffled_ties_across_sort_tiles(tw, co, mode):
 
 
 @pytest.mark.parametrize("mode", [0, 2])
+def test_append_arena_exhausted_mid_stream(tw, co, mode, monkeypatch):
+    """The plan, the relocation copies and the placement are queued back to
+    back and the plan's scalars read once at the end; when the plan finds the
+    node arena exhausted, the queued kernels must do nothing and the host must
+    repack into a fresh arena. TWG_ARENA_TIGHT sizes every fresh arena at the
+    minimum a repack needs, so streaming batches keep exhausting it: several
+    repacks happen, and the index after every batch (and the walks) still
+    equals the oracle's."""
+    monkeypatch.setenv("TWG_ARENA_TIGHT", "1")
+    batches = _ordered_stream(61 + mode, 12, 3000, 150, 100, skew=True)
+    exp_stats, exp_dumps = co.window_run(batches, 300, mode, every=True)
+    w = tw.WindowManager(300, tw.DirectionMode(mode))
+    serials = []
+    for i, (b, ed) in enumerate(zip(batches, exp_dumps)):
+        w.ingest_batch(b)
+        snap = w.snapshot()
+        assert_store(snap, ed)
+        if snap.is_streaming():
+            serials.append(snap.layout()["arena_serial"])
+        if i == len(batches) - 1:
+            _check_walks(tw, co, snap, ed, mode)
+    assert len(serials) == len(batches) - 1
+    assert len(set(serials)) >= 3, serials  # repacks after the first streaming batch
+
+
+@pytest.mark.parametrize("mode", [0, 2])
 def test_append_tie_boundary(tw, co, mode):
     """Batch boundaries sharing a timestamp: the first batch group and the
     first batch mark of a node merge with the survivors' last ones."""
