@@ -136,6 +136,10 @@ __device__ __forceinline__ u32 gallop_lb(TimeAt at, u32 lo, u32 hi, i64 c) {
 
 using Rec = BatchRec16;
 
+#ifndef TWG_BOUNDS_KEYS
+#define TWG_BOUNDS_KEYS 8  // k_bucket_bounds keys per thread (a multiple of 4)
+#endif
+
 // the admitted batch into the log ring
 __global__ void k_append_batch(const EdgeRec* b, Ring br, u64 n, EdgeRec* log, Ring wr) {
   for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
@@ -251,26 +255,31 @@ struct OwnerIn {
 };
 
 // bucket b = owner >> 8 of the bucket-sorted entries starts at bstart[b]
-// (empty buckets included); bstart[nb] = Yn. Four keys per thread (one
-// 128-bit load; the key before them from the neighbouring lane).
+// (empty buckets included); bstart[nb] = Yn. TWG_BOUNDS_KEYS keys per thread
+// (128-bit loads; the key before them re-read from the neighbouring group).
 __global__ void k_bucket_bounds(const u32* keys, u64 Yn, u64 nb, u32* bstart) {
-  const u64 quads = (Yn + 4) / 4;  // positions 0..Yn (Yn itself closes the last bucket)
-  for (u64 g = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; g < quads;
+  constexpr int kK = TWG_BOUNDS_KEYS;  // keys per thread (kK / 4 128-bit loads)
+  const u64 groups = (Yn + kK) / kK;   // positions 0..Yn (Yn itself closes the last bucket)
+  const bool aligned = (reinterpret_cast<uintptr_t>(keys) & 15) == 0;
+  for (u64 g = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; g < groups;
        g += static_cast<u64>(gridDim.x) * blockDim.x) {
-    const u64 q0 = 4 * g;
-    i64 cur[4];
-    if (q0 + 4 <= Yn && (reinterpret_cast<uintptr_t>(keys) & 15) == 0) {
-      const uint4 k4 = __ldg(reinterpret_cast<const uint4*>(keys) + g);
-      cur[0] = k4.x >> kBucketShift, cur[1] = k4.y >> kBucketShift, cur[2] = k4.z >> kBucketShift,
-      cur[3] = k4.w >> kBucketShift;
+    const u64 q0 = kK * g;
+    i64 cur[kK];
+    if (q0 + kK <= Yn && aligned) {
+#pragma unroll
+      for (int h = 0; h < kK / 4; ++h) {
+        const uint4 k4 = __ldg(reinterpret_cast<const uint4*>(keys + q0) + h);
+        cur[4 * h] = k4.x >> kBucketShift, cur[4 * h + 1] = k4.y >> kBucketShift,
+                cur[4 * h + 2] = k4.z >> kBucketShift, cur[4 * h + 3] = k4.w >> kBucketShift;
+      }
     } else {
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < kK; ++j)
         cur[j] = q0 + j < Yn ? static_cast<i64>(keys[q0 + j] >> kBucketShift) : static_cast<i64>(nb);
     }
     i64 prev = q0 == 0 ? -1 : static_cast<i64>(keys[q0 - 1] >> kBucketShift);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < kK; ++j) {
       const u64 q = q0 + j;
       if (q > Yn) break;
       for (i64 b = prev + 1; b <= cur[j]; ++b) bstart[b] = static_cast<u32>(q);
@@ -868,7 +877,7 @@ Store* ingest_append(Window& w, const Store& O, std::unique_ptr<Store> s, const 
       TWG_LAUNCHED(ctx);
     }
     DevBuf<u32> bstart(nb + 1, st);
-    k_bucket_bounds<<<grid(ctx, (Yn + 4) / 4), kBlock, 0, st>>>(kp, Yn, nb, bstart.p);
+    k_bucket_bounds<<<grid(ctx, (Yn + TWG_BOUNDS_KEYS) / TWG_BOUNDS_KEYS), kBlock, 0, st>>>(kp, Yn, nb, bstart.p);
     TWG_LAUNCHED(ctx);
     (kp == k0.p ? k1 : k0).release();  // the pass count decides which buffer holds the result
     (vp == v0.p ? v1 : v0).release();
